@@ -1,0 +1,256 @@
+"""CPU oracle of the JITServe GMAX step and trace replay (arXiv 2504.20068).
+
+TEST INFRASTRUCTURE ONLY: only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` leg may import this package.  The product path
+(``paper_2504_20068_b200``) never imports it and shares no code with it.
+
+The arithmetic lives in ``gmax_oracle.c`` (plain single-threaded C, ``-O2 -ffp-contract=off``);
+this module only compiles it on demand with gcc and marshals numpy arrays through ctypes.
+Every function in the C file cites the PAPER.md / SPEC.md passage it follows.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "gmax_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+NO_TASK = 0xFFFFFFFF
+MAX_STAGES = 8
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so next to the source (gcc, -O2 -ffp-contract=off)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-std=c11", "-fPIC", "-shared",
+                               "-o", tmp, _SRC])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class _Group(C.Structure):
+    _fields_ = [("type", C.c_uint32), ("w_in", C.c_uint32), ("w_out", C.c_uint32), ("_pad", C.c_uint32),
+                ("ttft_ns", C.c_int64), ("tbt_ns", C.c_int64), ("e2el_ns", C.c_int64),
+                ("be_deadline_ns", C.c_int64)]
+
+
+class _Config(C.Structure):
+    _fields_ = [(k, C.c_uint32) for k in ("token_budget", "max_batch", "prefill_chunk", "refine_interval",
+                                          "frame_steps", "q_num", "q_den", "p_num", "p_den", "delta_starve",
+                                          "len_key", "appb_filter")] + \
+               [("eps_ns", C.c_int64), ("waiting_ns", C.c_int64)]
+
+
+class _Table(C.Structure):
+    _fields_ = [("n_rows", C.c_uint32), ("n_bins", C.c_uint32), ("l_max", C.c_uint32), ("_pad", C.c_uint32),
+                ("edges", C.c_void_p), ("cum", C.c_void_p)]
+
+
+class _Pool(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("_pad", C.c_uint32)] + \
+               [(k, C.c_void_p) for k in ("id", "arrival_ns", "input_len", "generated", "prefilled", "meta",
+                                          "aux", "task", "override_R")]
+
+
+class _Tasks(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("_pad", C.c_uint32)] + \
+               [(k, C.c_void_p) for k in ("call_off", "arrival_ns", "deadline_ns", "cur_stage", "n_stages",
+                                          "pattern_ms", "goodput_done")]
+
+
+class _Result(C.Structure):
+    _fields_ = [(k, C.c_uint32) for k in ("n_pending", "n_selected", "total_tokens", "n_candidates", "b_star",
+                                          "n_dropped_now", "error", "_pad")] + \
+               [("bp", C.c_double), ("thr", C.c_double)]
+
+
+class _RowsOut(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in ("key", "rate", "t_rem", "lhat", "cost", "pending")]
+
+
+class _Trace(C.Structure):
+    _fields_ = [("n_rows", C.c_uint32), ("n_tasks", C.c_uint32)] + \
+               [(k, C.c_void_p) for k in ("arrival_ns", "input_len", "true_out", "group", "dist_row", "override_R",
+                                          "task", "task_arrival_ns", "task_deadline_ns", "task_n_stages",
+                                          "stage_kind", "stage_exec_ns", "stage_pattern_ms", "stage_call_begin",
+                                          "stage_call_end")]
+
+
+class _ReplayCfg(C.Structure):
+    _fields_ = [("n_steps", C.c_uint32), ("log_ids", C.c_uint32)] + \
+               [(k, C.c_int64) for k in ("v_token0_ns", "c0_ns", "c_att_ns", "c_lin_ns")] + \
+               [(k, C.c_uint64) for k in ("load_num", "load_den", "slo_num", "slo_den")]
+
+
+class _ReplayResult(C.Structure):
+    _fields_ = [("token_goodput", C.c_uint64), ("tokens_processed", C.c_uint64), ("sim_end_ns", C.c_int64)] + \
+               [(k, C.c_uint32) for k in ("request_goodput", "n_done", "n_dropped", "steps", "n_tasks_done",
+                                          "error")]
+
+
+STEP_LOG_DTYPE = np.dtype([("now_ns", "<i8"), ("n_selected", "<u4"), ("total_tokens", "<u4"),
+                           ("n_candidates", "<u4"), ("b_star", "<u4"), ("bp", "<f8"), ("ids_hash", "<u8")])
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        _lib.og_step.restype = C.c_int
+        _lib.og_replay.restype = C.c_int
+        _lib.og_length_bound.restype = C.c_uint32
+        _lib.og_length_bound.argtypes = [C.POINTER(_Table), C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                         C.c_uint32]
+    return _lib
+
+
+def _arr(a, dtype):
+    a = np.ascontiguousarray(a, dtype=dtype)
+    return a
+
+
+def _ptr(a):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+def _mk_config(cfg):
+    c = _Config()
+    for k, _ in _Config._fields_:
+        setattr(c, k, int(cfg[k]))
+    return c
+
+
+def _mk_groups(groups):
+    n = len(groups["type"])
+    arr = (_Group * max(n, 1))()
+    for i in range(n):
+        for k in ("type", "w_in", "w_out", "ttft_ns", "tbt_ns", "e2el_ns", "be_deadline_ns"):
+            setattr(arr[i], k, int(groups[k][i]))
+    return arr, n
+
+
+def _mk_table(table, keep):
+    edges = _arr(table["edges"], np.uint32)
+    cum = _arr(table["cum"], np.uint32)
+    keep += [edges, cum]
+    t = _Table()
+    t.n_rows, t.n_bins = cum.shape
+    t.l_max = int(table["l_max"])
+    t.edges = _ptr(edges)
+    t.cum = _ptr(cum)
+    return t
+
+
+def length_bound(table, row: int, g: int, R: int, q_num: int, q_den: int) -> int:
+    """Lhat = max(Q_q(L | L > R*floor(g/R)), g+1) on one length-table row (§4.1)."""
+    lib = _load()
+    keep = []
+    t = _mk_table(table, keep)
+    return int(lib.og_length_bound(C.byref(t), row, g, R, q_num, q_den))
+
+
+def step(cfg, groups, table, now_ns: int, v_token_ns: int, pool, tasks=None, rows_out: bool = True):
+    """One GMAX step (Alg. 1 Schedule) over a pool snapshot.
+
+    ``pool`` is a dict of numpy arrays (id, arrival_ns, input_len, generated, prefilled, meta, aux,
+    task, override_R).  meta/aux are copied and the updated copies are returned.
+    """
+    lib = _load()
+    keep = []
+    c = _mk_config(cfg)
+    g, ng = _mk_groups(groups)
+    t = _mk_table(table, keep)
+    n = len(pool["id"])
+    cols = {
+        "id": _arr(pool["id"], np.uint32), "arrival_ns": _arr(pool["arrival_ns"], np.int64),
+        "input_len": _arr(pool["input_len"], np.uint32), "generated": _arr(pool["generated"], np.uint32),
+        "prefilled": _arr(pool["prefilled"], np.uint32), "meta": np.array(pool["meta"], dtype=np.uint32),
+        "aux": np.array(pool["aux"], dtype=np.uint32), "task": _arr(pool["task"], np.uint32),
+        "override_R": _arr(pool["override_R"], np.uint32),
+    }
+    p = _Pool()
+    p.n = n
+    for k, v in cols.items():
+        setattr(p, k, _ptr(v))
+    tp = None
+    if tasks is not None and len(tasks["arrival_ns"]):
+        tcols = {
+            "call_off": _arr(tasks["call_off"], np.uint32), "arrival_ns": _arr(tasks["arrival_ns"], np.int64),
+            "deadline_ns": _arr(tasks["deadline_ns"], np.int64), "cur_stage": _arr(tasks["cur_stage"], np.uint32),
+            "n_stages": _arr(tasks["n_stages"], np.uint32), "pattern_ms": _arr(tasks["pattern_ms"], np.uint32),
+            "goodput_done": _arr(tasks["goodput_done"], np.uint64),
+        }
+        keep.append(tcols)
+        tp = _Tasks()
+        tp.n = len(tcols["arrival_ns"])
+        for k, v in tcols.items():
+            setattr(tp, k, _ptr(v))
+    res = _Result()
+    ids = np.zeros(max(n, 1), np.uint32)
+    toks = np.zeros(max(n, 1), np.uint32)
+    rows = np.zeros(max(n, 1), np.uint32)
+    ro = None
+    out_rows = {}
+    if rows_out:
+        out_rows = {"key": np.zeros(n, np.float64), "rate": np.zeros(n, np.float64),
+                    "t_rem": np.zeros(n, np.int64), "lhat": np.zeros(n, np.uint32),
+                    "cost": np.zeros(n, np.uint32), "pending": np.zeros(n, np.uint32)}
+        ro = _RowsOut(*[_ptr(out_rows[k]) for k in ("key", "rate", "t_rem", "lhat", "cost", "pending")])
+    rc = lib.og_step(C.byref(c), g, C.c_uint32(ng), C.byref(t), C.c_int64(now_ns), C.c_int64(v_token_ns),
+                     C.byref(p), C.byref(tp) if tp is not None else None, C.byref(res),
+                     _ptr(ids), _ptr(toks), _ptr(rows), C.byref(ro) if ro is not None else None)
+    k = res.n_selected
+    out = {"status": rc, "n_pending": res.n_pending, "n_selected": k, "total_tokens": res.total_tokens,
+           "n_candidates": res.n_candidates, "b_star": res.b_star, "n_dropped_now": res.n_dropped_now,
+           "bp": res.bp, "thr": res.thr, "batch_ids": ids[:k].copy(), "batch_tokens": toks[:k].copy(),
+           "batch_rows": rows[:k].copy(), "meta": cols["meta"], "aux": cols["aux"]}
+    out.update(out_rows)
+    return out
+
+
+def replay(cfg, groups, table, trace, rcfg, log: bool = False, log_ids: bool = False):
+    """Replay one trace under GMAX (a10): cost model S:395-403/S:438, goodput §3 P:209-216."""
+    lib = _load()
+    keep = []
+    c = _mk_config(cfg)
+    g, ng = _mk_groups(groups)
+    t = _mk_table(table, keep)
+    tr = _Trace()
+    types = {"arrival_ns": np.int64, "input_len": np.uint32, "true_out": np.uint32, "group": np.uint32,
+             "dist_row": np.uint32, "override_R": np.uint32, "task": np.uint32, "task_arrival_ns": np.int64,
+             "task_deadline_ns": np.int64, "task_n_stages": np.uint32, "stage_kind": np.uint32,
+             "stage_exec_ns": np.int64, "stage_pattern_ms": np.uint32, "stage_call_begin": np.uint32,
+             "stage_call_end": np.uint32}
+    cols = {}
+    for k, dt in types.items():
+        a = _arr(trace[k], dt)
+        if a.size == 0:
+            a = np.zeros(1, dt)
+        cols[k] = a
+        setattr(tr, k, _ptr(a))
+    tr.n_rows = len(trace["input_len"])
+    tr.n_tasks = len(trace["task_arrival_ns"])
+    rc = _ReplayCfg()
+    rc.n_steps = int(rcfg["n_steps"])
+    rc.log_ids = 1 if log_ids else 0
+    for k in ("v_token0_ns", "c0_ns", "c_att_ns", "c_lin_ns", "load_num", "load_den", "slo_num", "slo_den"):
+        setattr(rc, k, int(rcfg[k]))
+    res = _ReplayResult()
+    L = np.zeros(max(rc.n_steps, 1), STEP_LOG_DTYPE) if log else None
+    LI = np.zeros(max(rc.n_steps, 1) * int(cfg["max_batch"]), np.uint32) if log_ids else None
+    st = lib.og_replay(C.byref(c), g, C.c_uint32(ng), C.byref(t), C.byref(tr), C.byref(rc), C.byref(res),
+                       _ptr(L), _ptr(LI))
+    out = {"status": st, "token_goodput": res.token_goodput, "tokens_processed": res.tokens_processed,
+           "sim_end_ns": res.sim_end_ns, "request_goodput": res.request_goodput, "n_done": res.n_done,
+           "n_dropped": res.n_dropped, "steps": res.steps, "n_tasks_done": res.n_tasks_done}
+    if log:
+        out["log"] = L[:res.steps].copy()
+    if log_ids:
+        out["log_ids"] = LI.reshape(max(rc.n_steps, 1), int(cfg["max_batch"]))[:res.steps].copy()
+    return out

@@ -1,0 +1,750 @@
+/*
+ * oracle/gmax_oracle.c -- plain, slow, single-threaded CPU ORACLE of the JITServe
+ * GMAX scheduling step (arXiv 2504.20068) and of the trace replay used to count goodput.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Nothing in the product path (paper_2504_20068_b200/,
+ * include/) may include, link or call this file.  Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference leg load it (through oracle/__init__.py).
+ * It shares no code, header, table or constant generator with the CUDA path.
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n (section / algorithm named beside it),
+ * "S:n" = SPEC.md line n, "A<k>" = the reading number in DESIGN.md §3 (ambiguity register,
+ * taken from SURVEY.md §8(c).2).  The order of operations follows Alg. 1:
+ * AnalyzeRequest for every queued request, BatchPriority, Filter by cutoff, sort by length,
+ * sliding window, return BestGroup.
+ *
+ * Exactness contract: every time is int64 ns; lengths/costs are integers;
+ * the only floating point is (i) key = fl(A / B) with integers A, B < 2^53 (one IEEE
+ * division, correctly rounded), (ii) the reported rate, same form, and (iii)
+ * thr = fl(fl(p_num / p_den) * bp).  Window sums are exact u128 sums of floor(key * 2^32).
+ * Compile with -O2 -ffp-contract=off (no FMA contraction).
+ *
+ * Parity status: every function below is pinned by tests/test_oracle_pins.py
+ * except the items DESIGN.md lists as "parity unpinned" (synthetic table contents, the cost
+ * model constants of S:438, the phi inputs, absolute goodput levels of C2-C5).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef unsigned __int128 u128;
+
+/* ------------------------------------------------------------------------------------ */
+/* Types (the oracle's own; the CUDA library declares its own in include/jit_sched.h)   */
+/* ------------------------------------------------------------------------------------ */
+
+enum { OG_LAT = 0, OG_DDL = 1, OG_CMP = 2, OG_BE = 3 };           /* §3 P:209-216 + BE P:216 */
+enum { ST_QUEUED = 0, ST_RUNNING = 1, ST_PREEMPTED = 2, ST_DONE = 3, ST_DROPPED = 4,
+       ST_WAITING = 5 /* compound call of a stage not yet released */ };
+enum { FL_EVER = 1u, FL_COMPOUND = 2u, FL_OVERRIDE = 4u };
+#define NO_TASK 0xFFFFFFFFu
+#define MAX_STAGES 8u
+
+typedef struct {
+    uint32_t type, w_in, w_out, _pad;
+    int64_t ttft_ns, tbt_ns, e2el_ns, be_deadline_ns;
+} og_group;
+
+typedef struct {
+    uint32_t token_budget, max_batch, prefill_chunk, refine_interval, frame_steps;
+    uint32_t q_num, q_den, p_num, p_den, delta_starve;
+    uint32_t len_key, appb_filter;
+    int64_t eps_ns, waiting_ns;
+} og_config;
+
+typedef struct {
+    uint32_t n_rows, n_bins, l_max, _pad;
+    const uint32_t* edges;
+    const uint32_t* cum;
+} og_table;
+
+typedef struct {
+    uint32_t n, _pad;
+    const uint32_t* id;
+    const int64_t* arrival_ns;
+    const uint32_t* input_len;
+    const uint32_t* generated;
+    const uint32_t* prefilled;
+    uint32_t* meta;       /* in/out: group bits 0-7, state 8-11, flags 12-15 */
+    uint32_t* aux;        /* in/out: dist_row bits 0-15, steps_waited 16-31 */
+    const uint32_t* task; /* NO_TASK for standalone requests */
+    const uint32_t* override_R;
+} og_pool;
+
+typedef struct {
+    uint32_t n, _pad;
+    const uint32_t* call_off;     /* n+1: rows of task t are [call_off[t], call_off[t+1]) */
+    const int64_t* arrival_ns;    /* a_c */
+    const int64_t* deadline_ns;   /* D, relative to a_c */
+    const uint32_t* cur_stage;
+    const uint32_t* n_stages;
+    const uint32_t* pattern_ms;   /* n * MAX_STAGES matched-pattern stage times */
+    const uint64_t* goodput_done;
+} og_tasks;
+
+typedef struct {
+    uint32_t n_pending, n_selected, total_tokens, n_candidates, b_star, n_dropped_now;
+    uint32_t error, _pad;
+    double bp, thr;
+} og_result;
+
+typedef struct {          /* optional per-row outputs (each pointer may be NULL) */
+    double* key;
+    double* rate;
+    int64_t* t_rem;
+    uint32_t* lhat;
+    uint32_t* cost;
+    uint32_t* pending;
+} og_rows_out;
+
+enum { OG_OK = 0, OG_EMPTY = 1, OG_EINVAL = -1 };
+
+/* ------------------------------------------------------------------------------------ */
+/* (a2) Conditional upper-quantile length bound.                                        */
+/* §4.1: a high-quantile upper bound of the response length, re-derived      */
+/* "every 50 tokens" as generation progresses; north_star: the upper quantile of */
+/* the length distribution conditioned on the tokens generated so far.                  */
+/* Reading A4: type-1 (inverse CDF, no interpolation) quantile on the histogram row.    */
+/* Reading A5: condition on L > anchor, then clamp Lhat >= g + 1.  A6: anchor = R*floor(g/R). */
+/* Reading A7: no mass above the anchor -> L_max.                                        */
+/* ------------------------------------------------------------------------------------ */
+
+static uint32_t* g_qmemo = NULL;        /* memo of Q(row, anchor), 0 = not computed */
+static uint32_t g_qmemo_rows = 0, g_qmemo_anchors = 0;
+static const og_table* g_qmemo_tab = NULL;
+static uint32_t g_qmemo_qn = 0, g_qmemo_qd = 0, g_qmemo_R = 0;
+
+/* Q_q(L | L > anchor): the smallest edge e_k with q_den*(C[k]-C_below) >= q_num*(N-C_below),
+ * C_below = cumulative count of the bins whose upper edge is <= anchor.  Plain linear scans. */
+static uint32_t cond_quantile_scan(const og_table* T, uint32_t row, uint32_t anchor,
+                                   uint32_t q_num, uint32_t q_den) {
+    const uint32_t* C = T->cum + (size_t)row * T->n_bins;
+    uint32_t N = C[T->n_bins - 1];
+    uint32_t below = 0;
+    for (uint32_t k = 0; k < T->n_bins; ++k) {
+        if (T->edges[k] <= anchor) below = C[k];
+        else break;
+    }
+    if (N == below) return T->l_max;                        /* A7 */
+    for (uint32_t k = 0; k < T->n_bins; ++k) {
+        if (T->edges[k] <= anchor) continue;               /* only L > anchor */
+        uint64_t lhs = (uint64_t)q_den * (uint64_t)(C[k] - below);
+        uint64_t rhs = (uint64_t)q_num * (uint64_t)(N - below);
+        if (lhs >= rhs) return T->edges[k];
+    }
+    return T->l_max;  /* unreachable for q <= 1 */
+}
+
+static uint32_t cond_quantile(const og_table* T, uint32_t row, uint32_t anchor,
+                              uint32_t q_num, uint32_t q_den, uint32_t R) {
+    /* memo keyed by (row, anchor / R); the value is a pure function of its inputs */
+    if (g_qmemo_tab != T || g_qmemo_qn != q_num || g_qmemo_qd != q_den || g_qmemo_R != R ||
+        g_qmemo_rows != T->n_rows) {
+        free(g_qmemo);
+        g_qmemo_anchors = T->l_max / R + 2;
+        g_qmemo_rows = T->n_rows;
+        g_qmemo = (uint32_t*)calloc((size_t)g_qmemo_rows * g_qmemo_anchors, sizeof(uint32_t));
+        g_qmemo_tab = T; g_qmemo_qn = q_num; g_qmemo_qd = q_den; g_qmemo_R = R;
+    }
+    uint32_t a = anchor / R;
+    if (g_qmemo && a < g_qmemo_anchors) {
+        uint32_t* m = &g_qmemo[(size_t)row * g_qmemo_anchors + a];
+        if (*m == 0) *m = cond_quantile_scan(T, row, anchor, q_num, q_den);
+        return *m;
+    }
+    return cond_quantile_scan(T, row, anchor, q_num, q_den);
+}
+
+/* exported for the pins: Lhat = max(Q_q(L | L > R*floor(g/R)), g + 1) */
+uint32_t og_length_bound(const og_table* T, uint32_t row, uint32_t g, uint32_t R,
+                         uint32_t q_num, uint32_t q_den) {
+    uint32_t anchor = R * (g / R);
+    uint32_t q = cond_quantile_scan(T, row, anchor, q_num, q_den);
+    return q > g + 1 ? q : g + 1;
+}
+
+void og_reset_memo(void) {
+    free(g_qmemo); g_qmemo = NULL; g_qmemo_tab = NULL; g_qmemo_rows = 0;
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* Per-request analysis (Alg. 1 AnalyzeRequest; §4.2; App. B) */
+/* ------------------------------------------------------------------------------------ */
+
+static inline uint32_t m_group(uint32_t m) { return m & 0xFFu; }
+static inline uint32_t m_state(uint32_t m) { return (m >> 8) & 0xFu; }
+static inline uint32_t m_flags(uint32_t m) { return (m >> 12) & 0xFu; }
+static inline uint32_t m_set_state(uint32_t m, uint32_t s) { return (m & ~0xF00u) | (s << 8); }
+static inline uint32_t m_set_flags(uint32_t m, uint32_t f) { return (m & ~0xF000u) | (f << 12); }
+static inline uint32_t a_row(uint32_t a) { return a & 0xFFFFu; }
+static inline uint32_t a_waited(uint32_t a) { return a >> 16; }
+
+/* key = fl((G' * 10^9) / (t_gen + eps)); §4.2 P:462-467 Priority = goodput / t_gen, with the
+ * App. B indicator's eps (reading A1/A2); G' = G + delta * floor(waited / Delta)
+ * (starvation inflation P:467, reading A12).  Returns -1 when an operand leaves 2^53. */
+static int make_key(uint64_t Gp, uint64_t t_gen, int64_t eps, double* out) {
+    const uint64_t LIM = (uint64_t)1 << 53;
+    if (Gp >= LIM / 1000000000ull) return -1;
+    uint64_t A = Gp * 1000000000ull;
+    uint64_t B = t_gen + (uint64_t)eps;
+    if (B >= LIM || B < t_gen) return -1;
+    *out = (double)A / (double)B;
+    return 0;
+}
+
+/* reported JIT rate (tokens/s): len_rem * 10^9 / t_rem; +inf when t_rem <= 0 (A38) */
+static double make_rate(uint64_t len_rem, int64_t t_rem) {
+    if (t_rem <= 0) return __builtin_inf();
+    return (double)(len_rem * 1000000000ull) / (double)t_rem;
+}
+
+/* (a6) per-step token cost: 1 for a decode step, else the next prefill chunk (A25) */
+static uint32_t token_cost(uint32_t input_len, uint32_t prefilled, uint32_t chunk) {
+    if (prefilled >= input_len) return 1;
+    uint32_t rem = input_len - prefilled;
+    return rem < chunk ? rem : chunk;
+}
+
+/* A19: exact fixed-point image floor(min(key, 2^31-1) * 2^32) used for window sums */
+static uint64_t fixed_point(double key) {
+    double k = key < 2147483647.0 ? key : 2147483647.0;
+    return (uint64_t)(k * 4294967296.0);
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* One GMAX step over a request pool (Alg. 1 Schedule)                        */
+/* ------------------------------------------------------------------------------------ */
+
+typedef struct { double key; uint32_t id; uint32_t row; } by_key_t;
+typedef struct { uint64_t len; uint32_t id; uint32_t row; } by_len_t;
+
+static int cmp_key_desc_id_asc(const void* a, const void* b) {
+    const by_key_t* x = (const by_key_t*)a; const by_key_t* y = (const by_key_t*)b;
+    if (x->key > y->key) return -1;
+    if (x->key < y->key) return 1;
+    return (x->id > y->id) - (x->id < y->id);
+}
+static int cmp_len_asc_id_asc(const void* a, const void* b) {
+    const by_len_t* x = (const by_len_t*)a; const by_len_t* y = (const by_len_t*)b;
+    if (x->len != y->len) return x->len < y->len ? -1 : 1;
+    return (x->id > y->id) - (x->id < y->id);
+}
+
+/* task view for the compound pass (a4) */
+typedef struct {
+    uint32_t n;
+    const uint32_t* call_begin; const uint32_t* call_end;   /* current-stage rows */
+    const int64_t* arrival_ns; const int64_t* deadline_ns;  /* a_c, D */
+    const uint64_t* t_le_s; const uint64_t* t_total;        /* phi(s) = t_le_s / t_total */
+    const uint64_t* goodput_done;
+} task_view;
+
+/* The step.  On return, selected[0..n_selected) holds ROW indices in batch order. */
+static int gmax_step(const og_config* cfg, const og_group* G, uint32_t n_groups,
+                     const og_table* T, int64_t now, int64_t v_token,
+                     uint32_t n, const uint32_t* id, const int64_t* arrival,
+                     const uint32_t* input_len, const uint32_t* generated,
+                     const uint32_t* prefilled, uint32_t* meta, uint32_t* aux,
+                     const uint32_t* task, const uint32_t* override_R,
+                     const task_view* TV,
+                     og_result* res, uint32_t* selected, uint32_t* sel_cost,
+                     const og_rows_out* ro) {
+    memset(res, 0, sizeof(*res));
+    if (cfg->refine_interval == 0 || cfg->frame_steps == 0 || cfg->q_den == 0 ||
+        cfg->p_den == 0 || cfg->q_num == 0 || cfg->q_num > cfg->q_den || cfg->p_num == 0 ||
+        cfg->p_num > cfg->p_den || cfg->prefill_chunk == 0 ||
+        cfg->prefill_chunk > cfg->token_budget || cfg->max_batch == 0 || v_token <= 0 ||
+        cfg->eps_ns <= 0) { res->error = 1; return OG_EINVAL; }
+
+    double* key = (double*)calloc(n ? n : 1, sizeof(double));
+    uint32_t* lhat = (uint32_t*)calloc(n ? n : 1, sizeof(uint32_t));
+    uint32_t* cost = (uint32_t*)calloc(n ? n : 1, sizeof(uint32_t));
+    uint8_t* pend = (uint8_t*)calloc(n ? n : 1, 1);
+    int64_t* trem = (int64_t*)calloc(n ? n : 1, sizeof(int64_t));
+    double* rate = (double*)calloc(n ? n : 1, sizeof(double));
+    int rc = OG_OK;
+
+    /* (a1) admission control, P:545 (A29 strict) + pending set (Alg. 1 GetRequestQueue) */
+    uint32_t n_pend = 0;
+    for (uint32_t r = 0; r < n; ++r) {
+        uint32_t m = meta[r], st = m_state(m), fl = m_flags(m);
+        if (arrival[r] > now) continue;
+        if (st == ST_QUEUED && !(fl & FL_EVER) && !(fl & FL_COMPOUND) &&
+            now - arrival[r] > cfg->waiting_ns) {
+            meta[r] = m_set_state(m, ST_DROPPED);
+            res->n_dropped_now++;
+            continue;
+        }
+        if (st == ST_QUEUED || st == ST_RUNNING || st == ST_PREEMPTED) { pend[r] = 1; ++n_pend; }
+    }
+
+    /* AnalyzeRequest for every pending standalone request */
+    for (uint32_t r = 0; r < n && rc == OG_OK; ++r) {
+        if (!pend[r]) continue;
+        uint32_t m = meta[r], gi = m_group(m);
+        if (gi >= n_groups || a_row(aux[r]) >= T->n_rows || input_len[r] == 0) { rc = OG_EINVAL; break; }
+        uint32_t g = generated[r];
+        /* (a2) PredictLength: conditional upper quantile, refined every R tokens */
+        uint32_t anchor = cfg->refine_interval * (g / cfg->refine_interval);
+        uint32_t q = cond_quantile(T, a_row(aux[r]), anchor, cfg->q_num, cfg->q_den, cfg->refine_interval);
+        lhat[r] = q > g + 1 ? q : g + 1;
+        cost[r] = token_cost(input_len[r], prefilled[r], cfg->prefill_chunk);
+        if (m_flags(m) & FL_COMPOUND) continue;                 /* handled by (a4) below */
+        const og_group* gr = &G[gi];
+        uint64_t len_rem = (uint64_t)(lhat[r] - g);
+        uint64_t t_gen = len_rem * (uint64_t)v_token;          /* P:447 t_gen = len_rem * v_token */
+        /* (a3) EstimateRemainingTime per SLO type (reading A9 for LAT) */
+        int64_t t_rem;
+        switch (gr->type) {
+            case OG_LAT: t_rem = arrival[r] + gr->ttft_ns + (int64_t)(lhat[r] - 1) * gr->tbt_ns - now; break;
+            case OG_DDL: t_rem = arrival[r] + gr->e2el_ns - now; break;
+            case OG_BE:  t_rem = arrival[r] + gr->be_deadline_ns - now; break;
+            default: rc = OG_EINVAL; continue;  /* CMP group on a non-compound row */
+        }
+        /* (a5) EstimateGoodput (reading A10/A11; App. B R(k) P:905-908) */
+        uint64_t Gk;
+        if (gr->type == OG_DDL) Gk = (uint64_t)gr->w_in * input_len[r] + (uint64_t)gr->w_out * lhat[r];
+        else if (gr->type == OG_LAT) Gk = (uint64_t)gr->w_out * lhat[r];
+        else Gk = 0;                                             /* best effort: starvation only */
+        if (m_flags(m) & FL_OVERRIDE) Gk = override_R[r];       /* App. D sets R(k) directly */
+        if (t_rem <= 0) Gk = 0;                                  /* expired (A22) */
+        if (cfg->appb_filter && t_gen > (uint64_t)(t_rem > 0 ? t_rem : 0)) Gk = 0; /* App. B filter */
+        uint64_t Gp = Gk + (uint64_t)cfg->delta_starve * (a_waited(aux[r]) / cfg->frame_steps);
+        if (make_key(Gp, t_gen, cfg->eps_ns, &key[r]) != 0) { rc = OG_EINVAL; break; }
+        trem[r] = t_rem;
+        rate[r] = make_rate(len_rem, t_rem);
+    }
+
+    /* (a4) compound requests: len_rem and bandwidth aggregated over all subrequests of the
+     * current stage; stage sub-deadline D_s = phi(s) * D. */
+    if (rc == OG_OK && TV) {
+        for (uint32_t t = 0; t < TV->n && rc == OG_OK; ++t) {
+            uint64_t Tsum = 0, Gcur = 0; uint32_t cnt = 0;
+            for (uint32_t r = TV->call_begin[t]; r < TV->call_end[t]; ++r) {
+                if (!pend[r]) continue;
+                const og_group* gr = &G[m_group(meta[r])];
+                Tsum += (uint64_t)(lhat[r] - generated[r]);
+                Gcur += (uint64_t)gr->w_in * input_len[r] + (uint64_t)gr->w_out * lhat[r];
+                ++cnt;
+            }
+            if (!cnt) continue;
+            uint64_t Gtask = TV->goodput_done[t] + Gcur;
+            if (TV->arrival_ns[t] + TV->deadline_ns[t] <= now) Gtask = 0;   /* final deadline passed */
+            if (TV->t_total[t] == 0) { rc = OG_EINVAL; break; }
+            int64_t Ds = (int64_t)((u128)(uint64_t)TV->deadline_ns[t] * TV->t_le_s[t] / TV->t_total[t]);
+            int64_t t_rem = TV->arrival_ns[t] + Ds - now;                  /* advisory */
+            uint64_t t_gen = Tsum * (uint64_t)v_token;
+            if (cfg->appb_filter && t_gen > (uint64_t)(t_rem > 0 ? t_rem : 0)) Gtask = 0;
+            for (uint32_t r = TV->call_begin[t]; r < TV->call_end[t]; ++r) {
+                if (!pend[r]) continue;
+                uint64_t Gp = Gtask + (uint64_t)cfg->delta_starve * (a_waited(aux[r]) / cfg->frame_steps);
+                if (make_key(Gp, t_gen, cfg->eps_ns, &key[r]) != 0) { rc = OG_EINVAL; break; }
+                trem[r] = t_rem;
+                rate[r] = make_rate(Tsum, t_rem);
+            }
+        }
+    }
+    /* every row of a task range must be a compound call of that task with a CMP group */
+    if (rc == OG_OK && TV)
+        for (uint32_t t = 0; t < TV->n && rc == OG_OK; ++t)
+            for (uint32_t r = TV->call_begin[t]; r < TV->call_end[t]; ++r)
+                if (!(m_flags(meta[r]) & FL_COMPOUND) || task[r] != t || m_group(meta[r]) >= n_groups ||
+                    G[m_group(meta[r])].type != OG_CMP) { rc = OG_EINVAL; break; }
+    /* every pending compound row must have been covered by a task */
+    for (uint32_t r = 0; r < n && rc == OG_OK; ++r)
+        if (pend[r] && (m_flags(meta[r]) & FL_COMPOUND) && (!TV || task[r] == NO_TASK ||
+            task[r] >= TV->n || r < TV->call_begin[task[r]] || r >= TV->call_end[task[r]]))
+            rc = OG_EINVAL;
+
+    if (ro) {
+        for (uint32_t r = 0; r < n; ++r) {
+            if (ro->key) ro->key[r] = pend[r] ? key[r] : -1.0;
+            if (ro->rate) ro->rate[r] = pend[r] ? rate[r] : 0.0;
+            if (ro->t_rem) ro->t_rem[r] = pend[r] ? trem[r] : 0;
+            if (ro->lhat) ro->lhat[r] = pend[r] ? lhat[r] : 0;
+            if (ro->cost) ro->cost[r] = pend[r] ? cost[r] : 0;
+            if (ro->pending) ro->pending[r] = pend[r];
+        }
+    }
+    res->n_pending = n_pend;
+    if (rc != OG_OK) { res->error = 1; goto out; }
+    if (n_pend == 0) { rc = OG_EMPTY; goto out; }
+
+    {
+        /* (a7) BatchPriority (Alg. 1; §4.2): order by (key desc, id asc); B* is
+         * the largest prefix within the token budget and max_batch (A14); bp its last key. */
+        by_key_t* P = (by_key_t*)malloc(sizeof(by_key_t) * n_pend);
+        uint32_t k = 0;
+        for (uint32_t r = 0; r < n; ++r) if (pend[r]) { P[k].key = key[r]; P[k].id = id[r]; P[k].row = r; ++k; }
+        qsort(P, n_pend, sizeof(by_key_t), cmp_key_desc_id_asc);
+        uint64_t csum = 0; uint32_t bstar = 0;
+        while (bstar < n_pend && bstar + 1 <= cfg->max_batch &&
+               csum + cost[P[bstar].row] <= cfg->token_budget) {
+            csum += cost[P[bstar].row]; ++bstar;
+        }
+        double bp = P[bstar - 1].key;   /* bstar >= 1 because every cost <= chunk <= budget */
+        /* (a8) Filter (Alg. 1): key >= fl(fl(p_num/p_den) * bp) (A16) */
+        double p = (double)cfg->p_num / (double)cfg->p_den;
+        double thr = p * bp;
+        uint32_t ncd = 0;
+        for (uint32_t i = 0; i < n_pend; ++i) if (P[i].key >= thr) ++ncd;
+        by_len_t* Cd = (by_len_t*)malloc(sizeof(by_len_t) * ncd);
+        uint32_t c = 0;
+        for (uint32_t i = 0; i < n_pend; ++i) {
+            if (P[i].key < thr) continue;
+            uint32_t r = P[i].row;
+            Cd[c].len = cfg->len_key ? (uint64_t)input_len[r] + generated[r] : (uint64_t)input_len[r];
+            Cd[c].id = id[r]; Cd[c].row = r; ++c;
+        }
+        /* (a9) sort candidates by input length (Alg. 1; A17 tie by id), then slide a
+         * window and keep the first maximum of sum(priority) (strict '>'). */
+        qsort(Cd, ncd, sizeof(by_len_t), cmp_len_asc_id_asc);
+        u128* pf = (u128*)malloc(sizeof(u128) * (ncd + 1));
+        uint64_t* pc = (uint64_t*)malloc(sizeof(uint64_t) * (ncd + 1));
+        pf[0] = 0; pc[0] = 0;
+        for (uint32_t i = 0; i < ncd; ++i) {
+            pf[i + 1] = pf[i] + fixed_point(key[Cd[i].row]);
+            pc[i + 1] = pc[i] + cost[Cd[i].row];
+        }
+        u128 best = 0; int have = 0; uint32_t bi = 0, bj = 0, j = 0;
+        for (uint32_t i = 0; i < ncd; ++i) {
+            /* j(i): the largest j with sum_{i..j} c <= budget and j-i+1 <= max_batch; j(i) is
+             * nondecreasing in i, so it is extended from j(i-1). */
+            if (j < i) j = i;
+            while (j + 1 < ncd && pc[j + 2] - pc[i] <= cfg->token_budget &&
+                   (j + 1) - i + 1 <= cfg->max_batch) ++j;
+            u128 score = pf[j + 1] - pf[i];
+            if (!have || score > best) { best = score; bi = i; bj = j; have = 1; }
+        }
+        uint32_t tot = 0;
+        for (uint32_t i = bi; i <= bj; ++i) {
+            selected[i - bi] = Cd[i].row;
+            if (sel_cost) sel_cost[i - bi] = cost[Cd[i].row];
+            tot += cost[Cd[i].row];
+        }
+        res->n_selected = bj - bi + 1; res->total_tokens = tot; res->n_candidates = ncd;
+        res->b_star = bstar; res->bp = bp; res->thr = thr;
+
+        /* bookkeeping after selection: ever_scheduled / Running for the batch, and
+         * steps_waited += 1 (saturating) for every pending request left out (A12) */
+        uint8_t* insel = (uint8_t*)calloc(n, 1);
+        for (uint32_t i = 0; i < res->n_selected; ++i) insel[selected[i]] = 1;
+        for (uint32_t r = 0; r < n; ++r) {
+            if (!pend[r]) continue;
+            if (insel[r]) {
+                uint32_t m = meta[r];
+                m = m_set_flags(m, m_flags(m) | FL_EVER);
+                if (m_state(m) == ST_QUEUED || m_state(m) == ST_PREEMPTED) m = m_set_state(m, ST_RUNNING);
+                meta[r] = m;
+            } else {
+                uint32_t w = a_waited(aux[r]);
+                if (w < 0xFFFFu) ++w;
+                aux[r] = (aux[r] & 0xFFFFu) | (w << 16);
+            }
+        }
+        free(insel); free(pf); free(pc); free(Cd); free(P);
+    }
+out:
+    free(key); free(lhat); free(cost); free(pend); free(trem); free(rate);
+    return rc;
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* Public: one step over a pool snapshot                                                */
+/* ------------------------------------------------------------------------------------ */
+
+int og_step(const og_config* cfg, const og_group* groups, uint32_t n_groups,
+            const og_table* T, int64_t now_ns, int64_t v_token_ns,
+            const og_pool* pool, const og_tasks* tasks,
+            og_result* res, uint32_t* batch_ids, uint32_t* batch_tokens, uint32_t* batch_rows,
+            const og_rows_out* ro) {
+    uint32_t n = pool->n;
+    og_reset_memo();                 /* the memo lives for one call only */
+    task_view tv; task_view* tvp = NULL;
+    uint32_t *cb = NULL, *ce = NULL; uint64_t *tle = NULL, *tt = NULL;
+    if (tasks && tasks->n) {
+        uint32_t nt = tasks->n;
+        cb = (uint32_t*)malloc(4 * nt); ce = (uint32_t*)malloc(4 * nt);
+        tle = (uint64_t*)malloc(8 * nt); tt = (uint64_t*)malloc(8 * nt);
+        for (uint32_t t = 0; t < nt; ++t) {
+            cb[t] = tasks->call_off[t]; ce[t] = tasks->call_off[t + 1];
+            uint32_t S = tasks->n_stages[t], s = tasks->cur_stage[t];
+            if (S == 0 || S > MAX_STAGES || s >= S || ce[t] < cb[t] || ce[t] > n) {
+                res->error = 1; free(cb); free(ce); free(tle); free(tt); return OG_EINVAL;
+            }
+            /* phi(s) = t_{<=s} / t_total over the matched pattern */
+            uint64_t le = 0, tot = 0;
+            for (uint32_t u = 0; u < S; ++u) {
+                uint64_t ns = (uint64_t)tasks->pattern_ms[(size_t)t * MAX_STAGES + u] * 1000000ull;
+                tot += ns; if (u <= s) le += ns;
+            }
+            tle[t] = le; tt[t] = tot;
+        }
+        tv.n = nt; tv.call_begin = cb; tv.call_end = ce; tv.arrival_ns = tasks->arrival_ns;
+        tv.deadline_ns = tasks->deadline_ns; tv.t_le_s = tle; tv.t_total = tt;
+        tv.goodput_done = tasks->goodput_done;
+        tvp = &tv;
+    }
+    uint32_t* sel = (uint32_t*)malloc(sizeof(uint32_t) * (n ? n : 1));
+    uint32_t* sc = (uint32_t*)malloc(sizeof(uint32_t) * (n ? n : 1));
+    int rc = gmax_step(cfg, groups, n_groups, T, now_ns, v_token_ns, n, pool->id, pool->arrival_ns,
+                       pool->input_len, pool->generated, pool->prefilled, pool->meta, pool->aux,
+                       pool->task, pool->override_R, tvp, res, sel, sc, ro);
+    if (rc == OG_OK) {
+        for (uint32_t i = 0; i < res->n_selected; ++i) {
+            if (batch_ids) batch_ids[i] = pool->id[sel[i]];
+            if (batch_tokens) batch_tokens[i] = sc[i];
+            if (batch_rows) batch_rows[i] = sel[i];
+        }
+    }
+    free(sel); free(sc); free(cb); free(ce); free(tle); free(tt);
+    return rc;
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* (a10) Trace replay: iteration cost model, token timestamps,  */
+/* goodput accounting (§3), stage barriers, v_token as the */
+/* floor of the trailing mean of the last Delta iteration latencies (A24).          */
+/* ------------------------------------------------------------------------------------ */
+
+typedef struct {
+    uint32_t n_rows, n_tasks;
+    const int64_t* arrival_ns;      /* standalone rows; ignored for compound calls */
+    const uint32_t* input_len;
+    const uint32_t* true_out;       /* L_o >= 1 (hidden from the scheduler) */
+    const uint32_t* group;
+    const uint32_t* dist_row;
+    const uint32_t* override_R;
+    const uint32_t* task;           /* NO_TASK or the owning task */
+    const int64_t* task_arrival_ns;
+    const int64_t* task_deadline_ns;       /* D relative to a_c (before SLO scaling) */
+    const uint32_t* task_n_stages;
+    const uint32_t* stage_kind;            /* n_tasks*8: 0 LLM, 1 tool */
+    const int64_t* stage_exec_ns;          /* n_tasks*8: tool time */
+    const uint32_t* stage_pattern_ms;      /* n_tasks*8: matched-pattern stage time */
+    const uint32_t* stage_call_begin;      /* n_tasks*8: rows of an LLM stage */
+    const uint32_t* stage_call_end;
+} og_trace;
+
+typedef struct {
+    uint32_t n_steps, log_ids;
+    int64_t v_token0_ns, c0_ns, c_att_ns, c_lin_ns;
+    uint64_t load_num, load_den, slo_num, slo_den;   /* arrival' = a*load_den/load_num; SLO' = t*slo_num/slo_den */
+} og_replay_cfg;
+
+typedef struct {
+    uint64_t token_goodput, tokens_processed;
+    int64_t sim_end_ns;
+    uint32_t request_goodput, n_done, n_dropped, steps, n_tasks_done, error;
+} og_replay_result;
+
+typedef struct {
+    int64_t now_ns;
+    uint32_t n_selected, total_tokens, n_candidates, b_star;
+    double bp;
+    uint64_t ids_hash;
+} og_step_log;
+
+static uint64_t fnv1a_ids(const uint32_t* ids, uint32_t n) {
+    uint64_t h = 1469598103934665603ull;
+    for (uint32_t i = 0; i < n; ++i)
+        for (int b = 0; b < 4; ++b) { h ^= (ids[i] >> (8 * b)) & 0xFFu; h *= 1099511628211ull; }
+    return h;
+}
+
+int og_replay(const og_config* cfg, const og_group* groups_in, uint32_t n_groups,
+              const og_table* T, const og_trace* tr, const og_replay_cfg* rc,
+              og_replay_result* out, og_step_log* log, uint32_t* log_ids) {
+    memset(out, 0, sizeof(*out));
+    og_reset_memo();
+    uint32_t n = tr->n_rows, nt = tr->n_tasks;
+    if (!rc->load_num || !rc->load_den || !rc->slo_num || !rc->slo_den || n_groups > 256) { out->error = 1; return OG_EINVAL; }
+    /* SLO scaling of the group table (§6.4 P:784-786 sweep shape) */
+    og_group G[256];
+    for (uint32_t g = 0; g < n_groups; ++g) {
+        G[g] = groups_in[g];
+        G[g].ttft_ns = (int64_t)((u128)(uint64_t)G[g].ttft_ns * rc->slo_num / rc->slo_den);
+        G[g].tbt_ns = (int64_t)((u128)(uint64_t)G[g].tbt_ns * rc->slo_num / rc->slo_den);
+        G[g].e2el_ns = (int64_t)((u128)(uint64_t)G[g].e2el_ns * rc->slo_num / rc->slo_den);
+        G[g].be_deadline_ns = (int64_t)((u128)(uint64_t)G[g].be_deadline_ns * rc->slo_num / rc->slo_den);
+    }
+    uint32_t* id = (uint32_t*)malloc(4 * (n + 1));
+    int64_t* arr = (int64_t*)malloc(8 * (n + 1));
+    uint32_t* gen = (uint32_t*)calloc(n + 1, 4);
+    uint32_t* pre = (uint32_t*)calloc(n + 1, 4);
+    uint32_t* meta = (uint32_t*)malloc(4 * (n + 1));
+    uint32_t* aux = (uint32_t*)malloc(4 * (n + 1));
+    uint8_t* late = (uint8_t*)calloc(n + 1, 1);
+    uint32_t* sel = (uint32_t*)malloc(4 * (n + 1));
+    uint32_t* selc = (uint32_t*)malloc(4 * (n + 1));
+    uint32_t* selid = (uint32_t*)malloc(4 * (n + 1));
+    /* task state */
+    uint32_t* cur = (uint32_t*)calloc(nt + 1, 4);
+    uint32_t* left = (uint32_t*)calloc(nt + 1, 4);
+    uint8_t* tdone = (uint8_t*)calloc(nt + 1, 1);
+    int64_t* timer = (int64_t*)malloc(8 * (nt + 1));
+    int64_t* ta = (int64_t*)malloc(8 * (nt + 1));
+    int64_t* tD = (int64_t*)malloc(8 * (nt + 1));
+    uint64_t* gdone = (uint64_t*)calloc(nt + 1, 8);
+    uint32_t* cb = (uint32_t*)calloc(nt + 1, 4);
+    uint32_t* ce = (uint32_t*)calloc(nt + 1, 4);
+    uint64_t* tle = (uint64_t*)calloc(nt + 1, 8);
+    uint64_t* ttot = (uint64_t*)calloc(nt + 1, 8);
+    int64_t lat_ring[1024]; uint32_t ring_n = 0, ring_pos = 0; int64_t ring_sum = 0;
+    int ret = OG_OK;
+    if (cfg->frame_steps > 1024) { ret = OG_EINVAL; goto done; }
+
+    for (uint32_t r = 0; r < n; ++r) {
+        id[r] = r;
+        uint32_t fl = 0;
+        if (tr->task[r] != NO_TASK) fl |= FL_COMPOUND;
+        if (tr->override_R[r]) fl |= FL_OVERRIDE;
+        if (tr->input_len[r] == 0 || tr->true_out[r] == 0 || tr->group[r] >= n_groups) { ret = OG_EINVAL; goto done; }
+        if (tr->override_R[r] && groups_in[tr->group[r]].type != OG_DDL) { ret = OG_EINVAL; goto done; }
+        if ((tr->task[r] != NO_TASK) != (groups_in[tr->group[r]].type == OG_CMP)) { ret = OG_EINVAL; goto done; }
+        uint32_t st = (fl & FL_COMPOUND) ? ST_WAITING : ST_QUEUED;
+        meta[r] = tr->group[r] | (st << 8) | (fl << 12);
+        aux[r] = tr->dist_row[r] & 0xFFFFu;
+        arr[r] = (fl & FL_COMPOUND) ? INT64_MAX
+                                    : (int64_t)((u128)(uint64_t)tr->arrival_ns[r] * rc->load_den / rc->load_num);
+    }
+    for (uint32_t t = 0; t < nt; ++t) {
+        ta[t] = (int64_t)((u128)(uint64_t)tr->task_arrival_ns[t] * rc->load_den / rc->load_num);
+        tD[t] = (int64_t)((u128)(uint64_t)tr->task_deadline_ns[t] * rc->slo_num / rc->slo_den);
+        uint32_t S = tr->task_n_stages[t];
+        if (S == 0 || S > MAX_STAGES) { ret = OG_EINVAL; goto done; }
+        uint64_t tot = 0;
+        for (uint32_t u = 0; u < S; ++u) tot += (uint64_t)tr->stage_pattern_ms[t * MAX_STAGES + u] * 1000000ull;
+        ttot[t] = tot;
+        timer[t] = ta[t];      /* stage 0 "starts" when the task arrives */
+        cur[t] = 0;
+        cb[t] = ce[t] = 0;
+    }
+
+    int64_t now = 0;
+    uint32_t steps = 0;
+    for (;;) {
+        /* stage starts whose time has come: timer[t] is the start time of stage cur[t]
+         * (task arrival for stage 0, the end of the previous stage otherwise) */
+        for (uint32_t t = 0; t < nt; ++t) {
+            while (!tdone[t] && timer[t] <= now) {
+                int64_t at = timer[t];
+                uint32_t s = cur[t], S = tr->task_n_stages[t];
+                if (s == S) {                                   /* last stage ended at `at` */
+                    tdone[t] = 1; out->n_tasks_done++; timer[t] = INT64_MAX;
+                    if (at <= ta[t] + tD[t]) {                  /* §3 P:213 compound goodput */
+                        uint64_t tot = 0;
+                        for (uint32_t u = 0; u < S; ++u) {
+                            uint32_t kk = t * MAX_STAGES + u;
+                            if (tr->stage_kind[kk] == 0)
+                                for (uint32_t q = tr->stage_call_begin[kk]; q < tr->stage_call_end[kk]; ++q)
+                                    tot += (uint64_t)G[tr->group[q]].w_in * tr->input_len[q] +
+                                           (uint64_t)G[tr->group[q]].w_out * tr->true_out[q];
+                        }
+                        out->token_goodput += tot; out->request_goodput++;
+                    }
+                    break;
+                }
+                uint32_t k = t * MAX_STAGES + s;
+                if (tr->stage_kind[k] == 1) {                   /* tool node: fixed exec time */
+                    cur[t] = s + 1; timer[t] = at + tr->stage_exec_ns[k];
+                    continue;
+                }
+                /* LLM stage: release its calls with arrival = stage start */
+                cb[t] = tr->stage_call_begin[k]; ce[t] = tr->stage_call_end[k];
+                left[t] = ce[t] - cb[t];
+                if (left[t] == 0) { ret = OG_EINVAL; goto done; }
+                for (uint32_t r = cb[t]; r < ce[t]; ++r) { arr[r] = at; meta[r] = m_set_state(meta[r], ST_QUEUED); }
+                uint64_t le = 0;
+                for (uint32_t u = 0; u <= s; ++u) le += (uint64_t)tr->stage_pattern_ms[t * MAX_STAGES + u] * 1000000ull;
+                tle[t] = le;
+                timer[t] = INT64_MAX;
+            }
+        }
+        if (steps >= rc->n_steps) break;
+
+        int64_t v = ring_n ? ring_sum / (int64_t)ring_n : rc->v_token0_ns;
+        task_view tv = { nt, cb, ce, ta, tD, tle, ttot, gdone };
+        og_result res;
+        int st = gmax_step(cfg, G, n_groups, T, now, v, n, id, arr, tr->input_len, gen, pre, meta, aux,
+                           tr->task, tr->override_R, &tv, &res, sel, selc, NULL);
+        out->n_dropped += res.n_dropped_now;
+        if (st == OG_EINVAL) { ret = OG_EINVAL; goto done; }
+        if (st == OG_EMPTY) {
+            /* idle: jump to the next arrival or timer; stop when nothing is left (drained) */
+            int64_t nxt = INT64_MAX;
+            for (uint32_t r = 0; r < n; ++r)
+                if (!(m_flags(meta[r]) & FL_COMPOUND) && m_state(meta[r]) == ST_QUEUED && arr[r] > now && arr[r] < nxt) nxt = arr[r];
+            for (uint32_t t = 0; t < nt; ++t)
+                if (!tdone[t] && timer[t] != INT64_MAX && timer[t] > now && timer[t] < nxt) nxt = timer[t];
+            if (nxt == INT64_MAX) break;
+            now = nxt;
+            continue;
+        }
+        /* iteration latency: c0 + c_att * max context + c_lin * |batch| */
+        int64_t maxctx = 0;
+        for (uint32_t i = 0; i < res.n_selected; ++i) {
+            uint32_t r = sel[i];
+            int64_t ctx = pre[r] < tr->input_len[r] ? (int64_t)pre[r] + selc[i]
+                                                     : (int64_t)tr->input_len[r] + gen[r];
+            if (ctx > maxctx) maxctx = ctx;
+        }
+        int64_t latency = rc->c0_ns + rc->c_att_ns * maxctx + rc->c_lin_ns * (int64_t)res.n_selected;
+        now += latency;
+        ++steps;
+        out->tokens_processed += res.total_tokens;
+        if (log) {
+            for (uint32_t i = 0; i < res.n_selected; ++i) selid[i] = sel[i];
+            og_step_log* L = &log[steps - 1];
+            L->now_ns = now; L->n_selected = res.n_selected; L->total_tokens = res.total_tokens;
+            L->n_candidates = res.n_candidates; L->b_star = res.b_star; L->bp = res.bp;
+            L->ids_hash = fnv1a_ids(selid, res.n_selected);
+            if (log_ids) memcpy(log_ids + (size_t)(steps - 1) * cfg->max_batch, selid, 4 * res.n_selected);
+        }
+        /* progress of the executed batch (iteration end = token timestamp) */
+        for (uint32_t i = 0; i < res.n_selected; ++i) {
+            uint32_t r = sel[i];
+            const og_group* gr = &G[tr->group[r]];
+            int emit = 0;
+            if (pre[r] < tr->input_len[r]) {
+                pre[r] += selc[i];
+                if (pre[r] == tr->input_len[r]) emit = 1;   /* A28: prefill end emits token 0 */
+            } else emit = 1;
+            if (!emit) continue;
+            uint32_t tok = gen[r];
+            if (gr->type == OG_LAT) {                       /* §3, token i on the timeline */
+                if (now <= arr[r] + gr->ttft_ns + (int64_t)tok * gr->tbt_ns) out->token_goodput += gr->w_out;
+                else late[r] = 1;
+            }
+            gen[r] = tok + 1;
+            if (gen[r] < tr->true_out[r]) continue;
+            /* completion */
+            meta[r] = m_set_state(meta[r], ST_DONE);
+            out->n_done++;
+            if (gr->type == OG_DDL) {                       /* §3 P:212 all-or-nothing */
+                if (now <= arr[r] + gr->e2el_ns) {
+                    out->token_goodput += (m_flags(meta[r]) & FL_OVERRIDE) ? tr->override_R[r]
+                        : (uint64_t)gr->w_in * tr->input_len[r] + (uint64_t)gr->w_out * tr->true_out[r];
+                    out->request_goodput++;
+                }
+            } else if (gr->type == OG_LAT) {
+                if (!late[r]) out->request_goodput++;
+            } else if (gr->type == OG_CMP) {                /* §3 P:213 + stage barrier S:422-430 */
+                uint32_t t = tr->task[r];
+                gdone[t] += (uint64_t)gr->w_in * tr->input_len[r] + (uint64_t)gr->w_out * tr->true_out[r];
+                if (--left[t] == 0) {                       /* stage barrier: next stage starts now */
+                    cur[t] += 1; cb[t] = ce[t] = 0; timer[t] = now;
+                }
+            }
+        }
+        /* v_token: floor of the trailing mean of the last Delta latencies */
+        if (ring_n < cfg->frame_steps) { lat_ring[ring_n++] = latency; ring_sum += latency; }
+        else { ring_sum += latency - lat_ring[ring_pos]; lat_ring[ring_pos] = latency; ring_pos = (ring_pos + 1) % cfg->frame_steps; }
+    }
+    out->steps = steps; out->sim_end_ns = now;
+done:
+    out->error = ret != OG_OK;
+    free(id); free(arr); free(gen); free(pre); free(meta); free(aux); free(late); free(sel); free(selc); free(selid);
+    free(cur); free(left); free(tdone); free(timer); free(ta); free(tD); free(gdone); free(cb); free(ce); free(tle); free(ttot);
+    return ret;
+}
