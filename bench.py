@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""bench.py -- the JITServe GMAX scheduling step on B200 (contract: DESIGN.md §8).
+
+Headline (N=1): BASELINE config C3 -- one GMAX step (a1-a9) over a pool of 2^20 pending
+requests resident in HBM (16 SLO groups, token budget 8192, B_max 8192), timed on the device
+with CUDA events.  `value` = pending requests scheduled per second, summed over ranks (weak
+scaling: every rank owns a 2^20-row shard).  Also reported:
+  * roofline of the dominant kernel (k_score) against the measured HBM copy bandwidth;
+  * e2e: the same step through the C ABI from pinned HOST buffers (pool H2D + batch D2H);
+  * replay: BASELINE config C5(i) -- the load x SLO-scale sweep of independent trace replays,
+    replayed serving steps per second (replays sharded i -> rank i mod N, no communication);
+  * cpu_baseline: the CPU oracle (oracle/, plain C, 1 core) on a bounded sample of C3.
+`--impl reference` runs the oracle as the reference arm (rank 0 only).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = "pending requests scheduled/sec (1M pool)"
+UNIT = "requests/s"
+# algorithmic bytes of k_score: per row 32 B read (arrival 8, input_len, generated,
+# prefilled, cached bound, meta, aux) + 16 B written (8-B key image, cost, aux); per compound
+# task 72 B (call_off 8, arrival 8, deadline 8, stage 4, n_stages 4, pattern 32, goodput_done 8)
+BYTES_ROW, BYTES_TASK = 48, 72
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rows", type=int, default=1 << 20)
+    ap.add_argument("--rot", type=int, default=6, help="pool copies rotated to defeat the 126 MB L2")
+    ap.add_argument("--replays", type=int, default=4096)
+    ap.add_argument("--replay-steps", type=int, default=4096)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-replay", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return None
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, idx):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={idx}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = [l.split(",") for l in open(self.f.name).read().strip().splitlines() if l.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+            except Exception:
+                pass
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def build_c3(rank, rows):
+    d = W.pool_snapshot(3 + 1000 * rank, rows)
+    return d
+
+
+def oracle_step_timing(d, budget_s=10.0, max_steps=40):
+    """CPU oracle on the C3 pool, pinned to one host core (bounded sample)."""
+    import oracle
+    try:
+        os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
+    except Exception:
+        pass
+    pool = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in d["pool"].items()}
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while len(times) < max_steps and (not times or time.perf_counter() < t_end):
+        t0 = time.perf_counter()
+        out = oracle.step(d["cfg"], d["groups"], d["table"], d["now_ns"], d["v_token_ns"], pool, d["tasks"],
+                          rows_out=False)
+        times.append(time.perf_counter() - t0)
+        pool["meta"], pool["aux"] = out["meta"], out["aux"]
+    t = sum(times) / len(times)
+    return t, len(times)
+
+
+def cpu_model():
+    try:
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                return l.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    d = build_c3(0, args.rows)
+    n = len(d["pool"]["input_len"])
+    import oracle
+    oracle.build()
+    for _ in range(max(0, min(args.warmup, 1))):
+        oracle_step_timing(d, budget_s=0.0, max_steps=1)
+    t, k = oracle_step_timing(d, budget_s=60.0, max_steps=max(1, min(args.steps, 20)))
+    v = n / t
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": k,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C3: 2^20-row pending pool, 16 SLO groups, tau 8192, B_max 8192", "rows": n},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{k} oracle steps over the full C3 pool ({n} rows), 1 core of {cpu_model()}"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def pinned_pool(d):
+    import torch
+    out = {}
+    for k, v in d["pool"].items():
+        if isinstance(v, np.ndarray):
+            t = torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
+            out[k] = t
+        else:
+            out[k] = v
+    tasks = {}
+    for k, v in d["tasks"].items():
+        tasks[k] = torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
+    return out, tasks
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2504_20068_b200 import Scheduler
+    dev = local
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    def allmax(x):
+        if ws == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(x):
+        if ws == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    # ------------------------------------------------------------------ C3 pool step
+    d = build_c3(rank, args.rows)
+    n = len(d["pool"]["input_len"])
+    nt = len(d["tasks"]["arrival_ns"])
+    now, v = d["now_ns"], d["v_token_ns"]
+    K, Wm = args.steps, max(3, args.warmup)
+    hs = []
+    for i in range(args.rot):
+        s = Scheduler(d["cfg"], d["groups"], d["table"], capacity=n, task_capacity=nt, device=dev, stream=stream)
+        s.load(d["pool"], d["tasks"])
+        hs.append(s)
+    # warm-up (synchronous: validates that every step resolves on the graph's fast path)
+    statuses = []
+    for i in range(Wm):
+        r = hs[i % args.rot].step(now, v)
+        statuses.append(r["status"])
+    sel = r
+    for s in hs:
+        s.kernel_times(slots=K)
+    barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(K):
+        hs[k % args.rot].step_async(now, v)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1) / K
+    ms_max = allmax(ms)
+    # every timed step must have resolved on the fast path (checked on the last step of each handle)
+    fallback = 0
+    for s in hs:
+        rr = s.fetch()
+        fallback += int(rr["status"] not in (0, 1))
+    kt = np.zeros(5)
+    for i, s in enumerate(hs):
+        steps_i = len(range(i, K, args.rot))
+        if steps_i:
+            kt += np.array(s.kernel_times()) * steps_i
+    kt /= K
+    total_rows = allsum(float(n))
+    value = total_rows / (ms_max / 1e3)
+    alg_bytes = n * BYTES_ROW + nt * BYTES_TASK
+    pk = peaks()
+    hbm_peak = pk["hbm_gbs"] if pk else 6650.0
+    achieved = alg_bytes / (kt[0] / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "k_score", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if pk else "fallback 6650 GB/s",
+                "alg_bytes_per_launch": alg_bytes, "k_score_ms": kt[0],
+                "kernel_ms": {"score": kt[0], "select": kt[1], "candidates": kt[2], "group": kt[3], "chain": kt[4]},
+                "frac_of_8tbs_datasheet": achieved / 8000.0}
+
+    # ------------------------------------------------------------------ e2e through the C ABI
+    e2e = None
+    try:
+        hp, ht = pinned_pool(d)
+        s0 = hs[0]
+        h2d = sum(int(t.numel() * t.element_size()) for k, t in hp.items() if hasattr(t, "numel") and k != "true_out")
+        h2d += sum(int(t.numel() * t.element_size()) for t in ht.values())
+        for _ in range(2):
+            s0.load(hp, ht)
+            s0.step(now, v)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d2h = 0
+        for _ in range(args.e2e_steps):
+            s0.load(hp, ht)
+            rr = s0.step(now, v)
+            d2h += 248 + 12 * rr["n_selected"]
+        torch.cuda.synchronize()
+        te = (time.perf_counter() - t0) / args.e2e_steps
+        te = allmax(te)
+        e2e = {"value": total_rows / te, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": int(d2h / args.e2e_steps), "ms_per_step": te * 1e3,
+               "how": "wall clock around jit_sched_load(pinned host pool) + jit_sched_step (batch D2H), synchronized"}
+    except Exception as ex:  # pragma: no cover
+        e2e = {"value": None, "unit": UNIT, "error": str(ex)[:200]}
+    for s in hs:
+        s.close()
+
+    # ------------------------------------------------------------------ C5(i) replay sweep
+    replay = None
+    if not args.no_replay:
+        traces = [W.trace_mixed(k) for k in range(4)]
+        sweep = W.c5_sweep(args.replays)
+        specs = [dict(sp, trace=i % len(traces)) for i, sp in enumerate(sweep)]
+        mine = specs[rank::ws]
+        rc = dict(traces[0]["rcfg"], n_steps=args.replay_steps)
+        rs = Scheduler(traces[0]["cfg"], traces[0]["groups"], traces[0]["table"], capacity=64, task_capacity=8,
+                       device=dev, stream=stream)
+        rs.replay([t["trace"] for t in traces], mine[:min(len(mine), 64)], rc)     # warm-up
+        barrier()
+        torch.cuda.synchronize()
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record(stream)
+        res, _ = rs.replay([t["trace"] for t in traces], mine, rc)
+        r1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        rms = allmax(r0.elapsed_time(r1))
+        steps_done = allsum(float(sum(r["steps"] for r in res)))
+        replay = {"metric": "replayed serving steps/sec", "value": steps_done / (rms / 1e3), "unit": "steps/s",
+                  "workload": f"C5(i): {args.replays} replays (64 load x 64 SLO-scale points, 4 base mixed 1:1:1 traces "
+                              f"of 2048 rows), up to {args.replay_steps} steps each, tau 2048, B_max 128",
+                  "ms": rms, "steps_total": int(steps_done), "scaling": "weak" if ws > 1 else None,
+                  "goodput_tokens_sum": int(allsum(float(sum(r["token_goodput"] for r in res))))}
+        rs.close()
+
+    # ------------------------------------------------------------------ CPU oracle baseline
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        import oracle
+        t, k = oracle_step_timing(d, budget_s=12.0, max_steps=30)
+        cpu = {"value": n / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{k} oracle steps over the full C3 pool ({n} rows), pinned to 1 core of {cpu_model()}",
+               "ms_per_step": t * 1e3}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": Wm,
+                "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "C3: 2^20-row pending pool per GPU (40% chat, 30% deep-research, 30% compound "
+                                       "calls in 16-call tasks), 16 SLO groups, tau 8192, B_max 8192, v_token 15 ms",
+                           "rows_per_gpu": n, "tasks_per_gpu": nt,
+                           "l2": f"inputs larger than L2: {args.rot} rotated pool copies of ~{(n * 100) >> 20} MiB workspace each",
+                           "parallelism": f"{ws} independent 2^20-row shards (no data-path collective)" if ws > 1 else "single GPU",
+                           "fast_path_fallbacks": fallback, "last_batch": {"n_selected": sel["n_selected"],
+                                                                         "b_star": sel["b_star"],
+                                                                         "n_candidates": sel["n_candidates"]}},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 7 * K,
+                "clocks": clocks, "replay": replay}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

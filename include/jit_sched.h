@@ -1,0 +1,276 @@
+/*
+ * jit_sched.h -- C ABI of libjitsched.so: the JITServe GMAX scheduling step (arXiv 2504.20068)
+ * as hand-written CUDA for sm_100a (B200).
+ *
+ * The library runs, over every pending request of a pool resident in HBM, the per-iteration
+ * step of Alg. 1:
+ *   (a1) admission control: drop requests unscheduled after waiting_time
+ *   (a2) conservative remaining length: an upper quantile of the length distribution
+ *        conditioned on the tokens generated so far, refreshed every R tokens
+ *   (a3) just-in-time rate / remaining time per SLO type
+ *   (a4) compound requests: len_rem and goodput aggregated over the calls of the current
+ *        stage against the stage sub-deadline D_s = phi(s) D
+ *   (a5) margin-goodput key = goodput / t_gen (App. B I(k) P:911-915) with
+ *        starvation inflation
+ *   (a6) per-step token cost (chunked prefill)
+ *   (a7)-(a9) BatchPriority bp, cutoff filter p*bp and length-sorted sliding window
+ *        (Alg. 1; §4.2) under a per-step token budget
+ * and a trace replay (a10) that runs the step inside an iteration cost model and counts
+ * token / request goodput (§3).  Readings of the paper are numbered A1..A39 in
+ * DESIGN.md §3; the exact arithmetic contract is DESIGN.md §4.
+ *
+ * Conventions (all entry points):
+ *  - Plain C types only.  Every pointer is a HOST pointer unless the field says otherwise.
+ *  - The caller owns every buffer it passes.  Inputs are consumed during the call; nothing
+ *    is retained.  The library owns only its handle; all device memory it uses is carved
+ *    from the caller-provided workspace (allocated by PyTorch's caching allocator).
+ *  - Calls are synchronous with respect to their outputs on return, and enqueue their
+ *    device work on cfg.stream (a cudaStream_t; NULL = legacy default stream).
+ *  - Return value: JIT_OK (0), JIT_EMPTY (1, no pending request; an empty batch), or a
+ *    negative error.  jit_sched_last_error() returns a message owned by the handle.
+ *  - No C++ exception crosses the ABI.  A handle is not thread-safe; handles are independent.
+ */
+#ifndef JIT_SCHED_H
+#define JIT_SCHED_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    JIT_OK = 0,
+    JIT_EMPTY = 1,        /* no pending request (SPEC EmptyQueue); n_selected = 0 */
+    JIT_EINVAL = -1,      /* bad config / table / pool (S:55-63 InvalidLength, ConfigError) */
+    JIT_ETRACE = -2,      /* bad replay trace (S:417 InvalidTrace) */
+    JIT_ECAPACITY = -3,   /* more rows / tasks / candidates than the workspace was sized for */
+    JIT_ECUDA = -4,       /* a CUDA runtime error (message in last_error) */
+    JIT_ESTATE = -6       /* call order violated (e.g. step before load) */
+};
+
+/* SLO types, §3; best effort P:216 */
+enum { JIT_LAT = 0, JIT_DDL = 1, JIT_CMP = 2, JIT_BE = 3 };
+/* request states + WAITING = compound call whose stage is not released yet */
+enum { JIT_QUEUED = 0, JIT_RUNNING = 1, JIT_PREEMPTED = 2, JIT_DONE = 3, JIT_DROPPED = 4, JIT_WAITING = 5 };
+/* request flags */
+enum { JIT_F_EVER = 1, JIT_F_COMPOUND = 2, JIT_F_OVERRIDE = 4 };
+#define JIT_NO_TASK 0xFFFFFFFFu
+#define JIT_MAX_STAGES 8
+/* jit_config.flags */
+#define JIT_CFG_DEBUG_ROWS 1u   /* keep per-row rate / t_rem / Lhat / cost for jit_sched_read_rows */
+
+/* One SLO group (a row of the SLO table; reading A35).  Times are int64 ns.
+ * LAT uses ttft/tbt, DDL e2el, CMP e2el per stage (D = e2el * stages), BE be_deadline.
+ * Base goodput R(k) = w_in * L_i + w_out * L_o (App. B). */
+typedef struct jit_slo_group {
+    uint32_t type, w_in, w_out, reserved;
+    int64_t ttft_ns, tbt_ns, e2el_ns, be_deadline_ns;
+} jit_slo_group;
+
+/* Length-distribution table (stand-in for the QRF of P:269; reading A8).
+ * edges[n_bins]: strictly increasing, edges[0] >= 1, edges[n_bins-1] = l_max (< 65536).
+ * cum[n_rows * n_bins]: row-major, nondecreasing per row: cum[r][k] = #samples with L <= edges[k]. */
+typedef struct jit_len_table {
+    uint32_t n_rows, n_bins, l_max, reserved;
+    const uint32_t* edges;
+    const uint32_t* cum;
+} jit_len_table;
+
+/* Scheduler configuration (defaults in DESIGN.md §2 / SURVEY Appendix A). */
+typedef struct jit_config {
+    uint32_t token_budget;     /* tau: per-step token budget (A14) */
+    uint32_t max_batch;        /* B_max */
+    uint32_t prefill_chunk;    /* chunked-prefill size (A25), 1 <= chunk <= tau */
+    uint32_t refine_interval;  /* R: refresh the length bound every R tokens */
+    uint32_t frame_steps;      /* Delta: steps per starvation frame */
+    uint32_t q_num, q_den;     /* length quantile q = q_num/q_den in (0,1] (A3) */
+    uint32_t p_num, p_den;     /* cutoff p in (0,1] */
+    uint32_t delta_starve;     /* goodput added per frame waited (A12) */
+    uint32_t len_key;          /* 0: group by input length; 1: by input+generated (A17) */
+    uint32_t appb_filter;      /* 1: App. B filter t_gen <= t_rem, else goodput 0 (A22) */
+    int64_t eps_ns;            /* epsilon of App. B I(k) (A2) */
+    int64_t waiting_ns;        /* admission waiting_time, strict '>' (A29) */
+    uint32_t capacity;         /* max pool rows the workspace holds */
+    uint32_t task_capacity;    /* max compound tasks */
+    uint32_t flags;            /* JIT_CFG_* */
+    int32_t device;            /* CUDA device ordinal */
+    void* stream;              /* cudaStream_t for all device work */
+} jit_config;
+
+/* A pool snapshot (SoA, n rows).  Layout rule: standalone rows first, then compound calls
+ * grouped by task: rows of task t are [call_off[t], call_off[t+1]), call_off[0] = n_single,
+ * call_off[n_tasks] = n.  meta = group (bits 0-7) | state << 8 | flags << 12 (bits 16-31
+ * must be 0); aux = dist_row (bits 0-15) | steps_waited << 16.  If on_device != 0 every
+ * array pointer is a device pointer (read during the call only). */
+typedef struct jit_pool {
+    uint32_t n, n_single, n_tasks;
+    int32_t on_device;
+    const uint32_t* id;            /* request id, the tie-break of every order (A18) */
+    const int64_t* arrival_ns;
+    const uint32_t* input_len;     /* L_i >= 1 */
+    const uint32_t* generated;     /* g */
+    const uint32_t* prefilled;     /* prompt tokens already prefilled */
+    const uint32_t* meta;
+    const uint32_t* aux;
+    const uint32_t* task;          /* owning task or JIT_NO_TASK */
+    const uint32_t* override_R;    /* R(k) set directly (App. D constructions) when JIT_F_OVERRIDE */
+    /* compound tasks (may be NULL when n_tasks == 0) */
+    const uint32_t* call_off;      /* n_tasks + 1 */
+    const int64_t* task_arrival_ns;   /* a_c */
+    const int64_t* task_deadline_ns;  /* D relative to a_c */
+    const uint32_t* cur_stage;        /* s */
+    const uint32_t* n_stages;         /* S <= JIT_MAX_STAGES */
+    const uint32_t* pattern_ms;       /* n_tasks * 8: matched-pattern stage times (phi) */
+    const uint64_t* goodput_done;     /* goodput of the task's finished calls */
+} jit_pool;
+
+/* Per-step input.  Progress updates (optional) are applied before scoring: row indices into
+ * the loaded pool and their new generated / prefilled / state values (host arrays). */
+typedef struct jit_step_in {
+    int64_t now_ns;
+    int64_t v_token_ns;            /* average per-token generation time v_token */
+    uint32_t n_progress, reserved;
+    const uint32_t* prog_row;
+    const uint32_t* prog_generated;
+    const uint32_t* prog_prefilled;
+    const uint32_t* prog_state;
+} jit_step_in;
+
+/* Selected batch (BestGroup, Alg. 1), in window order (len asc, id asc; A20).
+ * ids / tokens / rows are host arrays of `capacity` entries (any may be NULL). */
+typedef struct jit_batch {
+    uint32_t capacity;
+    uint32_t n_selected, total_tokens, n_candidates, b_star, n_pending, n_dropped, status;
+    double bp, thr;                /* batch priority and cutoff threshold fl(p * bp) */
+    uint32_t* ids;
+    uint32_t* tokens;
+    uint32_t* rows;
+} jit_batch;
+
+typedef struct jit_sched jit_sched;
+
+/* Device workspace the handle needs for cfg (capacity / task_capacity / table size). */
+int jit_sched_workspace_bytes(const jit_config* cfg, const jit_len_table* table, uint64_t* bytes);
+
+/* Create a handle.  groups: n_groups <= 256 SLO groups; table: copied to the workspace.
+ * dev_workspace: device memory of ws_bytes >= jit_sched_workspace_bytes(), 256-B aligned. */
+int jit_sched_init(const jit_config* cfg, const jit_slo_group* groups, uint32_t n_groups,
+                   const jit_len_table* table, void* dev_workspace, uint64_t ws_bytes, jit_sched** out);
+
+/* Replace the resident pool (H2D or D2D copy + pack).  Invalidates the cached length bounds. */
+int jit_sched_load(jit_sched* h, const jit_pool* pool);
+
+/* One GMAX step over the resident pool; writes the batch.  Mutates the pool's admission
+ * state, steps_waited (+1 saturating for pending requests left out) and ever_scheduled. */
+int jit_sched_step(jit_sched* h, const jit_step_in* in, jit_batch* out);
+
+/* Enqueue one step without waiting for it (results stay on the device; read them with
+ * jit_sched_fetch_batch).  Used for device-side timing; progress updates not allowed. */
+int jit_sched_step_async(jit_sched* h, int64_t now_ns, int64_t v_token_ns);
+int jit_sched_fetch_batch(jit_sched* h, jit_batch* out);
+
+/* Copy per-row state / outputs of the last step to host arrays of n entries (NULL = skip).
+ * key: -1 for rows not pending.  rate / t_rem / lhat / cost need JIT_CFG_DEBUG_ROWS. */
+int jit_sched_read_rows(jit_sched* h, double* key, double* rate, int64_t* t_rem, uint32_t* lhat,
+                        uint32_t* cost, uint32_t* pending, uint32_t* meta, uint32_t* aux);
+
+/* Per-kernel device time, from CUDA events recorded (as graph event nodes) on cfg.stream
+ * around each kernel of the step.  enable > 0 keeps one event set per step for up to
+ * `enable` steps; 0 turns timing off; < 0 leaves it unchanged.  ms_out (n_out <= 5) gets the
+ * average in ms over the recorded steps of [score, select, candidates, group, whole step]. */
+int jit_sched_kernel_times(jit_sched* h, int enable, float* ms_out, uint32_t n_out);
+
+/* ---------------------------------------------------------------------------------------
+ * Trace replay (a10): one persistent CTA per replay runs the step, the iteration cost model
+ * c0 + c_att * max context + c_lin * |batch|, token timestamps at the
+ * iteration end, LAT/DDL/CMP goodput (§3), stage barriers and
+ * v_token = floor(mean of the last Delta latencies).  Replays are independent.
+ * ------------------------------------------------------------------------------------- */
+typedef struct jit_trace {
+    uint32_t n_rows, n_tasks;
+    const int64_t* arrival_ns;     /* standalone rows (compound calls arrive at stage release) */
+    const uint32_t* input_len;
+    const uint32_t* true_out;      /* L_o >= 1, hidden from the scheduler */
+    const uint32_t* group;
+    const uint32_t* dist_row;
+    const uint32_t* override_R;    /* 0 = none; only on DDL rows */
+    const uint32_t* task;          /* JIT_NO_TASK or owning task (CMP group) */
+    const int64_t* task_arrival_ns;
+    const int64_t* task_deadline_ns;
+    const uint32_t* task_n_stages;
+    const uint32_t* stage_kind;        /* n_tasks * 8: 0 LLM stage, 1 tool stage */
+    const int64_t* stage_exec_ns;      /* tool execution time */
+    const uint32_t* stage_pattern_ms;  /* matched-pattern stage time (phi) */
+    const uint32_t* stage_call_begin;  /* rows of an LLM stage: [begin, end) */
+    const uint32_t* stage_call_end;
+} jit_trace;
+
+typedef struct jit_replay_spec {
+    uint32_t trace;                /* index into the traces array */
+    uint32_t reserved;
+    uint64_t load_num, load_den;   /* arrival' = floor(arrival * load_den / load_num) */
+    uint64_t slo_num, slo_den;     /* SLO time' = floor(t * slo_num / slo_den) */
+} jit_replay_spec;
+
+typedef struct jit_replay_cfg {
+    uint32_t n_steps, n_replays, log_steps, reserved;   /* log_steps: rows of the step log */
+    int64_t v_token0_ns, c0_ns, c_att_ns, c_lin_ns;
+    const jit_replay_spec* specs;  /* n_replays */
+} jit_replay_cfg;
+
+typedef struct jit_replay_result {
+    uint64_t token_goodput, tokens_processed;
+    int64_t sim_end_ns;
+    uint32_t request_goodput, n_done, n_dropped, steps, n_tasks_done, error;
+} jit_replay_result;
+
+typedef struct jit_step_log {
+    int64_t now_ns;
+    uint32_t n_selected, total_tokens, n_candidates, b_star;
+    double bp;
+    uint64_t ids_hash;             /* FNV-1a 64 over the batch ids (u32 LE) in batch order */
+} jit_step_log;
+
+/* Device workspace for a replay call. */
+int jit_replay_workspace_bytes(const jit_config* cfg, const jit_trace* traces, uint32_t n_traces,
+                               const jit_replay_cfg* rc, uint64_t* bytes);
+
+/* Run rc->n_replays replays on h's device / stream.  out: n_replays results.  log (optional):
+ * n_replays * rc->log_steps entries (replay-major).  Uses h's groups, table and config
+ * (token_budget, max_batch, ... ); the pool state of h is untouched. */
+int jit_sched_replay(jit_sched* h, const jit_trace* traces, uint32_t n_traces, const jit_replay_cfg* rc,
+                     void* dev_workspace, uint64_t ws_bytes, jit_replay_result* out, jit_step_log* log);
+
+/* ---------------------------------------------------------------------------------------
+ * Exact sharded step over W ranks (north_star "pool sharded by request id ... NCCL allgather
+ * of candidates followed by a global merge").  Each rank loads its shard (ids
+ * unique across ranks) and calls, in order, with the caller allgathering in between:
+ *   jit_shard_prefix      (a1)-(a7) on the shard; writes the shard's first min(B*_r+1, |P_r|)
+ *                         requests in (key desc, id asc) order as jit_rec1 to d_rec1 (device,
+ *                         cap >= max_batch+1 records); *n_out = count.
+ *   -- allgather the round-1 records of all ranks (unused slots: img = ~0) --
+ *   jit_shard_merge       exact global B*, bp, thr from the union (every rank, identical).
+ *   jit_shard_candidates  the shard's candidates key >= thr as jit_rec2 to d_rec2 (device).
+ *   -- allgather the round-2 records (pad with img = ~0) --
+ *   jit_shard_finish      the window (a9) over the union: the identical batch on every rank;
+ *                         the bookkeeping is applied to this rank's own selected rows;
+ *                         out->rows[i] = local row, or 0xFFFFFFFF for another rank's request.
+ * Correctness: the global prefix restricted to a shard is a shard-local prefix within the
+ * budget, and the global boundary request is in a shard's prefix or is its first misfit. */
+typedef struct jit_rec1 { uint64_t img; uint32_t id, cost; } jit_rec1;
+typedef struct jit_rec2 { uint64_t img; uint32_t id, cost, len, row, rank, reserved; } jit_rec2;
+
+int jit_shard_prefix(jit_sched* h, int64_t now_ns, int64_t v_token_ns, void* d_rec1, uint32_t cap, uint32_t* n_out);
+int jit_shard_merge(jit_sched* h, const void* d_all_rec1, uint32_t n_all);
+int jit_shard_candidates(jit_sched* h, void* d_rec2, uint32_t cap, uint32_t rank, uint32_t* n_out);
+int jit_shard_finish(jit_sched* h, const void* d_all_rec2, uint32_t n_all, uint32_t rank, jit_batch* out);
+
+void jit_sched_destroy(jit_sched* h);
+const char* jit_sched_last_error(const jit_sched* h);
+const char* jit_sched_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* JIT_SCHED_H */

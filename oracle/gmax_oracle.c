@@ -436,6 +436,9 @@ static int gmax_step(const og_config* cfg, const og_group* G, uint32_t n_groups,
                 m = m_set_flags(m, m_flags(m) | FL_EVER);
                 if (m_state(m) == ST_QUEUED || m_state(m) == ST_PREEMPTED) m = m_set_state(m, ST_RUNNING);
                 meta[r] = m;
+                /* saturation edge of the 16-bit counter: a selected request whose
+                 * counter is >= 0xFFFE reads 0xFFFF afterwards */
+                if (a_waited(aux[r]) >= 0xFFFEu) aux[r] = (aux[r] & 0xFFFFu) | (0xFFFFu << 16);
             } else {
                 uint32_t w = a_waited(aux[r]);
                 if (w < 0xFFFFu) ++w;

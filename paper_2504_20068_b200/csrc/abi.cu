@@ -1,0 +1,548 @@
+// abi.cu -- libjitsched.so: the C ABI declared in include/jit_sched.h.
+// Host side: validation, workspace carving, CUDA-graph capture of the step, result readback.
+#include <cstdio>
+#include <cstring>
+#include <cstdarg>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "jit_sched.h"
+#include "common.cuh"
+#include "pool.cuh"
+#include "replay.cuh"
+#include "shard.cuh"
+
+using namespace jit;
+
+static_assert(sizeof(jit_slo_group) == sizeof(Group), "group layout");
+
+struct jit_sched {
+    jit_config cfg{};
+    Cfg c{};
+    Table T{};
+    Group* d_groups = nullptr;
+    uint32_t n_groups = 0;
+    Pool P{};
+    Scratch S{};
+    Ctrl* d_ctrl = nullptr;
+    Ctrl* h_ctrl = nullptr;           // pinned
+    uint32_t* d_stage = nullptr;      // progress staging (4 * capacity)
+    cudaStream_t stream = nullptr;    // caller's stream
+    cudaStream_t cap = nullptr;       // private capture stream
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t begin_node = nullptr;
+    cudaKernelNodeParams begin_params{};
+    void* begin_args[5];
+    int64_t arg_now = 0, arg_v = 0;
+    bool loaded = false, graph_dirty = true, timing = false, debug = false;
+    cudaEvent_t ev[6] = {};
+    cudaGraphNode_t ev_node[5] = {};      // event-record nodes of the timed graph
+    std::vector<cudaEvent_t> slots;       // 5 events per recorded step
+    uint32_t n_slots = 0, slot_used = 0;
+    int n_sm = 148;
+    uint32_t nb_rows = 1, nb_tasks = 0, grid_pass = 1;
+    std::string err;
+};
+
+static int set_err(jit_sched* h, int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (h) h->err = buf;
+    return code;
+}
+
+#define CK(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess) return set_err(h, JIT_ECUDA, "%s: %s (%s:%d)", #call,          \
+                                              cudaGetErrorString(e_), __FILE__, __LINE__);    \
+    } while (0)
+
+// ------------------------------------------------------------------------------------------
+// workspace layout
+// ------------------------------------------------------------------------------------------
+struct Carve {
+    uint64_t off = 0;
+    unsigned char* base = nullptr;
+    template <typename T>
+    T* take(uint64_t count) {
+        off = (off + 255) & ~255ull;
+        T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+        off += sizeof(T) * count;
+        return p;
+    }
+};
+
+static void carve(Carve& cv, const jit_config* cfg, const jit_len_table* tab, Pool& P, Scratch& S, Table& T,
+                  Group*& groups, Ctrl*& ctrl, uint32_t*& stage) {
+    const uint64_t N = ((uint64_t)cfg->capacity + 63) & ~63ull;
+    const uint64_t NT = (uint64_t)cfg->task_capacity + 1;
+    const bool dbg = (cfg->flags & JIT_CFG_DEBUG_ROWS) != 0;
+    P.arr = cv.take<int64_t>(N);
+    P.len_in = cv.take<uint32_t>(N); P.gen = cv.take<uint32_t>(N); P.pre = cv.take<uint32_t>(N);
+    P.lhat = cv.take<uint32_t>(N); P.meta = cv.take<uint32_t>(N); P.aux = cv.take<uint32_t>(N);
+    P.id = cv.take<uint32_t>(N); P.task = cv.take<uint32_t>(N); P.ovr = cv.take<uint32_t>(N);
+    P.img = cv.take<uint64_t>(N); P.cost = cv.take<uint32_t>(N);
+    P.dbg_rate = dbg ? cv.take<double>(N) : nullptr;
+    P.dbg_trem = dbg ? cv.take<int64_t>(N) : nullptr;
+    P.dbg_lhat = dbg ? cv.take<uint32_t>(N) : nullptr;
+    P.call_off = cv.take<uint32_t>(NT + 1); P.t_arr = cv.take<int64_t>(NT); P.t_dl = cv.take<int64_t>(NT);
+    P.cur_stage = cv.take<uint32_t>(NT); P.n_stages = cv.take<uint32_t>(NT);
+    P.pattern = cv.take<uint32_t>(NT * kMaxStages); P.gdone = cv.take<uint64_t>(NT);
+    T.edges = cv.take<uint32_t>(tab->n_bins);
+    T.cum = cv.take<uint32_t>((uint64_t)tab->n_rows * tab->n_bins);
+    groups = cv.take<Group>(256);
+    S.hcnt = cv.take<uint32_t>(4096); S.hcost = cv.take<unsigned long long>(4096);
+    S.bucket_ck = cv.take<u128>(kBucketCap); S.bucket_cost = cv.take<uint32_t>(kBucketCap);
+    uint64_t P2 = 1;                       // bitonic sorts pad |Cd| to a power of two
+    while (P2 < N) P2 <<= 1;
+    S.cand = cv.take<uint32_t>(N); S.sk = cv.take<uint64_t>(P2); S.sv = cv.take<uint32_t>(P2);
+    S.pc = cv.take<unsigned long long>(N + 1); S.pf = cv.take<u128>(N + 1);
+    S.out_ids = cv.take<uint32_t>(cfg->max_batch + 1); S.out_tokens = cv.take<uint32_t>(cfg->max_batch + 1);
+    S.out_rows = cv.take<uint32_t>(cfg->max_batch + 1);
+    S.cand_cap = (uint32_t)N;
+    ctrl = cv.take<Ctrl>(1);
+    stage = cv.take<uint32_t>(4 * N);
+}
+
+static int check_config(jit_sched* h, const jit_config* c, const jit_len_table* t) {
+    if (!c || !t) return set_err(h, JIT_EINVAL, "null config/table");
+    if (c->capacity == 0 || c->capacity > (1u << 30)) return set_err(h, JIT_EINVAL, "capacity out of range");
+    if (c->refine_interval == 0 || c->frame_steps == 0 || c->q_den == 0 || c->q_num == 0 || c->q_num > c->q_den ||
+        c->p_den == 0 || c->p_num == 0 || c->p_num > c->p_den || c->prefill_chunk == 0 ||
+        c->prefill_chunk > c->token_budget || c->max_batch == 0 || c->eps_ns <= 0 || c->waiting_ns < 0)
+        return set_err(h, JIT_EINVAL, "invalid scheduler constants (ConfigError, S:417)");
+    if (t->n_rows == 0 || t->n_rows > 65536 || t->n_bins == 0 || t->l_max == 0 || t->l_max >= 65536)
+        return set_err(h, JIT_EINVAL, "invalid length table shape");
+    return JIT_OK;
+}
+
+extern "C" int jit_sched_workspace_bytes(const jit_config* cfg, const jit_len_table* table, uint64_t* bytes) {
+    int rc = check_config(nullptr, cfg, table);
+    if (rc) return rc;
+    Carve cv;
+    Pool P; Scratch S; Table T; Group* g; Ctrl* c; uint32_t* st;
+    carve(cv, cfg, table, P, S, T, g, c, st);
+    *bytes = cv.off + 256;
+    return JIT_OK;
+}
+
+extern "C" int jit_sched_init(const jit_config* cfg, const jit_slo_group* groups, uint32_t n_groups,
+                              const jit_len_table* table, void* dev_workspace, uint64_t ws_bytes, jit_sched** out) {
+    if (!out) return JIT_EINVAL;
+    *out = nullptr;
+    jit_sched* h = new (std::nothrow) jit_sched();
+    if (!h) return JIT_ECAPACITY;
+    int rc = check_config(h, cfg, table);
+    if (rc) { *out = h; return rc; }
+    if (!groups || n_groups == 0 || n_groups > 256) { *out = h; return set_err(h, JIT_EINVAL, "n_groups must be 1..256"); }
+    // table sanity (host): edges strictly increasing, last = l_max; rows nondecreasing
+    for (uint32_t k = 0; k < table->n_bins; ++k) {
+        if ((k == 0 && table->edges[0] == 0) || (k > 0 && table->edges[k] <= table->edges[k - 1])) {
+            *out = h; return set_err(h, JIT_EINVAL, "table edges not strictly increasing");
+        }
+    }
+    if (table->edges[table->n_bins - 1] != table->l_max) { *out = h; return set_err(h, JIT_EINVAL, "edges[last] != l_max"); }
+    for (uint32_t r = 0; r < table->n_rows; ++r)
+        for (uint32_t k = 1; k < table->n_bins; ++k)
+            if (table->cum[(size_t)r * table->n_bins + k] < table->cum[(size_t)r * table->n_bins + k - 1]) {
+                *out = h; return set_err(h, JIT_EINVAL, "table row %u not monotone", r);
+            }
+    for (uint32_t g = 0; g < n_groups; ++g) {
+        if (groups[g].type > JIT_BE || groups[g].ttft_ns < 0 || groups[g].tbt_ns < 0 || groups[g].e2el_ns < 0 ||
+            groups[g].be_deadline_ns < 0) { *out = h; return set_err(h, JIT_EINVAL, "bad SLO group %u", g); }
+    }
+    uint64_t need = 0;
+    jit_sched_workspace_bytes(cfg, table, &need);
+    if (!dev_workspace || ws_bytes < need) { *out = h; return set_err(h, JIT_ECAPACITY, "workspace too small (%llu < %llu)",
+                                                                       (unsigned long long)ws_bytes, (unsigned long long)need); }
+    h->cfg = *cfg;
+    h->debug = (cfg->flags & JIT_CFG_DEBUG_ROWS) != 0;
+    *out = h;
+    CK(cudaSetDevice(cfg->device));
+    CK(cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, cfg->device));
+    h->stream = (cudaStream_t)cfg->stream;
+    CK(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
+    Carve cv;
+    cv.base = reinterpret_cast<unsigned char*>(((uintptr_t)dev_workspace + 255) & ~(uintptr_t)255);
+    carve(cv, cfg, table, h->P, h->S, h->T, h->d_groups, h->d_ctrl, h->d_stage);
+    h->T.n_rows = table->n_rows; h->T.n_bins = table->n_bins; h->T.l_max = table->l_max;
+    h->n_groups = n_groups;
+    Cfg& c = h->c;
+    c.token_budget = cfg->token_budget; c.max_batch = cfg->max_batch; c.chunk = cfg->prefill_chunk;
+    c.R = cfg->refine_interval; c.frame = cfg->frame_steps; c.qn = cfg->q_num; c.qd = cfg->q_den;
+    c.pn = cfg->p_num; c.pd = cfg->p_den; c.delta = cfg->delta_starve; c.len_key = cfg->len_key;
+    c.appb = cfg->appb_filter; c.eps = cfg->eps_ns; c.waiting = cfg->waiting_ns;
+    CK(cudaMemcpyAsync((void*)h->T.edges, table->edges, 4ull * table->n_bins, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync((void*)h->T.cum, table->cum, 4ull * table->n_rows * table->n_bins, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->d_groups, groups, sizeof(Group) * n_groups, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMallocHost(&h->h_ctrl, sizeof(Ctrl)));
+    for (auto& e : h->ev) CK(cudaEventCreate(&e));
+    CK(cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)((sizeof(u128) + 4) * kBucketCap)));
+    CK(cudaFuncSetAttribute(k_group, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(12 * kGroupSmemSort)));
+    CK(cudaStreamSynchronize(h->stream));
+    return JIT_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// load
+// ------------------------------------------------------------------------------------------
+extern "C" int jit_sched_load(jit_sched* h, const jit_pool* p) {
+    if (!h || !p) return JIT_EINVAL;
+    if (p->n > h->cfg.capacity || p->n_tasks > h->cfg.task_capacity)
+        return set_err(h, JIT_ECAPACITY, "pool of %u rows / %u tasks exceeds capacity", p->n, p->n_tasks);
+    if (p->n_single > p->n) return set_err(h, JIT_EINVAL, "n_single > n");
+    if (p->n_tasks && (!p->call_off || !p->task_arrival_ns || !p->task_deadline_ns || !p->cur_stage ||
+                       !p->n_stages || !p->pattern_ms || !p->goodput_done))
+        return set_err(h, JIT_EINVAL, "missing task arrays");
+    const cudaMemcpyKind kind = p->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    Pool& P = h->P;
+    const uint64_t n = p->n, nt = p->n_tasks;
+    if (n) {
+        CK(cudaMemcpyAsync(P.arr, p->arrival_ns, 8 * n, kind, h->stream));
+        CK(cudaMemcpyAsync(P.len_in, p->input_len, 4 * n, kind, h->stream));
+        CK(cudaMemcpyAsync(P.gen, p->generated, 4 * n, kind, h->stream));
+        CK(cudaMemcpyAsync(P.pre, p->prefilled, 4 * n, kind, h->stream));
+        CK(cudaMemcpyAsync(P.meta, p->meta, 4 * n, kind, h->stream));
+        CK(cudaMemcpyAsync(P.aux, p->aux, 4 * n, kind, h->stream));
+        CK(cudaMemcpyAsync(P.id, p->id, 4 * n, kind, h->stream));
+        CK(cudaMemcpyAsync(P.task, p->task, 4 * n, kind, h->stream));
+        CK(cudaMemcpyAsync(P.ovr, p->override_R, 4 * n, kind, h->stream));
+        CK(cudaMemsetAsync(P.lhat, 0, 4 * n, h->stream));      // invalidate cached bounds
+    }
+    if (nt) {
+        CK(cudaMemcpyAsync(P.call_off, p->call_off, 4 * (nt + 1), kind, h->stream));
+        CK(cudaMemcpyAsync(P.t_arr, p->task_arrival_ns, 8 * nt, kind, h->stream));
+        CK(cudaMemcpyAsync(P.t_dl, p->task_deadline_ns, 8 * nt, kind, h->stream));
+        CK(cudaMemcpyAsync(P.cur_stage, p->cur_stage, 4 * nt, kind, h->stream));
+        CK(cudaMemcpyAsync(P.n_stages, p->n_stages, 4 * nt, kind, h->stream));
+        CK(cudaMemcpyAsync(P.pattern, p->pattern_ms, 4 * nt * kMaxStages, kind, h->stream));
+        CK(cudaMemcpyAsync(P.gdone, p->goodput_done, 8 * nt, kind, h->stream));
+    }
+    const bool same_shape = h->loaded && P.n == p->n && P.n_single == p->n_single && P.n_tasks == p->n_tasks;
+    P.n = p->n; P.n_single = p->n_single; P.n_tasks = p->n_tasks;
+    // validate on the device (also covers device-resident pools)
+    k_begin<<<1, 32, 0, h->stream>>>(h->d_ctrl, h->S.hcnt, h->S.hcost, 0, 1);
+    const uint32_t vb = (uint32_t)std::min<uint64_t>((n + 255) / 256 + 1, (uint64_t)h->n_sm * 8);
+    k_validate<<<vb, 256, 0, h->stream>>>(P, h->d_groups, h->n_groups, h->T.n_rows, h->d_ctrl);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h->h_ctrl, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (h->h_ctrl->error) { h->loaded = false; return set_err(h, JIT_EINVAL, "invalid pool (layout / ranges / groups)"); }
+    // launch geometry
+    const uint32_t nq = (P.n_single + 3) / 4;
+    h->nb_rows = std::max<uint32_t>(1, std::min<uint32_t>((nq + kScoreThreads - 1) / kScoreThreads, (uint32_t)h->n_sm * 8));
+    h->nb_tasks = P.n_tasks ? std::min<uint32_t>((P.n_tasks + 7) / 8, (uint32_t)h->n_sm * 8) : 0;
+    h->grid_pass = std::max<uint32_t>(1, std::min<uint32_t>((P.n + kPassThreads - 1) / kPassThreads, (uint32_t)h->n_sm * 4));
+    if (!same_shape) h->graph_dirty = true;
+    h->loaded = true;
+    return JIT_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// step
+// ------------------------------------------------------------------------------------------
+static void enqueue_chain(jit_sched* h, cudaStream_t s, int64_t now, int64_t v, bool with_events, bool with_begin,
+                          uint32_t first_pass, uint32_t n_passes) {
+    Pool& P = h->P;
+    Scratch& S = h->S;
+    if (with_begin) k_begin<<<4, 1024, 0, s>>>(h->d_ctrl, S.hcnt, S.hcost, now, v);
+    if (with_events) cudaEventRecordWithFlags(h->ev[0], s, cudaEventRecordExternal);
+    if (with_begin) {
+        const uint32_t grid = h->nb_rows + h->nb_tasks;
+        if (h->debug) k_score<true><<<grid, kScoreThreads, 0, s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S.hcnt, S.hcost, h->nb_rows);
+        else k_score<false><<<grid, kScoreThreads, 0, s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S.hcnt, S.hcost, h->nb_rows);
+    }
+    if (with_events) cudaEventRecordWithFlags(h->ev[1], s, cudaEventRecordExternal);
+    for (uint32_t i = 0; i < n_passes; ++i)
+        k_pass<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->c, h->d_ctrl, S.hcnt, S.hcost, first_pass + i);
+    k_compact<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->d_ctrl, S);
+    k_resolve<<<1, 1024, (sizeof(u128) + 4) * kBucketCap, s>>>(h->c, h->d_ctrl, S);
+    if (with_events) cudaEventRecordWithFlags(h->ev[2], s, cudaEventRecordExternal);
+    k_cand<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->d_ctrl, S);
+    if (with_events) cudaEventRecordWithFlags(h->ev[3], s, cudaEventRecordExternal);
+    k_group<<<1, 1024, 12 * kGroupSmemSort, s>>>(P, h->c, h->d_ctrl, S);
+    if (with_events) cudaEventRecordWithFlags(h->ev[4], s, cudaEventRecordExternal);
+    cudaMemcpyAsync(h->h_ctrl, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s);
+}
+
+static int build_graph(jit_sched* h) {
+    if (h->exec) { cudaGraphExecDestroy(h->exec); h->exec = nullptr; }
+    if (h->graph) { cudaGraphDestroy(h->graph); h->graph = nullptr; }
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
+    enqueue_chain(h, h->cap, 0, 1, h->timing, true, 0, 1);
+    CK(cudaStreamEndCapture(h->cap, &g));
+    size_t nn = 0;
+    CK(cudaGraphGetNodes(g, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    CK(cudaGraphGetNodes(g, nodes.data(), &nn));
+    h->begin_node = nullptr;
+    for (auto nd : nodes) {
+        cudaGraphNodeType ty;
+        cudaGraphNodeGetType(nd, &ty);
+        if (ty != cudaGraphNodeTypeKernel) continue;
+        cudaKernelNodeParams kp;
+        cudaGraphKernelNodeGetParams(nd, &kp);
+        if (kp.func == (void*)k_begin) { h->begin_node = nd; h->begin_params = kp; break; }
+    }
+    if (!h->begin_node) { cudaGraphDestroy(g); return set_err(h, JIT_ECUDA, "graph: k_begin node not found"); }
+    for (auto& e : h->ev_node) e = nullptr;
+    for (auto nd : nodes) {
+        cudaGraphNodeType ty;
+        cudaGraphNodeGetType(nd, &ty);
+        if (ty != cudaGraphNodeTypeEventRecord) continue;
+        cudaEvent_t e;
+        cudaGraphEventRecordNodeGetEvent(nd, &e);
+        for (int i = 0; i < 5; ++i) if (e == h->ev[i]) h->ev_node[i] = nd;
+    }
+    h->graph = g;                      // kept alive: begin_node belongs to it
+    CK(cudaGraphInstantiate(&h->exec, g, 0));
+    h->graph_dirty = false;
+    return JIT_OK;
+}
+
+static int launch_step(jit_sched* h, int64_t now, int64_t v) {
+    if (h->graph_dirty) { int rc = build_graph(h); if (rc) return rc; }
+    h->arg_now = now; h->arg_v = v;
+    h->begin_args[0] = &h->d_ctrl; h->begin_args[1] = &h->S.hcnt; h->begin_args[2] = &h->S.hcost;
+    h->begin_args[3] = &h->arg_now; h->begin_args[4] = &h->arg_v;
+    cudaKernelNodeParams kp = h->begin_params;
+    kp.kernelParams = h->begin_args;
+    kp.extra = nullptr;
+    CK(cudaGraphExecKernelNodeSetParams(h->exec, h->begin_node, &kp));
+    if (h->timing && h->n_slots) {
+        // point the graph's event nodes at this step's slot so every timed step keeps its times
+        const uint32_t slot = h->slot_used % h->n_slots;
+        for (int i = 0; i < 5; ++i)
+            if (h->ev_node[i]) CK(cudaGraphExecEventRecordNodeSetEvent(h->exec, h->ev_node[i], h->slots[5 * slot + i]));
+        h->slot_used++;
+    }
+    CK(cudaGraphLaunch(h->exec, h->stream));
+    return JIT_OK;
+}
+
+static int finish_step(jit_sched* h, jit_batch* out) {
+    CK(cudaStreamSynchronize(h->stream));
+    if (h->h_ctrl->status == ST_HIST) {
+        // rare: the boundary bucket stayed large after the graph's passes (heavy key ties);
+        // finish the radix select with the remaining digits outside the graph
+        enqueue_chain(h, h->stream, 0, 0, false, false, 1, kLevels - 1);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(h->stream));
+    }
+    const Ctrl& c = *h->h_ctrl;
+    if (c.status == ST_ERROR || c.error) return set_err(h, JIT_EINVAL, "step: invalid input (error code %u)", c.error);
+    if (out) {
+        out->n_pending = c.n_pending; out->n_dropped = c.n_dropped; out->status = c.status;
+        out->n_selected = 0; out->total_tokens = 0; out->n_candidates = 0; out->b_star = 0; out->bp = 0; out->thr = 0;
+    }
+    if (c.status == ST_EMPTY) return JIT_EMPTY;
+    if (c.status != ST_RESOLVED) return set_err(h, JIT_ECUDA, "step: unexpected status %u", c.status);
+    if (out) {
+        out->n_selected = c.n_selected; out->total_tokens = c.total_tokens; out->n_candidates = c.n_cand;
+        out->b_star = c.b_star; out->bp = c.bp; out->thr = c.thr;
+        if (c.n_selected > out->capacity && (out->ids || out->tokens || out->rows))
+            return set_err(h, JIT_ECAPACITY, "batch capacity %u < %u", out->capacity, c.n_selected);
+        if (out->ids) CK(cudaMemcpyAsync(out->ids, h->S.out_ids, 4ull * c.n_selected, cudaMemcpyDeviceToHost, h->stream));
+        if (out->tokens) CK(cudaMemcpyAsync(out->tokens, h->S.out_tokens, 4ull * c.n_selected, cudaMemcpyDeviceToHost, h->stream));
+        if (out->rows) CK(cudaMemcpyAsync(out->rows, h->S.out_rows, 4ull * c.n_selected, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    }
+    return JIT_OK;
+}
+
+extern "C" int jit_sched_step(jit_sched* h, const jit_step_in* in, jit_batch* out) {
+    if (!h || !in) return JIT_EINVAL;
+    if (!h->loaded) return set_err(h, JIT_ESTATE, "step before load");
+    if (in->v_token_ns <= 0) return set_err(h, JIT_EINVAL, "v_token must be > 0");
+    if (in->n_progress) {
+        if (in->n_progress > h->cfg.capacity) return set_err(h, JIT_ECAPACITY, "too many progress rows");
+        const uint64_t m = in->n_progress, N = ((uint64_t)h->cfg.capacity + 63) & ~63ull;
+        CK(cudaMemcpyAsync(h->d_stage, in->prog_row, 4 * m, cudaMemcpyHostToDevice, h->stream));
+        CK(cudaMemcpyAsync(h->d_stage + N, in->prog_generated, 4 * m, cudaMemcpyHostToDevice, h->stream));
+        CK(cudaMemcpyAsync(h->d_stage + 2 * N, in->prog_prefilled, 4 * m, cudaMemcpyHostToDevice, h->stream));
+        CK(cudaMemcpyAsync(h->d_stage + 3 * N, in->prog_state, 4 * m, cudaMemcpyHostToDevice, h->stream));
+        k_progress<<<(uint32_t)((m + 255) / 256), 256, 0, h->stream>>>(h->P, h->d_stage, h->d_stage + N, h->d_stage + 2 * N,
+                                                                     h->d_stage + 3 * N, (uint32_t)m);
+        CK(cudaGetLastError());
+    }
+    int rc = launch_step(h, in->now_ns, in->v_token_ns);
+    if (rc) return rc;
+    return finish_step(h, out);
+}
+
+extern "C" int jit_sched_step_async(jit_sched* h, int64_t now_ns, int64_t v_token_ns) {
+    if (!h) return JIT_EINVAL;
+    if (!h->loaded) return set_err(h, JIT_ESTATE, "step before load");
+    if (v_token_ns <= 0) return set_err(h, JIT_EINVAL, "v_token must be > 0");
+    return launch_step(h, now_ns, v_token_ns);
+}
+
+extern "C" int jit_sched_fetch_batch(jit_sched* h, jit_batch* out) {
+    if (!h) return JIT_EINVAL;
+    return finish_step(h, out);
+}
+
+extern "C" int jit_sched_read_rows(jit_sched* h, double* key, double* rate, int64_t* t_rem, uint32_t* lhat,
+                                   uint32_t* cost, uint32_t* pending, uint32_t* meta, uint32_t* aux) {
+    if (!h) return JIT_EINVAL;
+    if (!h->loaded) return set_err(h, JIT_ESTATE, "read_rows before load");
+    const uint64_t n = h->P.n;
+    if ((rate || t_rem || lhat) && !h->debug) return set_err(h, JIT_ESTATE, "rate/t_rem/lhat need JIT_CFG_DEBUG_ROWS");
+    CK(cudaStreamSynchronize(h->stream));
+    std::vector<uint64_t> img;
+    if (key || pending) {
+        img.resize(n);
+        CK(cudaMemcpy(img.data(), h->P.img, 8 * n, cudaMemcpyDeviceToHost));
+        for (uint64_t r = 0; r < n; ++r) {
+            if (key) { double d; uint64_t b = img[r]; memcpy(&d, &b, 8); key[r] = b == kNone ? -1.0 : d; }
+            if (pending) pending[r] = img[r] != kNone;
+        }
+    }
+    if (rate) CK(cudaMemcpy(rate, h->P.dbg_rate, 8 * n, cudaMemcpyDeviceToHost));
+    if (t_rem) CK(cudaMemcpy(t_rem, h->P.dbg_trem, 8 * n, cudaMemcpyDeviceToHost));
+    if (lhat) CK(cudaMemcpy(lhat, h->P.dbg_lhat, 4 * n, cudaMemcpyDeviceToHost));
+    if (cost) CK(cudaMemcpy(cost, h->P.cost, 4 * n, cudaMemcpyDeviceToHost));
+    if (meta) {
+        CK(cudaMemcpy(meta, h->P.meta, 4 * n, cudaMemcpyDeviceToHost));
+        for (uint64_t r = 0; r < n; ++r) meta[r] &= 0xFFFFu;       // drop the internal epoch bits
+    }
+    if (aux) CK(cudaMemcpy(aux, h->P.aux, 4 * n, cudaMemcpyDeviceToHost));
+    return JIT_OK;
+}
+
+extern "C" int jit_sched_kernel_times(jit_sched* h, int enable, float* ms_out, uint32_t n_out) {
+    // enable > 0: record per-kernel events for up to `enable` steps (ring of event slots);
+    // enable = 0: off; enable < 0: leave as is.  ms_out gets the AVERAGE over the recorded
+    // steps of [k_score, radix select (passes+compact+resolve), k_cand, k_group, whole chain].
+    if (!h) return JIT_EINVAL;
+    if (enable >= 0) {
+        CK(cudaStreamSynchronize(h->stream));
+        for (auto e : h->slots) cudaEventDestroy(e);
+        h->slots.clear(); h->n_slots = 0; h->slot_used = 0;
+        if (enable > 0) {
+            h->slots.resize(5ull * (uint32_t)enable);
+            for (auto& e : h->slots) CK(cudaEventCreate(&e));
+            h->n_slots = (uint32_t)enable;
+        }
+        if ((enable > 0) != h->timing) { h->timing = enable > 0; h->graph_dirty = true; }
+    }
+    if (ms_out && n_out) {
+        if (!h->timing || !h->slot_used) return set_err(h, JIT_ESTATE, "kernel timing not enabled / no step recorded");
+        CK(cudaStreamSynchronize(h->stream));
+        double acc[5] = {0, 0, 0, 0, 0};
+        const uint32_t ns = std::min(h->slot_used, h->n_slots);
+        for (uint32_t k = 0; k < ns; ++k) {
+            cudaEvent_t* e = &h->slots[5 * k];
+            float t;
+            CK(cudaEventElapsedTime(&t, e[0], e[1])); acc[0] += t;   // k_score
+            CK(cudaEventElapsedTime(&t, e[1], e[2])); acc[1] += t;   // radix select passes + resolve
+            CK(cudaEventElapsedTime(&t, e[2], e[3])); acc[2] += t;   // candidates
+            CK(cudaEventElapsedTime(&t, e[3], e[4])); acc[3] += t;   // group
+            CK(cudaEventElapsedTime(&t, e[0], e[4])); acc[4] += t;   // total
+        }
+        for (uint32_t i = 0; i < n_out && i < 5; ++i) ms_out[i] = (float)(acc[i] / ns);
+    }
+    return JIT_OK;
+}
+
+extern "C" void jit_sched_destroy(jit_sched* h) {
+    if (!h) return;
+    if (h->exec) cudaGraphExecDestroy(h->exec);
+    if (h->graph) cudaGraphDestroy(h->graph);
+    if (h->cap) cudaStreamDestroy(h->cap);
+    if (h->h_ctrl) cudaFreeHost(h->h_ctrl);
+    for (auto e : h->ev) if (e) cudaEventDestroy(e);
+    for (auto e : h->slots) cudaEventDestroy(e);
+    delete h;
+}
+
+extern "C" const char* jit_sched_last_error(const jit_sched* h) { return h ? h->err.c_str() : "null handle"; }
+extern "C" const char* jit_sched_version(void) { return "jitsched 0.1 sm_100a"; }
+
+// ------------------------------------------------------------------------------------------
+// replay
+// ------------------------------------------------------------------------------------------
+#include "replay_host.inc"
+
+// ------------------------------------------------------------------------------------------
+// sharded step (shard.cuh): the caller runs the two allgathers between these calls
+// ------------------------------------------------------------------------------------------
+static_assert(sizeof(Rec1) == sizeof(jit_rec1) && sizeof(Rec2) == sizeof(jit_rec2), "record layout");
+constexpr uint32_t kMergeSmem = 8192;
+
+extern "C" int jit_shard_prefix(jit_sched* h, int64_t now_ns, int64_t v_token_ns, void* d_rec1, uint32_t cap,
+                                uint32_t* n_out) {
+    if (!h || !d_rec1 || !n_out) return JIT_EINVAL;
+    if (!h->loaded) return set_err(h, JIT_ESTATE, "shard_prefix before load");
+    if (v_token_ns <= 0) return set_err(h, JIT_EINVAL, "v_token must be > 0");
+    if (cap < h->cfg.max_batch + 1) return set_err(h, JIT_ECAPACITY, "round-1 buffer needs max_batch+1 records");
+    cudaStream_t s = h->stream;
+    Pool& P = h->P;
+    Scratch& S = h->S;
+    k_begin<<<4, 1024, 0, s>>>(h->d_ctrl, S.hcnt, S.hcost, now_ns, v_token_ns);
+    const uint32_t grid = h->nb_rows + h->nb_tasks;
+    if (h->debug) k_score<true><<<grid, kScoreThreads, 0, s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S.hcnt, S.hcost, h->nb_rows);
+    else k_score<false><<<grid, kScoreThreads, 0, s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S.hcnt, S.hcost, h->nb_rows);
+    for (uint32_t i = 0; i < kLevels - 1; ++i)
+        k_pass<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->c, h->d_ctrl, S.hcnt, S.hcost, i);
+    k_compact<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->d_ctrl, S);
+    k_resolve<<<1, 1024, (sizeof(u128) + 4) * kBucketCap, s>>>(h->c, h->d_ctrl, S);
+    k_export1<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->d_ctrl, S, (Rec1*)d_rec1, cap);
+    k_export1_tail<<<1, 1024, 0, s>>>(h->d_ctrl, S, (Rec1*)d_rec1, cap);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h->h_ctrl, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const Ctrl& c = *h->h_ctrl;
+    if (c.status == ST_ERROR || c.error || c.cand_overflow) return set_err(h, JIT_EINVAL, "shard_prefix failed (%u)", c.error);
+    *n_out = c.status == ST_RESOLVED ? c.n_cand : 0;
+    return c.status == ST_EMPTY ? JIT_EMPTY : JIT_OK;
+}
+
+extern "C" int jit_shard_merge(jit_sched* h, const void* d_all_rec1, uint32_t n_all) {
+    if (!h || (!d_all_rec1 && n_all)) return JIT_EINVAL;
+    uint64_t n2 = 1;
+    while (n2 < n_all) n2 <<= 1;
+    const uint64_t N = ((uint64_t)h->cfg.capacity + 63) & ~63ull;
+    if (n2 > kMergeSmem && n2 > N) return set_err(h, JIT_ECAPACITY, "merge of %u records exceeds the workspace", n_all);
+    const uint32_t smem = (uint32_t)((sizeof(u128) + 4) * kMergeSmem);
+    CK(cudaFuncSetAttribute(k_merge1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_merge1<<<1, 1024, smem, h->stream>>>(h->c, h->d_ctrl, (const Rec1*)d_all_rec1, n_all, h->S.pf, h->S.sv, kMergeSmem);
+    CK(cudaGetLastError());
+    return JIT_OK;
+}
+
+extern "C" int jit_shard_candidates(jit_sched* h, void* d_rec2, uint32_t cap, uint32_t rank, uint32_t* n_out) {
+    if (!h || !n_out) return JIT_EINVAL;
+    cudaStream_t s = h->stream;
+    k_cand<<<h->grid_pass, kPassThreads, 0, s>>>(h->P, h->d_ctrl, h->S);
+    k_export2<<<h->grid_pass, 256, 0, s>>>(h->P, h->c, h->d_ctrl, h->S, (Rec2*)d_rec2, cap, rank);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h->h_ctrl, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const Ctrl& c = *h->h_ctrl;
+    if (c.status == ST_EMPTY) { *n_out = 0; return JIT_EMPTY; }
+    if (c.status != ST_RESOLVED || c.error) return set_err(h, JIT_EINVAL, "shard_candidates: bad state %u", c.status);
+    if (c.cand_overflow || c.n_cand > cap) return set_err(h, JIT_ECAPACITY, "round-2 buffer too small (%u > %u)", c.n_cand, cap);
+    *n_out = c.n_cand;
+    return JIT_OK;
+}
+
+extern "C" int jit_shard_finish(jit_sched* h, const void* d_all_rec2, uint32_t n_all, uint32_t rank, jit_batch* out) {
+    if (!h) return JIT_EINVAL;
+    cudaStream_t s = h->stream;
+    uint64_t n2 = 1;
+    while (n2 < n_all) n2 <<= 1;
+    const uint64_t N = ((uint64_t)h->cfg.capacity + 63) & ~63ull;
+    if (n2 > kGroupSmemSort && n_all > N) return set_err(h, JIT_ECAPACITY, "window over %u records exceeds the workspace", n_all);
+    if (h->h_ctrl->status == ST_EMPTY) { if (out) { out->n_selected = 0; out->status = ST_EMPTY; } return JIT_EMPTY; }
+    k_group_rec<<<1, 1024, 12 * kGroupSmemSort, s>>>(h->P, h->c, h->d_ctrl, h->S, (const Rec2*)d_all_rec2, n_all, rank);
+    CK(cudaGetLastError());
+    return finish_step(h, out);
+}

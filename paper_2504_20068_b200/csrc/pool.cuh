@@ -1,0 +1,787 @@
+// pool.cuh -- the GMAX step over a request pool resident in HBM (sm_100a).
+//
+// Kernel chain of one step (captured once into a CUDA graph):
+//   k_begin    zero the control block / histograms, install (now, v_token)
+//   k_score    (a1)-(a6) for standalone rows (4 rows per thread, 128-bit SoA loads) and the
+//              compound pass (a4, one warp per task); writes the 8-B sort image of the key,
+//              the token cost and steps_waited+1; fuses the level-0 cost-weighted histogram
+//              of the key (exponent digit); the last CTA resolves level 0.
+//   k_pass     one more 12-bit digit of the cost-weighted radix select (only if the boundary
+//              bucket is still larger than kBucketCap); last CTA resolves it.
+//   k_compact  gathers the boundary bucket (composite key, cost) + the smallest key above it
+//   k_resolve  one CTA: sorts the bucket, block-scans costs -> exact B*, bp, thr (a7, a8)
+//   k_cand     compacts Cd = {key >= thr} (warp ballots)
+//   k_group    one CTA: sorts Cd by (len, id), u64/u128 prefix sums, sliding windows within
+//              the token budget, first argmax (a9); writes the batch and the bookkeeping.
+#pragma once
+#include "common.cuh"
+
+namespace jit {
+
+constexpr uint32_t kBucketCap = 4096;
+constexpr uint32_t kGroupSmemSort = 8192;     // |Cd| sorted in shared memory up to this size
+constexpr uint32_t kScoreThreads = 256;
+constexpr uint32_t kPassThreads = 512;
+
+enum : uint32_t { ST_RUN = 0, ST_HIST = 1, ST_COMPACT = 2, ST_RESOLVED = 3, ST_EMPTY = 4, ST_ERROR = 5 };
+
+struct Pool {
+    int64_t* arr;
+    uint32_t *len_in, *gen, *pre, *lhat, *meta, *aux, *id, *task, *ovr;
+    uint64_t* img;          // sort image = bits of the fp64 key; kNone when not pending
+    uint32_t* cost;         // token cost of the row this step (0 when not pending)
+    double* dbg_rate;       // optional debug outputs
+    int64_t* dbg_trem;
+    uint32_t* dbg_lhat;
+    uint32_t n, n_single, n_tasks, pad;
+    uint32_t* call_off;
+    int64_t *t_arr, *t_dl;
+    uint32_t *cur_stage, *n_stages, *pattern;
+    uint64_t* gdone;
+};
+
+struct alignas(16) Ctrl {
+    u128 prefix;                     // digits resolved so far (top bits of the composite key)
+    int64_t now, v;
+    unsigned long long min_img;      // smallest key image over pending rows
+    unsigned long long pred_min_img; // smallest key image above the final bucket
+    unsigned long long before_cost;  // cost of the rows strictly above the current bucket
+    unsigned long long thr_img;
+    double bp, thr;
+    uint32_t n_pending, n_dropped, error, status;
+    uint32_t level, bucket_count, bucket_fill, before_count;
+    uint32_t b_star, n_cand, n_selected, total_tokens;
+    uint32_t done[16];
+    uint32_t i_best, j_best, cand_overflow, exp_fill;
+};
+
+struct Scratch {
+    uint32_t* hcnt;          // 4096
+    unsigned long long* hcost;  // 4096
+    u128* bucket_ck;         // kBucketCap
+    uint32_t* bucket_cost;   // kBucketCap
+    uint32_t* cand;          // candidate rows (capacity)
+    uint64_t* sk;            // global sort keys (capacity)   -- large-|Cd| path
+    uint32_t* sv;            // global sort values
+    unsigned long long* pc;  // prefix costs (capacity+1)
+    u128* pf;                // prefix fixed-point keys (capacity+1)
+    uint32_t* out_ids;       // max_batch
+    uint32_t* out_tokens;
+    uint32_t* out_rows;
+    uint32_t cand_cap, pad;
+};
+
+__device__ __forceinline__ bool is_last_block(uint32_t* counter) {
+    __shared__ bool s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        uint32_t prev = atomicAdd(counter, 1u);
+        s_last = (prev == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (s_last) __threadfence();
+    return s_last;
+}
+
+// warp-aggregated shared-memory histogram update (all 32 lanes must call convergently)
+__device__ __forceinline__ void warp_hist_add(uint32_t* s_cnt, uint32_t* s_cost, bool valid, uint32_t bin,
+                                              uint32_t cost) {
+    const int lane = threadIdx.x & 31;
+    unsigned todo = __ballot_sync(0xffffffffu, valid);
+    while (todo) {
+        const int leader = __ffs(todo) - 1;
+        const uint32_t b = __shfl_sync(0xffffffffu, bin, leader);
+        const bool mine = valid && bin == b;
+        const unsigned m = __ballot_sync(0xffffffffu, mine);
+        const uint32_t c = __reduce_add_sync(0xffffffffu, mine ? cost : 0u);
+        if (lane == leader) {
+            atomicAdd(&s_cnt[b], (uint32_t)__popc(m));
+            atomicAdd(&s_cost[b], c);
+        }
+        todo &= ~m;
+    }
+}
+
+// --------------------------------------------------------------------------------------
+// Resolve one radix level from the global histogram (executed by the last CTA of a pass).
+// Bins are in ascending composite-key order = descending key.  The boundary bin is the
+// first whose inclusive cumulative (count, cost), plus what lies above the bucket, exceeds
+// (max_batch, token_budget) -- the (B*+1)-th request of Alg. 1's priority order lies in it.
+// --------------------------------------------------------------------------------------
+__device__ void resolve_level(const Cfg& c, Ctrl* ctrl, uint32_t* hcnt, unsigned long long* hcost, uint32_t L) {
+    __shared__ uint64_t s_scan[32];
+    __shared__ uint32_t s_first;
+    const uint32_t nb = digit_bins(L);
+    const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;
+    const uint32_t b0 = threadIdx.x * per;
+    uint64_t lc = 0, lk = 0;
+    for (uint32_t k = 0; k < per; ++k) {
+        uint32_t b = b0 + k;
+        if (b < nb) { lc += __ldcg(hcnt + b); lk += __ldcg(hcost + b); }
+    }
+    uint64_t tc, tk;
+    uint64_t ec = block_exclusive_scan_u64(lc, s_scan, &tc);
+    uint64_t ek = block_exclusive_scan_u64(lk, s_scan, &tk);
+    if (threadIdx.x == 0) s_first = nb;
+    __syncthreads();
+    const uint64_t bc = ctrl->before_count, bk = ctrl->before_cost;
+    uint64_t cc = ec, ck = ek;
+    uint32_t my_first = nb;
+    uint64_t my_exc = 0, my_exk = 0;
+    for (uint32_t k = 0; k < per; ++k) {
+        uint32_t b = b0 + k;
+        if (b >= nb) break;
+        const uint64_t hc = __ldcg(hcnt + b), hk = __ldcg(hcost + b);
+        if (bc + cc + hc > c.max_batch || bk + ck + hk > c.token_budget) {
+            my_first = b; my_exc = cc; my_exk = ck;
+            atomicMin(&s_first, b);
+            break;
+        }
+        cc += hc; ck += hk;
+    }
+    __syncthreads();
+    const uint32_t first = s_first;
+    if (my_first == first && first < nb) {     // the owner of the boundary bin publishes it
+        if (ctrl->error) {
+            ctrl->status = ST_ERROR;
+        } else if (L == 0 && ctrl->n_pending == 0) {
+            ctrl->status = ST_EMPTY;
+        } else {
+            ctrl->before_count += (uint32_t)my_exc;
+            ctrl->before_cost += my_exk;
+            ctrl->prefix = (L == 0) ? (u128)first : ((ctrl->prefix << 12) | (u128)first);
+            ctrl->bucket_count = __ldcg(hcnt + first);
+            ctrl->level = L + 1;
+            ctrl->status = (ctrl->bucket_count <= kBucketCap) ? ST_COMPACT : ST_HIST;
+        }
+    }
+    if (threadIdx.x == 0 && first == nb) {
+        if (ctrl->error) {
+            ctrl->status = ST_ERROR;
+        } else if (ctrl->n_pending == 0) {
+            ctrl->status = ST_EMPTY;
+        } else if (L == 0) {
+            // every pending request fits: B* = |P| and bp = the minimum key (A15)
+            ctrl->b_star = ctrl->n_pending;
+            const double bp = __longlong_as_double((long long)ctrl->min_img);
+            ctrl->bp = bp;
+            ctrl->thr = __dmul_rn(__ddiv_rn((double)c.pn, (double)c.pd), bp);
+            ctrl->thr_img = (unsigned long long)__double_as_longlong(ctrl->thr);
+            ctrl->status = ST_RESOLVED;
+        } else {
+            ctrl->error = 4; ctrl->status = ST_ERROR;     // a boundary bucket must contain the boundary
+        }
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < 4096; b += blockDim.x) { hcnt[b] = 0; hcost[b] = 0; }
+}
+
+// --------------------------------------------------------------------------------------
+// k_begin
+// --------------------------------------------------------------------------------------
+__global__ void k_begin(Ctrl* ctrl, uint32_t* hcnt, unsigned long long* hcost, int64_t now, int64_t v) {
+    for (uint32_t b = threadIdx.x + blockIdx.x * blockDim.x; b < 4096; b += blockDim.x * gridDim.x) {
+        hcnt[b] = 0; hcost[b] = 0;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        Ctrl z;
+        memset(&z, 0, sizeof(z));
+        z.now = now; z.v = v;
+        z.min_img = kNone; z.pred_min_img = kNone;
+        *ctrl = z;
+    }
+}
+
+// --------------------------------------------------------------------------------------
+// per-row scoring of a standalone request: (a1) admission, (a2) length bound, (a3) t_rem,
+// (a5) key, (a6) cost.  Pure function of the row + config; returns what to write back.
+// --------------------------------------------------------------------------------------
+struct RowRes {
+    uint64_t img;
+    uint32_t cost, meta, lhat, aux;
+    bool pending, dropped, w_meta, w_lhat, err;
+    double rate; int64_t trem; uint32_t lhatc;
+};
+
+template <bool kDebug>
+__device__ __forceinline__ void score_standalone(const Cfg& c, const Table& T, const Group* sg, uint32_t n_groups,
+                                                 const uint32_t* ovr, uint32_t row, int64_t now, int64_t v,
+                                                 int64_t arr, uint32_t L_i, uint32_t g, uint32_t pre,
+                                                 uint32_t lhat, uint32_t meta, uint32_t aux, RowRes& o) {
+    o.img = kNone; o.cost = 0; o.meta = meta; o.lhat = lhat; o.aux = aux;
+    o.pending = o.dropped = o.w_meta = o.w_lhat = o.err = false;
+    if (kDebug) { o.rate = 0.0; o.trem = 0; o.lhatc = 0; }
+    if (arr > now) return;
+    const uint32_t st = m_state(meta), fl = m_flags(meta);
+    if (st == kQueued && !(fl & kEver) && !(fl & kCompound) && now - arr > c.waiting) {   // (a1) P:545
+        o.meta = m_with_state(meta, kDropped); o.w_meta = true; o.dropped = true;
+        return;
+    }
+    if (st > kPreempted) return;
+    o.pending = true;
+    const uint32_t gi = m_group(meta);
+    const uint32_t drow = aux & 0xFFFFu;
+    if (gi >= n_groups || drow >= T.n_rows || (fl & kCompound)) { o.err = true; return; }
+    // (a2) conservative remaining length, refreshed every R tokens; cached per epoch
+    const uint32_t ep = g / c.R;
+    if (lhat == 0 || ep >= 65536u || m_epoch(meta) != ep) {
+        lhat = cond_quantile(T, drow, ep * c.R, c.qn, c.qd);
+        o.lhat = lhat; o.w_lhat = true;
+        if (ep < 65536u) { o.meta = (meta & 0xFFFFu) | (ep << 16); o.w_meta = true; }
+    }
+    const uint32_t Lh = lhat > g + 1 ? lhat : g + 1;
+    const uint64_t len_rem = (uint64_t)(Lh - g);
+    o.cost = token_cost(L_i, pre, c.chunk);
+    const Group G = sg[gi];
+    const uint64_t t_gen = len_rem * (uint64_t)v;
+    int64_t trem;
+    uint64_t Gk;
+    if (G.type == kLAT) {                                       // A9, A11
+        trem = arr + G.ttft_ns + (int64_t)(Lh - 1) * G.tbt_ns - now;
+        Gk = (uint64_t)G.w_out * Lh;
+    } else if (G.type == kDDL) {
+        trem = arr + G.e2el_ns - now;
+        Gk = (uint64_t)G.w_in * L_i + (uint64_t)G.w_out * Lh;
+    } else if (G.type == kBE) {
+        trem = arr + G.be_deadline_ns - now;
+        Gk = 0;
+    } else { o.err = true; return; }
+    if (m_flags(meta) & kOverride) Gk = __ldg(ovr + row);
+    if (trem <= 0) Gk = 0;                                      // A22
+    if (c.appb && t_gen > (uint64_t)(trem > 0 ? trem : 0)) Gk = 0;
+    const uint64_t Gp = Gk + (uint64_t)c.delta * ((aux >> 16) / c.frame);
+    double key;
+    if (!make_key(Gp, t_gen, c.eps, &key)) { o.err = true; return; }
+    o.img = (uint64_t)__double_as_longlong(key);
+    if ((aux >> 16) < 0xFFFFu) o.aux = aux + (1u << 16);       // steps_waited+1; undone if selected
+    if (kDebug) { o.rate = make_rate(len_rem, trem); o.trem = trem; o.lhatc = Lh; }
+}
+
+// --------------------------------------------------------------------------------------
+// k_score
+// --------------------------------------------------------------------------------------
+template <bool kDebug>
+__global__ void __launch_bounds__(kScoreThreads) k_score(Pool P, Table T, const Group* groups, uint32_t n_groups,
+                                                         Cfg c, Ctrl* ctrl, uint32_t* hcnt,
+                                                         unsigned long long* hcost, uint32_t nb_rows) {
+    __shared__ uint32_t s_cnt[2048], s_cost[2048];
+    __shared__ Group s_g[256];
+    __shared__ unsigned long long s_min;
+    __shared__ uint32_t s_pend, s_drop, s_err;
+    for (uint32_t b = threadIdx.x; b < 2048; b += blockDim.x) { s_cnt[b] = 0; s_cost[b] = 0; }
+    for (uint32_t gi = threadIdx.x; gi < n_groups; gi += blockDim.x) s_g[gi] = groups[gi];
+    if (threadIdx.x == 0) { s_min = kNone; s_pend = 0; s_drop = 0; s_err = 0; }
+    __syncthreads();
+    const int64_t now = ctrl->now, v = ctrl->v;
+    const int lane = threadIdx.x & 31;
+    uint32_t my_pend = 0, my_drop = 0, my_err = 0;
+    uint64_t my_min = kNone;
+
+    if (blockIdx.x < nb_rows) {
+        // ---------------- standalone rows: 4 consecutive rows per thread --------------------
+        const uint32_t nq = (P.n_single + 3) >> 2;
+        const uint32_t stride = nb_rows * blockDim.x;
+        for (uint32_t wq = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); wq < nq; wq += stride) {
+            const uint32_t q = wq + lane;
+            const bool act = q < nq;
+            const uint32_t r0 = q * 4;
+            RowRes o[4];
+            if (act && r0 + 4 <= P.n_single) {
+                const longlong2 a01 = reinterpret_cast<const longlong2*>(P.arr)[2 * q];
+                const longlong2 a23 = reinterpret_cast<const longlong2*>(P.arr)[2 * q + 1];
+                const uint4 li = reinterpret_cast<const uint4*>(P.len_in)[q];
+                const uint4 gg = reinterpret_cast<const uint4*>(P.gen)[q];
+                const uint4 pr = reinterpret_cast<const uint4*>(P.pre)[q];
+                const uint4 lh = reinterpret_cast<const uint4*>(P.lhat)[q];
+                const uint4 me = reinterpret_cast<const uint4*>(P.meta)[q];
+                const uint4 ax = reinterpret_cast<const uint4*>(P.aux)[q];
+                score_standalone<kDebug>(c, T, s_g, n_groups, P.ovr, r0 + 0, now, v, a01.x, li.x, gg.x, pr.x, lh.x, me.x, ax.x, o[0]);
+                score_standalone<kDebug>(c, T, s_g, n_groups, P.ovr, r0 + 1, now, v, a01.y, li.y, gg.y, pr.y, lh.y, me.y, ax.y, o[1]);
+                score_standalone<kDebug>(c, T, s_g, n_groups, P.ovr, r0 + 2, now, v, a23.x, li.z, gg.z, pr.z, lh.z, me.z, ax.z, o[2]);
+                score_standalone<kDebug>(c, T, s_g, n_groups, P.ovr, r0 + 3, now, v, a23.y, li.w, gg.w, pr.w, lh.w, me.w, ax.w, o[3]);
+                reinterpret_cast<ulonglong2*>(P.img)[2 * q] = make_ulonglong2(o[0].img, o[1].img);
+                reinterpret_cast<ulonglong2*>(P.img)[2 * q + 1] = make_ulonglong2(o[2].img, o[3].img);
+                reinterpret_cast<uint4*>(P.cost)[q] = make_uint4(o[0].cost, o[1].cost, o[2].cost, o[3].cost);
+                reinterpret_cast<uint4*>(P.aux)[q] = make_uint4(o[0].aux, o[1].aux, o[2].aux, o[3].aux);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (o[k].w_meta) P.meta[r0 + k] = o[k].meta;
+                    if (o[k].w_lhat) P.lhat[r0 + k] = o[k].lhat;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t r = r0 + k;
+                    if (act && r < P.n_single) {
+                        score_standalone<kDebug>(c, T, s_g, n_groups, P.ovr, r, now, v, P.arr[r], P.len_in[r], P.gen[r],
+                                                 P.pre[r], P.lhat[r], P.meta[r], P.aux[r], o[k]);
+                        P.img[r] = o[k].img; P.cost[r] = o[k].cost; P.aux[r] = o[k].aux;
+                        if (o[k].w_meta) P.meta[r] = o[k].meta;
+                        if (o[k].w_lhat) P.lhat[r] = o[k].lhat;
+                    } else {
+                        o[k].img = kNone; o[k].cost = 0; o[k].pending = o[k].dropped = o[k].err = false;
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t r = r0 + k;
+                if (kDebug && act && r < P.n_single) {
+                    P.dbg_rate[r] = o[k].pending ? o[k].rate : 0.0;
+                    P.dbg_trem[r] = o[k].pending ? o[k].trem : 0;
+                    P.dbg_lhat[r] = o[k].pending ? o[k].lhatc : 0;
+                }
+                const bool valid = act && o[k].img != kNone;
+                my_pend += valid; my_drop += (act && o[k].dropped); my_err |= (act && o[k].err);
+                if (valid && o[k].img < my_min) my_min = o[k].img;
+                const uint32_t bin = (uint32_t)(make_ck(o[k].img, 0) >> digit_shift(0)) & 2047u;
+                warp_hist_add(s_cnt, s_cost, valid, bin, o[k].cost);
+            }
+        }
+    } else {
+        // ---------------- (a4) compound tasks: one warp per task ---------------------------
+        const uint32_t wpb = blockDim.x >> 5;
+        const uint32_t w0 = (blockIdx.x - nb_rows) * wpb + (threadIdx.x >> 5);
+        const uint32_t nw = (gridDim.x - nb_rows) * wpb;
+        for (uint32_t t = w0; t < P.n_tasks; t += nw) {
+            const uint32_t b = P.call_off[t], e = P.call_off[t + 1];
+            uint64_t Tsum = 0, Gcur = 0;
+            uint32_t cnt = 0;
+            for (uint32_t base = b; base < e; base += 32) {          // pass 1: bounds and sums
+                const uint32_t r = base + lane;
+                if (r >= e) continue;
+                const uint32_t meta = P.meta[r];
+                const uint32_t st = m_state(meta);
+                if (P.arr[r] > now || st > kPreempted) continue;
+                const uint32_t g = P.gen[r], aux = P.aux[r];
+                const uint32_t gi = m_group(meta), drow = aux & 0xFFFFu;
+                if (gi >= n_groups || s_g[gi].type != kCMP || !(m_flags(meta) & kCompound) || drow >= T.n_rows ||
+                    P.task[r] != t) { my_err = 1; continue; }
+                uint32_t lhat = P.lhat[r];
+                const uint32_t ep = g / c.R;
+                if (lhat == 0 || ep >= 65536u || m_epoch(meta) != ep) {
+                    lhat = cond_quantile(T, drow, ep * c.R, c.qn, c.qd);
+                    P.lhat[r] = lhat;
+                    if (ep < 65536u) P.meta[r] = (meta & 0xFFFFu) | (ep << 16);
+                }
+                const uint32_t Lh = lhat > g + 1 ? lhat : g + 1;
+                Tsum += (uint64_t)(Lh - g);
+                Gcur += (uint64_t)s_g[gi].w_in * P.len_in[r] + (uint64_t)s_g[gi].w_out * Lh;
+                ++cnt;
+            }
+            Tsum = warp_sum(Tsum); Gcur = warp_sum(Gcur); cnt = warp_sum(cnt);
+            // task-level quantities: phi(s) sub-deadline, final deadline, JIT rate
+            const int64_t a_c = P.t_arr[t], D = P.t_dl[t];
+            const uint32_t s = P.cur_stage[t], S = P.n_stages[t];
+            uint64_t le = 0, tot = 0;
+            for (uint32_t u = 0; u < S && u < kMaxStages; ++u) {
+                const uint64_t ns = (uint64_t)P.pattern[t * kMaxStages + u] * 1000000ull;
+                tot += ns; if (u <= s) le += ns;
+            }
+            if (cnt && (tot == 0 || S == 0 || S > kMaxStages || s >= S)) my_err = 1;
+            const int64_t Ds = tot ? (int64_t)((u128)(uint64_t)D * le / tot) : 0;
+            const int64_t trem = a_c + Ds - now;
+            uint64_t Gt = P.gdone[t] + Gcur;
+            if (a_c + D <= now) Gt = 0;
+            const uint64_t t_gen = Tsum * (uint64_t)v;
+            if (c.appb && t_gen > (uint64_t)(trem > 0 ? trem : 0)) Gt = 0;
+            for (uint32_t base = b; base < e; base += 32) {          // pass 2: per-call keys
+                const uint32_t r = base + lane;
+                const bool inr = r < e;
+                bool pend = false;
+                uint64_t img = kNone;
+                uint32_t cost = 0;
+                if (inr) {
+                    const uint32_t meta = P.meta[r], aux = P.aux[r];
+                    pend = P.arr[r] <= now && m_state(meta) <= kPreempted;
+                    if (pend) {
+                        const uint64_t Gp = Gt + (uint64_t)c.delta * ((aux >> 16) / c.frame);
+                        double key;
+                        if (!make_key(Gp, t_gen, c.eps, &key)) my_err = 1;
+                        img = (uint64_t)__double_as_longlong(key);
+                        cost = token_cost(P.len_in[r], P.pre[r], c.chunk);
+                        if ((aux >> 16) < 0xFFFFu) P.aux[r] = aux + (1u << 16);
+                        if (kDebug) {
+                            const uint32_t lhat = P.lhat[r], g = P.gen[r];
+                            P.dbg_lhat[r] = lhat > g + 1 ? lhat : g + 1;
+                            P.dbg_rate[r] = make_rate(Tsum, trem);
+                            P.dbg_trem[r] = trem;
+                        }
+                    } else if (kDebug) {
+                        P.dbg_lhat[r] = 0; P.dbg_rate[r] = 0.0; P.dbg_trem[r] = 0;
+                    }
+                    P.img[r] = img; P.cost[r] = cost;
+                }
+                const bool valid = inr && pend;
+                my_pend += valid;
+                if (valid && img < my_min) my_min = img;
+                const uint32_t bin = (uint32_t)(make_ck(img, 0) >> digit_shift(0)) & 2047u;
+                warp_hist_add(s_cnt, s_cost, valid, bin, cost);
+            }
+        }
+    }
+    // ---- block reductions, histogram flush
+    my_pend = warp_sum(my_pend); my_drop = warp_sum(my_drop); my_err = __reduce_or_sync(0xffffffffu, my_err);
+    my_min = warp_min_u64(my_min);
+    if (lane == 0) {
+        atomicAdd(&s_pend, my_pend); atomicAdd(&s_drop, my_drop); atomicOr(&s_err, my_err);
+        atomicMin(&s_min, (unsigned long long)my_min);
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < 2048; b += blockDim.x) {
+        if (s_cnt[b]) { atomicAdd(hcnt + b, s_cnt[b]); atomicAdd(hcost + b, (unsigned long long)s_cost[b]); }
+    }
+    if (threadIdx.x == 0) {
+        if (s_pend) atomicAdd(&ctrl->n_pending, s_pend);
+        if (s_drop) atomicAdd(&ctrl->n_dropped, s_drop);
+        if (s_err) atomicOr(&ctrl->error, 1u);
+        if (s_min != kNone) atomicMin(&ctrl->min_img, s_min);
+    }
+    if (is_last_block(&ctrl->done[0])) resolve_level(c, ctrl, hcnt, hcost, 0);
+}
+
+// --------------------------------------------------------------------------------------
+// k_pass: one further digit of the cost-weighted radix select (only while status == HIST)
+// --------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kPassThreads) k_pass(Pool P, Cfg c, Ctrl* ctrl, uint32_t* hcnt,
+                                                       unsigned long long* hcost, uint32_t pass_idx) {
+    if (ctrl->status != ST_HIST) return;
+    __shared__ uint32_t s_cnt[4096], s_cost[4096];
+    for (uint32_t b = threadIdx.x; b < 4096; b += blockDim.x) { s_cnt[b] = 0; s_cost[b] = 0; }
+    __syncthreads();
+    const uint32_t L = ctrl->level;
+    const u128 prefix = ctrl->prefix;
+    const uint32_t sh_prev = digit_shift(L - 1), sh = digit_shift(L);
+    const bool need_id = sh < 32;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    for (uint32_t wr = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); wr < P.n; wr += stride) {
+        const uint32_t r = wr + lane;
+        bool valid = false;
+        uint32_t bin = 0, cost = 0;
+        if (r < P.n) {
+            const uint64_t img = P.img[r];
+            if (img != kNone) {
+                const u128 ck = make_ck(img, need_id ? P.id[r] : 0u);
+                if ((ck >> sh_prev) == prefix) {
+                    valid = true;
+                    bin = (uint32_t)(ck >> sh) & 4095u;
+                    cost = P.cost[r];
+                }
+            }
+        }
+        warp_hist_add(s_cnt, s_cost, valid, bin, cost);
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < 4096; b += blockDim.x)
+        if (s_cnt[b]) { atomicAdd(hcnt + b, s_cnt[b]); atomicAdd(hcost + b, (unsigned long long)s_cost[b]); }
+    if (is_last_block(&ctrl->done[1 + (pass_idx & 7)])) resolve_level(c, ctrl, hcnt, hcost, L);
+}
+
+// --------------------------------------------------------------------------------------
+// k_compact: gather the final bucket and the smallest key image above it
+// --------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kPassThreads) k_compact(Pool P, Ctrl* ctrl, Scratch S) {
+    if (ctrl->status != ST_COMPACT) return;
+    const uint32_t L = ctrl->level;
+    const u128 prefix = ctrl->prefix;
+    const uint32_t sh_prev = digit_shift(L - 1);
+    const bool need_id_prefix = sh_prev < 32;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    uint64_t my_min = kNone;
+    for (uint32_t wr = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); wr < P.n; wr += stride) {
+        const uint32_t r = wr + lane;
+        bool take = false;
+        u128 ck = 0;
+        if (r < P.n) {
+            const uint64_t img = P.img[r];
+            if (img != kNone) {
+                ck = make_ck(img, need_id_prefix ? P.id[r] : 0u);
+                const u128 top = ck >> sh_prev;
+                if (top == prefix) { take = true; if (!need_id_prefix) ck |= (u128)P.id[r]; }
+                else if (top < prefix && img < my_min) my_min = img;
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, take);
+        if (m) {
+            uint32_t base = 0;
+            if (lane == __ffs(m) - 1) base = atomicAdd(&ctrl->bucket_fill, (uint32_t)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+            if (take) {
+                const uint32_t slot = base + __popc(m & ((1u << lane) - 1u));
+                if (slot < kBucketCap) { S.bucket_ck[slot] = ck; S.bucket_cost[slot] = P.cost[r]; }
+            }
+        }
+    }
+    my_min = warp_min_u64(my_min);
+    if (lane == 0 && my_min != kNone) atomicMin(&ctrl->pred_min_img, (unsigned long long)my_min);
+}
+
+// --------------------------------------------------------------------------------------
+// k_resolve: one CTA (1024 threads) -- exact B*, bp, thr from the sorted bucket (a7, a8)
+// --------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_resolve(Cfg c, Ctrl* ctrl, Scratch S) {
+    if (ctrl->status != ST_COMPACT) return;
+    extern __shared__ __align__(16) unsigned char smem[];
+    u128* sk = reinterpret_cast<u128*>(smem);
+    uint32_t* sv = reinterpret_cast<uint32_t*>(smem + sizeof(u128) * kBucketCap);
+    __shared__ uint64_t s_scan[32];
+    __shared__ uint32_t s_fit;
+    const uint32_t n = ctrl->bucket_fill;
+    if (n > kBucketCap || n != ctrl->bucket_count) {       // cannot happen: counts are exact
+        if (threadIdx.x == 0) { ctrl->error = 1; ctrl->status = ST_ERROR; }
+        return;
+    }
+    uint32_t n2 = 1;
+    while (n2 < n) n2 <<= 1;
+    for (uint32_t i = threadIdx.x; i < n2; i += blockDim.x) {
+        if (i < n) { sk[i] = S.bucket_ck[i]; sv[i] = S.bucket_cost[i]; }
+        else { sk[i] = ~(u128)0; sv[i] = 0; }
+    }
+    __syncthreads();
+    block_bitonic_sort<u128>(sk, sv, n2);
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) { S.bucket_ck[i] = sk[i]; S.bucket_cost[i] = sv[i]; }
+    // block scan of costs over the sorted bucket (4 consecutive per thread)
+    const uint32_t i0 = threadIdx.x * 4;
+    uint64_t loc = 0;
+    for (uint32_t k = 0; k < 4; ++k) if (i0 + k < n) loc += sv[i0 + k];
+    uint64_t tot;
+    uint64_t ex = block_exclusive_scan_u64(loc, s_scan, &tot);
+    if (threadIdx.x == 0) s_fit = 0;
+    __syncthreads();
+    const uint64_t bc = ctrl->before_count, bk = ctrl->before_cost;
+    uint32_t fits = 0;
+    uint64_t run = ex;
+    for (uint32_t k = 0; k < 4; ++k) {
+        const uint32_t i = i0 + k;
+        if (i >= n) break;
+        run += sv[i];
+        if (bc + i + 1 <= c.max_batch && bk + run <= c.token_budget) ++fits;   // monotone predicate
+    }
+    if (fits) atomicAdd(&s_fit, fits);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t nf = s_fit;
+        ctrl->b_star = (uint32_t)bc + nf;
+        const uint64_t bimg = nf ? ck_img(sk[nf - 1]) : (uint64_t)ctrl->pred_min_img;
+        const double bp = __longlong_as_double((long long)bimg);
+        ctrl->bp = bp;
+        ctrl->thr = __dmul_rn(__ddiv_rn((double)c.pn, (double)c.pd), bp);   // A16
+        ctrl->thr_img = (unsigned long long)__double_as_longlong(ctrl->thr);
+        if (nf == 0 && ctrl->pred_min_img == kNone) { ctrl->error = 1; ctrl->status = ST_ERROR; }
+        else ctrl->status = ST_RESOLVED;
+    }
+}
+
+// --------------------------------------------------------------------------------------
+// k_cand: Cd = {pending : key >= thr} (Alg. 1 Filter)
+// --------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kPassThreads) k_cand(Pool P, Ctrl* ctrl, Scratch S) {
+    if (ctrl->status != ST_RESOLVED) return;
+    const uint64_t thr_img = ctrl->thr_img;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    for (uint32_t wr = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); wr < P.n; wr += stride) {
+        const uint32_t r = wr + lane;
+        bool take = false;
+        if (r < P.n) {
+            const uint64_t img = P.img[r];
+            take = img != kNone && img >= thr_img;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, take);
+        if (m) {
+            uint32_t base = 0;
+            if (lane == __ffs(m) - 1) base = atomicAdd(&ctrl->n_cand, (uint32_t)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+            if (take) {
+                const uint32_t slot = base + __popc(m & ((1u << lane) - 1u));
+                if (slot < S.cand_cap) S.cand[slot] = r; else ctrl->cand_overflow = 1;
+            }
+        }
+    }
+}
+
+// block exclusive scan of u128 (blockDim 1024)
+__device__ __forceinline__ u128 block_exclusive_scan_u128(u128 v, u128* scratch, u128* total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    u128 x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        u128 y = shfl_up_u128(x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) scratch[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        u128 s = lane < nw ? scratch[lane] : (u128)0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            u128 y = shfl_up_u128(s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < nw) scratch[lane] = s;
+    }
+    __syncthreads();
+    u128 base = wid ? scratch[wid - 1] : (u128)0;
+    u128 t = scratch[nw - 1];
+    __syncthreads();
+    if (total) *total = t;
+    return base + x - v;
+}
+
+// --------------------------------------------------------------------------------------
+// k_group: one CTA of 1024 threads -- Alg. 1 step 2 under the token budget
+// --------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_group(Pool P, Cfg c, Ctrl* ctrl, Scratch S) {
+    if (ctrl->status != ST_RESOLVED) return;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ u128 s_scan128[32];
+    __shared__ uint64_t s_scan[32];
+    __shared__ u128 s_best[32];
+    __shared__ uint32_t s_bi[32], s_bj[32];
+    const uint32_t n = ctrl->n_cand;
+    if (ctrl->cand_overflow || n == 0) {
+        if (threadIdx.x == 0) { ctrl->error = 1; ctrl->status = ST_ERROR; }
+        return;
+    }
+    uint32_t n2 = 1;
+    while (n2 < n) n2 <<= 1;
+    uint64_t* sk;
+    uint32_t* sv;
+    if (n2 <= kGroupSmemSort) { sk = reinterpret_cast<uint64_t*>(smem); sv = reinterpret_cast<uint32_t*>(smem + 8 * kGroupSmemSort); }
+    else { sk = S.sk; sv = S.sv; }
+    for (uint32_t i = threadIdx.x; i < n2; i += blockDim.x) {
+        if (i < n) {
+            const uint32_t r = S.cand[i];
+            const uint64_t len = c.len_key ? (uint64_t)P.len_in[r] + P.gen[r] : (uint64_t)P.len_in[r];
+            sk[i] = (len << 32) | P.id[r];                      // (len asc, id asc), A17/A18
+            sv[i] = r;
+        } else { sk[i] = ~0ull; sv[i] = 0; }
+    }
+    __syncthreads();
+    block_bitonic_sort<uint64_t>(sk, sv, n2);
+    // prefix sums of cost (u64) and fixed-point key (u128), chunks of blockDim with carry
+    uint64_t carry_c = 0;
+    u128 carry_f = 0;
+    for (uint32_t base = 0; base < n; base += blockDim.x) {
+        const uint32_t i = base + threadIdx.x;
+        uint64_t cv = 0; u128 fv = 0;
+        if (i < n) {
+            const uint32_t r = sv[i];
+            cv = P.cost[r];
+            fv = (u128)fixed_point(__longlong_as_double((long long)P.img[r]));
+        }
+        uint64_t tc; u128 tf;
+        const uint64_t ec = block_exclusive_scan_u64(cv, s_scan, &tc);
+        const u128 ef = block_exclusive_scan_u128(fv, s_scan128, &tf);
+        if (i < n) { S.pc[i] = carry_c + ec; S.pf[i] = carry_f + ef; }
+        carry_c += tc; carry_f += tf;
+    }
+    if (threadIdx.x == 0) { S.pc[n] = carry_c; S.pf[n] = carry_f; }
+    __syncthreads();
+    // windows: j(i) = largest j with pc[j+1]-pc[i] <= tau and j-i+1 <= B_max; first argmax
+    u128 best = 0; uint32_t bi = 0xFFFFFFFFu, bj = 0;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint64_t lim = (uint64_t)__ldcg(&S.pc[i]) + c.token_budget;
+        uint32_t lo = i, hi = (uint32_t)min((uint64_t)n - 1, (uint64_t)i + c.max_batch - 1);
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi + 1) >> 1;
+            if (__ldcg(&S.pc[mid + 1]) <= lim) lo = mid; else hi = mid - 1;
+        }
+        const u128 sc = S.pf[lo + 1] - S.pf[i];
+        if (bi == 0xFFFFFFFFu || sc > best) { best = sc; bi = i; bj = lo; }   // i increasing per thread
+    }
+    // block argmax: larger score, then smaller i
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const u128 ob = shfl_xor_u128(best, o);
+        const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o), oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        const bool take = (oi != 0xFFFFFFFFu) && (bi == 0xFFFFFFFFu || ob > best || (ob == best && oi < bi));
+        if (take) { best = ob; bi = oi; bj = oj; }
+    }
+    if (lane == 0) { s_best[wid] = best; s_bi[wid] = bi; s_bj[wid] = bj; }
+    __syncthreads();
+    if (wid == 0) {
+        best = lane < 32 ? s_best[lane] : (u128)0; bi = s_bi[lane]; bj = s_bj[lane];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const u128 ob = shfl_xor_u128(best, o);
+            const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o), oj = __shfl_xor_sync(0xffffffffu, bj, o);
+            const bool take = (oi != 0xFFFFFFFFu) && (bi == 0xFFFFFFFFu || ob > best || (ob == best && oi < bi));
+            if (take) { best = ob; bi = oi; bj = oj; }
+        }
+        if (lane == 0) { s_bi[0] = bi; s_bj[0] = bj; }
+    }
+    __syncthreads();
+    bi = s_bi[0]; bj = s_bj[0];
+    const uint32_t ns = bj - bi + 1;
+    for (uint32_t k = threadIdx.x; k < ns; k += blockDim.x) {
+        const uint32_t r = sv[bi + k];
+        S.out_ids[k] = P.id[r];
+        S.out_tokens[k] = P.cost[r];
+        S.out_rows[k] = r;
+        // bookkeeping for the batch: ever_scheduled, Running; undo the steps_waited increment
+        uint32_t m = P.meta[r];
+        m |= (kEver << 12);
+        if (m_state(m) == kQueued || m_state(m) == kPreempted) m = m_with_state(m, kRunning);
+        P.meta[r] = m;
+        const uint32_t aux = P.aux[r];
+        if ((aux >> 16) < 0xFFFFu) P.aux[r] = aux - (1u << 16);
+    }
+    if (threadIdx.x == 0) {
+        ctrl->n_selected = ns;
+        ctrl->total_tokens = (uint32_t)(S.pc[bj + 1] - S.pc[bi]);
+        ctrl->i_best = bi; ctrl->j_best = bj;
+    }
+}
+
+// progress updates from the engine, applied before scoring
+__global__ void k_progress(Pool P, const uint32_t* rows, const uint32_t* gen, const uint32_t* pre,
+                           const uint32_t* state, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t r = rows[i];
+    if (r >= P.n) return;
+    P.gen[r] = gen[i];
+    P.pre[r] = pre[i];
+    P.meta[r] = m_with_state(P.meta[r], state[i] & 0xFu);
+}
+
+// load-time validation of a pool (layout rule of jit_pool, group types, ranges)
+__global__ void k_validate(Pool P, const Group* groups, uint32_t n_groups, uint32_t n_rows_tab, Ctrl* ctrl) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    bool bad = false;
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < P.n; r += stride) {
+        const uint32_t meta = P.meta[r], aux = P.aux[r];
+        const uint32_t gi = m_group(meta);
+        const bool comp = (m_flags(meta) & kCompound) != 0;
+        if (gi >= n_groups || (aux & 0xFFFFu) >= n_rows_tab || P.len_in[r] == 0 || P.len_in[r] >= (1u << 24) ||
+            P.gen[r] >= (1u << 24) || (meta >> 16) != 0 || m_state(meta) > kWaiting) bad = true;
+        else if (r < P.n_single) {
+            if (comp || P.task[r] != kNoTask || groups[gi].type == kCMP) bad = true;
+        } else {
+            const uint32_t t = P.task[r];
+            if (!comp || t >= P.n_tasks || groups[gi].type != kCMP || (m_flags(meta) & kOverride)) bad = true;
+            else if (r < P.call_off[t] || r >= P.call_off[t + 1]) bad = true;
+        }
+    }
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < P.n_tasks; t += stride) {
+        const uint32_t S = P.n_stages[t], s = P.cur_stage[t];
+        if (P.call_off[t] > P.call_off[t + 1] || S == 0 || S > kMaxStages || s >= S) bad = true;
+        else {
+            uint64_t tot = 0;
+            for (uint32_t u = 0; u < S; ++u) tot += P.pattern[t * kMaxStages + u];
+            if (tot == 0) bad = true;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (P.n_tasks && (P.call_off[0] != P.n_single || P.call_off[P.n_tasks] != P.n)) bad = true;
+        if (!P.n_tasks && P.n_single != P.n) bad = true;
+    }
+    if (bad) atomicOr(&ctrl->error, 2u);
+}
+
+}  // namespace jit

@@ -1,0 +1,513 @@
+// replay.cuh -- (a10) persistent trace replay: one CTA per replay (grid-stride over replays).
+//
+// Each CTA owns one replay at a time; the request state lives in a per-CTA global slice
+// (L2-resident: 2048 rows x 44 B), the selection working set in shared memory when it fits.
+// Per simulated iteration: stage releases / tool timers -> GMAX step over the
+// replay's rows (a1-a9, block-level: bitonic sort of the pending composite keys, block scan
+// of costs for B*/bp, cutoff, bitonic sort of Cd by (len, id), u64/u128 prefix windows) ->
+// iteration latency c0 + c_att*max ctx + c_lin*|batch| -> token emission and goodput
+// accounting (§3) -> stage barriers -> v_token = floor(trailing mean of Delta
+// latencies).  Integer sums are order independent, so results are deterministic.
+#pragma once
+#include "common.cuh"
+#include "pool.cuh"
+
+namespace jit {
+
+constexpr uint32_t kReplayThreads = 512;
+constexpr uint32_t kReplaySmemRows = 2048;    // rows sorted in shared memory up to this size
+
+struct TraceMeta { uint32_t row_off, task_off, n_rows, n_tasks; };
+
+struct Spec { uint32_t trace, reserved; uint64_t load_num, load_den, slo_num, slo_den; };
+
+struct RLog { int64_t now_ns; uint32_t n_selected, total_tokens, n_candidates, b_star; double bp; uint64_t ids_hash; };
+
+struct RResult {
+    unsigned long long token_goodput, tokens_processed;
+    int64_t sim_end_ns;
+    uint32_t request_goodput, n_done, n_dropped, steps, n_tasks_done, error;
+};
+
+struct ReplayArgs {
+    const TraceMeta* traces;
+    const int64_t* arrival; const uint32_t *len_in, *true_out, *group, *dist_row, *ovr, *task;
+    const int64_t *t_arr, *t_dl; const uint32_t* t_nst;
+    const uint32_t* st_kind; const int64_t* st_exec; const uint32_t *st_pat, *st_cb, *st_ce;
+    const Spec* specs;
+    uint32_t n_replays, n_steps, log_steps, max_rows, max_tasks, n_groups, pad0, pad1;
+    int64_t v0, c0, c_att, c_lin;
+    Table T; const Group* groups; Cfg c;
+    unsigned char* state; uint64_t state_stride;
+    RResult* out; RLog* log;
+};
+
+// per-CTA state slice layout
+struct RState {
+    int64_t* arr; uint32_t *gen, *pre, *lhat, *meta, *aux, *late, *cost; uint64_t* img;
+    uint32_t *cur, *left, *tdone, *cb, *ce; int64_t *timer, *ta, *tD; unsigned long long* gdone;
+    uint64_t *tle, *ttot;
+    u128* gA; uint32_t* gAv; uint64_t* gB; uint32_t* gBv; unsigned long long* gpc; u128* gpf;  // global sort scratch
+    uint32_t* batch; int64_t* ring;
+};
+
+__host__ __device__ inline uint64_t replay_state_bytes(uint32_t M, uint32_t MT, uint32_t max_batch) {
+    const uint64_t m = M + 64, mt = MT + 1;
+    uint64_t b = 0;
+    b += 8 * m + 4 * m * 7 + 8 * m;            // arr, gen..cost, img
+    b += 4 * mt * 5 + 8 * mt * 3 + 8 * mt + 16 * mt;   // task u32 x5, i64 x3, gdone, tle+ttot
+    uint64_t p2 = 1;                            // bitonic sorts pad to a power of two
+    while (p2 < m) p2 <<= 1;
+    b += 16 * p2 + 4 * p2 + 8 * p2 + 4 * p2 + 8 * (m + 1) + 16 * (m + 1);
+    b += 4 * (uint64_t)(max_batch + 1) + 8 * 1024;
+    return b + 64 * 32;                         // alignment slack
+}
+
+__device__ inline RState carve_state(unsigned char* p, uint32_t M, uint32_t MT, uint32_t max_batch) {
+    const uint64_t m = M + 64, mt = MT + 1;
+    RState s;
+    auto take = [&](uint64_t bytes) { unsigned char* q = p; p += (bytes + 63) & ~63ull; return q; };
+    s.arr = (int64_t*)take(8 * m);
+    s.gen = (uint32_t*)take(4 * m); s.pre = (uint32_t*)take(4 * m); s.lhat = (uint32_t*)take(4 * m);
+    s.meta = (uint32_t*)take(4 * m); s.aux = (uint32_t*)take(4 * m); s.late = (uint32_t*)take(4 * m);
+    s.cost = (uint32_t*)take(4 * m); s.img = (uint64_t*)take(8 * m);
+    s.cur = (uint32_t*)take(4 * mt); s.left = (uint32_t*)take(4 * mt); s.tdone = (uint32_t*)take(4 * mt);
+    s.cb = (uint32_t*)take(4 * mt); s.ce = (uint32_t*)take(4 * mt);
+    s.timer = (int64_t*)take(8 * mt); s.ta = (int64_t*)take(8 * mt); s.tD = (int64_t*)take(8 * mt);
+    s.gdone = (unsigned long long*)take(8 * mt); s.tle = (uint64_t*)take(8 * mt); s.ttot = (uint64_t*)take(8 * mt);
+    uint64_t p2 = 1;
+    while (p2 < m) p2 <<= 1;
+    s.gA = (u128*)take(16 * p2); s.gAv = (uint32_t*)take(4 * p2); s.gB = (uint64_t*)take(8 * p2);
+    s.gBv = (uint32_t*)take(4 * p2); s.gpc = (unsigned long long*)take(8 * (m + 1)); s.gpf = (u128*)take(16 * (m + 1));
+    s.batch = (uint32_t*)take(4 * (uint64_t)(max_batch + 1)); s.ring = (int64_t*)take(8 * 1024);
+    return s;
+}
+
+__device__ __forceinline__ int64_t scale_t(int64_t t, uint64_t num, uint64_t den) {
+    return (int64_t)((u128)(uint64_t)t * num / den);
+}
+
+__device__ __forceinline__ uint64_t call_R(const Group& g, uint32_t L_i, uint32_t L_o) {
+    return (uint64_t)g.w_in * L_i + (uint64_t)g.w_out * L_o;
+}
+
+// block-wide chunked exclusive scan helpers over an array produced by a functor
+__global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    Group* sg = reinterpret_cast<Group*>(smem);                                   // 256 groups
+    unsigned char* sbuf = smem + sizeof(Group) * 256;
+    // region A (24 cap + 64 B): pending sort (u128 key + u32 row), later reused for the
+    // window prefix sums (u64 cost + u128 fixed-point key); region B: Cd sort (u64 + u32)
+    u128* sA = reinterpret_cast<u128*>(sbuf);
+    uint32_t* sAv = reinterpret_cast<uint32_t*>(sbuf + 16 * kReplaySmemRows);
+    uint64_t* sB = reinterpret_cast<uint64_t*>(sbuf + 24 * kReplaySmemRows + 64);
+    uint32_t* sBv = reinterpret_cast<uint32_t*>(sbuf + 32 * kReplaySmemRows + 64);
+    __shared__ uint64_t s_scan[32];
+    __shared__ u128 s_scan128[32];
+    __shared__ u128 s_best[32];
+    __shared__ uint32_t s_bi[32], s_bj[32];
+    __shared__ unsigned long long s_good, s_tok, s_min;
+    __shared__ uint32_t s_reqg, s_done, s_drop, s_tdone, s_err, s_npend, s_cnt;
+    __shared__ int64_t s_now, s_maxctx, s_nxt;
+    __shared__ uint32_t s_steps, s_ring_n, s_ring_pos;
+    __shared__ int64_t s_ring_sum;
+    __shared__ uint32_t s_bstar, s_ncd, s_nsel, s_tot;
+    __shared__ double s_bp, s_thr;
+    __shared__ uint64_t s_thr_img;
+    __shared__ bool s_stop;
+
+    const Cfg c = A.c;
+    const Table T = A.T;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    RState S = carve_state(A.state + (uint64_t)blockIdx.x * A.state_stride, A.max_rows, A.max_tasks, c.max_batch);
+
+    for (uint32_t rep = blockIdx.x; rep < A.n_replays; rep += gridDim.x) {
+        const Spec sp = A.specs[rep];
+        const TraceMeta tm = A.traces[sp.trace];
+        const uint32_t n = tm.n_rows, nt = tm.n_tasks;
+        const int64_t* tr_arr = A.arrival + tm.row_off;
+        const uint32_t* L_in = A.len_in + tm.row_off;
+        const uint32_t* L_out = A.true_out + tm.row_off;
+        const uint32_t* grp = A.group + tm.row_off;
+        const uint32_t* drow = A.dist_row + tm.row_off;
+        const uint32_t* ovr = A.ovr + tm.row_off;
+        const uint32_t* tsk = A.task + tm.row_off;
+        const uint32_t* st_kind = A.st_kind + (uint64_t)tm.task_off * kMaxStages;
+        const int64_t* st_exec = A.st_exec + (uint64_t)tm.task_off * kMaxStages;
+        const uint32_t* st_pat = A.st_pat + (uint64_t)tm.task_off * kMaxStages;
+        const uint32_t* st_cb = A.st_cb + (uint64_t)tm.task_off * kMaxStages;
+        const uint32_t* st_ce = A.st_ce + (uint64_t)tm.task_off * kMaxStages;
+        const bool in_smem = n <= kReplaySmemRows;
+        u128* bA = in_smem ? sA : S.gA;
+        uint32_t* bAv = in_smem ? sAv : S.gAv;
+        uint64_t* bB = in_smem ? sB : S.gB;
+        uint32_t* bBv = in_smem ? sBv : S.gBv;
+
+        // ---- setup: SLO-scaled groups, initial row and task state
+        for (uint32_t g = threadIdx.x; g < A.n_groups; g += blockDim.x) {
+            Group G = A.groups[g];
+            G.ttft_ns = scale_t(G.ttft_ns, sp.slo_num, sp.slo_den);
+            G.tbt_ns = scale_t(G.tbt_ns, sp.slo_num, sp.slo_den);
+            G.e2el_ns = scale_t(G.e2el_ns, sp.slo_num, sp.slo_den);
+            G.be_deadline_ns = scale_t(G.be_deadline_ns, sp.slo_num, sp.slo_den);
+            sg[g] = G;
+        }
+        if (threadIdx.x == 0) {
+            s_good = 0; s_tok = 0; s_reqg = 0; s_done = 0; s_drop = 0; s_tdone = 0; s_err = 0;
+            s_now = 0; s_steps = 0; s_ring_n = 0; s_ring_pos = 0; s_ring_sum = 0; s_stop = false;
+        }
+        __syncthreads();
+        for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
+            const bool comp = tsk[r] != kNoTask;
+            uint32_t fl = (comp ? kCompound : 0u) | (ovr[r] ? kOverride : 0u);
+            const uint32_t g = grp[r];
+            bool bad = L_in[r] == 0 || L_out[r] == 0 || g >= A.n_groups || drow[r] >= T.n_rows ||
+                       (ovr[r] && sg[g].type != kDDL) || (comp != (sg[g].type == kCMP)) || (comp && tsk[r] >= nt);
+            if (bad) atomicOr(&s_err, 1u);
+            S.meta[r] = g | ((comp ? kWaiting : kQueued) << 8) | (fl << 12);
+            S.aux[r] = drow[r] & 0xFFFFu;
+            S.gen[r] = 0; S.pre[r] = 0; S.lhat[r] = 0; S.late[r] = 0;
+            S.arr[r] = comp ? INT64_MAX : scale_t(tr_arr[r], sp.load_den, sp.load_num);
+        }
+        for (uint32_t t = threadIdx.x; t < nt; t += blockDim.x) {
+            const uint32_t tg = tm.task_off + t;
+            S.ta[t] = scale_t(A.t_arr[tg], sp.load_den, sp.load_num);
+            S.tD[t] = scale_t(A.t_dl[tg], sp.slo_num, sp.slo_den);
+            const uint32_t Sn = A.t_nst[tg];
+            if (Sn == 0 || Sn > kMaxStages) atomicOr(&s_err, 1u);
+            uint64_t tot = 0;
+            for (uint32_t u = 0; u < Sn && u < kMaxStages; ++u) tot += (uint64_t)st_pat[t * kMaxStages + u] * 1000000ull;
+            S.ttot[t] = tot; S.tle[t] = 0;
+            S.timer[t] = S.ta[t]; S.cur[t] = 0; S.cb[t] = 0; S.ce[t] = 0; S.left[t] = 0; S.tdone[t] = 0; S.gdone[t] = 0;
+        }
+        __syncthreads();
+
+        while (!s_err) {
+            const int64_t now = s_now;
+            // ---- stage starts whose time has come (task arrival or the end of the previous stage)
+            for (uint32_t t = threadIdx.x; t < nt; t += blockDim.x) {
+                const uint32_t Sn = A.t_nst[tm.task_off + t];
+                while (!S.tdone[t] && S.timer[t] <= now) {
+                    const int64_t at = S.timer[t];
+                    const uint32_t s = S.cur[t];
+                    if (s == Sn) {
+                        S.tdone[t] = 1; atomicAdd(&s_tdone, 1u); S.timer[t] = INT64_MAX;
+                        if (at <= S.ta[t] + S.tD[t]) {                       // §3
+                            unsigned long long tot = 0;
+                            for (uint32_t u = 0; u < Sn; ++u) {
+                                const uint32_t kk = t * kMaxStages + u;
+                                if (st_kind[kk] == 0)
+                                    for (uint32_t q = st_cb[kk]; q < st_ce[kk]; ++q) tot += call_R(sg[grp[q]], L_in[q], L_out[q]);
+                            }
+                            atomicAdd(&s_good, tot); atomicAdd(&s_reqg, 1u);
+                        }
+                        break;
+                    }
+                    const uint32_t k = t * kMaxStages + s;
+                    if (st_kind[k] == 1) { S.cur[t] = s + 1; S.timer[t] = at + st_exec[k]; continue; }
+                    const uint32_t b = st_cb[k], e = st_ce[k];
+                    if (b >= e || e > n) { atomicOr(&s_err, 1u); break; }
+                    S.cb[t] = b; S.ce[t] = e; S.left[t] = e - b;
+                    for (uint32_t r = b; r < e; ++r) { S.arr[r] = at; S.meta[r] = m_with_state(S.meta[r], kQueued); }
+                    uint64_t le = 0;
+                    for (uint32_t u = 0; u <= s; ++u) le += (uint64_t)st_pat[t * kMaxStages + u] * 1000000ull;
+                    S.tle[t] = le;
+                    S.timer[t] = INT64_MAX;
+                }
+            }
+            __syncthreads();
+            if (s_steps >= A.n_steps || s_err) break;
+            const int64_t v = s_ring_n ? s_ring_sum / (int64_t)s_ring_n : A.v0;
+
+            // ---- (a1)-(a6) scoring of every row; steps_waited+1 for pending rows
+            uint32_t my_pend = 0, my_drop = 0, my_err = 0;
+            for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
+                const uint32_t meta = S.meta[r];
+                if (m_flags(meta) & kCompound) continue;
+                RowRes o;
+                score_standalone<false>(c, T, sg, A.n_groups, ovr, r, now, v, S.arr[r], L_in[r], S.gen[r], S.pre[r],
+                                        S.lhat[r], meta, S.aux[r], o);
+                S.img[r] = o.img; S.cost[r] = o.cost; S.aux[r] = o.aux;
+                if (o.w_meta) S.meta[r] = o.meta;
+                if (o.w_lhat) S.lhat[r] = o.lhat;
+                my_pend += o.img != kNone; my_drop += o.dropped; my_err |= o.err;
+            }
+            for (uint32_t t = threadIdx.x; t < nt; t += blockDim.x) {       // (a4) one thread per task
+                const uint32_t b = S.cb[t], e = S.ce[t];
+                if (S.tdone[t]) continue;
+                uint64_t Tsum = 0, Gcur = 0; uint32_t cnt = 0;
+                for (uint32_t r = b; r < e; ++r) {
+                    uint32_t meta = S.meta[r];
+                    if (S.arr[r] > now || m_state(meta) > kPreempted) { S.img[r] = kNone; S.cost[r] = 0; continue; }
+                    const uint32_t g = S.gen[r];
+                    uint32_t lhat = S.lhat[r];
+                    const uint32_t ep = g / c.R;
+                    if (lhat == 0 || ep >= 65536u || m_epoch(meta) != ep) {
+                        lhat = cond_quantile(T, S.aux[r] & 0xFFFFu, ep * c.R, c.qn, c.qd);
+                        S.lhat[r] = lhat;
+                        if (ep < 65536u) S.meta[r] = (meta & 0xFFFFu) | (ep << 16);
+                    }
+                    const uint32_t Lh = lhat > g + 1 ? lhat : g + 1;
+                    Tsum += Lh - g;
+                    const Group& G = sg[m_group(meta)];
+                    Gcur += (uint64_t)G.w_in * L_in[r] + (uint64_t)G.w_out * Lh;
+                    ++cnt;
+                }
+                if (!cnt) continue;
+                uint64_t Gt = S.gdone[t] + Gcur;
+                if (S.ta[t] + S.tD[t] <= now) Gt = 0;
+                const int64_t Ds = S.ttot[t] ? (int64_t)((u128)(uint64_t)S.tD[t] * S.tle[t] / S.ttot[t]) : 0;
+                const int64_t trem = S.ta[t] + Ds - now;
+                const uint64_t t_gen = Tsum * (uint64_t)v;
+                if (c.appb && t_gen > (uint64_t)(trem > 0 ? trem : 0)) Gt = 0;
+                for (uint32_t r = b; r < e; ++r) {
+                    const uint32_t meta = S.meta[r];
+                    if (S.arr[r] > now || m_state(meta) > kPreempted) continue;
+                    const uint32_t aux = S.aux[r];
+                    const uint64_t Gp = Gt + (uint64_t)c.delta * ((aux >> 16) / c.frame);
+                    double key;
+                    if (!make_key(Gp, t_gen, c.eps, &key)) my_err = 1;
+                    S.img[r] = (uint64_t)__double_as_longlong(key);
+                    S.cost[r] = token_cost(L_in[r], S.pre[r], c.chunk);
+                    if ((aux >> 16) < 0xFFFFu) S.aux[r] = aux + (1u << 16);
+                    ++my_pend;
+                }
+            }
+            // compound rows outside a released stage are never pending
+            for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
+                const uint32_t meta = S.meta[r];
+                if ((m_flags(meta) & kCompound) && (S.arr[r] > now || m_state(meta) > kPreempted)) { S.img[r] = kNone; S.cost[r] = 0; }
+            }
+            my_pend = warp_sum(my_pend); my_drop = warp_sum(my_drop);
+            my_err = __reduce_or_sync(0xffffffffu, my_err);
+            if (threadIdx.x == 0) { s_npend = 0; }
+            __syncthreads();
+            if (lane == 0) { atomicAdd(&s_npend, my_pend); atomicAdd(&s_drop, my_drop); if (my_err) atomicOr(&s_err, 1u); }
+            __syncthreads();
+            if (s_err) break;
+            const uint32_t np = s_npend;
+            if (np == 0) {
+                // idle: jump to the next arrival / stage start; stop when drained
+                if (threadIdx.x == 0) s_nxt = INT64_MAX;
+                __syncthreads();
+                int64_t my = INT64_MAX;
+                for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
+                    const uint32_t meta = S.meta[r];
+                    if (!(m_flags(meta) & kCompound) && m_state(meta) == kQueued && S.arr[r] > now && S.arr[r] < my) my = S.arr[r];
+                }
+                for (uint32_t t = threadIdx.x; t < nt; t += blockDim.x)
+                    if (!S.tdone[t] && S.timer[t] != INT64_MAX && S.timer[t] > now && S.timer[t] < my) my = S.timer[t];
+                atomicMin((unsigned long long*)&s_nxt, (unsigned long long)my);
+                __syncthreads();
+                if (s_nxt == INT64_MAX) break;
+                if (threadIdx.x == 0) s_now = s_nxt;
+                __syncthreads();
+                continue;
+            }
+
+            // ---- (a7) order pending by (key desc, id asc): bitonic sort of composite keys
+            uint32_t n2 = 1;
+            while (n2 < np) n2 <<= 1;
+            {
+                uint32_t cntl = 0;
+                for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) cntl += S.img[r] != kNone;
+                uint64_t dummy;
+                uint32_t pos = (uint32_t)block_exclusive_scan_u64(cntl, s_scan, &dummy);
+                for (uint32_t r = threadIdx.x; r < n; r += blockDim.x)
+                    if (S.img[r] != kNone) { bA[pos] = make_ck(S.img[r], r); bAv[pos] = r; ++pos; }
+                for (uint32_t i = np + threadIdx.x; i < n2; i += blockDim.x) { bA[i] = ~(u128)0; bAv[i] = 0; }
+            }
+            __syncthreads();
+            block_bitonic_sort<u128>(bA, bAv, n2);
+            // B* = longest prefix within tau and B_max (monotone predicate -> count)
+            {
+                uint64_t carry = 0;
+                uint32_t fits = 0;
+                for (uint32_t base = 0; base < np; base += blockDim.x) {
+                    const uint32_t i = base + threadIdx.x;
+                    const uint64_t cv = i < np ? S.cost[bAv[i]] : 0;
+                    uint64_t tot;
+                    const uint64_t ex = block_exclusive_scan_u64(cv, s_scan, &tot);
+                    const bool f = i < np && (uint64_t)i + 1 <= c.max_batch && carry + ex + cv <= c.token_budget;
+                    fits += __syncthreads_count(f);
+                    carry += tot;
+                }
+                if (threadIdx.x == 0) {
+                    s_bstar = fits;
+                    const double bp = __longlong_as_double((long long)ck_img(bA[fits - 1]));
+                    s_bp = bp;
+                    s_thr = __dmul_rn(__ddiv_rn((double)c.pn, (double)c.pd), bp);
+                    s_thr_img = (uint64_t)__double_as_longlong(s_thr);
+                }
+                __syncthreads();
+            }
+            // ---- (a8) Cd = prefix of the key-ordered list with key >= thr
+            {
+                uint32_t ncd = 0;
+                for (uint32_t base = 0; base < np; base += blockDim.x) {
+                    const uint32_t i = base + threadIdx.x;
+                    ncd += __syncthreads_count(i < np && ck_img(bA[i]) >= s_thr_img);
+                }
+                if (threadIdx.x == 0) s_ncd = ncd;
+                __syncthreads();
+            }
+            const uint32_t ncd = s_ncd;
+            uint32_t m2 = 1;
+            while (m2 < ncd) m2 <<= 1;
+            for (uint32_t i = threadIdx.x; i < m2; i += blockDim.x) {
+                if (i < ncd) {
+                    const uint32_t r = bAv[i];
+                    const uint64_t len = c.len_key ? (uint64_t)L_in[r] + S.gen[r] : (uint64_t)L_in[r];
+                    bB[i] = (len << 32) | r; bBv[i] = r;
+                } else { bB[i] = ~0ull; bBv[i] = 0; }
+            }
+            __syncthreads();
+            // ---- (a9) sort Cd by (len, id); windows within tau / B_max; first argmax
+            block_bitonic_sort<uint64_t>(bB, bBv, m2);
+            unsigned long long* pc = in_smem ? reinterpret_cast<unsigned long long*>(sA) : S.gpc;   // reuse region A
+            u128* pf = in_smem ? reinterpret_cast<u128*>(sbuf + ((8 * (kReplaySmemRows + 1) + 15) & ~15u)) : S.gpf;
+            {
+                uint64_t carry_c = 0; u128 carry_f = 0;
+                for (uint32_t base = 0; base < ncd; base += blockDim.x) {
+                    const uint32_t i = base + threadIdx.x;
+                    uint64_t cv = 0; u128 fv = 0;
+                    if (i < ncd) {
+                        const uint32_t r = bBv[i];
+                        cv = S.cost[r];
+                        fv = (u128)fixed_point(__longlong_as_double((long long)S.img[r]));
+                    }
+                    uint64_t tc; u128 tf;
+                    const uint64_t ec = block_exclusive_scan_u64(cv, s_scan, &tc);
+                    const u128 ef = block_exclusive_scan_u128(fv, s_scan128, &tf);
+                    if (i < ncd) { pc[i] = carry_c + ec; pf[i] = carry_f + ef; }
+                    carry_c += tc; carry_f += tf;
+                }
+                if (threadIdx.x == 0) { pc[ncd] = carry_c; pf[ncd] = carry_f; }
+                __syncthreads();
+            }
+            {
+                u128 best = 0; uint32_t bi = 0xFFFFFFFFu, bj = 0;
+                for (uint32_t i = threadIdx.x; i < ncd; i += blockDim.x) {
+                    const uint64_t lim = (uint64_t)pc[i] + c.token_budget;
+                    uint32_t lo = i, hi = (uint32_t)min((uint64_t)ncd - 1, (uint64_t)i + c.max_batch - 1);
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi + 1) >> 1;
+                        if (pc[mid + 1] <= lim) lo = mid; else hi = mid - 1;
+                    }
+                    const u128 sc = pf[lo + 1] - pf[i];
+                    if (bi == 0xFFFFFFFFu || sc > best) { best = sc; bi = i; bj = lo; }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const u128 ob = shfl_xor_u128(best, o);
+                    const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o), oj = __shfl_xor_sync(0xffffffffu, bj, o);
+                    if ((oi != 0xFFFFFFFFu) && (bi == 0xFFFFFFFFu || ob > best || (ob == best && oi < bi))) { best = ob; bi = oi; bj = oj; }
+                }
+                if (lane == 0) { s_best[wid] = best; s_bi[wid] = bi; s_bj[wid] = bj; }
+                __syncthreads();
+                if (wid == 0) {
+                    const uint32_t nw = blockDim.x >> 5;
+                    best = lane < nw ? s_best[lane] : (u128)0; bi = lane < nw ? s_bi[lane] : 0xFFFFFFFFu; bj = lane < nw ? s_bj[lane] : 0;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        const u128 ob = shfl_xor_u128(best, o);
+                        const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o), oj = __shfl_xor_sync(0xffffffffu, bj, o);
+                        if ((oi != 0xFFFFFFFFu) && (bi == 0xFFFFFFFFu || ob > best || (ob == best && oi < bi))) { best = ob; bi = oi; bj = oj; }
+                    }
+                    if (lane == 0) {
+                        s_nsel = bj - bi + 1;
+                        s_tot = (uint32_t)(pc[bj + 1] - pc[bi]);
+                        s_bi[0] = bi;
+                    }
+                }
+                __syncthreads();
+            }
+            const uint32_t nsel = s_nsel, i0 = s_bi[0];
+            // batch rows, bookkeeping (ever_scheduled, Running, undo steps_waited+1), max context
+            int64_t myctx = 0;
+            for (uint32_t k = threadIdx.x; k < nsel; k += blockDim.x) {
+                const uint32_t r = bBv[i0 + k];
+                S.batch[k] = r;
+                uint32_t m = S.meta[r] | (kEver << 12);
+                if (m_state(m) == kQueued || m_state(m) == kPreempted) m = m_with_state(m, kRunning);
+                S.meta[r] = m;
+                const uint32_t aux = S.aux[r];
+                if ((aux >> 16) < 0xFFFFu) S.aux[r] = aux - (1u << 16);
+                const int64_t ctx = S.pre[r] < L_in[r] ? (int64_t)S.pre[r] + S.cost[r] : (int64_t)L_in[r] + S.gen[r];
+                myctx = ctx > myctx ? ctx : myctx;
+            }
+            if (threadIdx.x == 0) s_maxctx = 0;
+            __syncthreads();
+            atomicMax((unsigned long long*)&s_maxctx, (unsigned long long)myctx);
+            __syncthreads();
+            // ---- (a10) iteration latency and time advance
+            const int64_t latency = A.c0 + A.c_att * s_maxctx + A.c_lin * (int64_t)nsel;
+            const int64_t tnow = now + latency;
+            if (threadIdx.x == 0) {
+                s_now = tnow;
+                s_steps += 1;
+                s_tok += s_tot;
+                if (A.log && s_steps <= A.log_steps) {
+                    uint64_t h = 1469598103934665603ull;
+                    for (uint32_t k = 0; k < nsel; ++k) h = fnv1a_u32(h, S.batch[k]);
+                    RLog L;
+                    L.now_ns = tnow; L.n_selected = nsel; L.total_tokens = s_tot; L.n_candidates = ncd;
+                    L.b_star = s_bstar; L.bp = s_bp; L.ids_hash = h;
+                    A.log[(uint64_t)rep * A.log_steps + s_steps - 1] = L;
+                }
+                // v_token ring (Delta = frame_steps latencies)
+                if (s_ring_n < c.frame) { S.ring[s_ring_n] = latency; s_ring_n += 1; s_ring_sum += latency; }
+                else { s_ring_sum += latency - S.ring[s_ring_pos]; S.ring[s_ring_pos] = latency; s_ring_pos = (s_ring_pos + 1) % c.frame; }
+            }
+            __syncthreads();
+            // progress of the executed batch, token timestamps = iteration end
+            for (uint32_t k = threadIdx.x; k < nsel; k += blockDim.x) {
+                const uint32_t r = S.batch[k];
+                const Group& G = sg[grp[r]];
+                bool emit = false;
+                if (S.pre[r] < L_in[r]) {
+                    S.pre[r] += S.cost[r];
+                    if (S.pre[r] == L_in[r]) emit = true;            // prefill end emits token 0
+                } else emit = true;
+                if (!emit) continue;
+                const uint32_t tok = S.gen[r];
+                if (G.type == kLAT) {                                  // §3
+                    if (tnow <= S.arr[r] + G.ttft_ns + (int64_t)tok * G.tbt_ns) atomicAdd(&s_good, (unsigned long long)G.w_out);
+                    else S.late[r] = 1;
+                }
+                S.gen[r] = tok + 1;
+                if (tok + 1 < L_out[r]) continue;
+                S.meta[r] = m_with_state(S.meta[r], kDone);
+                atomicAdd(&s_done, 1u);
+                if (G.type == kDDL) {                                  // §3
+                    if (tnow <= S.arr[r] + G.e2el_ns) {
+                        atomicAdd(&s_good, (unsigned long long)(ovr[r] ? (uint64_t)ovr[r] : call_R(G, L_in[r], L_out[r])));
+                        atomicAdd(&s_reqg, 1u);
+                    }
+                } else if (G.type == kLAT) {
+                    if (!S.late[r]) atomicAdd(&s_reqg, 1u);
+                } else if (G.type == kCMP) {                           // stage barrier
+                    const uint32_t t = tsk[r];
+                    atomicAdd(&S.gdone[t], (unsigned long long)call_R(G, L_in[r], L_out[r]));
+                    if (atomicSub(&S.left[t], 1u) == 1u) {
+                        S.cur[t] += 1; S.cb[t] = 0; S.ce[t] = 0; S.timer[t] = tnow;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            RResult R;
+            R.token_goodput = s_good; R.tokens_processed = s_tok; R.sim_end_ns = s_now;
+            R.request_goodput = s_reqg; R.n_done = s_done; R.n_dropped = s_drop; R.steps = s_steps;
+            R.n_tasks_done = s_tdone; R.error = s_err;
+            A.out[rep] = R;
+        }
+        __syncthreads();
+    }
+}
+
+inline uint32_t replay_smem_bytes() { return (uint32_t)(sizeof(Group) * 256 + 36 * kReplaySmemRows + 64); }
+
+}  // namespace jit

@@ -1,0 +1,350 @@
+"""ctypes binding of libjitsched.so (include/jit_sched.h) -- argument marshalling only.
+
+Every step of the scheduling path runs in the CUDA kernels of libjitsched.so; this module
+only packs numpy / torch buffers into the C structs and calls the same-named C entry points.
+There is no CPU fallback: importing this module on a machine without the built library, or
+using it without a CUDA device, raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libjitsched.so")
+
+JIT_OK, JIT_EMPTY = 0, 1
+JIT_CFG_DEBUG_ROWS = 1
+NO_TASK = 0xFFFFFFFF
+
+
+class JitSchedError(RuntimeError):
+    pass
+
+
+class jit_slo_group(C.Structure):
+    _fields_ = [("type", C.c_uint32), ("w_in", C.c_uint32), ("w_out", C.c_uint32), ("reserved", C.c_uint32),
+                ("ttft_ns", C.c_int64), ("tbt_ns", C.c_int64), ("e2el_ns", C.c_int64), ("be_deadline_ns", C.c_int64)]
+
+
+class jit_len_table(C.Structure):
+    _fields_ = [("n_rows", C.c_uint32), ("n_bins", C.c_uint32), ("l_max", C.c_uint32), ("reserved", C.c_uint32),
+                ("edges", C.c_void_p), ("cum", C.c_void_p)]
+
+
+_CFG_U32 = ("token_budget", "max_batch", "prefill_chunk", "refine_interval", "frame_steps", "q_num", "q_den",
+            "p_num", "p_den", "delta_starve", "len_key", "appb_filter")
+
+
+class jit_config(C.Structure):
+    _fields_ = [(k, C.c_uint32) for k in _CFG_U32] + \
+               [("eps_ns", C.c_int64), ("waiting_ns", C.c_int64), ("capacity", C.c_uint32),
+                ("task_capacity", C.c_uint32), ("flags", C.c_uint32), ("device", C.c_int32), ("stream", C.c_void_p)]
+
+
+_POOL_ROWS = (("id", np.uint32), ("arrival_ns", np.int64), ("input_len", np.uint32), ("generated", np.uint32),
+              ("prefilled", np.uint32), ("meta", np.uint32), ("aux", np.uint32), ("task", np.uint32),
+              ("override_R", np.uint32))
+_POOL_TASKS = (("call_off", np.uint32), ("task_arrival_ns", np.int64), ("task_deadline_ns", np.int64),
+               ("cur_stage", np.uint32), ("n_stages", np.uint32), ("pattern_ms", np.uint32),
+               ("goodput_done", np.uint64))
+
+
+class jit_pool(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("n_single", C.c_uint32), ("n_tasks", C.c_uint32), ("on_device", C.c_int32)] + \
+               [(k, C.c_void_p) for k, _ in _POOL_ROWS] + [(k, C.c_void_p) for k, _ in _POOL_TASKS]
+
+
+class jit_step_in(C.Structure):
+    _fields_ = [("now_ns", C.c_int64), ("v_token_ns", C.c_int64), ("n_progress", C.c_uint32),
+                ("reserved", C.c_uint32), ("prog_row", C.c_void_p), ("prog_generated", C.c_void_p),
+                ("prog_prefilled", C.c_void_p), ("prog_state", C.c_void_p)]
+
+
+class jit_batch(C.Structure):
+    _fields_ = [("capacity", C.c_uint32), ("n_selected", C.c_uint32), ("total_tokens", C.c_uint32),
+                ("n_candidates", C.c_uint32), ("b_star", C.c_uint32), ("n_pending", C.c_uint32),
+                ("n_dropped", C.c_uint32), ("status", C.c_uint32), ("bp", C.c_double), ("thr", C.c_double),
+                ("ids", C.c_void_p), ("tokens", C.c_void_p), ("rows", C.c_void_p)]
+
+
+_TRACE = (("arrival_ns", np.int64), ("input_len", np.uint32), ("true_out", np.uint32), ("group", np.uint32),
+          ("dist_row", np.uint32), ("override_R", np.uint32), ("task", np.uint32), ("task_arrival_ns", np.int64),
+          ("task_deadline_ns", np.int64), ("task_n_stages", np.uint32), ("stage_kind", np.uint32),
+          ("stage_exec_ns", np.int64), ("stage_pattern_ms", np.uint32), ("stage_call_begin", np.uint32),
+          ("stage_call_end", np.uint32))
+
+
+class jit_trace(C.Structure):
+    _fields_ = [("n_rows", C.c_uint32), ("n_tasks", C.c_uint32)] + [(k, C.c_void_p) for k, _ in _TRACE]
+
+
+class jit_replay_spec(C.Structure):
+    _fields_ = [("trace", C.c_uint32), ("reserved", C.c_uint32), ("load_num", C.c_uint64), ("load_den", C.c_uint64),
+                ("slo_num", C.c_uint64), ("slo_den", C.c_uint64)]
+
+
+class jit_replay_cfg(C.Structure):
+    _fields_ = [("n_steps", C.c_uint32), ("n_replays", C.c_uint32), ("log_steps", C.c_uint32),
+                ("reserved", C.c_uint32), ("v_token0_ns", C.c_int64), ("c0_ns", C.c_int64), ("c_att_ns", C.c_int64),
+                ("c_lin_ns", C.c_int64), ("specs", C.c_void_p)]
+
+
+class jit_replay_result(C.Structure):
+    _fields_ = [("token_goodput", C.c_uint64), ("tokens_processed", C.c_uint64), ("sim_end_ns", C.c_int64)] + \
+               [(k, C.c_uint32) for k in ("request_goodput", "n_done", "n_dropped", "steps", "n_tasks_done", "error")]
+
+
+STEP_LOG_DTYPE = np.dtype([("now_ns", "<i8"), ("n_selected", "<u4"), ("total_tokens", "<u4"),
+                           ("n_candidates", "<u4"), ("b_star", "<u4"), ("bp", "<f8"), ("ids_hash", "<u8")])
+
+_lib = None
+EXPORTS = ("jit_sched_workspace_bytes", "jit_sched_init", "jit_sched_load", "jit_sched_step",
+           "jit_sched_step_async", "jit_sched_fetch_batch", "jit_sched_read_rows", "jit_sched_kernel_times",
+           "jit_replay_workspace_bytes", "jit_sched_replay", "jit_sched_destroy", "jit_sched_last_error",
+           "jit_sched_version")
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libjitsched.so (raises if it has not been built -- there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise JitSchedError(f"{path} not built: run __graft_entry__.build()")
+        lib = C.CDLL(path)
+        lib.jit_sched_last_error.restype = C.c_char_p
+        lib.jit_sched_last_error.argtypes = [C.c_void_p]
+        lib.jit_sched_version.restype = C.c_char_p
+        lib.jit_sched_destroy.restype = None
+        lib.jit_sched_destroy.argtypes = [C.c_void_p]
+        for name in EXPORTS:
+            if name not in ("jit_sched_last_error", "jit_sched_version", "jit_sched_destroy"):
+                getattr(lib, name).restype = C.c_int
+        _lib = lib
+    return _lib
+
+
+def _c(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+def _p(a):
+    return C.c_void_p(a.ctypes.data) if isinstance(a, np.ndarray) else C.c_void_p(a.data_ptr())
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise JitSchedError("libjitsched needs a CUDA device (no CPU fallback)")
+    return torch
+
+
+def make_config(cfg: dict, capacity: int, task_capacity: int, device: int = 0, stream=None, debug=False):
+    c = jit_config()
+    for k in _CFG_U32:
+        setattr(c, k, int(cfg[k]))
+    c.eps_ns = int(cfg["eps_ns"])
+    c.waiting_ns = int(cfg["waiting_ns"])
+    c.capacity = int(capacity)
+    c.task_capacity = int(task_capacity)
+    c.flags = JIT_CFG_DEBUG_ROWS if debug else 0
+    c.device = int(device)
+    c.stream = stream
+    return c
+
+
+def make_groups(groups: dict):
+    n = len(groups["type"])
+    arr = (jit_slo_group * n)()
+    for i in range(n):
+        for k in ("type", "w_in", "w_out", "ttft_ns", "tbt_ns", "e2el_ns", "be_deadline_ns"):
+            setattr(arr[i], k, int(groups[k][i]))
+    return arr, n
+
+
+class Scheduler:
+    """One jit_sched handle on one CUDA device; the workspace is a torch uint8 tensor."""
+
+    def __init__(self, cfg: dict, groups: dict, table: dict, capacity: int, task_capacity: int = 0,
+                 device: int = 0, stream=None, debug: bool = False):
+        torch = _torch()
+        self.lib = load_library()
+        self.device = device
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.torch_stream = stream
+        self._keep = []
+        self.cfg_dict = dict(cfg)
+        self.c = make_config(cfg, capacity, task_capacity, device, C.c_void_p(stream.cuda_stream), debug)
+        self.groups, self.n_groups = make_groups(groups)
+        edges = _c(table["edges"], np.uint32)
+        cum = _c(table["cum"], np.uint32)
+        self._table_arrays = (edges, cum)
+        self.t = jit_len_table(cum.shape[0], cum.shape[1], int(table["l_max"]), 0, _p(edges), _p(cum))
+        nbytes = C.c_uint64()
+        self._check(self.lib.jit_sched_workspace_bytes(C.byref(self.c), C.byref(self.t), C.byref(nbytes)), None)
+        self.ws = torch.empty(int(nbytes.value) + 256, dtype=torch.uint8, device=f"cuda:{device}")
+        h = C.c_void_p()
+        rc = self.lib.jit_sched_init(C.byref(self.c), self.groups, C.c_uint32(self.n_groups), C.byref(self.t),
+                                     C.c_void_p(self.ws.data_ptr()), C.c_uint64(self.ws.numel()), C.byref(h))
+        self.h = h
+        self._check(rc, h)
+        self.capacity = capacity
+        self.max_batch = int(cfg["max_batch"])
+        self._ids = np.zeros(self.max_batch, np.uint32)
+        self._tok = np.zeros(self.max_batch, np.uint32)
+        self._rows = np.zeros(self.max_batch, np.uint32)
+        self.n = 0
+
+    def _check(self, rc, h):
+        if rc < 0:
+            msg = self.lib.jit_sched_last_error(h).decode() if h is not None and h.value else "error"
+            raise JitSchedError(f"jitsched error {rc}: {msg}")
+        return rc
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.jit_sched_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ pool
+    def make_pool(self, pool: dict, tasks=None, on_device: bool = False):
+        """Build a jit_pool from numpy arrays (host) or torch CUDA tensors (on_device=True)."""
+        p = jit_pool()
+        keep = []
+        n = len(pool["input_len"])
+        p.n = n
+        p.n_single = int(pool.get("n_single", n))
+        def conv(a, dt):   # torch tensors (device, or pinned host) are passed through as-is
+            return a if (on_device or not isinstance(a, np.ndarray) and hasattr(a, "data_ptr")) else _c(a, dt)
+
+        for k, dt in _POOL_ROWS:
+            a = conv(pool[k], dt)
+            keep.append(a)
+            setattr(p, k, _p(a))
+        if tasks is not None and len(tasks["arrival_ns"]):
+            tmap = {"task_arrival_ns": "arrival_ns", "task_deadline_ns": "deadline_ns"}
+            p.n_tasks = len(tasks["arrival_ns"])
+            for k, dt in _POOL_TASKS:
+                a = conv(tasks[tmap.get(k, k)], dt)
+                keep.append(a)
+                setattr(p, k, _p(a))
+        p.on_device = 1 if on_device else 0
+        return p, keep
+
+    def load(self, pool: dict, tasks=None, on_device: bool = False):
+        p, keep = self.make_pool(pool, tasks, on_device)
+        self._check(self.lib.jit_sched_load(self.h, C.byref(p)), self.h)
+        self.n = p.n
+        return self
+
+    def load_struct(self, p):
+        self._check(self.lib.jit_sched_load(self.h, C.byref(p)), self.h)
+        self.n = p.n
+
+    # ------------------------------------------------------------------ step
+    def step(self, now_ns: int, v_token_ns: int, progress=None) -> dict:
+        si = jit_step_in()
+        si.now_ns = int(now_ns)
+        si.v_token_ns = int(v_token_ns)
+        keep = []
+        if progress is not None:
+            arrs = [_c(progress[k], np.uint32) for k in ("row", "generated", "prefilled", "state")]
+            keep += arrs
+            si.n_progress = len(arrs[0])
+            si.prog_row, si.prog_generated, si.prog_prefilled, si.prog_state = [_p(a) for a in arrs]
+        b = jit_batch()
+        b.capacity = self.max_batch
+        b.ids, b.tokens, b.rows = _p(self._ids), _p(self._tok), _p(self._rows)
+        rc = self._check(self.lib.jit_sched_step(self.h, C.byref(si), C.byref(b)), self.h)
+        return self._batch_dict(rc, b)
+
+    def step_async(self, now_ns: int, v_token_ns: int):
+        self._check(self.lib.jit_sched_step_async(self.h, C.c_int64(now_ns), C.c_int64(v_token_ns)), self.h)
+
+    def fetch(self) -> dict:
+        b = jit_batch()
+        b.capacity = self.max_batch
+        b.ids, b.tokens, b.rows = _p(self._ids), _p(self._tok), _p(self._rows)
+        rc = self._check(self.lib.jit_sched_fetch_batch(self.h, C.byref(b)), self.h)
+        return self._batch_dict(rc, b)
+
+    def _batch_dict(self, rc, b):
+        k = b.n_selected
+        return {"status": rc, "n_pending": b.n_pending, "n_selected": k, "total_tokens": b.total_tokens,
+                "n_candidates": b.n_candidates, "b_star": b.b_star, "n_dropped_now": b.n_dropped, "bp": b.bp,
+                "thr": b.thr, "batch_ids": self._ids[:k].copy(), "batch_tokens": self._tok[:k].copy(),
+                "batch_rows": self._rows[:k].copy()}
+
+    def read_rows(self, debug: bool = True) -> dict:
+        n = self.n
+        out = {"key": np.zeros(n, np.float64), "cost": np.zeros(n, np.uint32), "pending": np.zeros(n, np.uint32),
+               "meta": np.zeros(n, np.uint32), "aux": np.zeros(n, np.uint32)}
+        if debug:
+            out.update(rate=np.zeros(n, np.float64), t_rem=np.zeros(n, np.int64), lhat=np.zeros(n, np.uint32))
+        g = lambda k: _p(out[k]) if k in out else None
+        self._check(self.lib.jit_sched_read_rows(self.h, g("key"), g("rate"), g("t_rem"), g("lhat"), g("cost"),
+                                                 g("pending"), g("meta"), g("aux")), self.h)
+        return out
+
+    def kernel_times(self, slots=None):
+        """slots=k>0 records per-kernel events for up to k steps, 0 disables; with no argument
+        returns the average [score, select, cand, group, total] ms over the recorded steps."""
+        if slots is not None:
+            self._check(self.lib.jit_sched_kernel_times(self.h, C.c_int(int(slots)), None, 0), self.h)
+            return None
+        t = (C.c_float * 5)()
+        self._check(self.lib.jit_sched_kernel_times(self.h, C.c_int(-1), t, 5), self.h)
+        return list(t)
+
+    # ------------------------------------------------------------------ replay
+    def replay(self, traces, specs, rcfg: dict, log_steps: int = 0):
+        """Run len(specs) independent replays; traces: list of trace dicts; specs: list of dicts
+        (trace, load_num, load_den, slo_num, slo_den).  Returns (results list, log array or None)."""
+        torch = _torch()
+        keep = []
+        tarr = (jit_trace * len(traces))()
+        for i, tr in enumerate(traces):
+            for k, dt in _TRACE:
+                a = _c(tr[k], dt)
+                if a.size == 0:
+                    a = np.zeros(1, dt)
+                keep.append(a)
+                setattr(tarr[i], k, _p(a))
+            tarr[i].n_rows = len(tr["input_len"])
+            tarr[i].n_tasks = len(tr["task_arrival_ns"])
+        sp = (jit_replay_spec * len(specs))()
+        for i, s in enumerate(specs):
+            sp[i].trace = int(s.get("trace", 0))
+            for k in ("load_num", "load_den", "slo_num", "slo_den"):
+                setattr(sp[i], k, int(s[k]))
+        rc = jit_replay_cfg()
+        rc.n_steps = int(rcfg["n_steps"])
+        rc.n_replays = len(specs)
+        rc.log_steps = int(log_steps)
+        for k in ("v_token0_ns", "c0_ns", "c_att_ns", "c_lin_ns"):
+            setattr(rc, k, int(rcfg[k]))
+        rc.specs = C.cast(sp, C.c_void_p)
+        nbytes = C.c_uint64()
+        self._check(self.lib.jit_replay_workspace_bytes(C.byref(self.c), tarr, C.c_uint32(len(traces)), C.byref(rc),
+                                                        C.byref(nbytes)), self.h)
+        ws = torch.empty(int(nbytes.value) + 256, dtype=torch.uint8, device=f"cuda:{self.device}")
+        res = (jit_replay_result * len(specs))()
+        log = np.zeros(max(1, len(specs) * log_steps), STEP_LOG_DTYPE) if log_steps else None
+        self._check(self.lib.jit_sched_replay(self.h, tarr, C.c_uint32(len(traces)), C.byref(rc),
+                                              C.c_void_p(ws.data_ptr()), C.c_uint64(ws.numel()), res,
+                                              _p(log) if log is not None else None), self.h)
+        out = []
+        for r in res:
+            out.append({k: getattr(r, k) for k, _ in jit_replay_result._fields_})
+        if log is not None:
+            log = log.reshape(len(specs), log_steps)
+        return out, log
