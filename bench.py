@@ -30,10 +30,10 @@ import workloads as W  # noqa: E402
 
 METRIC = "pending requests scheduled/sec (1M pool)"
 UNIT = "requests/s"
-# algorithmic bytes of k_score: per row 32 B read (arrival 8, input_len, generated,
-# prefilled, cached bound, meta, aux) + 16 B written (8-B key image, cost, aux); per compound
-# task 72 B (call_off 8, arrival 8, deadline 8, stage 4, n_stages 4, pattern 32, goodput_done 8)
-BYTES_ROW, BYTES_TASK = 48, 72
+# algorithmic bytes of k_score: per standalone row 32 B read (arrival 8, input_len,
+# generated, prefilled, cached bound, meta, aux) + 16 B written (8-B key image, cost, aux); per
+# compound call 36 B read (+ task id) + 4 B written (cost); per task 16 B of accumulator updates
+BYTES_ROW, BYTES_CALL, BYTES_TASK = 48, 40, 16
 
 
 def parse():
@@ -178,6 +178,90 @@ def pinned_pool(d):
     return out, tasks
 
 
+def replay_leg(args, ws, rank, dev, stream, barrier, allmax, allsum):
+    """C5(i): the load x SLO-scale sweep of independent replays; replay i -> rank i mod N (no
+    communication; total work fixed, i.e. strong scaling over N)."""
+    import torch
+    from paper_2504_20068_b200 import Scheduler
+    traces = [W.trace_mixed(k) for k in range(4)]
+    sweep = W.c5_sweep(args.replays)
+    specs = [dict(sp, trace=i % len(traces)) for i, sp in enumerate(sweep)]
+    mine = specs[rank::ws]
+    rc = dict(traces[0]["rcfg"], n_steps=args.replay_steps)
+    rs = Scheduler(traces[0]["cfg"], traces[0]["groups"], traces[0]["table"], capacity=64, task_capacity=8,
+                   device=dev, stream=stream)
+    rs.replay([t["trace"] for t in traces], mine[:min(len(mine), 64)], rc)     # warm-up
+    barrier()
+    torch.cuda.synchronize()
+    r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    r0.record(stream)
+    res, _ = rs.replay([t["trace"] for t in traces], mine, rc)
+    r1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    rms = allmax(r0.elapsed_time(r1))
+    steps_done = allsum(float(sum(r["steps"] for r in res)))
+    rs.close()
+    return {"metric": "replayed serving steps/sec", "value": steps_done / (rms / 1e3), "unit": "steps/s",
+            "workload": f"C5(i): {args.replays} replays (64 load x 64 SLO-scale points, 4 base mixed 1:1:1 traces "
+                        f"of 2048 rows), up to {args.replay_steps} steps each, tau 2048, B_max 128",
+            "ms": rms, "steps_total": int(steps_done), "scaling": "strong (fixed sweep, replay i -> rank i mod N)",
+            "goodput_tokens_sum": int(allsum(float(sum(r["token_goodput"] for r in res)))),
+            "gpu_launches": 1}
+
+
+def run_sharded(args, ws, rank, dev, stream, barrier, allmax, allsum):
+    """N > 1: one pool of N x 2^20 requests sharded by request id (each rank owns 2^20 rows;
+    weak scaling); every step is the exact two-round protocol of shard.cuh with NCCL
+    allgathers over NVLink (torch.distributed), identical batch on every rank."""
+    import torch
+    from paper_2504_20068_b200 import Scheduler
+    from paper_2504_20068_b200.sharded import ShardedStep, nccl_allgather
+    d = build_c3(rank, args.rows)
+    d["pool"]["id"] = (d["pool"]["id"].astype(np.uint64) * ws + rank).astype(np.uint32)   # globally unique ids
+    n = len(d["pool"]["input_len"])
+    nt = len(d["tasks"]["arrival_ns"])
+    now, v = d["now_ns"], d["v_token_ns"]
+    cap = max(n, ws * (d["cfg"]["max_batch"] + 1))
+    s = Scheduler(d["cfg"], d["groups"], d["table"], capacity=cap, task_capacity=nt, device=dev, stream=stream)
+    s.load(d["pool"], d["tasks"])
+    st = ShardedStep(s, rank, ws, nccl_allgather())
+    K, Wm = args.steps, max(3, args.warmup)
+    for _ in range(Wm):
+        out = st.step(now, v)
+    barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(dev)
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(K):
+        out = st.step(now, v)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    ms = allmax(e0.elapsed_time(e1) / K)
+    total = allsum(float(n))
+    s.close()
+    replay = None if args.no_replay else replay_leg(args, ws, rank, dev, stream, barrier, allmax, allsum)
+    if rank == 0:
+        line = {"metric": METRIC, "value": total / (ms / 1e3), "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": Wm,
+                "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": f"C5(ii)-shaped: {ws} x 2^20-row shards of one pool (C3 generator), sharded by "
+                                       "request id, tau 8192, B_max 8192", "rows_total": int(total),
+                           "l2": "inputs larger than L2 (2^20 rows x ~100 B workspace per rank plus exchange buffers)",
+                           "parallelism": f"sharded pool, exact 2-round NCCL allgather merge over {ws} ranks",
+                           "last_batch": {"n_selected": out["n_selected"], "b_star": out["b_star"],
+                                          "n_candidates": out["n_candidates"]}},
+                "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": 18 * K, "clocks": clocks,
+                "replay": replay}
+        print(json.dumps(line), flush=True)
+    import torch.distributed as dist
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     ws, rank, local = dist_setup()
@@ -211,6 +295,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
+    if ws > 1:
+        return run_sharded(args, ws, rank, dev, stream, barrier, allmax, allsum)
     # ------------------------------------------------------------------ C3 pool step
     d = build_c3(rank, args.rows)
     n = len(d["pool"]["input_len"])
@@ -218,9 +304,17 @@ def main():
     now, v = d["now_ns"], d["v_token_ns"]
     K, Wm = args.steps, max(3, args.warmup)
     hs = []
+    first_ms = []
     for i in range(args.rot):
         s = Scheduler(d["cfg"], d["groups"], d["table"], capacity=n, task_capacity=nt, device=dev, stream=stream)
         s.load(d["pool"], d["tasks"])
+        # first step after load: every row computes its length bound (cold cache) -- timed apart
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        s.step(now, v)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        first_ms.append(f0.elapsed_time(f1))
         hs.append(s)
     # warm-up (synchronous: validates that every step resolves on the graph's fast path)
     statuses = []
@@ -232,7 +326,20 @@ def main():
         s.kernel_times(slots=K)
     barrier()
     torch.cuda.synchronize()
+    # clocks: the sampler runs through a ~0.6 s soak of the same step loop, the timed block
+    # and a short tail, so that nvidia-smi has samples under this load (B200_PROFILING.md)
     clk = Clocks(dev)
+    t_soak = time.perf_counter() + 0.6
+    j = 0
+    while time.perf_counter() < t_soak:
+        for _ in range(20):
+            hs[j % args.rot].step_async(now, v)
+            j += 1
+        torch.cuda.synchronize()
+    for s in hs:
+        s.kernel_times(slots=K)            # restart the per-step event slots for the timed block
+    barrier()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for k in range(K):
@@ -240,6 +347,11 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
+    for _ in range(3):
+        for k in range(20):
+            hs[k % args.rot].step_async(now, v)
+        torch.cuda.synchronize()
+        time.sleep(0.1)
     clocks = clk.stop()
     ms = e0.elapsed_time(e1) / K
     ms_max = allmax(ms)
@@ -256,7 +368,8 @@ def main():
     kt /= K
     total_rows = allsum(float(n))
     value = total_rows / (ms_max / 1e3)
-    alg_bytes = n * BYTES_ROW + nt * BYTES_TASK
+    n_single = int(d["pool"]["n_single"])
+    alg_bytes = n_single * BYTES_ROW + (n - n_single) * BYTES_CALL + nt * BYTES_TASK
     pk = peaks()
     hbm_peak = pk["hbm_gbs"] if pk else 6650.0
     achieved = alg_bytes / (kt[0] / 1e3) / 1e9
@@ -264,8 +377,10 @@ def main():
                 "frac": achieved / hbm_peak, "traffic": None,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if pk else "fallback 6650 GB/s",
                 "alg_bytes_per_launch": alg_bytes, "k_score_ms": kt[0],
-                "kernel_ms": {"score": kt[0], "select": kt[1], "candidates": kt[2], "group": kt[3], "chain": kt[4]},
-                "frac_of_8tbs_datasheet": achieved / 8000.0}
+                "kernel_ms": {"k_score": kt[0], "k_ckey": kt[1], "k_spec_window": kt[2], "fallback_body": kt[3],
+                              "chain": kt[4]},
+                "frac_of_8tbs_datasheet": achieved / 8000.0,
+                "first_step_after_load_ms": float(np.median(first_ms))}
 
     # ------------------------------------------------------------------ e2e through the C ABI
     e2e = None
@@ -296,33 +411,7 @@ def main():
     for s in hs:
         s.close()
 
-    # ------------------------------------------------------------------ C5(i) replay sweep
-    replay = None
-    if not args.no_replay:
-        traces = [W.trace_mixed(k) for k in range(4)]
-        sweep = W.c5_sweep(args.replays)
-        specs = [dict(sp, trace=i % len(traces)) for i, sp in enumerate(sweep)]
-        mine = specs[rank::ws]
-        rc = dict(traces[0]["rcfg"], n_steps=args.replay_steps)
-        rs = Scheduler(traces[0]["cfg"], traces[0]["groups"], traces[0]["table"], capacity=64, task_capacity=8,
-                       device=dev, stream=stream)
-        rs.replay([t["trace"] for t in traces], mine[:min(len(mine), 64)], rc)     # warm-up
-        barrier()
-        torch.cuda.synchronize()
-        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        r0.record(stream)
-        res, _ = rs.replay([t["trace"] for t in traces], mine, rc)
-        r1.record(stream)
-        torch.cuda.synchronize()
-        barrier()
-        rms = allmax(r0.elapsed_time(r1))
-        steps_done = allsum(float(sum(r["steps"] for r in res)))
-        replay = {"metric": "replayed serving steps/sec", "value": steps_done / (rms / 1e3), "unit": "steps/s",
-                  "workload": f"C5(i): {args.replays} replays (64 load x 64 SLO-scale points, 4 base mixed 1:1:1 traces "
-                              f"of 2048 rows), up to {args.replay_steps} steps each, tau 2048, B_max 128",
-                  "ms": rms, "steps_total": int(steps_done), "scaling": "weak" if ws > 1 else None,
-                  "goodput_tokens_sum": int(allsum(float(sum(r["token_goodput"] for r in res))))}
-        rs.close()
+    replay = None if args.no_replay else replay_leg(args, ws, rank, dev, stream, barrier, allmax, allsum)
 
     # ------------------------------------------------------------------ CPU oracle baseline
     cpu = None

@@ -59,6 +59,8 @@ enum { JIT_F_EVER = 1, JIT_F_COMPOUND = 2, JIT_F_OVERRIDE = 4 };
 #define JIT_MAX_STAGES 8
 /* jit_config.flags */
 #define JIT_CFG_DEBUG_ROWS 1u   /* keep per-row rate / t_rem / Lhat / cost for jit_sched_read_rows */
+#define JIT_CFG_NO_GRAPH 2u     /* launch the step's kernels directly instead of one CUDA graph
+                                   (profilers cannot look inside graphs with conditional nodes) */
 
 /* One SLO group (a row of the SLO table; reading A35).  Times are int64 ns.
  * LAT uses ttft/tbt, DDL e2el, CMP e2el per stage (D = e2el * stages), BE be_deadline.
@@ -142,6 +144,8 @@ typedef struct jit_step_in {
 typedef struct jit_batch {
     uint32_t capacity;
     uint32_t n_selected, total_tokens, n_candidates, b_star, n_pending, n_dropped, status;
+    uint32_t n_refresh;            /* length bounds recomputed this step (the rest hit the cache) */
+    uint32_t fallback, reserved;   /* 1: the exact radix path ran instead of the speculative set */
     double bp, thr;                /* batch priority and cutoff threshold fl(p * bp) */
     uint32_t* ids;
     uint32_t* tokens;

@@ -6,10 +6,12 @@
 #include <new>
 #include <string>
 #include <vector>
+#include <cstdlib>
 
 #include "jit_sched.h"
 #include "common.cuh"
-#include "pool.cuh"
+#include "select.cuh"
+#include "score.cuh"
 #include "replay.cuh"
 #include "shard.cuh"
 
@@ -30,11 +32,13 @@ struct jit_sched {
     uint32_t* d_stage = nullptr;      // progress staging (4 * capacity)
     cudaStream_t stream = nullptr;    // caller's stream
     cudaStream_t cap = nullptr;       // private capture stream
+    cudaStream_t cap2 = nullptr;      // capture stream of the conditional body
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     cudaGraphNode_t begin_node = nullptr;
     cudaKernelNodeParams begin_params{};
-    void* begin_args[5];
+    void* begin_args[7];
+    uint32_t arg_ntasks = 0;
     int64_t arg_now = 0, arg_v = 0;
     bool loaded = false, graph_dirty = true, timing = false, debug = false;
     cudaEvent_t ev[6] = {};
@@ -42,7 +46,7 @@ struct jit_sched {
     std::vector<cudaEvent_t> slots;       // 5 events per recorded step
     uint32_t n_slots = 0, slot_used = 0;
     int n_sm = 148;
-    uint32_t nb_rows = 1, nb_tasks = 0, grid_pass = 1;
+    uint32_t nb_score = 1, nb_ckey = 1, grid_pass = 1;
     std::string err;
 };
 
@@ -102,10 +106,16 @@ static void carve(Carve& cv, const jit_config* cfg, const jit_len_table* tab, Po
     uint64_t P2 = 1;                       // bitonic sorts pad |Cd| to a power of two
     while (P2 < N) P2 <<= 1;
     S.cand = cv.take<uint32_t>(N); S.sk = cv.take<uint64_t>(P2); S.sv = cv.take<uint32_t>(P2);
-    S.pc = cv.take<unsigned long long>(N + 1); S.pf = cv.take<u128>(N + 1);
+    S.pc = cv.take<unsigned long long>(N + 1);
+    S.pf = cv.take<u128>(P2 + 1);          // also the u128 sort keys of the shard merge (pow2 slots)
     S.out_ids = cv.take<uint32_t>(cfg->max_batch + 1); S.out_tokens = cv.take<uint32_t>(cfg->max_batch + 1);
     S.out_rows = cv.take<uint32_t>(cfg->max_batch + 1);
     S.cand_cap = (uint32_t)N;
+    S.spec_ck = cv.take<u128>(kSpecCap); S.spec_row = cv.take<uint32_t>(kSpecCap);
+    S.persist = cv.take<Persist>(1);
+    S.part = cv.take<BlockPart>(kMaxParts); S.part2 = cv.take<BlockPart>(kMaxParts);
+    S.tacc = cv.take<TaskAcc>(NT);
+    S.task_cap = (uint32_t)NT;
     ctrl = cv.take<Ctrl>(1);
     stage = cv.take<uint32_t>(4 * N);
 }
@@ -168,6 +178,7 @@ extern "C" int jit_sched_init(const jit_config* cfg, const jit_slo_group* groups
     CK(cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, cfg->device));
     h->stream = (cudaStream_t)cfg->stream;
     CK(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&h->cap2, cudaStreamNonBlocking));
     Carve cv;
     cv.base = reinterpret_cast<unsigned char*>(((uintptr_t)dev_workspace + 255) & ~(uintptr_t)255);
     carve(cv, cfg, table, h->P, h->S, h->T, h->d_groups, h->d_ctrl, h->d_stage);
@@ -178,6 +189,8 @@ extern "C" int jit_sched_init(const jit_config* cfg, const jit_slo_group* groups
     c.R = cfg->refine_interval; c.frame = cfg->frame_steps; c.qn = cfg->q_num; c.qd = cfg->q_den;
     c.pn = cfg->p_num; c.pd = cfg->p_den; c.delta = cfg->delta_starve; c.len_key = cfg->len_key;
     c.appb = cfg->appb_filter; c.eps = cfg->eps_ns; c.waiting = cfg->waiting_ns;
+    fastdiv_magic(c.R, &c.R_m, &c.R_l);
+    fastdiv_magic(c.frame, &c.F_m, &c.F_l);
     CK(cudaMemcpyAsync((void*)h->T.edges, table->edges, 4ull * table->n_bins, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemcpyAsync((void*)h->T.cum, table->cum, 4ull * table->n_rows * table->n_bins, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemcpyAsync(h->d_groups, groups, sizeof(Group) * n_groups, cudaMemcpyHostToDevice, h->stream));
@@ -185,6 +198,23 @@ extern "C" int jit_sched_init(const jit_config* cfg, const jit_slo_group* groups
     for (auto& e : h->ev) CK(cudaEventCreate(&e));
     CK(cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)((sizeof(u128) + 4) * kBucketCap)));
     CK(cudaFuncSetAttribute(k_group, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(12 * kGroupSmemSort)));
+    CK(cudaFuncSetAttribute(k_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)((sizeof(u128) + 4) * kSpecCap)));
+    CK(cudaFuncSetAttribute(k_group_rec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(12 * kGroupSmemSort)));
+    // one shared-memory carveout for every kernel of the step: switching the L1/shared split
+    // between consecutive kernels costs a drain + reconfiguration of the SMs (several µs each)
+    {
+        const void* ks[] = {(const void*)k_begin, (const void*)k_score<false>, (const void*)k_score<true>,
+                            (const void*)k_ckey<false>, (const void*)k_ckey<true>, (const void*)k_spec,
+                            (const void*)k_hist0, (const void*)k_pass, (const void*)k_compact, (const void*)k_resolve,
+                            (const void*)k_cand, (const void*)k_group};
+        for (const void* k : ks)
+            CK(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+    }
+    {
+        Persist ps{};
+        ps.t_guess = kNone;                 // no speculation before the first resolved step
+        CK(cudaMemcpyAsync(h->S.persist, &ps, sizeof ps, cudaMemcpyHostToDevice, h->stream));
+    }
     CK(cudaStreamSynchronize(h->stream));
     return JIT_OK;
 }
@@ -227,7 +257,7 @@ extern "C" int jit_sched_load(jit_sched* h, const jit_pool* p) {
     const bool same_shape = h->loaded && P.n == p->n && P.n_single == p->n_single && P.n_tasks == p->n_tasks;
     P.n = p->n; P.n_single = p->n_single; P.n_tasks = p->n_tasks;
     // validate on the device (also covers device-resident pools)
-    k_begin<<<1, 32, 0, h->stream>>>(h->d_ctrl, h->S.hcnt, h->S.hcost, 0, 1);
+    k_begin<<<1, 32, 0, h->stream>>>(h->d_ctrl, h->S.hcnt, h->S.hcost, 0, 1, h->S.tacc, 0);
     const uint32_t vb = (uint32_t)std::min<uint64_t>((n + 255) / 256 + 1, (uint64_t)h->n_sm * 8);
     k_validate<<<vb, 256, 0, h->stream>>>(P, h->d_groups, h->n_groups, h->T.n_rows, h->d_ctrl);
     CK(cudaGetLastError());
@@ -235,9 +265,14 @@ extern "C" int jit_sched_load(jit_sched* h, const jit_pool* p) {
     CK(cudaStreamSynchronize(h->stream));
     if (h->h_ctrl->error) { h->loaded = false; return set_err(h, JIT_EINVAL, "invalid pool (layout / ranges / groups)"); }
     // launch geometry
-    const uint32_t nq = (P.n_single + 3) / 4;
-    h->nb_rows = std::max<uint32_t>(1, std::min<uint32_t>((nq + kScoreThreads - 1) / kScoreThreads, (uint32_t)h->n_sm * 8));
-    h->nb_tasks = P.n_tasks ? std::min<uint32_t>((P.n_tasks + 7) / 8, (uint32_t)h->n_sm * 8) : 0;
+    // rows: grid-stride over a persistent-style grid (6 CTAs of 256 per SM); tasks: warp per task
+    h->nb_score = std::max<uint32_t>(1, std::min<uint32_t>((P.n + kScoreThreads - 1) / kScoreThreads, (uint32_t)h->n_sm * 6));
+    h->nb_ckey = std::max<uint32_t>(1, std::min<uint32_t>((P.n - P.n_single + kScoreThreads - 1) / kScoreThreads,
+                                                          (uint32_t)h->n_sm * 4));
+    h->nb_score = std::min(h->nb_score, kMaxParts);
+    h->nb_ckey = std::min(h->nb_ckey, kMaxParts);
+    h->S.n_part = h->nb_score; h->S.n_part2 = h->nb_ckey;
+    h->arg_ntasks = P.n_tasks;
     h->grid_pass = std::max<uint32_t>(1, std::min<uint32_t>((P.n + kPassThreads - 1) / kPassThreads, (uint32_t)h->n_sm * 4));
     if (!same_shape) h->graph_dirty = true;
     h->loaded = true;
@@ -247,71 +282,145 @@ extern "C" int jit_sched_load(jit_sched* h, const jit_pool* p) {
 // ------------------------------------------------------------------------------------------
 // step
 // ------------------------------------------------------------------------------------------
-static void enqueue_chain(jit_sched* h, cudaStream_t s, int64_t now, int64_t v, bool with_events, bool with_begin,
-                          uint32_t first_pass, uint32_t n_passes) {
+static void enqueue_score(jit_sched* h, cudaStream_t s, int64_t now, int64_t v, cudaEvent_t mid = nullptr,
+                          bool capturing = false) {
     Pool& P = h->P;
     Scratch& S = h->S;
-    if (with_begin) k_begin<<<4, 1024, 0, s>>>(h->d_ctrl, S.hcnt, S.hcost, now, v);
-    if (with_events) cudaEventRecordWithFlags(h->ev[0], s, cudaEventRecordExternal);
-    if (with_begin) {
-        const uint32_t grid = h->nb_rows + h->nb_tasks;
-        if (h->debug) k_score<true><<<grid, kScoreThreads, 0, s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S.hcnt, S.hcost, h->nb_rows);
-        else k_score<false><<<grid, kScoreThreads, 0, s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S.hcnt, S.hcost, h->nb_rows);
-    }
-    if (with_events) cudaEventRecordWithFlags(h->ev[1], s, cudaEventRecordExternal);
+    if (h->debug) k_score<true><<<h->nb_score, kScoreThreads, 0, s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S);
+    else k_score<false><<<h->nb_score, kScoreThreads, 0, s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S);
+    if (mid) cudaEventRecordWithFlags(mid, s, capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
+    if (h->debug) k_ckey<true><<<h->nb_ckey, kScoreThreads, 0, s>>>(P, h->c, h->d_ctrl, S);
+    else k_ckey<false><<<h->nb_ckey, kScoreThreads, 0, s>>>(P, h->c, h->d_ctrl, S);
+    (void)now; (void)v;
+}
+
+// radix-select path (level-0 histogram .. candidates); k_hist0 runs when forced or when the
+// speculative resolve fell back; k_pass runs only while the boundary bucket is too large
+static void enqueue_radix(jit_sched* h, cudaStream_t s, int force_hist0, uint32_t first_pass, uint32_t n_passes,
+                          int only_after_fallback) {
+    Pool& P = h->P;
+    Scratch& S = h->S;
+    if (force_hist0 >= 0) k_hist0<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->c, h->d_ctrl, S.hcnt, S.hcost, force_hist0);
     for (uint32_t i = 0; i < n_passes; ++i)
         k_pass<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->c, h->d_ctrl, S.hcnt, S.hcost, first_pass + i);
     k_compact<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->d_ctrl, S);
     k_resolve<<<1, 1024, (sizeof(u128) + 4) * kBucketCap, s>>>(h->c, h->d_ctrl, S);
-    if (with_events) cudaEventRecordWithFlags(h->ev[2], s, cudaEventRecordExternal);
-    k_cand<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->d_ctrl, S);
-    if (with_events) cudaEventRecordWithFlags(h->ev[3], s, cudaEventRecordExternal);
-    k_group<<<1, 1024, 12 * kGroupSmemSort, s>>>(P, h->c, h->d_ctrl, S);
-    if (with_events) cudaEventRecordWithFlags(h->ev[4], s, cudaEventRecordExternal);
-    cudaMemcpyAsync(h->h_ctrl, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s);
+    k_cand<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->d_ctrl, S, only_after_fallback);
 }
 
+static void enqueue_tail(jit_sched* h, cudaStream_t s) {
+    k_group<<<1, 1024, 12 * kGroupSmemSort, s>>>(h->P, h->c, h->d_ctrl, h->S);
+}
+
+// Step graph:  k_begin -> k_score -> k_spec -> IF(fallback){k_hist0 -> k_pass -> k_compact ->
+// k_resolve -> k_cand} -> k_group -> D2H(ctrl).  The IF is a device-side conditional node set
+// by k_spec (cudaGraphSetConditional), so the common case runs 4 kernels and no host logic.
 static int build_graph(jit_sched* h) {
     if (h->exec) { cudaGraphExecDestroy(h->exec); h->exec = nullptr; }
     if (h->graph) { cudaGraphDestroy(h->graph); h->graph = nullptr; }
     cudaGraph_t g;
-    CK(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
-    enqueue_chain(h, h->cap, 0, 1, h->timing, true, 0, 1);
-    CK(cudaStreamEndCapture(h->cap, &g));
+    cudaStream_t s = h->cap;
+    Scratch& S = h->S;
+    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t cg;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &cg, &deps, &nd));
+    const bool flat = getenv("JITSCHED_FLAT_GRAPH") != nullptr;   // A/B switch: no conditional node
+    cudaGraphConditionalHandle hc = 0;
+    if (!flat) CK(cudaGraphConditionalHandleCreate(&hc, cg, 0, cudaGraphCondAssignDefault));
+    k_begin<<<4, 1024, 0, s>>>(h->d_ctrl, S.hcnt, S.hcost, 0, 1, S.tacc, h->arg_ntasks);
+    if (h->timing) cudaEventRecordWithFlags(h->ev[0], s, cudaEventRecordExternal);
+    enqueue_score(h, s, 0, 1, h->timing ? h->ev[1] : nullptr, true);
+    if (h->timing) cudaEventRecordWithFlags(h->ev[2], s, cudaEventRecordExternal);
+    k_spec<<<1, kSpecThreads, (sizeof(u128) + 4) * kSpecCap, s>>>(h->P, h->c, h->d_ctrl, S, hc, flat ? 0 : 1, 0);
+    if (h->timing) cudaEventRecordWithFlags(h->ev[3], s, cudaEventRecordExternal);
+    if (flat) {
+        enqueue_radix(h, s, 0, 0, 1, 1);      // every kernel checks the status and exits when idle
+        enqueue_tail(h, s);
+    } else {
+        CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &cg, &deps, &nd));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = hc;
+        cp.conditional.type = cudaGraphCondTypeIf;
+        cp.conditional.size = 1;
+        cudaGraphNode_t cnode;
+        CK(cudaGraphAddNode(&cnode, cg, deps, nd, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        CK(cudaStreamBeginCaptureToGraph(h->cap2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        enqueue_radix(h, h->cap2, 0, 0, 1, 1);
+        enqueue_tail(h, h->cap2);
+        CK(cudaStreamEndCapture(h->cap2, nullptr));
+        CK(cudaStreamUpdateCaptureDependencies(s, &cnode, 1, cudaStreamSetCaptureDependencies));
+    }
+    if (h->timing) cudaEventRecordWithFlags(h->ev[4], s, cudaEventRecordExternal);
+    cudaMemcpyAsync(h->h_ctrl, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s);
+    CK(cudaStreamEndCapture(s, &g));
     size_t nn = 0;
     CK(cudaGraphGetNodes(g, nullptr, &nn));
     std::vector<cudaGraphNode_t> nodes(nn);
     CK(cudaGraphGetNodes(g, nodes.data(), &nn));
+    // locate the k_begin kernel node and the timing event nodes; the query of the conditional
+    // node's type can fail with this runtime/driver pair -- such nodes are skipped and the
+    // error state they leave behind is cleared
     h->begin_node = nullptr;
-    for (auto nd : nodes) {
-        cudaGraphNodeType ty;
-        cudaGraphNodeGetType(nd, &ty);
-        if (ty != cudaGraphNodeTypeKernel) continue;
-        cudaKernelNodeParams kp;
-        cudaGraphKernelNodeGetParams(nd, &kp);
-        if (kp.func == (void*)k_begin) { h->begin_node = nd; h->begin_params = kp; break; }
-    }
-    if (!h->begin_node) { cudaGraphDestroy(g); return set_err(h, JIT_ECUDA, "graph: k_begin node not found"); }
     for (auto& e : h->ev_node) e = nullptr;
     for (auto nd : nodes) {
         cudaGraphNodeType ty;
-        cudaGraphNodeGetType(nd, &ty);
-        if (ty != cudaGraphNodeTypeEventRecord) continue;
-        cudaEvent_t e;
-        cudaGraphEventRecordNodeGetEvent(nd, &e);
-        for (int i = 0; i < 5; ++i) if (e == h->ev[i]) h->ev_node[i] = nd;
+        if (cudaGraphNodeGetType(nd, &ty) != cudaSuccess) { (void)cudaGetLastError(); continue; }
+        if (ty == cudaGraphNodeTypeKernel && !h->begin_node) {
+            cudaKernelNodeParams kp;
+            if (cudaGraphKernelNodeGetParams(nd, &kp) != cudaSuccess) { (void)cudaGetLastError(); continue; }
+            if (kp.func == (void*)k_begin) { h->begin_node = nd; h->begin_params = kp; }
+        } else if (ty == cudaGraphNodeTypeEventRecord) {
+            cudaEvent_t e;
+            if (cudaGraphEventRecordNodeGetEvent(nd, &e) != cudaSuccess) { (void)cudaGetLastError(); continue; }
+            for (int i = 0; i < 5; ++i) if (e == h->ev[i]) h->ev_node[i] = nd;
+        }
     }
+    (void)cudaGetLastError();
+    if (!h->begin_node) { cudaGraphDestroy(g); return set_err(h, JIT_ECUDA, "graph: k_begin node not found"); }
     h->graph = g;                      // kept alive: begin_node belongs to it
     CK(cudaGraphInstantiate(&h->exec, g, 0));
     h->graph_dirty = false;
     return JIT_OK;
 }
 
+// JIT_CFG_NO_GRAPH: the same chain as direct launches (profilers cannot look inside graphs
+// that hold conditional nodes); every fallback kernel checks the status itself.
+static int launch_direct(jit_sched* h, int64_t now, int64_t v) {
+    cudaStream_t s = h->stream;
+    const bool ev = h->timing && h->n_slots;
+    cudaEvent_t* e = ev ? &h->slots[5 * (h->slot_used % h->n_slots)] : nullptr;
+    if (ev) h->slot_used++;
+    k_begin<<<4, 1024, 0, s>>>(h->d_ctrl, h->S.hcnt, h->S.hcost, now, v, h->S.tacc, h->arg_ntasks);
+    if (ev) cudaEventRecord(e[0], s);
+    enqueue_score(h, s, now, v, ev ? e[1] : nullptr, false);
+    if (ev) cudaEventRecord(e[2], s);
+    k_spec<<<1, kSpecThreads, (sizeof(u128) + 4) * kSpecCap, s>>>(h->P, h->c, h->d_ctrl, h->S, 0, 0, 0);
+    if (ev) cudaEventRecord(e[3], s);
+    enqueue_radix(h, s, 0, 0, 1, 1);
+    enqueue_tail(h, s);
+    if (ev) cudaEventRecord(e[4], s);
+    cudaMemcpyAsync(h->h_ctrl, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s);
+    CK(cudaGetLastError());
+    return JIT_OK;
+}
+
 static int launch_step(jit_sched* h, int64_t now, int64_t v) {
-    if (h->graph_dirty) { int rc = build_graph(h); if (rc) return rc; }
+    if (h->cfg.flags & JIT_CFG_NO_GRAPH) return launch_direct(h, now, v);
+    if (h->graph_dirty) {
+        CK(cudaGetLastError());
+        int rc = build_graph(h);
+        if (rc) return rc;
+        CK(cudaGetLastError());
+    }
     h->arg_now = now; h->arg_v = v;
     h->begin_args[0] = &h->d_ctrl; h->begin_args[1] = &h->S.hcnt; h->begin_args[2] = &h->S.hcost;
     h->begin_args[3] = &h->arg_now; h->begin_args[4] = &h->arg_v;
+    h->begin_args[5] = &h->S.tacc; h->begin_args[6] = &h->arg_ntasks;
     cudaKernelNodeParams kp = h->begin_params;
     kp.kernelParams = h->begin_args;
     kp.extra = nullptr;
@@ -323,16 +432,21 @@ static int launch_step(jit_sched* h, int64_t now, int64_t v) {
             if (h->ev_node[i]) CK(cudaGraphExecEventRecordNodeSetEvent(h->exec, h->ev_node[i], h->slots[5 * slot + i]));
         h->slot_used++;
     }
+    CK(cudaGetLastError());
     CK(cudaGraphLaunch(h->exec, h->stream));
+    CK(cudaGetLastError());
     return JIT_OK;
 }
 
 static int finish_step(jit_sched* h, jit_batch* out) {
     CK(cudaStreamSynchronize(h->stream));
+    CK(cudaGetLastError());
     if (h->h_ctrl->status == ST_HIST) {
         // rare: the boundary bucket stayed large after the graph's passes (heavy key ties);
         // finish the radix select with the remaining digits outside the graph
-        enqueue_chain(h, h->stream, 0, 0, false, false, 1, kLevels - 1);
+        enqueue_radix(h, h->stream, -1, 1, kLevels - 1, 0);
+        enqueue_tail(h, h->stream);
+        cudaMemcpyAsync(h->h_ctrl, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(h->stream));
     }
@@ -340,6 +454,7 @@ static int finish_step(jit_sched* h, jit_batch* out) {
     if (c.status == ST_ERROR || c.error) return set_err(h, JIT_EINVAL, "step: invalid input (error code %u)", c.error);
     if (out) {
         out->n_pending = c.n_pending; out->n_dropped = c.n_dropped; out->status = c.status;
+        out->n_refresh = c.n_refresh; out->fallback = c.fallback;
         out->n_selected = 0; out->total_tokens = 0; out->n_candidates = 0; out->b_star = 0; out->bp = 0; out->thr = 0;
     }
     if (c.status == ST_EMPTY) return JIT_EMPTY;
@@ -420,7 +535,7 @@ extern "C" int jit_sched_read_rows(jit_sched* h, double* key, double* rate, int6
 extern "C" int jit_sched_kernel_times(jit_sched* h, int enable, float* ms_out, uint32_t n_out) {
     // enable > 0: record per-kernel events for up to `enable` steps (ring of event slots);
     // enable = 0: off; enable < 0: leave as is.  ms_out gets the AVERAGE over the recorded
-    // steps of [k_score, radix select (passes+compact+resolve), k_cand, k_group, whole chain].
+    // steps of [k_score, k_ckey, k_spec (+ in-CTA window), fallback body (radix path + k_group), chain].
     if (!h) return JIT_EINVAL;
     if (enable >= 0) {
         CK(cudaStreamSynchronize(h->stream));
@@ -442,9 +557,9 @@ extern "C" int jit_sched_kernel_times(jit_sched* h, int enable, float* ms_out, u
             cudaEvent_t* e = &h->slots[5 * k];
             float t;
             CK(cudaEventElapsedTime(&t, e[0], e[1])); acc[0] += t;   // k_score
-            CK(cudaEventElapsedTime(&t, e[1], e[2])); acc[1] += t;   // radix select passes + resolve
-            CK(cudaEventElapsedTime(&t, e[2], e[3])); acc[2] += t;   // candidates
-            CK(cudaEventElapsedTime(&t, e[3], e[4])); acc[3] += t;   // group
+            CK(cudaEventElapsedTime(&t, e[1], e[2])); acc[1] += t;   // k_ckey
+            CK(cudaEventElapsedTime(&t, e[2], e[3])); acc[2] += t;   // k_spec + window
+            CK(cudaEventElapsedTime(&t, e[3], e[4])); acc[3] += t;   // conditional fallback body
             CK(cudaEventElapsedTime(&t, e[0], e[4])); acc[4] += t;   // total
         }
         for (uint32_t i = 0; i < n_out && i < 5; ++i) ms_out[i] = (float)(acc[i] / ns);
@@ -457,6 +572,7 @@ extern "C" void jit_sched_destroy(jit_sched* h) {
     if (h->exec) cudaGraphExecDestroy(h->exec);
     if (h->graph) cudaGraphDestroy(h->graph);
     if (h->cap) cudaStreamDestroy(h->cap);
+    if (h->cap2) cudaStreamDestroy(h->cap2);
     if (h->h_ctrl) cudaFreeHost(h->h_ctrl);
     for (auto e : h->ev) if (e) cudaEventDestroy(e);
     for (auto e : h->slots) cudaEventDestroy(e);
@@ -486,10 +602,12 @@ extern "C" int jit_shard_prefix(jit_sched* h, int64_t now_ns, int64_t v_token_ns
     cudaStream_t s = h->stream;
     Pool& P = h->P;
     Scratch& S = h->S;
-    k_begin<<<4, 1024, 0, s>>>(h->d_ctrl, S.hcnt, S.hcost, now_ns, v_token_ns);
-    const uint32_t grid = h->nb_rows + h->nb_tasks;
-    if (h->debug) k_score<true><<<grid, kScoreThreads, 0, s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S.hcnt, S.hcost, h->nb_rows);
-    else k_score<false><<<grid, kScoreThreads, 0, s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S.hcnt, S.hcost, h->nb_rows);
+    k_begin<<<4, 1024, 0, s>>>(h->d_ctrl, S.hcnt, S.hcost, now_ns, v_token_ns, S.tacc, h->arg_ntasks);
+    enqueue_score(h, s, now_ns, v_token_ns);
+    // k_spec reduces the scoring partials (n_pending, min key, ...); its speculative result is
+    // then superseded by the forced radix resolve below, which the round-1 export needs
+    k_spec<<<1, kSpecThreads, (sizeof(u128) + 4) * kSpecCap, s>>>(P, h->c, h->d_ctrl, S, 0, 0, 1);
+    k_hist0<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->c, h->d_ctrl, S.hcnt, S.hcost, 1);
     for (uint32_t i = 0; i < kLevels - 1; ++i)
         k_pass<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->c, h->d_ctrl, S.hcnt, S.hcost, i);
     k_compact<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->d_ctrl, S);
@@ -510,7 +628,9 @@ extern "C" int jit_shard_merge(jit_sched* h, const void* d_all_rec1, uint32_t n_
     uint64_t n2 = 1;
     while (n2 < n_all) n2 <<= 1;
     const uint64_t N = ((uint64_t)h->cfg.capacity + 63) & ~63ull;
-    if (n2 > kMergeSmem && n2 > N) return set_err(h, JIT_ECAPACITY, "merge of %u records exceeds the workspace", n_all);
+    uint64_t P2 = 1;
+    while (P2 < N) P2 <<= 1;
+    if (n2 > kMergeSmem && n2 > P2) return set_err(h, JIT_ECAPACITY, "merge of %u records exceeds the workspace", n_all);
     const uint32_t smem = (uint32_t)((sizeof(u128) + 4) * kMergeSmem);
     CK(cudaFuncSetAttribute(k_merge1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_merge1<<<1, 1024, smem, h->stream>>>(h->c, h->d_ctrl, (const Rec1*)d_all_rec1, n_all, h->S.pf, h->S.sv, kMergeSmem);
@@ -521,7 +641,7 @@ extern "C" int jit_shard_merge(jit_sched* h, const void* d_all_rec1, uint32_t n_
 extern "C" int jit_shard_candidates(jit_sched* h, void* d_rec2, uint32_t cap, uint32_t rank, uint32_t* n_out) {
     if (!h || !n_out) return JIT_EINVAL;
     cudaStream_t s = h->stream;
-    k_cand<<<h->grid_pass, kPassThreads, 0, s>>>(h->P, h->d_ctrl, h->S);
+    k_cand<<<h->grid_pass, kPassThreads, 0, s>>>(h->P, h->d_ctrl, h->S, 0);
     k_export2<<<h->grid_pass, 256, 0, s>>>(h->P, h->c, h->d_ctrl, h->S, (Rec2*)d_rec2, cap, rank);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(h->h_ctrl, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
@@ -540,9 +660,10 @@ extern "C" int jit_shard_finish(jit_sched* h, const void* d_all_rec2, uint32_t n
     uint64_t n2 = 1;
     while (n2 < n_all) n2 <<= 1;
     const uint64_t N = ((uint64_t)h->cfg.capacity + 63) & ~63ull;
-    if (n2 > kGroupSmemSort && n_all > N) return set_err(h, JIT_ECAPACITY, "window over %u records exceeds the workspace", n_all);
+    if (n_all > N) return set_err(h, JIT_ECAPACITY, "window over %u records exceeds the workspace", n_all);
     if (h->h_ctrl->status == ST_EMPTY) { if (out) { out->n_selected = 0; out->status = ST_EMPTY; } return JIT_EMPTY; }
     k_group_rec<<<1, 1024, 12 * kGroupSmemSort, s>>>(h->P, h->c, h->d_ctrl, h->S, (const Rec2*)d_all_rec2, n_all, rank);
     CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h->h_ctrl, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
     return finish_step(h, out);
 }

@@ -10,7 +10,7 @@
 // latencies).  Integer sums are order independent, so results are deterministic.
 #pragma once
 #include "common.cuh"
-#include "pool.cuh"
+#include "select.cuh"
 
 namespace jit {
 
@@ -95,7 +95,8 @@ __device__ __forceinline__ uint64_t call_R(const Group& g, uint32_t L_i, uint32_
 __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     Group* sg = reinterpret_cast<Group*>(smem);                                   // 256 groups
-    unsigned char* sbuf = smem + sizeof(Group) * 256;
+    GroupFast* sgf = reinterpret_cast<GroupFast*>(smem + sizeof(Group) * 256);   // their scoring form
+    unsigned char* sbuf = smem + (sizeof(Group) + sizeof(GroupFast)) * 256;
     // region A (24 cap + 64 B): pending sort (u128 key + u32 row), later reused for the
     // window prefix sums (u64 cost + u128 fixed-point key); region B: Cd sort (u64 + u32)
     u128* sA = reinterpret_cast<u128*>(sbuf);
@@ -151,6 +152,7 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
             G.e2el_ns = scale_t(G.e2el_ns, sp.slo_num, sp.slo_den);
             G.be_deadline_ns = scale_t(G.be_deadline_ns, sp.slo_num, sp.slo_den);
             sg[g] = G;
+            sgf[g] = make_fast(G);
         }
         if (threadIdx.x == 0) {
             s_good = 0; s_tok = 0; s_reqg = 0; s_done = 0; s_drop = 0; s_tdone = 0; s_err = 0;
@@ -225,7 +227,7 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                 const uint32_t meta = S.meta[r];
                 if (m_flags(meta) & kCompound) continue;
                 RowRes o;
-                score_standalone<false>(c, T, sg, A.n_groups, ovr, r, now, v, S.arr[r], L_in[r], S.gen[r], S.pre[r],
+                score_standalone<false>(c, T, sgf, A.n_groups, ovr, r, now, v, S.arr[r], L_in[r], S.gen[r], S.pre[r],
                                         S.lhat[r], meta, S.aux[r], o);
                 S.img[r] = o.img; S.cost[r] = o.cost; S.aux[r] = o.aux;
                 if (o.w_meta) S.meta[r] = o.meta;
@@ -508,6 +510,8 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
     }
 }
 
-inline uint32_t replay_smem_bytes() { return (uint32_t)(sizeof(Group) * 256 + 36 * kReplaySmemRows + 64); }
+inline uint32_t replay_smem_bytes() {
+    return (uint32_t)((sizeof(Group) + sizeof(GroupFast)) * 256 + 36 * kReplaySmemRows + 64);
+}
 
 }  // namespace jit

@@ -1,0 +1,367 @@
+// score.cuh -- the streaming pass over the pool (a1)-(a6) and the speculative resolve.
+//
+//   k_score  every row, one row per thread per iteration over a persistent-style grid: the
+//            32-B hot state is read with warp-coalesced loads (the next iteration's row is
+//            loaded before the current one is scored), standalone rows get their key image
+//            (a5) and cost (a6); compound calls get their bound and cost and add (len_rem,
+//            call goodput) to their task's accumulators through a segmented warp reduction
+//            (tasks are contiguous row ranges), i.e. (a4) is row-parallel whatever the fan-out.
+//            Per-CTA partial counts go to an array (no global atomics on a shared line).
+//   k_ckey   every compound call: its task's aggregate key (a4/a5) from the accumulators.
+//   k_spec   one CTA: exact B*, bp, thr, Cd from the speculative set.
+#pragma once
+#include "select.cuh"
+
+namespace jit {
+
+// Rows whose key image is >= the speculative threshold t (the previous step's cutoff with a
+// margin) join the speculative set; warp ballot + one atomic per warp (all lanes convergent).
+__device__ __forceinline__ void spec_add(Ctrl* ctrl, const Scratch& S, const uint32_t* ids, bool valid,
+                                         uint64_t img, uint32_t row, uint64_t t) {
+    const bool take = valid && img >= t;
+    const unsigned m = __ballot_sync(0xffffffffu, take);
+    if (!m) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(&ctrl->spec_n, (uint32_t)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (take) {
+        const uint32_t slot = base + __popc(m & ((1u << lane) - 1u));
+        if (slot < kSpecCap) { S.spec_ck[slot] = make_ck(img, __ldg(ids + row)); S.spec_row[slot] = row; }
+    }
+}
+
+// block reduction of the per-thread partials into part[blockIdx.x]
+__device__ __forceinline__ void store_part(BlockPart* part, uint32_t pend, uint32_t drop, uint32_t err,
+                                           uint64_t mn, uint64_t cost, uint32_t refresh) {
+    __shared__ unsigned long long s_min, s_cost;
+    __shared__ uint32_t s_pend, s_drop, s_err, s_ref;
+    if (threadIdx.x == 0) { s_min = kNone; s_cost = 0; s_pend = 0; s_drop = 0; s_err = 0; s_ref = 0; }
+    __syncthreads();
+    pend = warp_sum(pend); drop = warp_sum(drop); err = __reduce_or_sync(0xffffffffu, err);
+    mn = warp_min_u64(mn); cost = warp_sum(cost); refresh = warp_sum(refresh);
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&s_pend, pend); atomicAdd(&s_drop, drop); atomicOr(&s_err, err); atomicAdd(&s_ref, refresh);
+        atomicMin(&s_min, (unsigned long long)mn); atomicAdd(&s_cost, (unsigned long long)cost);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        BlockPart b;
+        b.min_img = s_min; b.tot_cost = s_cost; b.n_pending = s_pend; b.n_dropped = s_drop; b.err = s_err;
+        b.refresh = s_ref;
+        part[blockIdx.x] = b;
+    }
+}
+
+// compound call (a4, per row): bound, cost; returns pending
+template <bool kDebug>
+__device__ __forceinline__ bool score_call(const Cfg& c, const Table& T, const GroupFast* sg, uint32_t n_groups,
+                                           int64_t now, int64_t arr, uint32_t L_i, uint32_t g, uint32_t pre,
+                                           uint32_t lhat, uint32_t meta, uint32_t aux, uint32_t& o_lhat,
+                                           uint32_t& o_meta, bool& w_lh, uint64_t& len_rem, uint64_t& Gc,
+                                           uint32_t& cost, uint32_t& Lh_out, bool& err) {
+    w_lh = false; o_meta = meta; o_lhat = lhat; len_rem = 0; Gc = 0; cost = 0; Lh_out = 0;
+    if (arr > now || m_state(meta) > kPreempted) return false;      // no admission drop (A40)
+    const uint32_t gi = m_group(meta), drow = aux & 0xFFFFu;
+    if (gi >= n_groups || sg[gi].type != kCMP || !(m_flags(meta) & kCompound) || drow >= T.n_rows) {
+        err = true; return false;
+    }
+    const uint32_t ep = fastdiv(g, c.R, c.R_m, c.R_l);
+    if (lhat == 0 || ep >= 65536u || m_epoch(meta) != ep) {
+        lhat = cond_quantile(T, drow, ep * c.R, c.qn, c.qd);
+        o_lhat = lhat; w_lh = true;
+        if (ep < 65536u) o_meta = (meta & 0xFFFFu) | (ep << 16);
+    }
+    const uint32_t Lh = lhat > g + 1 ? lhat : g + 1;
+    len_rem = (uint64_t)(Lh - g);
+    Gc = (uint64_t)sg[gi].w_in_eff * L_i + (uint64_t)sg[gi].w_out_eff * Lh;
+    cost = token_cost(L_i, pre, c.chunk);
+    Lh_out = Lh;
+    return true;
+}
+
+template <bool kDebug>
+__global__ void __launch_bounds__(kScoreThreads) k_score(Pool P, Table T, const Group* groups, uint32_t n_groups,
+                                                         Cfg c, Ctrl* ctrl, Scratch S) {
+    __shared__ GroupFast s_g[256];
+    for (uint32_t gi = threadIdx.x; gi < n_groups; gi += blockDim.x) s_g[gi] = make_fast(groups[gi]);
+    __syncthreads();
+    const int64_t now = ctrl->now, v = ctrl->v;
+    const uint64_t t_guess = S.persist->t_guess;
+    const int lane = threadIdx.x & 31;
+    const bool any_compound = P.n_single < P.n;
+    uint32_t my_pend = 0, my_drop = 0, my_err = 0, my_ref = 0;
+    uint64_t my_min = kNone, my_cost = 0;
+    const uint32_t n = P.n, ns = P.n_single;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t a_arr = 0;
+    uint32_t a_li = 0, a_g = 0, a_pr = 0, a_lh = 0, a_me = 0, a_ax = 0, a_tk = kNoTask;
+    if (r < n) {
+        a_arr = __ldcs(P.arr + r); a_li = __ldcs(P.len_in + r); a_g = __ldcs(P.gen + r); a_pr = __ldcs(P.pre + r);
+        a_lh = __ldcs(P.lhat + r); a_me = __ldcs(P.meta + r); a_ax = __ldcs(P.aux + r);
+        if (r >= ns) a_tk = __ldg(P.task + r);
+    }
+#pragma unroll 1
+    for (uint32_t wr = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); wr < n; wr += stride, r += stride) {
+        const bool act = r < n;
+        const uint32_t rn = r + stride;
+        int64_t b_arr = 0;
+        uint32_t b_li = 0, b_g = 0, b_pr = 0, b_lh = 0, b_me = 0, b_ax = 0, b_tk = kNoTask;
+        if (rn < n) {                                    // prefetch the next iteration's row
+            b_arr = __ldcs(P.arr + rn); b_li = __ldcs(P.len_in + rn); b_g = __ldcs(P.gen + rn);
+            b_pr = __ldcs(P.pre + rn); b_lh = __ldcs(P.lhat + rn); b_me = __ldcs(P.meta + rn);
+            b_ax = __ldcs(P.aux + rn);
+            if (rn >= ns) b_tk = __ldg(P.task + rn);
+        }
+        uint64_t img = kNone;
+        bool valid = false;
+        uint64_t vT = 0, vG = 0;                       // compound contributions
+        uint32_t key_task = kNoTask;
+        if (act && r < ns) {
+            RowRes o;
+            score_standalone<kDebug>(c, T, s_g, n_groups, P.ovr, r, now, v, a_arr, a_li, a_g, a_pr, a_lh, a_me, a_ax, o);
+            P.img[r] = o.img; P.cost[r] = o.cost;
+            if (o.aux != a_ax) P.aux[r] = o.aux;
+            if (o.w_meta) P.meta[r] = o.meta;
+            if (o.w_lhat) P.lhat[r] = o.lhat;
+            if (kDebug) {
+                P.dbg_rate[r] = o.pending ? o.rate : 0.0;
+                P.dbg_trem[r] = o.pending ? o.trem : 0;
+                P.dbg_lhat[r] = o.pending ? o.lhatc : 0;
+            }
+            img = o.img;
+            valid = img != kNone;
+            my_drop += o.dropped; my_err |= o.err; my_ref += o.w_lhat;
+            if (valid) { my_pend += 1; my_cost += o.cost; if (img < my_min) my_min = img; }
+        } else if (act) {
+            uint32_t o_lhat, o_meta, cost, Lh;
+            bool w_lh, err = false;
+            uint64_t len_rem, Gc;
+            const bool pend = score_call<kDebug>(c, T, s_g, n_groups, now, a_arr, a_li, a_g, a_pr, a_lh, a_me, a_ax,
+                                                 o_lhat, o_meta, w_lh, len_rem, Gc, cost, Lh, err);
+            P.cost[r] = cost;                          // > 0 marks a pending call for k_ckey
+            if (w_lh) { P.lhat[r] = o_lhat; if (o_meta != a_me) P.meta[r] = o_meta; }
+            if (kDebug) P.dbg_lhat[r] = pend ? Lh : 0;
+            my_err |= err; my_ref += w_lh;
+            if (pend) { my_pend += 1; my_cost += cost; vT = len_rem; vG = Gc; }
+            key_task = (a_tk < P.n_tasks) ? a_tk : kNoTask;
+            if (a_tk >= P.n_tasks) my_err = 1;
+        }
+        // segmented warp reduction of (len_rem, goodput) per task (rows of a task are contiguous);
+        // warps that hold no compound call skip it (warp-uniform)
+        if (any_compound && __any_sync(0xffffffffu, key_task != kNoTask)) {
+            uint64_t sT = vT, sG = vG;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint64_t uT = __shfl_up_sync(0xffffffffu, sT, d);
+                const uint64_t uG = __shfl_up_sync(0xffffffffu, sG, d);
+                const uint32_t uk = __shfl_up_sync(0xffffffffu, key_task, d);
+                if (lane >= d && uk == key_task) { sT += uT; sG += uG; }
+            }
+            const uint32_t nk = __shfl_down_sync(0xffffffffu, key_task, 1);
+            if (key_task != kNoTask && (lane == 31 || nk != key_task) && (sT | sG)) {
+                atomicAdd(&S.tacc[key_task].T, (unsigned long long)sT);
+                atomicAdd(&S.tacc[key_task].G, (unsigned long long)sG);
+            }
+        }
+        spec_add(ctrl, S, P.id, valid, img, r, t_guess);
+        a_arr = b_arr; a_li = b_li; a_g = b_g; a_pr = b_pr; a_lh = b_lh; a_me = b_me; a_ax = b_ax; a_tk = b_tk;
+    }
+    store_part(S.part, my_pend, my_drop, my_err, my_min, my_cost, my_ref);
+}
+
+// --------------------------------------------------------------------------------------
+// k_ckey: per compound call, its task's key (a4/a5): G_task = goodput_done + sum of the
+// current stage's pending call goodput (zero once a_c + D has passed), t_gen = (sum len_rem)
+// * v_token; key = (G_task + delta*floor(waited/Delta)) * 1e9 / (t_gen + eps).
+// --------------------------------------------------------------------------------------
+template <bool kDebug>
+__global__ void __launch_bounds__(kScoreThreads) k_ckey(Pool P, Cfg c, Ctrl* ctrl, Scratch S) {
+    const int64_t now = ctrl->now, v = ctrl->v;
+    const uint64_t t_guess = S.persist->t_guess;
+    uint32_t my_err = 0;
+    uint64_t my_min = kNone;
+    const uint32_t n = P.n;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t wr = P.n_single + blockIdx.x * blockDim.x + (threadIdx.x & ~31u); wr < n; wr += stride) {
+        const uint32_t r = wr + (threadIdx.x & 31);
+        uint64_t img = kNone;
+        bool valid = false;
+        if (r < n) {
+            // issue the three per-row loads together; the task-level loads follow in one round
+            const uint32_t cost = P.cost[r], t = __ldg(P.task + r), aux = P.aux[r];
+            if (cost) {
+                const TaskAcc acc = S.tacc[t];
+                const int64_t a_c = __ldg(P.t_arr + t), D = __ldg(P.t_dl + t);
+                const uint32_t s = __ldg(P.cur_stage + t), Sn = __ldg(P.n_stages + t);
+                const uint4 p0 = __ldg(reinterpret_cast<const uint4*>(P.pattern) + 2 * t);
+                const uint4 p1 = __ldg(reinterpret_cast<const uint4*>(P.pattern) + 2 * t + 1);
+                const uint32_t pt[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+                // phi(s) = t_<=s / t_total, D_s = floor(D * phi); in ms the ratio is
+                // identical and D*le fits u64 when D < 2^40 ns and t_total < 2^24 ms
+                uint64_t le = 0, tot = 0;
+#pragma unroll
+                for (uint32_t u = 0; u < kMaxStages; ++u) {
+                    const uint64_t ms = u < Sn ? pt[u] : 0u;
+                    tot += ms; if (u <= s) le += ms;
+                }
+                if (tot == 0 || Sn == 0 || Sn > kMaxStages || s >= Sn) my_err = 1;
+                const int64_t Ds = !tot ? 0
+                    : ((uint64_t)D < (1ull << 40) && tot < (1ull << 24)) ? (int64_t)((uint64_t)D * le / tot)
+                                                                         : (int64_t)((u128)(uint64_t)D * le / tot);
+                const int64_t trem = a_c + Ds - now;               // advisory stage deadline
+                uint64_t Gt = __ldg(P.gdone + t) + acc.G;
+                if (a_c + D <= now) Gt = 0;                         // final deadline passed
+                const uint64_t t_gen = acc.T * (uint64_t)v;
+                if (c.appb && t_gen > (uint64_t)(trem > 0 ? trem : 0)) Gt = 0;
+                const uint64_t Gp = Gt + (uint64_t)c.delta * fastdiv(aux >> 16, c.frame, c.F_m, c.F_l);
+                double key;
+                if (!make_key(Gp, t_gen, c.eps, &key)) my_err = 1;
+                img = (uint64_t)__double_as_longlong(key);
+                valid = true;
+                if ((aux >> 16) < 0xFFFFu) P.aux[r] = aux + (1u << 16);
+                if (kDebug) { P.dbg_rate[r] = make_rate(acc.T, trem); P.dbg_trem[r] = trem; }
+                if (img < my_min) my_min = img;
+            } else if (kDebug) {
+                P.dbg_rate[r] = 0.0; P.dbg_trem[r] = 0;
+            }
+            P.img[r] = img;
+        }
+        spec_add(ctrl, S, P.id, valid, img, r, t_guess);
+    }
+    store_part(S.part2, 0, 0, my_err, my_min, 0, 0);
+}
+
+// --------------------------------------------------------------------------------------
+// k_spec: one CTA.  Reduces the scoring partials, then resolves (a7)/(a8) exactly from the
+// speculative set S = {key >= t}.  S is upward closed in the (key desc, id asc) order, i.e. a
+// PREFIX of it, so the budget walk over sorted S is the exact walk as long as it stops inside
+// S (or S holds every pending row); Cd = {key >= thr} lies in S when thr >= t.  Otherwise it
+// raises the fallback condition -> the radix path of select.cuh.
+// --------------------------------------------------------------------------------------
+// shared-memory layout of the in-CTA window (reuses the 16*kSpecCap bytes of the S sort keys)
+constexpr uint32_t kSpecWindow = 4032;
+constexpr uint32_t kWinPcOff = (8 * kSpecWindow + 15) & ~15u;
+constexpr uint32_t kWinPfOff = (kWinPcOff + 8 * (kSpecWindow + 1) + 15) & ~15u;
+static_assert(kWinPfOff + 16 * (kSpecWindow + 1) <= 16 * kSpecCap, "window arrays must fit the sort-key region");
+
+constexpr uint32_t kSpecThreads = 256;        // small CTA: the sets are small and every idle warp costs issue slots
+__global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl, Scratch S,
+                                               cudaGraphConditionalHandle fb_handle, int in_graph, int reduce_only) {
+    const uint32_t* __restrict__ cost_rows = P.cost;
+    extern __shared__ __align__(16) unsigned char smem[];
+    u128* sk = reinterpret_cast<u128*>(smem);
+    uint32_t* sv = reinterpret_cast<uint32_t*>(smem + sizeof(u128) * kSpecCap);
+    __shared__ uint64_t s_scan[32];
+    __shared__ unsigned long long s_min, s_cost;
+    __shared__ uint32_t s_pend, s_drop, s_err, s_ref;
+    __shared__ int s_fb;
+    if (threadIdx.x == 0) { s_min = kNone; s_cost = 0; s_pend = 0; s_drop = 0; s_err = 0; s_ref = 0; }
+    __syncthreads();
+    {   // partials of k_score and k_ckey
+        uint32_t pend = 0, drop = 0, err = 0, ref = 0;
+        uint64_t mn = kNone, cost = 0;
+        for (uint32_t i = threadIdx.x; i < S.n_part + S.n_part2; i += blockDim.x) {
+            const BlockPart b = i < S.n_part ? S.part[i] : S.part2[i - S.n_part];
+            pend += b.n_pending; drop += b.n_dropped; err |= b.err; cost += b.tot_cost; ref += b.refresh;
+            if (b.min_img < mn) mn = b.min_img;
+        }
+        pend = warp_sum(pend); drop = warp_sum(drop); err = __reduce_or_sync(0xffffffffu, err);
+        mn = warp_min_u64(mn); cost = warp_sum(cost); ref = warp_sum(ref);
+        if ((threadIdx.x & 31) == 0) {
+            atomicAdd(&s_pend, pend); atomicAdd(&s_drop, drop); atomicOr(&s_err, err); atomicAdd(&s_ref, ref);
+            atomicMin(&s_min, (unsigned long long)mn); atomicAdd(&s_cost, (unsigned long long)cost);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            ctrl->n_pending = s_pend; ctrl->n_dropped = s_drop; ctrl->min_img = s_min; ctrl->tot_cost = s_cost;
+            ctrl->n_refresh = s_ref;
+            if (s_err) ctrl->error |= 1u;
+        }
+    }
+    if (reduce_only) return;                               // sharded step: the radix path follows
+    const uint32_t n = ctrl->spec_n, np = s_pend;
+    if (threadIdx.x == 0) {
+        s_fb = 0;
+        if (s_err) { ctrl->status = ST_ERROR; s_fb = 2; }
+        else if (np == 0) { ctrl->status = ST_EMPTY; s_fb = 2; }
+        else if (n > kSpecCap || n == 0) s_fb = 1;
+    }
+    __syncthreads();
+    if (s_fb) {
+        if (threadIdx.x == 0 && s_fb == 1) {
+            ctrl->status = ST_FALLBACK; ctrl->fallback = 1;
+            if (in_graph) cudaGraphSetConditional(fb_handle, 1u);
+        }
+        return;
+    }
+    uint32_t n2 = 1;
+    while (n2 < n) n2 <<= 1;
+    for (uint32_t i = threadIdx.x; i < n2; i += blockDim.x) {
+        if (i < n) { sk[i] = S.spec_ck[i]; sv[i] = S.spec_row[i]; }
+        else { sk[i] = ~(u128)0; sv[i] = 0; }
+    }
+    __syncthreads();
+    block_bitonic_sort<u128>(sk, sv, n2);
+    // budget walk (monotone predicate): count of the prefix within tau and B_max
+    uint64_t cc = 0;
+    uint32_t fits = 0;
+    for (uint32_t base = 0; base < n; base += blockDim.x) {
+        const uint32_t i = base + threadIdx.x;
+        const uint64_t cv = i < n ? cost_rows[sv[i]] : 0;
+        uint64_t tot;
+        const uint64_t ex = block_exclusive_scan_u64(cv, s_scan, &tot);
+        fits += __syncthreads_count(i < n && (uint64_t)i + 1 <= c.max_batch && cc + ex + cv <= c.token_budget);
+        cc += tot;
+    }
+    const bool whole = (n == np);                          // S holds every pending row
+    if (threadIdx.x == 0) {
+        bool fb = (fits == n && !whole);
+        double bp = 0.0, thr = 0.0;
+        uint64_t thr_img = 0;
+        if (!fb) {
+            bp = __longlong_as_double((long long)ck_img(sk[fits - 1]));
+            thr = __dmul_rn(__ddiv_rn((double)c.pn, (double)c.pd), bp);
+            thr_img = (uint64_t)__double_as_longlong(thr);
+            if (!whole && thr_img < S.persist->t_guess) fb = true;
+        }
+        if (fb) {
+            ctrl->status = ST_FALLBACK; ctrl->fallback = 1;
+            if (in_graph) cudaGraphSetConditional(fb_handle, 1u);
+            s_fb = 1;
+        } else {
+            ctrl->b_star = fits; ctrl->bp = bp; ctrl->thr = thr; ctrl->thr_img = thr_img;
+        }
+    }
+    __syncthreads();
+    if (s_fb) return;
+    // Cd = the prefix of sorted S with key >= thr
+    const uint64_t thr_img = ctrl->thr_img;
+    uint32_t ncd = 0;
+    for (uint32_t base = 0; base < n; base += blockDim.x) {
+        const uint32_t i = base + threadIdx.x;
+        ncd += __syncthreads_count(i < n && ck_img(sk[i]) >= thr_img);
+    }
+    if (threadIdx.x == 0) { ctrl->n_cand = ncd; ctrl->status = ST_RESOLVED; }
+    if (ncd > kSpecWindow) {
+        // a large Cd: hand it to k_group (inside the conditional body; the radix kernels there
+        // see status RESOLVED / fallback = 0 and skip)
+        for (uint32_t i = threadIdx.x; i < ncd; i += blockDim.x) S.cand[i] = sv[i];
+        if (threadIdx.x == 0 && in_graph) cudaGraphSetConditional(fb_handle, 1u);
+        return;
+    }
+    // (a9) in this CTA: the sorted-S region is reused for the (len, id) sort keys and the
+    // prefix sums, all in shared memory; sv[0..ncd) already holds Cd's rows
+    uint64_t* wsk = reinterpret_cast<uint64_t*>(smem);
+    unsigned long long* pc = reinterpret_cast<unsigned long long*>(smem + kWinPcOff);
+    u128* pf = reinterpret_cast<u128*>(smem + kWinPfOff);
+    for (uint32_t i = threadIdx.x; i < ncd; i += blockDim.x) {
+        const uint32_t r = sv[i];
+        const uint64_t len = c.len_key ? (uint64_t)P.len_in[r] + P.gen[r] : (uint64_t)P.len_in[r];
+        wsk[i] = (len << 32) | P.id[r];
+    }
+    window_select(P, c, ctrl, S, wsk, sv, ncd, pc, pf);
+}
+
+}  // namespace jit

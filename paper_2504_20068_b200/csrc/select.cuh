@@ -1,4 +1,4 @@
-// pool.cuh -- the GMAX step over a request pool resident in HBM (sm_100a).
+// select.cuh -- the GMAX step over a request pool resident in HBM (sm_100a).
 //
 // Kernel chain of one step (captured once into a CUDA graph):
 //   k_begin    zero the control block / histograms, install (now, v_token)
@@ -19,11 +19,13 @@
 namespace jit {
 
 constexpr uint32_t kBucketCap = 4096;
+constexpr uint32_t kSpecCap = 8192;
+constexpr uint32_t kMaxParts = 4096;          // max CTAs of the scoring kernels (partials)           // speculative set resolved in shared memory up to this size
 constexpr uint32_t kGroupSmemSort = 8192;     // |Cd| sorted in shared memory up to this size
 constexpr uint32_t kScoreThreads = 256;
 constexpr uint32_t kPassThreads = 512;
 
-enum : uint32_t { ST_RUN = 0, ST_HIST = 1, ST_COMPACT = 2, ST_RESOLVED = 3, ST_EMPTY = 4, ST_ERROR = 5 };
+enum : uint32_t { ST_RUN = 0, ST_HIST = 1, ST_COMPACT = 2, ST_RESOLVED = 3, ST_EMPTY = 4, ST_ERROR = 5, ST_FALLBACK = 6 };
 
 struct Pool {
     int64_t* arr;
@@ -53,7 +55,25 @@ struct alignas(16) Ctrl {
     uint32_t b_star, n_cand, n_selected, total_tokens;
     uint32_t done[16];
     uint32_t i_best, j_best, cand_overflow, exp_fill;
+    unsigned long long tot_cost;     // sum of the token costs of all pending rows
+    uint32_t spec_n, spec_ovf, fallback, window_done;
+    uint32_t n_refresh, pad3[3];                // length-bound refreshes this step (a2)
 };
+
+// state that survives across steps of one handle (not cleared by k_begin)
+struct Persist {
+    unsigned long long t_guess;      // speculative key-image threshold for the next step
+    uint32_t steps, fallbacks;
+};
+
+// per-CTA partial results of the scoring kernels (reduced by k_spec -- no global atomics)
+struct BlockPart {
+    unsigned long long min_img, tot_cost;
+    uint32_t n_pending, n_dropped, err, refresh;
+};
+
+// per-task accumulators of the compound pass (a4): sum of len_rem and of the call goodput
+struct TaskAcc { unsigned long long T, G; };
 
 struct Scratch {
     uint32_t* hcnt;          // 4096
@@ -69,6 +89,13 @@ struct Scratch {
     uint32_t* out_tokens;
     uint32_t* out_rows;
     uint32_t cand_cap, pad;
+    u128* spec_ck;           // kSpecCap: rows with key image >= t_guess (composite key)
+    uint32_t* spec_row;
+    Persist* persist;
+    BlockPart* part;         // k_score partials (grid_score entries)
+    BlockPart* part2;        // k_ckey partials (grid_ckey entries)
+    TaskAcc* tacc;           // task_capacity, zeroed by k_begin every step
+    uint32_t n_part, n_part2, task_cap, pad3;
 };
 
 __device__ __forceinline__ bool is_last_block(uint32_t* counter) {
@@ -180,11 +207,12 @@ __device__ void resolve_level(const Cfg& c, Ctrl* ctrl, uint32_t* hcnt, unsigned
 // --------------------------------------------------------------------------------------
 // k_begin
 // --------------------------------------------------------------------------------------
-__global__ void k_begin(Ctrl* ctrl, uint32_t* hcnt, unsigned long long* hcost, int64_t now, int64_t v) {
-    for (uint32_t b = threadIdx.x + blockIdx.x * blockDim.x; b < 4096; b += blockDim.x * gridDim.x) {
-        hcnt[b] = 0; hcost[b] = 0;
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+__global__ void k_begin(Ctrl* ctrl, uint32_t* hcnt, unsigned long long* hcost, int64_t now, int64_t v,
+                        TaskAcc* tacc, uint32_t n_tasks) {
+    const uint32_t tid = threadIdx.x + blockIdx.x * blockDim.x, nt = blockDim.x * gridDim.x;
+    for (uint32_t b = tid; b < 4096; b += nt) { hcnt[b] = 0; hcost[b] = 0; }
+    for (uint32_t t = tid; t < n_tasks; t += nt) { tacc[t].T = 0; tacc[t].G = 0; }
+    if (tid == 0) {
         Ctrl z;
         memset(&z, 0, sizeof(z));
         z.now = now; z.v = v;
@@ -204,8 +232,26 @@ struct RowRes {
     double rate; int64_t trem; uint32_t lhatc;
 };
 
+// Per-group constants in the form the scoring loop uses (staged to shared memory per CTA):
+//   t_rem = arrival + base + (Lhat-1)*tok - now      (LAT: base=TTFT, tok=TBT  [A9];
+//                                                     DDL: base=E2EL; BE: base=default deadline)
+//   G     = w_in_eff * L_i + w_out_eff * Lhat        (DDL: w_in, w_out; LAT: 0, w_out; BE: 0, 0)
+struct GroupFast {
+    int64_t base, tok;
+    uint32_t w_in_eff, w_out_eff, type, pad;
+};
+__host__ __device__ inline GroupFast make_fast(const Group& g) {
+    GroupFast f;
+    f.type = g.type; f.pad = 0;
+    f.base = g.type == kLAT ? g.ttft_ns : g.type == kDDL ? g.e2el_ns : g.type == kBE ? g.be_deadline_ns : 0;
+    f.tok = g.type == kLAT ? g.tbt_ns : 0;
+    f.w_in_eff = (g.type == kDDL || g.type == kCMP) ? g.w_in : 0;   // CMP: used by the compound pass
+    f.w_out_eff = g.type != kBE ? g.w_out : 0;
+    return f;
+}
+
 template <bool kDebug>
-__device__ __forceinline__ void score_standalone(const Cfg& c, const Table& T, const Group* sg, uint32_t n_groups,
+__device__ __forceinline__ void score_standalone(const Cfg& c, const Table& T, const GroupFast* sg, uint32_t n_groups,
                                                  const uint32_t* ovr, uint32_t row, int64_t now, int64_t v,
                                                  int64_t arr, uint32_t L_i, uint32_t g, uint32_t pre,
                                                  uint32_t lhat, uint32_t meta, uint32_t aux, RowRes& o) {
@@ -223,34 +269,25 @@ __device__ __forceinline__ void score_standalone(const Cfg& c, const Table& T, c
     const uint32_t gi = m_group(meta);
     const uint32_t drow = aux & 0xFFFFu;
     if (gi >= n_groups || drow >= T.n_rows || (fl & kCompound)) { o.err = true; return; }
+    const GroupFast G = sg[gi];
+    if (G.type == kCMP) { o.err = true; return; }
     // (a2) conservative remaining length, refreshed every R tokens; cached per epoch
-    const uint32_t ep = g / c.R;
+    const uint32_t ep = fastdiv(g, c.R, c.R_m, c.R_l);
     if (lhat == 0 || ep >= 65536u || m_epoch(meta) != ep) {
         lhat = cond_quantile(T, drow, ep * c.R, c.qn, c.qd);
         o.lhat = lhat; o.w_lhat = true;
         if (ep < 65536u) { o.meta = (meta & 0xFFFFu) | (ep << 16); o.w_meta = true; }
     }
     const uint32_t Lh = lhat > g + 1 ? lhat : g + 1;
-    const uint64_t len_rem = (uint64_t)(Lh - g);
+    const uint32_t len_rem = Lh - g;
     o.cost = token_cost(L_i, pre, c.chunk);
-    const Group G = sg[gi];
-    const uint64_t t_gen = len_rem * (uint64_t)v;
-    int64_t trem;
-    uint64_t Gk;
-    if (G.type == kLAT) {                                       // A9, A11
-        trem = arr + G.ttft_ns + (int64_t)(Lh - 1) * G.tbt_ns - now;
-        Gk = (uint64_t)G.w_out * Lh;
-    } else if (G.type == kDDL) {
-        trem = arr + G.e2el_ns - now;
-        Gk = (uint64_t)G.w_in * L_i + (uint64_t)G.w_out * Lh;
-    } else if (G.type == kBE) {
-        trem = arr + G.be_deadline_ns - now;
-        Gk = 0;
-    } else { o.err = true; return; }
-    if (m_flags(meta) & kOverride) Gk = __ldg(ovr + row);
+    const uint64_t t_gen = (uint64_t)len_rem * (uint64_t)v;
+    const int64_t trem = arr + G.base + (int64_t)(Lh - 1) * G.tok - now;  // (a3)
+    uint64_t Gk = (uint64_t)G.w_in_eff * L_i + (uint64_t)G.w_out_eff * Lh;  // (a5) A10/A11
+    if (fl & kOverride) Gk = __ldg(ovr + row);
     if (trem <= 0) Gk = 0;                                      // A22
     if (c.appb && t_gen > (uint64_t)(trem > 0 ? trem : 0)) Gk = 0;
-    const uint64_t Gp = Gk + (uint64_t)c.delta * ((aux >> 16) / c.frame);
+    const uint64_t Gp = Gk + (uint64_t)c.delta * fastdiv(aux >> 16, c.frame, c.F_m, c.F_l);
     double key;
     if (!make_key(Gp, t_gen, c.eps, &key)) { o.err = true; return; }
     o.img = (uint64_t)__double_as_longlong(key);
@@ -260,184 +297,26 @@ __device__ __forceinline__ void score_standalone(const Cfg& c, const Table& T, c
 
 // --------------------------------------------------------------------------------------
 // k_score
-// --------------------------------------------------------------------------------------
-template <bool kDebug>
-__global__ void __launch_bounds__(kScoreThreads) k_score(Pool P, Table T, const Group* groups, uint32_t n_groups,
-                                                         Cfg c, Ctrl* ctrl, uint32_t* hcnt,
-                                                         unsigned long long* hcost, uint32_t nb_rows) {
+// level-0 histogram of the key images (fallback path only), last CTA resolves level 0
+__global__ void __launch_bounds__(kPassThreads) k_hist0(Pool P, Cfg c, Ctrl* ctrl, uint32_t* hcnt,
+                                                        unsigned long long* hcost, int force) {
+    if (!force && ctrl->status != ST_FALLBACK) return;
     __shared__ uint32_t s_cnt[2048], s_cost[2048];
-    __shared__ Group s_g[256];
-    __shared__ unsigned long long s_min;
-    __shared__ uint32_t s_pend, s_drop, s_err;
     for (uint32_t b = threadIdx.x; b < 2048; b += blockDim.x) { s_cnt[b] = 0; s_cost[b] = 0; }
-    for (uint32_t gi = threadIdx.x; gi < n_groups; gi += blockDim.x) s_g[gi] = groups[gi];
-    if (threadIdx.x == 0) { s_min = kNone; s_pend = 0; s_drop = 0; s_err = 0; }
     __syncthreads();
-    const int64_t now = ctrl->now, v = ctrl->v;
-    const int lane = threadIdx.x & 31;
-    uint32_t my_pend = 0, my_drop = 0, my_err = 0;
-    uint64_t my_min = kNone;
-
-    if (blockIdx.x < nb_rows) {
-        // ---------------- standalone rows: 4 consecutive rows per thread --------------------
-        const uint32_t nq = (P.n_single + 3) >> 2;
-        const uint32_t stride = nb_rows * blockDim.x;
-        for (uint32_t wq = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); wq < nq; wq += stride) {
-            const uint32_t q = wq + lane;
-            const bool act = q < nq;
-            const uint32_t r0 = q * 4;
-            RowRes o[4];
-            if (act && r0 + 4 <= P.n_single) {
-                const longlong2 a01 = reinterpret_cast<const longlong2*>(P.arr)[2 * q];
-                const longlong2 a23 = reinterpret_cast<const longlong2*>(P.arr)[2 * q + 1];
-                const uint4 li = reinterpret_cast<const uint4*>(P.len_in)[q];
-                const uint4 gg = reinterpret_cast<const uint4*>(P.gen)[q];
-                const uint4 pr = reinterpret_cast<const uint4*>(P.pre)[q];
-                const uint4 lh = reinterpret_cast<const uint4*>(P.lhat)[q];
-                const uint4 me = reinterpret_cast<const uint4*>(P.meta)[q];
-                const uint4 ax = reinterpret_cast<const uint4*>(P.aux)[q];
-                score_standalone<kDebug>(c, T, s_g, n_groups, P.ovr, r0 + 0, now, v, a01.x, li.x, gg.x, pr.x, lh.x, me.x, ax.x, o[0]);
-                score_standalone<kDebug>(c, T, s_g, n_groups, P.ovr, r0 + 1, now, v, a01.y, li.y, gg.y, pr.y, lh.y, me.y, ax.y, o[1]);
-                score_standalone<kDebug>(c, T, s_g, n_groups, P.ovr, r0 + 2, now, v, a23.x, li.z, gg.z, pr.z, lh.z, me.z, ax.z, o[2]);
-                score_standalone<kDebug>(c, T, s_g, n_groups, P.ovr, r0 + 3, now, v, a23.y, li.w, gg.w, pr.w, lh.w, me.w, ax.w, o[3]);
-                reinterpret_cast<ulonglong2*>(P.img)[2 * q] = make_ulonglong2(o[0].img, o[1].img);
-                reinterpret_cast<ulonglong2*>(P.img)[2 * q + 1] = make_ulonglong2(o[2].img, o[3].img);
-                reinterpret_cast<uint4*>(P.cost)[q] = make_uint4(o[0].cost, o[1].cost, o[2].cost, o[3].cost);
-                reinterpret_cast<uint4*>(P.aux)[q] = make_uint4(o[0].aux, o[1].aux, o[2].aux, o[3].aux);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    if (o[k].w_meta) P.meta[r0 + k] = o[k].meta;
-                    if (o[k].w_lhat) P.lhat[r0 + k] = o[k].lhat;
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint32_t r = r0 + k;
-                    if (act && r < P.n_single) {
-                        score_standalone<kDebug>(c, T, s_g, n_groups, P.ovr, r, now, v, P.arr[r], P.len_in[r], P.gen[r],
-                                                 P.pre[r], P.lhat[r], P.meta[r], P.aux[r], o[k]);
-                        P.img[r] = o[k].img; P.cost[r] = o[k].cost; P.aux[r] = o[k].aux;
-                        if (o[k].w_meta) P.meta[r] = o[k].meta;
-                        if (o[k].w_lhat) P.lhat[r] = o[k].lhat;
-                    } else {
-                        o[k].img = kNone; o[k].cost = 0; o[k].pending = o[k].dropped = o[k].err = false;
-                    }
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t r = r0 + k;
-                if (kDebug && act && r < P.n_single) {
-                    P.dbg_rate[r] = o[k].pending ? o[k].rate : 0.0;
-                    P.dbg_trem[r] = o[k].pending ? o[k].trem : 0;
-                    P.dbg_lhat[r] = o[k].pending ? o[k].lhatc : 0;
-                }
-                const bool valid = act && o[k].img != kNone;
-                my_pend += valid; my_drop += (act && o[k].dropped); my_err |= (act && o[k].err);
-                if (valid && o[k].img < my_min) my_min = o[k].img;
-                const uint32_t bin = (uint32_t)(make_ck(o[k].img, 0) >> digit_shift(0)) & 2047u;
-                warp_hist_add(s_cnt, s_cost, valid, bin, o[k].cost);
-            }
-        }
-    } else {
-        // ---------------- (a4) compound tasks: one warp per task ---------------------------
-        const uint32_t wpb = blockDim.x >> 5;
-        const uint32_t w0 = (blockIdx.x - nb_rows) * wpb + (threadIdx.x >> 5);
-        const uint32_t nw = (gridDim.x - nb_rows) * wpb;
-        for (uint32_t t = w0; t < P.n_tasks; t += nw) {
-            const uint32_t b = P.call_off[t], e = P.call_off[t + 1];
-            uint64_t Tsum = 0, Gcur = 0;
-            uint32_t cnt = 0;
-            for (uint32_t base = b; base < e; base += 32) {          // pass 1: bounds and sums
-                const uint32_t r = base + lane;
-                if (r >= e) continue;
-                const uint32_t meta = P.meta[r];
-                const uint32_t st = m_state(meta);
-                if (P.arr[r] > now || st > kPreempted) continue;
-                const uint32_t g = P.gen[r], aux = P.aux[r];
-                const uint32_t gi = m_group(meta), drow = aux & 0xFFFFu;
-                if (gi >= n_groups || s_g[gi].type != kCMP || !(m_flags(meta) & kCompound) || drow >= T.n_rows ||
-                    P.task[r] != t) { my_err = 1; continue; }
-                uint32_t lhat = P.lhat[r];
-                const uint32_t ep = g / c.R;
-                if (lhat == 0 || ep >= 65536u || m_epoch(meta) != ep) {
-                    lhat = cond_quantile(T, drow, ep * c.R, c.qn, c.qd);
-                    P.lhat[r] = lhat;
-                    if (ep < 65536u) P.meta[r] = (meta & 0xFFFFu) | (ep << 16);
-                }
-                const uint32_t Lh = lhat > g + 1 ? lhat : g + 1;
-                Tsum += (uint64_t)(Lh - g);
-                Gcur += (uint64_t)s_g[gi].w_in * P.len_in[r] + (uint64_t)s_g[gi].w_out * Lh;
-                ++cnt;
-            }
-            Tsum = warp_sum(Tsum); Gcur = warp_sum(Gcur); cnt = warp_sum(cnt);
-            // task-level quantities: phi(s) sub-deadline, final deadline, JIT rate
-            const int64_t a_c = P.t_arr[t], D = P.t_dl[t];
-            const uint32_t s = P.cur_stage[t], S = P.n_stages[t];
-            uint64_t le = 0, tot = 0;
-            for (uint32_t u = 0; u < S && u < kMaxStages; ++u) {
-                const uint64_t ns = (uint64_t)P.pattern[t * kMaxStages + u] * 1000000ull;
-                tot += ns; if (u <= s) le += ns;
-            }
-            if (cnt && (tot == 0 || S == 0 || S > kMaxStages || s >= S)) my_err = 1;
-            const int64_t Ds = tot ? (int64_t)((u128)(uint64_t)D * le / tot) : 0;
-            const int64_t trem = a_c + Ds - now;
-            uint64_t Gt = P.gdone[t] + Gcur;
-            if (a_c + D <= now) Gt = 0;
-            const uint64_t t_gen = Tsum * (uint64_t)v;
-            if (c.appb && t_gen > (uint64_t)(trem > 0 ? trem : 0)) Gt = 0;
-            for (uint32_t base = b; base < e; base += 32) {          // pass 2: per-call keys
-                const uint32_t r = base + lane;
-                const bool inr = r < e;
-                bool pend = false;
-                uint64_t img = kNone;
-                uint32_t cost = 0;
-                if (inr) {
-                    const uint32_t meta = P.meta[r], aux = P.aux[r];
-                    pend = P.arr[r] <= now && m_state(meta) <= kPreempted;
-                    if (pend) {
-                        const uint64_t Gp = Gt + (uint64_t)c.delta * ((aux >> 16) / c.frame);
-                        double key;
-                        if (!make_key(Gp, t_gen, c.eps, &key)) my_err = 1;
-                        img = (uint64_t)__double_as_longlong(key);
-                        cost = token_cost(P.len_in[r], P.pre[r], c.chunk);
-                        if ((aux >> 16) < 0xFFFFu) P.aux[r] = aux + (1u << 16);
-                        if (kDebug) {
-                            const uint32_t lhat = P.lhat[r], g = P.gen[r];
-                            P.dbg_lhat[r] = lhat > g + 1 ? lhat : g + 1;
-                            P.dbg_rate[r] = make_rate(Tsum, trem);
-                            P.dbg_trem[r] = trem;
-                        }
-                    } else if (kDebug) {
-                        P.dbg_lhat[r] = 0; P.dbg_rate[r] = 0.0; P.dbg_trem[r] = 0;
-                    }
-                    P.img[r] = img; P.cost[r] = cost;
-                }
-                const bool valid = inr && pend;
-                my_pend += valid;
-                if (valid && img < my_min) my_min = img;
-                const uint32_t bin = (uint32_t)(make_ck(img, 0) >> digit_shift(0)) & 2047u;
-                warp_hist_add(s_cnt, s_cost, valid, bin, cost);
-            }
-        }
-    }
-    // ---- block reductions, histogram flush
-    my_pend = warp_sum(my_pend); my_drop = warp_sum(my_drop); my_err = __reduce_or_sync(0xffffffffu, my_err);
-    my_min = warp_min_u64(my_min);
-    if (lane == 0) {
-        atomicAdd(&s_pend, my_pend); atomicAdd(&s_drop, my_drop); atomicOr(&s_err, my_err);
-        atomicMin(&s_min, (unsigned long long)my_min);
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t wr = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); wr < P.n; wr += stride) {
+        const uint32_t r = wr + (threadIdx.x & 31);
+        uint64_t img = kNone;
+        uint32_t cost = 0;
+        if (r < P.n) { img = P.img[r]; cost = P.cost[r]; }
+        const bool valid = img != kNone;
+        const uint32_t bin = (uint32_t)(make_ck(img, 0) >> digit_shift(0)) & 2047u;
+        warp_hist_add(s_cnt, s_cost, valid, bin, cost);
     }
     __syncthreads();
-    for (uint32_t b = threadIdx.x; b < 2048; b += blockDim.x) {
+    for (uint32_t b = threadIdx.x; b < 2048; b += blockDim.x)
         if (s_cnt[b]) { atomicAdd(hcnt + b, s_cnt[b]); atomicAdd(hcost + b, (unsigned long long)s_cost[b]); }
-    }
-    if (threadIdx.x == 0) {
-        if (s_pend) atomicAdd(&ctrl->n_pending, s_pend);
-        if (s_drop) atomicAdd(&ctrl->n_dropped, s_drop);
-        if (s_err) atomicOr(&ctrl->error, 1u);
-        if (s_min != kNone) atomicMin(&ctrl->min_img, s_min);
-    }
     if (is_last_block(&ctrl->done[0])) resolve_level(c, ctrl, hcnt, hcost, 0);
 }
 
@@ -578,8 +457,9 @@ __global__ void __launch_bounds__(1024) k_resolve(Cfg c, Ctrl* ctrl, Scratch S) 
 // --------------------------------------------------------------------------------------
 // k_cand: Cd = {pending : key >= thr} (Alg. 1 Filter)
 // --------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kPassThreads) k_cand(Pool P, Ctrl* ctrl, Scratch S) {
+__global__ void __launch_bounds__(kPassThreads) k_cand(Pool P, Ctrl* ctrl, Scratch S, int only_after_fallback) {
     if (ctrl->status != ST_RESOLVED) return;
+    if (only_after_fallback && !ctrl->fallback) return;      // k_spec already produced Cd
     const uint64_t thr_img = ctrl->thr_img;
     const uint32_t stride = gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31;
@@ -632,37 +512,24 @@ __device__ __forceinline__ u128 block_exclusive_scan_u128(u128 v, u128* scratch,
 }
 
 // --------------------------------------------------------------------------------------
-// k_group: one CTA of 1024 threads -- Alg. 1 step 2 under the token budget
+// (a9) Alg. 1 step 2 under the token budget, executed by ONE CTA of 1024 threads:
+// sort Cd by (len asc, id asc), u64 prefix of costs and u128 prefix of fixed-point keys,
+// j(i) = largest window end within tau and B_max (binary search), first argmax of the window
+// score (strict '>').  sk/sv: n2 (power of two) sort slots; pc/pf: n+1 prefix slots
+// (shared memory when they fit, else global scratch).  Writes the batch and the bookkeeping
+// (ever_scheduled, Running, undo steps_waited+1) and the next step's speculative threshold.
 // --------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) k_group(Pool P, Cfg c, Ctrl* ctrl, Scratch S) {
-    if (ctrl->status != ST_RESOLVED) return;
-    extern __shared__ __align__(16) unsigned char smem[];
+__device__ void window_select(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint64_t* sk, uint32_t* sv,
+                              uint32_t n, unsigned long long* pc, u128* pf) {
     __shared__ u128 s_scan128[32];
     __shared__ uint64_t s_scan[32];
     __shared__ u128 s_best[32];
     __shared__ uint32_t s_bi[32], s_bj[32];
-    const uint32_t n = ctrl->n_cand;
-    if (ctrl->cand_overflow || n == 0) {
-        if (threadIdx.x == 0) { ctrl->error = 1; ctrl->status = ST_ERROR; }
-        return;
-    }
     uint32_t n2 = 1;
     while (n2 < n) n2 <<= 1;
-    uint64_t* sk;
-    uint32_t* sv;
-    if (n2 <= kGroupSmemSort) { sk = reinterpret_cast<uint64_t*>(smem); sv = reinterpret_cast<uint32_t*>(smem + 8 * kGroupSmemSort); }
-    else { sk = S.sk; sv = S.sv; }
-    for (uint32_t i = threadIdx.x; i < n2; i += blockDim.x) {
-        if (i < n) {
-            const uint32_t r = S.cand[i];
-            const uint64_t len = c.len_key ? (uint64_t)P.len_in[r] + P.gen[r] : (uint64_t)P.len_in[r];
-            sk[i] = (len << 32) | P.id[r];                      // (len asc, id asc), A17/A18
-            sv[i] = r;
-        } else { sk[i] = ~0ull; sv[i] = 0; }
-    }
+    for (uint32_t i = n + threadIdx.x; i < n2; i += blockDim.x) { sk[i] = ~0ull; sv[i] = 0; }
     __syncthreads();
     block_bitonic_sort<uint64_t>(sk, sv, n2);
-    // prefix sums of cost (u64) and fixed-point key (u128), chunks of blockDim with carry
     uint64_t carry_c = 0;
     u128 carry_f = 0;
     for (uint32_t base = 0; base < n; base += blockDim.x) {
@@ -676,42 +543,38 @@ __global__ void __launch_bounds__(1024) k_group(Pool P, Cfg c, Ctrl* ctrl, Scrat
         uint64_t tc; u128 tf;
         const uint64_t ec = block_exclusive_scan_u64(cv, s_scan, &tc);
         const u128 ef = block_exclusive_scan_u128(fv, s_scan128, &tf);
-        if (i < n) { S.pc[i] = carry_c + ec; S.pf[i] = carry_f + ef; }
+        if (i < n) { pc[i] = carry_c + ec; pf[i] = carry_f + ef; }
         carry_c += tc; carry_f += tf;
     }
-    if (threadIdx.x == 0) { S.pc[n] = carry_c; S.pf[n] = carry_f; }
+    if (threadIdx.x == 0) { pc[n] = carry_c; pf[n] = carry_f; }
     __syncthreads();
-    // windows: j(i) = largest j with pc[j+1]-pc[i] <= tau and j-i+1 <= B_max; first argmax
     u128 best = 0; uint32_t bi = 0xFFFFFFFFu, bj = 0;
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const uint64_t lim = (uint64_t)__ldcg(&S.pc[i]) + c.token_budget;
+        const uint64_t lim = (uint64_t)pc[i] + c.token_budget;
         uint32_t lo = i, hi = (uint32_t)min((uint64_t)n - 1, (uint64_t)i + c.max_batch - 1);
         while (lo < hi) {
             const uint32_t mid = (lo + hi + 1) >> 1;
-            if (__ldcg(&S.pc[mid + 1]) <= lim) lo = mid; else hi = mid - 1;
+            if (pc[mid + 1] <= lim) lo = mid; else hi = mid - 1;
         }
-        const u128 sc = S.pf[lo + 1] - S.pf[i];
+        const u128 sc = pf[lo + 1] - pf[i];
         if (bi == 0xFFFFFFFFu || sc > best) { best = sc; bi = i; bj = lo; }   // i increasing per thread
     }
-    // block argmax: larger score, then smaller i
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const u128 ob = shfl_xor_u128(best, o);
         const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o), oj = __shfl_xor_sync(0xffffffffu, bj, o);
-        const bool take = (oi != 0xFFFFFFFFu) && (bi == 0xFFFFFFFFu || ob > best || (ob == best && oi < bi));
-        if (take) { best = ob; bi = oi; bj = oj; }
+        if ((oi != 0xFFFFFFFFu) && (bi == 0xFFFFFFFFu || ob > best || (ob == best && oi < bi))) { best = ob; bi = oi; bj = oj; }
     }
     if (lane == 0) { s_best[wid] = best; s_bi[wid] = bi; s_bj[wid] = bj; }
     __syncthreads();
     if (wid == 0) {
-        best = lane < 32 ? s_best[lane] : (u128)0; bi = s_bi[lane]; bj = s_bj[lane];
+        best = lane < nw ? s_best[lane] : (u128)0; bi = lane < nw ? s_bi[lane] : 0xFFFFFFFFu; bj = lane < nw ? s_bj[lane] : 0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             const u128 ob = shfl_xor_u128(best, o);
             const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o), oj = __shfl_xor_sync(0xffffffffu, bj, o);
-            const bool take = (oi != 0xFFFFFFFFu) && (bi == 0xFFFFFFFFu || ob > best || (ob == best && oi < bi));
-            if (take) { best = ob; bi = oi; bj = oj; }
+            if ((oi != 0xFFFFFFFFu) && (bi == 0xFFFFFFFFu || ob > best || (ob == best && oi < bi))) { best = ob; bi = oi; bj = oj; }
         }
         if (lane == 0) { s_bi[0] = bi; s_bj[0] = bj; }
     }
@@ -723,9 +586,7 @@ __global__ void __launch_bounds__(1024) k_group(Pool P, Cfg c, Ctrl* ctrl, Scrat
         S.out_ids[k] = P.id[r];
         S.out_tokens[k] = P.cost[r];
         S.out_rows[k] = r;
-        // bookkeeping for the batch: ever_scheduled, Running; undo the steps_waited increment
-        uint32_t m = P.meta[r];
-        m |= (kEver << 12);
+        uint32_t m = P.meta[r] | (kEver << 12);
         if (m_state(m) == kQueued || m_state(m) == kPreempted) m = m_with_state(m, kRunning);
         P.meta[r] = m;
         const uint32_t aux = P.aux[r];
@@ -733,9 +594,39 @@ __global__ void __launch_bounds__(1024) k_group(Pool P, Cfg c, Ctrl* ctrl, Scrat
     }
     if (threadIdx.x == 0) {
         ctrl->n_selected = ns;
-        ctrl->total_tokens = (uint32_t)(S.pc[bj + 1] - S.pc[bi]);
+        ctrl->total_tokens = (uint32_t)(pc[bj + 1] - pc[bi]);
         ctrl->i_best = bi; ctrl->j_best = bj;
+        ctrl->window_done = 1;
+        // next step's speculative threshold: this step's cutoff with a 15% margin
+        Persist* ps = S.persist;
+        ps->t_guess = (unsigned long long)__double_as_longlong(__dmul_rn(ctrl->thr, 0.85));
+        ps->steps += 1;
+        ps->fallbacks += ctrl->fallback;
     }
+}
+
+// k_group: the window over Cd = S.cand (after the radix path or a too-large speculative Cd)
+__global__ void __launch_bounds__(1024) k_group(Pool P, Cfg c, Ctrl* ctrl, Scratch S) {
+    if (ctrl->status != ST_RESOLVED || ctrl->window_done) return;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t n = ctrl->n_cand;
+    if (ctrl->cand_overflow || n == 0) {
+        if (threadIdx.x == 0) { ctrl->error = 1; ctrl->status = ST_ERROR; }
+        return;
+    }
+    uint32_t n2 = 1;
+    while (n2 < n) n2 <<= 1;
+    uint64_t* sk;
+    uint32_t* sv;
+    if (n2 <= kGroupSmemSort) { sk = reinterpret_cast<uint64_t*>(smem); sv = reinterpret_cast<uint32_t*>(smem + 8 * kGroupSmemSort); }
+    else { sk = S.sk; sv = S.sv; }
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint32_t r = S.cand[i];
+        const uint64_t len = c.len_key ? (uint64_t)P.len_in[r] + P.gen[r] : (uint64_t)P.len_in[r];
+        sk[i] = (len << 32) | P.id[r];                      // (len asc, id asc), A17/A18
+        sv[i] = r;
+    }
+    window_select(P, c, ctrl, S, sk, sv, n, S.pc, S.pf);
 }
 
 // progress updates from the engine, applied before scoring

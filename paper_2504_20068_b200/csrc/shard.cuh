@@ -10,7 +10,7 @@
 //           every rank runs the same window (a9) on it -> identical batch everywhere.
 // The exchanges themselves are NCCL allgathers issued by the caller (torch.distributed).
 #pragma once
-#include "pool.cuh"
+#include "select.cuh"
 
 namespace jit {
 

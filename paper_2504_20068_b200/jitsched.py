@@ -17,7 +17,9 @@ LIB_PATH = os.path.join(_HERE, "libjitsched.so")
 
 JIT_OK, JIT_EMPTY = 0, 1
 JIT_CFG_DEBUG_ROWS = 1
+JIT_CFG_NO_GRAPH = 2        # env JITSCHED_NO_GRAPH=1: direct launches (for ncu)
 NO_TASK = 0xFFFFFFFF
+REC1_BYTES, REC2_BYTES = 16, 32      # jit_rec1 / jit_rec2
 
 
 class JitSchedError(RuntimeError):
@@ -66,7 +68,8 @@ class jit_step_in(C.Structure):
 class jit_batch(C.Structure):
     _fields_ = [("capacity", C.c_uint32), ("n_selected", C.c_uint32), ("total_tokens", C.c_uint32),
                 ("n_candidates", C.c_uint32), ("b_star", C.c_uint32), ("n_pending", C.c_uint32),
-                ("n_dropped", C.c_uint32), ("status", C.c_uint32), ("bp", C.c_double), ("thr", C.c_double),
+                ("n_dropped", C.c_uint32), ("status", C.c_uint32), ("n_refresh", C.c_uint32),
+                ("fallback", C.c_uint32), ("reserved", C.c_uint32), ("bp", C.c_double), ("thr", C.c_double),
                 ("ids", C.c_void_p), ("tokens", C.c_void_p), ("rows", C.c_void_p)]
 
 
@@ -104,7 +107,7 @@ _lib = None
 EXPORTS = ("jit_sched_workspace_bytes", "jit_sched_init", "jit_sched_load", "jit_sched_step",
            "jit_sched_step_async", "jit_sched_fetch_batch", "jit_sched_read_rows", "jit_sched_kernel_times",
            "jit_replay_workspace_bytes", "jit_sched_replay", "jit_sched_destroy", "jit_sched_last_error",
-           "jit_sched_version")
+           "jit_sched_version", "jit_shard_prefix", "jit_shard_merge", "jit_shard_candidates", "jit_shard_finish")
 
 
 def load_library(path: str = LIB_PATH):
@@ -149,7 +152,7 @@ def make_config(cfg: dict, capacity: int, task_capacity: int, device: int = 0, s
     c.waiting_ns = int(cfg["waiting_ns"])
     c.capacity = int(capacity)
     c.task_capacity = int(task_capacity)
-    c.flags = JIT_CFG_DEBUG_ROWS if debug else 0
+    c.flags = (JIT_CFG_DEBUG_ROWS if debug else 0) | (JIT_CFG_NO_GRAPH if os.environ.get("JITSCHED_NO_GRAPH") else 0)
     c.device = int(device)
     c.stream = stream
     return c
@@ -281,7 +284,8 @@ class Scheduler:
         k = b.n_selected
         return {"status": rc, "n_pending": b.n_pending, "n_selected": k, "total_tokens": b.total_tokens,
                 "n_candidates": b.n_candidates, "b_star": b.b_star, "n_dropped_now": b.n_dropped, "bp": b.bp,
-                "thr": b.thr, "batch_ids": self._ids[:k].copy(), "batch_tokens": self._tok[:k].copy(),
+                "thr": b.thr, "n_refresh": b.n_refresh, "fallback": b.fallback,
+                "batch_ids": self._ids[:k].copy(), "batch_tokens": self._tok[:k].copy(),
                 "batch_rows": self._rows[:k].copy()}
 
     def read_rows(self, debug: bool = True) -> dict:
@@ -304,6 +308,34 @@ class Scheduler:
         t = (C.c_float * 5)()
         self._check(self.lib.jit_sched_kernel_times(self.h, C.c_int(-1), t, 5), self.h)
         return list(t)
+
+    # ------------------------------------------------------------------ sharded step
+    def shard_prefix(self, now_ns: int, v_token_ns: int, rec1) -> int:
+        n = C.c_uint32()
+        cap = rec1.numel() // REC1_BYTES
+        self._check(self.lib.jit_shard_prefix(self.h, C.c_int64(now_ns), C.c_int64(v_token_ns),
+                                              C.c_void_p(rec1.data_ptr()), C.c_uint32(cap), C.byref(n)), self.h)
+        return int(n.value)
+
+    def shard_merge(self, all_rec1):
+        self._check(self.lib.jit_shard_merge(self.h, C.c_void_p(all_rec1.data_ptr()),
+                                             C.c_uint32(all_rec1.numel() // REC1_BYTES)), self.h)
+
+    def shard_candidates(self, rec2, rank: int) -> int:
+        n = C.c_uint32()
+        self._check(self.lib.jit_shard_candidates(self.h, C.c_void_p(rec2.data_ptr()),
+                                                  C.c_uint32(rec2.numel() // REC2_BYTES), C.c_uint32(rank),
+                                                  C.byref(n)), self.h)
+        return int(n.value)
+
+    def shard_finish(self, all_rec2, rank: int) -> dict:
+        b = jit_batch()
+        b.capacity = self.max_batch
+        b.ids, b.tokens, b.rows = _p(self._ids), _p(self._tok), _p(self._rows)
+        rc = self._check(self.lib.jit_shard_finish(self.h, C.c_void_p(all_rec2.data_ptr()),
+                                                   C.c_uint32(all_rec2.numel() // REC2_BYTES), C.c_uint32(rank),
+                                                   C.byref(b)), self.h)
+        return self._batch_dict(rc, b)
 
     # ------------------------------------------------------------------ replay
     def replay(self, traces, specs, rcfg: dict, log_steps: int = 0):
