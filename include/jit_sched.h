@@ -145,7 +145,8 @@ typedef struct jit_batch {
     uint32_t capacity;
     uint32_t n_selected, total_tokens, n_candidates, b_star, n_pending, n_dropped, status;
     uint32_t n_refresh;            /* length bounds recomputed this step (the rest hit the cache) */
-    uint32_t fallback, reserved;   /* 1: the exact radix path ran instead of the speculative set */
+    uint32_t fallback;             /* 1: the exact radix path ran instead of the speculative set */
+    uint32_t n_spec;               /* size of the speculative set {key >= t_guess} */
     double bp, thr;                /* batch priority and cutoff threshold fl(p * bp) */
     uint32_t* ids;
     uint32_t* tokens;
@@ -184,6 +185,11 @@ int jit_sched_read_rows(jit_sched* h, double* key, double* rate, int64_t* t_rem,
  * `enable` steps; 0 turns timing off; < 0 leaves it unchanged.  ms_out (n_out <= 5) gets the
  * average in ms over the recorded steps of [score, select, candidates, group, whole step]. */
 int jit_sched_kernel_times(jit_sched* h, int enable, float* ms_out, uint32_t n_out);
+
+/* Diagnostics: %globaltimer stamps (ns) of the phases of the single-CTA resolve of the last
+ * synchronized step: [k_spec start, partials reduced, set loaded, set sorted, budget walk,
+ * Cd gathered, window sort start, window sorted, prefix sums, argmax, batch written]. */
+int jit_sched_phase_times(jit_sched* h, uint64_t* ns_out, uint32_t n_out);
 
 /* ---------------------------------------------------------------------------------------
  * Trace replay (a10): one persistent CTA per replay runs the step, the iteration cost model

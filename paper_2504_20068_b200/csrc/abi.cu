@@ -46,7 +46,7 @@ struct jit_sched {
     std::vector<cudaEvent_t> slots;       // 5 events per recorded step
     uint32_t n_slots = 0, slot_used = 0;
     int n_sm = 148;
-    uint32_t nb_score = 1, nb_ckey = 1, grid_pass = 1;
+    uint32_t nb_score = 1, nb_ctask = 1, nb_full = 1, grid_pass = 1;
     std::string err;
 };
 
@@ -204,7 +204,8 @@ extern "C" int jit_sched_init(const jit_config* cfg, const jit_slo_group* groups
     // between consecutive kernels costs a drain + reconfiguration of the SMs (several µs each)
     {
         const void* ks[] = {(const void*)k_begin, (const void*)k_score<false>, (const void*)k_score<true>,
-                            (const void*)k_ckey<false>, (const void*)k_ckey<true>, (const void*)k_spec,
+                            (const void*)k_ctask, (const void*)k_ckey_full<false>,
+                            (const void*)k_ckey_full<true>, (const void*)k_spec,
                             (const void*)k_hist0, (const void*)k_pass, (const void*)k_compact, (const void*)k_resolve,
                             (const void*)k_cand, (const void*)k_group};
         for (const void* k : ks)
@@ -265,13 +266,21 @@ extern "C" int jit_sched_load(jit_sched* h, const jit_pool* p) {
     CK(cudaStreamSynchronize(h->stream));
     if (h->h_ctrl->error) { h->loaded = false; return set_err(h, JIT_EINVAL, "invalid pool (layout / ranges / groups)"); }
     // launch geometry
-    // rows: grid-stride over a persistent-style grid (6 CTAs of 256 per SM); tasks: warp per task
-    h->nb_score = std::max<uint32_t>(1, std::min<uint32_t>((P.n + kScoreThreads - 1) / kScoreThreads, (uint32_t)h->n_sm * 6));
-    h->nb_ckey = std::max<uint32_t>(1, std::min<uint32_t>((P.n - P.n_single + kScoreThreads - 1) / kScoreThreads,
-                                                          (uint32_t)h->n_sm * 4));
+    // rows: grid-stride over a persistent-style grid (6 CTAs of 256 per SM); tasks: thread per
+    // task (k_ctask); compound rows: grid-stride (k_ckey_full)
+    // one wave: the persistent grid is exactly what fits (registers bound k_score's occupancy)
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &occ, h->debug ? (const void*)k_score<true> : (const void*)k_score<false>, kScoreThreads, 0));
+    occ = std::max(occ, 1);
+    h->nb_score = std::max<uint32_t>(1, std::min<uint32_t>((P.n + kScoreThreads - 1) / kScoreThreads, (uint32_t)(h->n_sm * occ)));
+    h->nb_ctask = std::max<uint32_t>(1, std::min<uint32_t>((P.n_tasks + kScoreThreads - 1) / kScoreThreads,
+                                                           (uint32_t)h->n_sm * 4));
+    h->nb_full = std::max<uint32_t>(1, std::min<uint32_t>((P.n - P.n_single + kScoreThreads - 1) / kScoreThreads,
+                                                          (uint32_t)h->n_sm * 6));
     h->nb_score = std::min(h->nb_score, kMaxParts);
-    h->nb_ckey = std::min(h->nb_ckey, kMaxParts);
-    h->S.n_part = h->nb_score; h->S.n_part2 = h->nb_ckey;
+    h->nb_ctask = std::min(h->nb_ctask, kMaxParts);
+    h->S.n_part = h->nb_score; h->S.n_part2 = h->nb_ctask;
     h->arg_ntasks = P.n_tasks;
     h->grid_pass = std::max<uint32_t>(1, std::min<uint32_t>((P.n + kPassThreads - 1) / kPassThreads, (uint32_t)h->n_sm * 4));
     if (!same_shape) h->graph_dirty = true;
@@ -289,8 +298,9 @@ static void enqueue_score(jit_sched* h, cudaStream_t s, int64_t now, int64_t v, 
     if (h->debug) k_score<true><<<h->nb_score, kScoreThreads, 0, s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S);
     else k_score<false><<<h->nb_score, kScoreThreads, 0, s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S);
     if (mid) cudaEventRecordWithFlags(mid, s, capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
-    if (h->debug) k_ckey<true><<<h->nb_ckey, kScoreThreads, 0, s>>>(P, h->c, h->d_ctrl, S);
-    else k_ckey<false><<<h->nb_ckey, kScoreThreads, 0, s>>>(P, h->c, h->d_ctrl, S);
+    k_ctask<<<h->nb_ctask, kScoreThreads, 0, s>>>(P, h->c, h->d_ctrl, S);
+    // debug: every compound call gets its key and rate outputs now (read_rows sees them all)
+    if (h->debug) k_ckey_full<true><<<h->nb_full, kScoreThreads, 0, s>>>(P, h->c, h->d_ctrl, S, 1);
     (void)now; (void)v;
 }
 
@@ -300,6 +310,9 @@ static void enqueue_radix(jit_sched* h, cudaStream_t s, int force_hist0, uint32_
                           int only_after_fallback) {
     Pool& P = h->P;
     Scratch& S = h->S;
+    // the radix path reads every key image: first key the compound calls k_ctask left tagged
+    if (force_hist0 >= 0 && P.n_single < P.n)
+        k_ckey_full<false><<<h->nb_full, kScoreThreads, 0, s>>>(P, h->c, h->d_ctrl, S, force_hist0);
     if (force_hist0 >= 0) k_hist0<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->c, h->d_ctrl, S.hcnt, S.hcost, force_hist0);
     for (uint32_t i = 0; i < n_passes; ++i)
         k_pass<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->c, h->d_ctrl, S.hcnt, S.hcost, first_pass + i);
@@ -328,15 +341,22 @@ static int build_graph(jit_sched* h) {
     size_t nd = 0;
     CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &cg, &deps, &nd));
     const bool flat = getenv("JITSCHED_FLAT_GRAPH") != nullptr;   // A/B switch: no conditional node
+    // overhead attribution only (profiles/host_overhead.py; results are NOT valid with these):
+    // bit 0 drops the fallback body, bit 1 the ctrl read-back, bit 2 adds one empty kernel node
+    const char* xe = getenv("JITSCHED_EXPERIMENT");
+    const int xm = xe ? atoi(xe) : 0;
     cudaGraphConditionalHandle hc = 0;
-    if (!flat) CK(cudaGraphConditionalHandleCreate(&hc, cg, 0, cudaGraphCondAssignDefault));
+    if (!flat && !(xm & 1)) CK(cudaGraphConditionalHandleCreate(&hc, cg, 0, cudaGraphCondAssignDefault));
     k_begin<<<4, 1024, 0, s>>>(h->d_ctrl, S.hcnt, S.hcost, 0, 1, S.tacc, h->arg_ntasks);
+    if (xm & 4) k_ckey_full<false><<<1, 32, 0, s>>>(h->P, h->c, h->d_ctrl, S, 0);   // exits at once
     if (h->timing) cudaEventRecordWithFlags(h->ev[0], s, cudaEventRecordExternal);
     enqueue_score(h, s, 0, 1, h->timing ? h->ev[1] : nullptr, true);
     if (h->timing) cudaEventRecordWithFlags(h->ev[2], s, cudaEventRecordExternal);
-    k_spec<<<1, kSpecThreads, (sizeof(u128) + 4) * kSpecCap, s>>>(h->P, h->c, h->d_ctrl, S, hc, flat ? 0 : 1, 0);
+    k_spec<<<1, kSpecThreads, (sizeof(u128) + 4) * kSpecCap, s>>>(h->P, h->c, h->d_ctrl, S, hc,
+                                                                  (flat || (xm & 1)) ? 0 : 1, 0);
     if (h->timing) cudaEventRecordWithFlags(h->ev[3], s, cudaEventRecordExternal);
-    if (flat) {
+    if (xm & 1) {
+    } else if (flat) {
         enqueue_radix(h, s, 0, 0, 1, 1);      // every kernel checks the status and exits when idle
         enqueue_tail(h, s);
     } else {
@@ -356,7 +376,7 @@ static int build_graph(jit_sched* h) {
         CK(cudaStreamUpdateCaptureDependencies(s, &cnode, 1, cudaStreamSetCaptureDependencies));
     }
     if (h->timing) cudaEventRecordWithFlags(h->ev[4], s, cudaEventRecordExternal);
-    cudaMemcpyAsync(h->h_ctrl, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s);
+    if (!(xm & 2)) cudaMemcpyAsync(h->h_ctrl, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s);
     CK(cudaStreamEndCapture(s, &g));
     size_t nn = 0;
     CK(cudaGraphGetNodes(g, nullptr, &nn));
@@ -454,7 +474,7 @@ static int finish_step(jit_sched* h, jit_batch* out) {
     if (c.status == ST_ERROR || c.error) return set_err(h, JIT_EINVAL, "step: invalid input (error code %u)", c.error);
     if (out) {
         out->n_pending = c.n_pending; out->n_dropped = c.n_dropped; out->status = c.status;
-        out->n_refresh = c.n_refresh; out->fallback = c.fallback;
+        out->n_refresh = c.n_refresh; out->fallback = c.fallback; out->n_spec = c.spec_n;
         out->n_selected = 0; out->total_tokens = 0; out->n_candidates = 0; out->b_star = 0; out->bp = 0; out->thr = 0;
     }
     if (c.status == ST_EMPTY) return JIT_EMPTY;
@@ -510,6 +530,11 @@ extern "C" int jit_sched_read_rows(jit_sched* h, double* key, double* rate, int6
     if (!h->loaded) return set_err(h, JIT_ESTATE, "read_rows before load");
     const uint64_t n = h->P.n;
     if ((rate || t_rem || lhat) && !h->debug) return set_err(h, JIT_ESTATE, "rate/t_rem/lhat need JIT_CFG_DEBUG_ROWS");
+    // compound calls of tasks that could not reach the batch still carry their frame tag
+    // (k_ctask); key them from the last step's task accumulators (idempotent)
+    if ((key || pending) && h->P.n_single < h->P.n)
+        k_ckey_full<false><<<h->nb_full, kScoreThreads, 0, h->stream>>>(h->P, h->c, h->d_ctrl, h->S, 1);
+    CK(cudaGetLastError());
     CK(cudaStreamSynchronize(h->stream));
     std::vector<uint64_t> img;
     if (key || pending) {
@@ -535,7 +560,7 @@ extern "C" int jit_sched_read_rows(jit_sched* h, double* key, double* rate, int6
 extern "C" int jit_sched_kernel_times(jit_sched* h, int enable, float* ms_out, uint32_t n_out) {
     // enable > 0: record per-kernel events for up to `enable` steps (ring of event slots);
     // enable = 0: off; enable < 0: leave as is.  ms_out gets the AVERAGE over the recorded
-    // steps of [k_score, k_ckey, k_spec (+ in-CTA window), fallback body (radix path + k_group), chain].
+    // steps of [k_score, k_ctask, k_spec (+ in-CTA window), fallback body (radix path + k_group), chain].
     if (!h) return JIT_EINVAL;
     if (enable >= 0) {
         CK(cudaStreamSynchronize(h->stream));
@@ -557,13 +582,20 @@ extern "C" int jit_sched_kernel_times(jit_sched* h, int enable, float* ms_out, u
             cudaEvent_t* e = &h->slots[5 * k];
             float t;
             CK(cudaEventElapsedTime(&t, e[0], e[1])); acc[0] += t;   // k_score
-            CK(cudaEventElapsedTime(&t, e[1], e[2])); acc[1] += t;   // k_ckey
+            CK(cudaEventElapsedTime(&t, e[1], e[2])); acc[1] += t;   // k_ctask
             CK(cudaEventElapsedTime(&t, e[2], e[3])); acc[2] += t;   // k_spec + window
             CK(cudaEventElapsedTime(&t, e[3], e[4])); acc[3] += t;   // conditional fallback body
             CK(cudaEventElapsedTime(&t, e[0], e[4])); acc[4] += t;   // total
         }
         for (uint32_t i = 0; i < n_out && i < 5; ++i) ms_out[i] = (float)(acc[i] / ns);
     }
+    return JIT_OK;
+}
+
+extern "C" int jit_sched_phase_times(jit_sched* h, uint64_t* ns_out, uint32_t n_out) {
+    if (!h || !ns_out) return JIT_EINVAL;
+    CK(cudaStreamSynchronize(h->stream));
+    for (uint32_t i = 0; i < n_out && i < 11; ++i) ns_out[i] = h->h_ctrl->ts[i];
     return JIT_OK;
 }
 
@@ -607,6 +639,7 @@ extern "C" int jit_shard_prefix(jit_sched* h, int64_t now_ns, int64_t v_token_ns
     // k_spec reduces the scoring partials (n_pending, min key, ...); its speculative result is
     // then superseded by the forced radix resolve below, which the round-1 export needs
     k_spec<<<1, kSpecThreads, (sizeof(u128) + 4) * kSpecCap, s>>>(P, h->c, h->d_ctrl, S, 0, 0, 1);
+    if (P.n_single < P.n) k_ckey_full<false><<<h->nb_full, kScoreThreads, 0, s>>>(P, h->c, h->d_ctrl, S, 1);
     k_hist0<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->c, h->d_ctrl, S.hcnt, S.hcost, 1);
     for (uint32_t i = 0; i < kLevels - 1; ++i)
         k_pass<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->c, h->d_ctrl, S.hcnt, S.hcost, i);

@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                 for (uint32_t i = np + threadIdx.x; i < n2; i += blockDim.x) { bA[i] = ~(u128)0; bAv[i] = 0; }
             }
             __syncthreads();
-            block_bitonic_sort<u128>(bA, bAv, n2);
+            block_sort<u128>(bA, bAv, n2);
             // B* = longest prefix within tau and B_max (monotone predicate -> count)
             {
                 uint64_t carry = 0;
@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
             }
             __syncthreads();
             // ---- (a9) sort Cd by (len, id); windows within tau / B_max; first argmax
-            block_bitonic_sort<uint64_t>(bB, bBv, m2);
+            block_sort<uint64_t>(bB, bBv, m2);
             unsigned long long* pc = in_smem ? reinterpret_cast<unsigned long long*>(sA) : S.gpc;   // reuse region A
             u128* pf = in_smem ? reinterpret_cast<u128*>(sbuf + ((8 * (kReplaySmemRows + 1) + 15) & ~15u)) : S.gpf;
             {

@@ -7,7 +7,9 @@
 //            call goodput) to their task's accumulators through a segmented warp reduction
 //            (tasks are contiguous row ranges), i.e. (a4) is row-parallel whatever the fan-out.
 //            Per-CTA partial counts go to an array (no global atomics on a shared line).
-//   k_ckey   every compound call: its task's aggregate key (a4/a5) from the accumulators.
+//   k_ctask  every task: its aggregate goodput / t_gen (a4/a5), min / max call key; keys the
+//            calls of tasks that can reach the speculative set.
+//   k_ckey_full  keys the remaining compound calls (fallback body, debug, shard path).
 //   k_spec   one CTA: exact B*, bp, thr, Cd from the speculative set.
 #pragma once
 #include "select.cuh"
@@ -80,8 +82,11 @@ __device__ __forceinline__ bool score_call(const Cfg& c, const Table& T, const G
     return true;
 }
 
+#ifndef JIT_SCORE_MINB
+#define JIT_SCORE_MINB 1
+#endif
 template <bool kDebug>
-__global__ void __launch_bounds__(kScoreThreads) k_score(Pool P, Table T, const Group* groups, uint32_t n_groups,
+__global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P, Table T, const Group* groups, uint32_t n_groups,
                                                          Cfg c, Ctrl* ctrl, Scratch S) {
     __shared__ GroupFast s_g[256];
     for (uint32_t gi = threadIdx.x; gi < n_groups; gi += blockDim.x) s_g[gi] = make_fast(groups[gi]);
@@ -117,6 +122,7 @@ __global__ void __launch_bounds__(kScoreThreads) k_score(Pool P, Table T, const 
         uint64_t img = kNone;
         bool valid = false;
         uint64_t vT = 0, vG = 0;                       // compound contributions
+        uint32_t fr = 0;
         uint32_t key_task = kNoTask;
         if (act && r < ns) {
             RowRes o;
@@ -140,29 +146,44 @@ __global__ void __launch_bounds__(kScoreThreads) k_score(Pool P, Table T, const 
             uint64_t len_rem, Gc;
             const bool pend = score_call<kDebug>(c, T, s_g, n_groups, now, a_arr, a_li, a_g, a_pr, a_lh, a_me, a_ax,
                                                  o_lhat, o_meta, w_lh, len_rem, Gc, cost, Lh, err);
-            P.cost[r] = cost;                          // > 0 marks a pending call for k_ckey
+            P.cost[r] = cost;                          // > 0 marks a pending call
             if (w_lh) { P.lhat[r] = o_lhat; if (o_meta != a_me) P.meta[r] = o_meta; }
             if (kDebug) P.dbg_lhat[r] = pend ? Lh : 0;
             my_err |= err; my_ref += w_lh;
-            if (pend) { my_pend += 1; my_cost += cost; vT = len_rem; vG = Gc; }
+            if (pend) {
+                // the key needs the task's sums: park floor(waited/Delta) (pre-increment value)
+                // in the key slot and do steps_waited+1 here (the task pass never touches aux)
+                fr = fastdiv(a_ax >> 16, c.frame, c.F_m, c.F_l);
+                P.img[r] = kFramesTag | fr;
+                if ((a_ax >> 16) < 0xFFFFu) P.aux[r] = a_ax + (1u << 16);
+                my_pend += 1; my_cost += cost; vT = len_rem; vG = Gc;
+            } else {
+                P.img[r] = kNone;
+            }
             key_task = (a_tk < P.n_tasks) ? a_tk : kNoTask;
             if (a_tk >= P.n_tasks) my_err = 1;
         }
-        // segmented warp reduction of (len_rem, goodput) per task (rows of a task are contiguous);
-        // warps that hold no compound call skip it (warp-uniform)
+        // segmented warp reduction per task (rows of a task are contiguous) of the sums of
+        // (len_rem, goodput) and the min / max starvation frames; warps that hold no compound
+        // call skip it (warp-uniform)
         if (any_compound && __any_sync(0xffffffffu, key_task != kNoTask)) {
             uint64_t sT = vT, sG = vG;
+            uint32_t fx = vT ? fr : 0u, fn = vT ? fr : 0xFFFFFFFFu;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
                 const uint64_t uT = __shfl_up_sync(0xffffffffu, sT, d);
                 const uint64_t uG = __shfl_up_sync(0xffffffffu, sG, d);
+                const uint32_t ux = __shfl_up_sync(0xffffffffu, fx, d);
+                const uint32_t un = __shfl_up_sync(0xffffffffu, fn, d);
                 const uint32_t uk = __shfl_up_sync(0xffffffffu, key_task, d);
-                if (lane >= d && uk == key_task) { sT += uT; sG += uG; }
+                if (lane >= d && uk == key_task) { sT += uT; sG += uG; fx = max(fx, ux); fn = min(fn, un); }
             }
             const uint32_t nk = __shfl_down_sync(0xffffffffu, key_task, 1);
-            if (key_task != kNoTask && (lane == 31 || nk != key_task) && (sT | sG)) {
+            if (key_task != kNoTask && (lane == 31 || nk != key_task) && sT) {
                 atomicAdd(&S.tacc[key_task].T, (unsigned long long)sT);
                 atomicAdd(&S.tacc[key_task].G, (unsigned long long)sG);
+                atomicMax(&S.tacc[key_task].fmax, fx);
+                atomicMin(&S.tacc[key_task].fmin, fn);
             }
         }
         spec_add(ctrl, S, P.id, valid, img, r, t_guess);
@@ -172,27 +193,34 @@ __global__ void __launch_bounds__(kScoreThreads) k_score(Pool P, Table T, const 
 }
 
 // --------------------------------------------------------------------------------------
-// k_ckey: per compound call, its task's key (a4/a5): G_task = goodput_done + sum of the
-// current stage's pending call goodput (zero once a_c + D has passed), t_gen = (sum len_rem)
-// * v_token; key = (G_task + delta*floor(waited/Delta)) * 1e9 / (t_gen + eps).
+// k_ctask: one thread per task (a4/a5).  G_task = goodput_done + sum of the current stage's
+// pending call goodput (zero once a_c + D has passed, A43), t_gen = (sum len_rem) * v_token;
+// the key of call i is (G_task + delta*floor(waited_i/Delta)) * 1e9 / (t_gen + eps).  The key
+// is non-decreasing in the frame count, so the task's extreme keys come from its min / max
+// frames (k_score): kmin feeds the pool minimum exactly, and only a task whose kmax reaches
+// the speculative threshold ("hot") has its calls keyed here -- by one warp, lanes over the
+// calls, so the speculative-set ballot stays convergent.  Every other call keeps its tagged
+// frame count until k_ckey_full (fallback body / debug / shard path) keys it.
 // --------------------------------------------------------------------------------------
-template <bool kDebug>
-__global__ void __launch_bounds__(kScoreThreads) k_ckey(Pool P, Cfg c, Ctrl* ctrl, Scratch S) {
+__device__ __forceinline__ bool is_frames_tag(uint64_t img) {
+    return (img & 0xFFF8000000000000ull) == kFramesTag;
+}
+
+__global__ void __launch_bounds__(kScoreThreads) k_ctask(Pool P, Cfg c, Ctrl* ctrl, Scratch S) {
     const int64_t now = ctrl->now, v = ctrl->v;
     const uint64_t t_guess = S.persist->t_guess;
+    const int lane = threadIdx.x & 31;
     uint32_t my_err = 0;
     uint64_t my_min = kNone;
-    const uint32_t n = P.n;
+    const uint32_t nt = P.n_tasks;
     const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t wr = P.n_single + blockIdx.x * blockDim.x + (threadIdx.x & ~31u); wr < n; wr += stride) {
-        const uint32_t r = wr + (threadIdx.x & 31);
-        uint64_t img = kNone;
-        bool valid = false;
-        if (r < n) {
-            // issue the three per-row loads together; the task-level loads follow in one round
-            const uint32_t cost = P.cost[r], t = __ldg(P.task + r), aux = P.aux[r];
-            if (cost) {
-                const TaskAcc acc = S.tacc[t];
+    for (uint32_t wt = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); wt < nt; wt += stride) {
+        const uint32_t t = wt + lane;
+        bool hot = false;
+        uint64_t Gt = 0, t_gen = 0;
+        if (t < nt) {
+            const TaskAcc acc = S.tacc[t];
+            if (acc.T) {
                 const int64_t a_c = __ldg(P.t_arr + t), D = __ldg(P.t_dl + t);
                 const uint32_t s = __ldg(P.cur_stage + t), Sn = __ldg(P.n_stages + t);
                 const uint4 p0 = __ldg(reinterpret_cast<const uint4*>(P.pattern) + 2 * t);
@@ -211,26 +239,75 @@ __global__ void __launch_bounds__(kScoreThreads) k_ckey(Pool P, Cfg c, Ctrl* ctr
                     : ((uint64_t)D < (1ull << 40) && tot < (1ull << 24)) ? (int64_t)((uint64_t)D * le / tot)
                                                                          : (int64_t)((u128)(uint64_t)D * le / tot);
                 const int64_t trem = a_c + Ds - now;               // advisory stage deadline
-                uint64_t Gt = __ldg(P.gdone + t) + acc.G;
+                Gt = __ldg(P.gdone + t) + acc.G;
                 if (a_c + D <= now) Gt = 0;                         // final deadline passed
-                const uint64_t t_gen = acc.T * (uint64_t)v;
+                t_gen = acc.T * (uint64_t)v;
                 if (c.appb && t_gen > (uint64_t)(trem > 0 ? trem : 0)) Gt = 0;
-                const uint64_t Gp = Gt + (uint64_t)c.delta * fastdiv(aux >> 16, c.frame, c.F_m, c.F_l);
-                double key;
-                if (!make_key(Gp, t_gen, c.eps, &key)) my_err = 1;
-                img = (uint64_t)__double_as_longlong(key);
-                valid = true;
-                if ((aux >> 16) < 0xFFFFu) P.aux[r] = aux + (1u << 16);
-                if (kDebug) { P.dbg_rate[r] = make_rate(acc.T, trem); P.dbg_trem[r] = trem; }
-                if (img < my_min) my_min = img;
-            } else if (kDebug) {
-                P.dbg_rate[r] = 0.0; P.dbg_trem[r] = 0;
+                double kmin, kmax;
+                const bool ok_min = make_key(Gt + (uint64_t)c.delta * acc.fmin, t_gen, c.eps, &kmin);
+                const bool ok_max = make_key(Gt + (uint64_t)c.delta * acc.fmax, t_gen, c.eps, &kmax);
+                if (!ok_min || !ok_max) my_err = 1;
+                const uint64_t imin = (uint64_t)__double_as_longlong(kmin);
+                const uint64_t imax = (uint64_t)__double_as_longlong(kmax);
+                if (imin < my_min) my_min = imin;
+                hot = ok_max && imax >= t_guess;
+                S.tacc[t].Gt = Gt; S.tacc[t].tgen = t_gen; S.tacc[t].trem = trem;
             }
-            P.img[r] = img;
         }
-        spec_add(ctrl, S, P.id, valid, img, r, t_guess);
+        // hot tasks: the warp keys their calls together (speculative-set ballot convergent)
+        unsigned hm = __ballot_sync(0xffffffffu, hot);
+        while (hm) {
+            const int src = __ffs(hm) - 1;
+            hm &= hm - 1;
+            const uint32_t ht = __shfl_sync(0xffffffffu, t, src);
+            const uint64_t hG = __shfl_sync(0xffffffffu, Gt, src);
+            const uint64_t hB = __shfl_sync(0xffffffffu, t_gen, src);
+            const uint32_t r0 = __ldg(P.call_off + ht), r1 = __ldg(P.call_off + ht + 1);
+            for (uint32_t wr = r0; wr < r1; wr += 32) {
+                const uint32_t r = wr + lane;
+                uint64_t img = kNone;
+                bool valid = false;
+                if (r < r1) {
+                    img = P.img[r];
+                    if (is_frames_tag(img)) {
+                        const uint32_t fr = (uint32_t)(img & 0xFFFFFFFFu);
+                        double key;
+                        make_key(hG + (uint64_t)c.delta * fr, hB, c.eps, &key);
+                        img = (uint64_t)__double_as_longlong(key);
+                        P.img[r] = img;
+                        valid = true;
+                    }
+                }
+                spec_add(ctrl, S, P.id, valid, img, r, t_guess);
+            }
+        }
     }
     store_part(S.part2, 0, 0, my_err, my_min, 0, 0);
+}
+
+// k_ckey_full: row-parallel keying of every call still carrying its frame tag (after
+// k_ctask); in debug mode also the per-call rate / t_rem outputs of every compound row.
+template <bool kDebug>
+__global__ void __launch_bounds__(kScoreThreads) k_ckey_full(Pool P, Cfg c, Ctrl* ctrl, Scratch S, int force) {
+    if (!force && ctrl->status != ST_FALLBACK) return;
+    const uint32_t n = P.n;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t r = P.n_single + blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride) {
+        const uint64_t img = P.img[r];
+        const bool tagged = is_frames_tag(img);
+        if (!tagged && !kDebug) continue;
+        const uint32_t t = __ldg(P.task + r);
+        if (t >= P.n_tasks) continue;
+        if (tagged) {
+            double key;
+            make_key(S.tacc[t].Gt + (uint64_t)c.delta * (uint32_t)(img & 0xFFFFFFFFu), S.tacc[t].tgen, c.eps, &key);
+            P.img[r] = (uint64_t)__double_as_longlong(key);
+        }
+        if (kDebug) {
+            if (P.cost[r]) { P.dbg_rate[r] = make_rate(S.tacc[t].T, S.tacc[t].trem); P.dbg_trem[r] = S.tacc[t].trem; }
+            else { P.dbg_rate[r] = 0.0; P.dbg_trem[r] = 0; }
+        }
+    }
 }
 
 // --------------------------------------------------------------------------------------
@@ -246,7 +323,7 @@ constexpr uint32_t kWinPcOff = (8 * kSpecWindow + 15) & ~15u;
 constexpr uint32_t kWinPfOff = (kWinPcOff + 8 * (kSpecWindow + 1) + 15) & ~15u;
 static_assert(kWinPfOff + 16 * (kSpecWindow + 1) <= 16 * kSpecCap, "window arrays must fit the sort-key region");
 
-constexpr uint32_t kSpecThreads = 256;        // small CTA: the sets are small and every idle warp costs issue slots
+constexpr uint32_t kSpecThreads = 512;        // sets up to 512 sort in registers/shuffles (block_sort_reg)
 __global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl, Scratch S,
                                                cudaGraphConditionalHandle fb_handle, int in_graph, int reduce_only) {
     const uint32_t* __restrict__ cost_rows = P.cost;
@@ -257,9 +334,10 @@ __global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl
     __shared__ unsigned long long s_min, s_cost;
     __shared__ uint32_t s_pend, s_drop, s_err, s_ref;
     __shared__ int s_fb;
+    stamp(ctrl, 0);
     if (threadIdx.x == 0) { s_min = kNone; s_cost = 0; s_pend = 0; s_drop = 0; s_err = 0; s_ref = 0; }
     __syncthreads();
-    {   // partials of k_score and k_ckey
+    {   // partials of k_score and k_ctask
         uint32_t pend = 0, drop = 0, err = 0, ref = 0;
         uint64_t mn = kNone, cost = 0;
         for (uint32_t i = threadIdx.x; i < S.n_part + S.n_part2; i += blockDim.x) {
@@ -281,6 +359,7 @@ __global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl
         }
     }
     if (reduce_only) return;                               // sharded step: the radix path follows
+    stamp(ctrl, 1);
     const uint32_t n = ctrl->spec_n, np = s_pend;
     if (threadIdx.x == 0) {
         s_fb = 0;
@@ -303,7 +382,9 @@ __global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl
         else { sk[i] = ~(u128)0; sv[i] = 0; }
     }
     __syncthreads();
-    block_bitonic_sort<u128>(sk, sv, n2);
+    stamp(ctrl, 2);
+    block_sort<u128>(sk, sv, n2);
+    stamp(ctrl, 3);
     // budget walk (monotone predicate): count of the prefix within tau and B_max
     uint64_t cc = 0;
     uint32_t fits = 0;
@@ -316,6 +397,7 @@ __global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl
         cc += tot;
     }
     const bool whole = (n == np);                          // S holds every pending row
+    stamp(ctrl, 4);
     if (threadIdx.x == 0) {
         bool fb = (fits == n && !whole);
         double bp = 0.0, thr = 0.0;
@@ -361,6 +443,7 @@ __global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl
         const uint64_t len = c.len_key ? (uint64_t)P.len_in[r] + P.gen[r] : (uint64_t)P.len_in[r];
         wsk[i] = (len << 32) | P.id[r];
     }
+    stamp(ctrl, 5);
     window_select(P, c, ctrl, S, wsk, sv, ncd, pc, pf);
 }
 

@@ -58,6 +58,7 @@ struct alignas(16) Ctrl {
     unsigned long long tot_cost;     // sum of the token costs of all pending rows
     uint32_t spec_n, spec_ovf, fallback, window_done;
     uint32_t n_refresh, pad3[3];                // length-bound refreshes this step (a2)
+    unsigned long long ts[12];                  // %globaltimer stamps of the single-CTA phases
 };
 
 // state that survives across steps of one handle (not cleared by k_begin)
@@ -73,7 +74,24 @@ struct BlockPart {
 };
 
 // per-task accumulators of the compound pass (a4): sum of len_rem and of the call goodput
-struct TaskAcc { unsigned long long T, G; };
+struct TaskAcc {
+    unsigned long long T, G;          // sums over the stage's pending calls (k_score)
+    unsigned long long Gt, tgen;      // task goodput and t_gen (k_ctask)
+    long long trem;                   // stage t_rem (k_ctask)
+    uint32_t fmax, fmin;              // max / min starvation frames of its pending calls (k_score)
+};
+// key-image placeholder of a pending compound call between k_score and its key pass:
+// a NaN pattern carrying floor(steps_waited / Delta) (real key images are < 0x7FF0...)
+constexpr uint64_t kFramesTag = 0x7FF8000000000000ull;
+
+// %globaltimer (ns) stamp of a phase boundary, taken by thread 0 of a single-CTA kernel
+__device__ __forceinline__ void stamp(Ctrl* ctrl, int i) {
+    if (threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        ctrl->ts[i] = t;
+    }
+}
 
 struct Scratch {
     uint32_t* hcnt;          // 4096
@@ -93,7 +111,7 @@ struct Scratch {
     uint32_t* spec_row;
     Persist* persist;
     BlockPart* part;         // k_score partials (grid_score entries)
-    BlockPart* part2;        // k_ckey partials (grid_ckey entries)
+    BlockPart* part2;        // k_ctask partials (grid_ctask entries)
     TaskAcc* tacc;           // task_capacity, zeroed by k_begin every step
     uint32_t n_part, n_part2, task_cap, pad3;
 };
@@ -211,7 +229,7 @@ __global__ void k_begin(Ctrl* ctrl, uint32_t* hcnt, unsigned long long* hcost, i
                         TaskAcc* tacc, uint32_t n_tasks) {
     const uint32_t tid = threadIdx.x + blockIdx.x * blockDim.x, nt = blockDim.x * gridDim.x;
     for (uint32_t b = tid; b < 4096; b += nt) { hcnt[b] = 0; hcost[b] = 0; }
-    for (uint32_t t = tid; t < n_tasks; t += nt) { tacc[t].T = 0; tacc[t].G = 0; }
+    for (uint32_t t = tid; t < n_tasks; t += nt) { tacc[t].T = 0; tacc[t].G = 0; tacc[t].fmax = 0; tacc[t].fmin = 0xFFFFFFFFu; }
     if (tid == 0) {
         Ctrl z;
         memset(&z, 0, sizeof(z));
@@ -420,7 +438,7 @@ __global__ void __launch_bounds__(1024) k_resolve(Cfg c, Ctrl* ctrl, Scratch S) 
         else { sk[i] = ~(u128)0; sv[i] = 0; }
     }
     __syncthreads();
-    block_bitonic_sort<u128>(sk, sv, n2);
+    block_sort<u128>(sk, sv, n2);
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) { S.bucket_ck[i] = sk[i]; S.bucket_cost[i] = sv[i]; }
     // block scan of costs over the sorted bucket (4 consecutive per thread)
     const uint32_t i0 = threadIdx.x * 4;
@@ -529,7 +547,9 @@ __device__ void window_select(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scr
     while (n2 < n) n2 <<= 1;
     for (uint32_t i = n + threadIdx.x; i < n2; i += blockDim.x) { sk[i] = ~0ull; sv[i] = 0; }
     __syncthreads();
-    block_bitonic_sort<uint64_t>(sk, sv, n2);
+    stamp(ctrl, 6);
+    block_sort<uint64_t>(sk, sv, n2);
+    stamp(ctrl, 7);
     uint64_t carry_c = 0;
     u128 carry_f = 0;
     for (uint32_t base = 0; base < n; base += blockDim.x) {
@@ -548,6 +568,7 @@ __device__ void window_select(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scr
     }
     if (threadIdx.x == 0) { pc[n] = carry_c; pf[n] = carry_f; }
     __syncthreads();
+    stamp(ctrl, 8);
     u128 best = 0; uint32_t bi = 0xFFFFFFFFu, bj = 0;
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
         const uint64_t lim = (uint64_t)pc[i] + c.token_budget;
@@ -580,6 +601,7 @@ __device__ void window_select(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scr
     }
     __syncthreads();
     bi = s_bi[0]; bj = s_bj[0];
+    stamp(ctrl, 9);
     const uint32_t ns = bj - bi + 1;
     for (uint32_t k = threadIdx.x; k < ns; k += blockDim.x) {
         const uint32_t r = sv[bi + k];
@@ -603,6 +625,7 @@ __device__ void window_select(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scr
         ps->steps += 1;
         ps->fallbacks += ctrl->fallback;
     }
+    stamp(ctrl, 10);
 }
 
 // k_group: the window over Cd = S.cand (after the radix path or a too-large speculative Cd)

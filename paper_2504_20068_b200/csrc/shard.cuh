@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(1024) k_merge1(Cfg c, Ctrl* ctrl, const Rec1* 
     }
     for (uint32_t i = nv + threadIdx.x; i < n2; i += blockDim.x) { k[i] = ~(u128)0; v[i] = 0; }
     __syncthreads();
-    block_bitonic_sort<u128>(k, v, n2);
+    block_sort<u128>(k, v, n2);
     uint64_t cc = 0;
     uint32_t fits = 0;
     for (uint32_t base = 0; base < nv; base += blockDim.x) {
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(1024) k_group_rec(Pool P, Cfg c, Ctrl* ctrl, S
     }
     for (uint32_t i = n + threadIdx.x; i < n2; i += blockDim.x) { sk[i] = ~0ull; sv[i] = 0; }
     __syncthreads();
-    block_bitonic_sort<uint64_t>(sk, sv, n2);
+    block_sort<uint64_t>(sk, sv, n2);
     uint64_t carry_c = 0;
     u128 carry_f = 0;
     for (uint32_t base = 0; base < n; base += blockDim.x) {

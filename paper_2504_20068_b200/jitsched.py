@@ -69,7 +69,7 @@ class jit_batch(C.Structure):
     _fields_ = [("capacity", C.c_uint32), ("n_selected", C.c_uint32), ("total_tokens", C.c_uint32),
                 ("n_candidates", C.c_uint32), ("b_star", C.c_uint32), ("n_pending", C.c_uint32),
                 ("n_dropped", C.c_uint32), ("status", C.c_uint32), ("n_refresh", C.c_uint32),
-                ("fallback", C.c_uint32), ("reserved", C.c_uint32), ("bp", C.c_double), ("thr", C.c_double),
+                ("fallback", C.c_uint32), ("n_spec", C.c_uint32), ("bp", C.c_double), ("thr", C.c_double),
                 ("ids", C.c_void_p), ("tokens", C.c_void_p), ("rows", C.c_void_p)]
 
 
@@ -107,7 +107,8 @@ _lib = None
 EXPORTS = ("jit_sched_workspace_bytes", "jit_sched_init", "jit_sched_load", "jit_sched_step",
            "jit_sched_step_async", "jit_sched_fetch_batch", "jit_sched_read_rows", "jit_sched_kernel_times",
            "jit_replay_workspace_bytes", "jit_sched_replay", "jit_sched_destroy", "jit_sched_last_error",
-           "jit_sched_version", "jit_shard_prefix", "jit_shard_merge", "jit_shard_candidates", "jit_shard_finish")
+           "jit_sched_version", "jit_shard_prefix", "jit_shard_merge", "jit_shard_candidates", "jit_shard_finish",
+           "jit_sched_phase_times")
 
 
 def load_library(path: str = LIB_PATH):
@@ -284,7 +285,7 @@ class Scheduler:
         k = b.n_selected
         return {"status": rc, "n_pending": b.n_pending, "n_selected": k, "total_tokens": b.total_tokens,
                 "n_candidates": b.n_candidates, "b_star": b.b_star, "n_dropped_now": b.n_dropped, "bp": b.bp,
-                "thr": b.thr, "n_refresh": b.n_refresh, "fallback": b.fallback,
+                "thr": b.thr, "n_refresh": b.n_refresh, "fallback": b.fallback, "n_spec": b.n_spec,
                 "batch_ids": self._ids[:k].copy(), "batch_tokens": self._tok[:k].copy(),
                 "batch_rows": self._rows[:k].copy()}
 
@@ -308,6 +309,13 @@ class Scheduler:
         t = (C.c_float * 5)()
         self._check(self.lib.jit_sched_kernel_times(self.h, C.c_int(-1), t, 5), self.h)
         return list(t)
+
+    def phase_times(self):
+        """%globaltimer stamps (ns, relative to the first) of the single-CTA resolve phases."""
+        t = (C.c_uint64 * 11)()
+        self._check(self.lib.jit_sched_phase_times(self.h, t, 11), self.h)
+        v = list(t)
+        return [x - v[0] if x else None for x in v]
 
     # ------------------------------------------------------------------ sharded step
     def shard_prefix(self, now_ns: int, v_token_ns: int, rec1) -> int:

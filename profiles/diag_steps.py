@@ -13,4 +13,5 @@ s.load(d["pool"], d["tasks"])
 for k in range(6):
     r = s.step(d["now_ns"], d["v_token_ns"])
     print(k, {x: r[x] for x in ("n_pending", "n_refresh", "fallback", "b_star", "n_candidates", "n_selected",
-                                "n_dropped_now")})
+                                "n_dropped_now", "n_spec")})
+    print("   phases ns:", s.phase_times())
