@@ -7,8 +7,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libjitsched.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "--fmad=false",
-         "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+# abi.cu (host code + the scoring kernels) is compiled whole-program; exact.cu (k_spec and
+# the exact path it launches from the device) with -rdc, device-linked against cudadevrt
+BASE = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "--fmad=false",
+        "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+UNITS = [("abi.cu", []), ("exact.cu", ["-rdc=true"])]
+LINK = ["-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-lcudadevrt"]
 
 
 def sources():
@@ -20,11 +24,22 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC] + FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", tmp, os.path.join(HERE, "csrc", "abi.cu")]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    inc = ["-I", os.path.join(ROOT, "include")]
+    objs, log = [], ""
+    for src, extra in UNITS:
+        obj = tmp + "." + src + ".o"
+        cmd = [NVCC] + BASE + extra + inc + ["-c", "-o", obj, os.path.join(HERE, "csrc", src)]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src}:\n" + r.stdout[-4000:] + r.stderr[-8000:])
+        objs.append(obj)
+        log += r.stderr
+    r = subprocess.run([NVCC] + LINK + ["-o", tmp] + objs, capture_output=True, text=True)
+    for o in objs:
+        os.remove(o)
     if r.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + r.stdout[-4000:] + r.stderr[-8000:])
+        raise RuntimeError("nvcc link failed:\n" + r.stdout[-4000:] + r.stderr[-8000:])
     if verbose:
-        print(r.stderr[-6000:])
+        print(log[-6000:])
     os.replace(tmp, LIB)
     return LIB

@@ -14,6 +14,7 @@
 #include "score.cuh"
 #include "replay.cuh"
 #include "shard.cuh"
+#include "exact_api.h"
 
 using namespace jit;
 
@@ -35,9 +36,9 @@ struct jit_sched {
     cudaStream_t cap2 = nullptr;      // capture stream of the conditional body
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
-    cudaGraphNode_t begin_node = nullptr;
-    cudaKernelNodeParams begin_params{};
-    void* begin_args[7];
+    cudaGraphNode_t score_node = nullptr;   // k_score: its (now, v) arguments change every step
+    cudaKernelNodeParams score_params{};
+    void* score_args[9];
     uint32_t arg_ntasks = 0;
     int64_t arg_now = 0, arg_v = 0;
     bool loaded = false, graph_dirty = true, timing = false, debug = false;
@@ -113,6 +114,7 @@ static void carve(Carve& cv, const jit_config* cfg, const jit_len_table* tab, Po
     S.cand_cap = (uint32_t)N;
     S.spec_ck = cv.take<u128>(kSpecCap); S.spec_row = cv.take<uint32_t>(kSpecCap);
     S.persist = cv.take<Persist>(1);
+    S.spec_cnt = cv.take<unsigned int>(1);
     S.part = cv.take<BlockPart>(kMaxParts); S.part2 = cv.take<BlockPart>(kMaxParts);
     S.tacc = cv.take<TaskAcc>(NT);
     S.task_cap = (uint32_t)NT;
@@ -195,19 +197,16 @@ extern "C" int jit_sched_init(const jit_config* cfg, const jit_slo_group* groups
     CK(cudaMemcpyAsync((void*)h->T.cum, table->cum, 4ull * table->n_rows * table->n_bins, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemcpyAsync(h->d_groups, groups, sizeof(Group) * n_groups, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMallocHost(&h->h_ctrl, sizeof(Ctrl)));
+    memset(h->h_ctrl, 0, sizeof(Ctrl));
+    h->S.h_ctrl = h->h_ctrl;              // pinned + mapped (UVA): the step's last kernel writes it
     for (auto& e : h->ev) CK(cudaEventCreate(&e));
-    CK(cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)((sizeof(u128) + 4) * kBucketCap)));
-    CK(cudaFuncSetAttribute(k_group, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(12 * kGroupSmemSort)));
-    CK(cudaFuncSetAttribute(k_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)((sizeof(u128) + 4) * kSpecCap)));
+    CK(exact::init_attributes());
     CK(cudaFuncSetAttribute(k_group_rec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(12 * kGroupSmemSort)));
     // one shared-memory carveout for every kernel of the step: switching the L1/shared split
     // between consecutive kernels costs a drain + reconfiguration of the SMs (several µs each)
     {
         const void* ks[] = {(const void*)k_begin, (const void*)k_score<false>, (const void*)k_score<true>,
-                            (const void*)k_ctask, (const void*)k_ckey_full<false>,
-                            (const void*)k_ckey_full<true>, (const void*)k_spec,
-                            (const void*)k_hist0, (const void*)k_pass, (const void*)k_compact, (const void*)k_resolve,
-                            (const void*)k_cand, (const void*)k_group};
+                            (const void*)k_ctask};
         for (const void* k : ks)
             CK(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
     }
@@ -258,7 +257,8 @@ extern "C" int jit_sched_load(jit_sched* h, const jit_pool* p) {
     const bool same_shape = h->loaded && P.n == p->n && P.n_single == p->n_single && P.n_tasks == p->n_tasks;
     P.n = p->n; P.n_single = p->n_single; P.n_tasks = p->n_tasks;
     // validate on the device (also covers device-resident pools)
-    k_begin<<<1, 32, 0, h->stream>>>(h->d_ctrl, h->S.hcnt, h->S.hcost, 0, 1, h->S.tacc, 0);
+    // full reset: control block, histograms, the task accumulators, the speculative-set counter
+    k_begin<<<4, 1024, 0, h->stream>>>(h->d_ctrl, h->S.hcnt, h->S.hcost, 0, 1, h->S.tacc, p->n_tasks, h->S.spec_cnt);
     const uint32_t vb = (uint32_t)std::min<uint64_t>((n + 255) / 256 + 1, (uint64_t)h->n_sm * 8);
     k_validate<<<vb, 256, 0, h->stream>>>(P, h->d_groups, h->n_groups, h->T.n_rows, h->d_ctrl);
     CK(cudaGetLastError());
@@ -283,6 +283,7 @@ extern "C" int jit_sched_load(jit_sched* h, const jit_pool* p) {
     h->S.n_part = h->nb_score; h->S.n_part2 = h->nb_ctask;
     h->arg_ntasks = P.n_tasks;
     h->grid_pass = std::max<uint32_t>(1, std::min<uint32_t>((P.n + kPassThreads - 1) / kPassThreads, (uint32_t)h->n_sm * 4));
+    h->S.nb_full = h->nb_full; h->S.grid_pass = h->grid_pass;    // for k_spec's device-side launches
     if (!same_shape) h->graph_dirty = true;
     h->loaded = true;
     return JIT_OK;
@@ -295,39 +296,32 @@ static void enqueue_score(jit_sched* h, cudaStream_t s, int64_t now, int64_t v, 
                           bool capturing = false) {
     Pool& P = h->P;
     Scratch& S = h->S;
-    if (h->debug) k_score<true><<<h->nb_score, kScoreThreads, 0, s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S);
-    else k_score<false><<<h->nb_score, kScoreThreads, 0, s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S);
+    if (h->debug)
+        k_score<true><<<h->nb_score, kScoreThreads, 0, s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S, now, v);
+    else
+        k_score<false><<<h->nb_score, kScoreThreads, 0, s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S, now, v);
     if (mid) cudaEventRecordWithFlags(mid, s, capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
     k_ctask<<<h->nb_ctask, kScoreThreads, 0, s>>>(P, h->c, h->d_ctrl, S);
     // debug: every compound call gets its key and rate outputs now (read_rows sees them all)
-    if (h->debug) k_ckey_full<true><<<h->nb_full, kScoreThreads, 0, s>>>(P, h->c, h->d_ctrl, S, 1);
-    (void)now; (void)v;
+    if (h->debug) exact::ckey_full(P, h->c, h->d_ctrl, S, h->nb_full, true, 1, s);
 }
 
-// radix-select path (level-0 histogram .. candidates); k_hist0 runs when forced or when the
-// speculative resolve fell back; k_pass runs only while the boundary bucket is too large
-static void enqueue_radix(jit_sched* h, cudaStream_t s, int force_hist0, uint32_t first_pass, uint32_t n_passes,
-                          int only_after_fallback) {
+// host-side continuation of the radix select (only for heavy key ties, see finish_step)
+static void enqueue_radix(jit_sched* h, cudaStream_t s, uint32_t first_pass, uint32_t n_passes) {
     Pool& P = h->P;
     Scratch& S = h->S;
-    // the radix path reads every key image: first key the compound calls k_ctask left tagged
-    if (force_hist0 >= 0 && P.n_single < P.n)
-        k_ckey_full<false><<<h->nb_full, kScoreThreads, 0, s>>>(P, h->c, h->d_ctrl, S, force_hist0);
-    if (force_hist0 >= 0) k_hist0<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->c, h->d_ctrl, S.hcnt, S.hcost, force_hist0);
-    for (uint32_t i = 0; i < n_passes; ++i)
-        k_pass<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->c, h->d_ctrl, S.hcnt, S.hcost, first_pass + i);
-    k_compact<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->d_ctrl, S);
-    k_resolve<<<1, 1024, (sizeof(u128) + 4) * kBucketCap, s>>>(h->c, h->d_ctrl, S);
-    k_cand<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->d_ctrl, S, only_after_fallback);
+    for (uint32_t i = 0; i < n_passes; ++i) exact::pass(P, h->c, h->d_ctrl, S, h->grid_pass, first_pass + i, s);
+    exact::compact(P, h->c, h->d_ctrl, S, h->grid_pass, s);
+    exact::resolve(P, h->c, h->d_ctrl, S, s);
+    exact::cand(P, h->c, h->d_ctrl, S, h->grid_pass, 0, s);
+    exact::group(P, h->c, h->d_ctrl, S, s);
 }
 
-static void enqueue_tail(jit_sched* h, cudaStream_t s) {
-    k_group<<<1, 1024, 12 * kGroupSmemSort, s>>>(h->P, h->c, h->d_ctrl, h->S);
-}
-
-// Step graph:  k_begin -> k_score -> k_spec -> IF(fallback){k_hist0 -> k_pass -> k_compact ->
-// k_resolve -> k_cand} -> k_group -> D2H(ctrl).  The IF is a device-side conditional node set
-// by k_spec (cudaGraphSetConditional), so the common case runs 4 kernels and no host logic.
+// Step graph: k_score -> k_ctask -> k_spec -> k_publish, four kernel nodes and nothing else.
+// k_score resets the control block, k_publish copies it to pinned host memory; when the
+// speculative resolve cannot be exact, k_spec itself launches the exact path (launch_exact_path,
+// a chain of device-side tail launches) -- no conditional node and no copy node, whose fixed
+// costs measured ~26 us and ~6 us per step on B200 (profiles/host_overhead.py).
 static int build_graph(jit_sched* h) {
     if (h->exec) { cudaGraphExecDestroy(h->exec); h->exec = nullptr; }
     if (h->graph) { cudaGraphDestroy(h->graph); h->graph = nullptr; }
@@ -335,65 +329,30 @@ static int build_graph(jit_sched* h) {
     cudaStream_t s = h->cap;
     Scratch& S = h->S;
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    cudaStreamCaptureStatus cs;
-    cudaGraph_t cg;
-    const cudaGraphNode_t* deps = nullptr;
-    size_t nd = 0;
-    CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &cg, &deps, &nd));
-    const bool flat = getenv("JITSCHED_FLAT_GRAPH") != nullptr;   // A/B switch: no conditional node
-    // overhead attribution only (profiles/host_overhead.py; results are NOT valid with these):
-    // bit 0 drops the fallback body, bit 1 the ctrl read-back, bit 2 adds one empty kernel node
-    const char* xe = getenv("JITSCHED_EXPERIMENT");
-    const int xm = xe ? atoi(xe) : 0;
-    cudaGraphConditionalHandle hc = 0;
-    if (!flat && !(xm & 1)) CK(cudaGraphConditionalHandleCreate(&hc, cg, 0, cudaGraphCondAssignDefault));
-    k_begin<<<4, 1024, 0, s>>>(h->d_ctrl, S.hcnt, S.hcost, 0, 1, S.tacc, h->arg_ntasks);
-    if (xm & 4) k_ckey_full<false><<<1, 32, 0, s>>>(h->P, h->c, h->d_ctrl, S, 0);   // exits at once
     if (h->timing) cudaEventRecordWithFlags(h->ev[0], s, cudaEventRecordExternal);
     enqueue_score(h, s, 0, 1, h->timing ? h->ev[1] : nullptr, true);
     if (h->timing) cudaEventRecordWithFlags(h->ev[2], s, cudaEventRecordExternal);
-    k_spec<<<1, kSpecThreads, (sizeof(u128) + 4) * kSpecCap, s>>>(h->P, h->c, h->d_ctrl, S, hc,
-                                                                  (flat || (xm & 1)) ? 0 : 1, 0);
+    exact::spec(h->P, h->c, h->d_ctrl, S, 0, s);
+    k_publish<<<1, 64, 0, s>>>(h->d_ctrl, h->h_ctrl);
     if (h->timing) cudaEventRecordWithFlags(h->ev[3], s, cudaEventRecordExternal);
-    if (xm & 1) {
-    } else if (flat) {
-        enqueue_radix(h, s, 0, 0, 1, 1);      // every kernel checks the status and exits when idle
-        enqueue_tail(h, s);
-    } else {
-        CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &cg, &deps, &nd));
-        cudaGraphNodeParams cp = {};
-        cp.type = cudaGraphNodeTypeConditional;
-        cp.conditional.handle = hc;
-        cp.conditional.type = cudaGraphCondTypeIf;
-        cp.conditional.size = 1;
-        cudaGraphNode_t cnode;
-        CK(cudaGraphAddNode(&cnode, cg, deps, nd, &cp));
-        cudaGraph_t body = cp.conditional.phGraph_out[0];
-        CK(cudaStreamBeginCaptureToGraph(h->cap2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-        enqueue_radix(h, h->cap2, 0, 0, 1, 1);
-        enqueue_tail(h, h->cap2);
-        CK(cudaStreamEndCapture(h->cap2, nullptr));
-        CK(cudaStreamUpdateCaptureDependencies(s, &cnode, 1, cudaStreamSetCaptureDependencies));
-    }
     if (h->timing) cudaEventRecordWithFlags(h->ev[4], s, cudaEventRecordExternal);
-    if (!(xm & 2)) cudaMemcpyAsync(h->h_ctrl, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s);
     CK(cudaStreamEndCapture(s, &g));
     size_t nn = 0;
     CK(cudaGraphGetNodes(g, nullptr, &nn));
     std::vector<cudaGraphNode_t> nodes(nn);
     CK(cudaGraphGetNodes(g, nodes.data(), &nn));
-    // locate the k_begin kernel node and the timing event nodes; the query of the conditional
-    // node's type can fail with this runtime/driver pair -- such nodes are skipped and the
-    // error state they leave behind is cleared
-    h->begin_node = nullptr;
+    // locate the k_score kernel node (its (now, v) arguments are updated per launch) and the
+    // timing event nodes
+    const void* score_fn = h->debug ? (const void*)k_score<true> : (const void*)k_score<false>;
+    h->score_node = nullptr;
     for (auto& e : h->ev_node) e = nullptr;
     for (auto nd : nodes) {
         cudaGraphNodeType ty;
         if (cudaGraphNodeGetType(nd, &ty) != cudaSuccess) { (void)cudaGetLastError(); continue; }
-        if (ty == cudaGraphNodeTypeKernel && !h->begin_node) {
+        if (ty == cudaGraphNodeTypeKernel && !h->score_node) {
             cudaKernelNodeParams kp;
             if (cudaGraphKernelNodeGetParams(nd, &kp) != cudaSuccess) { (void)cudaGetLastError(); continue; }
-            if (kp.func == (void*)k_begin) { h->begin_node = nd; h->begin_params = kp; }
+            if (kp.func == score_fn) { h->score_node = nd; h->score_params = kp; }
         } else if (ty == cudaGraphNodeTypeEventRecord) {
             cudaEvent_t e;
             if (cudaGraphEventRecordNodeGetEvent(nd, &e) != cudaSuccess) { (void)cudaGetLastError(); continue; }
@@ -401,30 +360,25 @@ static int build_graph(jit_sched* h) {
         }
     }
     (void)cudaGetLastError();
-    if (!h->begin_node) { cudaGraphDestroy(g); return set_err(h, JIT_ECUDA, "graph: k_begin node not found"); }
-    h->graph = g;                      // kept alive: begin_node belongs to it
+    if (!h->score_node) { cudaGraphDestroy(g); return set_err(h, JIT_ECUDA, "graph: k_score node not found"); }
+    h->graph = g;                      // kept alive: score_node belongs to it
     CK(cudaGraphInstantiate(&h->exec, g, 0));
     h->graph_dirty = false;
     return JIT_OK;
 }
 
-// JIT_CFG_NO_GRAPH: the same chain as direct launches (profilers cannot look inside graphs
-// that hold conditional nodes); every fallback kernel checks the status itself.
+// JIT_CFG_NO_GRAPH: the same three kernels as direct launches (for profilers)
 static int launch_direct(jit_sched* h, int64_t now, int64_t v) {
     cudaStream_t s = h->stream;
     const bool ev = h->timing && h->n_slots;
     cudaEvent_t* e = ev ? &h->slots[5 * (h->slot_used % h->n_slots)] : nullptr;
     if (ev) h->slot_used++;
-    k_begin<<<4, 1024, 0, s>>>(h->d_ctrl, h->S.hcnt, h->S.hcost, now, v, h->S.tacc, h->arg_ntasks);
     if (ev) cudaEventRecord(e[0], s);
     enqueue_score(h, s, now, v, ev ? e[1] : nullptr, false);
     if (ev) cudaEventRecord(e[2], s);
-    k_spec<<<1, kSpecThreads, (sizeof(u128) + 4) * kSpecCap, s>>>(h->P, h->c, h->d_ctrl, h->S, 0, 0, 0);
-    if (ev) cudaEventRecord(e[3], s);
-    enqueue_radix(h, s, 0, 0, 1, 1);
-    enqueue_tail(h, s);
-    if (ev) cudaEventRecord(e[4], s);
-    cudaMemcpyAsync(h->h_ctrl, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s);
+    exact::spec(h->P, h->c, h->d_ctrl, h->S, 0, s);
+    k_publish<<<1, 64, 0, s>>>(h->d_ctrl, h->h_ctrl);
+    if (ev) { cudaEventRecord(e[3], s); cudaEventRecord(e[4], s); }
     CK(cudaGetLastError());
     return JIT_OK;
 }
@@ -438,13 +392,13 @@ static int launch_step(jit_sched* h, int64_t now, int64_t v) {
         CK(cudaGetLastError());
     }
     h->arg_now = now; h->arg_v = v;
-    h->begin_args[0] = &h->d_ctrl; h->begin_args[1] = &h->S.hcnt; h->begin_args[2] = &h->S.hcost;
-    h->begin_args[3] = &h->arg_now; h->begin_args[4] = &h->arg_v;
-    h->begin_args[5] = &h->S.tacc; h->begin_args[6] = &h->arg_ntasks;
-    cudaKernelNodeParams kp = h->begin_params;
-    kp.kernelParams = h->begin_args;
+    void** a = h->score_args;     // k_score(Pool, Table, const Group*, uint32_t, Cfg, Ctrl*, Scratch, now, v)
+    a[0] = &h->P; a[1] = &h->T; a[2] = &h->d_groups; a[3] = &h->n_groups; a[4] = &h->c; a[5] = &h->d_ctrl;
+    a[6] = &h->S; a[7] = &h->arg_now; a[8] = &h->arg_v;
+    cudaKernelNodeParams kp = h->score_params;
+    kp.kernelParams = a;
     kp.extra = nullptr;
-    CK(cudaGraphExecKernelNodeSetParams(h->exec, h->begin_node, &kp));
+    CK(cudaGraphExecKernelNodeSetParams(h->exec, h->score_node, &kp));
     if (h->timing && h->n_slots) {
         // point the graph's event nodes at this step's slot so every timed step keeps its times
         const uint32_t slot = h->slot_used % h->n_slots;
@@ -461,12 +415,19 @@ static int launch_step(jit_sched* h, int64_t now, int64_t v) {
 static int finish_step(jit_sched* h, jit_batch* out) {
     CK(cudaStreamSynchronize(h->stream));
     CK(cudaGetLastError());
+    if (getenv("JITSCHED_DEBUG_CTRL")) {
+        Ctrl dc;
+        CK(cudaMemcpy(&dc, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+        fprintf(stderr, "[ctrl] device status %u err %u fb %u spec %u trace %x lerr %u chain %u | host status %u err %u "
+                "fb %u spec %u trace %x\n", dc.status, dc.error, dc.fallback, dc.spec_n, dc.trace, dc.launch_err, dc.chain,
+                h->h_ctrl->status, h->h_ctrl->error, h->h_ctrl->fallback, h->h_ctrl->spec_n, h->h_ctrl->trace);
+    }
     if (h->h_ctrl->status == ST_HIST) {
-        // rare: the boundary bucket stayed large after the graph's passes (heavy key ties);
-        // finish the radix select with the remaining digits outside the graph
-        enqueue_radix(h, h->stream, -1, 1, kLevels - 1, 0);
-        enqueue_tail(h, h->stream);
-        cudaMemcpyAsync(h->h_ctrl, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream);
+        // rare: the boundary bucket stayed large after the exact path's first two digits
+        // (heavy key ties); finish the radix select with the remaining digits from the host
+        // (k_group publishes ctrl again)
+        enqueue_radix(h, h->stream, 1, kLevels - 1);
+        k_publish<<<1, 64, 0, h->stream>>>(h->d_ctrl, h->h_ctrl);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(h->stream));
     }
@@ -533,7 +494,7 @@ extern "C" int jit_sched_read_rows(jit_sched* h, double* key, double* rate, int6
     // compound calls of tasks that could not reach the batch still carry their frame tag
     // (k_ctask); key them from the last step's task accumulators (idempotent)
     if ((key || pending) && h->P.n_single < h->P.n)
-        k_ckey_full<false><<<h->nb_full, kScoreThreads, 0, h->stream>>>(h->P, h->c, h->d_ctrl, h->S, 1);
+        exact::ckey_full(h->P, h->c, h->d_ctrl, h->S, h->nb_full, false, 1, h->stream);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(h->stream));
     std::vector<uint64_t> img;
@@ -634,17 +595,15 @@ extern "C" int jit_shard_prefix(jit_sched* h, int64_t now_ns, int64_t v_token_ns
     cudaStream_t s = h->stream;
     Pool& P = h->P;
     Scratch& S = h->S;
-    k_begin<<<4, 1024, 0, s>>>(h->d_ctrl, S.hcnt, S.hcost, now_ns, v_token_ns, S.tacc, h->arg_ntasks);
     enqueue_score(h, s, now_ns, v_token_ns);
-    // k_spec reduces the scoring partials (n_pending, min key, ...); its speculative result is
-    // then superseded by the forced radix resolve below, which the round-1 export needs
-    k_spec<<<1, kSpecThreads, (sizeof(u128) + 4) * kSpecCap, s>>>(P, h->c, h->d_ctrl, S, 0, 0, 1);
-    if (P.n_single < P.n) k_ckey_full<false><<<h->nb_full, kScoreThreads, 0, s>>>(P, h->c, h->d_ctrl, S, 1);
-    k_hist0<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->c, h->d_ctrl, S.hcnt, S.hcost, 1);
-    for (uint32_t i = 0; i < kLevels - 1; ++i)
-        k_pass<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->c, h->d_ctrl, S.hcnt, S.hcost, i);
-    k_compact<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->d_ctrl, S);
-    k_resolve<<<1, 1024, (sizeof(u128) + 4) * kBucketCap, s>>>(h->c, h->d_ctrl, S);
+    // k_spec only reduces the scoring partials (n_pending, min key, ...): the round-1 export
+    // needs the full radix resolve below
+    exact::spec(P, h->c, h->d_ctrl, S, 1, s);
+    if (P.n_single < P.n) exact::ckey_full(P, h->c, h->d_ctrl, S, h->nb_full, false, 1, s);
+    exact::hist0(P, h->c, h->d_ctrl, S, h->grid_pass, 1, s);
+    for (uint32_t i = 0; i < kLevels - 1; ++i) exact::pass(P, h->c, h->d_ctrl, S, h->grid_pass, i, s);
+    exact::compact(P, h->c, h->d_ctrl, S, h->grid_pass, s);
+    exact::resolve(P, h->c, h->d_ctrl, S, s);
     k_export1<<<h->grid_pass, kPassThreads, 0, s>>>(P, h->d_ctrl, S, (Rec1*)d_rec1, cap);
     k_export1_tail<<<1, 1024, 0, s>>>(h->d_ctrl, S, (Rec1*)d_rec1, cap);
     CK(cudaGetLastError());
@@ -674,7 +633,7 @@ extern "C" int jit_shard_merge(jit_sched* h, const void* d_all_rec1, uint32_t n_
 extern "C" int jit_shard_candidates(jit_sched* h, void* d_rec2, uint32_t cap, uint32_t rank, uint32_t* n_out) {
     if (!h || !n_out) return JIT_EINVAL;
     cudaStream_t s = h->stream;
-    k_cand<<<h->grid_pass, kPassThreads, 0, s>>>(h->P, h->d_ctrl, h->S, 0);
+    exact::cand(h->P, h->c, h->d_ctrl, h->S, h->grid_pass, 0, s);
     k_export2<<<h->grid_pass, 256, 0, s>>>(h->P, h->c, h->d_ctrl, h->S, (Rec2*)d_rec2, cap, rank);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(h->h_ctrl, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));

@@ -1,0 +1,61 @@
+// exact.cu -- the speculative resolve (k_spec) and the exact path it launches from the device
+// (k_ckey_full, k_hist0, k_pass, k_compact, k_resolve, k_cand, k_group).  Compiled with -rdc
+// (CUDA dynamic parallelism) and device-linked against cudadevrt; the hot scoring kernels live
+// in abi.cu, compiled whole-program.
+#define JIT_EXACT_TU 1
+#include "common.cuh"
+#include "select.cuh"
+#include "score.cuh"
+#include "exact_api.h"
+
+namespace jit {
+namespace exact {
+
+cudaError_t init_attributes() {
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)((sizeof(u128) + 4) * kBucketCap))) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(k_group, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(12 * kGroupSmemSort))) !=
+        cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(k_spec, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)((sizeof(u128) + 4) * kSpecCap))) != cudaSuccess) return e;
+    // one shared-memory carveout for every kernel of the step (see abi.cu)
+    const void* ks[] = {(const void*)k_ckey_full<false>, (const void*)k_ckey_full<true>, (const void*)k_spec,
+                        (const void*)k_hist0, (const void*)k_pass, (const void*)k_compact, (const void*)k_resolve,
+                        (const void*)k_cand, (const void*)k_group};
+    for (const void* k : ks)
+        if ((e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                      cudaSharedmemCarveoutMaxShared)) != cudaSuccess) return e;
+    return cudaSuccess;
+}
+
+void spec(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int reduce_only, cudaStream_t s) {
+    k_spec<<<1, kSpecThreads, (sizeof(u128) + 4) * kSpecCap, s>>>(P, c, ctrl, S, reduce_only);
+}
+void ckey_full(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t grid, bool debug, int force,
+               cudaStream_t s) {
+    if (debug) k_ckey_full<true><<<grid, kScoreThreads, 0, s>>>(P, c, ctrl, S, force);
+    else k_ckey_full<false><<<grid, kScoreThreads, 0, s>>>(P, c, ctrl, S, force);
+}
+void hist0(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t grid, int force, cudaStream_t s) {
+    k_hist0<<<grid, kPassThreads, 0, s>>>(P, c, ctrl, S, force);
+}
+void pass(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t grid, uint32_t pass_idx, cudaStream_t s) {
+    k_pass<<<grid, kPassThreads, 0, s>>>(P, c, ctrl, S, pass_idx);
+}
+void compact(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t grid, cudaStream_t s) {
+    k_compact<<<grid, kPassThreads, 0, s>>>(P, c, ctrl, S);
+}
+void resolve(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, cudaStream_t s) {
+    k_resolve<<<1, 1024, (sizeof(u128) + 4) * kBucketCap, s>>>(P, c, ctrl, S);
+}
+void cand(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t grid, int only_after_fallback,
+          cudaStream_t s) {
+    k_cand<<<grid, kPassThreads, 0, s>>>(P, c, ctrl, S, only_after_fallback);
+}
+void group(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, cudaStream_t s) {
+    k_group<<<1, 1024, 12 * kGroupSmemSort, s>>>(P, c, ctrl, S);
+}
+
+}  // namespace exact
+}  // namespace jit

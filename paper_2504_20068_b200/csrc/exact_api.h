@@ -1,0 +1,29 @@
+// exact_api.h -- host-side launchers of the kernels compiled into exact.cu (the speculative
+// resolve k_spec and the exact radix path it launches from the device).  exact.cu is compiled
+// with -rdc (dynamic parallelism); abi.cu, which holds the hot scoring kernels, is not.
+#pragma once
+#include <cuda_runtime.h>
+#include "select.cuh"
+
+namespace jit {
+namespace exact {
+
+// function attributes (dynamic shared memory, carveout) of every exact.cu kernel
+cudaError_t init_attributes();
+
+// k_spec: reduce the scoring partials; reduce_only = 0: resolve from the speculative set and
+// run the window (or launch the exact path from the device)
+void spec(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int reduce_only, cudaStream_t s);
+// k_ckey_full: key the compound calls still carrying a frame tag (force = 0: only after a fallback)
+void ckey_full(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t grid, bool debug, int force,
+               cudaStream_t s);
+void hist0(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t grid, int force, cudaStream_t s);
+void pass(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t grid, uint32_t pass_idx, cudaStream_t s);
+void compact(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t grid, cudaStream_t s);
+void resolve(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, cudaStream_t s);
+void cand(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t grid, int only_after_fallback,
+          cudaStream_t s);
+void group(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, cudaStream_t s);
+
+}  // namespace exact
+}  // namespace jit

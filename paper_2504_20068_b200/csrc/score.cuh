@@ -18,14 +18,14 @@ namespace jit {
 
 // Rows whose key image is >= the speculative threshold t (the previous step's cutoff with a
 // margin) join the speculative set; warp ballot + one atomic per warp (all lanes convergent).
-__device__ __forceinline__ void spec_add(Ctrl* ctrl, const Scratch& S, const uint32_t* ids, bool valid,
+__device__ __forceinline__ void spec_add(const Scratch& S, const uint32_t* ids, bool valid,
                                          uint64_t img, uint32_t row, uint64_t t) {
     const bool take = valid && img >= t;
     const unsigned m = __ballot_sync(0xffffffffu, take);
     if (!m) return;
     const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
     uint32_t base = 0;
-    if (lane == leader) base = atomicAdd(&ctrl->spec_n, (uint32_t)__popc(m));
+    if (lane == leader) base = atomicAdd(S.spec_cnt, (unsigned)__popc(m));
     base = __shfl_sync(0xffffffffu, base, leader);
     if (take) {
         const uint32_t slot = base + __popc(m & ((1u << lane) - 1u));
@@ -82,16 +82,30 @@ __device__ __forceinline__ bool score_call(const Cfg& c, const Table& T, const G
     return true;
 }
 
+__device__ __forceinline__ bool is_frames_tag(uint64_t img) {
+    return (img & 0xFFF8000000000000ull) == kFramesTag;
+}
+
+// k_score / k_ctask: the hot pass, compiled into abi.cu (whole-program mode: -rdc costs the
+// scoring loop ~50 registers); k_ckey_full / k_spec: the separately linked exact.cu
+#ifndef JIT_EXACT_TU
+// 4 CTAs of 256 per SM: caps k_score at 64 registers without spills (uncapped it takes ~104,
+// i.e. 2 CTAs per SM -- too few warps for a latency-bound streaming pass)
 #ifndef JIT_SCORE_MINB
-#define JIT_SCORE_MINB 1
+#define JIT_SCORE_MINB 4
 #endif
 template <bool kDebug>
 __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P, Table T, const Group* groups, uint32_t n_groups,
-                                                         Cfg c, Ctrl* ctrl, Scratch S) {
+                                                         Cfg c, Ctrl* ctrl, Scratch S, int64_t now, int64_t v) {
     __shared__ GroupFast s_g[256];
     for (uint32_t gi = threadIdx.x; gi < n_groups; gi += blockDim.x) s_g[gi] = make_fast(groups[gi]);
+    // first kernel of the step: a fresh control block (nothing else touches ctrl during this
+    // kernel) and cleared fallback histograms, spread over the CTAs
+    if (blockIdx.x == 0) reset_ctrl_block(ctrl, now, v);
+    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < 4096; b += gridDim.x * blockDim.x) {
+        S.hcnt[b] = 0; S.hcost[b] = 0;
+    }
     __syncthreads();
-    const int64_t now = ctrl->now, v = ctrl->v;
     const uint64_t t_guess = S.persist->t_guess;
     const int lane = threadIdx.x & 31;
     const bool any_compound = P.n_single < P.n;
@@ -186,7 +200,7 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
                 atomicMin(&S.tacc[key_task].fmin, fn);
             }
         }
-        spec_add(ctrl, S, P.id, valid, img, r, t_guess);
+        spec_add(S, P.id, valid, img, r, t_guess);
         a_arr = b_arr; a_li = b_li; a_g = b_g; a_pr = b_pr; a_lh = b_lh; a_me = b_me; a_ax = b_ax; a_tk = b_tk;
     }
     store_part(S.part, my_pend, my_drop, my_err, my_min, my_cost, my_ref);
@@ -202,10 +216,6 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
 // calls, so the speculative-set ballot stays convergent.  Every other call keeps its tagged
 // frame count until k_ckey_full (fallback body / debug / shard path) keys it.
 // --------------------------------------------------------------------------------------
-__device__ __forceinline__ bool is_frames_tag(uint64_t img) {
-    return (img & 0xFFF8000000000000ull) == kFramesTag;
-}
-
 __global__ void __launch_bounds__(kScoreThreads) k_ctask(Pool P, Cfg c, Ctrl* ctrl, Scratch S) {
     const int64_t now = ctrl->now, v = ctrl->v;
     const uint64_t t_guess = S.persist->t_guess;
@@ -251,7 +261,10 @@ __global__ void __launch_bounds__(kScoreThreads) k_ctask(Pool P, Cfg c, Ctrl* ct
                 const uint64_t imax = (uint64_t)__double_as_longlong(kmax);
                 if (imin < my_min) my_min = imin;
                 hot = ok_max && imax >= t_guess;
-                S.tacc[t].Gt = Gt; S.tacc[t].tgen = t_gen; S.tacc[t].trem = trem;
+                TaskAcc o;                                          // consumed: re-zero the sums
+                o.T = 0; o.G = 0; o.Gt = Gt; o.tgen = t_gen; o.trem = trem; o.Tr = acc.T;
+                o.fmax = 0; o.fmin = 0xFFFFFFFFu;
+                S.tacc[t] = o;
             }
         }
         // hot tasks: the warp keys their calls together (speculative-set ballot convergent)
@@ -278,17 +291,25 @@ __global__ void __launch_bounds__(kScoreThreads) k_ctask(Pool P, Cfg c, Ctrl* ct
                         valid = true;
                     }
                 }
-                spec_add(ctrl, S, P.id, valid, img, r, t_guess);
+                spec_add(S, P.id, valid, img, r, t_guess);
             }
         }
     }
     store_part(S.part2, 0, 0, my_err, my_min, 0, 0);
 }
+#endif  // !JIT_EXACT_TU
 
+#ifdef JIT_EXACT_TU
 // k_ckey_full: row-parallel keying of every call still carrying its frame tag (after
 // k_ctask); in debug mode also the per-call rate / t_rem outputs of every compound row.
 template <bool kDebug>
 __global__ void __launch_bounds__(kScoreThreads) k_ckey_full(Pool P, Cfg c, Ctrl* ctrl, Scratch S, int force) {
+    if (!kDebug && blockIdx.x == 0 && threadIdx.x == 0 && ctrl->chain) {   // exact path: next k_hist0
+        atomicOr(&ctrl->trace, 2u);
+        k_hist0<<<S.grid_pass, kPassThreads, 0, cudaStreamTailLaunch>>>(P, c, ctrl, S, 0);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) { ctrl->error |= 2u; ctrl->status = ST_ERROR; ctrl->launch_err = e; }
+    }
     if (!force && ctrl->status != ST_FALLBACK) return;
     const uint32_t n = P.n;
     const uint32_t stride = gridDim.x * blockDim.x;
@@ -304,7 +325,7 @@ __global__ void __launch_bounds__(kScoreThreads) k_ckey_full(Pool P, Cfg c, Ctrl
             P.img[r] = (uint64_t)__double_as_longlong(key);
         }
         if (kDebug) {
-            if (P.cost[r]) { P.dbg_rate[r] = make_rate(S.tacc[t].T, S.tacc[t].trem); P.dbg_trem[r] = S.tacc[t].trem; }
+            if (P.cost[r]) { P.dbg_rate[r] = make_rate(S.tacc[t].Tr, S.tacc[t].trem); P.dbg_trem[r] = S.tacc[t].trem; }
             else { P.dbg_rate[r] = 0.0; P.dbg_trem[r] = 0; }
         }
     }
@@ -324,18 +345,42 @@ constexpr uint32_t kWinPfOff = (kWinPcOff + 8 * (kSpecWindow + 1) + 15) & ~15u;
 static_assert(kWinPfOff + 16 * (kSpecWindow + 1) <= 16 * kSpecCap, "window arrays must fit the sort-key region");
 
 constexpr uint32_t kSpecThreads = 512;        // sets up to 512 sort in registers/shuffles (block_sort_reg)
-__global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl, Scratch S,
-                                               cudaGraphConditionalHandle fb_handle, int in_graph, int reduce_only) {
+
+// The exact path, launched from the device only when needed (CUDA dynamic parallelism): a
+// chain of tail launches, each kernel launching its successor (select.cuh) -- a tail launch
+// runs once its launching grid has finished, and the step (graph node or stream work)
+// completes only after the whole chain.  radix = false: just the window over a large Cd.
+// Called by one thread; false if the launch failed.
+__device__ __noinline__ bool launch_exact_path(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, bool radix) {
+    ctrl->chain = 1;
+    if (!radix)
+        k_group<<<1, 1024, 12 * kGroupSmemSort, cudaStreamTailLaunch>>>(P, c, ctrl, S);
+    else if (P.n_single < P.n)                 // key the compound calls still tagged, then k_hist0
+        k_ckey_full<false><<<S.nb_full, kScoreThreads, 0, cudaStreamTailLaunch>>>(P, c, ctrl, S, 1);
+    else
+        k_hist0<<<S.grid_pass, kPassThreads, 0, cudaStreamTailLaunch>>>(P, c, ctrl, S, 0);
+    const cudaError_t e = cudaGetLastError();
+    ctrl->trace |= 1u;
+    ctrl->launch_err = e;
+    return e == cudaSuccess;
+}
+
+__global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl, Scratch S, int reduce_only) {
     const uint32_t* __restrict__ cost_rows = P.cost;
     extern __shared__ __align__(16) unsigned char smem[];
     u128* sk = reinterpret_cast<u128*>(smem);
     uint32_t* sv = reinterpret_cast<uint32_t*>(smem + sizeof(u128) * kSpecCap);
     __shared__ uint64_t s_scan[32];
     __shared__ unsigned long long s_min, s_cost;
-    __shared__ uint32_t s_pend, s_drop, s_err, s_ref;
+    __shared__ uint32_t s_pend, s_drop, s_err, s_ref, s_n;
     __shared__ int s_fb;
     stamp(ctrl, 0);
-    if (threadIdx.x == 0) { s_min = kNone; s_cost = 0; s_pend = 0; s_drop = 0; s_err = 0; s_ref = 0; }
+    if (threadIdx.x == 0) {
+        s_min = kNone; s_cost = 0; s_pend = 0; s_drop = 0; s_err = 0; s_ref = 0;
+        s_n = *S.spec_cnt;
+        *S.spec_cnt = 0;                                   // next step's set starts empty
+        ctrl->spec_n = s_n;
+    }
     __syncthreads();
     {   // partials of k_score and k_ctask
         uint32_t pend = 0, drop = 0, err = 0, ref = 0;
@@ -360,21 +405,19 @@ __global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl
     }
     if (reduce_only) return;                               // sharded step: the radix path follows
     stamp(ctrl, 1);
-    const uint32_t n = ctrl->spec_n, np = s_pend;
+    const uint32_t n = s_n, np = s_pend;
     if (threadIdx.x == 0) {
         s_fb = 0;
         if (s_err) { ctrl->status = ST_ERROR; s_fb = 2; }
         else if (np == 0) { ctrl->status = ST_EMPTY; s_fb = 2; }
-        else if (n > kSpecCap || n == 0) s_fb = 1;
+        else if (n > kSpecCap || n == 0) {
+            ctrl->status = ST_FALLBACK; ctrl->fallback = 1;
+            s_fb = launch_exact_path(P, c, ctrl, S, true) ? 1 : 3;
+        }
+        if (s_fb == 3) { ctrl->status = ST_ERROR; ctrl->error |= 2u; }
     }
     __syncthreads();
-    if (s_fb) {
-        if (threadIdx.x == 0 && s_fb == 1) {
-            ctrl->status = ST_FALLBACK; ctrl->fallback = 1;
-            if (in_graph) cudaGraphSetConditional(fb_handle, 1u);
-        }
-        return;
-    }
+    if (s_fb) return;                                      // k_publish (next node) reports it
     uint32_t n2 = 1;
     while (n2 < n) n2 <<= 1;
     for (uint32_t i = threadIdx.x; i < n2; i += blockDim.x) {
@@ -410,8 +453,8 @@ __global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl
         }
         if (fb) {
             ctrl->status = ST_FALLBACK; ctrl->fallback = 1;
-            if (in_graph) cudaGraphSetConditional(fb_handle, 1u);
-            s_fb = 1;
+            s_fb = launch_exact_path(P, c, ctrl, S, true) ? 1 : 3;
+            if (s_fb == 3) { ctrl->status = ST_ERROR; ctrl->error |= 2u; }
         } else {
             ctrl->b_star = fits; ctrl->bp = bp; ctrl->thr = thr; ctrl->thr_img = thr_img;
         }
@@ -427,10 +470,14 @@ __global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl
     }
     if (threadIdx.x == 0) { ctrl->n_cand = ncd; ctrl->status = ST_RESOLVED; }
     if (ncd > kSpecWindow) {
-        // a large Cd: hand it to k_group (inside the conditional body; the radix kernels there
-        // see status RESOLVED / fallback = 0 and skip)
+        // a large Cd: hand it to k_group (launched from here)
         for (uint32_t i = threadIdx.x; i < ncd; i += blockDim.x) S.cand[i] = sv[i];
-        if (threadIdx.x == 0 && in_graph) cudaGraphSetConditional(fb_handle, 1u);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            s_fb = launch_exact_path(P, c, ctrl, S, false) ? 1 : 3;
+            if (s_fb == 3) { ctrl->status = ST_ERROR; ctrl->error |= 2u; }
+        }
         return;
     }
     // (a9) in this CTA: the sorted-S region is reused for the (len, id) sort keys and the
@@ -446,5 +493,6 @@ __global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl
     stamp(ctrl, 5);
     window_select(P, c, ctrl, S, wsk, sv, ncd, pc, pf);
 }
+#endif  // JIT_EXACT_TU
 
 }  // namespace jit

@@ -57,7 +57,9 @@ struct alignas(16) Ctrl {
     uint32_t i_best, j_best, cand_overflow, exp_fill;
     unsigned long long tot_cost;     // sum of the token costs of all pending rows
     uint32_t spec_n, spec_ovf, fallback, window_done;
-    uint32_t n_refresh, pad3[3];                // length-bound refreshes this step (a2)
+    uint32_t n_refresh;                         // length-bound refreshes this step (a2)
+    uint32_t chain;                             // 1 while the device-launched exact path runs
+    uint32_t trace, launch_err;                 // exact-path kernels that ran (bit mask) / device launch error
     unsigned long long ts[12];                  // %globaltimer stamps of the single-CTA phases
 };
 
@@ -74,10 +76,13 @@ struct BlockPart {
 };
 
 // per-task accumulators of the compound pass (a4): sum of len_rem and of the call goodput
+// T, G, fmax, fmin are accumulated by k_score and consumed + re-zeroed by k_ctask (so the next
+// step starts from zero without a clearing pass); Gt, tgen, trem, Tr stay for the keying passes
 struct TaskAcc {
     unsigned long long T, G;          // sums over the stage's pending calls (k_score)
     unsigned long long Gt, tgen;      // task goodput and t_gen (k_ctask)
     long long trem;                   // stage t_rem (k_ctask)
+    unsigned long long Tr;            // T of this step (k_ctask; debug rate output)
     uint32_t fmax, fmin;              // max / min starvation frames of its pending calls (k_score)
 };
 // key-image placeholder of a pending compound call between k_score and its key pass:
@@ -112,9 +117,23 @@ struct Scratch {
     Persist* persist;
     BlockPart* part;         // k_score partials (grid_score entries)
     BlockPart* part2;        // k_ctask partials (grid_ctask entries)
-    TaskAcc* tacc;           // task_capacity, zeroed by k_begin every step
+    TaskAcc* tacc;           // task_capacity (see TaskAcc)
     uint32_t n_part, n_part2, task_cap, pad3;
+    unsigned int* spec_cnt;  // size of the speculative set (k_score / k_ctask atomics; reset by k_spec)
+    Ctrl* h_ctrl;            // pinned host copy of the control block, written by the step's last kernel
+    uint32_t nb_full, grid_pass;   // launch geometry of the fallback chain (device-side launches)
 };
+
+// The last kernel of a step writes the control block straight into pinned host memory (no
+// memcpy node in the graph); whole block, after its last write to ctrl.
+__device__ __forceinline__ void publish_ctrl(const Ctrl* ctrl, Ctrl* host) {
+    __syncthreads();
+    constexpr uint32_t kWords = sizeof(Ctrl) / 16;
+    static_assert(sizeof(Ctrl) % 16 == 0, "ctrl is copied in 16-byte words");
+    for (uint32_t i = threadIdx.x; i < kWords; i += blockDim.x)
+        reinterpret_cast<uint4*>(host)[i] = __ldcg(reinterpret_cast<const uint4*>(ctrl) + i);
+    __threadfence_system();
+}
 
 __device__ __forceinline__ bool is_last_block(uint32_t* counter) {
     __shared__ bool s_last;
@@ -154,7 +173,7 @@ __device__ __forceinline__ void warp_hist_add(uint32_t* s_cnt, uint32_t* s_cost,
 // first whose inclusive cumulative (count, cost), plus what lies above the bucket, exceeds
 // (max_batch, token_budget) -- the (B*+1)-th request of Alg. 1's priority order lies in it.
 // --------------------------------------------------------------------------------------
-__device__ void resolve_level(const Cfg& c, Ctrl* ctrl, uint32_t* hcnt, unsigned long long* hcost, uint32_t L) {
+static __device__ void resolve_level(const Cfg& c, Ctrl* ctrl, uint32_t* hcnt, unsigned long long* hcost, uint32_t L) {
     __shared__ uint64_t s_scan[32];
     __shared__ uint32_t s_first;
     const uint32_t nb = digit_bins(L);
@@ -225,19 +244,34 @@ __device__ void resolve_level(const Cfg& c, Ctrl* ctrl, uint32_t* hcnt, unsigned
 // --------------------------------------------------------------------------------------
 // k_begin
 // --------------------------------------------------------------------------------------
+// fresh control block of a step (written by one thread before any other use in the step)
+__device__ __forceinline__ void reset_ctrl(Ctrl* ctrl, int64_t now, int64_t v) {
+    Ctrl z;
+    memset(&z, 0, sizeof(z));
+    z.now = now; z.v = v;
+    z.min_img = kNone; z.pred_min_img = kNone;
+    *ctrl = z;
+}
+
+// the same by a whole CTA in 16-byte words (no Ctrl temporary in registers / on the stack)
+__device__ __forceinline__ void reset_ctrl_block(Ctrl* ctrl, int64_t now, int64_t v) {
+    for (uint32_t i = threadIdx.x; i < sizeof(Ctrl) / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(ctrl)[i] = make_uint4(0u, 0u, 0u, 0u);
+    __syncthreads();
+    if (threadIdx.x == 0) { ctrl->now = now; ctrl->v = v; ctrl->min_img = kNone; ctrl->pred_min_img = kNone; }
+}
+
+#ifndef JIT_EXACT_TU
+// full reset (load / sharded step); the graph step needs none: k_score resets ctrl and the
+// histograms, k_ctask re-zeroes the task accumulators it consumed, k_spec the set counter
 __global__ void k_begin(Ctrl* ctrl, uint32_t* hcnt, unsigned long long* hcost, int64_t now, int64_t v,
-                        TaskAcc* tacc, uint32_t n_tasks) {
+                        TaskAcc* tacc, uint32_t n_tasks, unsigned int* spec_cnt) {
     const uint32_t tid = threadIdx.x + blockIdx.x * blockDim.x, nt = blockDim.x * gridDim.x;
     for (uint32_t b = tid; b < 4096; b += nt) { hcnt[b] = 0; hcost[b] = 0; }
     for (uint32_t t = tid; t < n_tasks; t += nt) { tacc[t].T = 0; tacc[t].G = 0; tacc[t].fmax = 0; tacc[t].fmin = 0xFFFFFFFFu; }
-    if (tid == 0) {
-        Ctrl z;
-        memset(&z, 0, sizeof(z));
-        z.now = now; z.v = v;
-        z.min_img = kNone; z.pred_min_img = kNone;
-        *ctrl = z;
-    }
+    if (tid == 0) { reset_ctrl(ctrl, now, v); *spec_cnt = 0; }
 }
+#endif  // !JIT_EXACT_TU
 
 // --------------------------------------------------------------------------------------
 // per-row scoring of a standalone request: (a1) admission, (a2) length bound, (a3) t_rem,
@@ -313,12 +347,69 @@ __device__ __forceinline__ void score_standalone(const Cfg& c, const Table& T, c
     if (kDebug) { o.rate = make_rate(len_rem, trem); o.trem = trem; o.lhatc = Lh; }
 }
 
-// --------------------------------------------------------------------------------------
-// k_score
+// ======================================================================================
+// The exact path (radix select .. window): compiled into the separately linked unit
+// exact.cu only, because k_spec launches these kernels from the device (-rdc).
+// ======================================================================================
+// block exclusive scan of u128 (blockDim 1024)
+__device__ __forceinline__ u128 block_exclusive_scan_u128(u128 v, u128* scratch, u128* total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    u128 x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        u128 y = shfl_up_u128(x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) scratch[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        u128 s = lane < nw ? scratch[lane] : (u128)0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            u128 y = shfl_up_u128(s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < nw) scratch[lane] = s;
+    }
+    __syncthreads();
+    u128 base = wid ? scratch[wid - 1] : (u128)0;
+    u128 t = scratch[nw - 1];
+    __syncthreads();
+    if (total) *total = t;
+    return base + x - v;
+}
+
+#ifdef JIT_EXACT_TU
+// The exact path launched by k_spec runs as a chain of tail launches: each kernel launches its
+// successor (a tail launch runs once the launching grid has finished; one per grid).  Only
+// while ctrl->chain is set -- the same kernels launched from the host never chain.
+__global__ void k_pass(Pool P, Cfg c, Ctrl* ctrl, Scratch S, uint32_t pass_idx);
+__global__ void k_compact(Pool P, Cfg c, Ctrl* ctrl, Scratch S);
+__global__ void k_resolve(Pool P, Cfg c, Ctrl* ctrl, Scratch S);
+__global__ void k_cand(Pool P, Cfg c, Ctrl* ctrl, Scratch S, int only_after_fallback);
+__global__ void k_group(Pool P, Cfg c, Ctrl* ctrl, Scratch S);
+
+// successor of a radix level (k_hist0 = level 0, k_pass(i) = level i+1), decided by the
+// last CTA after it resolved the level; called by its thread 0
+__device__ __noinline__ void chain_after_level(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S,
+                                               uint32_t next_pass) {
+    const uint32_t st = *(volatile uint32_t*)&ctrl->status;
+    if (st == ST_HIST && next_pass < kLevels - 1)
+        k_pass<<<S.grid_pass, kPassThreads, 0, cudaStreamTailLaunch>>>(P, c, ctrl, S, next_pass);
+    else if (st == ST_COMPACT) k_compact<<<S.grid_pass, kPassThreads, 0, cudaStreamTailLaunch>>>(P, c, ctrl, S);
+    else if (st == ST_RESOLVED) k_cand<<<S.grid_pass, kPassThreads, 0, cudaStreamTailLaunch>>>(P, c, ctrl, S, 1);
+    else k_group<<<1, 1024, 12 * kGroupSmemSort, cudaStreamTailLaunch>>>(P, c, ctrl, S);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { ctrl->error |= 2u; ctrl->status = ST_ERROR; ctrl->launch_err = e; }
+    atomicOr(&ctrl->trace, 8u);
+}
+
 // level-0 histogram of the key images (fallback path only), last CTA resolves level 0
-__global__ void __launch_bounds__(kPassThreads) k_hist0(Pool P, Cfg c, Ctrl* ctrl, uint32_t* hcnt,
-                                                        unsigned long long* hcost, int force) {
+__global__ void __launch_bounds__(kPassThreads) k_hist0(Pool P, Cfg c, Ctrl* ctrl, Scratch S, int force) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&ctrl->trace, 4u);
     if (!force && ctrl->status != ST_FALLBACK) return;
+    uint32_t* hcnt = S.hcnt;
+    unsigned long long* hcost = S.hcost;
     __shared__ uint32_t s_cnt[2048], s_cost[2048];
     for (uint32_t b = threadIdx.x; b < 2048; b += blockDim.x) { s_cnt[b] = 0; s_cost[b] = 0; }
     __syncthreads();
@@ -335,15 +426,21 @@ __global__ void __launch_bounds__(kPassThreads) k_hist0(Pool P, Cfg c, Ctrl* ctr
     __syncthreads();
     for (uint32_t b = threadIdx.x; b < 2048; b += blockDim.x)
         if (s_cnt[b]) { atomicAdd(hcnt + b, s_cnt[b]); atomicAdd(hcost + b, (unsigned long long)s_cost[b]); }
-    if (is_last_block(&ctrl->done[0])) resolve_level(c, ctrl, hcnt, hcost, 0);
+    if (is_last_block(&ctrl->done[0])) {
+        resolve_level(c, ctrl, hcnt, hcost, 0);
+        __syncthreads();
+        if (threadIdx.x == 0 && ctrl->chain) chain_after_level(P, c, ctrl, S, 0);
+    }
 }
 
 // --------------------------------------------------------------------------------------
 // k_pass: one further digit of the cost-weighted radix select (only while status == HIST)
 // --------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kPassThreads) k_pass(Pool P, Cfg c, Ctrl* ctrl, uint32_t* hcnt,
-                                                       unsigned long long* hcost, uint32_t pass_idx) {
+__global__ void __launch_bounds__(kPassThreads) k_pass(Pool P, Cfg c, Ctrl* ctrl, Scratch S, uint32_t pass_idx) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&ctrl->trace, 16u);
     if (ctrl->status != ST_HIST) return;
+    uint32_t* hcnt = S.hcnt;
+    unsigned long long* hcost = S.hcost;
     __shared__ uint32_t s_cnt[4096], s_cost[4096];
     for (uint32_t b = threadIdx.x; b < 4096; b += blockDim.x) { s_cnt[b] = 0; s_cost[b] = 0; }
     __syncthreads();
@@ -373,13 +470,22 @@ __global__ void __launch_bounds__(kPassThreads) k_pass(Pool P, Cfg c, Ctrl* ctrl
     __syncthreads();
     for (uint32_t b = threadIdx.x; b < 4096; b += blockDim.x)
         if (s_cnt[b]) { atomicAdd(hcnt + b, s_cnt[b]); atomicAdd(hcost + b, (unsigned long long)s_cost[b]); }
-    if (is_last_block(&ctrl->done[1 + (pass_idx & 7)])) resolve_level(c, ctrl, hcnt, hcost, L);
+    if (is_last_block(&ctrl->done[1 + (pass_idx & 7)])) {
+        resolve_level(c, ctrl, hcnt, hcost, L);
+        __syncthreads();
+        if (threadIdx.x == 0 && ctrl->chain) chain_after_level(P, c, ctrl, S, pass_idx + 1);
+    }
 }
 
 // --------------------------------------------------------------------------------------
 // k_compact: gather the final bucket and the smallest key image above it
 // --------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kPassThreads) k_compact(Pool P, Ctrl* ctrl, Scratch S) {
+__global__ void __launch_bounds__(kPassThreads) k_compact(Pool P, Cfg c, Ctrl* ctrl, Scratch S) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&ctrl->trace, 32u);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && ctrl->chain) {
+        k_resolve<<<1, 1024, (sizeof(u128) + 4) * kBucketCap, cudaStreamTailLaunch>>>(P, c, ctrl, S);
+        if (cudaGetLastError() != cudaSuccess) { ctrl->error |= 2u; ctrl->status = ST_ERROR; }
+    }
     if (ctrl->status != ST_COMPACT) return;
     const uint32_t L = ctrl->level;
     const u128 prefix = ctrl->prefix;
@@ -419,7 +525,12 @@ __global__ void __launch_bounds__(kPassThreads) k_compact(Pool P, Ctrl* ctrl, Sc
 // --------------------------------------------------------------------------------------
 // k_resolve: one CTA (1024 threads) -- exact B*, bp, thr from the sorted bucket (a7, a8)
 // --------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) k_resolve(Cfg c, Ctrl* ctrl, Scratch S) {
+__global__ void __launch_bounds__(1024) k_resolve(Pool P, Cfg c, Ctrl* ctrl, Scratch S) {
+    if (threadIdx.x == 0) atomicOr(&ctrl->trace, 64u);
+    if (threadIdx.x == 0 && ctrl->chain) {
+        k_cand<<<S.grid_pass, kPassThreads, 0, cudaStreamTailLaunch>>>(P, c, ctrl, S, 1);
+        if (cudaGetLastError() != cudaSuccess) { ctrl->error |= 2u; ctrl->status = ST_ERROR; }
+    }
     if (ctrl->status != ST_COMPACT) return;
     extern __shared__ __align__(16) unsigned char smem[];
     u128* sk = reinterpret_cast<u128*>(smem);
@@ -475,7 +586,12 @@ __global__ void __launch_bounds__(1024) k_resolve(Cfg c, Ctrl* ctrl, Scratch S) 
 // --------------------------------------------------------------------------------------
 // k_cand: Cd = {pending : key >= thr} (Alg. 1 Filter)
 // --------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kPassThreads) k_cand(Pool P, Ctrl* ctrl, Scratch S, int only_after_fallback) {
+__global__ void __launch_bounds__(kPassThreads) k_cand(Pool P, Cfg c, Ctrl* ctrl, Scratch S, int only_after_fallback) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&ctrl->trace, 128u);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && ctrl->chain) {
+        k_group<<<1, 1024, 12 * kGroupSmemSort, cudaStreamTailLaunch>>>(P, c, ctrl, S);
+        if (cudaGetLastError() != cudaSuccess) { ctrl->error |= 2u; ctrl->status = ST_ERROR; }
+    }
     if (ctrl->status != ST_RESOLVED) return;
     if (only_after_fallback && !ctrl->fallback) return;      // k_spec already produced Cd
     const uint64_t thr_img = ctrl->thr_img;
@@ -501,33 +617,8 @@ __global__ void __launch_bounds__(kPassThreads) k_cand(Pool P, Ctrl* ctrl, Scrat
     }
 }
 
-// block exclusive scan of u128 (blockDim 1024)
-__device__ __forceinline__ u128 block_exclusive_scan_u128(u128 v, u128* scratch, u128* total) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    u128 x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        u128 y = shfl_up_u128(x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) scratch[wid] = x;
-    __syncthreads();
-    if (wid == 0) {
-        u128 s = lane < nw ? scratch[lane] : (u128)0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            u128 y = shfl_up_u128(s, o);
-            if (lane >= o) s += y;
-        }
-        if (lane < nw) scratch[lane] = s;
-    }
-    __syncthreads();
-    u128 base = wid ? scratch[wid - 1] : (u128)0;
-    u128 t = scratch[nw - 1];
-    __syncthreads();
-    if (total) *total = t;
-    return base + x - v;
-}
+
+#endif  // JIT_EXACT_TU
 
 // --------------------------------------------------------------------------------------
 // (a9) Alg. 1 step 2 under the token budget, executed by ONE CTA of 1024 threads:
@@ -537,7 +628,7 @@ __device__ __forceinline__ u128 block_exclusive_scan_u128(u128 v, u128* scratch,
 // (shared memory when they fit, else global scratch).  Writes the batch and the bookkeeping
 // (ever_scheduled, Running, undo steps_waited+1) and the next step's speculative threshold.
 // --------------------------------------------------------------------------------------
-__device__ void window_select(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint64_t* sk, uint32_t* sv,
+static __device__ void window_select(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint64_t* sk, uint32_t* sv,
                               uint32_t n, unsigned long long* pc, u128* pf) {
     __shared__ u128 s_scan128[32];
     __shared__ uint64_t s_scan[32];
@@ -628,10 +719,20 @@ __device__ void window_select(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scr
     stamp(ctrl, 10);
 }
 
+#ifdef JIT_EXACT_TU
 // k_group: the window over Cd = S.cand (after the radix path or a too-large speculative Cd)
+static __device__ void group_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, unsigned char* smem);
 __global__ void __launch_bounds__(1024) k_group(Pool P, Cfg c, Ctrl* ctrl, Scratch S) {
-    if (ctrl->status != ST_RESOLVED || ctrl->window_done) return;
     extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int s_run;
+    if (threadIdx.x == 0) { s_run = ctrl->status == ST_RESOLVED && !ctrl->window_done; atomicOr(&ctrl->trace, 256u); }
+    __syncthreads();
+    if (s_run) group_body(P, c, ctrl, S, smem);
+    __syncthreads();
+    if (threadIdx.x == 0) ctrl->chain = 0;                  // the exact path ends here
+}
+
+static __device__ void group_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, unsigned char* smem) {
     const uint32_t n = ctrl->n_cand;
     if (ctrl->cand_overflow || n == 0) {
         if (threadIdx.x == 0) { ctrl->error = 1; ctrl->status = ST_ERROR; }
@@ -651,6 +752,15 @@ __global__ void __launch_bounds__(1024) k_group(Pool P, Cfg c, Ctrl* ctrl, Scrat
     }
     window_select(P, c, ctrl, S, sk, sv, n, S.pc, S.pf);
 }
+
+#endif  // JIT_EXACT_TU
+
+#ifndef JIT_EXACT_TU
+// k_publish: the step's last graph node -- copies the control block to pinned host memory.
+// It also makes the graph wait for the exact path: when the node that made device-side tail
+// launches is the graph's LAST node, graph completion was measured NOT to wait for nested
+// tail launches (profiles/micro_cdp2.cu, mode 5); any node after it restores the ordering.
+__global__ void k_publish(const Ctrl* ctrl, Ctrl* host) { publish_ctrl(ctrl, host); }
 
 // progress updates from the engine, applied before scoring
 __global__ void k_progress(Pool P, const uint32_t* rows, const uint32_t* gen, const uint32_t* pre,
@@ -697,5 +807,7 @@ __global__ void k_validate(Pool P, const Group* groups, uint32_t n_groups, uint3
     }
     if (bad) atomicOr(&ctrl->error, 2u);
 }
+
+#endif  // !JIT_EXACT_TU
 
 }  // namespace jit
