@@ -183,7 +183,8 @@ int jit_sched_read_rows(jit_sched* h, double* key, double* rate, int64_t* t_rem,
 /* Per-kernel device time, from CUDA events recorded (as graph event nodes) on cfg.stream
  * around each kernel of the step.  enable > 0 keeps one event set per step for up to
  * `enable` steps; 0 turns timing off; < 0 leaves it unchanged.  ms_out (n_out <= 5) gets the
- * average in ms over the recorded steps of [score, select, candidates, group, whole step]. */
+ * average in ms over the recorded steps of [k_score, k_ctask, k_spec (including the exact
+ * path it launched, if any), k_publish, whole step]. */
 int jit_sched_kernel_times(jit_sched* h, int enable, float* ms_out, uint32_t n_out);
 
 /* Diagnostics: %globaltimer stamps (ns) of the phases of the single-CTA resolve of the last

@@ -112,7 +112,9 @@ static void carve(Carve& cv, const jit_config* cfg, const jit_len_table* tab, Po
     S.out_ids = cv.take<uint32_t>(cfg->max_batch + 1); S.out_tokens = cv.take<uint32_t>(cfg->max_batch + 1);
     S.out_rows = cv.take<uint32_t>(cfg->max_batch + 1);
     S.cand_cap = (uint32_t)N;
-    S.spec_ck = cv.take<u128>(kSpecCap); S.spec_row = cv.take<uint32_t>(kSpecCap);
+    S.spec_img = cv.take<uint64_t>(kSpecCap);
+    S.spec_id = cv.take<uint32_t>(kSpecCap); S.spec_row = cv.take<uint32_t>(kSpecCap);
+    S.spec_cost = cv.take<uint32_t>(kSpecCap); S.spec_len = cv.take<uint32_t>(kSpecCap);
     S.persist = cv.take<Persist>(1);
     S.spec_cnt = cv.take<unsigned int>(1);
     S.part = cv.take<BlockPart>(kMaxParts); S.part2 = cv.take<BlockPart>(kMaxParts);
@@ -333,8 +335,8 @@ static int build_graph(jit_sched* h) {
     enqueue_score(h, s, 0, 1, h->timing ? h->ev[1] : nullptr, true);
     if (h->timing) cudaEventRecordWithFlags(h->ev[2], s, cudaEventRecordExternal);
     exact::spec(h->P, h->c, h->d_ctrl, S, 0, s);
-    k_publish<<<1, 64, 0, s>>>(h->d_ctrl, h->h_ctrl);
     if (h->timing) cudaEventRecordWithFlags(h->ev[3], s, cudaEventRecordExternal);
+    k_publish<<<1, 64, 0, s>>>(h->d_ctrl, h->h_ctrl);
     if (h->timing) cudaEventRecordWithFlags(h->ev[4], s, cudaEventRecordExternal);
     CK(cudaStreamEndCapture(s, &g));
     size_t nn = 0;
@@ -377,8 +379,9 @@ static int launch_direct(jit_sched* h, int64_t now, int64_t v) {
     enqueue_score(h, s, now, v, ev ? e[1] : nullptr, false);
     if (ev) cudaEventRecord(e[2], s);
     exact::spec(h->P, h->c, h->d_ctrl, h->S, 0, s);
+    if (ev) cudaEventRecord(e[3], s);
     k_publish<<<1, 64, 0, s>>>(h->d_ctrl, h->h_ctrl);
-    if (ev) { cudaEventRecord(e[3], s); cudaEventRecord(e[4], s); }
+    if (ev) cudaEventRecord(e[4], s);
     CK(cudaGetLastError());
     return JIT_OK;
 }
@@ -521,7 +524,7 @@ extern "C" int jit_sched_read_rows(jit_sched* h, double* key, double* rate, int6
 extern "C" int jit_sched_kernel_times(jit_sched* h, int enable, float* ms_out, uint32_t n_out) {
     // enable > 0: record per-kernel events for up to `enable` steps (ring of event slots);
     // enable = 0: off; enable < 0: leave as is.  ms_out gets the AVERAGE over the recorded
-    // steps of [k_score, k_ctask, k_spec (+ in-CTA window), fallback body (radix path + k_group), chain].
+    // steps of [k_score, k_ctask, k_spec (+ the exact path it launched), k_publish, whole step].
     if (!h) return JIT_EINVAL;
     if (enable >= 0) {
         CK(cudaStreamSynchronize(h->stream));
@@ -544,8 +547,8 @@ extern "C" int jit_sched_kernel_times(jit_sched* h, int enable, float* ms_out, u
             float t;
             CK(cudaEventElapsedTime(&t, e[0], e[1])); acc[0] += t;   // k_score
             CK(cudaEventElapsedTime(&t, e[1], e[2])); acc[1] += t;   // k_ctask
-            CK(cudaEventElapsedTime(&t, e[2], e[3])); acc[2] += t;   // k_spec + window
-            CK(cudaEventElapsedTime(&t, e[3], e[4])); acc[3] += t;   // conditional fallback body
+            CK(cudaEventElapsedTime(&t, e[2], e[3])); acc[2] += t;   // k_spec (+ the exact path it launched)
+            CK(cudaEventElapsedTime(&t, e[3], e[4])); acc[3] += t;   // k_publish
             CK(cudaEventElapsedTime(&t, e[0], e[4])); acc[4] += t;   // total
         }
         for (uint32_t i = 0; i < n_out && i < 5; ++i) ms_out[i] = (float)(acc[i] / ns);

@@ -17,8 +17,8 @@ cudaError_t init_attributes() {
                                   (int)((sizeof(u128) + 4) * kBucketCap))) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(k_group, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(12 * kGroupSmemSort))) !=
         cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(k_spec, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)((sizeof(u128) + 4) * kSpecCap))) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(k_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSpecSmem)) !=
+        cudaSuccess) return e;
     // one shared-memory carveout for every kernel of the step (see abi.cu)
     const void* ks[] = {(const void*)k_ckey_full<false>, (const void*)k_ckey_full<true>, (const void*)k_spec,
                         (const void*)k_hist0, (const void*)k_pass, (const void*)k_compact, (const void*)k_resolve,
@@ -30,7 +30,7 @@ cudaError_t init_attributes() {
 }
 
 void spec(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int reduce_only, cudaStream_t s) {
-    k_spec<<<1, kSpecThreads, (sizeof(u128) + 4) * kSpecCap, s>>>(P, c, ctrl, S, reduce_only);
+    k_spec<<<1, kSpecThreads, kSpecSmem, s>>>(P, c, ctrl, S, reduce_only);
 }
 void ckey_full(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t grid, bool debug, int force,
                cudaStream_t s) {

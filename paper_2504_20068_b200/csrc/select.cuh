@@ -112,8 +112,10 @@ struct Scratch {
     uint32_t* out_tokens;
     uint32_t* out_rows;
     uint32_t cand_cap, pad;
-    u128* spec_ck;           // kSpecCap: rows with key image >= t_guess (composite key)
-    uint32_t* spec_row;
+    // the speculative set (kSpecCap entries): rows with key image >= t_guess, with what k_spec
+    // needs of them (key image, id, row, token cost, window length key)
+    uint64_t* spec_img;
+    uint32_t *spec_id, *spec_row, *spec_cost, *spec_len;
     Persist* persist;
     BlockPart* part;         // k_score partials (grid_score entries)
     BlockPart* part2;        // k_ctask partials (grid_ctask entries)

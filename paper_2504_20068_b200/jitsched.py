@@ -302,7 +302,8 @@ class Scheduler:
 
     def kernel_times(self, slots=None):
         """slots=k>0 records per-kernel events for up to k steps, 0 disables; with no argument
-        returns the average [score, select, cand, group, total] ms over the recorded steps."""
+        returns the average [k_score, k_ctask, k_spec (+ exact path), k_publish, total] ms over
+        the recorded steps."""
         if slots is not None:
             self._check(self.lib.jit_sched_kernel_times(self.h, C.c_int(int(slots)), None, 0), self.h)
             return None
