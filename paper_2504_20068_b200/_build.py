@@ -19,16 +19,18 @@ def sources():
     return sorted(glob.glob(os.path.join(HERE, "csrc", "*")) + [os.path.join(ROOT, "include", "jit_sched.h")])
 
 
-def build_library(force: bool = False, verbose: bool = False) -> str:
+def build_library(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    """Build the library at `out` (default: the in-tree libjitsched.so); `defines` are extra -D
+    flags for tuning experiments (profiles/variants.sh builds variants beside the default)."""
     newest = max(os.path.getmtime(s) for s in sources())
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
-        return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= newest:
+        return out
+    tmp = out + f".tmp{os.getpid()}"
     inc = ["-I", os.path.join(ROOT, "include")]
     objs, log = [], ""
     for src, extra in UNITS:
         obj = tmp + "." + src + ".o"
-        cmd = [NVCC] + BASE + extra + inc + ["-c", "-o", obj, os.path.join(HERE, "csrc", src)]
+        cmd = [NVCC] + BASE + extra + list(defines) + inc + ["-c", "-o", obj, os.path.join(HERE, "csrc", src)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n" + r.stdout[-4000:] + r.stderr[-8000:])
@@ -41,5 +43,5 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc link failed:\n" + r.stdout[-4000:] + r.stderr[-8000:])
     if verbose:
         print(log[-6000:])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out

@@ -41,13 +41,15 @@ struct jit_sched {
     void* score_args[9];
     uint32_t arg_ntasks = 0;
     int64_t arg_now = 0, arg_v = 0;
-    bool loaded = false, graph_dirty = true, timing = false, debug = false;
+    bool loaded = false, graph_dirty = true, timing = false, debug = false, pdl = true;
     cudaEvent_t ev[6] = {};
     cudaGraphNode_t ev_node[5] = {};      // event-record nodes of the timed graph
     std::vector<cudaEvent_t> slots;       // 5 events per recorded step
     uint32_t n_slots = 0, slot_used = 0;
     int n_sm = 148;
-    uint32_t nb_score = 1, nb_ctask = 1, nb_full = 1, grid_pass = 1;
+    uint32_t nb_score = 1, grid_pass = 1;
+    std::vector<uint32_t> h_off;          // host copy of call_off (device-resident pools)
+    std::vector<CRange> h_rng;
     std::string err;
 };
 
@@ -117,9 +119,8 @@ static void carve(Carve& cv, const jit_config* cfg, const jit_len_table* tab, Po
     S.spec_cost = cv.take<uint32_t>(kSpecCap); S.spec_len = cv.take<uint32_t>(kSpecCap);
     S.persist = cv.take<Persist>(1);
     S.spec_cnt = cv.take<unsigned int>(1);
-    S.part = cv.take<BlockPart>(kMaxParts); S.part2 = cv.take<BlockPart>(kMaxParts);
-    S.tacc = cv.take<TaskAcc>(NT);
-    S.task_cap = (uint32_t)NT;
+    S.part = cv.take<BlockPart>(N / kTile + NT + 2);   // one per k_score CTA (<= work items)
+    S.crange = cv.take<CRange>(NT + 1);
     ctrl = cv.take<Ctrl>(1);
     stage = cv.take<uint32_t>(4 * N);
 }
@@ -204,11 +205,12 @@ extern "C" int jit_sched_init(const jit_config* cfg, const jit_slo_group* groups
     for (auto& e : h->ev) CK(cudaEventCreate(&e));
     CK(exact::init_attributes());
     CK(cudaFuncSetAttribute(k_group_rec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(12 * kGroupSmemSort)));
+    CK(cudaFuncSetAttribute(k_score<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)score_smem_bytes(false)));
+    CK(cudaFuncSetAttribute(k_score<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)score_smem_bytes(true)));
     // one shared-memory carveout for every kernel of the step: switching the L1/shared split
     // between consecutive kernels costs a drain + reconfiguration of the SMs (several µs each)
     {
-        const void* ks[] = {(const void*)k_begin, (const void*)k_score<false>, (const void*)k_score<true>,
-                            (const void*)k_ctask};
+        const void* ks[] = {(const void*)k_begin, (const void*)k_score<false>, (const void*)k_score<true>};
         for (const void* k : ks)
             CK(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
     }
@@ -260,32 +262,51 @@ extern "C" int jit_sched_load(jit_sched* h, const jit_pool* p) {
     P.n = p->n; P.n_single = p->n_single; P.n_tasks = p->n_tasks;
     // validate on the device (also covers device-resident pools)
     // full reset: control block, histograms, the task accumulators, the speculative-set counter
-    k_begin<<<4, 1024, 0, h->stream>>>(h->d_ctrl, h->S.hcnt, h->S.hcost, 0, 1, h->S.tacc, p->n_tasks, h->S.spec_cnt);
+    k_begin<<<4, 1024, 0, h->stream>>>(h->d_ctrl, h->S.hcnt, h->S.hcost, 0, 1, h->S.spec_cnt);
     const uint32_t vb = (uint32_t)std::min<uint64_t>((n + 255) / 256 + 1, (uint64_t)h->n_sm * 8);
     k_validate<<<vb, 256, 0, h->stream>>>(P, h->d_groups, h->n_groups, h->T.n_rows, h->d_ctrl);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(h->h_ctrl, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     if (h->h_ctrl->error) { h->loaded = false; return set_err(h, JIT_EINVAL, "invalid pool (layout / ranges / groups)"); }
-    // launch geometry
-    // rows: grid-stride over a persistent-style grid (6 CTAs of 256 per SM); tasks: thread per
-    // task (k_ctask); compound rows: grid-stride (k_ckey_full)
-    // one wave: the persistent grid is exactly what fits (registers bound k_score's occupancy)
-    int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &occ, h->debug ? (const void*)k_score<true> : (const void*)k_score<false>, kScoreThreads, 0));
-    occ = std::max(occ, 1);
-    h->nb_score = std::max<uint32_t>(1, std::min<uint32_t>((P.n + kScoreThreads - 1) / kScoreThreads, (uint32_t)(h->n_sm * occ)));
-    h->nb_ctask = std::max<uint32_t>(1, std::min<uint32_t>((P.n_tasks + kScoreThreads - 1) / kScoreThreads,
-                                                           (uint32_t)h->n_sm * 4));
-    h->nb_full = std::max<uint32_t>(1, std::min<uint32_t>((P.n - P.n_single + kScoreThreads - 1) / kScoreThreads,
-                                                          (uint32_t)h->n_sm * 6));
-    h->nb_score = std::min(h->nb_score, kMaxParts);
-    h->nb_ctask = std::min(h->nb_ctask, kMaxParts);
-    h->S.n_part = h->nb_score; h->S.n_part2 = h->nb_ctask;
-    h->arg_ntasks = P.n_tasks;
+    // launch geometry of k_score: standalone tiles of kTile rows, then the compound ranges --
+    // whole tasks packed greedily so that a range spans at most one tile of aligned quads
+    // (a task of more than kTile calls gets a range of its own, scored in several tiles)
+    const uint32_t n_std = (P.n_single + kTile - 1) / kTile;
+    h->h_rng.clear();
+    if (nt) {
+        const uint32_t* off = p->call_off;
+        if (p->on_device) {
+            h->h_off.resize(nt + 1);
+            CK(cudaMemcpy(h->h_off.data(), p->call_off, 4 * (nt + 1), cudaMemcpyDeviceToHost));
+            off = h->h_off.data();
+        }
+        CRange cur{off[0], off[0], 0, 0};
+        for (uint32_t t = 0; t < nt; ++t) {
+            if (t > cur.t0 && off[t + 1] - (cur.r0 & ~3u) > kTile) {
+                cur.r1 = off[t]; cur.t1 = t;
+                h->h_rng.push_back(cur);
+                cur.r0 = off[t]; cur.t0 = t;
+            }
+        }
+        cur.r1 = off[nt]; cur.t1 = (uint32_t)nt;
+        h->h_rng.push_back(cur);
+        CK(cudaMemcpyAsync((void*)h->S.crange, h->h_rng.data(), sizeof(CRange) * h->h_rng.size(),
+                           cudaMemcpyHostToDevice, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    }
+    h->S.n_std = n_std;
+    h->S.n_crange = (uint32_t)h->h_rng.size();
+    {   // persistent grid: every CTA that fits (two tile buffers each), at most one per item
+        const void* kf = h->debug ? (const void*)k_score<true> : (const void*)k_score<false>;
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, kScoreThreads, score_smem_bytes(h->debug)));
+        const uint32_t items = h->S.n_std + h->S.n_crange;
+        h->nb_score = std::max<uint32_t>(1, std::min<uint32_t>(items, (uint32_t)(h->n_sm * std::max(occ, 1))));
+    }
+    h->S.n_part = h->nb_score;
     h->grid_pass = std::max<uint32_t>(1, std::min<uint32_t>((P.n + kPassThreads - 1) / kPassThreads, (uint32_t)h->n_sm * 4));
-    h->S.nb_full = h->nb_full; h->S.grid_pass = h->grid_pass;    // for k_spec's device-side launches
+    h->S.grid_pass = h->grid_pass;    // for k_spec's device-side launches
     if (!same_shape) h->graph_dirty = true;
     h->loaded = true;
     return JIT_OK;
@@ -299,13 +320,10 @@ static void enqueue_score(jit_sched* h, cudaStream_t s, int64_t now, int64_t v, 
     Pool& P = h->P;
     Scratch& S = h->S;
     if (h->debug)
-        k_score<true><<<h->nb_score, kScoreThreads, 0, s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S, now, v);
+        k_score<true><<<h->nb_score, kScoreThreads, score_smem_bytes(true), s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S, now, v);
     else
-        k_score<false><<<h->nb_score, kScoreThreads, 0, s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S, now, v);
+        k_score<false><<<h->nb_score, kScoreThreads, score_smem_bytes(false), s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S, now, v);
     if (mid) cudaEventRecordWithFlags(mid, s, capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
-    k_ctask<<<h->nb_ctask, kScoreThreads, 0, s>>>(P, h->c, h->d_ctrl, S);
-    // debug: every compound call gets its key and rate outputs now (read_rows sees them all)
-    if (h->debug) exact::ckey_full(P, h->c, h->d_ctrl, S, h->nb_full, true, 1, s);
 }
 
 // host-side continuation of the radix select (only for heavy key ties, see finish_step)
@@ -319,11 +337,13 @@ static void enqueue_radix(jit_sched* h, cudaStream_t s, uint32_t first_pass, uin
     exact::group(P, h->c, h->d_ctrl, S, s);
 }
 
-// Step graph: k_score -> k_ctask -> k_spec -> k_publish, four kernel nodes and nothing else.
-// k_score resets the control block, k_publish copies it to pinned host memory; when the
-// speculative resolve cannot be exact, k_spec itself launches the exact path (launch_exact_path,
-// a chain of device-side tail launches) -- no conditional node and no copy node, whose fixed
-// costs measured ~26 us and ~6 us per step on B200 (profiles/host_overhead.py).
+// Step graph: k_score -> k_spec, two kernel nodes and nothing else.  k_score resets the control
+// block; k_spec (programmatic dependent launch: its launch overlaps k_score) resolves the batch
+// and copies the control block to pinned host memory.  When the speculative resolve cannot be
+// exact, k_spec marks the step and finish_step runs the exact radix path from the host -- no
+// device-side launches, no conditional or copy nodes (their fixed costs measured ~26 us and ~6 us
+// per step on B200, profiles/host_overhead.py).  With kernel timing on, event-record nodes
+// separate the kernels (full dependencies, no PDL).
 static int build_graph(jit_sched* h) {
     if (h->exec) { cudaGraphExecDestroy(h->exec); h->exec = nullptr; }
     if (h->graph) { cudaGraphDestroy(h->graph); h->graph = nullptr; }
@@ -334,10 +354,18 @@ static int build_graph(jit_sched* h) {
     if (h->timing) cudaEventRecordWithFlags(h->ev[0], s, cudaEventRecordExternal);
     enqueue_score(h, s, 0, 1, h->timing ? h->ev[1] : nullptr, true);
     if (h->timing) cudaEventRecordWithFlags(h->ev[2], s, cudaEventRecordExternal);
-    exact::spec(h->P, h->c, h->d_ctrl, S, 0, s);
-    if (h->timing) cudaEventRecordWithFlags(h->ev[3], s, cudaEventRecordExternal);
-    k_publish<<<1, 64, 0, s>>>(h->d_ctrl, h->h_ctrl);
-    if (h->timing) cudaEventRecordWithFlags(h->ev[4], s, cudaEventRecordExternal);
+    const cudaError_t le = exact::spec(h->P, h->c, h->d_ctrl, S, 0, s, !h->timing && h->pdl);
+    if (h->timing) {
+        cudaEventRecordWithFlags(h->ev[3], s, cudaEventRecordExternal);
+        cudaEventRecordWithFlags(h->ev[4], s, cudaEventRecordExternal);
+    }
+    if (le != cudaSuccess) {
+        cudaStreamEndCapture(s, &g);
+        if (g) cudaGraphDestroy(g);
+        (void)cudaGetLastError();
+        if (h->pdl) { h->pdl = false; return build_graph(h); }   // no PDL in graphs here: plain edge
+        return set_err(h, JIT_ECUDA, "graph capture of k_spec: %s", cudaGetErrorString(le));
+    }
     CK(cudaStreamEndCapture(s, &g));
     size_t nn = 0;
     CK(cudaGraphGetNodes(g, nullptr, &nn));
@@ -369,7 +397,7 @@ static int build_graph(jit_sched* h) {
     return JIT_OK;
 }
 
-// JIT_CFG_NO_GRAPH: the same three kernels as direct launches (for profilers)
+// JIT_CFG_NO_GRAPH: the same kernels as direct launches (for profilers)
 static int launch_direct(jit_sched* h, int64_t now, int64_t v) {
     cudaStream_t s = h->stream;
     const bool ev = h->timing && h->n_slots;
@@ -378,10 +406,8 @@ static int launch_direct(jit_sched* h, int64_t now, int64_t v) {
     if (ev) cudaEventRecord(e[0], s);
     enqueue_score(h, s, now, v, ev ? e[1] : nullptr, false);
     if (ev) cudaEventRecord(e[2], s);
-    exact::spec(h->P, h->c, h->d_ctrl, h->S, 0, s);
-    if (ev) cudaEventRecord(e[3], s);
-    k_publish<<<1, 64, 0, s>>>(h->d_ctrl, h->h_ctrl);
-    if (ev) cudaEventRecord(e[4], s);
+    CK(exact::spec(h->P, h->c, h->d_ctrl, h->S, 0, s, !ev && h->pdl));
+    if (ev) { cudaEventRecord(e[3], s); cudaEventRecord(e[4], s); }
     CK(cudaGetLastError());
     return JIT_OK;
 }
@@ -425,11 +451,18 @@ static int finish_step(jit_sched* h, jit_batch* out) {
                 "fb %u spec %u trace %x\n", dc.status, dc.error, dc.fallback, dc.spec_n, dc.trace, dc.launch_err, dc.chain,
                 h->h_ctrl->status, h->h_ctrl->error, h->h_ctrl->fallback, h->h_ctrl->spec_n, h->h_ctrl->trace);
     }
-    if (h->h_ctrl->status == ST_HIST) {
-        // rare: the boundary bucket stayed large after the exact path's first two digits
-        // (heavy key ties); finish the radix select with the remaining digits from the host
-        // (k_group publishes ctrl again)
-        enqueue_radix(h, h->stream, 1, kLevels - 1);
+    const uint32_t st0 = h->h_ctrl->status;
+    if (st0 == ST_FALLBACK || (st0 == ST_RESOLVED && !h->h_ctrl->window_done && !h->h_ctrl->error)) {
+        // the speculative resolve could not be exact (first step after a load, a threshold far
+        // off, heavy key ties) or Cd was too large for k_spec's window: the exact path --
+        // cost-weighted radix select over every key, candidates, window -- from the host
+        Pool& P = h->P;
+        if (st0 == ST_FALLBACK) {
+            exact::hist0(P, h->c, h->d_ctrl, h->S, h->grid_pass, 0, h->stream);
+            enqueue_radix(h, h->stream, 0, kLevels - 1);
+        } else {
+            exact::group(P, h->c, h->d_ctrl, h->S, h->stream);
+        }
         k_publish<<<1, 64, 0, h->stream>>>(h->d_ctrl, h->h_ctrl);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(h->stream));
@@ -494,10 +527,6 @@ extern "C" int jit_sched_read_rows(jit_sched* h, double* key, double* rate, int6
     if (!h->loaded) return set_err(h, JIT_ESTATE, "read_rows before load");
     const uint64_t n = h->P.n;
     if ((rate || t_rem || lhat) && !h->debug) return set_err(h, JIT_ESTATE, "rate/t_rem/lhat need JIT_CFG_DEBUG_ROWS");
-    // compound calls of tasks that could not reach the batch still carry their frame tag
-    // (k_ctask); key them from the last step's task accumulators (idempotent)
-    if ((key || pending) && h->P.n_single < h->P.n)
-        exact::ckey_full(h->P, h->c, h->d_ctrl, h->S, h->nb_full, false, 1, h->stream);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(h->stream));
     std::vector<uint64_t> img;
@@ -524,7 +553,7 @@ extern "C" int jit_sched_read_rows(jit_sched* h, double* key, double* rate, int6
 extern "C" int jit_sched_kernel_times(jit_sched* h, int enable, float* ms_out, uint32_t n_out) {
     // enable > 0: record per-kernel events for up to `enable` steps (ring of event slots);
     // enable = 0: off; enable < 0: leave as is.  ms_out gets the AVERAGE over the recorded
-    // steps of [k_score, k_ctask, k_spec (+ the exact path it launched), k_publish, whole step].
+    // steps of [k_score, (unused, 0), k_spec, (unused, 0), whole step].
     if (!h) return JIT_EINVAL;
     if (enable >= 0) {
         CK(cudaStreamSynchronize(h->stream));
@@ -546,9 +575,9 @@ extern "C" int jit_sched_kernel_times(jit_sched* h, int enable, float* ms_out, u
             cudaEvent_t* e = &h->slots[5 * k];
             float t;
             CK(cudaEventElapsedTime(&t, e[0], e[1])); acc[0] += t;   // k_score
-            CK(cudaEventElapsedTime(&t, e[1], e[2])); acc[1] += t;   // k_ctask
+            CK(cudaEventElapsedTime(&t, e[1], e[2])); acc[1] += t;   // (empty: k_score has no successor pass)
             CK(cudaEventElapsedTime(&t, e[2], e[3])); acc[2] += t;   // k_spec (+ the exact path it launched)
-            CK(cudaEventElapsedTime(&t, e[3], e[4])); acc[3] += t;   // k_publish
+            CK(cudaEventElapsedTime(&t, e[3], e[4])); acc[3] += t;   // (empty: k_spec publishes)
             CK(cudaEventElapsedTime(&t, e[0], e[4])); acc[4] += t;   // total
         }
         for (uint32_t i = 0; i < n_out && i < 5; ++i) ms_out[i] = (float)(acc[i] / ns);
@@ -601,8 +630,7 @@ extern "C" int jit_shard_prefix(jit_sched* h, int64_t now_ns, int64_t v_token_ns
     enqueue_score(h, s, now_ns, v_token_ns);
     // k_spec only reduces the scoring partials (n_pending, min key, ...): the round-1 export
     // needs the full radix resolve below
-    exact::spec(P, h->c, h->d_ctrl, S, 1, s);
-    if (P.n_single < P.n) exact::ckey_full(P, h->c, h->d_ctrl, S, h->nb_full, false, 1, s);
+    CK(exact::spec(P, h->c, h->d_ctrl, S, 1, s, false));
     exact::hist0(P, h->c, h->d_ctrl, S, h->grid_pass, 1, s);
     for (uint32_t i = 0; i < kLevels - 1; ++i) exact::pass(P, h->c, h->d_ctrl, S, h->grid_pass, i, s);
     exact::compact(P, h->c, h->d_ctrl, S, h->grid_pass, s);

@@ -1,5 +1,5 @@
 // exact.cu -- the speculative resolve (k_spec) and the exact path it launches from the device
-// (k_ckey_full, k_hist0, k_pass, k_compact, k_resolve, k_cand, k_group).  Compiled with -rdc
+// (k_hist0, k_pass, k_compact, k_resolve, k_cand, k_group).  Compiled with -rdc
 // (CUDA dynamic parallelism) and device-linked against cudadevrt; the hot scoring kernels live
 // in abi.cu, compiled whole-program.
 #define JIT_EXACT_TU 1
@@ -20,7 +20,7 @@ cudaError_t init_attributes() {
     if ((e = cudaFuncSetAttribute(k_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSpecSmem)) !=
         cudaSuccess) return e;
     // one shared-memory carveout for every kernel of the step (see abi.cu)
-    const void* ks[] = {(const void*)k_ckey_full<false>, (const void*)k_ckey_full<true>, (const void*)k_spec,
+    const void* ks[] = {(const void*)k_spec,
                         (const void*)k_hist0, (const void*)k_pass, (const void*)k_compact, (const void*)k_resolve,
                         (const void*)k_cand, (const void*)k_group};
     for (const void* k : ks)
@@ -29,13 +29,14 @@ cudaError_t init_attributes() {
     return cudaSuccess;
 }
 
-void spec(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int reduce_only, cudaStream_t s) {
-    k_spec<<<1, kSpecThreads, kSpecSmem, s>>>(P, c, ctrl, S, reduce_only);
-}
-void ckey_full(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t grid, bool debug, int force,
-               cudaStream_t s) {
-    if (debug) k_ckey_full<true><<<grid, kScoreThreads, 0, s>>>(P, c, ctrl, S, force);
-    else k_ckey_full<false><<<grid, kScoreThreads, 0, s>>>(P, c, ctrl, S, force);
+cudaError_t spec(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int reduce_only, cudaStream_t s, bool pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1); cfg.blockDim = dim3(kSpecThreads); cfg.dynamicSmemBytes = kSpecSmem; cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at; cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k_spec, P, c, ctrl, S, reduce_only);
 }
 void hist0(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t grid, int force, cudaStream_t s) {
     k_hist0<<<grid, kPassThreads, 0, s>>>(P, c, ctrl, S, force);

@@ -11,12 +11,11 @@ namespace exact {
 // function attributes (dynamic shared memory, carveout) of every exact.cu kernel
 cudaError_t init_attributes();
 
-// k_spec: reduce the scoring partials; reduce_only = 0: resolve from the speculative set and
-// run the window (or launch the exact path from the device)
-void spec(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int reduce_only, cudaStream_t s);
-// k_ckey_full: key the compound calls still carrying a frame tag (force = 0: only after a fallback)
-void ckey_full(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t grid, bool debug, int force,
-               cudaStream_t s);
+// k_spec: reduce the scoring partials; reduce_only = 0: resolve from the speculative set and run
+// the window, or mark the step for the host-driven exact path (status FALLBACK / window_done 0);
+// publishes the control block to pinned host memory.  pdl: programmatic dependent launch after
+// k_score (its launch overlaps k_score; it waits with griddepcontrol.wait)
+cudaError_t spec(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int reduce_only, cudaStream_t s, bool pdl);
 void hist0(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t grid, int force, cudaStream_t s);
 void pass(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t grid, uint32_t pass_idx, cudaStream_t s);
 void compact(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t grid, cudaStream_t s);

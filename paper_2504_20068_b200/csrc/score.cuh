@@ -1,15 +1,10 @@
 // score.cuh -- the streaming pass over the pool (a1)-(a6) and the speculative resolve.
 //
-//   k_score  every row, one row per thread per iteration over a persistent-style grid: the
-//            32-B hot state is read with warp-coalesced loads (the next iteration's row is
-//            loaded before the current one is scored), standalone rows get their key image
-//            (a5) and cost (a6); compound calls get their bound and cost and add (len_rem,
-//            call goodput) to their task's accumulators through a segmented warp reduction
-//            (tasks are contiguous row ranges), i.e. (a4) is row-parallel whatever the fan-out.
-//            Per-CTA partial counts go to an array (no global atomics on a shared line).
-//   k_ctask  every task: its aggregate goodput / t_gen (a4/a5), min / max call key; keys the
-//            calls of tasks that can reach the speculative set.
-//   k_ckey_full  keys the remaining compound calls (fallback body, debug, shard path).
+//   k_score  every row, 4 consecutive rows per thread with 128-bit SoA loads / stores; standalone
+//            rows get their key image (a5) and cost (a6); compound calls are scored by CTAs that
+//            own whole tasks, so the task aggregate (a4) and the calls' keys come out of the
+//            same pass (shared-memory sums, no global atomics).  Per-CTA partial counts go to
+//            an array (no global atomics on a shared line).
 //   k_spec   one CTA: exact B*, bp, thr, Cd from the speculative set.
 #pragma once
 #include "select.cuh"
@@ -58,293 +53,533 @@ __device__ __forceinline__ void store_part(BlockPart* part, uint32_t pend, uint3
     }
 }
 
-// compound call (a4, per row): bound, cost; returns pending
+// Per-row scoring of the pool pass, written branch-light (the length-bound refresh is the only
+// real branch; rows that are not pending compute and discard).  Group / table / flag ranges were
+// validated at load (k_validate) and the device never changes them.
+struct RowOut {
+    uint64_t img;
+    uint32_t cost, aux, Lh, len_rem;
+    bool err;
+};
+
+// standalone request, after (a1) admission and (a2) the bound refresh: (a3) t_rem, (a5) key,
+// (a6) cost, steps_waited+1.  Rows that are not pending compute and discard.
 template <bool kDebug>
-__device__ __forceinline__ bool score_call(const Cfg& c, const Table& T, const GroupFast* sg, uint32_t n_groups,
-                                           int64_t now, int64_t arr, uint32_t L_i, uint32_t g, uint32_t pre,
-                                           uint32_t lhat, uint32_t meta, uint32_t aux, uint32_t& o_lhat,
-                                           uint32_t& o_meta, bool& w_lh, uint64_t& len_rem, uint64_t& Gc,
-                                           uint32_t& cost, uint32_t& Lh_out, bool& err) {
-    w_lh = false; o_meta = meta; o_lhat = lhat; len_rem = 0; Gc = 0; cost = 0; Lh_out = 0;
-    if (arr > now || m_state(meta) > kPreempted) return false;      // no admission drop (A40)
-    const uint32_t gi = m_group(meta), drow = aux & 0xFFFFu;
-    if (gi >= n_groups || sg[gi].type != kCMP || !(m_flags(meta) & kCompound) || drow >= T.n_rows) {
-        err = true; return false;
-    }
-    const uint32_t ep = fastdiv(g, c.R, c.R_m, c.R_l);
-    if (lhat == 0 || ep >= 65536u || m_epoch(meta) != ep) {
-        lhat = cond_quantile(T, drow, ep * c.R, c.qn, c.qd);
-        o_lhat = lhat; w_lh = true;
-        if (ep < 65536u) o_meta = (meta & 0xFFFFu) | (ep << 16);
-    }
-    const uint32_t Lh = lhat > g + 1 ? lhat : g + 1;
-    len_rem = (uint64_t)(Lh - g);
-    Gc = (uint64_t)sg[gi].w_in_eff * L_i + (uint64_t)sg[gi].w_out_eff * Lh;
-    cost = token_cost(L_i, pre, c.chunk);
-    Lh_out = Lh;
-    return true;
+__device__ __forceinline__ void row_std(const Cfg& c, const GroupFast* sg, const uint32_t* ovr, uint32_t row,
+                                        bool pend, int64_t now, int64_t v, double v_d, double eps_d, int64_t arr,
+                                        uint32_t L_i, uint32_t g, uint32_t pre, uint32_t lhat, uint32_t meta,
+                                        uint32_t aux, RowOut& o, double& d_rate, int64_t& d_trem) {
+    const uint32_t Lh = max(lhat, g + 1);
+    const uint32_t len_rem = Lh - g;
+    const GroupFast G = sg[m_group(meta)];
+    const int64_t trem = arr + G.base + (int64_t)(Lh - 1) * G.tok - now;             // (a3), A9
+    uint64_t Gk = (uint64_t)G.w_in_eff * L_i + (uint64_t)G.w_out_eff * Lh;          // (a5) A10/A11
+    if (m_flags(meta) & kOverride) Gk = __ldg(ovr + row);
+    if (trem <= 0) Gk = 0;                                                          // A22
+    if (c.appb && (uint64_t)len_rem * (uint64_t)v > (uint64_t)(trem > 0 ? trem : 0)) Gk = 0;
+    const uint64_t Gp = Gk + (uint64_t)c.delta * fastdiv(aux >> 16, c.frame, c.F_m, c.F_l);
+    double key;
+    const bool ok = make_key_lv(Gp, len_rem, v_d, eps_d, &key);
+    o.err = pend && !ok;
+    o.img = (pend && ok) ? (uint64_t)__double_as_longlong(key) : kNone;
+    o.cost = pend ? token_cost(L_i, pre, c.chunk) : 0u;
+    o.aux = (pend && (aux >> 16) < 0xFFFFu) ? aux + (1u << 16) : aux;   // steps_waited+1; undone if selected
+    o.Lh = Lh; o.len_rem = len_rem;
+    if (kDebug) { d_rate = pend ? make_rate(len_rem, trem) : 0.0; d_trem = pend ? trem : 0; }
+}
+
+// 64-bit shared-memory sum of a value < 2^32 with 32-bit atomics (a 64-bit shared atomicAdd is a
+// CAS loop on sm_100): add to the low word, carry into the high word on wrap-around
+__device__ __forceinline__ void smem_add64(unsigned long long* p, uint32_t x) {
+    uint32_t* w = reinterpret_cast<uint32_t*>(p);
+    const uint32_t old = atomicAdd(w, x);
+    if (old + x < old) atomicAdd(w + 1, 1u);
 }
 
 __device__ __forceinline__ bool is_frames_tag(uint64_t img) {
     return (img & 0xFFF8000000000000ull) == kFramesTag;
 }
 
-// k_score / k_ctask: the hot pass, compiled into abi.cu (whole-program mode: -rdc costs the
-// scoring loop ~50 registers); k_ckey_full / k_spec: the separately linked exact.cu
+// k_score: the hot pass, compiled into abi.cu (whole-program mode: -rdc costs the scoring loop
+// registers).  Persistent CTAs walk work items of at most kTile rows; the next item's hot state
+// streams into shared memory through bulk asynchronous copies (TMA 1D, mbarrier completion)
+// while the current one is scored, 4 consecutive rows per thread (128-bit shared loads, 128-bit
+// global stores of key image, cost and steps_waited).
+//   * standalone items: tile i = rows [kTile i, kTile i + kTile) of [0, n_single) -- (a1)-(a3),
+//     (a5), (a6) per row;
+//   * compound items: one CRange of whole tasks each (a4): phase A scores the calls and sums
+//     (len_rem, call goodput) per task in shared memory, phase B turns the sums into the task's
+//     goodput and t_gen (one thread per task), phase C keys every pending call
+//     (G_task + delta * frames) * 1e9 / (t_gen + eps) from registers -- no global atomics, no
+//     second kernel.  A range wider than one tile (a single task > kTile calls) is read from
+//     global memory and parks the frame count in the key slot between A and C.
+// Every row whose key image reaches the speculative threshold joins the speculative set; per-CTA
+// partial counts go to S.part[blockIdx.x] (no global atomics on a shared line).
+// --------------------------------------------------------------------------------------
 #ifndef JIT_EXACT_TU
-// 4 CTAs of 256 per SM: caps k_score at 64 registers without spills (uncapped it takes ~104,
-// i.e. 2 CTAs per SM -- too few warps for a latency-bound streaming pass)
 #ifndef JIT_SCORE_MINB
-#define JIT_SCORE_MINB 4
+#define JIT_SCORE_MINB 2
 #endif
+struct Acc {
+    uint32_t pend, drop, err, ref;
+    uint64_t mn;
+    uint32_t cost;                 // per thread: <= (rows per thread) x chunk, far below 2^32
+};
+
+__device__ __forceinline__ uint4 ld_v4(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
+__device__ __forceinline__ void st_v4(uint32_t* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    *reinterpret_cast<uint4*>(p) = make_uint4(a, b, c, d);
+}
+__device__ __forceinline__ void st_img4(uint64_t* p, const uint64_t* v) {
+    reinterpret_cast<ulonglong2*>(p)[0] = make_ulonglong2(v[0], v[1]);
+    reinterpret_cast<ulonglong2*>(p)[1] = make_ulonglong2(v[2], v[3]);
+}
+
+// the 32-B hot state of rows q0..q0+3 (q0 % 4 == 0; the SoA capacity is padded to 64 rows)
+struct Quad {
+    int64_t ar[4];
+    uint32_t li[4], ge[4], pr[4], lh[4], me[4], ax[4];
+};
+__device__ __forceinline__ void load_quad(const Pool& P, uint32_t q0, Quad& Q) {
+    const longlong2 a0 = *reinterpret_cast<const longlong2*>(P.arr + q0);
+    const longlong2 a1 = *reinterpret_cast<const longlong2*>(P.arr + q0 + 2);
+    const uint4 l = ld_v4(P.len_in + q0), g = ld_v4(P.gen + q0), p = ld_v4(P.pre + q0);
+    const uint4 h = ld_v4(P.lhat + q0), m = ld_v4(P.meta + q0), x = ld_v4(P.aux + q0);
+    Q.ar[0] = a0.x; Q.ar[1] = a0.y; Q.ar[2] = a1.x; Q.ar[3] = a1.y;
+    Q.li[0] = l.x; Q.li[1] = l.y; Q.li[2] = l.z; Q.li[3] = l.w;
+    Q.ge[0] = g.x; Q.ge[1] = g.y; Q.ge[2] = g.z; Q.ge[3] = g.w;
+    Q.pr[0] = p.x; Q.pr[1] = p.y; Q.pr[2] = p.z; Q.pr[3] = p.w;
+    Q.lh[0] = h.x; Q.lh[1] = h.y; Q.lh[2] = h.z; Q.lh[3] = h.w;
+    Q.me[0] = m.x; Q.me[1] = m.y; Q.me[2] = m.z; Q.me[3] = m.w;
+    Q.ax[0] = x.x; Q.ax[1] = x.y; Q.ax[2] = x.z; Q.ax[3] = x.w;
+}
+
+// One staged tile: kTile rows starting at an aligned quad, one array per SoA field, filled by
+// bulk asynchronous copies (cp.async.bulk, the 1D TMA path) that complete on an mbarrier.
+struct TileBuf {
+    int64_t ar[kTile];
+    uint32_t li[kTile], ge[kTile], pr[kTile], lh[kTile], me[kTile], ax[kTile], tk[kTile];
+};
+__device__ __forceinline__ void load_quad_smem(const TileBuf* B, uint32_t o, Quad& Q, uint32_t* tk) {
+    const longlong2 a0 = *reinterpret_cast<const longlong2*>(B->ar + o);
+    const longlong2 a1 = *reinterpret_cast<const longlong2*>(B->ar + o + 2);
+    const uint4 l = ld_v4(B->li + o), g = ld_v4(B->ge + o), p = ld_v4(B->pr + o);
+    const uint4 h = ld_v4(B->lh + o), m = ld_v4(B->me + o), x = ld_v4(B->ax + o);
+    Q.ar[0] = a0.x; Q.ar[1] = a0.y; Q.ar[2] = a1.x; Q.ar[3] = a1.y;
+    Q.li[0] = l.x; Q.li[1] = l.y; Q.li[2] = l.z; Q.li[3] = l.w;
+    Q.ge[0] = g.x; Q.ge[1] = g.y; Q.ge[2] = g.z; Q.ge[3] = g.w;
+    Q.pr[0] = p.x; Q.pr[1] = p.y; Q.pr[2] = p.z; Q.pr[3] = p.w;
+    Q.lh[0] = h.x; Q.lh[1] = h.y; Q.lh[2] = h.z; Q.lh[3] = h.w;
+    Q.me[0] = m.x; Q.me[1] = m.y; Q.me[2] = m.z; Q.me[3] = m.w;
+    Q.ax[0] = x.x; Q.ax[1] = x.y; Q.ax[2] = x.z; Q.ax[3] = x.w;
+    if (tk) { const uint4 t = ld_v4(B->tk + o); tk[0] = t.x; tk[1] = t.y; tk[2] = t.z; tk[3] = t.w; }
+}
+
+// --- mbarrier + bulk copy (PTX; sm_90+) ---
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile("{\n\t.reg .pred p;\n"
+                 "WAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)), "r"(parity) : "memory");
+}
+
+// standalone rows q0..q0+3 (those < n_single)
 template <bool kDebug>
-__global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P, Table T, const Group* groups, uint32_t n_groups,
-                                                         Cfg c, Ctrl* ctrl, Scratch S, int64_t now, int64_t v) {
+__device__ __forceinline__ void std_quad(const Pool& P, const Table& T, const GroupFast* s_g, const Cfg& c,
+                                         const Scratch& S, int64_t now, int64_t v, uint64_t t_guess, uint32_t q0,
+                                         uint32_t ns, const TileBuf* B, uint32_t o, uint64_t* empty, Acc& A) {
+    const bool any = q0 < ns, full = q0 + 3 < ns;
+    const double v_d = (double)v, eps_d = (double)c.eps;
+    Quad Q;
+    if (any) load_quad_smem(B, o, Q, nullptr);
+    else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { Q.ar[k] = 0; Q.li[k] = Q.ge[k] = Q.pr[k] = Q.lh[k] = Q.me[k] = Q.ax[k] = 0; }
+    }
+    mbar_arrive(empty);                                    // this thread is done with the tile buffer
+    // (a1) admission and pending, (a2) which cached bounds are stale
+    uint32_t pendm = 0, dropm = 0, needm = 0, ep[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t st = m_state(Q.me[k]), fl = m_flags(Q.me[k]);
+        const bool arrived = q0 + k < ns && Q.ar[k] <= now;
+        const bool drop = arrived && st == kQueued && !(fl & (kEver | kCompound)) && now - Q.ar[k] > c.waiting;
+        const bool pend = arrived && !drop && st <= kPreempted;
+        ep[k] = fastdiv(Q.ge[k], c.R, c.R_m, c.R_l);
+        const bool need = pend && (Q.lh[k] == 0 || ep[k] >= 65536u || m_epoch(Q.me[k]) != ep[k]);
+        pendm |= (uint32_t)pend << k; dropm |= (uint32_t)drop << k; needm |= (uint32_t)need << k;
+    }
+    if (__any_sync(0xffffffffu, needm != 0)) {            // rare in steady state: refresh off the main path
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (needm & (1u << k)) {
+                Q.lh[k] = cond_quantile(T, Q.ax[k] & 0xFFFFu, ep[k] * c.R, c.qn, c.qd);
+                P.lhat[q0 + k] = Q.lh[k];
+                if (ep[k] < 65536u) P.meta[q0 + k] = (Q.me[k] & 0xFFFFu) | (ep[k] << 16);
+            }
+        }
+        A.ref += __popc(needm);
+    }
+    if (dropm) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) if (dropm & (1u << k)) P.meta[q0 + k] = m_with_state(Q.me[k], kDropped);
+        A.drop += __popc(dropm);
+    }
+    uint64_t img[4];
+    uint32_t cost[4], aux[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t r = q0 + k;
+        RowOut ro;
+        double d_rate = 0.0;
+        int64_t d_trem = 0;
+        const bool pend = (pendm >> k) & 1u;
+        row_std<kDebug>(c, s_g, P.ovr, r, pend, now, v, v_d, eps_d, Q.ar[k], Q.li[k], Q.ge[k], Q.pr[k], Q.lh[k],
+                        Q.me[k], Q.ax[k], ro, d_rate, d_trem);
+        img[k] = ro.img; cost[k] = ro.cost; aux[k] = ro.aux;
+        A.err |= ro.err;
+        A.pend += ro.img != kNone; A.cost += ro.cost;
+        A.mn = ro.img < A.mn ? ro.img : A.mn;
+        if (kDebug && r < ns) { P.dbg_rate[r] = d_rate; P.dbg_trem[r] = d_trem; P.dbg_lhat[r] = pend ? ro.Lh : 0; }
+    }
+    if (full) {
+        st_img4(P.img + q0, img);
+        st_v4(P.cost + q0, cost[0], cost[1], cost[2], cost[3]);
+        st_v4(P.aux + q0, aux[0], aux[1], aux[2], aux[3]);
+    } else if (any) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (q0 + k < ns) { P.img[q0 + k] = img[k]; P.cost[q0 + k] = cost[k]; P.aux[q0 + k] = aux[k]; }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        spec_add(S, P.id, img[k] != kNone, img[k], q0 + k, cost[k], c.len_key ? Q.li[k] + Q.ge[k] : Q.li[k], t_guess);
+}
+
+// phase B of a compound range: the task's goodput and t_gen (a4)
+__device__ __forceinline__ void task_totals(const Pool& P, const Cfg& c, int64_t now, int64_t v, uint32_t t,
+                                            uint64_t Tsum, uint64_t Gsum, uint64_t& Gt, uint64_t& t_gen,
+                                            int64_t& trem, uint32_t& err) {
+    const int64_t a_c = __ldg(P.t_arr + t), D = __ldg(P.t_dl + t);
+    const uint32_t s = __ldg(P.cur_stage + t), Sn = __ldg(P.n_stages + t);
+    const uint4 p0 = __ldg(reinterpret_cast<const uint4*>(P.pattern) + 2 * t);
+    const uint4 p1 = __ldg(reinterpret_cast<const uint4*>(P.pattern) + 2 * t + 1);
+    const uint32_t pt[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+    // phi(s) = t_<=s / t_total, D_s = floor(D * phi); in ms the ratio is identical
+    // and D*le fits u64 when D < 2^40 ns and t_total < 2^24 ms
+    uint64_t le = 0, tot = 0;
+#pragma unroll
+    for (uint32_t u = 0; u < kMaxStages; ++u) {
+        const uint64_t ms = u < Sn ? pt[u] : 0u;
+        tot += ms; if (u <= s) le += ms;
+    }
+    if (tot == 0 || Sn == 0 || Sn > kMaxStages || s >= Sn) err = 1;
+    const int64_t Ds = !tot ? 0
+        : ((uint64_t)D < (1ull << 40) && tot < (1ull << 24)) ? (int64_t)((uint64_t)D * le / tot)
+                                                             : (int64_t)((u128)(uint64_t)D * le / tot);
+    trem = a_c + Ds - now;                                  // advisory stage deadline
+    Gt = __ldg(P.gdone + t) + Gsum;
+    if (a_c + D <= now) Gt = 0;                             // final deadline passed (A43)
+    t_gen = Tsum * (uint64_t)v;
+    if (c.appb && t_gen > (uint64_t)(trem > 0 ? trem : 0)) Gt = 0;
+}
+
+// phase C key of one call: (G_task + delta * frames) * 1e9 / (t_gen + eps); B_d < 0 marks a task
+// whose t_gen + eps left the exact range
+__device__ __forceinline__ uint64_t call_key(uint64_t Gt, uint32_t fr, const Cfg& c, double B_d, uint32_t& err) {
+    const uint64_t Gp = Gt + (uint64_t)c.delta * fr;
+    if (Gp >= kTwo53 / 1000000000ull || B_d < 0.0) { err = 1; return kNone; }
+    return (uint64_t)__double_as_longlong(div_rn_int(__dmul_rn(__uint2double_rn((uint32_t)Gp), 1e9), B_d));
+}
+
+// one compound range (see above); every thread of the CTA calls it.  kStaged: the range is one
+// tile already staged in B (rows from rg.r0 & ~3); else it is read from global memory.
+template <bool kDebug, bool kStaged>
+__device__ __forceinline__ void cmp_range(const Pool& P, const Table& T, const GroupFast* s_g, const Cfg& c,
+                                          const Scratch& S, int64_t now, int64_t v, uint64_t t_guess,
+                                          const CRange rg, unsigned long long* s_T, unsigned long long* s_G,
+                                          long long* s_R, double* s_rate, const TileBuf* B, uint64_t* empty, Acc& A) {
+    const uint32_t tid = threadIdx.x;
+    const uint32_t ntl = rg.t1 - rg.t0;
+    __syncthreads();                                       // the previous range's phase C is done with s_T / s_G
+    for (uint32_t i = tid; i < ntl; i += kScoreThreads) { s_T[i] = 0; s_G[i] = 0; }
+    __syncthreads();
+    const uint32_t qbase = rg.r0 & ~3u;
+    const bool single = kStaged || rg.r1 - qbase <= kTile;
+    uint32_t kf[4] = {0u, 0u, 0u, 0u};      // pending: 0x80000000 | floor(steps_waited / Delta)
+    uint32_t kt[4] = {0u, 0u, 0u, 0u}, kc[4] = {0u, 0u, 0u, 0u}, kl[4] = {0u, 0u, 0u, 0u};
+    // ---- phase A: per call (a2, a6) + the task sums
+    for (uint32_t base = qbase; base < rg.r1; base += kTile) {     // one iteration when staged
+        const uint32_t q0 = base + 4 * tid;
+        const bool any = q0 < rg.r1, full = q0 >= rg.r0 && q0 + 3 < rg.r1;
+        Quad Q;
+        uint32_t tk[4] = {kNoTask, kNoTask, kNoTask, kNoTask};
+        if (any && kStaged) {
+            load_quad_smem(B, q0 - qbase, Q, tk);
+        } else if (any) {
+            load_quad(P, q0, Q);
+            const uint4 t4 = ld_v4(P.task + q0);
+            tk[0] = t4.x; tk[1] = t4.y; tk[2] = t4.z; tk[3] = t4.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) { Q.ar[k] = 0; Q.li[k] = Q.ge[k] = Q.pr[k] = Q.lh[k] = Q.me[k] = Q.ax[k] = 0; }
+        }
+        // pending calls (no admission drop, A40) and stale cached bounds
+        uint32_t inm = 0, pendm = 0, needm = 0, ep[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t r = q0 + k;
+            const bool in = any && r >= rg.r0 && r < rg.r1;
+            const bool pend = in && Q.ar[k] <= now && m_state(Q.me[k]) <= kPreempted && tk[k] - rg.t0 < ntl;
+            ep[k] = fastdiv(Q.ge[k], c.R, c.R_m, c.R_l);
+            const bool need = pend && (Q.lh[k] == 0 || ep[k] >= 65536u || m_epoch(Q.me[k]) != ep[k]);
+            inm |= (uint32_t)in << k; pendm |= (uint32_t)pend << k; needm |= (uint32_t)need << k;
+            if (in && tk[k] - rg.t0 >= ntl) A.err = 1;          // a call outside its range (validated at load)
+        }
+        if (__any_sync(0xffffffffu, needm != 0)) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (needm & (1u << k)) {
+                    Q.lh[k] = cond_quantile(T, Q.ax[k] & 0xFFFFu, ep[k] * c.R, c.qn, c.qd);
+                    P.lhat[q0 + k] = Q.lh[k];
+                    if (ep[k] < 65536u) P.meta[q0 + k] = (Q.me[k] & 0xFFFFu) | (ep[k] << 16);
+                }
+            }
+            A.ref += __popc(needm);
+        }
+        uint32_t cost[4], aux[4];
+        uint64_t img[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const bool pend = (pendm >> k) & 1u;
+            const uint32_t Lh = max(Q.lh[k], Q.ge[k] + 1);
+            const GroupFast G = s_g[m_group(Q.me[k])];
+            const uint64_t Gc = (uint64_t)G.w_in_eff * Q.li[k] + (uint64_t)G.w_out_eff * Lh;   // call goodput
+            const uint32_t lt = tk[k] - rg.t0;
+            cost[k] = pend ? token_cost(Q.li[k], Q.pr[k], c.chunk) : 0u;
+            aux[k] = (pend && (Q.ax[k] >> 16) < 0xFFFFu) ? Q.ax[k] + (1u << 16) : Q.ax[k];
+            img[k] = kNone; kf[k] = 0;
+            if (kDebug && ((inm >> k) & 1u)) P.dbg_lhat[q0 + k] = pend ? Lh : 0;
+            if (pend) {
+                if (Gc >> 32) A.err = 1;                          // goodput out of the exact range
+                const uint32_t fr = fastdiv(Q.ax[k] >> 16, c.frame, c.F_m, c.F_l);   // pre-increment value
+                smem_add64(&s_T[lt], Lh - Q.ge[k]);
+                smem_add64(&s_G[lt], (uint32_t)Gc);
+                kf[k] = 0x80000000u | fr; kt[k] = lt; kc[k] = cost[k];
+                kl[k] = c.len_key ? Q.li[k] + Q.ge[k] : Q.li[k];
+                img[k] = kFramesTag | fr;
+                A.pend += 1; A.cost += cost[k];
+            }
+        }
+        if (full) {
+            st_v4(P.cost + q0, cost[0], cost[1], cost[2], cost[3]);
+            st_v4(P.aux + q0, aux[0], aux[1], aux[2], aux[3]);
+            if (!single) st_img4(P.img + q0, img);
+        } else if (any) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t r = q0 + k;
+                if (r >= rg.r0 && r < rg.r1) { P.cost[r] = cost[k]; P.aux[r] = aux[k]; if (!single) P.img[r] = img[k]; }
+            }
+        }
+    }
+    if (kStaged) mbar_arrive(empty);                       // this thread is done with the tile buffer
+    __syncthreads();
+    // ---- phase B: per task of the range (a4); s_G <- G_task, s_T <- fp64 (t_gen + eps)
+    for (uint32_t i = tid; i < ntl; i += kScoreThreads) {
+        const uint64_t Tsum = s_T[i];
+        if (!Tsum) continue;
+        uint64_t Gt, t_gen;
+        int64_t trem;
+        task_totals(P, c, now, v, rg.t0 + i, Tsum, s_G[i], Gt, t_gen, trem, A.err);
+        const uint64_t B = t_gen + (uint64_t)c.eps;
+        const bool okB = B < kTwo53 && B >= t_gen && t_gen / (uint64_t)v == Tsum;
+        s_G[i] = Gt;
+        s_T[i] = (unsigned long long)__double_as_longlong(okB ? __ull2double_rn(B) : -1.0);
+        if (kDebug) { s_R[i] = trem; s_rate[i] = make_rate(Tsum, trem); }
+    }
+    __syncthreads();
+    // ---- phase C: the key of every pending call (a5 over the task aggregate)
+    if (single) {
+        const uint32_t q0 = qbase + 4 * tid;
+        const bool any = q0 < rg.r1, full = q0 >= rg.r0 && q0 + 3 < rg.r1;
+        uint64_t img[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            img[k] = kNone;
+            if (kf[k]) {
+                img[k] = call_key(s_G[kt[k]], kf[k] & 0xFFFFu, c, __longlong_as_double((long long)s_T[kt[k]]), A.err);
+                A.mn = img[k] < A.mn ? img[k] : A.mn;
+            }
+        }
+        if (full) st_img4(P.img + q0, img);
+        else if (any) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) if (q0 + k >= rg.r0 && q0 + k < rg.r1) P.img[q0 + k] = img[k];
+        }
+        if (kDebug) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t r = q0 + k;
+                if (any && r >= rg.r0 && r < rg.r1) {
+                    P.dbg_rate[r] = kf[k] ? s_rate[kt[k]] : 0.0;
+                    P.dbg_trem[r] = kf[k] ? s_R[kt[k]] : 0;
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) spec_add(S, P.id, img[k] != kNone, img[k], q0 + k, kc[k], kl[k], t_guess);
+    } else if (!kStaged) {
+        for (uint32_t base = qbase; base < rg.r1; base += kTile) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t r = base + 4 * tid + k;
+                uint64_t img = kNone;
+                uint32_t cst = 0, len = 0;
+                if (r >= rg.r0 && r < rg.r1) {
+                    img = P.img[r];
+                    const uint32_t t = P.task[r] - rg.t0;
+                    if (is_frames_tag(img) && t < ntl) {
+                        img = call_key(s_G[t], (uint32_t)(img & 0xFFFFu), c, __longlong_as_double((long long)s_T[t]), A.err);
+                        A.mn = img < A.mn ? img : A.mn;
+                        cst = P.cost[r];
+                        len = c.len_key ? P.len_in[r] + P.gen[r] : P.len_in[r];
+                    }
+                    P.img[r] = img;
+                    if (kDebug && t < ntl) {
+                        const bool pd = img != kNone;
+                        P.dbg_rate[r] = pd ? s_rate[t] : 0.0;
+                        P.dbg_trem[r] = pd ? s_R[t] : 0;
+                    }
+                }
+                spec_add(S, P.id, img != kNone, img, r, cst, len, t_guess);
+            }
+        }
+    }
+}
+
+// the rows of work item `it`: standalone tile it (< n_std) or compound range it - n_std
+__device__ __forceinline__ CRange item_rows(const Pool& P, const Scratch& S, uint32_t it) {
+    if (it < S.n_std) {
+        const uint32_t r0 = it * kTile;
+        return CRange{r0, min(r0 + kTile, P.n_single), 0u, 0u};
+    }
+    return S.crange[it - S.n_std];
+}
+__device__ __forceinline__ bool stageable(const CRange& rg) { return rg.r1 - (rg.r0 & ~3u) <= kTile; }
+
+// thread 0: bulk-copy the hot state of an item into a tile buffer (completes on bar)
+__device__ __forceinline__ void stage_item(const Pool& P, const CRange& rg, bool compound, TileBuf* B, uint64_t* bar) {
+    const uint32_t q0 = rg.r0 & ~3u;
+    const uint32_t nr = (rg.r1 - q0 + 3) & ~3u;          // whole quads; <= kTile; the SoA is padded
+    const uint32_t bytes = nr * (8u + 24u + (compound ? 4u : 0u));
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(B->ar, P.arr + q0, 8 * nr, bar);
+    bulk_g2s(B->li, P.len_in + q0, 4 * nr, bar);
+    bulk_g2s(B->ge, P.gen + q0, 4 * nr, bar);
+    bulk_g2s(B->pr, P.pre + q0, 4 * nr, bar);
+    bulk_g2s(B->lh, P.lhat + q0, 4 * nr, bar);
+    bulk_g2s(B->me, P.meta + q0, 4 * nr, bar);
+    bulk_g2s(B->ax, P.aux + q0, 4 * nr, bar);
+    if (compound) bulk_g2s(B->tk, P.task + q0, 4 * nr, bar);
+}
+
+// dynamic shared memory of k_score: two tile buffers + the task sums (+ debug per-task outputs)
+__host__ __device__ constexpr uint32_t score_smem_bytes(bool debug) {
+    return 2u * (uint32_t)sizeof(TileBuf) + 16u * kTile + (debug ? 16u * kTile : 0u);
+}
+
+// Persistent: CTA b walks the work items b, b + grid, ...; while it scores one item the next one
+// is already streaming into the other tile buffer (double buffering: HBM reads overlap compute).
+template <bool kDebug>
+__global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P, Table T, const Group* groups,
+                                                                         uint32_t n_groups, Cfg c, Ctrl* ctrl,
+                                                                         Scratch S, int64_t now, int64_t v) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    TileBuf* buf = reinterpret_cast<TileBuf*>(smem);
+    unsigned long long* s_T = reinterpret_cast<unsigned long long*>(smem + 2 * sizeof(TileBuf));
+    unsigned long long* s_G = s_T + kTile;
+    long long* s_R = reinterpret_cast<long long*>(s_G + kTile);          // kDebug only
+    double* s_rate = reinterpret_cast<double*>(s_R + kTile);              // kDebug only
     __shared__ GroupFast s_g[256];
-    for (uint32_t gi = threadIdx.x; gi < n_groups; gi += blockDim.x) s_g[gi] = make_fast(groups[gi]);
+    __shared__ __align__(8) uint64_t s_full[2], s_empty[2];
+    const uint32_t tid = threadIdx.x;
+    const uint32_t n_items = S.n_std + S.n_crange;
+    uint32_t uses = 0;                                     // thread 0: fills of buffer b in bits 16b..16b+15
+    if (tid == 0) {
+        mbar_init(&s_full[0], 1); mbar_init(&s_full[1], 1);
+        mbar_init(&s_empty[0], kScoreThreads); mbar_init(&s_empty[1], kScoreThreads);
+        mbar_init_fence();
+        if (blockIdx.x < n_items) {
+            const CRange rg = item_rows(P, S, blockIdx.x);
+            if (stageable(rg)) { stage_item(P, rg, blockIdx.x >= S.n_std, &buf[0], &s_full[0]); uses = 1; }
+        }
+    }
+    for (uint32_t gi = tid; gi < n_groups; gi += kScoreThreads) s_g[gi] = make_fast(groups[gi]);
     // first kernel of the step: a fresh control block (nothing else touches ctrl during this
     // kernel) and cleared fallback histograms, spread over the CTAs
     if (blockIdx.x == 0) reset_ctrl_block(ctrl, now, v);
-    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < 4096; b += gridDim.x * blockDim.x) {
+    for (uint32_t b = blockIdx.x * kScoreThreads + tid; b < 4096; b += gridDim.x * kScoreThreads) {
         S.hcnt[b] = 0; S.hcost[b] = 0;
     }
     __syncthreads();
     const uint64_t t_guess = S.persist->t_guess;
-    const int lane = threadIdx.x & 31;
-    const bool any_compound = P.n_single < P.n;
-    uint32_t my_pend = 0, my_drop = 0, my_err = 0, my_ref = 0;
-    uint64_t my_min = kNone, my_cost = 0;
-    const uint32_t n = P.n, ns = P.n_single;
-    const uint32_t stride = gridDim.x * blockDim.x;
-    uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t a_arr = 0;
-    uint32_t a_li = 0, a_g = 0, a_pr = 0, a_lh = 0, a_me = 0, a_ax = 0, a_tk = kNoTask;
-    if (r < n) {
-        a_arr = __ldcs(P.arr + r); a_li = __ldcs(P.len_in + r); a_g = __ldcs(P.gen + r); a_pr = __ldcs(P.pre + r);
-        a_lh = __ldcs(P.lhat + r); a_me = __ldcs(P.meta + r); a_ax = __ldcs(P.aux + r);
-        if (r >= ns) a_tk = __ldg(P.task + r);
-    }
-#pragma unroll 1
-    for (uint32_t wr = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); wr < n; wr += stride, r += stride) {
-        const bool act = r < n;
-        const uint32_t rn = r + stride;
-        int64_t b_arr = 0;
-        uint32_t b_li = 0, b_g = 0, b_pr = 0, b_lh = 0, b_me = 0, b_ax = 0, b_tk = kNoTask;
-        if (rn < n) {                                    // prefetch the next iteration's row
-            b_arr = __ldcs(P.arr + rn); b_li = __ldcs(P.len_in + rn); b_g = __ldcs(P.gen + rn);
-            b_pr = __ldcs(P.pre + rn); b_lh = __ldcs(P.lhat + rn); b_me = __ldcs(P.meta + rn);
-            b_ax = __ldcs(P.aux + rn);
-            if (rn >= ns) b_tk = __ldg(P.task + rn);
-        }
-        uint64_t img = kNone;
-        bool valid = false;
-        uint64_t vT = 0, vG = 0;                       // compound contributions
-        uint32_t fr = 0, sp_cost = 0;
-        uint32_t key_task = kNoTask;
-        if (act && r < ns) {
-            RowRes o;
-            score_standalone<kDebug>(c, T, s_g, n_groups, P.ovr, r, now, v, a_arr, a_li, a_g, a_pr, a_lh, a_me, a_ax, o);
-            P.img[r] = o.img; P.cost[r] = o.cost;
-            sp_cost = o.cost;
-            if (o.aux != a_ax) P.aux[r] = o.aux;
-            if (o.w_meta) P.meta[r] = o.meta;
-            if (o.w_lhat) P.lhat[r] = o.lhat;
-            if (kDebug) {
-                P.dbg_rate[r] = o.pending ? o.rate : 0.0;
-                P.dbg_trem[r] = o.pending ? o.trem : 0;
-                P.dbg_lhat[r] = o.pending ? o.lhatc : 0;
-            }
-            img = o.img;
-            valid = img != kNone;
-            my_drop += o.dropped; my_err |= o.err; my_ref += o.w_lhat;
-            if (valid) { my_pend += 1; my_cost += o.cost; if (img < my_min) my_min = img; }
-        } else if (act) {
-            uint32_t o_lhat, o_meta, cost, Lh;
-            bool w_lh, err = false;
-            uint64_t len_rem, Gc;
-            const bool pend = score_call<kDebug>(c, T, s_g, n_groups, now, a_arr, a_li, a_g, a_pr, a_lh, a_me, a_ax,
-                                                 o_lhat, o_meta, w_lh, len_rem, Gc, cost, Lh, err);
-            P.cost[r] = cost;                          // > 0 marks a pending call
-            if (w_lh) { P.lhat[r] = o_lhat; if (o_meta != a_me) P.meta[r] = o_meta; }
-            if (kDebug) P.dbg_lhat[r] = pend ? Lh : 0;
-            my_err |= err; my_ref += w_lh;
-            if (pend) {
-                // the key needs the task's sums: park floor(waited/Delta) (pre-increment value)
-                // in the key slot and do steps_waited+1 here (the task pass never touches aux)
-                fr = fastdiv(a_ax >> 16, c.frame, c.F_m, c.F_l);
-                P.img[r] = kFramesTag | fr;
-                if ((a_ax >> 16) < 0xFFFFu) P.aux[r] = a_ax + (1u << 16);
-                my_pend += 1; my_cost += cost; vT = len_rem; vG = Gc;
-            } else {
-                P.img[r] = kNone;
-            }
-            key_task = (a_tk < P.n_tasks) ? a_tk : kNoTask;
-            if (a_tk >= P.n_tasks) my_err = 1;
-        }
-        // segmented warp reduction per task (rows of a task are contiguous) of the sums of
-        // (len_rem, goodput) and the min / max starvation frames; warps that hold no compound
-        // call skip it (warp-uniform)
-        if (any_compound && __any_sync(0xffffffffu, key_task != kNoTask)) {
-            uint64_t sT = vT, sG = vG;
-            uint32_t fx = vT ? fr : 0u, fn = vT ? fr : 0xFFFFFFFFu;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint64_t uT = __shfl_up_sync(0xffffffffu, sT, d);
-                const uint64_t uG = __shfl_up_sync(0xffffffffu, sG, d);
-                const uint32_t ux = __shfl_up_sync(0xffffffffu, fx, d);
-                const uint32_t un = __shfl_up_sync(0xffffffffu, fn, d);
-                const uint32_t uk = __shfl_up_sync(0xffffffffu, key_task, d);
-                if (lane >= d && uk == key_task) { sT += uT; sG += uG; fx = max(fx, ux); fn = min(fn, un); }
-            }
-            const uint32_t nk = __shfl_down_sync(0xffffffffu, key_task, 1);
-            if (key_task != kNoTask && (lane == 31 || nk != key_task) && sT) {
-                atomicAdd(&S.tacc[key_task].T, (unsigned long long)sT);
-                atomicAdd(&S.tacc[key_task].G, (unsigned long long)sG);
-                atomicMax(&S.tacc[key_task].fmax, fx);
-                atomicMin(&S.tacc[key_task].fmin, fn);
+    pdl_launch_dependents();                               // k_spec may launch now (it waits for us)
+    Acc A{0u, 0u, 0u, 0u, kNone, 0u};
+    uint32_t par = 0, b = 0;                               // consumer parity bit per buffer
+    for (uint32_t it = blockIdx.x; it < n_items; it += gridDim.x, b ^= 1u) {
+        const uint32_t nx = it + gridDim.x;
+        if (tid == 0 && nx < n_items) {
+            const CRange rn = item_rows(P, S, nx);
+            if (stageable(rn)) {
+                const uint32_t bn = b ^ 1u, u = (uses >> (16 * bn)) & 0xFFFFu;
+                if (u) mbar_wait(&s_empty[bn], (u - 1) & 1u);   // every thread released its last fill
+                stage_item(P, rn, nx >= S.n_std, &buf[bn], &s_full[bn]);
+                uses += 1u << (16 * bn);
             }
         }
-        spec_add(S, P.id, valid, img, r, sp_cost, c.len_key ? a_li + a_g : a_li, t_guess);
-        a_arr = b_arr; a_li = b_li; a_g = b_g; a_pr = b_pr; a_lh = b_lh; a_me = b_me; a_ax = b_ax; a_tk = b_tk;
-    }
-    store_part(S.part, my_pend, my_drop, my_err, my_min, my_cost, my_ref);
-}
-
-// --------------------------------------------------------------------------------------
-// k_ctask: one thread per task (a4/a5).  G_task = goodput_done + sum of the current stage's
-// pending call goodput (zero once a_c + D has passed, A43), t_gen = (sum len_rem) * v_token;
-// the key of call i is (G_task + delta*floor(waited_i/Delta)) * 1e9 / (t_gen + eps).  The key
-// is non-decreasing in the frame count, so the task's extreme keys come from its min / max
-// frames (k_score): kmin feeds the pool minimum exactly, and only a task whose kmax reaches
-// the speculative threshold ("hot") has its calls keyed here -- by one warp, lanes over the
-// calls, so the speculative-set ballot stays convergent.  Every other call keeps its tagged
-// frame count until k_ckey_full (fallback body / debug / shard path) keys it.
-// --------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kScoreThreads) k_ctask(Pool P, Cfg c, Ctrl* ctrl, Scratch S) {
-    const int64_t now = ctrl->now, v = ctrl->v;
-    const uint64_t t_guess = S.persist->t_guess;
-    const int lane = threadIdx.x & 31;
-    uint32_t my_err = 0;
-    uint64_t my_min = kNone;
-    const uint32_t nt = P.n_tasks;
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t wt = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); wt < nt; wt += stride) {
-        const uint32_t t = wt + lane;
-        bool hot = false;
-        uint64_t Gt = 0, t_gen = 0;
-        if (t < nt) {
-            const TaskAcc acc = S.tacc[t];
-            if (acc.T) {
-                const int64_t a_c = __ldg(P.t_arr + t), D = __ldg(P.t_dl + t);
-                const uint32_t s = __ldg(P.cur_stage + t), Sn = __ldg(P.n_stages + t);
-                const uint4 p0 = __ldg(reinterpret_cast<const uint4*>(P.pattern) + 2 * t);
-                const uint4 p1 = __ldg(reinterpret_cast<const uint4*>(P.pattern) + 2 * t + 1);
-                const uint32_t pt[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-                // phi(s) = t_<=s / t_total, D_s = floor(D * phi); in ms the ratio is
-                // identical and D*le fits u64 when D < 2^40 ns and t_total < 2^24 ms
-                uint64_t le = 0, tot = 0;
-#pragma unroll
-                for (uint32_t u = 0; u < kMaxStages; ++u) {
-                    const uint64_t ms = u < Sn ? pt[u] : 0u;
-                    tot += ms; if (u <= s) le += ms;
-                }
-                if (tot == 0 || Sn == 0 || Sn > kMaxStages || s >= Sn) my_err = 1;
-                const int64_t Ds = !tot ? 0
-                    : ((uint64_t)D < (1ull << 40) && tot < (1ull << 24)) ? (int64_t)((uint64_t)D * le / tot)
-                                                                         : (int64_t)((u128)(uint64_t)D * le / tot);
-                const int64_t trem = a_c + Ds - now;               // advisory stage deadline
-                Gt = __ldg(P.gdone + t) + acc.G;
-                if (a_c + D <= now) Gt = 0;                         // final deadline passed
-                t_gen = acc.T * (uint64_t)v;
-                if (c.appb && t_gen > (uint64_t)(trem > 0 ? trem : 0)) Gt = 0;
-                double kmin, kmax;
-                const bool ok_min = make_key(Gt + (uint64_t)c.delta * acc.fmin, t_gen, c.eps, &kmin);
-                const bool ok_max = make_key(Gt + (uint64_t)c.delta * acc.fmax, t_gen, c.eps, &kmax);
-                if (!ok_min || !ok_max) my_err = 1;
-                const uint64_t imin = (uint64_t)__double_as_longlong(kmin);
-                const uint64_t imax = (uint64_t)__double_as_longlong(kmax);
-                if (imin < my_min) my_min = imin;
-                hot = ok_max && imax >= t_guess;
-                TaskAcc o;                                          // consumed: re-zero the sums
-                o.T = 0; o.G = 0; o.Gt = Gt; o.tgen = t_gen; o.trem = trem; o.Tr = acc.T;
-                o.fmax = 0; o.fmin = 0xFFFFFFFFu;
-                S.tacc[t] = o;
-            }
-        }
-        // hot tasks: the warp keys their calls together (speculative-set ballot convergent)
-        unsigned hm = __ballot_sync(0xffffffffu, hot);
-        while (hm) {
-            const int src = __ffs(hm) - 1;
-            hm &= hm - 1;
-            const uint32_t ht = __shfl_sync(0xffffffffu, t, src);
-            const uint64_t hG = __shfl_sync(0xffffffffu, Gt, src);
-            const uint64_t hB = __shfl_sync(0xffffffffu, t_gen, src);
-            const uint32_t r0 = __ldg(P.call_off + ht), r1 = __ldg(P.call_off + ht + 1);
-            for (uint32_t wr = r0; wr < r1; wr += 32) {
-                const uint32_t r = wr + lane;
-                uint64_t img = kNone;
-                bool valid = false;
-                uint32_t cost = 0, len = 0;
-                if (r < r1) {
-                    img = P.img[r];
-                    if (is_frames_tag(img)) {
-                        const uint32_t fr = (uint32_t)(img & 0xFFFFFFFFu);
-                        double key;
-                        make_key(hG + (uint64_t)c.delta * fr, hB, c.eps, &key);
-                        img = (uint64_t)__double_as_longlong(key);
-                        P.img[r] = img;
-                        valid = true;
-                        cost = P.cost[r];
-                        len = c.len_key ? P.len_in[r] + P.gen[r] : P.len_in[r];
-                    }
-                }
-                spec_add(S, P.id, valid, img, r, cost, len, t_guess);
-            }
+        const CRange rg = item_rows(P, S, it);
+        if (it < S.n_std) {
+            mbar_wait(&s_full[b], (par >> b) & 1u); par ^= 1u << b;
+            std_quad<kDebug>(P, T, s_g, c, S, now, v, t_guess, rg.r0 + 4 * tid, rg.r1, &buf[b], 4 * tid, &s_empty[b], A);
+        } else if (stageable(rg)) {
+            mbar_wait(&s_full[b], (par >> b) & 1u); par ^= 1u << b;
+            cmp_range<kDebug, true>(P, T, s_g, c, S, now, v, t_guess, rg, s_T, s_G, s_R, s_rate, &buf[b], &s_empty[b], A);
+        } else {
+            cmp_range<kDebug, false>(P, T, s_g, c, S, now, v, t_guess, rg, s_T, s_G, s_R, s_rate, nullptr, nullptr, A);
         }
     }
-    store_part(S.part2, 0, 0, my_err, my_min, 0, 0);
+    store_part(S.part, A.pend, A.drop, A.err, A.mn, A.cost, A.ref);
 }
 #endif  // !JIT_EXACT_TU
 
-#ifdef JIT_EXACT_TU
-// k_ckey_full: row-parallel keying of every call still carrying its frame tag (after
-// k_ctask); in debug mode also the per-call rate / t_rem outputs of every compound row.
-template <bool kDebug>
-__global__ void __launch_bounds__(kScoreThreads) k_ckey_full(Pool P, Cfg c, Ctrl* ctrl, Scratch S, int force) {
-    if (!kDebug && blockIdx.x == 0 && threadIdx.x == 0 && ctrl->chain) {   // exact path: next k_hist0
-        atomicOr(&ctrl->trace, 2u);
-        k_hist0<<<S.grid_pass, kPassThreads, 0, cudaStreamTailLaunch>>>(P, c, ctrl, S, 0);
-        const cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) { ctrl->error |= 2u; ctrl->status = ST_ERROR; ctrl->launch_err = e; }
-    }
-    if (!force && ctrl->status != ST_FALLBACK) return;
-    const uint32_t n = P.n;
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t r = P.n_single + blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride) {
-        const uint64_t img = P.img[r];
-        const bool tagged = is_frames_tag(img);
-        if (!tagged && !kDebug) continue;
-        const uint32_t t = __ldg(P.task + r);
-        if (t >= P.n_tasks) continue;
-        if (tagged) {
-            double key;
-            make_key(S.tacc[t].Gt + (uint64_t)c.delta * (uint32_t)(img & 0xFFFFFFFFu), S.tacc[t].tgen, c.eps, &key);
-            P.img[r] = (uint64_t)__double_as_longlong(key);
-        }
-        if (kDebug) {
-            if (P.cost[r]) { P.dbg_rate[r] = make_rate(S.tacc[t].Tr, S.tacc[t].trem); P.dbg_trem[r] = S.tacc[t].trem; }
-            else { P.dbg_rate[r] = 0.0; P.dbg_trem[r] = 0; }
-        }
-    }
-}
 
+#ifdef JIT_EXACT_TU
 // --------------------------------------------------------------------------------------
 // k_spec: one CTA of 512 threads.  Reduces the scoring partials, then resolves (a7)/(a8)
 // exactly from the speculative set S = {key >= t} and runs the window (a9) on Cd, all in
 // shared memory.  S is upward closed in the (key desc, id asc) order, i.e. a PREFIX of the
 // priority order, so the budget walk restricted to S is the exact walk as long as it stops
 // inside S (or S holds every pending row); Cd = {key >= thr} lies in S when thr >= t.
-// Otherwise the exact radix path runs (launch_exact_path).
+// Otherwise the host runs the exact radix path after the step (finish_step in abi.cu).
 //   1. one pass over S: key images / costs to smem + a cost-weighted histogram of the key
 //      image (2048 bins of 2^-9 relative width above t, the top bin open-ended);
 //   2. one block scan over the bins (count and cost packed in one u64) finds the boundary bin,
@@ -385,34 +620,25 @@ __device__ __forceinline__ uint32_t spec_bin(uint64_t img, uint64_t t_img) {
 }
 constexpr uint64_t kPackCount = 1ull << 48;   // histogram word: count << 48 | cost (cost sum < 2^48)
 
-// The exact path, launched from the device only when needed (CUDA dynamic parallelism): a
-// chain of tail launches, each kernel launching its successor (select.cuh) -- a tail launch
-// runs once its launching grid has finished, and the step (graph node or stream work)
-// completes only after the whole chain.  radix = false: just the window over a large Cd.
-// Called by one thread; false if the launch failed.
-__device__ __noinline__ bool launch_exact_path(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, bool radix) {
-    ctrl->chain = 1;
-    if (!radix)
-        k_group<<<1, 1024, 12 * kGroupSmemSort, cudaStreamTailLaunch>>>(P, c, ctrl, S);
-    else if (P.n_single < P.n)                 // key the compound calls still tagged, then k_hist0
-        k_ckey_full<false><<<S.nb_full, kScoreThreads, 0, cudaStreamTailLaunch>>>(P, c, ctrl, S, 1);
-    else
-        k_hist0<<<S.grid_pass, kPassThreads, 0, cudaStreamTailLaunch>>>(P, c, ctrl, S, 0);
-    const cudaError_t e = cudaGetLastError();
-    ctrl->trace |= 1u;
-    ctrl->launch_err = e;
-    return e == cudaSuccess;
-}
-
-// thread 0: give up on the speculative resolve -> exact path (sets *fb: 1 launched, 3 failed)
-__device__ __forceinline__ void spec_fallback(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int* fb) {
+// thread 0: give up on the speculative resolve -> the host runs the exact radix path after the
+// step (finish_step in abi.cu); rare: first step after a load, a threshold far off, huge ties
+__device__ __forceinline__ void spec_fallback(Ctrl* ctrl, int* fb) {
     ctrl->status = ST_FALLBACK; ctrl->fallback = 1;
-    *fb = launch_exact_path(P, c, ctrl, S, true) ? 1 : 3;
-    if (*fb == 3) { ctrl->status = ST_ERROR; ctrl->error |= 2u; }
+    *fb = 1;
 }
 
+static __device__ void spec_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int reduce_only,
+                                 unsigned char* smem);
+// the step's last kernel: resolve, then publish the control block to pinned host memory
 __global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl, Scratch S, int reduce_only) {
     extern __shared__ __align__(16) unsigned char smem[];
+    pdl_wait();
+    spec_body(P, c, ctrl, S, reduce_only, smem);
+    publish_ctrl(ctrl, S.h_ctrl);
+}
+
+static __device__ void spec_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int reduce_only,
+                                 unsigned char* smem) {
     uint64_t* s_img = reinterpret_cast<uint64_t*>(smem + kSpImgOff);
     uint32_t* s_cost = reinterpret_cast<uint32_t*>(smem + kSpCostOff);
     unsigned long long* s_hist = reinterpret_cast<unsigned long long*>(smem + kSpHistOff);
@@ -442,11 +668,11 @@ __global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl
     for (uint32_t b = tid; b < kSpecBins; b += kSpecThreads) s_hist[b] = 0;
     __syncthreads();
     const uint32_t n = s_n < kSpecCap ? s_n : kSpecCap;
-    {   // partials of k_score and k_ctask, and (1) the set -> smem + histogram, in one pass
+    {   // partials of k_score, and (1) the set -> smem + histogram, in one pass
         uint32_t pend = 0, drop = 0, err = 0, ref = 0;
         uint64_t mn = kNone, cost = 0;
-        for (uint32_t i = tid; i < S.n_part + S.n_part2; i += kSpecThreads) {
-            const BlockPart b = i < S.n_part ? S.part[i] : S.part2[i - S.n_part];
+        for (uint32_t i = tid; i < S.n_part; i += kSpecThreads) {
+            const BlockPart b = S.part[i];
             pend += b.n_pending; drop += b.n_dropped; err |= b.err; cost += b.tot_cost; ref += b.refresh;
             if (b.min_img < mn) mn = b.min_img;
         }
@@ -478,10 +704,10 @@ __global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl
     if (tid == 0) {
         if (s_err) { ctrl->status = ST_ERROR; s_fb = 2; }
         else if (np == 0) { ctrl->status = ST_EMPTY; s_fb = 2; }
-        else if (s_n > kSpecCap || s_n == 0) spec_fallback(P, c, ctrl, S, &s_fb);
+        else if (s_n > kSpecCap || s_n == 0) spec_fallback(ctrl, &s_fb);
     }
     __syncthreads();
-    if (s_fb) return;                                      // k_publish (next node) reports it
+    if (s_fb) return;                                      // published as is (k_spec)
     // (2) boundary bin: thread t owns bins [2047 - 4t - 3, 2047 - 4t], scanned from the top
     {
         uint64_t h[4], loc = 0;
@@ -510,7 +736,7 @@ __global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl
     if (first == kSpecBins) {
         // every entry of S fits the budget: exact only if S is the whole pending set
         if (tid == 0) {
-            if (!whole) spec_fallback(P, c, ctrl, S, &s_fb);
+            if (!whole) spec_fallback(ctrl, &s_fb);
             else {
                 s_fits = n;
                 const double bp = __longlong_as_double((long long)s_min);
@@ -540,7 +766,7 @@ __global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl
         __syncthreads();
         const uint32_t m = s_nsel;
         if (m > kSelCap) {                                 // a huge tie bin: exact path
-            if (tid == 0) spec_fallback(P, c, ctrl, S, &s_fb);
+            if (tid == 0) spec_fallback(ctrl, &s_fb);
             __syncthreads();
             return;
         }
@@ -598,7 +824,7 @@ __global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl
                     const double bp = __longlong_as_double((long long)bimg);
                     const double thr = __dmul_rn(__ddiv_rn((double)c.pn, (double)c.pd), bp);
                     const uint64_t ti = (uint64_t)__double_as_longlong(thr);
-                    if (!whole && ti < t_img) spec_fallback(P, c, ctrl, S, &s_fb);
+                    if (!whole && ti < t_img) spec_fallback(ctrl, &s_fb);
                     else { ctrl->b_star = fits; ctrl->bp = bp; ctrl->thr = thr; ctrl->thr_img = s_thr_img = ti; }
                 }
             }
@@ -631,12 +857,7 @@ __global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl
         for (uint32_t i = tid; i < n; i += kSpecThreads)
             if (s_img[i] >= thr_img) S.cand[atomicAdd(&s_nsel, 1u)] = S.spec_row[i];
         __syncthreads();
-        if (tid == 0) {
-            __threadfence();
-            s_fb = launch_exact_path(P, c, ctrl, S, false) ? 1 : 3;
-            if (s_fb == 3) { ctrl->status = ST_ERROR; ctrl->error |= 2u; }
-        }
-        return;
+        return;                                            // window_done = 0: the host runs k_group
     }
     stamp(ctrl, 4);
     // (a9) sort Cd by (len, id) (keys unique): s_ord[rank] = slot.  Rank sort when small,

@@ -19,10 +19,10 @@
 namespace jit {
 
 constexpr uint32_t kBucketCap = 4096;
-constexpr uint32_t kSpecCap = 8192;
-constexpr uint32_t kMaxParts = 4096;          // max CTAs of the scoring kernels (partials)           // speculative set resolved in shared memory up to this size
+constexpr uint32_t kSpecCap = 8192;            // speculative set resolved in shared memory up to this size
 constexpr uint32_t kGroupSmemSort = 8192;     // |Cd| sorted in shared memory up to this size
 constexpr uint32_t kScoreThreads = 256;
+constexpr uint32_t kTile = 4 * kScoreThreads;    // rows per k_score CTA tile (4 per thread)
 constexpr uint32_t kPassThreads = 512;
 
 enum : uint32_t { ST_RUN = 0, ST_HIST = 1, ST_COMPACT = 2, ST_RESOLVED = 3, ST_EMPTY = 4, ST_ERROR = 5, ST_FALLBACK = 6 };
@@ -75,18 +75,13 @@ struct BlockPart {
     uint32_t n_pending, n_dropped, err, refresh;
 };
 
-// per-task accumulators of the compound pass (a4): sum of len_rem and of the call goodput
-// T, G, fmax, fmin are accumulated by k_score and consumed + re-zeroed by k_ctask (so the next
-// step starts from zero without a clearing pass); Gt, tgen, trem, Tr stay for the keying passes
-struct TaskAcc {
-    unsigned long long T, G;          // sums over the stage's pending calls (k_score)
-    unsigned long long Gt, tgen;      // task goodput and t_gen (k_ctask)
-    long long trem;                   // stage t_rem (k_ctask)
-    unsigned long long Tr;            // T of this step (k_ctask; debug rate output)
-    uint32_t fmax, fmin;              // max / min starvation frames of its pending calls (k_score)
+// compound CTA range of k_score: whole tasks [t0, t1) = call rows [r0, r1), packed greedily at
+// load so that r1 - (r0 & ~3) <= kTile unless one task alone is larger (then several tiles)
+struct CRange {
+    uint32_t r0, r1, t0, t1;
 };
-// key-image placeholder of a pending compound call between k_score and its key pass:
-// a NaN pattern carrying floor(steps_waited / Delta) (real key images are < 0x7FF0...)
+// key-image placeholder of a pending compound call between the two phases of a multi-tile
+// compound range: a NaN pattern carrying floor(steps_waited / Delta) (real key images are < 0x7FF0...)
 constexpr uint64_t kFramesTag = 0x7FF8000000000000ull;
 
 // %globaltimer (ns) stamp of a phase boundary, taken by thread 0 of a single-CTA kernel
@@ -117,11 +112,10 @@ struct Scratch {
     uint64_t* spec_img;
     uint32_t *spec_id, *spec_row, *spec_cost, *spec_len;
     Persist* persist;
-    BlockPart* part;         // k_score partials (grid_score entries)
-    BlockPart* part2;        // k_ctask partials (grid_ctask entries)
-    TaskAcc* tacc;           // task_capacity (see TaskAcc)
-    uint32_t n_part, n_part2, task_cap, pad3;
-    unsigned int* spec_cnt;  // size of the speculative set (k_score / k_ctask atomics; reset by k_spec)
+    BlockPart* part;         // k_score partials (one per CTA: n_part)
+    const CRange* crange;    // compound CTA ranges (n_crange)
+    uint32_t n_part, n_std, n_crange, pad3;   // partials = k_score CTAs; items = n_std tiles + ranges
+    unsigned int* spec_cnt;  // size of the speculative set (k_score atomics; reset by k_spec)
     Ctrl* h_ctrl;            // pinned host copy of the control block, written by the step's last kernel
     uint32_t nb_full, grid_pass;   // launch geometry of the fallback chain (device-side launches)
 };
@@ -265,12 +259,11 @@ __device__ __forceinline__ void reset_ctrl_block(Ctrl* ctrl, int64_t now, int64_
 
 #ifndef JIT_EXACT_TU
 // full reset (load / sharded step); the graph step needs none: k_score resets ctrl and the
-// histograms, k_ctask re-zeroes the task accumulators it consumed, k_spec the set counter
+// histograms, k_spec the set counter
 __global__ void k_begin(Ctrl* ctrl, uint32_t* hcnt, unsigned long long* hcost, int64_t now, int64_t v,
-                        TaskAcc* tacc, uint32_t n_tasks, unsigned int* spec_cnt) {
+                        unsigned int* spec_cnt) {
     const uint32_t tid = threadIdx.x + blockIdx.x * blockDim.x, nt = blockDim.x * gridDim.x;
     for (uint32_t b = tid; b < 4096; b += nt) { hcnt[b] = 0; hcost[b] = 0; }
-    for (uint32_t t = tid; t < n_tasks; t += nt) { tacc[t].T = 0; tacc[t].G = 0; tacc[t].fmax = 0; tacc[t].fmin = 0xFFFFFFFFu; }
     if (tid == 0) { reset_ctrl(ctrl, now, v); *spec_cnt = 0; }
 }
 #endif  // !JIT_EXACT_TU

@@ -233,6 +233,7 @@ __global__ void __launch_bounds__(1024) k_group_rec(Pool P, Cfg c, Ctrl* ctrl, S
         ctrl->n_selected = ns;
         ctrl->n_cand = n;
         ctrl->total_tokens = (uint32_t)(S.pc[bj + 1] - S.pc[bi]);
+        ctrl->window_done = 1;
     }
 }
 

@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libjitsched.so")
+# JITSCHED_LIB: an alternative in-tree build of the same library (tuning variants, profiles/)
+LIB_PATH = os.environ.get("JITSCHED_LIB") or os.path.join(_HERE, "libjitsched.so")
 
 JIT_OK, JIT_EMPTY = 0, 1
 JIT_CFG_DEBUG_ROWS = 1
