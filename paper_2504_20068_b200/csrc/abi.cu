@@ -101,6 +101,7 @@ static void carve(Carve& cv, const jit_config* cfg, const jit_len_table* tab, Po
     P.call_off = cv.take<uint32_t>(NT + 1); P.t_arr = cv.take<int64_t>(NT); P.t_dl = cv.take<int64_t>(NT);
     P.cur_stage = cv.take<uint32_t>(NT); P.n_stages = cv.take<uint32_t>(NT);
     P.pattern = cv.take<uint32_t>(NT * kMaxStages); P.gdone = cv.take<uint64_t>(NT);
+    P.tinfo = cv.take<TaskInfo>(NT);
     T.edges = cv.take<uint32_t>(tab->n_bins);
     T.cum = cv.take<uint32_t>((uint64_t)tab->n_rows * tab->n_bins);
     groups = cv.take<Group>(256);
@@ -265,6 +266,7 @@ extern "C" int jit_sched_load(jit_sched* h, const jit_pool* p) {
     k_begin<<<4, 1024, 0, h->stream>>>(h->d_ctrl, h->S.hcnt, h->S.hcost, 0, 1, h->S.spec_cnt);
     const uint32_t vb = (uint32_t)std::min<uint64_t>((n + 255) / 256 + 1, (uint64_t)h->n_sm * 8);
     k_validate<<<vb, 256, 0, h->stream>>>(P, h->d_groups, h->n_groups, h->T.n_rows, h->d_ctrl);
+    if (nt) k_task_prep<<<(uint32_t)std::min<uint64_t>((nt + 255) / 256, (uint64_t)h->n_sm * 8), 256, 0, h->stream>>>(P);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(h->h_ctrl, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));

@@ -103,8 +103,8 @@ __device__ __forceinline__ bool is_frames_tag(uint64_t img) {
 // k_score: the hot pass, compiled into abi.cu (whole-program mode: -rdc costs the scoring loop
 // registers).  Persistent CTAs walk work items of at most kTile rows; the next item's hot state
 // streams into shared memory through bulk asynchronous copies (TMA 1D, mbarrier completion)
-// while the current one is scored, 4 consecutive rows per thread (128-bit shared loads, 128-bit
-// global stores of key image, cost and steps_waited).
+// while the current one is scored, kRPT consecutive rows per thread (vector shared loads and
+// vector global stores of key image, cost and steps_waited).
 //   * standalone items: tile i = rows [kTile i, kTile i + kTile) of [0, n_single) -- (a1)-(a3),
 //     (a5), (a6) per row;
 //   * compound items: one CRange of whole tasks each (a4): phase A scores the calls and sums
@@ -118,7 +118,7 @@ __device__ __forceinline__ bool is_frames_tag(uint64_t img) {
 // --------------------------------------------------------------------------------------
 #ifndef JIT_EXACT_TU
 #ifndef JIT_SCORE_MINB
-#define JIT_SCORE_MINB 2
+#define JIT_SCORE_MINB 3
 #endif
 struct Acc {
     uint32_t pend, drop, err, ref;
@@ -126,53 +126,66 @@ struct Acc {
     uint32_t cost;                 // per thread: <= (rows per thread) x chunk, far below 2^32
 };
 
-__device__ __forceinline__ uint4 ld_v4(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
-__device__ __forceinline__ void st_v4(uint32_t* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-    *reinterpret_cast<uint4*>(p) = make_uint4(a, b, c, d);
+// kRPT consecutive rows per thread: vector loads / stores of kRPT fields (64- or 128-bit)
+__device__ __forceinline__ void ld_rows(const uint32_t* p, uint32_t* v) {
+    if constexpr (kRPT == 4) { const uint4 t = *reinterpret_cast<const uint4*>(p); v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w; }
+    else if constexpr (kRPT == 2) { const uint2 t = *reinterpret_cast<const uint2*>(p); v[0] = t.x; v[1] = t.y; }
+    else v[0] = *p;
 }
-__device__ __forceinline__ void st_img4(uint64_t* p, const uint64_t* v) {
-    reinterpret_cast<ulonglong2*>(p)[0] = make_ulonglong2(v[0], v[1]);
-    reinterpret_cast<ulonglong2*>(p)[1] = make_ulonglong2(v[2], v[3]);
+__device__ __forceinline__ void ld_rows64(const int64_t* p, int64_t* v) {
+    if constexpr (kRPT >= 2) {
+        const longlong2 a = *reinterpret_cast<const longlong2*>(p);
+        v[0] = a.x; v[1] = a.y;
+    } else {
+        v[0] = *p;
+    }
+    if constexpr (kRPT == 4) { const longlong2 b = *reinterpret_cast<const longlong2*>(p + 2); v[2] = b.x; v[3] = b.y; }
+}
+__device__ __forceinline__ void st_rows(uint32_t* p, const uint32_t* v) {
+    if constexpr (kRPT == 4) *reinterpret_cast<uint4*>(p) = make_uint4(v[0], v[1], v[2], v[3]);
+    else if constexpr (kRPT == 2) *reinterpret_cast<uint2*>(p) = make_uint2(v[0], v[1]);
+    else *p = v[0];
+}
+__device__ __forceinline__ void st_rows64(uint64_t* p, const uint64_t* v) {
+    if constexpr (kRPT >= 2) reinterpret_cast<ulonglong2*>(p)[0] = make_ulonglong2(v[0], v[1]);
+    else *p = v[0];
+    if constexpr (kRPT == 4) reinterpret_cast<ulonglong2*>(p)[1] = make_ulonglong2(v[2], v[3]);
 }
 
-// the 32-B hot state of rows q0..q0+3 (q0 % 4 == 0; the SoA capacity is padded to 64 rows)
+// the 32-B hot state of rows q0..q0+kRPT-1 (q0 % kRPT == 0; the SoA capacity is padded to 64 rows)
 struct Quad {
-    int64_t ar[4];
-    uint32_t li[4], ge[4], pr[4], lh[4], me[4], ax[4];
+    int64_t ar[kRPT];
+    uint32_t li[kRPT], ge[kRPT], pr[kRPT], lh[kRPT], me[kRPT], ax[kRPT];
 };
 __device__ __forceinline__ void load_quad(const Pool& P, uint32_t q0, Quad& Q) {
-    const longlong2 a0 = *reinterpret_cast<const longlong2*>(P.arr + q0);
-    const longlong2 a1 = *reinterpret_cast<const longlong2*>(P.arr + q0 + 2);
-    const uint4 l = ld_v4(P.len_in + q0), g = ld_v4(P.gen + q0), p = ld_v4(P.pre + q0);
-    const uint4 h = ld_v4(P.lhat + q0), m = ld_v4(P.meta + q0), x = ld_v4(P.aux + q0);
-    Q.ar[0] = a0.x; Q.ar[1] = a0.y; Q.ar[2] = a1.x; Q.ar[3] = a1.y;
-    Q.li[0] = l.x; Q.li[1] = l.y; Q.li[2] = l.z; Q.li[3] = l.w;
-    Q.ge[0] = g.x; Q.ge[1] = g.y; Q.ge[2] = g.z; Q.ge[3] = g.w;
-    Q.pr[0] = p.x; Q.pr[1] = p.y; Q.pr[2] = p.z; Q.pr[3] = p.w;
-    Q.lh[0] = h.x; Q.lh[1] = h.y; Q.lh[2] = h.z; Q.lh[3] = h.w;
-    Q.me[0] = m.x; Q.me[1] = m.y; Q.me[2] = m.z; Q.me[3] = m.w;
-    Q.ax[0] = x.x; Q.ax[1] = x.y; Q.ax[2] = x.z; Q.ax[3] = x.w;
+    ld_rows64(P.arr + q0, Q.ar);
+    ld_rows(P.len_in + q0, Q.li); ld_rows(P.gen + q0, Q.ge); ld_rows(P.pre + q0, Q.pr);
+    ld_rows(P.lhat + q0, Q.lh); ld_rows(P.meta + q0, Q.me); ld_rows(P.aux + q0, Q.ax);
+}
+__device__ __forceinline__ void zero_quad(Quad& Q) {
+#pragma unroll
+    for (int k = 0; k < (int)kRPT; ++k) { Q.ar[k] = 0; Q.li[k] = Q.ge[k] = Q.pr[k] = Q.lh[k] = Q.me[k] = Q.ax[k] = 0; }
 }
 
-// One staged tile: kTile rows starting at an aligned quad, one array per SoA field, filled by
-// bulk asynchronous copies (cp.async.bulk, the 1D TMA path) that complete on an mbarrier.
+// One staged tile: kTile rows starting at a 16-byte aligned row (r0 & ~3), one array per SoA
+// field, filled by bulk asynchronous copies (cp.async.bulk, the 1D TMA path) that complete on an
+// mbarrier; compound items also stage the constants of their first kTaskStage tasks.  A ring
+// of kStages such buffers per CTA keeps kStages - 1 items in flight while one is scored.
+#ifndef JIT_STAGES
+#define JIT_STAGES 2
+#endif
+constexpr uint32_t kStages = JIT_STAGES;
+constexpr uint32_t kTaskStage = 64;
 struct TileBuf {
     int64_t ar[kTile];
     uint32_t li[kTile], ge[kTile], pr[kTile], lh[kTile], me[kTile], ax[kTile], tk[kTile];
+    TaskInfo ti[kTaskStage];
 };
 __device__ __forceinline__ void load_quad_smem(const TileBuf* B, uint32_t o, Quad& Q, uint32_t* tk) {
-    const longlong2 a0 = *reinterpret_cast<const longlong2*>(B->ar + o);
-    const longlong2 a1 = *reinterpret_cast<const longlong2*>(B->ar + o + 2);
-    const uint4 l = ld_v4(B->li + o), g = ld_v4(B->ge + o), p = ld_v4(B->pr + o);
-    const uint4 h = ld_v4(B->lh + o), m = ld_v4(B->me + o), x = ld_v4(B->ax + o);
-    Q.ar[0] = a0.x; Q.ar[1] = a0.y; Q.ar[2] = a1.x; Q.ar[3] = a1.y;
-    Q.li[0] = l.x; Q.li[1] = l.y; Q.li[2] = l.z; Q.li[3] = l.w;
-    Q.ge[0] = g.x; Q.ge[1] = g.y; Q.ge[2] = g.z; Q.ge[3] = g.w;
-    Q.pr[0] = p.x; Q.pr[1] = p.y; Q.pr[2] = p.z; Q.pr[3] = p.w;
-    Q.lh[0] = h.x; Q.lh[1] = h.y; Q.lh[2] = h.z; Q.lh[3] = h.w;
-    Q.me[0] = m.x; Q.me[1] = m.y; Q.me[2] = m.z; Q.me[3] = m.w;
-    Q.ax[0] = x.x; Q.ax[1] = x.y; Q.ax[2] = x.z; Q.ax[3] = x.w;
-    if (tk) { const uint4 t = ld_v4(B->tk + o); tk[0] = t.x; tk[1] = t.y; tk[2] = t.z; tk[3] = t.w; }
+    ld_rows64(B->ar + o, Q.ar);
+    ld_rows(B->li + o, Q.li); ld_rows(B->ge + o, Q.ge); ld_rows(B->pr + o, Q.pr);
+    ld_rows(B->lh + o, Q.lh); ld_rows(B->me + o, Q.me); ld_rows(B->ax + o, Q.ax);
+    if (tk) ld_rows(B->tk + o, tk);
 }
 
 // --- mbarrier + bulk copy (PTX; sm_90+) ---
@@ -201,24 +214,33 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
                  "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)), "r"(parity) : "memory");
 }
 
-// standalone rows q0..q0+3 (those < n_single)
+// standalone rows q0..q0+kRPT-1 (those < n_single)
 template <bool kDebug>
 __device__ __forceinline__ void std_quad(const Pool& P, const Table& T, const GroupFast* s_g, const Cfg& c,
                                          const Scratch& S, int64_t now, int64_t v, uint64_t t_guess, uint32_t q0,
                                          uint32_t ns, const TileBuf* B, uint32_t o, uint64_t* empty, Acc& A) {
-    const bool any = q0 < ns, full = q0 + 3 < ns;
+    const bool any = q0 < ns, full = q0 + kRPT - 1 < ns;
     const double v_d = (double)v, eps_d = (double)c.eps;
     Quad Q;
     if (any) load_quad_smem(B, o, Q, nullptr);
-    else {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) { Q.ar[k] = 0; Q.li[k] = Q.ge[k] = Q.pr[k] = Q.lh[k] = Q.me[k] = Q.ax[k] = 0; }
-    }
+    else zero_quad(Q);
     mbar_arrive(empty);                                    // this thread is done with the tile buffer
-    // (a1) admission and pending (P:545), (a2) which cached bounds are stale (P:283)
-    uint32_t pendm = 0, dropm = 0, needm = 0, ep[4];
+#ifdef JIT_SCORE_FLOOR
+    {   // timing experiment only (profiles/variants.sh): the memory pipeline without the row math
+        uint64_t img[kRPT];
+        uint32_t cost[kRPT], aux[kRPT];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < (int)kRPT; ++k) {
+            img[k] = (uint64_t)Q.ar[k] ^ Q.li[k] ^ Q.ge[k]; cost[k] = Q.pr[k] ^ Q.lh[k]; aux[k] = Q.me[k] ^ Q.ax[k];
+        }
+        if (full) { st_rows64(P.img + q0, img); st_rows(P.cost + q0, cost); st_rows(P.aux + q0, aux); }
+        return;
+    }
+#endif
+    // (a1) admission and pending (P:545), (a2) which cached bounds are stale (P:283)
+    uint32_t pendm = 0, dropm = 0, needm = 0, ep[kRPT];
+#pragma unroll
+    for (int k = 0; k < (int)kRPT; ++k) {
         const uint32_t st = m_state(Q.me[k]), fl = m_flags(Q.me[k]);
         const bool arrived = q0 + k < ns && Q.ar[k] <= now;
         const bool drop = arrived && st == kQueued && !(fl & (kEver | kCompound)) && now - Q.ar[k] > c.waiting;
@@ -229,7 +251,7 @@ __device__ __forceinline__ void std_quad(const Pool& P, const Table& T, const Gr
     }
     if (__any_sync(0xffffffffu, needm != 0)) {            // rare in steady state: refresh off the main path
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < (int)kRPT; ++k) {
             if (needm & (1u << k)) {
                 Q.lh[k] = cond_quantile(T, Q.ax[k] & 0xFFFFu, ep[k] * c.R, c.qn, c.qd);
                 P.lhat[q0 + k] = Q.lh[k];
@@ -240,13 +262,13 @@ __device__ __forceinline__ void std_quad(const Pool& P, const Table& T, const Gr
     }
     if (dropm) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) if (dropm & (1u << k)) P.meta[q0 + k] = m_with_state(Q.me[k], kDropped);
+        for (int k = 0; k < (int)kRPT; ++k) if (dropm & (1u << k)) P.meta[q0 + k] = m_with_state(Q.me[k], kDropped);
         A.drop += __popc(dropm);
     }
-    uint64_t img[4];
-    uint32_t cost[4], aux[4];
+    uint64_t img[kRPT];
+    uint32_t cost[kRPT], aux[kRPT];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < (int)kRPT; ++k) {
         const uint32_t r = q0 + k;
         RowOut ro;
         double d_rate = 0.0;
@@ -261,45 +283,28 @@ __device__ __forceinline__ void std_quad(const Pool& P, const Table& T, const Gr
         if (kDebug && r < ns) { P.dbg_rate[r] = d_rate; P.dbg_trem[r] = d_trem; P.dbg_lhat[r] = pend ? ro.Lh : 0; }
     }
     if (full) {
-        st_img4(P.img + q0, img);
-        st_v4(P.cost + q0, cost[0], cost[1], cost[2], cost[3]);
-        st_v4(P.aux + q0, aux[0], aux[1], aux[2], aux[3]);
+        st_rows64(P.img + q0, img);
+        st_rows(P.cost + q0, cost);
+        st_rows(P.aux + q0, aux);
     } else if (any) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < (int)kRPT; ++k)
             if (q0 + k < ns) { P.img[q0 + k] = img[k]; P.cost[q0 + k] = cost[k]; P.aux[q0 + k] = aux[k]; }
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < (int)kRPT; ++k)
         spec_add(S, P.id, img[k] != kNone, img[k], q0 + k, cost[k], c.len_key ? Q.li[k] + Q.ge[k] : Q.li[k], t_guess);
 }
 
-// phase B of a compound range: the task's goodput and t_gen (a4)
-__device__ __forceinline__ void task_totals(const Pool& P, const Cfg& c, int64_t now, int64_t v, uint32_t t,
-                                            uint64_t Tsum, uint64_t Gsum, uint64_t& Gt, uint64_t& t_gen,
-                                            int64_t& trem, uint32_t& err) {
-    const int64_t a_c = __ldg(P.t_arr + t), D = __ldg(P.t_dl + t);
-    const uint32_t s = __ldg(P.cur_stage + t), Sn = __ldg(P.n_stages + t);
-    const uint4 p0 = __ldg(reinterpret_cast<const uint4*>(P.pattern) + 2 * t);
-    const uint4 p1 = __ldg(reinterpret_cast<const uint4*>(P.pattern) + 2 * t + 1);
-    const uint32_t pt[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-    // phi(s) = t_<=s / t_total, D_s = floor(D * phi); in ms the ratio is identical
-    // and D*le fits u64 when D < 2^40 ns and t_total < 2^24 ms
-    uint64_t le = 0, tot = 0;
-#pragma unroll
-    for (uint32_t u = 0; u < kMaxStages; ++u) {
-        const uint64_t ms = u < Sn ? pt[u] : 0u;
-        tot += ms; if (u <= s) le += ms;
-    }
-    if (tot == 0 || Sn == 0 || Sn > kMaxStages || s >= Sn) err = 1;
-    const int64_t Ds = !tot ? 0
-        : ((uint64_t)D < (1ull << 40) && tot < (1ull << 24)) ? (int64_t)((uint64_t)D * le / tot)
-                                                             : (int64_t)((u128)(uint64_t)D * le / tot);
-    trem = a_c + Ds - now;                                  // advisory stage deadline
-    Gt = __ldg(P.gdone + t) + Gsum;
-    if (a_c + D <= now) Gt = 0;                             // final deadline passed (A43)
+// phase B of a compound range: the task's goodput and t_gen (a4) from its load-time constants
+__device__ __forceinline__ void task_totals(const Cfg& c, int64_t now, int64_t v, const TaskInfo& ti, uint64_t Tsum,
+                                            uint64_t Gsum, uint64_t& Gt, uint64_t& t_gen, int64_t& trem,
+                                            uint32_t& err) {
+    trem = ti.dls - now;                                    // stage sub-deadline (advisory)
+    Gt = ti.dlf <= now ? 0 : ti.gdone + Gsum;               // final deadline passed (A43)
     t_gen = Tsum * (uint64_t)v;
     if (c.appb && t_gen > (uint64_t)(trem > 0 ? trem : 0)) Gt = 0;
+    err |= ti.err;
 }
 
 // phase C key of one call: (G_task + delta * frames) * 1e9 / (t_gen + eps); B_d < 0 marks a task
@@ -324,28 +329,27 @@ __device__ __forceinline__ void cmp_range(const Pool& P, const Table& T, const G
     __syncthreads();
     const uint32_t qbase = rg.r0 & ~3u;
     const bool single = kStaged || rg.r1 - qbase <= kTile;
-    uint32_t kf[4] = {0u, 0u, 0u, 0u};      // pending: 0x80000000 | floor(steps_waited / Delta)
-    uint32_t kt[4] = {0u, 0u, 0u, 0u}, kc[4] = {0u, 0u, 0u, 0u}, kl[4] = {0u, 0u, 0u, 0u};
+    uint32_t kf[kRPT] = {}, kt[kRPT] = {}, kc[kRPT] = {}, kl[kRPT] = {};   // kf: 0x80000000 | frames if pending
     // ---- phase A: per call (a2, a6) + the task sums
     for (uint32_t base = qbase; base < rg.r1; base += kTile) {     // one iteration when staged
-        const uint32_t q0 = base + 4 * tid;
-        const bool any = q0 < rg.r1, full = q0 >= rg.r0 && q0 + 3 < rg.r1;
+        const uint32_t q0 = base + kRPT * tid;
+        const bool any = q0 < rg.r1, full = q0 >= rg.r0 && q0 + kRPT - 1 < rg.r1;
         Quad Q;
-        uint32_t tk[4] = {kNoTask, kNoTask, kNoTask, kNoTask};
+        uint32_t tk[kRPT];
+#pragma unroll
+        for (int k = 0; k < (int)kRPT; ++k) tk[k] = kNoTask;
         if (any && kStaged) {
             load_quad_smem(B, q0 - qbase, Q, tk);
         } else if (any) {
             load_quad(P, q0, Q);
-            const uint4 t4 = ld_v4(P.task + q0);
-            tk[0] = t4.x; tk[1] = t4.y; tk[2] = t4.z; tk[3] = t4.w;
+            ld_rows(P.task + q0, tk);
         } else {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) { Q.ar[k] = 0; Q.li[k] = Q.ge[k] = Q.pr[k] = Q.lh[k] = Q.me[k] = Q.ax[k] = 0; }
+            zero_quad(Q);
         }
         // pending calls (no admission drop, A40) and stale cached bounds
-        uint32_t inm = 0, pendm = 0, needm = 0, ep[4];
+        uint32_t inm = 0, pendm = 0, needm = 0, ep[kRPT];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < (int)kRPT; ++k) {
             const uint32_t r = q0 + k;
             const bool in = any && r >= rg.r0 && r < rg.r1;
             const bool pend = in && Q.ar[k] <= now && m_state(Q.me[k]) <= kPreempted && tk[k] - rg.t0 < ntl;
@@ -356,7 +360,7 @@ __device__ __forceinline__ void cmp_range(const Pool& P, const Table& T, const G
         }
         if (__any_sync(0xffffffffu, needm != 0)) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < (int)kRPT; ++k) {
                 if (needm & (1u << k)) {
                     Q.lh[k] = cond_quantile(T, Q.ax[k] & 0xFFFFu, ep[k] * c.R, c.qn, c.qd);
                     P.lhat[q0 + k] = Q.lh[k];
@@ -365,10 +369,10 @@ __device__ __forceinline__ void cmp_range(const Pool& P, const Table& T, const G
             }
             A.ref += __popc(needm);
         }
-        uint32_t cost[4], aux[4];
-        uint64_t img[4];
+        uint32_t cost[kRPT], aux[kRPT];
+        uint64_t img[kRPT];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < (int)kRPT; ++k) {
             const bool pend = (pendm >> k) & 1u;
             const uint32_t Lh = max(Q.lh[k], Q.ge[k] + 1);
             const GroupFast G = s_g[m_group(Q.me[k])];
@@ -390,12 +394,12 @@ __device__ __forceinline__ void cmp_range(const Pool& P, const Table& T, const G
             }
         }
         if (full) {
-            st_v4(P.cost + q0, cost[0], cost[1], cost[2], cost[3]);
-            st_v4(P.aux + q0, aux[0], aux[1], aux[2], aux[3]);
-            if (!single) st_img4(P.img + q0, img);
+            st_rows(P.cost + q0, cost);
+            st_rows(P.aux + q0, aux);
+            if (!single) st_rows64(P.img + q0, img);
         } else if (any) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < (int)kRPT; ++k) {
                 const uint32_t r = q0 + k;
                 if (r >= rg.r0 && r < rg.r1) { P.cost[r] = cost[k]; P.aux[r] = aux[k]; if (!single) P.img[r] = img[k]; }
             }
@@ -409,7 +413,8 @@ __device__ __forceinline__ void cmp_range(const Pool& P, const Table& T, const G
         if (!Tsum) continue;
         uint64_t Gt, t_gen;
         int64_t trem;
-        task_totals(P, c, now, v, rg.t0 + i, Tsum, s_G[i], Gt, t_gen, trem, A.err);
+        const TaskInfo ti = (kStaged && i < kTaskStage) ? B->ti[i] : P.tinfo[rg.t0 + i];
+        task_totals(c, now, v, ti, Tsum, s_G[i], Gt, t_gen, trem, A.err);
         const uint64_t B = t_gen + (uint64_t)c.eps;
         const bool okB = B < kTwo53 && B >= t_gen && t_gen / (uint64_t)v == Tsum;
         s_G[i] = Gt;
@@ -419,25 +424,25 @@ __device__ __forceinline__ void cmp_range(const Pool& P, const Table& T, const G
     __syncthreads();
     // ---- phase C: the key of every pending call (a5 over the task aggregate)
     if (single) {
-        const uint32_t q0 = qbase + 4 * tid;
-        const bool any = q0 < rg.r1, full = q0 >= rg.r0 && q0 + 3 < rg.r1;
-        uint64_t img[4];
+        const uint32_t q0 = qbase + kRPT * tid;
+        const bool any = q0 < rg.r1, full = q0 >= rg.r0 && q0 + kRPT - 1 < rg.r1;
+        uint64_t img[kRPT];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < (int)kRPT; ++k) {
             img[k] = kNone;
             if (kf[k]) {
                 img[k] = call_key(s_G[kt[k]], kf[k] & 0xFFFFu, c, __longlong_as_double((long long)s_T[kt[k]]), A.err);
                 A.mn = img[k] < A.mn ? img[k] : A.mn;
             }
         }
-        if (full) st_img4(P.img + q0, img);
+        if (full) st_rows64(P.img + q0, img);
         else if (any) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) if (q0 + k >= rg.r0 && q0 + k < rg.r1) P.img[q0 + k] = img[k];
+            for (int k = 0; k < (int)kRPT; ++k) if (q0 + k >= rg.r0 && q0 + k < rg.r1) P.img[q0 + k] = img[k];
         }
         if (kDebug) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < (int)kRPT; ++k) {
                 const uint32_t r = q0 + k;
                 if (any && r >= rg.r0 && r < rg.r1) {
                     P.dbg_rate[r] = kf[k] ? s_rate[kt[k]] : 0.0;
@@ -446,12 +451,12 @@ __device__ __forceinline__ void cmp_range(const Pool& P, const Table& T, const G
             }
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) spec_add(S, P.id, img[k] != kNone, img[k], q0 + k, kc[k], kl[k], t_guess);
+        for (int k = 0; k < (int)kRPT; ++k) spec_add(S, P.id, img[k] != kNone, img[k], q0 + k, kc[k], kl[k], t_guess);
     } else if (!kStaged) {
         for (uint32_t base = qbase; base < rg.r1; base += kTile) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t r = base + 4 * tid + k;
+            for (int k = 0; k < (int)kRPT; ++k) {
+                const uint32_t r = base + kRPT * tid + k;
                 uint64_t img = kNone;
                 uint32_t cst = 0, len = 0;
                 if (r >= rg.r0 && r < rg.r1) {
@@ -490,7 +495,8 @@ __device__ __forceinline__ bool stageable(const CRange& rg) { return rg.r1 - (rg
 __device__ __forceinline__ void stage_item(const Pool& P, const CRange& rg, bool compound, TileBuf* B, uint64_t* bar) {
     const uint32_t q0 = rg.r0 & ~3u;
     const uint32_t nr = (rg.r1 - q0 + 3) & ~3u;          // whole quads; <= kTile; the SoA is padded
-    const uint32_t bytes = nr * (8u + 24u + (compound ? 4u : 0u));
+    const uint32_t bytes = nr * (8u + 24u + (compound ? 4u : 0u)) +
+                           (compound ? (uint32_t)sizeof(TaskInfo) * min(rg.t1 - rg.t0, kTaskStage) : 0u);
     mbar_expect_tx(bar, bytes);
     bulk_g2s(B->ar, P.arr + q0, 8 * nr, bar);
     bulk_g2s(B->li, P.len_in + q0, 4 * nr, bar);
@@ -499,70 +505,74 @@ __device__ __forceinline__ void stage_item(const Pool& P, const CRange& rg, bool
     bulk_g2s(B->lh, P.lhat + q0, 4 * nr, bar);
     bulk_g2s(B->me, P.meta + q0, 4 * nr, bar);
     bulk_g2s(B->ax, P.aux + q0, 4 * nr, bar);
-    if (compound) bulk_g2s(B->tk, P.task + q0, 4 * nr, bar);
+    if (compound) {
+        bulk_g2s(B->tk, P.task + q0, 4 * nr, bar);
+        const uint32_t nt = min(rg.t1 - rg.t0, kTaskStage);
+        if (nt) bulk_g2s(B->ti, P.tinfo + rg.t0, (uint32_t)sizeof(TaskInfo) * nt, bar);
+    }
 }
 
-// dynamic shared memory of k_score: two tile buffers + the task sums (+ debug per-task outputs)
+// dynamic shared memory of k_score: the tile ring + the task sums (+ debug per-task outputs)
 __host__ __device__ constexpr uint32_t score_smem_bytes(bool debug) {
-    return 2u * (uint32_t)sizeof(TileBuf) + 16u * kTile + (debug ? 16u * kTile : 0u);
+    return kStages * (uint32_t)sizeof(TileBuf) + 16u * kTile + (debug ? 16u * kTile : 0u);
 }
 
-// Persistent: CTA b walks the work items b, b + grid, ...; while it scores one item the next one
-// is already streaming into the other tile buffer (double buffering: HBM reads overlap compute).
+// Persistent: CTA b walks the work items b, b + grid, ...; item j of the CTA lives in ring slot
+// j % kStages, and thread 0 keeps the next kStages - 1 items streaming in (HBM reads of several
+// items overlap the scoring of one).  Per slot: `full` completes when the bulk copies land,
+// `empty` when every thread has read its rows out of the slot.
 template <bool kDebug>
 __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P, Table T, const Group* groups,
                                                                          uint32_t n_groups, Cfg c, Ctrl* ctrl,
                                                                          Scratch S, int64_t now, int64_t v) {
     extern __shared__ __align__(128) unsigned char smem[];
     TileBuf* buf = reinterpret_cast<TileBuf*>(smem);
-    unsigned long long* s_T = reinterpret_cast<unsigned long long*>(smem + 2 * sizeof(TileBuf));
+    unsigned long long* s_T = reinterpret_cast<unsigned long long*>(smem + kStages * sizeof(TileBuf));
     unsigned long long* s_G = s_T + kTile;
     long long* s_R = reinterpret_cast<long long*>(s_G + kTile);          // kDebug only
     double* s_rate = reinterpret_cast<double*>(s_R + kTile);              // kDebug only
     __shared__ GroupFast s_g[256];
-    __shared__ __align__(8) uint64_t s_full[2], s_empty[2];
+    __shared__ __align__(8) uint64_t s_full[kStages], s_empty[kStages];
     const uint32_t tid = threadIdx.x;
     const uint32_t n_items = S.n_std + S.n_crange;
-    uint32_t uses = 0;                                     // thread 0: fills of buffer b in bits 16b..16b+15
+    const uint32_t G = gridDim.x;
+    uint32_t fpar = 0, fused = 0;                          // thread 0, per slot: fill-count parity, ever filled
+    // thread 0: fill slot s with item it (after every thread released the slot's previous fill)
+    auto produce = [&](uint32_t it, uint32_t s) {
+        if (it >= n_items) return;
+        const CRange rn = item_rows(P, S, it);
+        if (!stageable(rn)) return;
+        if (fused & (1u << s)) mbar_wait(&s_empty[s], ((fpar >> s) & 1u) ^ 1u);
+        stage_item(P, rn, it >= S.n_std, &buf[s], &s_full[s]);
+        fpar ^= 1u << s; fused |= 1u << s;
+    };
     if (tid == 0) {
-        mbar_init(&s_full[0], 1); mbar_init(&s_full[1], 1);
-        mbar_init(&s_empty[0], kScoreThreads); mbar_init(&s_empty[1], kScoreThreads);
+        for (uint32_t s = 0; s < kStages; ++s) { mbar_init(&s_full[s], 1); mbar_init(&s_empty[s], kScoreThreads); }
         mbar_init_fence();
-        if (blockIdx.x < n_items) {
-            const CRange rg = item_rows(P, S, blockIdx.x);
-            if (stageable(rg)) { stage_item(P, rg, blockIdx.x >= S.n_std, &buf[0], &s_full[0]); uses = 1; }
-        }
+        for (uint32_t j = 0; j + 1 < kStages; ++j) produce(blockIdx.x + j * G, j);
     }
     for (uint32_t gi = tid; gi < n_groups; gi += kScoreThreads) s_g[gi] = make_fast(groups[gi]);
     // first kernel of the step: a fresh control block (nothing else touches ctrl during this
     // kernel) and cleared fallback histograms, spread over the CTAs
     if (blockIdx.x == 0) reset_ctrl_block(ctrl, now, v);
-    for (uint32_t b = blockIdx.x * kScoreThreads + tid; b < 4096; b += gridDim.x * kScoreThreads) {
+    for (uint32_t b = blockIdx.x * kScoreThreads + tid; b < 4096; b += G * kScoreThreads) {
         S.hcnt[b] = 0; S.hcost[b] = 0;
     }
     __syncthreads();
     const uint64_t t_guess = S.persist->t_guess;
     pdl_launch_dependents();                               // k_spec may launch now (it waits for us)
     Acc A{0u, 0u, 0u, 0u, kNone, 0u};
-    uint32_t par = 0, b = 0;                               // consumer parity bit per buffer
-    for (uint32_t it = blockIdx.x; it < n_items; it += gridDim.x, b ^= 1u) {
-        const uint32_t nx = it + gridDim.x;
-        if (tid == 0 && nx < n_items) {
-            const CRange rn = item_rows(P, S, nx);
-            if (stageable(rn)) {
-                const uint32_t bn = b ^ 1u, u = (uses >> (16 * bn)) & 0xFFFFu;
-                if (u) mbar_wait(&s_empty[bn], (u - 1) & 1u);   // every thread released its last fill
-                stage_item(P, rn, nx >= S.n_std, &buf[bn], &s_full[bn]);
-                uses += 1u << (16 * bn);
-            }
-        }
+    uint32_t cpar = 0;                                     // consumer: per-slot parity of the fills consumed
+    uint32_t s = 0;
+    for (uint32_t it = blockIdx.x; it < n_items; it += G, s = (s + 1 == kStages) ? 0u : s + 1) {
+        if (tid == 0) produce(it + (kStages - 1) * G, s == 0 ? kStages - 1 : s - 1);
         const CRange rg = item_rows(P, S, it);
         if (it < S.n_std) {
-            mbar_wait(&s_full[b], (par >> b) & 1u); par ^= 1u << b;
-            std_quad<kDebug>(P, T, s_g, c, S, now, v, t_guess, rg.r0 + 4 * tid, rg.r1, &buf[b], 4 * tid, &s_empty[b], A);
+            mbar_wait(&s_full[s], (cpar >> s) & 1u); cpar ^= 1u << s;
+            std_quad<kDebug>(P, T, s_g, c, S, now, v, t_guess, rg.r0 + kRPT * tid, rg.r1, &buf[s], kRPT * tid, &s_empty[s], A);
         } else if (stageable(rg)) {
-            mbar_wait(&s_full[b], (par >> b) & 1u); par ^= 1u << b;
-            cmp_range<kDebug, true>(P, T, s_g, c, S, now, v, t_guess, rg, s_T, s_G, s_R, s_rate, &buf[b], &s_empty[b], A);
+            mbar_wait(&s_full[s], (cpar >> s) & 1u); cpar ^= 1u << s;
+            cmp_range<kDebug, true>(P, T, s_g, c, S, now, v, t_guess, rg, s_T, s_G, s_R, s_rate, &buf[s], &s_empty[s], A);
         } else {
             cmp_range<kDebug, false>(P, T, s_g, c, S, now, v, t_guess, rg, s_T, s_G, s_R, s_rate, nullptr, nullptr, A);
         }

@@ -21,11 +21,27 @@ namespace jit {
 constexpr uint32_t kBucketCap = 4096;
 constexpr uint32_t kSpecCap = 8192;            // speculative set resolved in shared memory up to this size
 constexpr uint32_t kGroupSmemSort = 8192;     // |Cd| sorted in shared memory up to this size
-constexpr uint32_t kScoreThreads = 256;
-constexpr uint32_t kTile = 4 * kScoreThreads;    // rows per k_score CTA tile (4 per thread)
+#ifndef JIT_SCORE_THREADS
+#define JIT_SCORE_THREADS 256
+#endif
+constexpr uint32_t kScoreThreads = JIT_SCORE_THREADS;
+#ifndef JIT_RPT
+#define JIT_RPT 2
+#endif
+constexpr uint32_t kRPT = JIT_RPT;               // consecutive rows per k_score thread (2 or 4)
+constexpr uint32_t kTile = kRPT * kScoreThreads;  // rows per k_score work item (tile)
 constexpr uint32_t kPassThreads = 512;
 
 enum : uint32_t { ST_RUN = 0, ST_HIST = 1, ST_COMPACT = 2, ST_RESOLVED = 3, ST_EMPTY = 4, ST_ERROR = 5, ST_FALLBACK = 6 };
+
+// per-task constants of the compound pass (a4), derived at load by k_task_prep from the task
+// arrays: absolute stage sub-deadline a_c + D_s (D_s = floor(D * t_<=s / t_total)),
+// absolute final deadline a_c + D, goodput of the finished stages; err = malformed pattern
+struct TaskInfo {
+    int64_t dls, dlf;
+    uint64_t gdone;
+    uint32_t err, pad;
+};
 
 struct Pool {
     int64_t* arr;
@@ -40,6 +56,7 @@ struct Pool {
     int64_t *t_arr, *t_dl;
     uint32_t *cur_stage, *n_stages, *pattern;
     uint64_t* gdone;
+    TaskInfo* tinfo;
 };
 
 struct alignas(16) Ctrl {
@@ -767,6 +784,29 @@ __global__ void k_progress(Pool P, const uint32_t* rows, const uint32_t* gen, co
     P.gen[r] = gen[i];
     P.pre[r] = pre[i];
     P.meta[r] = m_with_state(P.meta[r], state[i] & 0xFu);
+}
+
+// load-time per-task constants (TaskInfo); D * le fits u64 when D < 2^40 ns and t_total < 2^24 ms
+__global__ void k_task_prep(Pool P) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < P.n_tasks; t += gridDim.x * blockDim.x) {
+        const int64_t a_c = P.t_arr[t], D = P.t_dl[t];
+        const uint32_t s = P.cur_stage[t], Sn = P.n_stages[t];
+        uint64_t le = 0, tot = 0;
+        for (uint32_t u = 0; u < kMaxStages; ++u) {
+            const uint64_t ms = u < Sn ? P.pattern[(size_t)t * kMaxStages + u] : 0u;
+            tot += ms; if (u <= s) le += ms;
+        }
+        TaskInfo ti;
+        ti.err = (tot == 0 || Sn == 0 || Sn > kMaxStages || s >= Sn) ? 1u : 0u;
+        const int64_t Ds = !tot ? 0
+            : ((uint64_t)D < (1ull << 40) && tot < (1ull << 24)) ? (int64_t)((uint64_t)D * le / tot)
+                                                                 : (int64_t)((u128)(uint64_t)D * le / tot);
+        ti.dls = a_c + Ds;                // advisory stage deadline: missing it only sets rate = inf
+        ti.dlf = a_c + D;                 // final deadline: missing it zeroes the task goodput (A43)
+        ti.gdone = P.gdone[t];
+        ti.pad = 0;
+        P.tinfo[t] = ti;
+    }
 }
 
 // load-time validation of a pool (layout rule of jit_pool, group types, ranges)

@@ -72,3 +72,13 @@ print("lines:")
 for k, n in byl.most_common(25):
     print(f"  {k}  {n * 32 / N:7.1f}/row")
 print("ops:", [(o, round(n * 32 / N, 1)) for o, n in ops.most_common(20)])
+
+# stall hot spots (the stall is charged to the instruction after a deferred BAR / BSYNC)
+hs = out and list(csv.reader(io.StringIO(out)))[1]
+cols = [c for c in ("stall_barrier", "stall_wait", "stall_long_sb", "stall_short_sb", "stall_branch_resolving")
+        if c in hs]
+for cname in cols:
+    ci = hs.index(cname)
+    vals = [(int(r[ci] or 0), i) for i, r in enumerate(rows[2:]) if len(r) > ci]
+    top = sorted(vals, reverse=True)[:5]
+    print(cname, [(v, seq[i][0], seq[i - 1][1][:28]) for v, i in top if i < len(seq)])
