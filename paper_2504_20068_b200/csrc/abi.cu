@@ -342,10 +342,12 @@ static void enqueue_radix(jit_sched* h, cudaStream_t s, uint32_t first_pass, uin
 // Step graph: k_score -> k_spec, two kernel nodes and nothing else.  k_score resets the control
 // block; k_spec (programmatic dependent launch: its launch overlaps k_score) resolves the batch
 // and copies the control block to pinned host memory.  When the speculative resolve cannot be
-// exact, k_spec marks the step and finish_step runs the exact radix path from the host -- no
-// device-side launches, no conditional or copy nodes (their fixed costs measured ~26 us and ~6 us
-// per step on B200, profiles/host_overhead.py).  With kernel timing on, event-record nodes
-// separate the kernels (full dependencies, no PDL).
+// exact (or the set is large), the status says so and finish_step runs the exact path from the
+// host -- no device-side launches, no conditional or copy nodes (their fixed costs measured
+// ~26 us and ~6 us per step on B200, profiles/host_overhead.py).  With kernel timing on,
+// event-record nodes separate the kernels (full dependencies, no PDL).
+// (Resolving inside k_score's last CTA instead was measured slower on B200: the resolve is
+// latency-bound, ran ~40% slower in a 256-thread k_score CTA, and its code slowed k_score.)
 static int build_graph(jit_sched* h) {
     if (h->exec) { cudaGraphExecDestroy(h->exec); h->exec = nullptr; }
     if (h->graph) { cudaGraphDestroy(h->graph); h->graph = nullptr; }
@@ -453,6 +455,12 @@ static int finish_step(jit_sched* h, jit_batch* out) {
                 "fb %u spec %u trace %x\n", dc.status, dc.error, dc.fallback, dc.spec_n, dc.trace, dc.launch_err, dc.chain,
                 h->h_ctrl->status, h->h_ctrl->error, h->h_ctrl->fallback, h->h_ctrl->spec_n, h->h_ctrl->trace);
     }
+    if (h->h_ctrl->status == ST_SPEC_BIG) {
+        // a speculative set too large for k_spec's fast path (e.g. after a shift of the keys)
+        exact::spec_big(h->P, h->c, h->d_ctrl, h->S, h->stream);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(h->stream));
+    }
     const uint32_t st0 = h->h_ctrl->status;
     if (st0 == ST_FALLBACK || (st0 == ST_RESOLVED && !h->h_ctrl->window_done && !h->h_ctrl->error)) {
         // the speculative resolve could not be exact (first step after a load, a threshold far
@@ -555,7 +563,7 @@ extern "C" int jit_sched_read_rows(jit_sched* h, double* key, double* rate, int6
 extern "C" int jit_sched_kernel_times(jit_sched* h, int enable, float* ms_out, uint32_t n_out) {
     // enable > 0: record per-kernel events for up to `enable` steps (ring of event slots);
     // enable = 0: off; enable < 0: leave as is.  ms_out gets the AVERAGE over the recorded
-    // steps of [k_score, (unused, 0), k_spec, (unused, 0), whole step].
+    // steps of [k_score, 0, k_spec, 0, whole step].
     if (!h) return JIT_EINVAL;
     if (enable >= 0) {
         CK(cudaStreamSynchronize(h->stream));

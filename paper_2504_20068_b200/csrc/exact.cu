@@ -19,8 +19,10 @@ cudaError_t init_attributes() {
         cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(k_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSpecSmem)) !=
         cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(k_spec_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSpecSmem)) !=
+        cudaSuccess) return e;
     // one shared-memory carveout for every kernel of the step (see abi.cu)
-    const void* ks[] = {(const void*)k_spec,
+    const void* ks[] = {(const void*)k_spec, (const void*)k_spec_big,
                         (const void*)k_hist0, (const void*)k_pass, (const void*)k_compact, (const void*)k_resolve,
                         (const void*)k_cand, (const void*)k_group};
     for (const void* k : ks)
@@ -37,6 +39,9 @@ cudaError_t spec(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int 
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at; cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, k_spec, P, c, ctrl, S, reduce_only);
+}
+void spec_big(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, cudaStream_t s) {
+    k_spec_big<<<1, kSpecThreads, kSpecSmem, s>>>(P, c, ctrl, S);
 }
 void hist0(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t grid, int force, cudaStream_t s) {
     k_hist0<<<grid, kPassThreads, 0, s>>>(P, c, ctrl, S, force);

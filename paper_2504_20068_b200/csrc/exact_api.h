@@ -16,6 +16,8 @@ cudaError_t init_attributes();
 // publishes the control block to pinned host memory.  pdl: programmatic dependent launch after
 // k_score (its launch overlaps k_score; it waits with griddepcontrol.wait)
 cudaError_t spec(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int reduce_only, cudaStream_t s, bool pdl);
+// k_spec_big: the resolve of a speculative set larger than k_spec's fast path (status ST_SPEC_BIG)
+void spec_big(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, cudaStream_t s);
 void hist0(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t grid, int force, cudaStream_t s);
 void pass(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t grid, uint32_t pass_idx, cudaStream_t s);
 void compact(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t grid, cudaStream_t s);

@@ -100,6 +100,218 @@ __device__ __forceinline__ bool is_frames_tag(uint64_t img) {
     return (img & 0xFFF8000000000000ull) == kFramesTag;
 }
 
+// --------------------------------------------------------------------------------------
+// The small-set resolve, shared by k_score's last CTA (the step's fast path) and k_spec
+// --------------------------------------------------------------------------------------
+// thread 0: give up on the speculative resolve -> the host runs the exact radix path after the
+// step (finish_step in abi.cu); rare: first step after a load, a threshold far off, huge ties
+__device__ __forceinline__ void spec_fallback(Ctrl* ctrl, int* fb) {
+    ctrl->status = ST_FALLBACK; ctrl->fallback = 1;
+    *fb = 1;
+}
+
+// Small speculative set (n <= kSpecFast, the steady state): one element per thread and no sort.
+// Element i's rank in the priority order (key desc, id asc) and its inclusive cost prefix come
+// from one pass over the set (shared-memory broadcast reads), so B* = #{i : rank_i < B_max and
+// prefix_i <= tau} (monotone in the rank) is one barrier count; the same for Cd's (len, id) order.
+constexpr uint32_t kSpecFast = 256;
+struct SpecEl {                 // one element of the speculative set, preloaded by k_spec
+    uint64_t img;
+    uint32_t id, cost, len, row, meta, aux;
+};
+template <uint32_t NT>
+static __device__ __noinline__ void spec_fast(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t n,
+                                              bool whole, uint64_t t_img, uint64_t min_img, const SpecEl& el,
+                                              unsigned char* smem) {
+    ulonglong2* f_rec = reinterpret_cast<ulonglong2*>(smem);                 // [kSpecFast] (img, id | cost << 32)
+    uint64_t* f_img = reinterpret_cast<uint64_t*>(f_rec + kSpecFast);        // [kSpecFast]
+    uint32_t* f_id = reinterpret_cast<uint32_t*>(f_img + kSpecFast);         // [kSpecFast]
+    uint32_t* f_cost = f_id + kSpecFast;                                     // [kSpecFast]
+    uint64_t* f_wk = reinterpret_cast<uint64_t*>(f_cost + kSpecFast);        // window key (len << 32 | id), ~0 if not in Cd
+    unsigned long long* pc = reinterpret_cast<unsigned long long*>(f_wk + kSpecFast);   // [kSpecFast + 1]
+    u128* pf = reinterpret_cast<u128*>(pc + kSpecFast + 2);                               // [kSpecFast + 1]
+    uint32_t* o_elem = reinterpret_cast<uint32_t*>(pf + kSpecFast + 1);                  // window position -> element
+    __shared__ uint64_t f_scan[32];
+    __shared__ u128 f_scan128[32];
+    __shared__ uint64_t f_bp_img;
+    __shared__ int f_fb;
+    __shared__ u128 f_best[32];
+    __shared__ uint32_t f_bi[32], f_bj[32];
+    const uint32_t tid = threadIdx.x;
+    const int lane = tid & 31, wid = tid >> 5;
+    const bool own = tid < n;
+    const uint64_t img = own ? el.img : kNone;
+    const uint32_t id = el.id, cost = own ? el.cost : 0u, len = el.len;
+    if (own) {
+        f_rec[tid] = make_ulonglong2(img, (uint64_t)id | ((uint64_t)cost << 32));
+        f_img[tid] = img; f_id[tid] = id; f_cost[tid] = cost;
+    }
+    if (tid == 0) { f_fb = 0; f_bp_img = kNone; }
+    __syncthreads();
+    stamp(ctrl, 2);
+    // (a7) rank in the priority order and inclusive cost prefix: element i is counted by threads i
+    // (first half of the set) and i + kSpecFast (second half) when the CTA has 2 * kSpecFast
+    // threads, else by thread i alone; 16-B broadcast reads, 2 accumulators
+    constexpr bool kSplit = NT >= 2 * kSpecFast;
+    __shared__ uint32_t f_rank2[kSpecFast];
+    __shared__ unsigned long long f_pre2[kSpecFast];
+    {
+        const uint32_t e = tid & (kSpecFast - 1), half = kSplit ? tid / kSpecFast : (tid < kSpecFast ? 0u : 2u);
+        const uint32_t j0 = half == 1 ? n / 2 : 0, j1 = half == 1 ? n : (kSplit ? n / 2 : n);
+        uint32_t ra = 0, rb = 0;
+        uint64_t pa = 0, pb = 0;
+        if (e < n && half < 2) {
+            const ulonglong2 me = f_rec[e];
+            const uint64_t mi = me.x;
+            const uint32_t md = (uint32_t)me.y;
+            uint32_t j = j0;
+            for (; j + 1 < j1; j += 2) {
+                const ulonglong2 q0 = f_rec[j], q1 = f_rec[j + 1];
+                const bool b0 = q0.x > mi || (q0.x == mi && (uint32_t)q0.y < md);
+                const bool b1 = q1.x > mi || (q1.x == mi && (uint32_t)q1.y < md);
+                ra += b0; pa += b0 ? (q0.y >> 32) : 0ull;
+                rb += b1; pb += b1 ? (q1.y >> 32) : 0ull;
+            }
+            if (j < j1) {
+                const ulonglong2 q0 = f_rec[j];
+                const bool b0 = q0.x > mi || (q0.x == mi && (uint32_t)q0.y < md);
+                ra += b0; pa += b0 ? (q0.y >> 32) : 0ull;
+            }
+            if (half == 1) { f_rank2[e] = ra + rb; f_pre2[e] = pa + pb; }
+        }
+        __syncthreads();
+        ra += rb; pa += pb;
+        if (kSplit && half == 0 && e < n) { ra += f_rank2[e]; pa += f_pre2[e]; }
+        if (half == 0) { f_rank2[e] = ra; f_pre2[e] = pa; }
+    }
+    uint32_t rank = own ? f_rank2[tid] : 0u;          // own => tid < kSpecFast: written by itself
+    const uint64_t pre = own ? f_pre2[tid] + cost : 0ull;
+    const bool fits = own && rank + 1 <= c.max_batch && pre <= c.token_budget;
+    const uint32_t bstar = (uint32_t)__syncthreads_count(fits);
+    if (fits && rank + 1 == bstar) f_bp_img = img;          // the B*-th request (A15)
+    __syncthreads();
+    stamp(ctrl, 3);
+    if (tid == 0) {
+        if (bstar == 0) { ctrl->error |= 1u; ctrl->status = ST_ERROR; f_fb = 2; }
+        else {
+            // every entry of S fits: exact only when S is the whole pending set (bp = min key)
+            if (bstar == n && !whole) spec_fallback(ctrl, &f_fb);
+            else {
+                const uint64_t bimg = bstar == n ? min_img : f_bp_img;
+                const double bp = __longlong_as_double((long long)bimg);
+                const double thr = __dmul_rn(__ddiv_rn((double)c.pn, (double)c.pd), bp);   // A16
+                const uint64_t ti = (uint64_t)__double_as_longlong(thr);
+                if (!whole && ti < t_img) spec_fallback(ctrl, &f_fb);   // Cd may leave S
+                else { ctrl->b_star = bstar; ctrl->bp = bp; ctrl->thr = thr; ctrl->thr_img = ti; f_bp_img = ti; }
+            }
+        }
+    }
+    __syncthreads();
+    if (f_fb) return;
+    // (a8) Cd = {key >= thr}; (a9) its (len, id) order (A17/A18)
+    const uint64_t thr_img = f_bp_img;
+    const bool cd = own && img >= thr_img;
+    const uint64_t wk = ((uint64_t)len << 32) | id;
+    if (tid < kSpecFast) f_wk[tid] = cd ? wk : ~0ull;
+    const uint32_t ncd = (uint32_t)__syncthreads_count(cd);
+    {   // window position of each Cd element (two threads per element when the CTA is large)
+        const uint32_t e = tid & (kSpecFast - 1), half = kSplit ? tid / kSpecFast : (tid < kSpecFast ? 0u : 2u);
+        const uint32_t j0 = half == 1 ? n / 2 : 0, j1 = half == 1 ? n : (kSplit ? n / 2 : n);
+        const uint64_t mk = (e < n && half < 2) ? f_wk[e] : ~0ull;
+        uint32_t pa = 0, pb = 0;
+        if (mk != ~0ull) {
+            uint32_t j = j0;
+            for (; j + 1 < j1; j += 2) { pa += f_wk[j] < mk; pb += f_wk[j + 1] < mk; }
+            if (j < j1) pa += f_wk[j] < mk;
+            if (half == 1) f_rank2[e] = pa + pb;
+        }
+        __syncthreads();
+        if (half == 0 && mk != ~0ull) o_elem[pa + pb + (kSplit ? f_rank2[e] : 0u)] = e;
+    }
+    __shared__ uint32_t f_row[kSpecFast], f_meta[kSpecFast], f_aux[kSpecFast];
+    if (own) { f_row[tid] = el.row; f_meta[tid] = el.meta; f_aux[tid] = el.aux; }
+    if (tid == 0) { ctrl->n_cand = ncd; ctrl->status = ST_RESOLVED; }
+    __syncthreads();
+    stamp(ctrl, 4);
+    // prefix sums in window order: position p = tid
+    {
+        uint64_t cv = 0;
+        u128 fv = 0;
+        if (tid < ncd) {
+            const uint32_t e = o_elem[tid];
+            cv = f_cost[e];
+            fv = (u128)fixed_point(__longlong_as_double((long long)f_img[e]));    // A19
+        }
+        uint64_t tc;
+        u128 tf;
+        const uint64_t ec = block_exclusive_scan_u64(cv, f_scan, &tc);
+        const u128 ef = block_exclusive_scan_u128(fv, f_scan128, &tf);
+        if (tid < ncd) { pc[tid] = ec; pf[tid] = ef; }
+        if (tid == 0) { pc[ncd] = tc; pf[ncd] = tf; }
+    }
+    __syncthreads();
+    stamp(ctrl, 5);
+    // first argmax over i of the window [i, j(i)] (j(i): largest end within tau and B_max; P:424 strict >)
+    u128 best = 0;
+    uint32_t bi = 0xFFFFFFFFu, bj = 0;
+    if (tid < ncd) {
+        const uint64_t lim = (uint64_t)pc[tid] + c.token_budget;
+        uint32_t lo = tid, hi = (uint32_t)min((uint64_t)ncd - 1, (uint64_t)tid + c.max_batch - 1);
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi + 1) >> 1;
+            if (pc[mid + 1] <= lim) lo = mid; else hi = mid - 1;
+        }
+        best = pf[lo + 1] - pf[tid]; bi = tid; bj = lo;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const u128 ob = shfl_xor_u128(best, o);
+        const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o), oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        if ((oi != 0xFFFFFFFFu) && (bi == 0xFFFFFFFFu || ob > best || (ob == best && oi < bi))) { best = ob; bi = oi; bj = oj; }
+    }
+    if (lane == 0) { f_best[wid] = best; f_bi[wid] = bi; f_bj[wid] = bj; }
+    __syncthreads();
+    if (wid == 0) {
+        constexpr int nw = NT / 32;
+        best = lane < nw ? f_best[lane] : (u128)0; bi = lane < nw ? f_bi[lane] : 0xFFFFFFFFu; bj = lane < nw ? f_bj[lane] : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const u128 ob = shfl_xor_u128(best, o);
+            const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o), oj = __shfl_xor_sync(0xffffffffu, bj, o);
+            if ((oi != 0xFFFFFFFFu) && (bi == 0xFFFFFFFFu || ob > best || (ob == best && oi < bi))) { best = ob; bi = oi; bj = oj; }
+        }
+        if (lane == 0) { f_bi[0] = bi; f_bj[0] = bj; }
+    }
+    __syncthreads();
+    bi = f_bi[0]; bj = f_bj[0];
+    stamp(ctrl, 6);
+    // the batch in window order and its bookkeeping: ever_scheduled, Running, undo steps_waited+1
+    const uint32_t ns = bj - bi + 1;
+    if (tid < ns) {
+        const uint32_t e = o_elem[bi + tid];
+        const uint32_t r = f_row[e];
+        S.out_ids[tid] = f_id[e];
+        S.out_tokens[tid] = f_cost[e];
+        S.out_rows[tid] = r;
+        uint32_t mt = f_meta[e] | (kEver << 12);            // meta / aux as k_score left them (preloaded)
+        if (m_state(mt) == kQueued || m_state(mt) == kPreempted) mt = m_with_state(mt, kRunning);
+        P.meta[r] = mt;
+        const uint32_t aux = f_aux[e];
+        if ((aux >> 16) < 0xFFFFu) P.aux[r] = aux - (1u << 16);
+    }
+    if (tid == 0) {
+        ctrl->n_selected = ns;
+        ctrl->total_tokens = (uint32_t)(pc[bj + 1] - pc[bi]);
+        ctrl->i_best = bi; ctrl->j_best = bj;
+        ctrl->window_done = 1;
+        // next step's speculative threshold: this step's cutoff with a 15% margin
+        Persist* ps = S.persist;
+        ps->t_guess = (unsigned long long)__double_as_longlong(__dmul_rn(ctrl->thr, 0.85));
+        ps->steps += 1;
+    }
+    stamp(ctrl, 7);
+}
+
 // k_score: the hot pass, compiled into abi.cu (whole-program mode: -rdc costs the scoring loop
 // registers).  Persistent CTAs walk work items of at most kTile rows; the next item's hot state
 // streams into shared memory through bulk asynchronous copies (TMA 1D, mbarrier completion)
@@ -141,15 +353,16 @@ __device__ __forceinline__ void ld_rows64(const int64_t* p, int64_t* v) {
     }
     if constexpr (kRPT == 4) { const longlong2 b = *reinterpret_cast<const longlong2*>(p + 2); v[2] = b.x; v[3] = b.y; }
 }
+// per-row outputs: streaming stores (cache-streaming: evict-first in L2)
 __device__ __forceinline__ void st_rows(uint32_t* p, const uint32_t* v) {
-    if constexpr (kRPT == 4) *reinterpret_cast<uint4*>(p) = make_uint4(v[0], v[1], v[2], v[3]);
-    else if constexpr (kRPT == 2) *reinterpret_cast<uint2*>(p) = make_uint2(v[0], v[1]);
-    else *p = v[0];
+    if constexpr (kRPT == 4) __stcs(reinterpret_cast<uint4*>(p), make_uint4(v[0], v[1], v[2], v[3]));
+    else if constexpr (kRPT == 2) __stcs(reinterpret_cast<uint2*>(p), make_uint2(v[0], v[1]));
+    else __stcs(p, v[0]);
 }
 __device__ __forceinline__ void st_rows64(uint64_t* p, const uint64_t* v) {
-    if constexpr (kRPT >= 2) reinterpret_cast<ulonglong2*>(p)[0] = make_ulonglong2(v[0], v[1]);
-    else *p = v[0];
-    if constexpr (kRPT == 4) reinterpret_cast<ulonglong2*>(p)[1] = make_ulonglong2(v[2], v[3]);
+    if constexpr (kRPT >= 2) __stcs(reinterpret_cast<ulonglong2*>(p), make_ulonglong2(v[0], v[1]));
+    else __stcs(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v[0]);
+    if constexpr (kRPT == 4) __stcs(reinterpret_cast<ulonglong2*>(p) + 1, make_ulonglong2(v[2], v[3]));
 }
 
 // the 32-B hot state of rows q0..q0+kRPT-1 (q0 % kRPT == 0; the SoA capacity is padded to 64 rows)
@@ -200,9 +413,16 @@ __device__ __forceinline__ void mbar_init_fence() {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
 }
+// The pool streams through L2 once per step: its bulk reads carry an evict-first policy so that
+// what is reused every step (code, tables, partials, the speculative set) keeps its L2 lines
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(evict_first_policy()) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
@@ -630,23 +850,26 @@ __device__ __forceinline__ uint32_t spec_bin(uint64_t img, uint64_t t_img) {
 }
 constexpr uint64_t kPackCount = 1ull << 48;   // histogram word: count << 48 | cost (cost sum < 2^48)
 
-// thread 0: give up on the speculative resolve -> the host runs the exact radix path after the
-// step (finish_step in abi.cu); rare: first step after a load, a threshold far off, huge ties
-__device__ __forceinline__ void spec_fallback(Ctrl* ctrl, int* fb) {
-    ctrl->status = ST_FALLBACK; ctrl->fallback = 1;
-    *fb = 1;
-}
-
+template <bool kBig>
 static __device__ void spec_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int reduce_only,
                                  unsigned char* smem);
-// the step's last kernel: resolve, then publish the control block to pinned host memory
+// the step's last kernel: resolve a small speculative set (the steady state), then publish the
+// control block to pinned host memory.  Its code is kept small on purpose: it runs on one SM
+// once per step, so every instruction-cache line it touches is a miss to L2 / HBM; a larger set
+// is resolved by k_spec_big, which the host launches (status ST_SPEC_BIG).
 __global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl, Scratch S, int reduce_only) {
     extern __shared__ __align__(16) unsigned char smem[];
     pdl_wait();
-    spec_body(P, c, ctrl, S, reduce_only, smem);
+    spec_body<false>(P, c, ctrl, S, reduce_only, smem);
+    publish_ctrl(ctrl, S.h_ctrl);
+}
+__global__ void __launch_bounds__(kSpecThreads) k_spec_big(Pool P, Cfg c, Ctrl* ctrl, Scratch S) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    spec_body<true>(P, c, ctrl, S, 0, smem);
     publish_ctrl(ctrl, S.h_ctrl);
 }
 
+template <bool kBig>
 static __device__ void spec_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int reduce_only,
                                  unsigned char* smem) {
     uint64_t* s_img = reinterpret_cast<uint64_t*>(smem + kSpImgOff);
@@ -668,15 +891,24 @@ static __device__ void spec_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const 
     const int lane = tid & 31, wid = tid >> 5;
     stamp(ctrl, 0);
     const uint64_t t_img = S.persist->t_guess;
+    // every thread reads the set size, and in the steady state (small set) its own element and the
+    // element's meta / aux right away: these loads overlap the partials' reduction below
+    const uint32_t n_set = kBig ? ctrl->spec_n : *reinterpret_cast<volatile unsigned int*>(S.spec_cnt);
+    SpecEl el{kNone, 0u, 0u, 0u, 0u, 0u, 0u};
+    if (!kBig && !reduce_only && n_set <= kSpecFast && tid < n_set) {
+        el.img = S.spec_img[tid]; el.id = S.spec_id[tid]; el.cost = S.spec_cost[tid]; el.len = S.spec_len[tid];
+        el.row = S.spec_row[tid];
+        el.meta = P.meta[el.row]; el.aux = P.aux[el.row];
+    }
     if (tid == 0) {
         s_min = kNone; s_cost_tot = 0; s_pend = 0; s_drop = 0; s_err = 0; s_ref = 0;
-        s_n = *S.spec_cnt;
-        *S.spec_cnt = 0;                                   // next step's set starts empty
+        s_n = n_set;
         ctrl->spec_n = s_n;
         s_first = kSpecBins; s_nsel = 0; s_ncd = 0; s_min_above = kNone; s_above = 0; s_fb = 0;
     }
-    for (uint32_t b = tid; b < kSpecBins; b += kSpecThreads) s_hist[b] = 0;
+    if (kBig) for (uint32_t b = tid; b < kSpecBins; b += kSpecThreads) s_hist[b] = 0;
     __syncthreads();
+    if (!kBig && tid == 0) *S.spec_cnt = 0;                // next step's set starts empty (all read it)
     const uint32_t n = s_n < kSpecCap ? s_n : kSpecCap;
     {   // partials of k_score, and (1) the set -> smem + histogram, in one pass
         uint32_t pend = 0, drop = 0, err = 0, ref = 0;
@@ -686,7 +918,7 @@ static __device__ void spec_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const 
             pend += b.n_pending; drop += b.n_dropped; err |= b.err; cost += b.tot_cost; ref += b.refresh;
             if (b.min_img < mn) mn = b.min_img;
         }
-        if (!reduce_only) {
+        if (kBig) {
             for (uint32_t i = tid; i < n; i += kSpecThreads) {
                 const uint64_t img = S.spec_img[i];
                 const uint32_t cs = S.spec_cost[i];
@@ -718,6 +950,11 @@ static __device__ void spec_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const 
     }
     __syncthreads();
     if (s_fb) return;                                      // published as is (k_spec)
+    if constexpr (!kBig) {
+        if (n <= kSpecFast) spec_fast<kSpecThreads>(P, c, ctrl, S, n, whole, t_img, (uint64_t)s_min, el, smem);
+        else if (tid == 0) ctrl->status = ST_SPEC_BIG;     // the host launches k_spec_big
+        return;
+    }
     // (2) boundary bin: thread t owns bins [2047 - 4t - 3, 2047 - 4t], scanned from the top
     {
         uint64_t h[4], loc = 0;

@@ -32,7 +32,8 @@ constexpr uint32_t kRPT = JIT_RPT;               // consecutive rows per k_score
 constexpr uint32_t kTile = kRPT * kScoreThreads;  // rows per k_score work item (tile)
 constexpr uint32_t kPassThreads = 512;
 
-enum : uint32_t { ST_RUN = 0, ST_HIST = 1, ST_COMPACT = 2, ST_RESOLVED = 3, ST_EMPTY = 4, ST_ERROR = 5, ST_FALLBACK = 6 };
+enum : uint32_t { ST_RUN = 0, ST_HIST = 1, ST_COMPACT = 2, ST_RESOLVED = 3, ST_EMPTY = 4, ST_ERROR = 5, ST_FALLBACK = 6,
+                  ST_SPEC_BIG = 7 };
 
 // per-task constants of the compound pass (a4), derived at load by k_task_prep from the task
 // arrays: absolute stage sub-deadline a_c + D_s (D_s = floor(D * t_<=s / t_total)),
@@ -145,7 +146,8 @@ __device__ __forceinline__ void publish_ctrl(const Ctrl* ctrl, Ctrl* host) {
     static_assert(sizeof(Ctrl) % 16 == 0, "ctrl is copied in 16-byte words");
     for (uint32_t i = threadIdx.x; i < kWords; i += blockDim.x)
         reinterpret_cast<uint4*>(host)[i] = __ldcg(reinterpret_cast<const uint4*>(ctrl) + i);
-    __threadfence_system();
+    // no system fence: the host reads the block only after synchronizing with the stream, and
+    // kernel completion makes these writes visible
 }
 
 __device__ __forceinline__ bool is_last_block(uint32_t* counter) {

@@ -15,3 +15,8 @@ for k in range(6):
     print(k, {x: r[x] for x in ("n_pending", "n_refresh", "fallback", "b_star", "n_candidates", "n_selected",
                                 "n_dropped_now", "n_spec")})
     print("   phases ns:", s.phase_times())
+    import ctypes as C
+    t = (C.c_uint64 * 11)()
+    s.lib.jit_sched_phase_times(s.h, t, 11)
+    if t[9] and t[10] and t[3] > t[2]:
+        print("   resolve phase 2->3: %d cycles in %d ns = %.0f MHz" % (t[10] - t[9], t[3] - t[2], (t[10] - t[9]) / (t[3] - t[2]) * 1e3))

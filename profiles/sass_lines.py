@@ -17,6 +17,10 @@ lib = os.path.join(ROOT, "paper_2504_20068_b200", "libjitsched.so")
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
                      text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
+# the source page lists the kernel, then any non-inlined callee: keep the kernel's section
+ends = [i for i, r in enumerate(rows) if i > 1 and r and r[0] == "Kernel Name"]
+if ends:
+    rows = rows[:ends[0]]
 h = rows[1]
 ie, smp = h.index("Instructions Executed"), h.index("Warp Stall Sampling (All Samples)")
 data = [(r[1], int(r[ie] or 0), int(r[smp] or 0)) for r in rows[2:] if len(r) > ie]
