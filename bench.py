@@ -31,9 +31,20 @@ import workloads as W  # noqa: E402
 METRIC = "pending requests scheduled/sec (1M pool)"
 UNIT = "requests/s"
 # algorithmic bytes of k_score: per standalone row 32 B read (arrival 8, input_len,
-# generated, prefilled, cached bound, meta, aux) + 16 B written (8-B key image, cost, aux); per
-# compound call 36 B read (+ task id) + 4 B written (cost); per task 16 B of accumulator updates
-BYTES_ROW, BYTES_CALL, BYTES_TASK = 48, 40, 16
+# generated, prefilled, cached bound, meta, aux) + 16 B written (8-B key image, cost, steps_waited);
+# per compound call the same + 4 B read (task id); per task 32 B read (its load-time constants)
+BYTES_ROW, BYTES_CALL, BYTES_TASK = 48, 52, 32
+
+
+def ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum of k_score per launch, from the committed
+    ncu --set full capture summary (profiles/k_score_traffic.json, written by
+    profiles/summarize.py); None when absent."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "k_score_traffic.json")))
+        return t
+    except Exception:
+        return None
 
 
 def parse():
@@ -371,6 +382,7 @@ def main():
         if steps_i:
             kt += np.array(s.kernel_times()) * steps_i
     kt /= K
+    tr = ncu_traffic()
     total_rows = allsum(float(n))
     value = total_rows / (ms_max / 1e3)
     n_single = int(d["pool"]["n_single"])
@@ -379,11 +391,11 @@ def main():
     hbm_peak = pk["hbm_gbs"] if pk else 6650.0
     achieved = alg_bytes / (kt[0] / 1e3) / 1e9
     roofline = {"bound": "hbm", "kernel": "k_score", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None,
+                "frac": achieved / hbm_peak, "traffic": tr["bytes_per_launch"] if tr else None,
+                "traffic_source": tr["source"] if tr else None,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if pk else "fallback 6650 GB/s",
                 "alg_bytes_per_launch": alg_bytes, "k_score_ms": kt[0],
-                "kernel_ms": {"k_score": kt[0], "k_ctask": kt[1], "k_spec": kt[2], "k_publish": kt[3],
-                              "step_graph": kt[4]},
+                "kernel_ms": {"k_score": kt[0], "k_spec": kt[2], "step_graph_with_event_nodes": kt[4]},
                 "frac_of_8tbs_datasheet": achieved / 8000.0,
                 "first_step_after_load_ms": float(np.median(first_ms)),
                 "ms_per_step_with_event_nodes": ms_events,
@@ -443,7 +455,7 @@ def main():
                            "fast_path_fallbacks": fallback, "last_batch": {"n_selected": sel["n_selected"],
                                                                          "b_star": sel["b_star"],
                                                                          "n_candidates": sel["n_candidates"]}},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 7 * K,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 2 * K,
                 "clocks": clocks, "replay": replay}
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -303,7 +303,7 @@ class Scheduler:
 
     def kernel_times(self, slots=None):
         """slots=k>0 records per-kernel events for up to k steps, 0 disables; with no argument
-        returns the average [k_score, k_ctask, k_spec (+ exact path), k_publish, total] ms over
+        returns the average [k_score, 0, k_spec, 0, total] ms over
         the recorded steps."""
         if slots is not None:
             self._check(self.lib.jit_sched_kernel_times(self.h, C.c_int(int(slots)), None, 0), self.h)

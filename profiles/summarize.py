@@ -3,6 +3,8 @@
 usage: python profiles/summarize.py gpurun_out/launches.csv [gpurun_out/prof_score.ncu-rep ...] > profiles/rNN_ncu.md
 """
 import collections
+import json
+import os
 import csv
 import subprocess
 import sys
@@ -72,7 +74,34 @@ def report(path):
     return "\n".join(out) + "\n"
 
 
+def traffic_json(path, out_json):
+    """k_score's DRAM traffic per launch (read + write) from a --set full capture -> json for bench.py."""
+    r = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True)
+    rows = list(csv.reader(r.stdout.splitlines()))
+    if len(rows) < 3:
+        return
+    h = rows[0]
+    for row in rows[2:]:
+        name = row[h.index("Kernel Name")]
+        if "k_score" not in name:
+            continue
+        units = rows[1]
+        def val(m):
+            v = float(row[h.index(m)].replace(",", ""))
+            u = units[h.index(m)]
+            return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+        rd, wr = val("dram__bytes_read.sum"), val("dram__bytes_write.sum")
+        json.dump({"bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+                   "gpu_time_us": float(row[h.index("gpu__time_duration.sum")]),
+                   "source": f"ncu --set full capture {os.path.basename(path)} (one launch, cold L2)"},
+                  open(out_json, "w"), indent=1)
+        return
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 2 and sys.argv[1] == "--traffic":
+        traffic_json(sys.argv[2], sys.argv[3])
+        sys.exit(0)
     print("## Launch list (ncu, cold-cache, serialised)\n")
     print(launches(sys.argv[1]))
     for p in sys.argv[2:]:
