@@ -189,6 +189,8 @@ extern "C" int jit_sched_init(const jit_config* cfg, const jit_slo_group* groups
     cv.base = reinterpret_cast<unsigned char*>(((uintptr_t)dev_workspace + 255) & ~(uintptr_t)255);
     carve(cv, cfg, table, h->P, h->S, h->T, h->d_groups, h->d_ctrl, h->d_stage);
     h->T.n_rows = table->n_rows; h->T.n_bins = table->n_bins; h->T.l_max = table->l_max;
+    h->T.unit = 1;
+    for (uint32_t k = 0; k < table->n_bins && h->T.unit; ++k) h->T.unit = table->edges[k] == k + 1;
     h->n_groups = n_groups;
     Cfg& c = h->c;
     c.token_budget = cfg->token_budget; c.max_batch = cfg->max_batch; c.chunk = cfg->prefill_chunk;
@@ -285,7 +287,9 @@ extern "C" int jit_sched_load(jit_sched* h, const jit_pool* p) {
         }
         CRange cur{off[0], off[0], 0, 0};
         for (uint32_t t = 0; t < nt; ++t) {
-            if (t > cur.t0 && off[t + 1] - (cur.r0 & ~3u) > kTile) {
+            // a range holds at most kTile rows of aligned quads and at most kTile tasks (the task
+            // sums live in kTile shared-memory slots; a shard can hold many empty tasks)
+            if (t > cur.t0 && (off[t + 1] - (cur.r0 & ~3u) > kTile || t - cur.t0 >= kTile)) {
                 cur.r1 = off[t]; cur.t1 = t;
                 h->h_rng.push_back(cur);
                 cur.r0 = off[t]; cur.t0 = t;
@@ -302,7 +306,7 @@ extern "C" int jit_sched_load(jit_sched* h, const jit_pool* p) {
     {   // persistent grid: every CTA that fits (two tile buffers each), at most one per item
         const void* kf = h->debug ? (const void*)k_score<true> : (const void*)k_score<false>;
         int occ = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, kScoreThreads, score_smem_bytes(h->debug)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, kScoreThreads, score_smem_bytes(h->debug, h->n_groups)));
         const uint32_t items = h->S.n_std + h->S.n_crange;
         h->nb_score = std::max<uint32_t>(1, std::min<uint32_t>(items, (uint32_t)(h->n_sm * std::max(occ, 1))));
     }
@@ -322,9 +326,9 @@ static void enqueue_score(jit_sched* h, cudaStream_t s, int64_t now, int64_t v, 
     Pool& P = h->P;
     Scratch& S = h->S;
     if (h->debug)
-        k_score<true><<<h->nb_score, kScoreThreads, score_smem_bytes(true), s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S, now, v);
+        k_score<true><<<h->nb_score, kScoreThreads, score_smem_bytes(true, h->n_groups), s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S, now, v);
     else
-        k_score<false><<<h->nb_score, kScoreThreads, score_smem_bytes(false), s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S, now, v);
+        k_score<false><<<h->nb_score, kScoreThreads, score_smem_bytes(false, h->n_groups), s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S, now, v);
     if (mid) cudaEventRecordWithFlags(mid, s, capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
 }
 

@@ -71,7 +71,7 @@ __device__ __forceinline__ void row_std(const Cfg& c, const GroupFast* sg, const
                                         uint32_t aux, RowOut& o, double& d_rate, int64_t& d_trem) {
     const uint32_t Lh = max(lhat, g + 1);
     const uint32_t len_rem = Lh - g;
-    const GroupFast G = sg[m_group(meta)];
+    const GroupFast G = sg[pend ? m_group(meta) : 0u];      // rows outside the item: any valid group
     const int64_t trem = arr + G.base + (int64_t)(Lh - 1) * G.tok - now;             // (a3), A9
     uint64_t Gk = (uint64_t)G.w_in_eff * L_i + (uint64_t)G.w_out_eff * Lh;          // (a5) A10/A11
     if (m_flags(meta) & kOverride) Gk = __ldg(ovr + row);
@@ -388,7 +388,10 @@ __device__ __forceinline__ void zero_quad(Quad& Q) {
 #define JIT_STAGES 2
 #endif
 constexpr uint32_t kStages = JIT_STAGES;
-constexpr uint32_t kTaskStage = 64;
+#ifndef JIT_TASK_STAGE
+#define JIT_TASK_STAGE 64
+#endif
+constexpr uint32_t kTaskStage = JIT_TASK_STAGE;
 struct TileBuf {
     int64_t ar[kTile];
     uint32_t li[kTile], ge[kTile], pr[kTile], lh[kTile], me[kTile], ax[kTile], tk[kTile];
@@ -595,7 +598,7 @@ __device__ __forceinline__ void cmp_range(const Pool& P, const Table& T, const G
         for (int k = 0; k < (int)kRPT; ++k) {
             const bool pend = (pendm >> k) & 1u;
             const uint32_t Lh = max(Q.lh[k], Q.ge[k] + 1);
-            const GroupFast G = s_g[m_group(Q.me[k])];
+            const GroupFast G = s_g[pend ? m_group(Q.me[k]) : 0u];
             const uint64_t Gc = (uint64_t)G.w_in_eff * Q.li[k] + (uint64_t)G.w_out_eff * Lh;   // call goodput
             const uint32_t lt = tk[k] - rg.t0;
             cost[k] = pend ? token_cost(Q.li[k], Q.pr[k], c.chunk) : 0u;
@@ -718,23 +721,27 @@ __device__ __forceinline__ void stage_item(const Pool& P, const CRange& rg, bool
     const uint32_t bytes = nr * (8u + 24u + (compound ? 4u : 0u)) +
                            (compound ? (uint32_t)sizeof(TaskInfo) * min(rg.t1 - rg.t0, kTaskStage) : 0u);
     mbar_expect_tx(bar, bytes);
-    bulk_g2s(B->ar, P.arr + q0, 8 * nr, bar);
-    bulk_g2s(B->li, P.len_in + q0, 4 * nr, bar);
-    bulk_g2s(B->ge, P.gen + q0, 4 * nr, bar);
-    bulk_g2s(B->pr, P.pre + q0, 4 * nr, bar);
-    bulk_g2s(B->lh, P.lhat + q0, 4 * nr, bar);
-    bulk_g2s(B->me, P.meta + q0, 4 * nr, bar);
-    bulk_g2s(B->ax, P.aux + q0, 4 * nr, bar);
+    if (nr) {                                            // a range of empty tasks has no rows
+        bulk_g2s(B->ar, P.arr + q0, 8 * nr, bar);
+        bulk_g2s(B->li, P.len_in + q0, 4 * nr, bar);
+        bulk_g2s(B->ge, P.gen + q0, 4 * nr, bar);
+        bulk_g2s(B->pr, P.pre + q0, 4 * nr, bar);
+        bulk_g2s(B->lh, P.lhat + q0, 4 * nr, bar);
+        bulk_g2s(B->me, P.meta + q0, 4 * nr, bar);
+        bulk_g2s(B->ax, P.aux + q0, 4 * nr, bar);
+    }
     if (compound) {
-        bulk_g2s(B->tk, P.task + q0, 4 * nr, bar);
+        if (nr) bulk_g2s(B->tk, P.task + q0, 4 * nr, bar);
         const uint32_t nt = min(rg.t1 - rg.t0, kTaskStage);
         if (nt) bulk_g2s(B->ti, P.tinfo + rg.t0, (uint32_t)sizeof(TaskInfo) * nt, bar);
     }
 }
 
 // dynamic shared memory of k_score: the tile ring + the task sums (+ debug per-task outputs)
-__host__ __device__ constexpr uint32_t score_smem_bytes(bool debug) {
-    return kStages * (uint32_t)sizeof(TileBuf) + 16u * kTile + (debug ? 16u * kTile : 0u);
+// (the SLO-group table sits at the end, sized by the handle's group count)
+__host__ __device__ constexpr uint32_t score_smem_bytes(bool debug, uint32_t n_groups = 256) {
+    return kStages * (uint32_t)sizeof(TileBuf) + 16u * kTile + (debug ? 16u * kTile : 0u) +
+           (uint32_t)sizeof(GroupFast) * n_groups;
 }
 
 // Persistent: CTA b walks the work items b, b + grid, ...; item j of the CTA lives in ring slot
@@ -751,7 +758,7 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
     unsigned long long* s_G = s_T + kTile;
     long long* s_R = reinterpret_cast<long long*>(s_G + kTile);          // kDebug only
     double* s_rate = reinterpret_cast<double*>(s_R + kTile);              // kDebug only
-    __shared__ GroupFast s_g[256];
+    GroupFast* s_g = reinterpret_cast<GroupFast*>(smem + score_smem_bytes(kDebug, 0));
     __shared__ __align__(8) uint64_t s_full[kStages], s_empty[kStages];
     const uint32_t tid = threadIdx.x;
     const uint32_t n_items = S.n_std + S.n_crange;
