@@ -118,6 +118,7 @@ static void carve(Carve& cv, const jit_config* cfg, const jit_len_table* tab, Po
     S.spec_img = cv.take<uint64_t>(kSpecCap);
     S.spec_id = cv.take<uint32_t>(kSpecCap); S.spec_row = cv.take<uint32_t>(kSpecCap);
     S.spec_cost = cv.take<uint32_t>(kSpecCap); S.spec_len = cv.take<uint32_t>(kSpecCap);
+    S.spec_meta = cv.take<uint32_t>(kSpecCap); S.spec_aux = cv.take<uint32_t>(kSpecCap);
     S.persist = cv.take<Persist>(1);
     S.spec_cnt = cv.take<unsigned int>(1);
     S.part = cv.take<BlockPart>(N / kTile + NT + 2);   // one per k_score CTA (<= work items)

@@ -13,8 +13,11 @@ namespace jit {
 
 // Rows whose key image is >= the speculative threshold t (the previous step's cutoff with a
 // margin) join the speculative set; warp ballot + one atomic per warp (all lanes convergent).
+// The entry carries everything the resolve needs (key image, id, row, cost, window length, and
+// the row's meta / aux as this pass left them), so k_spec needs no dependent loads.
 __device__ __forceinline__ void spec_add(const Scratch& S, const uint32_t* ids, bool valid, uint64_t img,
-                                         uint32_t row, uint32_t cost, uint32_t len, uint64_t t) {
+                                         uint32_t row, uint32_t cost, uint32_t len, uint32_t meta, uint32_t aux,
+                                         uint64_t t) {
     const bool take = valid && img >= t;
     const unsigned m = __ballot_sync(0xffffffffu, take);
     if (!m) return;
@@ -26,7 +29,7 @@ __device__ __forceinline__ void spec_add(const Scratch& S, const uint32_t* ids, 
         const uint32_t slot = base + __popc(m & ((1u << lane) - 1u));
         if (slot < kSpecCap) {
             S.spec_img[slot] = img; S.spec_id[slot] = __ldg(ids + row); S.spec_row[slot] = row;
-            S.spec_cost[slot] = cost; S.spec_len[slot] = len;
+            S.spec_cost[slot] = cost; S.spec_len[slot] = len; S.spec_meta[slot] = meta; S.spec_aux[slot] = aux;
         }
     }
 }
@@ -478,7 +481,7 @@ __device__ __forceinline__ void std_quad(const Pool& P, const Table& T, const Gr
             if (needm & (1u << k)) {
                 Q.lh[k] = cond_quantile(T, Q.ax[k] & 0xFFFFu, ep[k] * c.R, c.qn, c.qd);
                 P.lhat[q0 + k] = Q.lh[k];
-                if (ep[k] < 65536u) P.meta[q0 + k] = (Q.me[k] & 0xFFFFu) | (ep[k] << 16);
+                if (ep[k] < 65536u) { Q.me[k] = (Q.me[k] & 0xFFFFu) | (ep[k] << 16); P.meta[q0 + k] = Q.me[k]; }
             }
         }
         A.ref += __popc(needm);
@@ -516,7 +519,8 @@ __device__ __forceinline__ void std_quad(const Pool& P, const Table& T, const Gr
     }
 #pragma unroll
     for (int k = 0; k < (int)kRPT; ++k)
-        spec_add(S, P.id, img[k] != kNone, img[k], q0 + k, cost[k], c.len_key ? Q.li[k] + Q.ge[k] : Q.li[k], t_guess);
+        spec_add(S, P.id, img[k] != kNone, img[k], q0 + k, cost[k], c.len_key ? Q.li[k] + Q.ge[k] : Q.li[k], Q.me[k],
+                 aux[k], t_guess);
 }
 
 // phase B of a compound range: the task's goodput and t_gen (a4) from its load-time constants
@@ -553,6 +557,7 @@ __device__ __forceinline__ void cmp_range(const Pool& P, const Table& T, const G
     const uint32_t qbase = rg.r0 & ~3u;
     const bool single = kStaged || rg.r1 - qbase <= kTile;
     uint32_t kf[kRPT] = {}, kt[kRPT] = {}, kc[kRPT] = {}, kl[kRPT] = {};   // kf: 0x80000000 | frames if pending
+    uint32_t km[kRPT] = {}, ka[kRPT] = {};                                 // meta / aux after this pass
     // ---- phase A: per call (a2, a6) + the task sums
     for (uint32_t base = qbase; base < rg.r1; base += kTile) {     // one iteration when staged
         const uint32_t q0 = base + kRPT * tid;
@@ -587,7 +592,7 @@ __device__ __forceinline__ void cmp_range(const Pool& P, const Table& T, const G
                 if (needm & (1u << k)) {
                     Q.lh[k] = cond_quantile(T, Q.ax[k] & 0xFFFFu, ep[k] * c.R, c.qn, c.qd);
                     P.lhat[q0 + k] = Q.lh[k];
-                    if (ep[k] < 65536u) P.meta[q0 + k] = (Q.me[k] & 0xFFFFu) | (ep[k] << 16);
+                    if (ep[k] < 65536u) { Q.me[k] = (Q.me[k] & 0xFFFFu) | (ep[k] << 16); P.meta[q0 + k] = Q.me[k]; }
                 }
             }
             A.ref += __popc(needm);
@@ -612,6 +617,7 @@ __device__ __forceinline__ void cmp_range(const Pool& P, const Table& T, const G
                 smem_add64(&s_G[lt], (uint32_t)Gc);
                 kf[k] = 0x80000000u | fr; kt[k] = lt; kc[k] = cost[k];
                 kl[k] = c.len_key ? Q.li[k] + Q.ge[k] : Q.li[k];
+                km[k] = Q.me[k]; ka[k] = aux[k];
                 img[k] = kFramesTag | fr;
                 A.pend += 1; A.cost += cost[k];
             }
@@ -674,7 +680,8 @@ __device__ __forceinline__ void cmp_range(const Pool& P, const Table& T, const G
             }
         }
 #pragma unroll
-        for (int k = 0; k < (int)kRPT; ++k) spec_add(S, P.id, img[k] != kNone, img[k], q0 + k, kc[k], kl[k], t_guess);
+        for (int k = 0; k < (int)kRPT; ++k)
+            spec_add(S, P.id, img[k] != kNone, img[k], q0 + k, kc[k], kl[k], km[k], ka[k], t_guess);
     } else if (!kStaged) {
         for (uint32_t base = qbase; base < rg.r1; base += kTile) {
 #pragma unroll
@@ -698,7 +705,8 @@ __device__ __forceinline__ void cmp_range(const Pool& P, const Table& T, const G
                         P.dbg_trem[r] = pd ? s_R[t] : 0;
                     }
                 }
-                spec_add(S, P.id, img != kNone, img, r, cst, len, t_guess);
+                spec_add(S, P.id, img != kNone, img, r, cst, len, img != kNone ? P.meta[r] : 0u,
+                         img != kNone ? P.aux[r] : 0u, t_guess);
             }
         }
     }
@@ -904,8 +912,7 @@ static __device__ void spec_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const 
     SpecEl el{kNone, 0u, 0u, 0u, 0u, 0u, 0u};
     if (!kBig && !reduce_only && n_set <= kSpecFast && tid < n_set) {
         el.img = S.spec_img[tid]; el.id = S.spec_id[tid]; el.cost = S.spec_cost[tid]; el.len = S.spec_len[tid];
-        el.row = S.spec_row[tid];
-        el.meta = P.meta[el.row]; el.aux = P.aux[el.row];
+        el.row = S.spec_row[tid]; el.meta = S.spec_meta[tid]; el.aux = S.spec_aux[tid];
     }
     if (tid == 0) {
         s_min = kNone; s_cost_tot = 0; s_pend = 0; s_drop = 0; s_err = 0; s_ref = 0;

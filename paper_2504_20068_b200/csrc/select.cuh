@@ -128,7 +128,7 @@ struct Scratch {
     // the speculative set (kSpecCap entries): rows with key image >= t_guess, with what k_spec
     // needs of them (key image, id, row, token cost, window length key)
     uint64_t* spec_img;
-    uint32_t *spec_id, *spec_row, *spec_cost, *spec_len;
+    uint32_t *spec_id, *spec_row, *spec_cost, *spec_len, *spec_meta, *spec_aux;
     Persist* persist;
     BlockPart* part;         // k_score partials (one per CTA: n_part)
     const CRange* crange;    // compound CTA ranges (n_crange)
