@@ -28,7 +28,24 @@ __device__ __forceinline__ void wait_par(uint64_t* bar, uint32_t par) {
                  ::"r"(sa(bar)), "r"(par) : "memory");
 }
 
-template <int T, int S>
+// synthetic per-row math of roughly the pool pass's size: M rounds of mixed 64-bit integer and
+// fp64 work (a dependent chain per row, 2 rows per thread are independent)
+template <int M>
+__device__ __forceinline__ uint64_t fake_math(uint64_t a, uint32_t b, uint32_t c) {
+    uint64_t x = a;
+    double d = (double)b + 1.0;
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        x = x * 0x9E3779B97F4A7C15ull + (b ^ (uint32_t)i);
+        const uint32_t q = __umulhi((uint32_t)x, 0x51EB851Fu) >> 4;
+        x ^= (uint64_t)q << 17;
+        d = __fma_rn(d, 1.0000001, (double)(c & 0xFF));
+        if ((x & 7) == 3) x += c;
+    }
+    return x ^ (uint64_t)__double_as_longlong(d);
+}
+
+template <int T, int S, int M = 0>
 __global__ void __launch_bounds__(256) k_tma(Pool P, uint32_t n_items) {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr uint32_t kB = T * 32;                     // bytes per stage
@@ -72,6 +89,7 @@ __global__ void __launch_bounds__(256) k_tma(Pool P, uint32_t n_items) {
             const int64_t a = reinterpret_cast<const int64_t*>(b)[o];
             const uint32_t* u = reinterpret_cast<const uint32_t*>(b + 8 * T);
             im[k] = (uint64_t)a ^ u[o] ^ u[T + o]; co[k] = u[2 * T + o] ^ u[3 * T + o]; ax[k] = u[4 * T + o] ^ u[5 * T + o];
+            if constexpr (M > 0) im[k] = fake_math<M>(im[k], co[k], ax[k]);
         }
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(&empty[s])) : "memory");
 #pragma unroll
@@ -150,6 +168,15 @@ int main() {
     }
     TMA(512, 4, 2) TMA(512, 4, 3) TMA(1024, 3, 2) TMA(1024, 4, 1) TMA(2048, 3, 1) TMA(2048, 2, 2) TMA(256, 8, 4)
     TMA(512, 8, 2) TMA(1024, 6, 1)
+#define TMAM(T, S, CPS, M)                                                                                  \
+    {                                                                                                      \
+        const uint32_t smem = (T) * 32 * (S);                                                              \
+        cudaFuncSetAttribute(k_tma<T, S, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
+        char nm[64];                                                                                       \
+        snprintf(nm, sizeof nm, "tma T=%d S=%d ctas/sm=%d math=%d", T, S, CPS, M);                         \
+        run(nm, [&](Pool P) { k_tma<T, S, M><<<nsm * (CPS), 256, smem>>>(P, N / (T)); });                  \
+    }
+    TMAM(512, 4, 3, 4) TMAM(512, 4, 3, 8) TMAM(512, 4, 3, 16) TMAM(512, 4, 3, 24) TMAM(512, 2, 3, 16)
     for (int cps : {2, 4, 8}) {
         char nm[64];
         snprintf(nm, sizeof nm, "ldg R=4 persistent ctas/sm=%d", cps);
