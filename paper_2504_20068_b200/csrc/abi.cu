@@ -53,6 +53,12 @@ struct jit_sched {
     std::string err;
 };
 
+// k_score instantiation: (debug row outputs) x (App. B feasibility filter)
+static const void* score_fn(bool debug, bool appb) {
+    return debug ? (appb ? (const void*)k_score<true, true> : (const void*)k_score<true, false>)
+                 : (appb ? (const void*)k_score<false, true> : (const void*)k_score<false, false>);
+}
+
 static int set_err(jit_sched* h, int code, const char* fmt, ...) {
     char buf[512];
     va_list ap;
@@ -209,12 +215,14 @@ extern "C" int jit_sched_init(const jit_config* cfg, const jit_slo_group* groups
     for (auto& e : h->ev) CK(cudaEventCreate(&e));
     CK(exact::init_attributes());
     CK(cudaFuncSetAttribute(k_group_rec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(12 * kGroupSmemSort)));
-    CK(cudaFuncSetAttribute(k_score<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)score_smem_bytes(false)));
-    CK(cudaFuncSetAttribute(k_score<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)score_smem_bytes(true)));
+    for (int m = 0; m < 4; ++m)
+        CK(cudaFuncSetAttribute(score_fn(m & 1, m & 2), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)score_smem_bytes(m & 1)));
     // one shared-memory carveout for every kernel of the step: switching the L1/shared split
     // between consecutive kernels costs a drain + reconfiguration of the SMs (several µs each)
     {
-        const void* ks[] = {(const void*)k_begin, (const void*)k_score<false>, (const void*)k_score<true>};
+        const void* ks[] = {(const void*)k_begin, score_fn(false, false), score_fn(true, false), score_fn(false, true),
+                            score_fn(true, true)};
         for (const void* k : ks)
             CK(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
     }
@@ -305,7 +313,7 @@ extern "C" int jit_sched_load(jit_sched* h, const jit_pool* p) {
     h->S.n_std = n_std;
     h->S.n_crange = (uint32_t)h->h_rng.size();
     {   // persistent grid: every CTA that fits (two tile buffers each), at most one per item
-        const void* kf = h->debug ? (const void*)k_score<true> : (const void*)k_score<false>;
+        const void* kf = score_fn(h->debug, h->c.appb != 0);
         int occ = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, kScoreThreads, score_smem_bytes(h->debug, h->n_groups)));
         const uint32_t items = h->S.n_std + h->S.n_crange;
@@ -326,10 +334,9 @@ static void enqueue_score(jit_sched* h, cudaStream_t s, int64_t now, int64_t v, 
                           bool capturing = false) {
     Pool& P = h->P;
     Scratch& S = h->S;
-    if (h->debug)
-        k_score<true><<<h->nb_score, kScoreThreads, score_smem_bytes(true, h->n_groups), s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S, now, v);
-    else
-        k_score<false><<<h->nb_score, kScoreThreads, score_smem_bytes(false, h->n_groups), s>>>(P, h->T, h->d_groups, h->n_groups, h->c, h->d_ctrl, S, now, v);
+    void* args[] = {&P, &h->T, &h->d_groups, &h->n_groups, &h->c, &h->d_ctrl, &S, &now, &v};
+    cudaLaunchKernel(score_fn(h->debug, h->c.appb != 0), dim3(h->nb_score), dim3(kScoreThreads), args,
+                     score_smem_bytes(h->debug, h->n_groups), s);
     if (mid) cudaEventRecordWithFlags(mid, s, capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
 }
 
@@ -382,7 +389,7 @@ static int build_graph(jit_sched* h) {
     CK(cudaGraphGetNodes(g, nodes.data(), &nn));
     // locate the k_score kernel node (its (now, v) arguments are updated per launch) and the
     // timing event nodes
-    const void* score_fn = h->debug ? (const void*)k_score<true> : (const void*)k_score<false>;
+    const void* score_kernel = score_fn(h->debug, h->c.appb != 0);
     h->score_node = nullptr;
     for (auto& e : h->ev_node) e = nullptr;
     for (auto nd : nodes) {
@@ -391,7 +398,7 @@ static int build_graph(jit_sched* h) {
         if (ty == cudaGraphNodeTypeKernel && !h->score_node) {
             cudaKernelNodeParams kp;
             if (cudaGraphKernelNodeGetParams(nd, &kp) != cudaSuccess) { (void)cudaGetLastError(); continue; }
-            if (kp.func == score_fn) { h->score_node = nd; h->score_params = kp; }
+            if (kp.func == score_kernel) { h->score_node = nd; h->score_params = kp; }
         } else if (ty == cudaGraphNodeTypeEventRecord) {
             cudaEvent_t e;
             if (cudaGraphEventRecordNodeGetEvent(nd, &e) != cudaSuccess) { (void)cudaGetLastError(); continue; }

@@ -67,7 +67,7 @@ struct RowOut {
 
 // standalone request, after (a1) admission and (a2) the bound refresh: (a3) t_rem, (a5) key,
 // (a6) cost, steps_waited+1.  Rows that are not pending compute and discard.
-template <bool kDebug>
+template <bool kDebug, bool kAppB>
 __device__ __forceinline__ void row_std(const Cfg& c, const GroupFast* sg, const uint32_t* ovr, uint32_t row,
                                         bool pend, int64_t now, int64_t v, double v_d, double eps_d, int64_t arr,
                                         uint32_t L_i, uint32_t g, uint32_t pre, uint32_t lhat, uint32_t meta,
@@ -79,7 +79,7 @@ __device__ __forceinline__ void row_std(const Cfg& c, const GroupFast* sg, const
     uint64_t Gk = (uint64_t)G.w_in_eff * L_i + (uint64_t)G.w_out_eff * Lh;          // (a5) A10/A11
     if (m_flags(meta) & kOverride) Gk = __ldg(ovr + row);
     if (trem <= 0) Gk = 0;                                                          // A22
-    if (c.appb && (uint64_t)len_rem * (uint64_t)v > (uint64_t)(trem > 0 ? trem : 0)) Gk = 0;
+    if (kAppB && (uint64_t)len_rem * (uint64_t)v > (uint64_t)(trem > 0 ? trem : 0)) Gk = 0;   // App. B filter
     const uint64_t Gp = Gk + (uint64_t)c.delta * fastdiv(aux >> 16, c.frame, c.F_m, c.F_l);
     double key;
     const bool ok = make_key_lv(Gp, len_rem, v_d, eps_d, &key);
@@ -337,8 +337,9 @@ static __device__ __noinline__ void spec_fast(const Pool& P, const Cfg& c, Ctrl*
 #endif
 struct Acc {
     uint32_t pend, drop, err, ref;
-    uint64_t mn;
+    uint64_t mn;                   // smallest key image (compound path)
     uint32_t cost;                 // per thread: <= (rows per thread) x chunk, far below 2^32
+    double mn_d;                   // smallest key (standalone path; keys >= 0 order like their images)
 };
 
 // kRPT consecutive rows per thread: vector loads / stores of kRPT fields (64- or 128-bit)
@@ -441,7 +442,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // standalone rows q0..q0+kRPT-1 (those < n_single)
-template <bool kDebug>
+template <bool kDebug, bool kAppB>
 __device__ __forceinline__ void std_quad(const Pool& P, const Table& T, const GroupFast* s_g, const Cfg& c,
                                          const Scratch& S, int64_t now, int64_t v, uint64_t t_guess, uint32_t q0,
                                          uint32_t ns, const TileBuf* B, uint32_t o, uint64_t* empty, Acc& A) {
@@ -464,32 +465,35 @@ __device__ __forceinline__ void std_quad(const Pool& P, const Table& T, const Gr
     }
 #endif
     // (a1) admission and pending, (a2) which cached bounds are stale
-    uint32_t pendm = 0, dropm = 0, needm = 0, ep[kRPT];
+    const int64_t drop_before = now - c.waiting;           // now - arrival > waiting <=> arrival < now - waiting
+    bool pend[kRPT], drop[kRPT], need[kRPT];
+    uint32_t ep[kRPT];
+    bool any_need = false, any_drop = false;
 #pragma unroll
     for (int k = 0; k < (int)kRPT; ++k) {
         const uint32_t st = m_state(Q.me[k]), fl = m_flags(Q.me[k]);
         const bool arrived = q0 + k < ns && Q.ar[k] <= now;
-        const bool drop = arrived && st == kQueued && !(fl & (kEver | kCompound)) && now - Q.ar[k] > c.waiting;
-        const bool pend = arrived && !drop && st <= kPreempted;
+        drop[k] = arrived && st == kQueued && !(fl & (kEver | kCompound)) && Q.ar[k] < drop_before;
+        pend[k] = arrived && !drop[k] && st <= kPreempted;
         ep[k] = fastdiv(Q.ge[k], c.R, c.R_m, c.R_l);
-        const bool need = pend && (Q.lh[k] == 0 || ep[k] >= 65536u || m_epoch(Q.me[k]) != ep[k]);
-        pendm |= (uint32_t)pend << k; dropm |= (uint32_t)drop << k; needm |= (uint32_t)need << k;
+        need[k] = pend[k] && (Q.lh[k] == 0 || ep[k] >= 65536u || m_epoch(Q.me[k]) != ep[k]);
+        any_need |= need[k]; any_drop |= drop[k];
     }
-    if (__any_sync(0xffffffffu, needm != 0)) {            // rare in steady state: refresh off the main path
+    if (__any_sync(0xffffffffu, any_need)) {              // rare in steady state: refresh off the main path
 #pragma unroll
         for (int k = 0; k < (int)kRPT; ++k) {
-            if (needm & (1u << k)) {
+            if (need[k]) {
                 Q.lh[k] = cond_quantile(T, Q.ax[k] & 0xFFFFu, ep[k] * c.R, c.qn, c.qd);
                 P.lhat[q0 + k] = Q.lh[k];
                 if (ep[k] < 65536u) { Q.me[k] = (Q.me[k] & 0xFFFFu) | (ep[k] << 16); P.meta[q0 + k] = Q.me[k]; }
+                A.ref += 1;
             }
         }
-        A.ref += __popc(needm);
     }
-    if (dropm) {
+    if (any_drop) {
 #pragma unroll
-        for (int k = 0; k < (int)kRPT; ++k) if (dropm & (1u << k)) P.meta[q0 + k] = m_with_state(Q.me[k], kDropped);
-        A.drop += __popc(dropm);
+        for (int k = 0; k < (int)kRPT; ++k)
+            if (drop[k]) { P.meta[q0 + k] = m_with_state(Q.me[k], kDropped); A.drop += 1; }
     }
     uint64_t img[kRPT];
     uint32_t cost[kRPT], aux[kRPT];
@@ -499,14 +503,13 @@ __device__ __forceinline__ void std_quad(const Pool& P, const Table& T, const Gr
         RowOut ro;
         double d_rate = 0.0;
         int64_t d_trem = 0;
-        const bool pend = (pendm >> k) & 1u;
-        row_std<kDebug>(c, s_g, P.ovr, r, pend, now, v, v_d, eps_d, Q.ar[k], Q.li[k], Q.ge[k], Q.pr[k], Q.lh[k],
-                        Q.me[k], Q.ax[k], ro, d_rate, d_trem);
+        row_std<kDebug, kAppB>(c, s_g, P.ovr, r, pend[k], now, v, v_d, eps_d, Q.ar[k], Q.li[k], Q.ge[k], Q.pr[k],
+                               Q.lh[k], Q.me[k], Q.ax[k], ro, d_rate, d_trem);
         img[k] = ro.img; cost[k] = ro.cost; aux[k] = ro.aux;
         A.err |= ro.err;
-        A.pend += ro.img != kNone; A.cost += ro.cost;
-        A.mn = ro.img < A.mn ? ro.img : A.mn;
-        if (kDebug && r < ns) { P.dbg_rate[r] = d_rate; P.dbg_trem[r] = d_trem; P.dbg_lhat[r] = pend ? ro.Lh : 0; }
+        A.pend += pend[k]; A.cost += ro.cost;                 // (an error fails the whole step)
+        A.mn_d = fmin(A.mn_d, __longlong_as_double((long long)ro.img));   // kNone is a NaN: ignored
+        if (kDebug && r < ns) { P.dbg_rate[r] = d_rate; P.dbg_trem[r] = d_trem; P.dbg_lhat[r] = pend[k] ? ro.Lh : 0; }
     }
     if (full) {
         st_rows64(P.img + q0, img);
@@ -524,13 +527,14 @@ __device__ __forceinline__ void std_quad(const Pool& P, const Table& T, const Gr
 }
 
 // phase B of a compound range: the task's goodput and t_gen (a4) from its load-time constants
+template <bool kAppB>
 __device__ __forceinline__ void task_totals(const Cfg& c, int64_t now, int64_t v, const TaskInfo& ti, uint64_t Tsum,
                                             uint64_t Gsum, uint64_t& Gt, uint64_t& t_gen, int64_t& trem,
                                             uint32_t& err) {
     trem = ti.dls - now;                                    // stage sub-deadline (advisory)
     Gt = ti.dlf <= now ? 0 : ti.gdone + Gsum;               // final deadline passed (A43)
     t_gen = Tsum * (uint64_t)v;
-    if (c.appb && t_gen > (uint64_t)(trem > 0 ? trem : 0)) Gt = 0;
+    if (kAppB && t_gen > (uint64_t)(trem > 0 ? trem : 0)) Gt = 0;
     err |= ti.err;
 }
 
@@ -544,7 +548,7 @@ __device__ __forceinline__ uint64_t call_key(uint64_t Gt, uint32_t fr, const Cfg
 
 // one compound range (see above); every thread of the CTA calls it.  kStaged: the range is one
 // tile already staged in B (rows from rg.r0 & ~3); else it is read from global memory.
-template <bool kDebug, bool kStaged>
+template <bool kDebug, bool kAppB, bool kStaged>
 __device__ __forceinline__ void cmp_range(const Pool& P, const Table& T, const GroupFast* s_g, const Cfg& c,
                                           const Scratch& S, int64_t now, int64_t v, uint64_t t_guess,
                                           const CRange rg, unsigned long long* s_T, unsigned long long* s_G,
@@ -643,7 +647,7 @@ __device__ __forceinline__ void cmp_range(const Pool& P, const Table& T, const G
         uint64_t Gt, t_gen;
         int64_t trem;
         const TaskInfo ti = (kStaged && i < kTaskStage) ? B->ti[i] : P.tinfo[rg.t0 + i];
-        task_totals(c, now, v, ti, Tsum, s_G[i], Gt, t_gen, trem, A.err);
+        task_totals<kAppB>(c, now, v, ti, Tsum, s_G[i], Gt, t_gen, trem, A.err);
         const uint64_t B = t_gen + (uint64_t)c.eps;
         const bool okB = B < kTwo53 && B >= t_gen && t_gen / (uint64_t)v == Tsum;
         s_G[i] = Gt;
@@ -756,7 +760,7 @@ __host__ __device__ constexpr uint32_t score_smem_bytes(bool debug, uint32_t n_g
 // j % kStages, and thread 0 keeps the next kStages - 1 items streaming in (HBM reads of several
 // items overlap the scoring of one).  Per slot: `full` completes when the bulk copies land,
 // `empty` when every thread has read its rows out of the slot.
-template <bool kDebug>
+template <bool kDebug, bool kAppB>
 __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P, Table T, const Group* groups,
                                                                          uint32_t n_groups, Cfg c, Ctrl* ctrl,
                                                                          Scratch S, int64_t now, int64_t v) {
@@ -796,7 +800,7 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
     __syncthreads();
     const uint64_t t_guess = S.persist->t_guess;
     pdl_launch_dependents();                               // k_spec may launch now (it waits for us)
-    Acc A{0u, 0u, 0u, 0u, kNone, 0u};
+    Acc A{0u, 0u, 0u, 0u, kNone, 0u, __longlong_as_double((long long)kNone)};
     uint32_t cpar = 0;                                     // consumer: per-slot parity of the fills consumed
     uint32_t s = 0;
     for (uint32_t it = blockIdx.x; it < n_items; it += G, s = (s + 1 == kStages) ? 0u : s + 1) {
@@ -804,15 +808,19 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
         const CRange rg = item_rows(P, S, it);
         if (it < S.n_std) {
             mbar_wait(&s_full[s], (cpar >> s) & 1u); cpar ^= 1u << s;
-            std_quad<kDebug>(P, T, s_g, c, S, now, v, t_guess, rg.r0 + kRPT * tid, rg.r1, &buf[s], kRPT * tid, &s_empty[s], A);
+            std_quad<kDebug, kAppB>(P, T, s_g, c, S, now, v, t_guess, rg.r0 + kRPT * tid, rg.r1, &buf[s], kRPT * tid, &s_empty[s], A);
         } else if (stageable(rg)) {
             mbar_wait(&s_full[s], (cpar >> s) & 1u); cpar ^= 1u << s;
-            cmp_range<kDebug, true>(P, T, s_g, c, S, now, v, t_guess, rg, s_T, s_G, s_R, s_rate, &buf[s], &s_empty[s], A);
+            cmp_range<kDebug, kAppB, true>(P, T, s_g, c, S, now, v, t_guess, rg, s_T, s_G, s_R, s_rate, &buf[s], &s_empty[s], A);
         } else {
-            cmp_range<kDebug, false>(P, T, s_g, c, S, now, v, t_guess, rg, s_T, s_G, s_R, s_rate, nullptr, nullptr, A);
+            cmp_range<kDebug, kAppB, false>(P, T, s_g, c, S, now, v, t_guess, rg, s_T, s_G, s_R, s_rate, nullptr, nullptr, A);
         }
     }
-    store_part(S.part, A.pend, A.drop, A.err, A.mn, A.cost, A.ref);
+    {
+        const uint64_t md = (uint64_t)__double_as_longlong(A.mn_d);
+        const uint64_t m_std = A.mn_d == A.mn_d ? md : kNone;    // NaN: no pending standalone row
+        store_part(S.part, A.pend, A.drop, A.err, m_std < A.mn ? m_std : A.mn, A.cost, A.ref);
+    }
 }
 #endif  // !JIT_EXACT_TU
 
