@@ -439,7 +439,7 @@ def main():
         ms_med = float(np.median(ms_s))
         steady = {"ms_per_step_wall_median": ms_med, "value": n / (ms_med / 1e3), "unit": UNIT, "steps": KS,
                   "refresh_per_step_mean": float(np.mean(refresh)), "fallback_steps": fb,
-                  "how": "synchronous jit_sched_step with the previous batch's progress (H2D) and the batch D2H, "
+                  "how": "synchronous jit_sched_step with the previous batch's progress (one pinned H2D) and the batch (written by the GPU into pinned host memory), "
                          "wall clock, median over steps, 6 rotated pools"}
     except Exception as ex:  # pragma: no cover
         steady = {"error": str(ex)[:200]}

@@ -30,6 +30,9 @@ struct jit_sched {
     Scratch S{};
     Ctrl* d_ctrl = nullptr;
     Ctrl* h_ctrl = nullptr;           // pinned
+    uint32_t* h_batch = nullptr;      // pinned: the fast path writes the batch here (ids | tokens | rows)
+    uint32_t* h_prog = nullptr;       // pinned staging of progress rows (4 x prog_cap)
+    uint64_t prog_cap = 0;
     uint32_t* d_stage = nullptr;      // progress staging (4 * capacity)
     cudaStream_t stream = nullptr;    // caller's stream
     cudaStream_t cap = nullptr;       // private capture stream
@@ -210,6 +213,8 @@ extern "C" int jit_sched_init(const jit_config* cfg, const jit_slo_group* groups
     CK(cudaMemcpyAsync((void*)h->T.cum, table->cum, 4ull * table->n_rows * table->n_bins, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemcpyAsync(h->d_groups, groups, sizeof(Group) * n_groups, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMallocHost(&h->h_ctrl, sizeof(Ctrl)));
+    CK(cudaMallocHost(&h->h_batch, 3ull * 4 * (cfg->max_batch + 1)));
+    h->S.h_batch = h->h_batch;
     memset(h->h_ctrl, 0, sizeof(Ctrl));
     h->S.h_ctrl = h->h_ctrl;              // pinned + mapped (UVA): the step's last kernel writes it
     for (auto& e : h->ev) CK(cudaEventCreate(&e));
@@ -503,10 +508,19 @@ static int finish_step(jit_sched* h, jit_batch* out) {
         out->b_star = c.b_star; out->bp = c.bp; out->thr = c.thr;
         if (c.n_selected > out->capacity && (out->ids || out->tokens || out->rows))
             return set_err(h, JIT_ECAPACITY, "batch capacity %u < %u", out->capacity, c.n_selected);
-        if (out->ids) CK(cudaMemcpyAsync(out->ids, h->S.out_ids, 4ull * c.n_selected, cudaMemcpyDeviceToHost, h->stream));
-        if (out->tokens) CK(cudaMemcpyAsync(out->tokens, h->S.out_tokens, 4ull * c.n_selected, cudaMemcpyDeviceToHost, h->stream));
-        if (out->rows) CK(cudaMemcpyAsync(out->rows, h->S.out_rows, 4ull * c.n_selected, cudaMemcpyDeviceToHost, h->stream));
-        CK(cudaStreamSynchronize(h->stream));
+        if (c.batch_on_host) {
+            // the fast path already wrote the batch into pinned host memory
+            const uint32_t* hb = h->h_batch;
+            const uint64_t B = h->cfg.max_batch + 1;
+            if (out->ids) memcpy(out->ids, hb, 4ull * c.n_selected);
+            if (out->tokens) memcpy(out->tokens, hb + B, 4ull * c.n_selected);
+            if (out->rows) memcpy(out->rows, hb + 2 * B, 4ull * c.n_selected);
+        } else {
+            if (out->ids) CK(cudaMemcpyAsync(out->ids, h->S.out_ids, 4ull * c.n_selected, cudaMemcpyDeviceToHost, h->stream));
+            if (out->tokens) CK(cudaMemcpyAsync(out->tokens, h->S.out_tokens, 4ull * c.n_selected, cudaMemcpyDeviceToHost, h->stream));
+            if (out->rows) CK(cudaMemcpyAsync(out->rows, h->S.out_rows, 4ull * c.n_selected, cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+        }
     }
     return JIT_OK;
 }
@@ -517,13 +531,23 @@ extern "C" int jit_sched_step(jit_sched* h, const jit_step_in* in, jit_batch* ou
     if (in->v_token_ns <= 0) return set_err(h, JIT_EINVAL, "v_token must be > 0");
     if (in->n_progress) {
         if (in->n_progress > h->cfg.capacity) return set_err(h, JIT_ECAPACITY, "too many progress rows");
-        const uint64_t m = in->n_progress, N = ((uint64_t)h->cfg.capacity + 63) & ~63ull;
-        CK(cudaMemcpyAsync(h->d_stage, in->prog_row, 4 * m, cudaMemcpyHostToDevice, h->stream));
-        CK(cudaMemcpyAsync(h->d_stage + N, in->prog_generated, 4 * m, cudaMemcpyHostToDevice, h->stream));
-        CK(cudaMemcpyAsync(h->d_stage + 2 * N, in->prog_prefilled, 4 * m, cudaMemcpyHostToDevice, h->stream));
-        CK(cudaMemcpyAsync(h->d_stage + 3 * N, in->prog_state, 4 * m, cudaMemcpyHostToDevice, h->stream));
-        k_progress<<<(uint32_t)((m + 255) / 256), 256, 0, h->stream>>>(h->P, h->d_stage, h->d_stage + N, h->d_stage + 2 * N,
-                                                                     h->d_stage + 3 * N, (uint32_t)m);
+        const uint64_t m = in->n_progress;
+        // one H2D copy: the four arrays are packed into pinned staging first (grown on demand;
+        // the previous step has completed, so the staging is free)
+        if (m > h->prog_cap) {
+            if (h->h_prog) cudaFreeHost(h->h_prog);
+            h->h_prog = nullptr; h->prog_cap = 0;
+            const uint64_t cap = std::max<uint64_t>(m, 4096);
+            CK(cudaMallocHost(&h->h_prog, 16 * cap));
+            h->prog_cap = cap;
+        }
+        memcpy(h->h_prog, in->prog_row, 4 * m);
+        memcpy(h->h_prog + m, in->prog_generated, 4 * m);
+        memcpy(h->h_prog + 2 * m, in->prog_prefilled, 4 * m);
+        memcpy(h->h_prog + 3 * m, in->prog_state, 4 * m);
+        CK(cudaMemcpyAsync(h->d_stage, h->h_prog, 16 * m, cudaMemcpyHostToDevice, h->stream));
+        k_progress<<<(uint32_t)((m + 255) / 256), 256, 0, h->stream>>>(h->P, h->d_stage, h->d_stage + m, h->d_stage + 2 * m,
+                                                                     h->d_stage + 3 * m, (uint32_t)m);
         CK(cudaGetLastError());
     }
     int rc = launch_step(h, in->now_ns, in->v_token_ns);
@@ -621,6 +645,8 @@ extern "C" void jit_sched_destroy(jit_sched* h) {
     if (h->cap) cudaStreamDestroy(h->cap);
     if (h->cap2) cudaStreamDestroy(h->cap2);
     if (h->h_ctrl) cudaFreeHost(h->h_ctrl);
+    if (h->h_batch) cudaFreeHost(h->h_batch);
+    if (h->h_prog) cudaFreeHost(h->h_prog);
     for (auto e : h->ev) if (e) cudaEventDestroy(e);
     for (auto e : h->slots) cudaEventDestroy(e);
     delete h;

@@ -296,6 +296,8 @@ static __device__ __noinline__ void spec_fast(const Pool& P, const Cfg& c, Ctrl*
         S.out_ids[tid] = f_id[e];
         S.out_tokens[tid] = f_cost[e];
         S.out_rows[tid] = r;
+        const uint32_t B = c.max_batch + 1;                 // and the pinned host mirror (no D2H copy)
+        S.h_batch[tid] = f_id[e]; S.h_batch[B + tid] = f_cost[e]; S.h_batch[2 * B + tid] = r;
         uint32_t mt = f_meta[e] | (kEver << 12);            // meta / aux as k_score left them (preloaded)
         if (m_state(mt) == kQueued || m_state(mt) == kPreempted) mt = m_with_state(mt, kRunning);
         P.meta[r] = mt;
@@ -306,7 +308,7 @@ static __device__ __noinline__ void spec_fast(const Pool& P, const Cfg& c, Ctrl*
         ctrl->n_selected = ns;
         ctrl->total_tokens = (uint32_t)(pc[bj + 1] - pc[bi]);
         ctrl->i_best = bi; ctrl->j_best = bj;
-        ctrl->window_done = 1;
+        ctrl->window_done = 1; ctrl->batch_on_host = 1;
         // next step's speculative threshold: this step's cutoff with a 15% margin
         Persist* ps = S.persist;
         ps->t_guess = (unsigned long long)__double_as_longlong(__dmul_rn(ctrl->thr, 0.85));

@@ -76,6 +76,7 @@ struct alignas(16) Ctrl {
     unsigned long long tot_cost;     // sum of the token costs of all pending rows
     uint32_t spec_n, spec_ovf, fallback, window_done;
     uint32_t n_refresh;                         // length-bound refreshes this step (a2)
+    uint32_t batch_on_host, pad_b;              // 1: the batch is in the pinned host mirror (fast path)
     uint32_t chain;                             // 1 while the device-launched exact path runs
     uint32_t trace, launch_err;                 // exact-path kernels that ran (bit mask) / device launch error
     unsigned long long ts[12];                  // %globaltimer stamps of the single-CTA phases
@@ -135,6 +136,7 @@ struct Scratch {
     uint32_t n_part, n_std, n_crange, pad3;   // partials = k_score CTAs; items = n_std tiles + ranges
     unsigned int* spec_cnt;  // size of the speculative set (k_score atomics; reset by k_spec)
     Ctrl* h_ctrl;            // pinned host copy of the control block, written by the step's last kernel
+    uint32_t* h_batch;       // pinned host mirror of the batch: ids | tokens | rows, (max_batch + 1) each
     uint32_t nb_full, grid_pass;   // launch geometry of the fallback chain (device-side launches)
 };
 
