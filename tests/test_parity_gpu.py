@@ -183,3 +183,28 @@ def test_determinism_double_run():
     b, _, rb = _run_both(d)
     assert np.array_equal(a["batch_ids"], b["batch_ids"]) and a["bp"] == b["bp"]
     assert np.array_equal(ra["key"].view(np.uint64), rb["key"].view(np.uint64))
+
+
+def test_speculative_paths_against_oracle_chain():
+    """Consecutive steps on one handle: the first step after a load takes the exact radix path
+    (no threshold yet), later steps resolve from the speculative set -- in k_spec's fast path
+    (|S| <= 256) or in k_spec_big (larger sets).  Every step is checked against the oracle run on
+    the state the previous oracle step left (meta / aux bookkeeping), and both speculative paths
+    must have been exercised."""
+    seen_fast = seen_big = False
+    for tau, bmax, n in [(8192, 8192, 200_000), (65536, 65536, 200_000), (4096, 64, 100_000)]:
+        d = W.pool_snapshot(21, n, table_draws=1 << 16)
+        d["cfg"] = W.default_config(token_budget=tau, max_batch=bmax)
+        s = _sched(d, debug=False)
+        s.load(d["pool"], d["tasks"])
+        pool = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in d["pool"].items()}
+        for k in range(4):
+            ref = oracle.step(d["cfg"], d["groups"], d["table"], d["now_ns"], d["v_token_ns"], pool, d["tasks"])
+            got = s.step(d["now_ns"], d["v_token_ns"])
+            _compare(got, ref, ctx=f"tau={tau} step {k} n_spec={got['n_spec']} fallback={got['fallback']}")
+            if k > 0 and not got["fallback"]:
+                seen_fast |= got["n_spec"] <= 256
+                seen_big |= got["n_spec"] > 256
+            pool["meta"], pool["aux"] = ref["meta"], ref["aux"]
+        s.close()
+    assert seen_fast and seen_big, (seen_fast, seen_big)
