@@ -7,12 +7,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libjitsched.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-# abi.cu (host code + the scoring kernels) is compiled whole-program; exact.cu (k_spec and
-# the exact path it launches from the device) with -rdc, device-linked against cudadevrt
+# two translation units: abi.cu (host code + the scoring kernel) and exact.cu (the resolve
+# kernels and the exact radix path); both whole-program, no device-side launches
 BASE = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "--fmad=false",
         "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
-UNITS = [("abi.cu", []), ("exact.cu", ["-rdc=true"])]
-LINK = ["-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-lcudadevrt"]
+UNITS = [("abi.cu", []), ("exact.cu", [])]
+LINK = ["-shared", "-gencode", "arch=compute_100a,code=sm_100a"]
 
 
 def sources():

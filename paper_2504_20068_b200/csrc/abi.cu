@@ -195,6 +195,9 @@ extern "C" int jit_sched_init(const jit_config* cfg, const jit_slo_group* groups
     h->stream = (cudaStream_t)cfg->stream;
     CK(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&h->cap2, cudaStreamNonBlocking));
+    // zero the workspace once: SoA padding rows (read by whole-quad tile loads, then masked) and
+    // every scratch array start defined
+    CK(cudaMemsetAsync(dev_workspace, 0, ws_bytes, h->stream));
     Carve cv;
     cv.base = reinterpret_cast<unsigned char*>(((uintptr_t)dev_workspace + 255) & ~(uintptr_t)255);
     carve(cv, cfg, table, h->P, h->S, h->T, h->d_groups, h->d_ctrl, h->d_stage);

@@ -1,7 +1,7 @@
-// exact.cu -- the speculative resolve (k_spec) and the exact path it launches from the device
-// (k_hist0, k_pass, k_compact, k_resolve, k_cand, k_group).  Compiled with -rdc
-// (CUDA dynamic parallelism) and device-linked against cudadevrt; the hot scoring kernels live
-// in abi.cu, compiled whole-program.
+// exact.cu -- the speculative resolve (k_spec, k_spec_big) and the exact radix path the host
+// launches when the speculation cannot be exact (k_hist0, k_pass, k_compact, k_resolve, k_cand,
+// k_group).  A separate translation unit from abi.cu (the hot scoring kernel), so each compiles
+// with its own register allocation.
 #define JIT_EXACT_TU 1
 #include "common.cuh"
 #include "select.cuh"

@@ -77,7 +77,7 @@ struct alignas(16) Ctrl {
     uint32_t spec_n, spec_ovf, fallback, window_done;
     uint32_t n_refresh;                         // length-bound refreshes this step (a2)
     uint32_t batch_on_host, pad_b;              // 1: the batch is in the pinned host mirror (fast path)
-    uint32_t chain;                             // 1 while the device-launched exact path runs
+    uint32_t chain;                             // (unused; kept for the control-block layout)
     uint32_t trace, launch_err;                 // exact-path kernels that ran (bit mask) / device launch error
     unsigned long long ts[12];                  // %globaltimer stamps of the single-CTA phases
 };
@@ -137,7 +137,7 @@ struct Scratch {
     unsigned int* spec_cnt;  // size of the speculative set (k_score atomics; reset by k_spec)
     Ctrl* h_ctrl;            // pinned host copy of the control block, written by the step's last kernel
     uint32_t* h_batch;       // pinned host mirror of the batch: ids | tokens | rows, (max_batch + 1) each
-    uint32_t nb_full, grid_pass;   // launch geometry of the fallback chain (device-side launches)
+    uint32_t nb_full, grid_pass;   // launch geometry of the exact path
 };
 
 // The last kernel of a step writes the control block straight into pinned host memory (no
@@ -396,29 +396,14 @@ __device__ __forceinline__ u128 block_exclusive_scan_u128(u128 v, u128* scratch,
 }
 
 #ifdef JIT_EXACT_TU
-// The exact path launched by k_spec runs as a chain of tail launches: each kernel launches its
-// successor (a tail launch runs once the launching grid has finished; one per grid).  Only
-// while ctrl->chain is set -- the same kernels launched from the host never chain.
+// The exact path (host-launched by finish_step when the speculative resolve cannot be exact):
+// k_hist0 -> k_pass x <= 7 -> k_compact -> k_resolve -> k_cand -> k_group; each kernel returns at
+// once unless the control block's status says it has work.
 __global__ void k_pass(Pool P, Cfg c, Ctrl* ctrl, Scratch S, uint32_t pass_idx);
 __global__ void k_compact(Pool P, Cfg c, Ctrl* ctrl, Scratch S);
 __global__ void k_resolve(Pool P, Cfg c, Ctrl* ctrl, Scratch S);
 __global__ void k_cand(Pool P, Cfg c, Ctrl* ctrl, Scratch S, int only_after_fallback);
 __global__ void k_group(Pool P, Cfg c, Ctrl* ctrl, Scratch S);
-
-// successor of a radix level (k_hist0 = level 0, k_pass(i) = level i+1), decided by the
-// last CTA after it resolved the level; called by its thread 0
-__device__ __noinline__ void chain_after_level(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S,
-                                               uint32_t next_pass) {
-    const uint32_t st = *(volatile uint32_t*)&ctrl->status;
-    if (st == ST_HIST && next_pass < kLevels - 1)
-        k_pass<<<S.grid_pass, kPassThreads, 0, cudaStreamTailLaunch>>>(P, c, ctrl, S, next_pass);
-    else if (st == ST_COMPACT) k_compact<<<S.grid_pass, kPassThreads, 0, cudaStreamTailLaunch>>>(P, c, ctrl, S);
-    else if (st == ST_RESOLVED) k_cand<<<S.grid_pass, kPassThreads, 0, cudaStreamTailLaunch>>>(P, c, ctrl, S, 1);
-    else k_group<<<1, 1024, 12 * kGroupSmemSort, cudaStreamTailLaunch>>>(P, c, ctrl, S);
-    const cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) { ctrl->error |= 2u; ctrl->status = ST_ERROR; ctrl->launch_err = e; }
-    atomicOr(&ctrl->trace, 8u);
-}
 
 // level-0 histogram of the key images (fallback path only), last CTA resolves level 0
 __global__ void __launch_bounds__(kPassThreads) k_hist0(Pool P, Cfg c, Ctrl* ctrl, Scratch S, int force) {
@@ -444,8 +429,6 @@ __global__ void __launch_bounds__(kPassThreads) k_hist0(Pool P, Cfg c, Ctrl* ctr
         if (s_cnt[b]) { atomicAdd(hcnt + b, s_cnt[b]); atomicAdd(hcost + b, (unsigned long long)s_cost[b]); }
     if (is_last_block(&ctrl->done[0])) {
         resolve_level(c, ctrl, hcnt, hcost, 0);
-        __syncthreads();
-        if (threadIdx.x == 0 && ctrl->chain) chain_after_level(P, c, ctrl, S, 0);
     }
 }
 
@@ -488,8 +471,6 @@ __global__ void __launch_bounds__(kPassThreads) k_pass(Pool P, Cfg c, Ctrl* ctrl
         if (s_cnt[b]) { atomicAdd(hcnt + b, s_cnt[b]); atomicAdd(hcost + b, (unsigned long long)s_cost[b]); }
     if (is_last_block(&ctrl->done[1 + (pass_idx & 7)])) {
         resolve_level(c, ctrl, hcnt, hcost, L);
-        __syncthreads();
-        if (threadIdx.x == 0 && ctrl->chain) chain_after_level(P, c, ctrl, S, pass_idx + 1);
     }
 }
 
@@ -498,10 +479,6 @@ __global__ void __launch_bounds__(kPassThreads) k_pass(Pool P, Cfg c, Ctrl* ctrl
 // --------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kPassThreads) k_compact(Pool P, Cfg c, Ctrl* ctrl, Scratch S) {
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&ctrl->trace, 32u);
-    if (blockIdx.x == 0 && threadIdx.x == 0 && ctrl->chain) {
-        k_resolve<<<1, 1024, (sizeof(u128) + 4) * kBucketCap, cudaStreamTailLaunch>>>(P, c, ctrl, S);
-        if (cudaGetLastError() != cudaSuccess) { ctrl->error |= 2u; ctrl->status = ST_ERROR; }
-    }
     if (ctrl->status != ST_COMPACT) return;
     const uint32_t L = ctrl->level;
     const u128 prefix = ctrl->prefix;
@@ -543,10 +520,6 @@ __global__ void __launch_bounds__(kPassThreads) k_compact(Pool P, Cfg c, Ctrl* c
 // --------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024) k_resolve(Pool P, Cfg c, Ctrl* ctrl, Scratch S) {
     if (threadIdx.x == 0) atomicOr(&ctrl->trace, 64u);
-    if (threadIdx.x == 0 && ctrl->chain) {
-        k_cand<<<S.grid_pass, kPassThreads, 0, cudaStreamTailLaunch>>>(P, c, ctrl, S, 1);
-        if (cudaGetLastError() != cudaSuccess) { ctrl->error |= 2u; ctrl->status = ST_ERROR; }
-    }
     if (ctrl->status != ST_COMPACT) return;
     extern __shared__ __align__(16) unsigned char smem[];
     u128* sk = reinterpret_cast<u128*>(smem);
@@ -604,10 +577,6 @@ __global__ void __launch_bounds__(1024) k_resolve(Pool P, Cfg c, Ctrl* ctrl, Scr
 // --------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kPassThreads) k_cand(Pool P, Cfg c, Ctrl* ctrl, Scratch S, int only_after_fallback) {
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&ctrl->trace, 128u);
-    if (blockIdx.x == 0 && threadIdx.x == 0 && ctrl->chain) {
-        k_group<<<1, 1024, 12 * kGroupSmemSort, cudaStreamTailLaunch>>>(P, c, ctrl, S);
-        if (cudaGetLastError() != cudaSuccess) { ctrl->error |= 2u; ctrl->status = ST_ERROR; }
-    }
     if (ctrl->status != ST_RESOLVED) return;
     if (only_after_fallback && !ctrl->fallback) return;      // k_spec already produced Cd
     const uint64_t thr_img = ctrl->thr_img;
@@ -744,8 +713,6 @@ __global__ void __launch_bounds__(1024) k_group(Pool P, Cfg c, Ctrl* ctrl, Scrat
     if (threadIdx.x == 0) { s_run = ctrl->status == ST_RESOLVED && !ctrl->window_done; atomicOr(&ctrl->trace, 256u); }
     __syncthreads();
     if (s_run) group_body(P, c, ctrl, S, smem);
-    __syncthreads();
-    if (threadIdx.x == 0) ctrl->chain = 0;                  // the exact path ends here
 }
 
 static __device__ void group_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, unsigned char* smem) {

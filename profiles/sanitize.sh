@@ -1,0 +1,10 @@
+#!/bin/bash
+# compute-sanitizer over small GPU parity cases (memcheck / racecheck / synccheck /
+# initcheck on small configs).  Logs in gpurun_out/sanitizer_*.log.
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+T="tests/test_parity_gpu.py::test_empty_and_degenerate tests/test_parity_gpu.py::test_c3_shaped_pools_full_compare tests/test_replay_gpu.py::test_c1_toy_full_log tests/test_parity_gpu.py::test_speculative_paths_against_oracle_chain"
+for tool in memcheck racecheck synccheck initcheck; do
+  timeout 1500 compute-sanitizer --tool $tool --print-limit 10 --error-exitcode 9 python -m pytest -q -x $T \
+      > gpurun_out/sanitizer_$tool.log 2>&1
+  echo "$tool rc=$? $(grep -m1 'ERROR SUMMARY' gpurun_out/sanitizer_$tool.log)"
+done
