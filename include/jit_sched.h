@@ -59,8 +59,8 @@ enum { JIT_F_EVER = 1, JIT_F_COMPOUND = 2, JIT_F_OVERRIDE = 4 };
 #define JIT_MAX_STAGES 8
 /* jit_config.flags */
 #define JIT_CFG_DEBUG_ROWS 1u   /* keep per-row rate / t_rem / Lhat / cost for jit_sched_read_rows */
-#define JIT_CFG_NO_GRAPH 2u     /* launch the step's kernels directly instead of one CUDA graph
-                                   (profilers cannot look inside graphs with conditional nodes) */
+#define JIT_CFG_NO_GRAPH 2u     /* launch the step's kernels (k_score, k_spec) directly instead of
+                                   as one CUDA graph (for tools that do not follow graphs) */
 
 /* One SLO group (a row of the SLO table; reading A35).  Times are int64 ns.
  * LAT uses ttft/tbt, DDL e2el, CMP e2el per stage (D = e2el * stages), BE be_deadline.
@@ -183,8 +183,8 @@ int jit_sched_read_rows(jit_sched* h, double* key, double* rate, int64_t* t_rem,
 /* Per-kernel device time, from CUDA events recorded (as graph event nodes) on cfg.stream
  * around each kernel of the step.  enable > 0 keeps one event set per step for up to
  * `enable` steps; 0 turns timing off; < 0 leaves it unchanged.  ms_out (n_out <= 5) gets the
- * average in ms over the recorded steps of [k_score, k_ctask, k_spec (including the exact
- * path it launched, if any), k_publish, whole step]. */
+ * average in ms over the recorded steps of [k_score, 0, k_spec, 0, whole step] (the exact
+ * path, when the host runs it after a step, is not included). */
 int jit_sched_kernel_times(jit_sched* h, int enable, float* ms_out, uint32_t n_out);
 
 /* Diagnostics: %globaltimer stamps (ns) of the phases of the single-CTA resolve of the last

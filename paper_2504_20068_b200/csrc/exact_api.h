@@ -1,6 +1,6 @@
-// exact_api.h -- host-side launchers of the kernels compiled into exact.cu (the speculative
-// resolve k_spec and the exact radix path it launches from the device).  exact.cu is compiled
-// with -rdc (dynamic parallelism); abi.cu, which holds the hot scoring kernels, is not.
+// exact_api.h -- host-side launchers of the kernels compiled into exact.cu: the speculative
+// resolve (k_spec, k_spec_big) and the exact radix path the host runs when the speculation
+// cannot be exact.
 #pragma once
 #include <cuda_runtime.h>
 #include "select.cuh"
