@@ -145,28 +145,29 @@ static __device__ __noinline__ void spec_fast(const Pool& P, const Cfg& c, Ctrl*
     const bool own = tid < n;
     const uint64_t img = own ? el.img : kNone;
     const uint32_t id = el.id, cost = own ? el.cost : 0u, len = el.len;
+    __shared__ uint32_t f_rank2[kSpecFast];
+    __shared__ unsigned long long f_pre2[kSpecFast];
     if (own) {
         f_rec[tid] = make_ulonglong2(img, (uint64_t)id | ((uint64_t)cost << 32));
         f_img[tid] = img; f_id[tid] = id; f_cost[tid] = cost;
+        f_rank2[tid] = 0; f_pre2[tid] = 0;
     }
     if (tid == 0) { f_fb = 0; f_bp_img = kNone; }
     __syncthreads();
     stamp(ctrl, 2);
-    // (a7) rank in the priority order and inclusive cost prefix: element i is counted by threads i
-    // (first half of the set) and i + kSpecFast (second half) when the CTA has 2 * kSpecFast
-    // threads, else by thread i alone; 16-B broadcast reads, 2 accumulators
-    constexpr bool kSplit = NT >= 2 * kSpecFast;
-    __shared__ uint32_t f_rank2[kSpecFast];
-    __shared__ unsigned long long f_pre2[kSpecFast];
+    // (a7) rank in the priority order and inclusive cost prefix.  The n^2 comparisons are spread
+    // over the whole CTA: element e is counted by F = NT / n threads (tid = e + n * part), each
+    // over a 1/F share of the set (16-B broadcast reads, 2 accumulators), summed in shared memory.
     {
-        const uint32_t e = tid & (kSpecFast - 1), half = kSplit ? tid / kSpecFast : (tid < kSpecFast ? 0u : 2u);
-        const uint32_t j0 = half == 1 ? n / 2 : 0, j1 = half == 1 ? n : (kSplit ? n / 2 : n);
-        uint32_t ra = 0, rb = 0;
-        uint64_t pa = 0, pb = 0;
-        if (e < n && half < 2) {
+        const uint32_t F = n ? min(NT / n, 8u) : 1u;
+        const uint32_t e = n ? tid % n : 0u, part = n ? tid / n : 1u;
+        if (part < F) {
+            const uint32_t j0 = (uint32_t)((uint64_t)n * part / F), j1 = (uint32_t)((uint64_t)n * (part + 1) / F);
             const ulonglong2 me = f_rec[e];
             const uint64_t mi = me.x;
             const uint32_t md = (uint32_t)me.y;
+            uint32_t ra = 0, rb = 0;
+            uint64_t pa = 0, pb = 0;
             uint32_t j = j0;
             for (; j + 1 < j1; j += 2) {
                 const ulonglong2 q0 = f_rec[j], q1 = f_rec[j + 1];
@@ -180,12 +181,10 @@ static __device__ __noinline__ void spec_fast(const Pool& P, const Cfg& c, Ctrl*
                 const bool b0 = q0.x > mi || (q0.x == mi && (uint32_t)q0.y < md);
                 ra += b0; pa += b0 ? (q0.y >> 32) : 0ull;
             }
-            if (half == 1) { f_rank2[e] = ra + rb; f_pre2[e] = pa + pb; }
+            if (F == 1) { f_rank2[e] = ra + rb; f_pre2[e] = pa + pb; }
+            else { atomicAdd(&f_rank2[e], ra + rb); atomicAdd(&f_pre2[e], (unsigned long long)(pa + pb)); }
         }
         __syncthreads();
-        ra += rb; pa += pb;
-        if (kSplit && half == 0 && e < n) { ra += f_rank2[e]; pa += f_pre2[e]; }
-        if (half == 0) { f_rank2[e] = ra; f_pre2[e] = pa; }
     }
     uint32_t rank = own ? f_rank2[tid] : 0u;          // own => tid < kSpecFast: written by itself
     const uint64_t pre = own ? f_pre2[tid] + cost : 0ull;
@@ -216,20 +215,22 @@ static __device__ __noinline__ void spec_fast(const Pool& P, const Cfg& c, Ctrl*
     const bool cd = own && img >= thr_img;
     const uint64_t wk = ((uint64_t)len << 32) | id;
     if (tid < kSpecFast) f_wk[tid] = cd ? wk : ~0ull;
+    if (own) f_rank2[tid] = 0;                             // reused for the window positions
     const uint32_t ncd = (uint32_t)__syncthreads_count(cd);
-    {   // window position of each Cd element (two threads per element when the CTA is large)
-        const uint32_t e = tid & (kSpecFast - 1), half = kSplit ? tid / kSpecFast : (tid < kSpecFast ? 0u : 2u);
-        const uint32_t j0 = half == 1 ? n / 2 : 0, j1 = half == 1 ? n : (kSplit ? n / 2 : n);
-        const uint64_t mk = (e < n && half < 2) ? f_wk[e] : ~0ull;
-        uint32_t pa = 0, pb = 0;
+    {   // window position of each Cd element: #{Cd elements before it in (len, id) order}, the
+        // comparisons spread over the CTA as above
+        const uint32_t F = n ? min(NT / n, 8u) : 1u;
+        const uint32_t e = n ? tid % n : 0u, part = n ? tid / n : 1u;
+        const uint64_t mk = (part < F && e < n) ? f_wk[e] : ~0ull;
         if (mk != ~0ull) {
-            uint32_t j = j0;
+            const uint32_t j0 = (uint32_t)((uint64_t)n * part / F), j1 = (uint32_t)((uint64_t)n * (part + 1) / F);
+            uint32_t pa = 0, pb = 0, j = j0;
             for (; j + 1 < j1; j += 2) { pa += f_wk[j] < mk; pb += f_wk[j + 1] < mk; }
             if (j < j1) pa += f_wk[j] < mk;
-            if (half == 1) f_rank2[e] = pa + pb;
+            if (F == 1) f_rank2[e] = pa + pb; else atomicAdd(&f_rank2[e], pa + pb);
         }
         __syncthreads();
-        if (half == 0 && mk != ~0ull) o_elem[pa + pb + (kSplit ? f_rank2[e] : 0u)] = e;
+        if (cd) o_elem[f_rank2[tid]] = tid;
     }
     __shared__ uint32_t f_row[kSpecFast], f_meta[kSpecFast], f_aux[kSpecFast];
     if (own) { f_row[tid] = el.row; f_meta[tid] = el.meta; f_aux[tid] = el.aux; }
