@@ -130,7 +130,8 @@ static void carve(Carve& cv, const jit_config* cfg, const jit_len_table* tab, Po
     S.spec_meta = cv.take<uint32_t>(kSpecCap); S.spec_aux = cv.take<uint32_t>(kSpecCap);
     S.persist = cv.take<Persist>(1);
     S.spec_cnt = cv.take<unsigned int>(1);
-    S.part = cv.take<BlockPart>(N / kTile + NT + 2);   // one per k_score CTA (<= work items)
+    S.part = cv.take<BlockPart>(1);
+    S.gpart = cv.take<BlockPart>(1);
     S.crange = cv.take<CRange>(NT + 1);
     ctrl = cv.take<Ctrl>(1);
     stage = cv.take<uint32_t>(4 * N);
@@ -238,6 +239,9 @@ extern "C" int jit_sched_init(const jit_config* cfg, const jit_slo_group* groups
         Persist ps{};
         ps.t_guess = kNone;                 // no speculation before the first resolved step
         CK(cudaMemcpyAsync(h->S.persist, &ps, sizeof ps, cudaMemcpyHostToDevice, h->stream));
+        BlockPart g{};
+        g.min_img = kNone;                  // the empty step record (k_spec resets it after reading)
+        CK(cudaMemcpyAsync(h->S.gpart, &g, sizeof g, cudaMemcpyHostToDevice, h->stream));
     }
     CK(cudaStreamSynchronize(h->stream));
     return JIT_OK;

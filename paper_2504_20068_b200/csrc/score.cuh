@@ -34,8 +34,9 @@ __device__ __forceinline__ void spec_add(const Scratch& S, const uint32_t* ids, 
     }
 }
 
-// block reduction of the per-thread partials into part[blockIdx.x]
-__device__ __forceinline__ void store_part(BlockPart* part, uint32_t pend, uint32_t drop, uint32_t err,
+// block reduction of the per-thread partials, then one set of atomics per CTA into the step's
+// global accumulator (read and reset by k_spec: a single record instead of one per CTA)
+__device__ __forceinline__ void store_part(BlockPart* gpart, uint32_t pend, uint32_t drop, uint32_t err,
                                            uint64_t mn, uint64_t cost, uint32_t refresh) {
     __shared__ unsigned long long s_min, s_cost;
     __shared__ uint32_t s_pend, s_drop, s_err, s_ref;
@@ -49,10 +50,12 @@ __device__ __forceinline__ void store_part(BlockPart* part, uint32_t pend, uint3
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        BlockPart b;
-        b.min_img = s_min; b.tot_cost = s_cost; b.n_pending = s_pend; b.n_dropped = s_drop; b.err = s_err;
-        b.refresh = s_ref;
-        part[blockIdx.x] = b;
+        if (s_min != kNone) atomicMin(&gpart->min_img, s_min);
+        if (s_cost) atomicAdd(&gpart->tot_cost, s_cost);
+        if (s_pend) atomicAdd(&gpart->n_pending, s_pend);
+        if (s_drop) atomicAdd(&gpart->n_dropped, s_drop);
+        if (s_err) atomicOr(&gpart->err, s_err);
+        if (s_ref) atomicAdd(&gpart->refresh, s_ref);
     }
 }
 
@@ -332,7 +335,7 @@ static __device__ __noinline__ void spec_fast(const Pool& P, const Cfg& c, Ctrl*
 //     second kernel.  A range wider than one tile (a single task > kTile calls) is read from
 //     global memory and parks the frame count in the key slot between A and C.
 // Every row whose key image reaches the speculative threshold joins the speculative set; per-CTA
-// partial counts go to S.part[blockIdx.x] (no global atomics on a shared line).
+// partial counts are reduced per CTA, then added atomically into one global record.
 // --------------------------------------------------------------------------------------
 #ifndef JIT_EXACT_TU
 #ifndef JIT_SCORE_MINB
@@ -830,7 +833,7 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
     {
         const uint64_t md = (uint64_t)__double_as_longlong(A.mn_d);
         const uint64_t m_std = A.mn_d == A.mn_d ? md : kNone;    // NaN: no pending standalone row
-        store_part(S.part, A.pend, A.drop, A.err, m_std < A.mn ? m_std : A.mn, A.cost, A.ref);
+        store_part(S.gpart, A.pend, A.drop, A.err, m_std < A.mn ? m_std : A.mn, A.cost, A.ref);
     }
 }
 #endif  // !JIT_EXACT_TU
@@ -946,10 +949,14 @@ static __device__ void spec_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const 
     {   // partials of k_score, and (1) the set -> smem + histogram, in one pass
         uint32_t pend = 0, drop = 0, err = 0, ref = 0;
         uint64_t mn = kNone, cost = 0;
-        for (uint32_t i = tid; i < S.n_part; i += kSpecThreads) {
-            const BlockPart b = S.part[i];
-            pend += b.n_pending; drop += b.n_dropped; err |= b.err; cost += b.tot_cost; ref += b.refresh;
-            if (b.min_img < mn) mn = b.min_img;
+        if (kBig) {                                        // k_spec already reduced them into ctrl
+            if (tid == 0) { pend = ctrl->n_pending; drop = ctrl->n_dropped; mn = ctrl->min_img; cost = ctrl->tot_cost;
+                            ref = ctrl->n_refresh; }
+        } else if (tid == 0) {                             // k_score's global record; reset for the next step
+            BlockPart* g = S.gpart;
+            pend = __ldcg(&g->n_pending); drop = __ldcg(&g->n_dropped); err = __ldcg(&g->err);
+            cost = __ldcg(&g->tot_cost); ref = __ldcg(&g->refresh); mn = __ldcg(&g->min_img);
+            g->n_pending = 0; g->n_dropped = 0; g->err = 0; g->tot_cost = 0; g->refresh = 0; g->min_img = kNone;
         }
         if (kBig) {
             for (uint32_t i = tid; i < n; i += kSpecThreads) {

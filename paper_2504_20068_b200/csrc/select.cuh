@@ -131,7 +131,8 @@ struct Scratch {
     uint64_t* spec_img;
     uint32_t *spec_id, *spec_row, *spec_cost, *spec_len, *spec_meta, *spec_aux;
     Persist* persist;
-    BlockPart* part;         // k_score partials (one per CTA: n_part)
+    BlockPart* part;         // (unused)
+    BlockPart* gpart;        // the step's k_score partials, reduced atomically (reset by k_spec)
     const CRange* crange;    // compound CTA ranges (n_crange)
     uint32_t n_part, n_std, n_crange, pad3;   // partials = k_score CTAs; items = n_std tiles + ranges
     unsigned int* spec_cnt;  // size of the speculative set (k_score atomics; reset by k_spec)
