@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-replay", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: exercise the N>1 code path with all ranks on one GPU (test mode; the "
+                         "exchange goes through host memory, numbers are not NVLink numbers)")
     return ap.parse_args()
 
 
@@ -226,6 +229,7 @@ def run_sharded(args, ws, rank, dev, stream, barrier, allmax, allsum):
     weak scaling); every step is the exact two-round protocol of shard.cuh with NCCL
     allgathers over NVLink (torch.distributed), identical batch on every rank."""
     import torch
+    import torch.distributed as dist
     from paper_2504_20068_b200 import Scheduler
     from paper_2504_20068_b200.sharded import ShardedStep, nccl_allgather
     d = build_c3(rank, args.rows)
@@ -236,10 +240,19 @@ def run_sharded(args, ws, rank, dev, stream, barrier, allmax, allsum):
     cap = max(n, ws * (d["cfg"]["max_batch"] + 1))
     s = Scheduler(d["cfg"], d["groups"], d["table"], capacity=cap, task_capacity=nt, device=dev, stream=stream)
     s.load(d["pool"], d["tasks"])
-    st = ShardedStep(s, rank, ws, nccl_allgather())
+    if args.backend == "gloo":
+        def gather(t):                                   # test mode: through host memory
+            c = t.cpu()
+            out = [torch.empty_like(c) for _ in range(ws)]
+            dist.all_gather(out, c)
+            return torch.cat(out).to(t.device)
+        st = ShardedStep(s, rank, ws, gather)
+    else:
+        st = ShardedStep(s, rank, ws, nccl_allgather())
     K, Wm = args.steps, max(3, args.warmup)
     for _ in range(Wm):
         out = st.step(now, v)
+    st.n_fast = st.n_exact = 0
     barrier()
     torch.cuda.synchronize()
     clk = Clocks(dev)
@@ -263,13 +276,15 @@ def run_sharded(args, ws, rank, dev, stream, barrier, allmax, allsum):
                 "config": {"workload": f"C5(ii)-shaped: {ws} x 2^20-row shards of one pool (C3 generator), sharded by "
                                        "request id, tau 8192, B_max 8192", "rows_total": int(total),
                            "l2": "inputs larger than L2 (2^20 rows x ~100 B workspace per rank plus exchange buffers)",
-                           "parallelism": f"sharded pool, exact 2-round NCCL allgather merge over {ws} ranks",
+                           "parallelism": f"sharded pool over {ws} ranks: speculative sets allgathered over NCCL and "
+                                          "resolved identically on every rank (exact 2-round protocol as fallback)",
+                           "steps_speculative": st.n_fast, "steps_exact_protocol": st.n_exact,
                            "last_batch": {"n_selected": out["n_selected"], "b_star": out["b_star"],
                                           "n_candidates": out["n_candidates"]}},
-                "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": 18 * K, "clocks": clocks,
+                "roofline": None, "cpu_baseline": None, "e2e": None,
+                "gpu_launches": 3 * st.n_fast + 18 * st.n_exact, "clocks": clocks,
                 "replay": replay}
         print(json.dumps(line), flush=True)
-    import torch.distributed as dist
     dist.destroy_process_group()
 
 
@@ -281,9 +296,14 @@ def main():
         return
     import torch
     import torch.distributed as dist
+    if args.backend == "gloo":
+        local = 0                                        # test mode: every rank on GPU 0
     torch.cuda.set_device(local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     from paper_2504_20068_b200 import Scheduler
     dev = local
     stream = torch.cuda.current_stream(dev)
@@ -292,17 +312,19 @@ def main():
         if ws > 1:
             dist.barrier()
 
+    red_dev = "cpu" if args.backend == "gloo" else f"cuda:{dev}"
+
     def allmax(x):
         if ws == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def allsum(x):
         if ws == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 

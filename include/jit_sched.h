@@ -42,6 +42,7 @@ extern "C" {
 enum {
     JIT_OK = 0,
     JIT_EMPTY = 1,        /* no pending request (SPEC EmptyQueue); n_selected = 0 */
+    JIT_RETRY = 2,        /* jit_shard_spec_resolve only: resolve this step with the exact protocol */
     JIT_EINVAL = -1,      /* bad config / table / pool (S:55-63 InvalidLength, ConfigError) */
     JIT_ETRACE = -2,      /* bad replay trace (S:417 InvalidTrace) */
     JIT_ECAPACITY = -3,   /* more rows / tasks / candidates than the workspace was sized for */
@@ -273,6 +274,26 @@ typedef struct jit_rec1 { uint64_t img; uint32_t id, cost; } jit_rec1;
 typedef struct jit_rec2 { uint64_t img; uint32_t id, cost, len, row, rank, reserved; } jit_rec2;
 
 int jit_shard_prefix(jit_sched* h, int64_t now_ns, int64_t v_token_ns, void* d_rec1, uint32_t cap, uint32_t* n_out);
+
+/* Fast sharded step (the speculative resolve of DESIGN.md §7 across ranks), tried first:
+ *   jit_shard_spec_export   (a1)-(a6) on the shard, then writes jit_shard_spec_bytes() bytes to
+ *                           d_out (device): a 64-byte header (the shard's pending count, cost sum,
+ *                           min key, errors, set size) and the shard's speculative set
+ *                           {key >= t} as 32-byte records (at most 1024; asynchronous).
+ *   -- allgather the W exports in rank order (W * jit_shard_spec_bytes() bytes) --
+ *   jit_shard_spec_resolve  every rank resolves the union: all ranks share the threshold t (they
+ *                           resolved the same previous step), so the union of the local sets is
+ *                           the global speculative set, a prefix of the global priority order,
+ *                           and the exactness checks of the single-GPU resolve apply with the
+ *                           global pending count.  Returns JIT_OK / JIT_EMPTY with the batch
+ *                           (identical on every rank; bookkeeping on the owner's rows;
+ *                           out->rows[i] = 0xFFFFFFFF for another rank's request), or JIT_RETRY:
+ *                           the set is too large or a check failed -- continue this step with
+ *                           jit_shard_prefix ... jit_shard_finish (the keys are not recomputed). */
+uint32_t jit_shard_spec_bytes(void);
+int jit_shard_spec_export(jit_sched* h, int64_t now_ns, int64_t v_token_ns, void* d_out, uint32_t cap_bytes,
+                          uint32_t rank);
+int jit_shard_spec_resolve(jit_sched* h, const void* d_all, uint32_t world, uint32_t rank, jit_batch* out);
 int jit_shard_merge(jit_sched* h, const void* d_all_rec1, uint32_t n_all);
 int jit_shard_candidates(jit_sched* h, void* d_rec2, uint32_t cap, uint32_t rank, uint32_t* n_out);
 int jit_shard_finish(jit_sched* h, const void* d_all_rec2, uint32_t n_all, uint32_t rank, jit_batch* out);

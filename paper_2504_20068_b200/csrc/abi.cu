@@ -45,6 +45,7 @@ struct jit_sched {
     uint32_t arg_ntasks = 0;
     int64_t arg_now = 0, arg_v = 0;
     bool loaded = false, graph_dirty = true, timing = false, debug = false, pdl = true;
+    bool keys_ready = false;          // k_score already ran this step (fast sharded attempt)
     cudaEvent_t ev[6] = {};
     cudaGraphNode_t ev_node[5] = {};      // event-record nodes of the timed graph
     std::vector<cudaEvent_t> slots;       // 5 events per recorded step
@@ -682,10 +683,13 @@ extern "C" int jit_shard_prefix(jit_sched* h, int64_t now_ns, int64_t v_token_ns
     cudaStream_t s = h->stream;
     Pool& P = h->P;
     Scratch& S = h->S;
-    enqueue_score(h, s, now_ns, v_token_ns);
-    // k_spec only reduces the scoring partials (n_pending, min key, ...): the round-1 export
-    // needs the full radix resolve below
-    CK(exact::spec(P, h->c, h->d_ctrl, S, 1, s, false));
+    if (!h->keys_ready) {
+        enqueue_score(h, s, now_ns, v_token_ns);
+        // k_spec only reduces the scoring partials (n_pending, min key, ...): the round-1 export
+        // needs the full radix resolve below
+        CK(exact::spec(P, h->c, h->d_ctrl, S, 1, s, false));
+    }
+    h->keys_ready = false;                 // (after a failed fast attempt the keys are this step's)
     exact::hist0(P, h->c, h->d_ctrl, S, h->grid_pass, 1, s);
     for (uint32_t i = 0; i < kLevels - 1; ++i) exact::pass(P, h->c, h->d_ctrl, S, h->grid_pass, i, s);
     exact::compact(P, h->c, h->d_ctrl, S, h->grid_pass, s);
@@ -699,6 +703,34 @@ extern "C" int jit_shard_prefix(jit_sched* h, int64_t now_ns, int64_t v_token_ns
     if (c.status == ST_ERROR || c.error || c.cand_overflow) return set_err(h, JIT_EINVAL, "shard_prefix failed (%u)", c.error);
     *n_out = c.status == ST_RESOLVED ? c.n_cand : 0;
     return c.status == ST_EMPTY ? JIT_EMPTY : JIT_OK;
+}
+
+// fast sharded step (speculative sets; see k_spec_export / k_spec_merge)
+extern "C" uint32_t jit_shard_spec_bytes(void) { return exact::spec_export_bytes(); }
+
+extern "C" int jit_shard_spec_export(jit_sched* h, int64_t now_ns, int64_t v_token_ns, void* d_out, uint32_t cap_bytes,
+                                     uint32_t rank) {
+    if (!h || !d_out) return JIT_EINVAL;
+    if (!h->loaded) return set_err(h, JIT_ESTATE, "shard_spec_export before load");
+    if (v_token_ns <= 0) return set_err(h, JIT_EINVAL, "v_token must be > 0");
+    if (cap_bytes < exact::spec_export_bytes()) return set_err(h, JIT_ECAPACITY, "export buffer needs %u bytes",
+                                                                exact::spec_export_bytes());
+    enqueue_score(h, h->stream, now_ns, v_token_ns);
+    CK(exact::spec_export(h->S, h->d_ctrl, d_out, rank, h->stream));
+    h->keys_ready = true;
+    return JIT_OK;
+}
+
+extern "C" int jit_shard_spec_resolve(jit_sched* h, const void* d_all, uint32_t world, uint32_t rank, jit_batch* out) {
+    if (!h || !d_all || world == 0 || world > 64 || rank >= world) return JIT_EINVAL;
+    if (!h->keys_ready) return set_err(h, JIT_ESTATE, "shard_spec_resolve without shard_spec_export");
+    CK(exact::spec_merge(h->P, h->c, h->d_ctrl, h->S, d_all, world, rank, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    const Ctrl& c = *h->h_ctrl;
+    if (c.status == ST_FALLBACK) return JIT_RETRY;          // keys stay: jit_shard_prefix continues
+    h->keys_ready = false;
+    if (out) { out->fallback = 0; }
+    return finish_step(h, out);
 }
 
 extern "C" int jit_shard_merge(jit_sched* h, const void* d_all_rec1, uint32_t n_all) {

@@ -21,6 +21,8 @@ cudaError_t init_attributes() {
         cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(k_spec_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSpecSmem)) !=
         cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(k_spec_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSpecSmem)) !=
+        cudaSuccess) return e;
     // one shared-memory carveout for every kernel of the step (see abi.cu)
     const void* ks[] = {(const void*)k_spec, (const void*)k_spec_big,
                         (const void*)k_hist0, (const void*)k_pass, (const void*)k_compact, (const void*)k_resolve,
@@ -40,6 +42,16 @@ cudaError_t spec(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int 
     cfg.attrs = at; cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, k_spec, P, c, ctrl, S, reduce_only);
 }
+cudaError_t spec_export(const Scratch& S, Ctrl* ctrl, void* out, uint32_t rank, cudaStream_t s) {
+    k_spec_export<<<1, kSpecThreads, 0, s>>>(ctrl, S, reinterpret_cast<unsigned char*>(out), rank);
+    return cudaGetLastError();
+}
+cudaError_t spec_merge(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, const void* all, uint32_t world,
+                       uint32_t rank, cudaStream_t s) {
+    k_spec_merge<<<1, kSpecThreads, kSpecSmem, s>>>(P, c, ctrl, S, reinterpret_cast<const unsigned char*>(all), world, rank);
+    return cudaGetLastError();
+}
+uint32_t spec_export_bytes() { return kSpecExportBytes; }
 void spec_big(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, cudaStream_t s) {
     k_spec_big<<<1, kSpecThreads, kSpecSmem, s>>>(P, c, ctrl, S);
 }

@@ -16,6 +16,12 @@ cudaError_t init_attributes();
 // publishes the control block to pinned host memory.  pdl: programmatic dependent launch after
 // k_score (its launch overlaps k_score; it waits with griddepcontrol.wait)
 cudaError_t spec(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int reduce_only, cudaStream_t s, bool pdl);
+// fast sharded step: export this rank's speculative set + totals (after k_score), and resolve the
+// allgathered union on every rank (status FALLBACK: run the exact two-round protocol)
+cudaError_t spec_export(const Scratch& S, Ctrl* ctrl, void* out, uint32_t rank, cudaStream_t s);
+cudaError_t spec_merge(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, const void* all, uint32_t world,
+                       uint32_t rank, cudaStream_t s);
+uint32_t spec_export_bytes();
 // k_spec_big: the resolve of a speculative set larger than k_spec's fast path (status ST_SPEC_BIG)
 void spec_big(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, cudaStream_t s);
 void hist0(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t grid, int force, cudaStream_t s);

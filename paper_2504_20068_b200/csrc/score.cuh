@@ -124,6 +124,7 @@ constexpr uint32_t kSpecFast = 256;
 struct SpecEl {                 // one element of the speculative set, preloaded by k_spec
     uint64_t img;
     uint32_t id, cost, len, row, meta, aux;
+    uint32_t own;               // 1: the row belongs to this handle (a sharded step merges all ranks' sets)
 };
 template <uint32_t NT>
 static __device__ __noinline__ void spec_fast(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t n,
@@ -236,7 +237,7 @@ static __device__ __noinline__ void spec_fast(const Pool& P, const Cfg& c, Ctrl*
         if (cd) o_elem[f_rank2[tid]] = tid;
     }
     __shared__ uint32_t f_row[kSpecFast], f_meta[kSpecFast], f_aux[kSpecFast];
-    if (own) { f_row[tid] = el.row; f_meta[tid] = el.meta; f_aux[tid] = el.aux; }
+    if (own) { f_row[tid] = el.own ? el.row : 0xFFFFFFFFu; f_meta[tid] = el.meta; f_aux[tid] = el.aux; }
     if (tid == 0) { ctrl->n_cand = ncd; ctrl->status = ST_RESOLVED; }
     __syncthreads();
     stamp(ctrl, 4);
@@ -302,11 +303,13 @@ static __device__ __noinline__ void spec_fast(const Pool& P, const Cfg& c, Ctrl*
         S.out_rows[tid] = r;
         const uint32_t B = c.max_batch + 1;                 // and the pinned host mirror (no D2H copy)
         S.h_batch[tid] = f_id[e]; S.h_batch[B + tid] = f_cost[e]; S.h_batch[2 * B + tid] = r;
-        uint32_t mt = f_meta[e] | (kEver << 12);            // meta / aux as k_score left them (preloaded)
-        if (m_state(mt) == kQueued || m_state(mt) == kPreempted) mt = m_with_state(mt, kRunning);
-        P.meta[r] = mt;
-        const uint32_t aux = f_aux[e];
-        if ((aux >> 16) < 0xFFFFu) P.aux[r] = aux - (1u << 16);
+        if (r != 0xFFFFFFFFu) {                             // bookkeeping of this handle's rows
+            uint32_t mt = f_meta[e] | (kEver << 12);        // meta / aux as k_score left them (preloaded)
+            if (m_state(mt) == kQueued || m_state(mt) == kPreempted) mt = m_with_state(mt, kRunning);
+            P.meta[r] = mt;
+            const uint32_t aux = f_aux[e];
+            if ((aux >> 16) < 0xFFFFu) P.aux[r] = aux - (1u << 16);
+        }
     }
     if (tid == 0) {
         ctrl->n_selected = ns;
@@ -889,7 +892,7 @@ constexpr uint64_t kPackCount = 1ull << 48;   // histogram word: count << 48 | c
 
 template <bool kBig>
 static __device__ void spec_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int reduce_only,
-                                 unsigned char* smem);
+                                 unsigned char* smem, bool merged = false);
 // the step's last kernel: resolve a small speculative set (the steady state), then publish the
 // control block to pinned host memory.  Its code is kept small on purpose: it runs on one SM
 // once per step, so every instruction-cache line it touches is a miss to L2 / HBM; a larger set
@@ -906,9 +909,113 @@ __global__ void __launch_bounds__(kSpecThreads) k_spec_big(Pool P, Cfg c, Ctrl* 
     publish_ctrl(ctrl, S.h_ctrl);
 }
 
+// ---- fast sharded step (the speculative variant): every rank scores its shard and
+// exports its speculative set; after an allgather every rank resolves the union exactly like
+// k_spec.  All ranks share the threshold t (they resolved the same previous step), so the union
+// of the local sets {key >= t} IS the global speculative set and the exactness checks carry over
+// with the global pending count.  Anything else (a set too large, a failed check) falls back to
+// the exact two-round protocol (shard.cuh) without rescoring.
+struct SpecHdr {                 // first 64 B of a rank's export
+    unsigned long long min_img, tot_cost;
+    uint32_t n_pending, n_dropped, err, refresh, n_set, rank, pad[6];
+};
+struct SpecRec {                 // 32 B per element
+    unsigned long long img;
+    uint32_t id, cost, len, row, meta, aux;
+};
+constexpr uint32_t kSpecExportCap = 1024;        // records per rank
+constexpr uint32_t kSpecExportBytes = 64 + 32 * kSpecExportCap;
+static_assert(sizeof(SpecHdr) == 64 && sizeof(SpecRec) == 32, "export layout");
+
+__global__ void __launch_bounds__(kSpecThreads) k_spec_export(Ctrl* ctrl, Scratch S, unsigned char* out, uint32_t rank) {
+    const uint32_t tid = threadIdx.x;
+    const uint32_t n_set = *reinterpret_cast<volatile unsigned int*>(S.spec_cnt);
+    SpecRec* rec = reinterpret_cast<SpecRec*>(out + 64);
+    for (uint32_t i = tid; i < kSpecExportCap; i += blockDim.x) {
+        SpecRec q;
+        if (i < n_set && n_set <= kSpecExportCap) {
+            q.img = S.spec_img[i]; q.id = S.spec_id[i]; q.cost = S.spec_cost[i]; q.len = S.spec_len[i];
+            q.row = S.spec_row[i]; q.meta = S.spec_meta[i]; q.aux = S.spec_aux[i];
+        } else {
+            q.img = kNone; q.id = q.cost = q.len = q.row = q.meta = q.aux = 0;
+        }
+        rec[i] = q;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        BlockPart* g = S.gpart;
+        SpecHdr hd{};
+        hd.min_img = __ldcg(&g->min_img); hd.tot_cost = __ldcg(&g->tot_cost); hd.n_pending = __ldcg(&g->n_pending);
+        hd.n_dropped = __ldcg(&g->n_dropped); hd.err = __ldcg(&g->err); hd.refresh = __ldcg(&g->refresh);
+        hd.n_set = n_set; hd.rank = rank;
+        *reinterpret_cast<SpecHdr*>(out) = hd;
+        // this rank's own totals, as k_spec(reduce_only) would leave them for the exact protocol
+        ctrl->n_pending = hd.n_pending; ctrl->n_dropped = hd.n_dropped; ctrl->min_img = hd.min_img;
+        ctrl->tot_cost = hd.tot_cost; ctrl->n_refresh = hd.refresh; ctrl->spec_n = n_set;
+        if (hd.err) ctrl->error |= 1u;
+        g->n_pending = 0; g->n_dropped = 0; g->err = 0; g->tot_cost = 0; g->refresh = 0; g->min_img = kNone;
+        *S.spec_cnt = 0;
+    }
+}
+
+__global__ void __launch_bounds__(kSpecThreads) k_spec_merge(Pool P, Cfg c, Ctrl* ctrl, Scratch S, const unsigned char* all,
+                                                             uint32_t world, uint32_t rank) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint32_t m_off[65], m_pend, m_err, m_fb;
+    __shared__ unsigned long long m_min;
+    const uint32_t tid = threadIdx.x;
+    if (tid == 0) {
+        uint32_t off = 0, pend = 0, err = 0, big = 0;
+        unsigned long long mn = kNone;
+        for (uint32_t w = 0; w < world; ++w) {
+            const SpecHdr* hd = reinterpret_cast<const SpecHdr*>(all + (size_t)w * kSpecExportBytes);
+            m_off[w] = off;
+            off += hd->n_set; pend += hd->n_pending; err |= hd->err; big |= hd->n_set > kSpecExportCap;
+            if (hd->min_img < mn) mn = hd->min_img;
+        }
+        m_off[world] = off; m_pend = pend; m_err = err; m_min = mn;
+        // a rank whose own set overflowed its export, or nothing to resolve: the exact protocol
+        m_fb = (err || pend == 0 || off == 0 || off > kSpecCap || big) ? 1u : 0u;
+        ctrl->spec_n = off;
+        if (m_fb) { ctrl->status = (err ? ST_ERROR : pend == 0 ? ST_EMPTY : ST_FALLBACK); if (err) ctrl->error |= 1u; }
+    }
+    __syncthreads();
+    if (m_fb) { publish_ctrl(ctrl, S.h_ctrl); return; }
+    if (m_off[world] > kSpecFast) {
+        // a larger union: copy it into this handle's speculative-set arrays (another rank's rows
+        // get row = ~0) and resolve it with k_spec_big's histogram path
+        const uint32_t n = m_off[world];
+        for (uint32_t i = tid; i < n; i += kSpecThreads) {
+            uint32_t w = 0;
+            while (m_off[w + 1] <= i) ++w;
+            const SpecRec q = reinterpret_cast<const SpecRec*>(all + (size_t)w * kSpecExportBytes + 64)[i - m_off[w]];
+            S.spec_img[i] = q.img; S.spec_id[i] = q.id; S.spec_cost[i] = q.cost; S.spec_len[i] = q.len;
+            S.spec_row[i] = (w == rank) ? q.row : 0xFFFFFFFFu;
+        }
+        if (tid == 0) { ctrl->n_pending = m_pend; ctrl->min_img = m_min; ctrl->spec_n = n; }
+        __syncthreads();
+        spec_body<true>(P, c, ctrl, S, 0, smem, true);
+        publish_ctrl(ctrl, S.h_ctrl);
+        return;
+    }
+    // element tid of the union: rank w = the one whose range holds tid (ranks in order)
+    SpecEl el{kNone, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    const uint32_t n = m_off[world];
+    if (tid < n) {
+        uint32_t w = 0;
+        while (m_off[w + 1] <= tid) ++w;
+        const SpecRec q = reinterpret_cast<const SpecRec*>(all + (size_t)w * kSpecExportBytes + 64)[tid - m_off[w]];
+        el.img = q.img; el.id = q.id; el.cost = q.cost; el.len = q.len; el.row = q.row; el.meta = q.meta; el.aux = q.aux;
+        el.own = (w == rank) ? 1u : 0u;
+    }
+    if (tid == 0) { ctrl->n_pending = m_pend; ctrl->min_img = m_min; }
+    spec_fast<kSpecThreads>(P, c, ctrl, S, n, n == m_pend, S.persist->t_guess, m_min, el, smem);
+    publish_ctrl(ctrl, S.h_ctrl);
+}
+
 template <bool kBig>
 static __device__ void spec_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int reduce_only,
-                                 unsigned char* smem) {
+                                 unsigned char* smem, bool merged) {
     uint64_t* s_img = reinterpret_cast<uint64_t*>(smem + kSpImgOff);
     uint32_t* s_cost = reinterpret_cast<uint32_t*>(smem + kSpCostOff);
     unsigned long long* s_hist = reinterpret_cast<unsigned long long*>(smem + kSpHistOff);
@@ -931,7 +1038,7 @@ static __device__ void spec_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const 
     // every thread reads the set size, and in the steady state (small set) its own element and the
     // element's meta / aux right away: these loads overlap the partials' reduction below
     const uint32_t n_set = kBig ? ctrl->spec_n : *reinterpret_cast<volatile unsigned int*>(S.spec_cnt);
-    SpecEl el{kNone, 0u, 0u, 0u, 0u, 0u, 0u};
+    SpecEl el{kNone, 0u, 0u, 0u, 0u, 0u, 0u, 1u};
     if (!kBig && !reduce_only && n_set <= kSpecFast && tid < n_set) {
         el.img = S.spec_img[tid]; el.id = S.spec_id[tid]; el.cost = S.spec_cost[tid]; el.len = S.spec_len[tid];
         el.row = S.spec_row[tid]; el.meta = S.spec_meta[tid]; el.aux = S.spec_aux[tid];
@@ -1137,6 +1244,10 @@ static __device__ void spec_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const 
     __syncthreads();
     const uint32_t ncd = s_ncd;
     if (tid == 0) { ctrl->n_cand = ncd; ctrl->status = ST_RESOLVED; }
+    if (ncd > kSpecWindow && merged) {                     // a sharded union: the exact protocol takes over
+        if (tid == 0) { ctrl->status = ST_FALLBACK; ctrl->fallback = 1; }
+        return;
+    }
     if (ncd > kSpecWindow) {
         // a large Cd: hand it to k_group (launched from here)
         if (tid == 0) s_nsel = 0;
@@ -1235,6 +1346,7 @@ static __device__ void spec_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const 
         S.out_ids[k] = (uint32_t)w_key[j];
         S.out_tokens[k] = w_cost[j];
         S.out_rows[k] = r;
+        if (r == 0xFFFFFFFFu) continue;                     // another rank's request (sharded union)
         uint32_t mt = P.meta[r] | (kEver << 12);
         if (m_state(mt) == kQueued || m_state(mt) == kPreempted) mt = m_with_state(mt, kRunning);
         P.meta[r] = mt;

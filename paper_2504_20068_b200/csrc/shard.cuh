@@ -234,6 +234,8 @@ __global__ void __launch_bounds__(1024) k_group_rec(Pool P, Cfg c, Ctrl* ctrl, S
         ctrl->n_cand = n;
         ctrl->total_tokens = (uint32_t)(S.pc[bj + 1] - S.pc[bi]);
         ctrl->window_done = 1;
+        // next step's speculative threshold (identical on every rank: thr is global)
+        S.persist->t_guess = (unsigned long long)__double_as_longlong(__dmul_rn(ctrl->thr, 0.85));
     }
 }
 

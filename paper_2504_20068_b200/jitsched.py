@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # JITSCHED_LIB: an alternative in-tree build of the same library (tuning variants, profiles/)
 LIB_PATH = os.environ.get("JITSCHED_LIB") or os.path.join(_HERE, "libjitsched.so")
 
-JIT_OK, JIT_EMPTY = 0, 1
+JIT_OK, JIT_EMPTY, JIT_RETRY = 0, 1, 2
 JIT_CFG_DEBUG_ROWS = 1
 JIT_CFG_NO_GRAPH = 2        # env JITSCHED_NO_GRAPH=1: direct launches (for ncu)
 NO_TASK = 0xFFFFFFFF
@@ -109,7 +109,7 @@ EXPORTS = ("jit_sched_workspace_bytes", "jit_sched_init", "jit_sched_load", "jit
            "jit_sched_step_async", "jit_sched_fetch_batch", "jit_sched_read_rows", "jit_sched_kernel_times",
            "jit_replay_workspace_bytes", "jit_sched_replay", "jit_sched_destroy", "jit_sched_last_error",
            "jit_sched_version", "jit_shard_prefix", "jit_shard_merge", "jit_shard_candidates", "jit_shard_finish",
-           "jit_sched_phase_times")
+           "jit_sched_phase_times", "jit_shard_spec_bytes", "jit_shard_spec_export", "jit_shard_spec_resolve")
 
 
 def load_library(path: str = LIB_PATH):
@@ -127,6 +127,7 @@ def load_library(path: str = LIB_PATH):
         for name in EXPORTS:
             if name not in ("jit_sched_last_error", "jit_sched_version", "jit_sched_destroy"):
                 getattr(lib, name).restype = C.c_int
+        lib.jit_shard_spec_bytes.restype = C.c_uint32
         _lib = lib
     return _lib
 
@@ -345,6 +346,25 @@ class Scheduler:
         rc = self._check(self.lib.jit_shard_finish(self.h, C.c_void_p(all_rec2.data_ptr()),
                                                    C.c_uint32(all_rec2.numel() // REC2_BYTES), C.c_uint32(rank),
                                                    C.byref(b)), self.h)
+        return self._batch_dict(rc, b)
+
+    # fast sharded step: speculative-set export / union resolve (None: use the exact protocol)
+    def shard_spec_bytes(self) -> int:
+        return int(self.lib.jit_shard_spec_bytes())
+
+    def shard_spec_export(self, now_ns: int, v_token_ns: int, buf, rank: int):
+        self._check(self.lib.jit_shard_spec_export(self.h, C.c_int64(now_ns), C.c_int64(v_token_ns),
+                                                   C.c_void_p(buf.data_ptr()), C.c_uint32(buf.numel()),
+                                                   C.c_uint32(rank)), self.h)
+
+    def shard_spec_resolve(self, all_buf, world: int, rank: int):
+        b = jit_batch()
+        b.capacity = self.max_batch
+        b.ids, b.tokens, b.rows = _p(self._ids), _p(self._tok), _p(self._rows)
+        rc = self._check(self.lib.jit_shard_spec_resolve(self.h, C.c_void_p(all_buf.data_ptr()), C.c_uint32(world),
+                                                         C.c_uint32(rank), C.byref(b)), self.h)
+        if rc == JIT_RETRY:
+            return None
         return self._batch_dict(rc, b)
 
     # ------------------------------------------------------------------ replay

@@ -1,7 +1,11 @@
 """Exact GMAX step over a request pool sharded across ranks (shard.cuh).
 
 One process per GPU.  Each rank's Scheduler holds its shard (request ids unique across
-ranks).  A step is two rounds, each a fixed-size allgather of records over NCCL/NVLink:
+ranks).  A step first tries the speculative resolve across ranks: each rank exports its
+speculative set {key >= t} (t is the same on every rank), one allgather, and every rank resolves
+the union (jit_shard_spec_export / jit_shard_spec_resolve).  When that cannot be exact (first
+step, a set too large, a failed check) the step continues -- without rescoring -- with the exact
+protocol of two rounds, each a fixed-size allgather of records over NCCL/NVLink:
 
   round 1  jit_shard_prefix  -> first min(B*_r+1, |P_r|) local requests (key desc, id asc)
            allgather         -> every rank: jit_shard_merge -> exact global B*, bp, thr
@@ -40,9 +44,26 @@ class ShardedStep:
         self.rec1 = torch.full(((sched.max_batch + 1) * REC1,), 0xFF, dtype=torch.uint8, device=dev)
         self.rec2 = torch.full((max(sched.capacity, 1) * REC2,), 0xFF, dtype=torch.uint8, device=dev)
         self.cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.fast = hasattr(sched, "shard_spec_export")
+        self.spec = torch.zeros(sched.shard_spec_bytes() if self.fast else 1, dtype=torch.uint8, device=dev)
         self.last = {}
+        self.n_fast = self.n_exact = 0
 
     def step(self, now_ns: int, v_token_ns: int) -> dict:
+        s = self.s
+        if self.fast:
+            # fast path: one allgather of the speculative sets, resolved identically on every rank
+            s.shard_spec_export(now_ns, v_token_ns, self.spec, self.rank)
+            out = s.shard_spec_resolve(self.allgather(self.spec), self.world, self.rank)
+            if out is not None:
+                out["path"] = "speculative"
+                self.n_fast += 1
+                self.last = out
+                return out
+        self.n_exact += 1
+        return self._exact(now_ns, v_token_ns)
+
+    def _exact(self, now_ns: int, v_token_ns: int) -> dict:
         s = self.s
         self.rec1.fill_(0xFF)                                # unused slots: img = ~0 (invalid)
         n1 = s.shard_prefix(now_ns, v_token_ns, self.rec1)
@@ -58,6 +79,7 @@ class ShardedStep:
         out["n_export1"] = n1
         out["n_candidates_local"] = n2
         out["n_candidates"] = int(counts.sum().item())
+        out["path"] = "exact"
         self.last = out
         return out
 
@@ -67,6 +89,16 @@ def virtual_shards_step(steps, now_ns: int, v_token_ns: int):
     allgather is a concatenation of the W ranks' buffers, executed phase by phase."""
     import torch
     W = len(steps)
+    if all(st.fast for st in steps):
+        for st in steps:
+            st.s.shard_spec_export(now_ns, v_token_ns, st.spec, st.rank)
+        allspec = torch.cat([st.spec for st in steps])
+        outs = [st.s.shard_spec_resolve(allspec, W, st.rank) for st in steps]
+        if all(o is not None for o in outs):
+            for o in outs:
+                o["path"] = "speculative"
+            return outs
+        assert all(o is None for o in outs), "ranks disagree on the fast path"
     for st in steps:
         st.rec1.fill_(0xFF)
     n1 = [st.s.shard_prefix(now_ns, v_token_ns, st.rec1) for st in steps]
@@ -81,6 +113,7 @@ def virtual_shards_step(steps, now_ns: int, v_token_ns: int):
     outs = [st.s.shard_finish(all2, st.rank) for st in steps]
     for o, a, b in zip(outs, n1, n2):
         o["n_export1"], o["n_candidates_local"], o["n_candidates"] = a, b, sum(n2)
+        o["path"] = "exact"
     del W
     return outs
 

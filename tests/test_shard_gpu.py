@@ -62,3 +62,37 @@ def test_virtual_shards_c5_pool_16m():
     ref = oracle.step(d["cfg"], d["groups"], d["table"], d["now_ns"], d["v_token_ns"], d["pool"], d["tasks"],
                       rows_out=False)
     _check(_run(d, 8), ref, "C5(ii)")
+
+
+@pytest.mark.parametrize("world,rows", [(2, 200_000), (4, 200_000), (4, 1 << 21)])
+def test_virtual_shards_consecutive_steps_fast_path(world, rows):
+    """Consecutive sharded steps: the first takes the exact two-round protocol (no threshold yet),
+    later ones the speculative resolve across ranks (one exchange of speculative sets).  Every
+    step must equal the oracle over the whole pool, run on the state its previous step left."""
+    from paper_2504_20068_b200 import Scheduler
+    from paper_2504_20068_b200.sharded import ShardedStep, shard_pool, virtual_shards_step
+    d = W.pool_snapshot(31, rows, table_draws=1 << 16)
+    steps = []
+    for r in range(world):
+        sp, st = shard_pool(d["pool"], d["tasks"], r, world)
+        n = max(len(sp["input_len"]), 1)
+        nt = 0 if st is None else len(st["arrival_ns"])
+        s = Scheduler(d["cfg"], d["groups"], d["table"], capacity=max(n, world * (d["cfg"]["max_batch"] + 1)),
+                      task_capacity=max(nt, 1))
+        s.load(sp, st)
+        steps.append(ShardedStep(s, r, world, None))
+    pool = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in d["pool"].items()}
+    paths, sizes = [], []
+    for k in range(4 if rows < (1 << 20) else 3):
+        ref = oracle.step(d["cfg"], d["groups"], d["table"], d["now_ns"], d["v_token_ns"], pool, d["tasks"],
+                          rows_out=False)
+        outs = virtual_shards_step(steps, d["now_ns"], d["v_token_ns"])
+        _check(outs, ref, f"W={world} step {k}")
+        paths.append(outs[0]["path"])
+        sizes.append(outs[0]["n_spec"])
+        pool["meta"], pool["aux"] = ref["meta"], ref["aux"]
+    for st in steps:
+        st.s.close()
+    assert paths[0] == "exact" and "speculative" in paths[1:], paths
+    if rows >= (1 << 21):        # a union larger than the small-set path: the histogram resolve ran
+        assert max(sizes[1:]) > 256, sizes
