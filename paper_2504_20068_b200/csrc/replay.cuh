@@ -114,7 +114,8 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
     __shared__ int64_t s_ring_sum;
     __shared__ uint32_t s_bstar, s_ncd, s_nsel, s_tot;
     __shared__ double s_bp, s_thr;
-    __shared__ uint64_t s_thr_img;
+    __shared__ uint64_t s_thr_img, s_tguess;
+    __shared__ uint32_t s_m, s_spec_ok;
     __shared__ bool s_stop;
 
     const Cfg c = A.c;
@@ -157,6 +158,7 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
         if (threadIdx.x == 0) {
             s_good = 0; s_tok = 0; s_reqg = 0; s_done = 0; s_drop = 0; s_tdone = 0; s_err = 0;
             s_now = 0; s_steps = 0; s_ring_n = 0; s_ring_pos = 0; s_ring_sum = 0; s_stop = false;
+            s_tguess = kNone;                              // no speculative threshold before the first step
         }
         __syncthreads();
         for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
@@ -307,30 +309,43 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                 continue;
             }
 
-            // ---- (a7) order pending by (key desc, id asc): bitonic sort of composite keys
-            uint32_t n2 = 1;
-            while (n2 < np) n2 <<= 1;
-            {
-                uint32_t cntl = 0;
-                for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) cntl += S.img[r] != kNone;
-                uint64_t dummy;
-                uint32_t pos = (uint32_t)block_exclusive_scan_u64(cntl, s_scan, &dummy);
-                for (uint32_t r = threadIdx.x; r < n; r += blockDim.x)
-                    if (S.img[r] != kNone) { bA[pos] = make_ck(S.img[r], r); bAv[pos] = r; ++pos; }
-                for (uint32_t i = np + threadIdx.x; i < n2; i += blockDim.x) { bA[i] = ~(u128)0; bAv[i] = 0; }
-            }
-            __syncthreads();
-            block_sort<u128>(bA, bAv, n2);
-            // B* = longest prefix within tau and B_max (monotone predicate -> count)
-            {
+            // ---- (a7) order pending by (key desc, id asc).  Attempt 0 sorts only the speculative
+            // set S = {key >= t} (t = 0.85 x the previous step's cutoff): S is a prefix of the
+            // priority order, so its budget walk is exact when it stops inside S (or S holds every
+            // pending row), and Cd lies in S when thr >= t.  Otherwise attempt 1
+            // sorts every pending row.  Both give the same B*, bp, thr and Cd.
+            for (uint32_t attempt = 0; attempt < 2; ++attempt) {
+                const uint64_t t = attempt == 0 ? s_tguess : 0ull;
+                {
+                    uint32_t cntl = 0;
+                    for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) cntl += S.img[r] != kNone && S.img[r] >= t;
+                    uint64_t tot;
+                    uint32_t pos = (uint32_t)block_exclusive_scan_u64(cntl, s_scan, &tot);
+                    const uint32_t m = (uint32_t)tot;
+                    if (attempt == 0 && (m == 0 || m > kReplayThreads)) {     // not worth it / too big: full sort
+                        if (threadIdx.x == 0) s_m = 0;
+                        __syncthreads();
+                        continue;
+                    }
+                    for (uint32_t r = threadIdx.x; r < n; r += blockDim.x)
+                        if (S.img[r] != kNone && S.img[r] >= t) { bA[pos] = make_ck(S.img[r], r); bAv[pos] = r; ++pos; }
+                    uint32_t m2 = 1;
+                    while (m2 < m) m2 <<= 1;
+                    for (uint32_t i = m + threadIdx.x; i < m2; i += blockDim.x) { bA[i] = ~(u128)0; bAv[i] = 0; }
+                    if (threadIdx.x == 0) s_m = m;
+                    __syncthreads();
+                    block_sort<u128>(bA, bAv, m2);
+                }
+                const uint32_t m = s_m;
+                // B* = longest prefix within tau and B_max (monotone predicate -> count)
                 uint64_t carry = 0;
                 uint32_t fits = 0;
-                for (uint32_t base = 0; base < np; base += blockDim.x) {
+                for (uint32_t base = 0; base < m; base += blockDim.x) {
                     const uint32_t i = base + threadIdx.x;
-                    const uint64_t cv = i < np ? S.cost[bAv[i]] : 0;
+                    const uint64_t cv = i < m ? S.cost[bAv[i]] : 0;
                     uint64_t tot;
                     const uint64_t ex = block_exclusive_scan_u64(cv, s_scan, &tot);
-                    const bool f = i < np && (uint64_t)i + 1 <= c.max_batch && carry + ex + cv <= c.token_budget;
+                    const bool f = i < m && (uint64_t)i + 1 <= c.max_batch && carry + ex + cv <= c.token_budget;
                     fits += __syncthreads_count(f);
                     carry += tot;
                 }
@@ -340,15 +355,21 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                     s_bp = bp;
                     s_thr = __dmul_rn(__ddiv_rn((double)c.pn, (double)c.pd), bp);
                     s_thr_img = (uint64_t)__double_as_longlong(s_thr);
+                    // speculative attempt: exact iff the walk stopped inside S (or S = all pending)
+                    // and Cd = {key >= thr} lies in S
+                    s_spec_ok = attempt == 1 || m == np || (fits < m && s_thr_img >= t);
                 }
                 __syncthreads();
+                if (s_spec_ok) break;
             }
+            if (threadIdx.x == 0) s_tguess = (uint64_t)__double_as_longlong(__dmul_rn(s_thr, 0.85));
+            const uint32_t np_sorted = s_m;   // rows in the sorted prefix array bA (Cd is a prefix of it)
             // ---- (a8) Cd = prefix of the key-ordered list with key >= thr
             {
                 uint32_t ncd = 0;
-                for (uint32_t base = 0; base < np; base += blockDim.x) {
+                for (uint32_t base = 0; base < np_sorted; base += blockDim.x) {
                     const uint32_t i = base + threadIdx.x;
-                    ncd += __syncthreads_count(i < np && ck_img(bA[i]) >= s_thr_img);
+                    ncd += __syncthreads_count(i < np_sorted && ck_img(bA[i]) >= s_thr_img);
                 }
                 if (threadIdx.x == 0) s_ncd = ncd;
                 __syncthreads();
