@@ -334,7 +334,7 @@ extern "C" int jit_sched_load(jit_sched* h, const jit_pool* p) {
     }
     h->S.n_part = h->nb_score;
     h->grid_pass = std::max<uint32_t>(1, std::min<uint32_t>((P.n + kPassThreads - 1) / kPassThreads, (uint32_t)h->n_sm * 4));
-    h->S.grid_pass = h->grid_pass;    // for k_spec's device-side launches
+    h->S.grid_pass = h->grid_pass;    // launch geometry of the exact path
     if (!same_shape) h->graph_dirty = true;
     h->loaded = true;
     return JIT_OK;

@@ -1,18 +1,17 @@
-// select.cuh -- the GMAX step over a request pool resident in HBM (sm_100a).
+// select.cuh -- shared types of the pool step (Pool, Ctrl, Scratch, TaskInfo, ...), the row
+// scoring helpers used by the replay, and the EXACT path of the step (sm_100a).
 //
-// Kernel chain of one step (captured once into a CUDA graph):
-//   k_begin    zero the control block / histograms, install (now, v_token)
-//   k_score    (a1)-(a6) for standalone rows (4 rows per thread, 128-bit SoA loads) and the
-//              compound pass (a4, one warp per task); writes the 8-B sort image of the key,
-//              the token cost and steps_waited+1; fuses the level-0 cost-weighted histogram
-//              of the key (exponent digit); the last CTA resolves level 0.
-//   k_pass     one more 12-bit digit of the cost-weighted radix select (only if the boundary
-//              bucket is still larger than kBucketCap); last CTA resolves it.
+// The step itself is k_score (score.cuh) -> k_spec (the speculative resolve).
+// When the speculation cannot be exact, finish_step (abi.cu) runs the exact path from the host:
+//   k_hist0    level-0 cost-weighted histogram of the composite key (key desc, id asc); the last
+//              CTA resolves the boundary bin
+//   k_pass     one more 12-bit digit while the boundary bucket is larger than kBucketCap
 //   k_compact  gathers the boundary bucket (composite key, cost) + the smallest key above it
 //   k_resolve  one CTA: sorts the bucket, block-scans costs -> exact B*, bp, thr (a7, a8)
 //   k_cand     compacts Cd = {key >= thr} (warp ballots)
 //   k_group    one CTA: sorts Cd by (len, id), u64/u128 prefix sums, sliding windows within
-//              the token budget, first argmax (a9); writes the batch and the bookkeeping.
+//              the token budget, first argmax (a9); writes the batch and the bookkeeping
+//   k_publish  copies the control block to pinned host memory
 #pragma once
 #include "common.cuh"
 
@@ -740,10 +739,7 @@ static __device__ void group_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const
 #endif  // JIT_EXACT_TU
 
 #ifndef JIT_EXACT_TU
-// k_publish: the step's last graph node -- copies the control block to pinned host memory.
-// It also makes the graph wait for the exact path: when the node that made device-side tail
-// launches is the graph's LAST node, graph completion was measured NOT to wait for nested
-// tail launches (profiles/micro_cdp2.cu, mode 5); any node after it restores the ordering.
+// k_publish: copies the control block to pinned host memory (end of the host-run exact path)
 __global__ void k_publish(const Ctrl* ctrl, Ctrl* host) { publish_ctrl(ctrl, host); }
 
 // progress updates from the engine, applied before scoring
