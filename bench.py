@@ -386,6 +386,11 @@ def main():
     for s in hs:
         s.kernel_times(slots=K)
     ms_events = timed_block()
+    # (3) k_score alone, back to back over the rotated pools (launch overlapped by the previous
+    # kernel, as inside the step where k_spec hides it): the roofline's kernel duration
+    barrier()
+    n_b2b = max(60, K)
+    k_b2b = Scheduler.time_scoring(hs, now, v, n_b2b)
     for _ in range(3):
         for k in range(20):
             hs[k % args.rot].step_async(now, v)
@@ -411,19 +416,23 @@ def main():
     alg_bytes = n_single * BYTES_ROW + (n - n_single) * BYTES_CALL + nt * BYTES_TASK
     pk = peaks()
     hbm_peak = pk["hbm_gbs"] if pk else 6650.0
-    achieved = alg_bytes / (kt[0] / 1e3) / 1e9
+    achieved = alg_bytes / (k_b2b / 1e3) / 1e9
+    achieved_nodes = alg_bytes / (kt[0] / 1e3) / 1e9
     roofline = {"bound": "hbm", "kernel": "k_score", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": tr["bytes_per_launch"] if tr else None,
                 "traffic_source": tr["source"] if tr else None,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if pk else "fallback 6650 GB/s",
-                "alg_bytes_per_launch": alg_bytes, "k_score_ms": kt[0],
-                "kernel_ms": {"k_score": kt[0], "k_spec": kt[2], "step_graph_with_event_nodes": kt[4]},
+                "alg_bytes_per_launch": alg_bytes, "k_score_ms": k_b2b,
+                "how": f"{n_b2b} back-to-back k_score launches rotating over the {args.rot} L2-defeating pool "
+                       "copies, CUDA events on the library stream around the sequence (jit_sched_time_scoring)",
+                "kernel_ms_event_nodes": {"k_score": kt[0], "k_spec": kt[2], "step_graph": kt[4]},
+                "frac_event_nodes": achieved_nodes / hbm_peak,
+                "how_event_nodes": "CUDA event nodes around each kernel inside the step graph, averaged over "
+                                   "the K steps of a second timed block; each node pair also counts the "
+                                   "kernel node's launch latency (~5 us)",
                 "frac_of_8tbs_datasheet": achieved / 8000.0,
                 "first_step_after_load_ms": float(np.median(first_ms)),
-                "ms_per_step_with_event_nodes": ms_events,
-                "how": "k_score device time from CUDA event nodes placed around each kernel inside the step "
-                       "graph (re-pointed to a fresh event slot every launch), averaged over the K timed steps "
-                       "of a second timed block identical to the headline one"}
+                "ms_per_step_with_event_nodes": ms_events}
 
     # ------------------------------------------------------------------ steady state with progress
     # the engine loop: every step reports the progress of each handle's previous batch (decode

@@ -188,6 +188,13 @@ int jit_sched_read_rows(jit_sched* h, double* key, double* rate, int64_t* t_rem,
  * path, when the host runs it after a step, is not included). */
 int jit_sched_kernel_times(jit_sched* h, int enable, float* ms_out, uint32_t n_out);
 
+/* Measurement: `launches` back-to-back launches of the scoring kernel (k_score, rows (a1)-(a6)),
+ * rotating over n_handles loaded handles that share one stream, timed with CUDA events around
+ * the sequence; *ms_per_launch = average.  Each launch advances steps_waited like a step whose
+ * batch is empty (the pools' state changes); the per-step accumulators are reset afterwards. */
+int jit_sched_time_scoring(jit_sched** hs, uint32_t n_handles, int64_t now_ns, int64_t v_token_ns, uint32_t launches,
+                           float* ms_per_launch);
+
 /* Diagnostics: %globaltimer stamps (ns) of the phases of the single-CTA resolve of the last
  * synchronized step: [k_spec start, partials reduced, set loaded, set sorted, budget walk,
  * Cd gathered, window sort start, window sorted, prefix sums, argmax, batch written]. */

@@ -639,6 +639,34 @@ extern "C" int jit_sched_kernel_times(jit_sched* h, int enable, float* ms_out, u
     return JIT_OK;
 }
 
+// Back-to-back k_score launches rotating over handles (that share one stream), timed with CUDA
+// events around the whole sequence: the kernel's average duration with its launch overlapped by
+// the previous kernel (a single launch bracketed by event nodes also counts the node's launch
+// latency).  Each handle's per-step accumulators are reset afterwards (outside the timing).
+extern "C" int jit_sched_time_scoring(jit_sched** hs, uint32_t n_handles, int64_t now_ns, int64_t v_token_ns,
+                                      uint32_t launches, float* ms_per_launch) {
+    if (!hs || !n_handles || !launches || !ms_per_launch) return JIT_EINVAL;
+    jit_sched* h = hs[0];
+    for (uint32_t i = 0; i < n_handles; ++i) {
+        if (!hs[i] || !hs[i]->loaded) return set_err(h, JIT_ESTATE, "time_scoring: handle %u not loaded", i);
+        if (hs[i]->stream != h->stream) return set_err(h, JIT_EINVAL, "time_scoring: handles must share one stream");
+    }
+    cudaStream_t s = h->stream;
+    cudaEvent_t e0 = h->ev[0], e1 = h->ev[1];
+    CK(cudaStreamSynchronize(s));
+    CK(cudaEventRecord(e0, s));
+    for (uint32_t k = 0; k < launches; ++k) enqueue_score(hs[k % n_handles], s, now_ns, v_token_ns);
+    CK(cudaEventRecord(e1, s));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    *ms_per_launch = ms / (float)launches;
+    for (uint32_t i = 0; i < n_handles; ++i)       // consume the accumulated partials / sets
+        CK(exact::spec(hs[i]->P, hs[i]->c, hs[i]->d_ctrl, hs[i]->S, 1, s, false));
+    CK(cudaStreamSynchronize(s));
+    return JIT_OK;
+}
+
 extern "C" int jit_sched_phase_times(jit_sched* h, uint64_t* ns_out, uint32_t n_out) {
     if (!h || !ns_out) return JIT_EINVAL;
     CK(cudaStreamSynchronize(h->stream));

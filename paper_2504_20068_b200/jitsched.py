@@ -109,7 +109,8 @@ EXPORTS = ("jit_sched_workspace_bytes", "jit_sched_init", "jit_sched_load", "jit
            "jit_sched_step_async", "jit_sched_fetch_batch", "jit_sched_read_rows", "jit_sched_kernel_times",
            "jit_replay_workspace_bytes", "jit_sched_replay", "jit_sched_destroy", "jit_sched_last_error",
            "jit_sched_version", "jit_shard_prefix", "jit_shard_merge", "jit_shard_candidates", "jit_shard_finish",
-           "jit_sched_phase_times", "jit_shard_spec_bytes", "jit_shard_spec_export", "jit_shard_spec_resolve")
+           "jit_sched_phase_times", "jit_shard_spec_bytes", "jit_shard_spec_export", "jit_shard_spec_resolve",
+           "jit_sched_time_scoring")
 
 
 def load_library(path: str = LIB_PATH):
@@ -347,6 +348,17 @@ class Scheduler:
                                                    C.c_uint32(all_rec2.numel() // REC2_BYTES), C.c_uint32(rank),
                                                    C.byref(b)), self.h)
         return self._batch_dict(rc, b)
+
+    @staticmethod
+    def time_scoring(handles, now_ns: int, v_token_ns: int, launches: int) -> float:
+        """Average ms of back-to-back k_score launches rotating over `handles` (same stream)."""
+        lib = load_library()
+        arr = (C.c_void_p * len(handles))(*[h.h.value for h in handles])
+        ms = C.c_float()
+        rc = lib.jit_sched_time_scoring(arr, C.c_uint32(len(handles)), C.c_int64(now_ns), C.c_int64(v_token_ns),
+                                        C.c_uint32(launches), C.byref(ms))
+        handles[0]._check(rc, handles[0].h)
+        return float(ms.value)
 
     # fast sharded step: speculative-set export / union resolve (None: use the exact protocol)
     def shard_spec_bytes(self) -> int:

@@ -208,3 +208,38 @@ def test_speculative_paths_against_oracle_chain():
             pool["meta"], pool["aux"] = ref["meta"], ref["aux"]
         s.close()
     assert seen_fast and seen_big, (seen_fast, seen_big)
+
+
+def test_time_scoring_leaves_state_consistent():
+    """bench.py's roofline timing (jit_sched_time_scoring: back-to-back k_score launches over
+    several handles) must leave each handle as L empty steps would: every pending row's
+    steps_waited advanced by L (saturating, P:467's wait counter), meta untouched, and the per-step
+    partials / speculative set consumed -- the next step still equals the oracle's."""
+    from paper_2504_20068_b200 import Scheduler
+    L = 5
+    ds, hs, pools = [], [], []
+    for seed in (31, 32):
+        d = W.pool_snapshot(seed, 150_000, table_draws=1 << 16)
+        d["cfg"] = W.default_config(token_budget=8192, max_batch=8192)
+        s = _sched(d, debug=True)
+        s.load(d["pool"], d["tasks"])
+        pool = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in d["pool"].items()}
+        for _ in range(2):                       # second step: a speculative threshold exists
+            ref = oracle.step(d["cfg"], d["groups"], d["table"], d["now_ns"], d["v_token_ns"], pool, d["tasks"])
+            _compare(s.step(d["now_ns"], d["v_token_ns"]), ref)
+            pool["meta"], pool["aux"] = ref["meta"], ref["aux"]
+        pend = ref["pending"].astype(bool)
+        waited = pool["aux"] >> 16
+        pool["aux"] = np.where(pend, (pool["aux"] & 0xFFFF) | (np.minimum(waited + L, 0xFFFF) << 16),
+                               pool["aux"]).astype(pool["aux"].dtype)
+        ds.append(d); hs.append(s); pools.append(pool)
+    ms = Scheduler.time_scoring(hs, ds[0]["now_ns"], ds[0]["v_token_ns"], L * len(hs))
+    assert ms > 0
+    for d, s, pool in zip(ds, hs, pools):
+        rows = s.read_rows(debug=True)
+        assert np.array_equal(rows["meta"], pool["meta"])
+        assert np.array_equal(rows["aux"], pool["aux"])
+        ref = oracle.step(d["cfg"], d["groups"], d["table"], d["now_ns"], d["v_token_ns"], pool, d["tasks"])
+        got = s.step(d["now_ns"], d["v_token_ns"])
+        _compare(got, ref, ctx=f"after time_scoring n_spec={got['n_spec']} fallback={got['fallback']}")
+        s.close()
