@@ -127,7 +127,7 @@ struct SpecEl {                 // one element of the speculative set, preloaded
     uint32_t own;               // 1: the row belongs to this handle (a sharded step merges all ranks' sets)
 };
 template <uint32_t NT>
-static __device__ __noinline__ void spec_fast(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t n,
+static __device__ __forceinline__ void spec_fast(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t n,
                                               bool whole, uint64_t t_img, uint64_t min_img, const SpecEl& el,
                                               unsigned char* smem) {
     ulonglong2* f_rec = reinterpret_cast<ulonglong2*>(smem);                 // [kSpecFast] (img, id | cost << 32)
