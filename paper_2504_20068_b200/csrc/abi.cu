@@ -212,6 +212,7 @@ extern "C" int jit_sched_init(const jit_config* cfg, const jit_slo_group* groups
     c.R = cfg->refine_interval; c.frame = cfg->frame_steps; c.qn = cfg->q_num; c.qd = cfg->q_den;
     c.pn = cfg->p_num; c.pd = cfg->p_den; c.delta = cfg->delta_starve; c.len_key = cfg->len_key;
     c.appb = cfg->appb_filter; c.eps = cfg->eps_ns; c.waiting = cfg->waiting_ns;
+    c.p = (double)c.pn / (double)c.pd;      // IEEE division, correctly rounded like __ddiv_rn
     fastdiv_magic(c.R, &c.R_m, &c.R_l);
     fastdiv_magic(c.frame, &c.F_m, &c.F_l);
     CK(cudaMemcpyAsync((void*)h->T.edges, table->edges, 4ull * table->n_bins, cudaMemcpyHostToDevice, h->stream));

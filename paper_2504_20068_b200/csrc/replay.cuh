@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                     s_bstar = fits;
                     const double bp = __longlong_as_double((long long)ck_img(bA[fits - 1]));
                     s_bp = bp;
-                    s_thr = __dmul_rn(__ddiv_rn((double)c.pn, (double)c.pd), bp);
+                    s_thr = __dmul_rn(c.p, bp);
                     s_thr_img = (uint64_t)__double_as_longlong(s_thr);
                     // speculative attempt: exact iff the walk stopped inside S (or S = all pending)
                     // and Cd = {key >= thr} lies in S

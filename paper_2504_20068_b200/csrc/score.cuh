@@ -205,7 +205,7 @@ static __device__ __forceinline__ void spec_fast(const Pool& P, const Cfg& c, Ct
             else {
                 const uint64_t bimg = bstar == n ? min_img : f_bp_img;
                 const double bp = __longlong_as_double((long long)bimg);
-                const double thr = __dmul_rn(__ddiv_rn((double)c.pn, (double)c.pd), bp);   // A16
+                const double thr = __dmul_rn(c.p, bp);   // A16
                 const uint64_t ti = (uint64_t)__double_as_longlong(thr);
                 if (!whole && ti < t_img) spec_fallback(ctrl, &f_fb);   // Cd may leave S
                 else { ctrl->b_star = bstar; ctrl->bp = bp; ctrl->thr = thr; ctrl->thr_img = ti; f_bp_img = ti; }
@@ -447,9 +447,16 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // after ~2^26 hardware-suspended probes instead of hanging the GPU.
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
     uint32_t ok;
+#ifdef JIT_MBAR_HINT
+    // suspend (not spin) until the phase completes or the hint (ns) expires
+    asm volatile("{\n\t.reg .pred p;\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(smem_addr(bar)), "r"(parity), "n"(JIT_MBAR_HINT) : "memory");
+#else
     asm volatile("{\n\t.reg .pred p;\n\t"
                  "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
                  "selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(smem_addr(bar)), "r"(parity) : "memory");
+#endif
     return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -897,11 +904,24 @@ static __device__ void spec_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const 
 // control block to pinned host memory.  Its code is kept small on purpose: it runs on one SM
 // once per step, so every instruction-cache line it touches is a miss to L2 / HBM; a larger set
 // is resolved by k_spec_big, which the host launches (status ST_SPEC_BIG).
+// The control block lives in shared memory while k_spec runs: it starts as the reset block k_score
+// wrote (built here before the dependency wait, so no global read-back) and is stored once at the
+// end to the device copy and the pinned host mirror -- no load round trip on the tail.
+// (now / v, word 1, are left as k_score wrote them: nothing reads them back.)
+static_assert(offsetof(Ctrl, now) == 16 && offsetof(Ctrl, v) == 24, "ctrl word 1 = (now, v)");
 __global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl, Scratch S, int reduce_only) {
     extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ Ctrl s_ctrl;
+    reset_ctrl_block(&s_ctrl, 0, 0);
     pdl_wait();
-    spec_body<false>(P, c, ctrl, S, reduce_only, smem);
-    publish_ctrl(ctrl, S.h_ctrl);
+    spec_body<false>(P, c, &s_ctrl, S, reduce_only, smem);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < sizeof(Ctrl) / 16; i += blockDim.x) {
+        if (i == 1) continue;
+        const uint4 w = reinterpret_cast<const uint4*>(&s_ctrl)[i];
+        reinterpret_cast<uint4*>(ctrl)[i] = w;
+        reinterpret_cast<uint4*>(S.h_ctrl)[i] = w;
+    }
 }
 __global__ void __launch_bounds__(kSpecThreads) k_spec_big(Pool P, Cfg c, Ctrl* ctrl, Scratch S) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -1134,7 +1154,7 @@ static __device__ void spec_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const 
             else {
                 s_fits = n;
                 const double bp = __longlong_as_double((long long)s_min);
-                const double thr = __dmul_rn(__ddiv_rn((double)c.pn, (double)c.pd), bp);
+                const double thr = __dmul_rn(c.p, bp);
                 ctrl->b_star = n; ctrl->bp = bp; ctrl->thr = thr;
                 ctrl->thr_img = s_thr_img = (uint64_t)__double_as_longlong(thr);
             }
@@ -1216,7 +1236,7 @@ static __device__ void spec_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const 
                     ctrl->error |= 1u; ctrl->status = ST_ERROR; s_fb = 2;
                 } else {
                     const double bp = __longlong_as_double((long long)bimg);
-                    const double thr = __dmul_rn(__ddiv_rn((double)c.pn, (double)c.pd), bp);
+                    const double thr = __dmul_rn(c.p, bp);
                     const uint64_t ti = (uint64_t)__double_as_longlong(thr);
                     if (!whole && ti < t_img) spec_fallback(ctrl, &s_fb);
                     else { ctrl->b_star = fits; ctrl->bp = bp; ctrl->thr = thr; ctrl->thr_img = s_thr_img = ti; }

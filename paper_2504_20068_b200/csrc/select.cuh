@@ -247,7 +247,7 @@ static __device__ void resolve_level(const Cfg& c, Ctrl* ctrl, uint32_t* hcnt, u
             ctrl->b_star = ctrl->n_pending;
             const double bp = __longlong_as_double((long long)ctrl->min_img);
             ctrl->bp = bp;
-            ctrl->thr = __dmul_rn(__ddiv_rn((double)c.pn, (double)c.pd), bp);
+            ctrl->thr = __dmul_rn(c.p, bp);
             ctrl->thr_img = (unsigned long long)__double_as_longlong(ctrl->thr);
             ctrl->status = ST_RESOLVED;
         } else {
@@ -565,7 +565,7 @@ __global__ void __launch_bounds__(1024) k_resolve(Pool P, Cfg c, Ctrl* ctrl, Scr
         const uint64_t bimg = nf ? ck_img(sk[nf - 1]) : (uint64_t)ctrl->pred_min_img;
         const double bp = __longlong_as_double((long long)bimg);
         ctrl->bp = bp;
-        ctrl->thr = __dmul_rn(__ddiv_rn((double)c.pn, (double)c.pd), bp);   // A16
+        ctrl->thr = __dmul_rn(c.p, bp);   // A16
         ctrl->thr_img = (unsigned long long)__double_as_longlong(ctrl->thr);
         if (nf == 0 && ctrl->pred_min_img == kNone) { ctrl->error = 1; ctrl->status = ST_ERROR; }
         else ctrl->status = ST_RESOLVED;

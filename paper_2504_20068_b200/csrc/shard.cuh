@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(1024) k_merge1(Cfg c, Ctrl* ctrl, const Rec1* 
         ctrl->b_star = fits;
         const double bp = __longlong_as_double((long long)ck_img(k[fits - 1]));
         ctrl->bp = bp;
-        ctrl->thr = __dmul_rn(__ddiv_rn((double)c.pn, (double)c.pd), bp);
+        ctrl->thr = __dmul_rn(c.p, bp);
         ctrl->thr_img = (unsigned long long)__double_as_longlong(ctrl->thr);
         ctrl->status = ST_RESOLVED;
         ctrl->n_cand = 0;

@@ -15,7 +15,7 @@ import json
 try:
     d = json.loads(open("gpurun_out/bench_$name.log").read().strip().splitlines()[-1])
     r = d["roofline"]
-    print("$name", "defs=$defs", "ms/step %.4f" % d["ms_per_step"], "kernel_ms", {k: round(v * 1e3, 2) for k, v in r["kernel_ms"].items()}, "frac %.3f" % r["frac"])
+    print("$name", "defs=$defs", "ms/step %.4f" % d["ms_per_step"], "k_score b2b us %.2f" % (r["k_score_ms"] * 1e3), "nodes", {k: round(v * 1e3, 2) for k, v in r["kernel_ms_event_nodes"].items()}, "frac %.3f" % r["frac"])
 except Exception as e:
     print("$name failed", e, open("gpurun_out/bench_$name.log").read()[-800:])
 PY
