@@ -121,6 +121,22 @@ __device__ __forceinline__ void spec_fallback(Ctrl* ctrl, int* fb) {
 // from one pass over the set (shared-memory broadcast reads), so B* = #{i : rank_i < B_max and
 // prefix_i <= tau} (monotone in the rank) is one barrier count; the same for Cd's (len, id) order.
 constexpr uint32_t kSpecFast = 256;
+constexpr uint32_t kSpecFastChunk = 1u << 24;   // costs <= chunk: kSpecFast costs sum below 2^32
+// priority-order rank record: (key image, id) as one 96-bit word V = img_hi : img_lo : ~id, so
+// "q before me" (key desc, id asc) is V_q > V_me -- the borrow of V_me - V_q (three subtractions);
+// w = -cost, so borrow_mask * w adds cost
+__device__ __forceinline__ uint4 rank_rec(uint64_t img, uint32_t id, uint32_t cost) {
+    return make_uint4(~id, (uint32_t)img, (uint32_t)(img >> 32), 0u - cost);
+}
+__device__ __forceinline__ uint32_t before_mask(const uint4& q, const uint4& me) {
+    uint32_t t, b;
+    asm("sub.cc.u32 %0, %2, %5;\n\t"
+        "subc.cc.u32 %0, %3, %6;\n\t"
+        "subc.cc.u32 %0, %4, %7;\n\t"
+        "subc.u32 %1, 0, 0;"
+        : "=&r"(t), "=r"(b) : "r"(me.x), "r"(me.y), "r"(me.z), "r"(q.x), "r"(q.y), "r"(q.z));
+    return b;                                   // 0xFFFFFFFF when q precedes me, else 0
+}
 struct SpecEl {                 // one element of the speculative set, preloaded by k_spec
     uint64_t img;
     uint32_t id, cost, len, row, meta, aux;
@@ -130,7 +146,7 @@ template <uint32_t NT>
 static __device__ __forceinline__ void spec_fast(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t n,
                                               bool whole, uint64_t t_img, uint64_t min_img, const SpecEl& el,
                                               unsigned char* smem) {
-    ulonglong2* f_rec = reinterpret_cast<ulonglong2*>(smem);                 // [kSpecFast] (img, id | cost << 32)
+    uint4* f_rec = reinterpret_cast<uint4*>(smem);                           // [kSpecFast] rank_rec
     uint64_t* f_img = reinterpret_cast<uint64_t*>(f_rec + kSpecFast);        // [kSpecFast]
     uint32_t* f_id = reinterpret_cast<uint32_t*>(f_img + kSpecFast);         // [kSpecFast]
     uint32_t* f_cost = f_id + kSpecFast;                                     // [kSpecFast]
@@ -150,9 +166,9 @@ static __device__ __forceinline__ void spec_fast(const Pool& P, const Cfg& c, Ct
     const uint64_t img = own ? el.img : kNone;
     const uint32_t id = el.id, cost = own ? el.cost : 0u, len = el.len;
     __shared__ uint32_t f_rank2[kSpecFast];
-    __shared__ unsigned long long f_pre2[kSpecFast];
+    __shared__ uint32_t f_pre2[kSpecFast];
     if (own) {
-        f_rec[tid] = make_ulonglong2(img, (uint64_t)id | ((uint64_t)cost << 32));
+        f_rec[tid] = rank_rec(img, id, cost);
         f_img[tid] = img; f_id[tid] = id; f_cost[tid] = cost;
         f_rank2[tid] = 0; f_pre2[tid] = 0;
     }
@@ -167,31 +183,27 @@ static __device__ __forceinline__ void spec_fast(const Pool& P, const Cfg& c, Ct
         const uint32_t e = n ? tid % n : 0u, part = n ? tid / n : 1u;
         if (part < F) {
             const uint32_t j0 = (uint32_t)((uint64_t)n * part / F), j1 = (uint32_t)((uint64_t)n * (part + 1) / F);
-            const ulonglong2 me = f_rec[e];
-            const uint64_t mi = me.x;
-            const uint32_t md = (uint32_t)me.y;
-            uint32_t ra = 0, rb = 0;
-            uint64_t pa = 0, pb = 0;
+            const uint4 me = f_rec[e];
+            uint32_t ra = 0, rb = 0, pa = 0, pb = 0;   // cost prefixes < 2^32 (costs <= kSpecFastChunk)
             uint32_t j = j0;
             for (; j + 1 < j1; j += 2) {
-                const ulonglong2 q0 = f_rec[j], q1 = f_rec[j + 1];
-                const bool b0 = q0.x > mi || (q0.x == mi && (uint32_t)q0.y < md);
-                const bool b1 = q1.x > mi || (q1.x == mi && (uint32_t)q1.y < md);
-                ra += b0; pa += b0 ? (q0.y >> 32) : 0ull;
-                rb += b1; pb += b1 ? (q1.y >> 32) : 0ull;
+                const uint4 q0 = f_rec[j], q1 = f_rec[j + 1];
+                const uint32_t b0 = before_mask(q0, me), b1 = before_mask(q1, me);
+                ra -= b0; pa += b0 * q0.w;
+                rb -= b1; pb += b1 * q1.w;
             }
             if (j < j1) {
-                const ulonglong2 q0 = f_rec[j];
-                const bool b0 = q0.x > mi || (q0.x == mi && (uint32_t)q0.y < md);
-                ra += b0; pa += b0 ? (q0.y >> 32) : 0ull;
+                const uint4 q0 = f_rec[j];
+                const uint32_t b0 = before_mask(q0, me);
+                ra -= b0; pa += b0 * q0.w;
             }
             if (F == 1) { f_rank2[e] = ra + rb; f_pre2[e] = pa + pb; }
-            else { atomicAdd(&f_rank2[e], ra + rb); atomicAdd(&f_pre2[e], (unsigned long long)(pa + pb)); }
+            else { atomicAdd(&f_rank2[e], ra + rb); atomicAdd(&f_pre2[e], pa + pb); }
         }
         __syncthreads();
     }
     uint32_t rank = own ? f_rank2[tid] : 0u;          // own => tid < kSpecFast: written by itself
-    const uint64_t pre = own ? f_pre2[tid] + cost : 0ull;
+    const uint64_t pre = own ? (uint64_t)f_pre2[tid] + cost : 0ull;
     const bool fits = own && rank + 1 <= c.max_batch && pre <= c.token_budget;
     const uint32_t bstar = (uint32_t)__syncthreads_count(fits);
     if (fits && rank + 1 == bstar) f_bp_img = img;          // the B*-th request (A15)
@@ -1001,7 +1013,7 @@ __global__ void __launch_bounds__(kSpecThreads) k_spec_merge(Pool P, Cfg c, Ctrl
     }
     __syncthreads();
     if (m_fb) { publish_ctrl(ctrl, S.h_ctrl); return; }
-    if (m_off[world] > kSpecFast) {
+    if (m_off[world] > kSpecFast || c.chunk > kSpecFastChunk) {
         // a larger union: copy it into this handle's speculative-set arrays (another rank's rows
         // get row = ~0) and resolve it with k_spec_big's histogram path
         const uint32_t n = m_off[world];
@@ -1118,7 +1130,8 @@ static __device__ void spec_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const 
     __syncthreads();
     if (s_fb) return;                                      // published as is (k_spec)
     if constexpr (!kBig) {
-        if (n <= kSpecFast) spec_fast<kSpecThreads>(P, c, ctrl, S, n, whole, t_img, (uint64_t)s_min, el, smem);
+        if (n <= kSpecFast && c.chunk <= kSpecFastChunk)
+            spec_fast<kSpecThreads>(P, c, ctrl, S, n, whole, t_img, (uint64_t)s_min, el, smem);
         else if (tid == 0) ctrl->status = ST_SPEC_BIG;     // the host launches k_spec_big
         return;
     }
