@@ -230,23 +230,25 @@ static __device__ __forceinline__ void spec_fast(const Pool& P, const Cfg& c, Ct
     const uint64_t thr_img = f_bp_img;
     const bool cd = own && img >= thr_img;
     const uint64_t wk = ((uint64_t)len << 32) | id;
-    if (tid < kSpecFast) f_wk[tid] = cd ? wk : ~0ull;
-    if (own) f_rank2[tid] = 0;                             // reused for the window positions
+    // Cd is a prefix of the priority order: its elements hold the ranks 0..|Cd|-1, which serve as
+    // compact indices (f_pre2 is free again: reused for the window positions)
+    if (cd) f_wk[rank] = wk;
+    if (tid < kSpecFast) f_pre2[tid] = 0;
     const uint32_t ncd = (uint32_t)__syncthreads_count(cd);
     {   // window position of each Cd element: #{Cd elements before it in (len, id) order}, the
         // comparisons spread over the CTA as above
-        const uint32_t F = n ? min(NT / n, 8u) : 1u;
-        const uint32_t e = n ? tid % n : 0u, part = n ? tid / n : 1u;
-        const uint64_t mk = (part < F && e < n) ? f_wk[e] : ~0ull;
-        if (mk != ~0ull) {
-            const uint32_t j0 = (uint32_t)((uint64_t)n * part / F), j1 = (uint32_t)((uint64_t)n * (part + 1) / F);
+        const uint32_t F = ncd ? min(NT / ncd, 8u) : 1u;
+        const uint32_t e = ncd ? tid % ncd : 0u, part = ncd ? tid / ncd : 1u;
+        if (part < F && e < ncd) {
+            const uint64_t mk = f_wk[e];
+            const uint32_t j0 = (uint32_t)((uint64_t)ncd * part / F), j1 = (uint32_t)((uint64_t)ncd * (part + 1) / F);
             uint32_t pa = 0, pb = 0, j = j0;
             for (; j + 1 < j1; j += 2) { pa += f_wk[j] < mk; pb += f_wk[j + 1] < mk; }
             if (j < j1) pa += f_wk[j] < mk;
-            if (F == 1) f_rank2[e] = pa + pb; else atomicAdd(&f_rank2[e], pa + pb);
+            if (F == 1) f_pre2[e] = pa + pb; else atomicAdd(&f_pre2[e], pa + pb);
         }
         __syncthreads();
-        if (cd) o_elem[f_rank2[tid]] = tid;
+        if (cd) o_elem[f_pre2[rank]] = tid;
     }
     __shared__ uint32_t f_row[kSpecFast], f_meta[kSpecFast], f_aux[kSpecFast];
     if (own) { f_row[tid] = el.own ? el.row : 0xFFFFFFFFu; f_meta[tid] = el.meta; f_aux[tid] = el.aux; }

@@ -1,6 +1,7 @@
 """Attribute ncu per-instruction counts (source page, SASS) of k_score to source lines / functions
 using the line table of the local build (same sources and flags).  Run here (no GPU):
-  python profiles/sass_lines.py gpurun_out/prof_score.ncu-rep [kernel-mangled-prefix]"""
+  python profiles/sass_lines.py gpurun_out/prof_score.ncu-rep [kernel-mangled-prefix] [cubin-prefix]
+(k_spec: python profiles/sass_lines.py gpurun_out/prof_spec.ncu-rep _ZN3jit6k_spec exact)"""
 import collections
 import csv
 import io
@@ -26,7 +27,7 @@ ie, smp = h.index("Instructions Executed"), h.index("Warp Stall Sampling (All Sa
 data = [(r[1], int(r[ie] or 0), int(r[smp] or 0)) for r in rows[2:] if len(r) > ie]
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", lib], cwd=tmp, capture_output=True)
-cub = [f for f in os.listdir(tmp) if f.startswith("abi")][0]
+cub = [f for f in os.listdir(tmp) if f.startswith(sys.argv[3] if len(sys.argv) > 3 else "abi")][0]
 sass = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout.splitlines()
 start = [i for i, l in enumerate(sass) if l.startswith(".text." + kern)][0]
 seq, cur = [], None
@@ -86,3 +87,11 @@ for cname in cols:
     vals = [(int(r[ci] or 0), i) for i, r in enumerate(rows[2:]) if len(r) > ci]
     top = sorted(vals, reverse=True)[:5]
     print(cname, [(v, seq[i][0], seq[i - 1][1][:28]) for v, i in top if i < len(seq)])
+
+# warp-stall samples per source line (all reasons), top 30
+byls = collections.Counter()
+for (loc, ins), (s, n, k) in zip(seq, data):
+    byls[loc] += k
+print("samples by line:", sum(byls.values()))
+for k, v in byls.most_common(30):
+    print(f"  {k}  {v}")
