@@ -368,13 +368,17 @@ def main():
             j += 1
         torch.cuda.synchronize()
 
+    host_us = []                                          # host time to submit one step (launch loop)
+
     def timed_block():
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        h0 = time.perf_counter()
         for k in range(K):
             hs[k % args.rot].step_async(now, v)
+        host_us.append((time.perf_counter() - h0) / K * 1e6)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -524,7 +528,7 @@ def main():
                            "rows_per_gpu": n, "tasks_per_gpu": nt,
                            "l2": f"inputs larger than L2: {args.rot} rotated pool copies of ~{(n * 100) >> 20} MiB workspace each",
                            "parallelism": f"{ws} independent 2^20-row shards (no data-path collective)" if ws > 1 else "single GPU",
-                           "fast_path_fallbacks": fallback, "last_batch": {"n_selected": sel["n_selected"],
+                           "fast_path_fallbacks": fallback, "host_submit_us_per_step": round(host_us[0], 2), "last_batch": {"n_selected": sel["n_selected"],
                                                                          "b_star": sel["b_star"],
                                                                          "n_candidates": sel["n_candidates"]}},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "steady_with_progress": steady,

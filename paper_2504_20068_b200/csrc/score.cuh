@@ -1069,56 +1069,47 @@ static __device__ void spec_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const 
     const int lane = tid & 31, wid = tid >> 5;
     stamp(ctrl, 0);
     const uint64_t t_img = S.persist->t_guess;
-    // every thread reads the set size, and in the steady state (small set) its own element and the
-    // element's meta / aux right away: these loads overlap the partials' reduction below
+    // every load of this prologue is issued at once (one L2 round trip): the set size, each
+    // thread's element of a small set -- loaded before the size is known, entries past it are
+    // ignored (the workspace is zeroed at init) -- and, by thread 0, k_score's partials record
     const uint32_t n_set = kBig ? ctrl->spec_n : *reinterpret_cast<volatile unsigned int*>(S.spec_cnt);
     SpecEl el{kNone, 0u, 0u, 0u, 0u, 0u, 0u, 1u};
-    if (!kBig && !reduce_only && n_set <= kSpecFast && tid < n_set) {
+    if (!kBig && !reduce_only && tid < kSpecFast) {
         el.img = S.spec_img[tid]; el.id = S.spec_id[tid]; el.cost = S.spec_cost[tid]; el.len = S.spec_len[tid];
         el.row = S.spec_row[tid]; el.meta = S.spec_meta[tid]; el.aux = S.spec_aux[tid];
     }
     if (tid == 0) {
-        s_min = kNone; s_cost_tot = 0; s_pend = 0; s_drop = 0; s_err = 0; s_ref = 0;
-        s_n = n_set;
-        ctrl->spec_n = s_n;
-        s_first = kSpecBins; s_nsel = 0; s_ncd = 0; s_min_above = kNone; s_above = 0; s_fb = 0;
-    }
-    if (kBig) for (uint32_t b = tid; b < kSpecBins; b += kSpecThreads) s_hist[b] = 0;
-    __syncthreads();
-    if (!kBig && tid == 0) *S.spec_cnt = 0;                // next step's set starts empty (all read it)
-    const uint32_t n = s_n < kSpecCap ? s_n : kSpecCap;
-    {   // partials of k_score, and (1) the set -> smem + histogram, in one pass
-        uint32_t pend = 0, drop = 0, err = 0, ref = 0;
-        uint64_t mn = kNone, cost = 0;
+        uint32_t pend, drop, err = 0, ref;
+        uint64_t mn, cost;
         if (kBig) {                                        // k_spec already reduced them into ctrl
-            if (tid == 0) { pend = ctrl->n_pending; drop = ctrl->n_dropped; mn = ctrl->min_img; cost = ctrl->tot_cost;
-                            ref = ctrl->n_refresh; }
-        } else if (tid == 0) {                             // k_score's global record; reset for the next step
+            pend = ctrl->n_pending; drop = ctrl->n_dropped; mn = ctrl->min_img; cost = ctrl->tot_cost;
+            ref = ctrl->n_refresh;
+        } else {                                           // k_score's global record; reset for the next step
             BlockPart* g = S.gpart;
             pend = __ldcg(&g->n_pending); drop = __ldcg(&g->n_dropped); err = __ldcg(&g->err);
             cost = __ldcg(&g->tot_cost); ref = __ldcg(&g->refresh); mn = __ldcg(&g->min_img);
             g->n_pending = 0; g->n_dropped = 0; g->err = 0; g->tot_cost = 0; g->refresh = 0; g->min_img = kNone;
         }
-        if (kBig) {
-            for (uint32_t i = tid; i < n; i += kSpecThreads) {
-                const uint64_t img = S.spec_img[i];
-                const uint32_t cs = S.spec_cost[i];
-                s_img[i] = img; s_cost[i] = cs;
-                atomicAdd(&s_hist[spec_bin(img, t_img)], kPackCount | cs);
-            }
-        }
-        pend = warp_sum(pend); drop = warp_sum(drop); err = __reduce_or_sync(0xffffffffu, err);
-        mn = warp_min_u64(mn); cost = warp_sum(cost); ref = warp_sum(ref);
-        if (lane == 0) {
-            atomicAdd(&s_pend, pend); atomicAdd(&s_drop, drop); atomicOr(&s_err, err); atomicAdd(&s_ref, ref);
-            atomicMin(&s_min, (unsigned long long)mn); atomicAdd(&s_cost_tot, (unsigned long long)cost);
+        s_pend = pend; s_drop = drop; s_err = err; s_ref = ref; s_min = mn; s_cost_tot = cost;
+        s_n = n_set;
+        s_first = kSpecBins; s_nsel = 0; s_ncd = 0; s_min_above = kNone; s_above = 0; s_fb = 0;
+        ctrl->spec_n = n_set;
+        ctrl->n_pending = pend; ctrl->n_dropped = drop; ctrl->min_img = mn; ctrl->tot_cost = cost;
+        ctrl->n_refresh = ref;
+        if (err) ctrl->error |= 1u;
+    }
+    if (kBig) for (uint32_t b = tid; b < kSpecBins; b += kSpecThreads) s_hist[b] = 0;
+    __syncthreads();
+    if (!kBig && tid == 0) *S.spec_cnt = 0;                // next step's set starts empty (all read it)
+    const uint32_t n = s_n < kSpecCap ? s_n : kSpecCap;
+    if (kBig) {                                            // (1) the set -> smem + histogram
+        for (uint32_t i = tid; i < n; i += kSpecThreads) {
+            const uint64_t img = S.spec_img[i];
+            const uint32_t cs = S.spec_cost[i];
+            s_img[i] = img; s_cost[i] = cs;
+            atomicAdd(&s_hist[spec_bin(img, t_img)], kPackCount | cs);
         }
         __syncthreads();
-        if (tid == 0) {
-            ctrl->n_pending = s_pend; ctrl->n_dropped = s_drop; ctrl->min_img = s_min; ctrl->tot_cost = s_cost_tot;
-            ctrl->n_refresh = s_ref;
-            if (s_err) ctrl->error |= 1u;
-        }
     }
     if (reduce_only) return;                               // sharded step: the radix path follows
     stamp(ctrl, 1);
