@@ -589,13 +589,23 @@ __device__ __forceinline__ uint64_t call_key(uint64_t Gt, uint32_t fr, const Cfg
 template <bool kDebug, bool kAppB, bool kStaged>
 __device__ __forceinline__ void cmp_range(const Pool& P, const Table& T, const GroupFast* s_g, const Cfg& c,
                                           const Scratch& S, int64_t now, int64_t v, uint64_t t_guess,
-                                          const CRange rg, unsigned long long* s_T, unsigned long long* s_G,
+                                          const CRange rg, unsigned long long* s_TG, uint32_t tbz,
                                           long long* s_R, double* s_rate, const TileBuf* B, uint64_t* empty, Acc& A) {
     const uint32_t tid = threadIdx.x;
     const uint32_t ntl = rg.t1 - rg.t0;
+#ifdef JIT_TG_DOUBLE
+    // s_T / s_G arrive zeroed: the task sums are double-buffered (tbz bit 0 = this range's buffer),
+    // and phase B of a range clears the other buffer's first tbz >> 1 entries (the previous range's
+    // tasks; every thread is past that range's phase C once this range's A -> B barrier is passed)
+    unsigned long long* s_T = s_TG + 2 * (tbz & 1u) * kTile;
+    unsigned long long* s_G = s_T + kTile;
+#else
+    unsigned long long* s_T = s_TG;
+    unsigned long long* s_G = s_T + kTile;
     __syncthreads();                                       // the previous range's phase C is done with s_T / s_G
     for (uint32_t i = tid; i < ntl; i += kScoreThreads) { s_T[i] = 0; s_G[i] = 0; }
     __syncthreads();
+#endif
     const uint32_t qbase = rg.r0 & ~3u;
     const bool single = kStaged || rg.r1 - qbase <= kTile;
     uint32_t kf[kRPT] = {}, kt[kRPT] = {}, kc[kRPT] = {}, kl[kRPT] = {};   // kf: 0x80000000 | frames if pending
@@ -692,6 +702,12 @@ __device__ __forceinline__ void cmp_range(const Pool& P, const Table& T, const G
         s_T[i] = (unsigned long long)__double_as_longlong(okB ? __ull2double_rn(B) : -1.0);
         if (kDebug) { s_R[i] = trem; s_rate[i] = make_rate(Tsum, trem); }
     }
+#ifdef JIT_TG_DOUBLE
+    {
+        unsigned long long* z = s_TG + 2 * ((tbz & 1u) ^ 1u) * kTile;
+        for (uint32_t i = tid; i < (tbz >> 1); i += kScoreThreads) { z[i] = 0; z[kTile + i] = 0; }
+    }
+#endif
     __syncthreads();
     // ---- phase C: the key of every pending call (a5 over the task aggregate)
     if (single) {
@@ -787,10 +803,15 @@ __device__ __forceinline__ void stage_item(const Pool& P, const CRange& rg, bool
     }
 }
 
+#ifdef JIT_TG_DOUBLE
+constexpr uint32_t kTGBuffers = 2;
+#else
+constexpr uint32_t kTGBuffers = 1;
+#endif
 // dynamic shared memory of k_score: the tile ring + the task sums (+ debug per-task outputs)
 // (the SLO-group table sits at the end, sized by the handle's group count)
 __host__ __device__ constexpr uint32_t score_smem_bytes(bool debug, uint32_t n_groups = 256) {
-    return kStages * (uint32_t)sizeof(TileBuf) + 16u * kTile + (debug ? 16u * kTile : 0u) +
+    return kStages * (uint32_t)sizeof(TileBuf) + kTGBuffers * 16u * kTile + (debug ? 16u * kTile : 0u) +
            (uint32_t)sizeof(GroupFast) * n_groups;
 }
 
@@ -804,9 +825,8 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
                                                                          Scratch S, int64_t now, int64_t v) {
     extern __shared__ __align__(128) unsigned char smem[];
     TileBuf* buf = reinterpret_cast<TileBuf*>(smem);
-    unsigned long long* s_T = reinterpret_cast<unsigned long long*>(smem + kStages * sizeof(TileBuf));
-    unsigned long long* s_G = s_T + kTile;
-    long long* s_R = reinterpret_cast<long long*>(s_G + kTile);          // kDebug only
+    unsigned long long* s_TG = reinterpret_cast<unsigned long long*>(smem + kStages * sizeof(TileBuf));  // task sums
+    long long* s_R = reinterpret_cast<long long*>(s_TG + kTGBuffers * 2 * kTile);   // kDebug only
     double* s_rate = reinterpret_cast<double*>(s_R + kTile);              // kDebug only
     GroupFast* s_g = reinterpret_cast<GroupFast*>(smem + score_smem_bytes(kDebug, 0));
     __shared__ __align__(8) uint64_t s_full[kStages], s_empty[kStages];
@@ -829,6 +849,9 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
         for (uint32_t j = 0; j + 1 < kStages; ++j) produce(blockIdx.x + j * G, j);
     }
     for (uint32_t gi = tid; gi < n_groups; gi += kScoreThreads) s_g[gi] = make_fast(groups[gi]);
+#ifdef JIT_TG_DOUBLE
+    for (uint32_t i = tid; i < 4 * kTile; i += kScoreThreads) s_TG[i] = 0;
+#endif
     // first kernel of the step: a fresh control block (nothing else touches ctrl during this
     // kernel) and cleared fallback histograms, spread over the CTAs
     if (blockIdx.x == 0) reset_ctrl_block(ctrl, now, v);
@@ -840,6 +863,7 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
     pdl_launch_dependents();                               // k_spec may launch now (it waits for us)
     Acc A{0u, 0u, 0u, 0u, kNone, 0u, __longlong_as_double((long long)kNone)};
     uint32_t cpar = 0;                                     // consumer: per-slot parity of the fills consumed
+    uint32_t tbz = 0;                                      // JIT_TG_DOUBLE: task-sum buffer | entries to clear << 1
     uint32_t s = 0;
     for (uint32_t it = blockIdx.x; it < n_items; it += G, s = (s + 1 == kStages) ? 0u : s + 1) {
         if (tid == 0) produce(it + (kStages - 1) * G, s == 0 ? kStages - 1 : s - 1);
@@ -849,9 +873,11 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
             std_quad<kDebug, kAppB>(P, T, s_g, c, S, now, v, t_guess, rg.r0 + kRPT * tid, rg.r1, &buf[s], kRPT * tid, &s_empty[s], A);
         } else if (stageable(rg)) {
             mbar_wait(&s_full[s], (cpar >> s) & 1u); cpar ^= 1u << s;
-            cmp_range<kDebug, kAppB, true>(P, T, s_g, c, S, now, v, t_guess, rg, s_T, s_G, s_R, s_rate, &buf[s], &s_empty[s], A);
+            cmp_range<kDebug, kAppB, true>(P, T, s_g, c, S, now, v, t_guess, rg, s_TG, tbz, s_R, s_rate, &buf[s], &s_empty[s], A);
+            tbz = ((rg.t1 - rg.t0) << 1) | ((tbz & 1u) ^ 1u);
         } else {
-            cmp_range<kDebug, kAppB, false>(P, T, s_g, c, S, now, v, t_guess, rg, s_T, s_G, s_R, s_rate, nullptr, nullptr, A);
+            cmp_range<kDebug, kAppB, false>(P, T, s_g, c, S, now, v, t_guess, rg, s_TG, tbz, s_R, s_rate, nullptr, nullptr, A);
+            tbz = ((rg.t1 - rg.t0) << 1) | ((tbz & 1u) ^ 1u);
         }
     }
     {
