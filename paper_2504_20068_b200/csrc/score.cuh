@@ -120,6 +120,10 @@ __device__ __forceinline__ void spec_fallback(Ctrl* ctrl, int* fb) {
 // Element i's rank in the priority order (key desc, id asc) and its inclusive cost prefix come
 // from one pass over the set (shared-memory broadcast reads), so B* = #{i : rank_i < B_max and
 // prefix_i <= tau} (monotone in the rank) is one barrier count; the same for Cd's (len, id) order.
+#ifndef JIT_SPEC_UNROLL
+#define JIT_SPEC_UNROLL 5              // the window argmax's shuffle levels (1: a loop, smaller code)
+#endif
+constexpr int kSpecUnroll = JIT_SPEC_UNROLL;
 constexpr uint32_t kSpecFast = 256;
 constexpr uint32_t kSpecFastChunk = 1u << 24;   // costs <= chunk: kSpecFast costs sum below 2^32
 // priority-order rank record: (key image, id) as one 96-bit word V = img_hi : img_lo : ~id, so
@@ -135,6 +139,7 @@ __device__ __forceinline__ uint32_t before_mask(const uint4& q, const uint4& me)
         "subc.cc.u32 %0, %4, %7;\n\t"
         "subc.u32 %1, 0, 0;"
         : "=&r"(t), "=r"(b) : "r"(me.x), "r"(me.y), "r"(me.z), "r"(q.x), "r"(q.y), "r"(q.z));
+    (void)t;
     return b;                                   // 0xFFFFFFFF when q precedes me, else 0
 }
 struct SpecEl {                 // one element of the speculative set, preloaded by k_spec
@@ -264,12 +269,35 @@ static __device__ __forceinline__ void spec_fast(const Pool& P, const Cfg& c, Ct
             cv = f_cost[e];
             fv = (u128)fixed_point(__longlong_as_double((long long)f_img[e]));    // A19
         }
-        uint64_t tc;
-        u128 tf;
-        const uint64_t ec = block_exclusive_scan_u64(cv, f_scan, &tc);
-        const u128 ef = block_exclusive_scan_u128(fv, f_scan128, &tf);
-        if (tid < ncd) { pc[tid] = ec; pf[tid] = ef; }
-        if (tid == 0) { pc[ncd] = tc; pf[ncd] = tf; }
+        // one exclusive block scan of the pair (two barriers, not two scans of three)
+        uint64_t xc = cv;
+        u128 xf = fv;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t yc = __shfl_up_sync(0xffffffffu, xc, o);
+            const u128 yf = shfl_up_u128(xf, o);
+            if (lane >= o) { xc += yc; xf += yf; }
+        }
+        if (lane == 31) { f_scan[wid] = xc; f_scan128[wid] = xf; }
+        __syncthreads();
+        constexpr int nw = NT / 32;
+        if (wid == 0) {
+            uint64_t sc = lane < nw ? f_scan[lane] : 0ull;
+            u128 sf = lane < nw ? f_scan128[lane] : (u128)0;
+#pragma unroll
+            for (int o = 1; o < nw; o <<= 1) {
+                const uint64_t yc = __shfl_up_sync(0xffffffffu, sc, o);
+                const u128 yf = shfl_up_u128(sf, o);
+                if (lane >= o) { sc += yc; sf += yf; }
+            }
+            if (lane < nw) { f_scan[lane] = sc; f_scan128[lane] = sf; }
+        }
+        __syncthreads();
+        if (tid < ncd) {
+            pc[tid] = (wid ? f_scan[wid - 1] : 0ull) + xc - cv;
+            pf[tid] = (wid ? f_scan128[wid - 1] : (u128)0) + xf - fv;
+        }
+        if (tid == 0) { pc[ncd] = f_scan[nw - 1]; pf[ncd] = f_scan128[nw - 1]; }
     }
     __syncthreads();
     stamp(ctrl, 5);
@@ -285,7 +313,7 @@ static __device__ __forceinline__ void spec_fast(const Pool& P, const Cfg& c, Ct
         }
         best = pf[lo + 1] - pf[tid]; bi = tid; bj = lo;
     }
-#pragma unroll
+#pragma unroll kSpecUnroll
     for (int o = 16; o > 0; o >>= 1) {
         const u128 ob = shfl_xor_u128(best, o);
         const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o), oj = __shfl_xor_sync(0xffffffffu, bj, o);
@@ -296,7 +324,7 @@ static __device__ __forceinline__ void spec_fast(const Pool& P, const Cfg& c, Ct
     if (wid == 0) {
         constexpr int nw = NT / 32;
         best = lane < nw ? f_best[lane] : (u128)0; bi = lane < nw ? f_bi[lane] : 0xFFFFFFFFu; bj = lane < nw ? f_bj[lane] : 0;
-#pragma unroll
+#pragma unroll kSpecUnroll
         for (int o = 16; o > 0; o >>= 1) {
             const u128 ob = shfl_xor_u128(best, o);
             const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o), oj = __shfl_xor_sync(0xffffffffu, bj, o);
