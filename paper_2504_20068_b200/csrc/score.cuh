@@ -383,6 +383,9 @@ static __device__ __forceinline__ void spec_fast(const Pool& P, const Cfg& c, Ct
 // partial counts are reduced per CTA, then added atomically into one global record.
 // --------------------------------------------------------------------------------------
 #ifndef JIT_EXACT_TU
+#ifndef JIT_ITEM_SNAKE
+#define JIT_ITEM_SNAKE 1
+#endif
 #ifndef JIT_SCORE_MINB
 #define JIT_SCORE_MINB 3
 #endif
@@ -861,6 +864,20 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
     const uint32_t tid = threadIdx.x;
     const uint32_t n_items = S.n_std + S.n_crange;
     const uint32_t G = gridDim.x;
+    // the CTA's item of round r (r-th pass over the grid).  JIT_ITEM_SNAKE: compound ranges (the
+    // heavier items) first, and odd rounds walk the grid backwards, so the CTAs that draw a
+    // compound range in the partial rounds are not the ones that draw an item in the last round
+    const uint32_t bx = blockIdx.x;
+    auto item_at = [&](uint32_t r) -> uint32_t {
+#if JIT_ITEM_SNAKE
+        const uint32_t lg = r * G + ((r & 1u) ? G - 1u - bx : bx);
+        if (lg >= n_items) return 0xFFFFFFFFu;
+        return lg < S.n_crange ? S.n_std + lg : lg - S.n_crange;
+#else
+        const uint32_t lg = r * G + bx;
+        return lg < n_items ? lg : 0xFFFFFFFFu;
+#endif
+    };
     uint32_t fpar = 0, fused = 0;                          // thread 0, per slot: fill-count parity, ever filled
     // thread 0: fill slot s with item it (after every thread released the slot's previous fill)
     auto produce = [&](uint32_t it, uint32_t s) {
@@ -874,7 +891,7 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
     if (tid == 0) {
         for (uint32_t s = 0; s < kStages; ++s) { mbar_init(&s_full[s], 1); mbar_init(&s_empty[s], kScoreThreads); }
         mbar_init_fence();
-        for (uint32_t j = 0; j + 1 < kStages; ++j) produce(blockIdx.x + j * G, j);
+        for (uint32_t j = 0; j + 1 < kStages; ++j) produce(item_at(j), j);
     }
     for (uint32_t gi = tid; gi < n_groups; gi += kScoreThreads) s_g[gi] = make_fast(groups[gi]);
 #ifdef JIT_TG_DOUBLE
@@ -893,8 +910,10 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
     uint32_t cpar = 0;                                     // consumer: per-slot parity of the fills consumed
     uint32_t tbz = 0;                                      // JIT_TG_DOUBLE: task-sum buffer | entries to clear << 1
     uint32_t s = 0;
-    for (uint32_t it = blockIdx.x; it < n_items; it += G, s = (s + 1 == kStages) ? 0u : s + 1) {
-        if (tid == 0) produce(it + (kStages - 1) * G, s == 0 ? kStages - 1 : s - 1);
+    for (uint32_t r = 0;; ++r, s = (s + 1 == kStages) ? 0u : s + 1) {
+        const uint32_t it = item_at(r);
+        if (it == 0xFFFFFFFFu) break;
+        if (tid == 0) produce(item_at(r + kStages - 1), s == 0 ? kStages - 1 : s - 1);
         const CRange rg = item_rows(P, S, it);
         if (it < S.n_std) {
             mbar_wait(&s_full[s], (cpar >> s) & 1u); cpar ^= 1u << s;
