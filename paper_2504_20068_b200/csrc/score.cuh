@@ -125,7 +125,7 @@ __device__ __forceinline__ void spec_fallback(Ctrl* ctrl, int* fb) {
 #endif
 constexpr int kSpecUnroll = JIT_SPEC_UNROLL;
 constexpr uint32_t kSpecFast = 256;
-constexpr uint32_t kSpecFastChunk = 1u << 24;   // costs <= chunk: kSpecFast costs sum below 2^32
+constexpr uint32_t kSpecFastChunk = (1u << 24) - 1;   // costs <= chunk: kSpecFast costs sum below 2^32
 // priority-order rank record: (key image, id) as one 96-bit word V = img_hi : img_lo : ~id, so
 // "q before me" (key desc, id asc) is V_q > V_me -- the borrow of V_me - V_q (three subtractions);
 // w = -cost, so borrow_mask * w adds cost
@@ -954,7 +954,10 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
 //      sorted by (len, id), scanned, and the first argmax window is taken.
 // No full sort of S, and no pool gathers until the batch is written.
 // --------------------------------------------------------------------------------------
-constexpr uint32_t kSpecThreads = 512;
+#ifndef JIT_SPEC_THREADS
+#define JIT_SPEC_THREADS 512
+#endif
+constexpr uint32_t kSpecThreads = JIT_SPEC_THREADS;
 constexpr uint32_t kSpecWindow = 2048;        // |Cd| windowed in this CTA (larger: k_group)
 constexpr uint32_t kSelCap = 2048;            // boundary-bin entries ordered in this CTA
 constexpr uint32_t kSpecBins = 2048;
