@@ -162,7 +162,6 @@ static __device__ __forceinline__ void spec_fast(const Pool& P, const Cfg& c, Ct
     __shared__ uint64_t f_scan[32];
     __shared__ u128 f_scan128[32];
     __shared__ uint64_t f_bp_img;
-    __shared__ int f_fb;
     __shared__ u128 f_best[32];
     __shared__ uint32_t f_bi[32], f_bj[32];
     const uint32_t tid = threadIdx.x;
@@ -177,7 +176,7 @@ static __device__ __forceinline__ void spec_fast(const Pool& P, const Cfg& c, Ct
         f_img[tid] = img; f_id[tid] = id; f_cost[tid] = cost;
         f_rank2[tid] = 0; f_pre2[tid] = 0;
     }
-    if (tid == 0) { f_fb = 0; f_bp_img = kNone; }
+    if (tid == 0) f_bp_img = kNone;
     __syncthreads();
     stamp(ctrl, 2);
     // (a7) rank in the priority order and inclusive cost prefix.  The n^2 comparisons are spread
@@ -214,25 +213,28 @@ static __device__ __forceinline__ void spec_fast(const Pool& P, const Cfg& c, Ct
     if (fits && rank + 1 == bstar) f_bp_img = img;          // the B*-th request (A15)
     __syncthreads();
     stamp(ctrl, 3);
-    if (tid == 0) {
-        if (bstar == 0) { ctrl->error |= 1u; ctrl->status = ST_ERROR; f_fb = 2; }
-        else {
-            // every entry of S fits: exact only when S is the whole pending set (bp = min key)
-            if (bstar == n && !whole) spec_fallback(ctrl, &f_fb);
-            else {
-                const uint64_t bimg = bstar == n ? min_img : f_bp_img;
-                const double bp = __longlong_as_double((long long)bimg);
-                const double thr = __dmul_rn(c.p, bp);   // A16
-                const uint64_t ti = (uint64_t)__double_as_longlong(thr);
-                if (!whole && ti < t_img) spec_fallback(ctrl, &f_fb);   // Cd may leave S
-                else { ctrl->b_star = bstar; ctrl->bp = bp; ctrl->thr = thr; ctrl->thr_img = ti; f_bp_img = ti; }
-            }
+    // every thread derives bp, thr and the exactness verdict from the same block-uniform values
+    // (no serial thread-0 section and no broadcast barrier); thread 0 records them
+    uint64_t thr_img = 0;
+    {
+        int fb = 0;
+        double bp = 0.0, thr = 0.0;
+        if (bstar == 0) fb = 2;
+        else if (bstar == n && !whole) fb = 1;          // every entry of S fits: exact only when S
+        else {                                          // is the whole pending set (bp = min key)
+            bp = __longlong_as_double((long long)(bstar == n ? min_img : f_bp_img));
+            thr = __dmul_rn(c.p, bp);                   // A16
+            thr_img = (uint64_t)__double_as_longlong(thr);
+            if (!whole && thr_img < t_img) fb = 1;      // Cd may leave S
         }
+        if (tid == 0) {
+            if (fb == 2) { ctrl->error |= 1u; ctrl->status = ST_ERROR; }
+            else if (fb == 1) { ctrl->status = ST_FALLBACK; ctrl->fallback = 1; }
+            else { ctrl->b_star = bstar; ctrl->bp = bp; ctrl->thr = thr; ctrl->thr_img = thr_img; }
+        }
+        if (fb) return;
     }
-    __syncthreads();
-    if (f_fb) return;
     // (a8) Cd = {key >= thr}; (a9) its (len, id) order (A17/A18)
-    const uint64_t thr_img = f_bp_img;
     const bool cd = own && img >= thr_img;
     const uint64_t wk = ((uint64_t)len << 32) | id;
     // Cd is a prefix of the priority order: its elements hold the ranks 0..|Cd|-1, which serve as
