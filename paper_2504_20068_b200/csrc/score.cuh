@@ -389,7 +389,7 @@ static __device__ __forceinline__ void spec_fast(const Pool& P, const Cfg& c, Ct
 #define JIT_ITEM_SNAKE 1
 #endif
 #ifndef JIT_SCORE_MINB
-#define JIT_SCORE_MINB 3
+#define JIT_SCORE_MINB 6
 #endif
 struct Acc {
     uint32_t pend, drop, err, ref;

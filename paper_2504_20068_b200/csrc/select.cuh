@@ -21,7 +21,7 @@ constexpr uint32_t kBucketCap = 4096;
 constexpr uint32_t kSpecCap = 8192;            // speculative set resolved in shared memory up to this size
 constexpr uint32_t kGroupSmemSort = 8192;     // |Cd| sorted in shared memory up to this size
 #ifndef JIT_SCORE_THREADS
-#define JIT_SCORE_THREADS 256
+#define JIT_SCORE_THREADS 128
 #endif
 constexpr uint32_t kScoreThreads = JIT_SCORE_THREADS;
 #ifndef JIT_RPT
