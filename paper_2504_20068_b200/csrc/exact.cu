@@ -35,7 +35,8 @@ cudaError_t init_attributes() {
 
 cudaError_t spec(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int reduce_only, cudaStream_t s, bool pdl) {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(1); cfg.blockDim = dim3(kSpecThreads); cfg.dynamicSmemBytes = kSpecSmem; cfg.stream = s;
+    // k_spec only runs the small-set resolve (a larger set goes to k_spec_big): its smem is small
+    cfg.gridDim = dim3(1); cfg.blockDim = dim3(kSpecThreads); cfg.dynamicSmemBytes = kSpecFastSmem; cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;

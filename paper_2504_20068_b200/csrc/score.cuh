@@ -142,6 +142,10 @@ __device__ __forceinline__ uint32_t before_mask(const uint4& q, const uint4& me)
     (void)t;
     return b;                                   // 0xFFFFFFFF when q precedes me, else 0
 }
+// dynamic shared memory of the small-set resolve (f_rec, f_img, f_id, f_cost, f_wk, pc, pf, o_elem):
+// k_spec launches with only this much, so its CTA fits beside k_score's draining CTAs early
+constexpr uint32_t kSpecFastSmem = 16 * kSpecFast + 8 * kSpecFast + 4 * kSpecFast + 4 * kSpecFast + 8 * kSpecFast +
+                                   8 * (kSpecFast + 2) + 16 * (kSpecFast + 1) + 4 * kSpecFast;
 struct SpecEl {                 // one element of the speculative set, preloaded by k_spec
     uint64_t img;
     uint32_t id, cost, len, row, meta, aux;
