@@ -319,27 +319,24 @@ static __device__ __forceinline__ void spec_fast(const Pool& P, const Cfg& c, Ct
         }
         best = pf[lo + 1] - pf[tid]; bi = tid; bj = lo;
     }
-#pragma unroll kSpecUnroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const u128 ob = shfl_xor_u128(best, o);
-        const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o), oj = __shfl_xor_sync(0xffffffffu, bj, o);
-        if ((oi != 0xFFFFFFFFu) && (bi == 0xFFFFFFFFu || ob > best || (ob == best && oi < bi))) { best = ob; bi = oi; bj = oj; }
-    }
-    if (lane == 0) { f_best[wid] = best; f_bi[wid] = bi; f_bj[wid] = bj; }
-    __syncthreads();
-    if (wid == 0) {
-        constexpr int nw = NT / 32;
-        best = lane < nw ? f_best[lane] : (u128)0; bi = lane < nw ? f_bi[lane] : 0xFFFFFFFFu; bj = lane < nw ? f_bj[lane] : 0;
+    const uint32_t nwc = (ncd + 31) >> 5;                  // warps holding window starts (ncd >= 1: bp is in Cd)
+    if ((uint32_t)wid < nwc) {
 #pragma unroll kSpecUnroll
         for (int o = 16; o > 0; o >>= 1) {
             const u128 ob = shfl_xor_u128(best, o);
             const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o), oj = __shfl_xor_sync(0xffffffffu, bj, o);
             if ((oi != 0xFFFFFFFFu) && (bi == 0xFFFFFFFFu || ob > best || (ob == best && oi < bi))) { best = ob; bi = oi; bj = oj; }
         }
-        if (lane == 0) { f_bi[0] = bi; f_bj[0] = bj; }
+        if (lane == 0) { f_best[wid] = best; f_bi[wid] = bi; f_bj[wid] = bj; }
     }
     __syncthreads();
-    bi = f_bi[0]; bj = f_bj[0];
+    // every thread reduces the per-warp winners in warp (= start position) order; strict > keeps
+    // the first maximum -- no second barrier
+    best = f_best[0]; bi = f_bi[0]; bj = f_bj[0];
+    for (uint32_t w = 1; w < nwc; ++w) {
+        const u128 ob = f_best[w];
+        if (ob > best) { best = ob; bi = f_bi[w]; bj = f_bj[w]; }
+    }
     stamp(ctrl, 6);
     // the batch in window order and its bookkeeping: ever_scheduled, Running, undo steps_waited+1
     const uint32_t ns = bj - bi + 1;
