@@ -243,3 +243,23 @@ def test_time_scoring_leaves_state_consistent():
         got = s.step(d["now_ns"], d["v_token_ns"])
         _compare(got, ref, ctx=f"after time_scoring n_spec={got['n_spec']} fallback={got['fallback']}")
         s.close()
+
+
+def test_large_prefill_chunk_routes_small_sets_to_histogram_resolve():
+    """The small-set resolve keeps 32-bit cost prefixes, valid while |S| * chunk < 2^32
+    (kSpecFastChunk); a larger chunk (here 2^24 with tau = 2^26) must route even small speculative
+    sets through k_spec_big -- every step still equal to the oracle (S:417 allows any chunk <= tau)."""
+    d = W.pool_snapshot(23, 60_000, table_draws=1 << 16)
+    d["cfg"] = W.default_config(token_budget=1 << 26, max_batch=64, prefill_chunk=1 << 24)
+    s = _sched(d, debug=False)
+    s.load(d["pool"], d["tasks"])
+    pool = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in d["pool"].items()}
+    resolved = 0
+    for k in range(3):
+        ref = oracle.step(d["cfg"], d["groups"], d["table"], d["now_ns"], d["v_token_ns"], pool, d["tasks"])
+        got = s.step(d["now_ns"], d["v_token_ns"])
+        _compare(got, ref, ctx=f"step {k} n_spec={got['n_spec']} fallback={got['fallback']}")
+        resolved += int(k > 0 and not got["fallback"])
+        pool["meta"], pool["aux"] = ref["meta"], ref["aux"]
+    s.close()
+    assert resolved >= 1
