@@ -1,11 +1,13 @@
 // score.cuh -- the streaming pass over the pool (a1)-(a6) and the speculative resolve.
 //
-//   k_score  every row, 4 consecutive rows per thread with 128-bit SoA loads / stores; standalone
-//            rows get their key image (a5) and cost (a6); compound calls are scored by CTAs that
-//            own whole tasks, so the task aggregate (a4) and the calls' keys come out of the
-//            same pass (shared-memory sums, no global atomics).  Per-CTA partial counts go to
-//            an array (no global atomics on a shared line).
-//   k_spec   one CTA: exact B*, bp, thr, Cd from the speculative set.
+//   k_score  every row: persistent 128-thread CTAs (6 per SM) walk 256-row work items whose
+//            SoA slices are staged into a shared-memory ring by bulk (TMA 1-D) copies, kRPT = 2
+//            consecutive rows per thread; standalone rows get their key image (a5) and cost
+//            (a6); compound calls are scored by CTAs that own whole tasks, so the task aggregate
+//            (a4) and the calls' keys come out of the same pass (shared-memory sums, no global
+//            atomics).  Per-CTA partial counts are reduced in the CTA and added once into a
+//            global record.
+//   k_spec   one CTA: exact B*, bp, thr, Cd and the window from the speculative set.
 #pragma once
 #include "select.cuh"
 
