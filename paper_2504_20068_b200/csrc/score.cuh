@@ -126,6 +126,11 @@ __device__ __forceinline__ void spec_fallback(Ctrl* ctrl, int* fb) {
 #define JIT_SPEC_UNROLL 5              // the window argmax's shuffle levels (1: a loop, smaller code)
 #endif
 constexpr int kSpecUnroll = JIT_SPEC_UNROLL;
+#ifndef JIT_SPEC_BUCKET
+#define JIT_SPEC_BUCKET 0              // 1: small-set ranks by a counting sort on the key image
+#endif
+constexpr uint32_t kFB = 1024;         // JIT_SPEC_BUCKET bins: 128 per octave of the key above t
+constexpr uint32_t kFBShift = 45;
 constexpr uint32_t kSpecFast = 256;
 constexpr uint32_t kSpecFastChunk = (1u << 24) - 1;   // costs <= chunk: kSpecFast costs sum below 2^32
 // priority-order rank record: (key image, id) as one 96-bit word V = img_hi : img_lo : ~id, so
@@ -183,8 +188,52 @@ static __device__ __forceinline__ void spec_fast(const Pool& P, const Cfg& c, Ct
         f_rank2[tid] = 0; f_pre2[tid] = 0;
     }
     if (tid == 0) f_bp_img = kNone;
+#if JIT_SPEC_BUCKET
+    __shared__ unsigned long long f_h[kFB + 1];           // per bin: count << 32 | cost; then the prefix
+    __shared__ uint4 f_srt[kSpecFast];                     // rank records grouped by bin
+    __shared__ uint64_t f_bscan[32];
+    for (uint32_t i = tid; i <= kFB; i += NT) f_h[i] = 0ull;
+#endif
     __syncthreads();
     stamp(ctrl, 2);
+#if JIT_SPEC_BUCKET
+    // (a7) rank and cost prefix via a counting sort on the key image: bins of 2^-7 relative width
+    // above t (the top bin open-ended) in priority order (rb = 0: the highest keys); an element's
+    // rank / prefix = the bins before its own (one block scan) + the elements of its own bin
+    // that precede it (one 96-bit comparison each)
+    {
+        uint32_t rb = 0, slot = 0;
+        if (own) {
+            const uint64_t d = img > t_img ? (img - t_img) >> kFBShift : 0ull;
+            rb = kFB - 1u - (uint32_t)(d >= kFB - 1u ? kFB - 1u : d);
+            slot = (uint32_t)(atomicAdd(&f_h[rb], (1ull << 32) | cost) >> 32);
+        }
+        __syncthreads();
+        static_assert(kFB % NT == 0, "bins per thread");
+        constexpr uint32_t kPer = kFB / NT;                // bins per thread
+        unsigned long long loc[kPer], v = 0;
+#pragma unroll
+        for (uint32_t k = 0; k < kPer; ++k) { loc[k] = f_h[tid * kPer + k]; v += loc[k]; }
+        unsigned long long tot;
+        unsigned long long base = block_exclusive_scan_u64(v, f_bscan, reinterpret_cast<uint64_t*>(&tot));
+#pragma unroll
+        for (uint32_t k = 0; k < kPer; ++k) { f_h[tid * kPer + k] = base; base += loc[k]; }
+        if (tid == 0) f_h[kFB] = tot;
+        __syncthreads();
+        const uint4 me = own ? f_rec[tid] : make_uint4(0u, 0u, 0u, 0u);
+        const unsigned long long b0 = own ? f_h[rb] : 0ull;
+        const uint32_t lo = (uint32_t)(b0 >> 32), hi = own ? (uint32_t)(f_h[rb + 1] >> 32) : 0u;
+        if (own) f_srt[lo + slot] = me;
+        __syncthreads();
+        uint32_t ra = lo, pa = (uint32_t)b0;
+        for (uint32_t j = lo; j < hi; ++j) {
+            const uint4 q = f_srt[j];
+            const uint32_t bm = before_mask(q, me);
+            ra -= bm; pa += bm * q.w;
+        }
+        if (own) { f_rank2[tid] = ra; f_pre2[tid] = pa; }
+    }
+#else
     // (a7) rank in the priority order and inclusive cost prefix.  The n^2 comparisons are spread
     // over the whole CTA: element e is counted by F = NT / n threads (tid = e + n * part), each
     // over a 1/F share of the set (16-B broadcast reads, 2 accumulators), summed in shared memory.
@@ -212,6 +261,7 @@ static __device__ __forceinline__ void spec_fast(const Pool& P, const Cfg& c, Ct
         }
         __syncthreads();
     }
+#endif
     uint32_t rank = own ? f_rank2[tid] : 0u;          // own => tid < kSpecFast: written by itself
     const uint64_t pre = own ? (uint64_t)f_pre2[tid] + cost : 0ull;
     const bool fits = own && rank + 1 <= c.max_batch && pre <= c.token_budget;
