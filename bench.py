@@ -268,6 +268,33 @@ def run_sharded(args, ws, rank, dev, stream, barrier, allmax, allsum):
     ms = allmax(e0.elapsed_time(e1) / K)
     total = allsum(float(n))
     n_fast, n_exact = st.n_fast, st.n_exact              # the timed steps' paths (before the e2e leg)
+    # roofline of k_score on every rank (as at N = 1: back-to-back launches rotating over this
+    # rank's shard and 5 more copies of it, to defeat the L2), max over ranks
+    roofline = None
+    try:
+        extra = []
+        for _ in range(5):
+            s2 = Scheduler(d["cfg"], d["groups"], d["table"], capacity=n, task_capacity=nt, device=dev, stream=stream)
+            s2.load(d["pool"], d["tasks"])
+            s2.step(now, v)
+            extra.append(s2)
+        torch.cuda.synchronize()
+        k_ms = allmax(Scheduler.time_scoring([s] + extra, now, v, 60))
+        for s2 in extra:
+            s2.close()
+        n_single = int(d["pool"]["n_single"])
+        alg_bytes = n_single * BYTES_ROW + (n - n_single) * BYTES_CALL + nt * BYTES_TASK
+        pk = peaks()
+        hbm_peak = pk["hbm_gbs"] if pk else 6650.0
+        tr = ncu_traffic()
+        achieved = alg_bytes / (k_ms / 1e3) / 1e9
+        roofline = {"bound": "hbm", "kernel": "k_score", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": achieved / hbm_peak, "traffic": tr["bytes_per_launch"] if tr else None,
+                    "alg_bytes_per_launch": alg_bytes, "k_score_ms": k_ms,
+                    "how": "per rank: 60 back-to-back k_score launches over 6 copies of its shard "
+                           "(jit_sched_time_scoring), max over ranks"}
+    except Exception as ex:  # pragma: no cover
+        roofline = {"error": str(ex)[:200]}
     # e2e through the C ABI: every rank loads its shard from pinned host buffers (H2D) and runs the
     # sharded step (exchange + batch D2H); wall clock, max over ranks
     e2e = None
@@ -307,7 +334,7 @@ def run_sharded(args, ws, rank, dev, stream, barrier, allmax, allsum):
                            "steps_speculative": n_fast, "steps_exact_protocol": n_exact,
                            "last_batch": {"n_selected": out["n_selected"], "b_star": out["b_star"],
                                           "n_candidates": out["n_candidates"]}},
-                "roofline": None, "cpu_baseline": None, "e2e": e2e,
+                "roofline": roofline, "cpu_baseline": None, "e2e": e2e,
                 "gpu_launches": 3 * n_fast + 18 * n_exact, "clocks": clocks,
                 "replay": replay}
         print(json.dumps(line), flush=True)
