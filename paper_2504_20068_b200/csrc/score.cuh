@@ -172,7 +172,6 @@ static __device__ __forceinline__ void spec_fast(const Pool& P, const Cfg& c, Ct
     uint32_t* o_elem = reinterpret_cast<uint32_t*>(pf + kSpecFast + 1);                  // window position -> element
     __shared__ uint64_t f_scan[32];
     __shared__ u128 f_scan128[32];
-    __shared__ uint64_t f_bp_img;
     __shared__ u128 f_best[32];
     __shared__ uint32_t f_bi[32], f_bj[32];
     const uint32_t tid = threadIdx.x;
@@ -187,7 +186,6 @@ static __device__ __forceinline__ void spec_fast(const Pool& P, const Cfg& c, Ct
         f_img[tid] = img; f_id[tid] = id; f_cost[tid] = cost;
         f_rank2[tid] = 0; f_pre2[tid] = 0;
     }
-    if (tid == 0) f_bp_img = kNone;
 #if JIT_SPEC_BUCKET
     __shared__ unsigned long long f_h[kFB + 1];           // per bin: count << 32 | cost; then the prefix
     __shared__ uint4 f_srt[kSpecFast];                     // rank records grouped by bin
@@ -265,9 +263,10 @@ static __device__ __forceinline__ void spec_fast(const Pool& P, const Cfg& c, Ct
     uint32_t rank = own ? f_rank2[tid] : 0u;          // own => tid < kSpecFast: written by itself
     const uint64_t pre = own ? (uint64_t)f_pre2[tid] + cost : 0ull;
     const bool fits = own && rank + 1 <= c.max_batch && pre <= c.token_budget;
+    __shared__ uint64_t f_byrank[kSpecFast];                // key image by priority rank
+    if (own) f_byrank[rank] = img;
     const uint32_t bstar = (uint32_t)__syncthreads_count(fits);
-    if (fits && rank + 1 == bstar) f_bp_img = img;          // the B*-th request (A15)
-    __syncthreads();
+    const uint64_t bp_img = bstar ? f_byrank[bstar - 1] : kNone;   // the B*-th request (A15)
     stamp(ctrl, 3);
     // every thread derives bp, thr and the exactness verdict from the same block-uniform values
     // (no serial thread-0 section and no broadcast barrier); thread 0 records them
@@ -278,7 +277,7 @@ static __device__ __forceinline__ void spec_fast(const Pool& P, const Cfg& c, Ct
         if (bstar == 0) fb = 2;
         else if (bstar == n && !whole) fb = 1;          // every entry of S fits: exact only when S
         else {                                          // is the whole pending set (bp = min key)
-            bp = __longlong_as_double((long long)(bstar == n ? min_img : f_bp_img));
+            bp = __longlong_as_double((long long)(bstar == n ? min_img : bp_img));
             thr = __dmul_rn(c.p, bp);                   // A16
             thr_img = (uint64_t)__double_as_longlong(thr);
             if (!whole && thr_img < t_img) fb = 1;      // Cd may leave S
