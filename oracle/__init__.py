@@ -91,11 +91,12 @@ class _ReplayCfg(C.Structure):
 class _ReplayResult(C.Structure):
     _fields_ = [("token_goodput", C.c_uint64), ("tokens_processed", C.c_uint64), ("sim_end_ns", C.c_int64)] + \
                [(k, C.c_uint32) for k in ("request_goodput", "n_done", "n_dropped", "steps", "n_tasks_done",
-                                          "error")]
+                                          "n_tasks_dropped", "error", "_pad")]
 
 
 STEP_LOG_DTYPE = np.dtype([("now_ns", "<i8"), ("n_selected", "<u4"), ("total_tokens", "<u4"),
-                           ("n_candidates", "<u4"), ("b_star", "<u4"), ("bp", "<f8"), ("ids_hash", "<u8")])
+                           ("n_candidates", "<u4"), ("b_star", "<u4"), ("bp", "<f8"), ("ids_hash", "<u8"),
+                           ("v_token_ns", "<i8")])
 
 
 def _load():
@@ -248,7 +249,8 @@ def replay(cfg, groups, table, trace, rcfg, log: bool = False, log_ids: bool = F
                        _ptr(L), _ptr(LI))
     out = {"status": st, "token_goodput": res.token_goodput, "tokens_processed": res.tokens_processed,
            "sim_end_ns": res.sim_end_ns, "request_goodput": res.request_goodput, "n_done": res.n_done,
-           "n_dropped": res.n_dropped, "steps": res.steps, "n_tasks_done": res.n_tasks_done}
+           "n_dropped": res.n_dropped, "steps": res.steps, "n_tasks_done": res.n_tasks_done,
+           "n_tasks_dropped": res.n_tasks_dropped}
     if log:
         out["log"] = L[:res.steps].copy()
     if log_ids:

@@ -230,13 +230,15 @@ static int cmp_len_asc_id_asc(const void* a, const void* b) {
     return (x->id > y->id) - (x->id < y->id);
 }
 
-/* task view for the compound pass (a4) */
+/* task view for the compound pass (a4) and the task-level admission drop (a1, reading A40) */
 typedef struct {
     uint32_t n;
     const uint32_t* call_begin; const uint32_t* call_end;   /* current-stage rows */
     const int64_t* arrival_ns; const int64_t* deadline_ns;  /* a_c, D */
     const uint64_t* t_le_s; const uint64_t* t_total;        /* phi(s) = t_le_s / t_total */
     const uint64_t* goodput_done;
+    const uint8_t* ever;                                     /* 1: some call of the task was scheduled */
+    uint8_t* dropped;                                        /* out (may be NULL): 1 if dropped now */
 } task_view;
 
 /* The step.  On return, selected[0..n_selected) holds ROW indices in batch order. */
@@ -264,8 +266,28 @@ static int gmax_step(const og_config* cfg, const og_group* G, uint32_t n_groups,
     double* rate = (double*)calloc(n ? n : 1, sizeof(double));
     int rc = OG_OK;
 
-    /* (a1) admission control, P:545 (A29 strict) + pending set (Alg. 1 GetRequestQueue) */
+    /* (a1) admission control, P:545 ("requests unscheduled beyond [waiting_time] are dropped",
+     * A29 strict) + pending set (Alg. 1 GetRequestQueue).  Reading A40: a compound task is
+     * ONE API request (the API of P:544 creates it); it is dropped when none of its calls has ever
+     * been scheduled and now - a_c > waiting_time, and dropping it drops every call of it that is
+     * still Queued or Waiting.  A standalone request is dropped by its own arrival and flag. */
     uint32_t n_pend = 0;
+    if (TV) {
+        for (uint32_t t = 0; t < TV->n; ++t) {
+            if (TV->dropped) TV->dropped[t] = 0;
+            if (TV->ever[t] || now - TV->arrival_ns[t] <= cfg->waiting_ns) continue;
+            uint32_t hit = 0;
+            for (uint32_t r = TV->call_begin[t]; r < TV->call_end[t]; ++r) {
+                uint32_t st = m_state(meta[r]);
+                if (st == ST_QUEUED || st == ST_WAITING) {
+                    meta[r] = m_set_state(meta[r], ST_DROPPED);
+                    res->n_dropped_now++;
+                    hit = 1;
+                }
+            }
+            if (TV->dropped) TV->dropped[t] = (uint8_t)hit;
+        }
+    }
     for (uint32_t r = 0; r < n; ++r) {
         uint32_t m = meta[r], st = m_state(m), fl = m_flags(m);
         if (arrival[r] > now) continue;
@@ -426,7 +448,8 @@ static int gmax_step(const og_config* cfg, const og_group* G, uint32_t n_groups,
         res->b_star = bstar; res->bp = bp; res->thr = thr;
 
         /* bookkeeping after selection: ever_scheduled / Running for the batch, and
-         * steps_waited += 1 (saturating) for every pending request left out (A12) */
+         * steps_waited += 1 (saturating at 0xFFFF) for every pending request left out; a selected
+         * request keeps its counter ("per frame" waited; reading A12) */
         uint8_t* insel = (uint8_t*)calloc(n, 1);
         for (uint32_t i = 0; i < res->n_selected; ++i) insel[selected[i]] = 1;
         for (uint32_t r = 0; r < n; ++r) {
@@ -436,9 +459,6 @@ static int gmax_step(const og_config* cfg, const og_group* G, uint32_t n_groups,
                 m = m_set_flags(m, m_flags(m) | FL_EVER);
                 if (m_state(m) == ST_QUEUED || m_state(m) == ST_PREEMPTED) m = m_set_state(m, ST_RUNNING);
                 meta[r] = m;
-                /* saturation edge of the 16-bit counter: a selected request whose
-                 * counter is >= 0xFFFE reads 0xFFFF afterwards */
-                if (a_waited(aux[r]) >= 0xFFFEu) aux[r] = (aux[r] & 0xFFFFu) | (0xFFFFu << 16);
             } else {
                 uint32_t w = a_waited(aux[r]);
                 if (w < 0xFFFFu) ++w;
@@ -464,17 +484,21 @@ int og_step(const og_config* cfg, const og_group* groups, uint32_t n_groups,
     uint32_t n = pool->n;
     og_reset_memo();                 /* the memo lives for one call only */
     task_view tv; task_view* tvp = NULL;
-    uint32_t *cb = NULL, *ce = NULL; uint64_t *tle = NULL, *tt = NULL;
+    uint32_t *cb = NULL, *ce = NULL; uint64_t *tle = NULL, *tt = NULL; uint8_t* tever = NULL;
     if (tasks && tasks->n) {
         uint32_t nt = tasks->n;
         cb = (uint32_t*)malloc(4 * nt); ce = (uint32_t*)malloc(4 * nt);
         tle = (uint64_t*)malloc(8 * nt); tt = (uint64_t*)malloc(8 * nt);
+        tever = (uint8_t*)calloc(nt, 1);
         for (uint32_t t = 0; t < nt; ++t) {
             cb[t] = tasks->call_off[t]; ce[t] = tasks->call_off[t + 1];
             uint32_t S = tasks->n_stages[t], s = tasks->cur_stage[t];
             if (S == 0 || S > MAX_STAGES || s >= S || ce[t] < cb[t] || ce[t] > n) {
-                res->error = 1; free(cb); free(ce); free(tle); free(tt); return OG_EINVAL;
+                res->error = 1; free(cb); free(ce); free(tle); free(tt); free(tever); return OG_EINVAL;
             }
+            /* A40: the task has been scheduled iff one of its calls in the pool carries ever_scheduled */
+            for (uint32_t r = cb[t]; r < ce[t]; ++r)
+                if (m_flags(pool->meta[r]) & FL_EVER) tever[t] = 1;
             /* phi(s) = t_{<=s} / t_total over the matched pattern */
             uint64_t le = 0, tot = 0;
             for (uint32_t u = 0; u < S; ++u) {
@@ -486,6 +510,7 @@ int og_step(const og_config* cfg, const og_group* groups, uint32_t n_groups,
         tv.n = nt; tv.call_begin = cb; tv.call_end = ce; tv.arrival_ns = tasks->arrival_ns;
         tv.deadline_ns = tasks->deadline_ns; tv.t_le_s = tle; tv.t_total = tt;
         tv.goodput_done = tasks->goodput_done;
+        tv.ever = tever; tv.dropped = NULL;
         tvp = &tv;
     }
     uint32_t* sel = (uint32_t*)malloc(sizeof(uint32_t) * (n ? n : 1));
@@ -500,7 +525,7 @@ int og_step(const og_config* cfg, const og_group* groups, uint32_t n_groups,
             if (batch_rows) batch_rows[i] = sel[i];
         }
     }
-    free(sel); free(sc); free(cb); free(ce); free(tle); free(tt);
+    free(sel); free(sc); free(cb); free(ce); free(tle); free(tt); free(tever);
     return rc;
 }
 
@@ -538,7 +563,7 @@ typedef struct {
 typedef struct {
     uint64_t token_goodput, tokens_processed;
     int64_t sim_end_ns;
-    uint32_t request_goodput, n_done, n_dropped, steps, n_tasks_done, error;
+    uint32_t request_goodput, n_done, n_dropped, steps, n_tasks_done, n_tasks_dropped, error, _pad;
 } og_replay_result;
 
 typedef struct {
@@ -546,6 +571,7 @@ typedef struct {
     uint32_t n_selected, total_tokens, n_candidates, b_star;
     double bp;
     uint64_t ids_hash;
+    int64_t v_token_ns;   /* the v_token the step's keys used */
 } og_step_log;
 
 static uint64_t fnv1a_ids(const uint32_t* ids, uint32_t n) {
@@ -593,6 +619,8 @@ int og_replay(const og_config* cfg, const og_group* groups_in, uint32_t n_groups
     uint32_t* ce = (uint32_t*)calloc(nt + 1, 4);
     uint64_t* tle = (uint64_t*)calloc(nt + 1, 8);
     uint64_t* ttot = (uint64_t*)calloc(nt + 1, 8);
+    uint8_t* tever = (uint8_t*)calloc(nt + 1, 1);      /* A40: some call of the task was scheduled */
+    uint8_t* tdrop = (uint8_t*)calloc(nt + 1, 1);
     int64_t lat_ring[1024]; uint32_t ring_n = 0, ring_pos = 0; int64_t ring_sum = 0;
     int ret = OG_OK;
     if (cfg->frame_steps > 1024) { ret = OG_EINVAL; goto done; }
@@ -667,12 +695,26 @@ int og_replay(const og_config* cfg, const og_group* groups_in, uint32_t n_groups
         if (steps >= rc->n_steps) break;
 
         int64_t v = ring_n ? ring_sum / (int64_t)ring_n : rc->v_token0_ns;
-        task_view tv = { nt, cb, ce, ta, tD, tle, ttot, gdone };
+        task_view tv = { nt, cb, ce, ta, tD, tle, ttot, gdone, tever, tdrop };
         og_result res;
         int st = gmax_step(cfg, G, n_groups, T, now, v, n, id, arr, tr->input_len, gen, pre, meta, aux,
                            tr->task, tr->override_R, &tv, &res, sel, selc, NULL);
         out->n_dropped += res.n_dropped_now;
         if (st == OG_EINVAL) { ret = OG_EINVAL; goto done; }
+        /* A40: a dropped task ends without goodput; the calls of its later stages are dropped too */
+        for (uint32_t t = 0; t < nt; ++t) {
+            if (!tdrop[t]) continue;
+            tdone[t] = 1; timer[t] = INT64_MAX; cb[t] = ce[t] = 0; out->n_tasks_dropped++;
+            for (uint32_t u = 0; u < tr->task_n_stages[t]; ++u) {
+                uint32_t kk = t * MAX_STAGES + u;
+                if (tr->stage_kind[kk] != 0) continue;
+                for (uint32_t q = tr->stage_call_begin[kk]; q < tr->stage_call_end[kk]; ++q)
+                    if (m_state(meta[q]) == ST_WAITING) { meta[q] = m_set_state(meta[q], ST_DROPPED); out->n_dropped++; }
+            }
+        }
+        if (st == OG_OK)
+            for (uint32_t i = 0; i < res.n_selected; ++i)
+                if (tr->task[sel[i]] != NO_TASK) tever[tr->task[sel[i]]] = 1;
         if (st == OG_EMPTY) {
             /* idle: jump to the next arrival or timer; stop when nothing is left (drained) */
             int64_t nxt = INT64_MAX;
@@ -702,6 +744,7 @@ int og_replay(const og_config* cfg, const og_group* groups_in, uint32_t n_groups
             L->now_ns = now; L->n_selected = res.n_selected; L->total_tokens = res.total_tokens;
             L->n_candidates = res.n_candidates; L->b_star = res.b_star; L->bp = res.bp;
             L->ids_hash = fnv1a_ids(selid, res.n_selected);
+            L->v_token_ns = v;
             if (log_ids) memcpy(log_ids + (size_t)(steps - 1) * cfg->max_batch, selid, 4 * res.n_selected);
         }
         /* progress of the executed batch (iteration end = token timestamp) */
@@ -749,5 +792,6 @@ done:
     out->error = ret != OG_OK;
     free(id); free(arr); free(gen); free(pre); free(meta); free(aux); free(late); free(sel); free(selc); free(selid);
     free(cur); free(left); free(tdone); free(timer); free(ta); free(tD); free(gdone); free(cb); free(ce); free(tle); free(ttot);
+    free(tever); free(tdrop);
     return ret;
 }

@@ -456,7 +456,7 @@ def test_replay_invariants_and_determinism():
         assert a["request_goodput"] <= n_req
         # drained: token conservation; every non-dropped request processed L_i + L_o - 1
         assert a["n_done"] + a["n_dropped"] == len(tr["input_len"])
-        assert a["n_tasks_done"] == len(tr["task_arrival_ns"])
+        assert a["n_tasks_done"] + a["n_tasks_dropped"] == len(tr["task_arrival_ns"])
 
 
 def test_replay_token_conservation_no_drops():
