@@ -30,10 +30,13 @@ import workloads as W  # noqa: E402
 
 METRIC = "pending requests scheduled/sec (1M pool)"
 UNIT = "requests/s"
-# algorithmic bytes of k_score: per standalone row 32 B read (arrival 8, input_len,
-# generated, prefilled, cached bound, meta, aux) + 16 B written (8-B key image, cost, steps_waited);
-# per compound call the same + 4 B read (task id); per task 32 B read (its load-time constants)
-BYTES_ROW, BYTES_CALL, BYTES_TASK = 48, 52, 32
+# algorithmic bytes of k_score: per standalone row its 32-B hot row read (arrival 8,
+# input_len, generated, prefilled, dist_row | cached bound, meta, steps_waited stamp), nothing
+# written in the steady state; per compound call the same + 4 B read (task id); per task 32 B read
+# (its constants).  SURVEY §8(d) counts 40 B per request (32 B read + an 8-B key write this design
+# does not need); `frac_8d` reports that accounting too.
+BYTES_ROW, BYTES_CALL, BYTES_TASK = 32, 36, 32
+BYTES_8D = 40
 
 
 def ncu_traffic():
@@ -412,6 +415,7 @@ def main():
     torch.cuda.synchronize()
     # clocks: the sampler runs through a ~0.6 s soak of the same step loop, the timed blocks
     # and a short tail, so that nvidia-smi has samples under this load (B200_PROFILING.md)
+    c_before = [s.counters() for s in hs]
     clk = Clocks(dev)
     t_soak = time.perf_counter() + 0.6
     j = 0
@@ -443,6 +447,12 @@ def main():
     for s in hs:
         s.kernel_times(slots=K)
     ms_events = timed_block()
+    # every timed step must have resolved on the device's fast path: the device counters of every
+    # handle over the soak + timed blocks (exact-path steps, and chained steps skipped because an
+    # earlier one needed the host) must not have moved
+    for s in hs:
+        s.fetch()
+    c_after = [s.counters() for s in hs]
     # (3) k_score alone, back to back over the rotated pools (launch overlapped by the previous
     # kernel, as inside the step where k_spec hides it): the roofline's kernel duration
     barrier()
@@ -453,13 +463,13 @@ def main():
             hs[k % args.rot].step_async(now, v)
         torch.cuda.synchronize()
         time.sleep(0.1)
+    for s in hs:
+        s.fetch()
     clocks = clk.stop()
     ms_max = allmax(ms)
-    # every timed step must have resolved on the fast path (checked on the last step of each handle)
-    fallback = 0
-    for s in hs:
-        rr = s.fetch()
-        fallback += int(rr["status"] not in (0, 1))
+    fallback = sum(b["fallbacks"] - a["fallbacks"] for a, b in zip(c_before, c_after))
+    skipped = sum(b["skipped"] - a["skipped"] for a, b in zip(c_before, c_after))
+    steps_dev = sum(b["steps"] - a["steps"] for a, b in zip(c_before, c_after))
     kt = np.zeros(5)
     for i, s in enumerate(hs):
         steps_i = len(range(i, K, args.rot))
@@ -480,6 +490,7 @@ def main():
                 "traffic_source": tr["source"] if tr else None,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if pk else "fallback 6650 GB/s",
                 "alg_bytes_per_launch": alg_bytes, "k_score_ms": k_b2b,
+                "frac_8d": n * BYTES_8D / (k_b2b / 1e3) / 1e9 / hbm_peak,
                 "how": f"{n_b2b} back-to-back k_score launches rotating over the {args.rot} L2-defeating pool "
                        "copies, CUDA events on the library stream around the sequence (jit_sched_time_scoring)",
                 "kernel_ms_event_nodes": {"k_score": kt[0], "k_spec": kt[2], "step_graph": kt[4]},
@@ -581,7 +592,9 @@ def main():
                            "rows_per_gpu": n, "tasks_per_gpu": nt,
                            "l2": f"inputs larger than L2: {args.rot} rotated pool copies of ~{(n * 100) >> 20} MiB workspace each",
                            "parallelism": f"{ws} independent 2^20-row shards (no data-path collective)" if ws > 1 else "single GPU",
-                           "fast_path_fallbacks": fallback, "host_submit_us_per_step": round(host_us[0], 2), "last_batch": {"n_selected": sel["n_selected"],
+                           "fast_path_fallbacks": fallback, "chained_steps_skipped": skipped,
+                           "device_steps_resolved": steps_dev,
+                           "host_submit_us_per_step": round(host_us[0], 2), "last_batch": {"n_selected": sel["n_selected"],
                                                                          "b_star": sel["b_star"],
                                                                          "n_candidates": sel["n_candidates"]}},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "steady_with_progress": steady,

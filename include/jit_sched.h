@@ -172,7 +172,12 @@ int jit_sched_load(jit_sched* h, const jit_pool* pool);
 int jit_sched_step(jit_sched* h, const jit_step_in* in, jit_batch* out);
 
 /* Enqueue one step without waiting for it (results stay on the device; read them with
- * jit_sched_fetch_batch).  Used for device-side timing; progress updates not allowed. */
+ * jit_sched_fetch_batch).  Steps may be chained (several step_async before one fetch): each
+ * step that resolves on the device (the steady state) leaves its bookkeeping done; if a step
+ * needs the host (exact path, large speculative set), every later step of the chain does
+ * nothing (counted in jit_sched_counters' `skipped`) until fetch_batch runs the host's part and
+ * returns that step's batch.  jit_sched_step / load after an unfinished async step fail with
+ * JIT_ESTATE (fetch first).  Progress updates are not allowed here. */
 int jit_sched_step_async(jit_sched* h, int64_t now_ns, int64_t v_token_ns);
 int jit_sched_fetch_batch(jit_sched* h, jit_batch* out);
 
@@ -194,6 +199,16 @@ int jit_sched_kernel_times(jit_sched* h, int enable, float* ms_out, uint32_t n_o
  * batch is empty (the pools' state changes); the per-step accumulators are reset afterwards. */
 int jit_sched_time_scoring(jit_sched** hs, uint32_t n_handles, int64_t now_ns, int64_t v_token_ns, uint32_t launches,
                            float* ms_per_launch);
+
+/* Device counters of the handle (synchronizes its stream): steps resolved since init (the
+ * steps_waited stamps count against this counter), steps resolved by the exact radix path, and
+ * chained jit_sched_step_async steps that did nothing because an earlier step of the chain still
+ * needed the host (each of those must be re-run; a timed region must see 0). */
+int jit_sched_counters(jit_sched* h, uint32_t* steps, uint32_t* fallbacks, uint32_t* skipped);
+
+/* Diagnostics: copy the first n u64 of the exact path's sort scratch to host memory `out`
+ * (JIT_TIMELINE builds of the scoring kernel leave per-warp %globaltimer stamps there). */
+int jit_sched_debug_scratch(jit_sched* h, uint64_t* out, uint32_t n);
 
 /* Diagnostics: %globaltimer stamps (ns) of the phases of the single-CTA resolve of the last
  * synchronized step: [k_spec start, partials reduced, set loaded, set sorted, budget walk,
@@ -241,7 +256,9 @@ typedef struct jit_replay_cfg {
 typedef struct jit_replay_result {
     uint64_t token_goodput, tokens_processed;
     int64_t sim_end_ns;
-    uint32_t request_goodput, n_done, n_dropped, steps, n_tasks_done, error;
+    uint32_t request_goodput, n_done, n_dropped, steps, n_tasks_done;
+    uint32_t n_tasks_dropped;      /* compound tasks dropped by admission (never scheduled, A40) */
+    uint32_t error, reserved;
 } jit_replay_result;
 
 typedef struct jit_step_log {
@@ -249,6 +266,7 @@ typedef struct jit_step_log {
     uint32_t n_selected, total_tokens, n_candidates, b_star;
     double bp;
     uint64_t ids_hash;             /* FNV-1a 64 over the batch ids (u32 LE) in batch order */
+    int64_t v_token_ns;            /* the v_token the step's keys used */
 } jit_step_log;
 
 /* Device workspace for a replay call. */

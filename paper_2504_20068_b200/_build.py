@@ -28,19 +28,22 @@ def build_library(force: bool = False, verbose: bool = False, out: str = LIB, de
     tmp = out + f".tmp{os.getpid()}"
     inc = ["-I", os.path.join(ROOT, "include")]
     objs, log = [], ""
-    for src, extra in UNITS:
-        obj = tmp + "." + src + ".o"
-        cmd = [NVCC] + BASE + extra + list(defines) + inc + ["-c", "-o", obj, os.path.join(HERE, "csrc", src)]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+    try:
+        for src, extra in UNITS:
+            obj = tmp + "." + src + ".o"
+            objs.append(obj)
+            cmd = [NVCC] + BASE + extra + list(defines) + inc + ["-c", "-o", obj, os.path.join(HERE, "csrc", src)]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if r.returncode != 0:
+                raise RuntimeError(f"nvcc failed on {src}:\n" + r.stdout[-4000:] + r.stderr[-8000:])
+            log += r.stderr
+        r = subprocess.run([NVCC] + LINK + ["-o", tmp] + objs, capture_output=True, text=True)
         if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed on {src}:\n" + r.stdout[-4000:] + r.stderr[-8000:])
-        objs.append(obj)
-        log += r.stderr
-    r = subprocess.run([NVCC] + LINK + ["-o", tmp] + objs, capture_output=True, text=True)
-    for o in objs:
-        os.remove(o)
-    if r.returncode != 0:
-        raise RuntimeError("nvcc link failed:\n" + r.stdout[-4000:] + r.stderr[-8000:])
+            raise RuntimeError("nvcc link failed:\n" + r.stdout[-4000:] + r.stderr[-8000:])
+    finally:
+        for o in objs:
+            if os.path.exists(o):
+                os.remove(o)
     if verbose:
         print(log[-6000:])
     os.replace(tmp, out)

@@ -11,7 +11,7 @@
 #include "jit_sched.h"
 #include "common.cuh"
 #include "select.cuh"
-#include "score.cuh"
+#include "stream.cuh"
 #include "replay.cuh"
 #include "shard.cuh"
 #include "exact_api.h"
@@ -28,24 +28,28 @@ struct jit_sched {
     uint32_t n_groups = 0;
     Pool P{};
     Scratch S{};
+    Item* d_items = nullptr;          // k_score work items (S.items), capacity item_cap
+    uint32_t* d_n_items = nullptr;    // their count (S.n_items)
+    uint32_t item_cap = 0;
+    unsigned char* d_load = nullptr;  // load / delta staging (32 B per row of capacity)
     Ctrl* d_ctrl = nullptr;
     Ctrl* h_ctrl = nullptr;           // pinned
     uint32_t* h_batch = nullptr;      // pinned: the fast path writes the batch here (ids | tokens | rows)
     uint32_t* h_prog = nullptr;       // pinned staging of progress rows (4 x prog_cap)
     uint64_t prog_cap = 0;
-    uint32_t* d_stage = nullptr;      // progress staging (4 * capacity)
     cudaStream_t stream = nullptr;    // caller's stream
     cudaStream_t cap = nullptr;       // private capture stream
-    cudaStream_t cap2 = nullptr;      // capture stream of the conditional body
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     cudaGraphNode_t score_node = nullptr;   // k_score: its (now, v) arguments change every step
     cudaKernelNodeParams score_params{};
-    void* score_args[9];
-    uint32_t arg_ntasks = 0;
+    void* score_args[10];
+    int arg_mode = 0;
     int64_t arg_now = 0, arg_v = 0;
     bool loaded = false, graph_dirty = true, timing = false, debug = false, pdl = true;
     bool keys_ready = false;          // k_score already ran this step (fast sharded attempt)
+    bool unfinished = false;          // a step was launched and not finished (step_async)
+    uint64_t launched = 0;            // steps launched (the stamp rebase runs every 2^30)
     cudaEvent_t ev[6] = {};
     cudaGraphNode_t ev_node[5] = {};      // event-record nodes of the timed graph
     std::vector<cudaEvent_t> slots;       // 5 events per recorded step
@@ -53,14 +57,16 @@ struct jit_sched {
     int n_sm = 148;
     uint32_t nb_score = 1, grid_pass = 1;
     std::vector<uint32_t> h_off;          // host copy of call_off (device-resident pools)
-    std::vector<CRange> h_rng;
+    std::vector<Item> h_items;
     std::string err;
 };
 
-// k_score instantiation: (debug row outputs) x (App. B feasibility filter)
-static const void* score_fn(bool debug, bool appb) {
-    return debug ? (appb ? (const void*)k_score<true, true> : (const void*)k_score<true, false>)
-                 : (appb ? (const void*)k_score<false, true> : (const void*)k_score<false, false>);
+// k_score instantiations: kMat (every key materialized: debug handles and the exact path's
+// re-score) x kDebug (per-row debug outputs) x App. B feasibility filter
+static const void* score_fn(bool mat, bool debug, bool appb) {
+    if (debug) return appb ? (const void*)k_score<true, true, true> : (const void*)k_score<true, true, false>;
+    if (mat) return appb ? (const void*)k_score<true, false, true> : (const void*)k_score<true, false, false>;
+    return appb ? (const void*)k_score<false, false, true> : (const void*)k_score<false, false, false>;
 }
 
 static int set_err(jit_sched* h, int code, const char* fmt, ...) {
@@ -95,23 +101,24 @@ struct Carve {
     }
 };
 
+// items of k_score for `cap` rows / `tcap` tasks: standalone chunks + one per task at most + slack
+static uint32_t item_capacity(uint64_t cap, uint64_t tcap) { return (uint32_t)(cap / kItemRows + tcap + 64); }
+
 static void carve(Carve& cv, const jit_config* cfg, const jit_len_table* tab, Pool& P, Scratch& S, Table& T,
-                  Group*& groups, Ctrl*& ctrl, uint32_t*& stage) {
+                  Group*& groups, Ctrl*& ctrl, Item*& items, uint32_t*& n_items, unsigned char*& load) {
     const uint64_t N = ((uint64_t)cfg->capacity + 63) & ~63ull;
     const uint64_t NT = (uint64_t)cfg->task_capacity + 1;
     const bool dbg = (cfg->flags & JIT_CFG_DEBUG_ROWS) != 0;
-    P.arr = cv.take<int64_t>(N);
-    P.len_in = cv.take<uint32_t>(N); P.gen = cv.take<uint32_t>(N); P.pre = cv.take<uint32_t>(N);
-    P.lhat = cv.take<uint32_t>(N); P.meta = cv.take<uint32_t>(N); P.aux = cv.take<uint32_t>(N);
+    P.rows = cv.take<HotRow>(N);
     P.id = cv.take<uint32_t>(N); P.task = cv.take<uint32_t>(N); P.ovr = cv.take<uint32_t>(N);
     P.img = cv.take<uint64_t>(N); P.cost = cv.take<uint32_t>(N);
     P.dbg_rate = dbg ? cv.take<double>(N) : nullptr;
     P.dbg_trem = dbg ? cv.take<int64_t>(N) : nullptr;
     P.dbg_lhat = dbg ? cv.take<uint32_t>(N) : nullptr;
-    P.call_off = cv.take<uint32_t>(NT + 1); P.t_arr = cv.take<int64_t>(NT); P.t_dl = cv.take<int64_t>(NT);
+    P.call_off = cv.take<uint32_t>(NT + 8); P.t_arr = cv.take<int64_t>(NT); P.t_dl = cv.take<int64_t>(NT);
     P.cur_stage = cv.take<uint32_t>(NT); P.n_stages = cv.take<uint32_t>(NT);
     P.pattern = cv.take<uint32_t>(NT * kMaxStages); P.gdone = cv.take<uint64_t>(NT);
-    P.tinfo = cv.take<TaskInfo>(NT);
+    P.tinfo = cv.take<TaskInfo>(NT); P.tever = cv.take<uint32_t>(NT + 4);   // + bulk-copy padding
     T.edges = cv.take<uint32_t>(tab->n_bins);
     T.cum = cv.take<uint32_t>((uint64_t)tab->n_rows * tab->n_bins);
     groups = cv.take<Group>(256);
@@ -131,11 +138,12 @@ static void carve(Carve& cv, const jit_config* cfg, const jit_len_table* tab, Po
     S.spec_meta = cv.take<uint32_t>(kSpecCap); S.spec_aux = cv.take<uint32_t>(kSpecCap);
     S.persist = cv.take<Persist>(1);
     S.spec_cnt = cv.take<unsigned int>(1);
-    S.part = cv.take<BlockPart>(1);
     S.gpart = cv.take<BlockPart>(1);
-    S.crange = cv.take<CRange>(NT + 1);
+    items = cv.take<Item>(item_capacity(N, NT));
+    n_items = cv.take<uint32_t>(1);
+    S.items = items; S.n_items = n_items;
     ctrl = cv.take<Ctrl>(1);
-    stage = cv.take<uint32_t>(4 * N);
+    load = cv.take<unsigned char>(32 * N);
 }
 
 static int check_config(jit_sched* h, const jit_config* c, const jit_len_table* t) {
@@ -143,7 +151,8 @@ static int check_config(jit_sched* h, const jit_config* c, const jit_len_table* 
     if (c->capacity == 0 || c->capacity > (1u << 30)) return set_err(h, JIT_EINVAL, "capacity out of range");
     if (c->refine_interval == 0 || c->frame_steps == 0 || c->q_den == 0 || c->q_num == 0 || c->q_num > c->q_den ||
         c->p_den == 0 || c->p_num == 0 || c->p_num > c->p_den || c->prefill_chunk == 0 ||
-        c->prefill_chunk > c->token_budget || c->max_batch == 0 || c->eps_ns <= 0 || c->waiting_ns < 0)
+        c->prefill_chunk > c->token_budget || c->max_batch == 0 || c->eps_ns <= 0 || c->eps_ns >= (1ll << 36) ||
+        c->waiting_ns < 0)
         return set_err(h, JIT_EINVAL, "invalid scheduler constants (ConfigError, S:417)");
     if (t->n_rows == 0 || t->n_rows > 65536 || t->n_bins == 0 || t->l_max == 0 || t->l_max >= 65536)
         return set_err(h, JIT_EINVAL, "invalid length table shape");
@@ -154,8 +163,8 @@ extern "C" int jit_sched_workspace_bytes(const jit_config* cfg, const jit_len_ta
     int rc = check_config(nullptr, cfg, table);
     if (rc) return rc;
     Carve cv;
-    Pool P; Scratch S; Table T; Group* g; Ctrl* c; uint32_t* st;
-    carve(cv, cfg, table, P, S, T, g, c, st);
+    Pool P; Scratch S; Table T; Group* g; Ctrl* c; Item* it; uint32_t* ni; unsigned char* ld;
+    carve(cv, cfg, table, P, S, T, g, c, it, ni, ld);
     *bytes = cv.off + 256;
     return JIT_OK;
 }
@@ -184,6 +193,10 @@ extern "C" int jit_sched_init(const jit_config* cfg, const jit_slo_group* groups
     for (uint32_t g = 0; g < n_groups; ++g) {
         if (groups[g].type > JIT_BE || groups[g].ttft_ns < 0 || groups[g].tbt_ns < 0 || groups[g].e2el_ns < 0 ||
             groups[g].be_deadline_ns < 0) { *out = h; return set_err(h, JIT_EINVAL, "bad SLO group %u", g); }
+        // the pass forms (Lhat - 1) * TBT as one 32 x 32-bit product: TBT < 2^32 ns (4.29 s)
+        if (groups[g].type == JIT_LAT && groups[g].tbt_ns >= (1ll << 32)) {
+            *out = h; return set_err(h, JIT_EINVAL, "SLO group %u: TBT must be < 2^32 ns", g);
+        }
     }
     uint64_t need = 0;
     jit_sched_workspace_bytes(cfg, table, &need);
@@ -196,13 +209,14 @@ extern "C" int jit_sched_init(const jit_config* cfg, const jit_slo_group* groups
     CK(cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, cfg->device));
     h->stream = (cudaStream_t)cfg->stream;
     CK(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&h->cap2, cudaStreamNonBlocking));
     // zero the workspace once: SoA padding rows (read by whole-quad tile loads, then masked) and
     // every scratch array start defined
     CK(cudaMemsetAsync(dev_workspace, 0, ws_bytes, h->stream));
     Carve cv;
     cv.base = reinterpret_cast<unsigned char*>(((uintptr_t)dev_workspace + 255) & ~(uintptr_t)255);
-    carve(cv, cfg, table, h->P, h->S, h->T, h->d_groups, h->d_ctrl, h->d_stage);
+    carve(cv, cfg, table, h->P, h->S, h->T, h->d_groups, h->d_ctrl, h->d_items, h->d_n_items, h->d_load);
+    h->item_cap = item_capacity(((uint64_t)cfg->capacity + 63) & ~63ull, (uint64_t)cfg->task_capacity + 1);
+    h->S.item_cap = h->item_cap;
     h->T.n_rows = table->n_rows; h->T.n_bins = table->n_bins; h->T.l_max = table->l_max;
     h->T.unit = 1;
     for (uint32_t k = 0; k < table->n_bins && h->T.unit; ++k) h->T.unit = table->edges[k] == k + 1;
@@ -226,23 +240,19 @@ extern "C" int jit_sched_init(const jit_config* cfg, const jit_slo_group* groups
     for (auto& e : h->ev) CK(cudaEventCreate(&e));
     CK(exact::init_attributes());
     CK(cudaFuncSetAttribute(k_group_rec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(12 * kGroupSmemSort)));
-    for (int m = 0; m < 4; ++m)
-        CK(cudaFuncSetAttribute(score_fn(m & 1, m & 2), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)score_smem_bytes(m & 1)));
     // one shared-memory carveout for every kernel of the step: switching the L1/shared split
     // between consecutive kernels costs a drain + reconfiguration of the SMs (several µs each)
-    {
-        const void* ks[] = {(const void*)k_begin, score_fn(false, false), score_fn(true, false), score_fn(false, true),
-                            score_fn(true, true)};
-        for (const void* k : ks)
-            CK(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+    for (int m = 0; m < 8; ++m) {
+        const void* k = score_fn(m & 1, m & 2, m & 4);
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)score_smem_bytes(256)));
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
     }
+    CK(cudaFuncSetAttribute(k_begin, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
     {
         Persist ps{};
         ps.t_guess = kNone;                 // no speculation before the first resolved step
         CK(cudaMemcpyAsync(h->S.persist, &ps, sizeof ps, cudaMemcpyHostToDevice, h->stream));
-        BlockPart g{};
-        g.min_img = kNone;                  // the empty step record (k_spec resets it after reading)
+        BlockPart g{};                      // the empty step record (k_spec resets it after reading)
         CK(cudaMemcpyAsync(h->S.gpart, &g, sizeof g, cudaMemcpyHostToDevice, h->stream));
     }
     CK(cudaStreamSynchronize(h->stream));
@@ -260,20 +270,32 @@ extern "C" int jit_sched_load(jit_sched* h, const jit_pool* p) {
     if (p->n_tasks && (!p->call_off || !p->task_arrival_ns || !p->task_deadline_ns || !p->cur_stage ||
                        !p->n_stages || !p->pattern_ms || !p->goodput_done))
         return set_err(h, JIT_EINVAL, "missing task arrays");
+    if (h->unfinished) return set_err(h, JIT_ESTATE, "load while a step is unfinished (fetch its batch first)");
     const cudaMemcpyKind kind = p->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     Pool& P = h->P;
     const uint64_t n = p->n, nt = p->n_tasks;
+    const uint64_t N = ((uint64_t)h->cfg.capacity + 63) & ~63ull;
     if (n) {
-        CK(cudaMemcpyAsync(P.arr, p->arrival_ns, 8 * n, kind, h->stream));
-        CK(cudaMemcpyAsync(P.len_in, p->input_len, 4 * n, kind, h->stream));
-        CK(cudaMemcpyAsync(P.gen, p->generated, 4 * n, kind, h->stream));
-        CK(cudaMemcpyAsync(P.pre, p->prefilled, 4 * n, kind, h->stream));
-        CK(cudaMemcpyAsync(P.meta, p->meta, 4 * n, kind, h->stream));
-        CK(cudaMemcpyAsync(P.aux, p->aux, 4 * n, kind, h->stream));
+        // the hot fields go through the staging area (or are read in place from a device pool)
+        // and are packed into 32-byte rows; the cold per-row arrays are copied as they are
+        const int64_t* arr = p->arrival_ns;
+        const uint32_t *li = p->input_len, *ge = p->generated, *pr = p->prefilled, *me = p->meta, *ax = p->aux;
+        if (!p->on_device) {
+            int64_t* s_arr = reinterpret_cast<int64_t*>(h->d_load);
+            uint32_t* s_u = reinterpret_cast<uint32_t*>(h->d_load + 8 * N);
+            CK(cudaMemcpyAsync(s_arr, p->arrival_ns, 8 * n, kind, h->stream));
+            CK(cudaMemcpyAsync(s_u, p->input_len, 4 * n, kind, h->stream));
+            CK(cudaMemcpyAsync(s_u + N, p->generated, 4 * n, kind, h->stream));
+            CK(cudaMemcpyAsync(s_u + 2 * N, p->prefilled, 4 * n, kind, h->stream));
+            CK(cudaMemcpyAsync(s_u + 3 * N, p->meta, 4 * n, kind, h->stream));
+            CK(cudaMemcpyAsync(s_u + 4 * N, p->aux, 4 * n, kind, h->stream));
+            arr = s_arr; li = s_u; ge = s_u + N; pr = s_u + 2 * N; me = s_u + 3 * N; ax = s_u + 4 * N;
+        }
+        k_pack<<<(uint32_t)std::min<uint64_t>((n + 255) / 256, (uint64_t)h->n_sm * 16), 256, 0, h->stream>>>(
+            P.rows, (uint32_t)n, arr, li, ge, pr, me, ax);
         CK(cudaMemcpyAsync(P.id, p->id, 4 * n, kind, h->stream));
         CK(cudaMemcpyAsync(P.task, p->task, 4 * n, kind, h->stream));
         CK(cudaMemcpyAsync(P.ovr, p->override_R, 4 * n, kind, h->stream));
-        CK(cudaMemsetAsync(P.lhat, 0, 4 * n, h->stream));      // invalidate cached bounds
     }
     if (nt) {
         CK(cudaMemcpyAsync(P.call_off, p->call_off, 4 * (nt + 1), kind, h->stream));
@@ -284,23 +306,26 @@ extern "C" int jit_sched_load(jit_sched* h, const jit_pool* p) {
         CK(cudaMemcpyAsync(P.pattern, p->pattern_ms, 4 * nt * kMaxStages, kind, h->stream));
         CK(cudaMemcpyAsync(P.gdone, p->goodput_done, 8 * nt, kind, h->stream));
     }
-    const bool same_shape = h->loaded && P.n == p->n && P.n_single == p->n_single && P.n_tasks == p->n_tasks;
     P.n = p->n; P.n_single = p->n_single; P.n_tasks = p->n_tasks;
-    // validate on the device (also covers device-resident pools)
-    // full reset: control block, histograms, the task accumulators, the speculative-set counter
+    // full reset: control block, histograms, the speculative-set counter; validate on the device
+    // (also covers device-resident pools)
     k_begin<<<4, 1024, 0, h->stream>>>(h->d_ctrl, h->S.hcnt, h->S.hcost, 0, 1, h->S.spec_cnt);
+    CK(cudaMemsetAsync(h->S.gpart, 0, sizeof(BlockPart), h->stream));
     const uint32_t vb = (uint32_t)std::min<uint64_t>((n + 255) / 256 + 1, (uint64_t)h->n_sm * 8);
-    k_validate<<<vb, 256, 0, h->stream>>>(P, h->d_groups, h->n_groups, h->T.n_rows, h->d_ctrl);
-    if (nt) k_task_prep<<<(uint32_t)std::min<uint64_t>((nt + 255) / 256, (uint64_t)h->n_sm * 8), 256, 0, h->stream>>>(P);
+    k_validate<<<vb, 256, 0, h->stream>>>(P, h->d_groups, h->n_groups, h->T.n_rows, h->T.l_max, h->d_ctrl, 0u, 0u);
+    if (nt) k_task_prep<<<(uint32_t)std::min<uint64_t>((nt + 255) / 256, (uint64_t)h->n_sm * 8), 256, 0, h->stream>>>(P, 0u);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(h->h_ctrl, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     if (h->h_ctrl->error) { h->loaded = false; return set_err(h, JIT_EINVAL, "invalid pool (layout / ranges / groups)"); }
-    // launch geometry of k_score: standalone tiles of kTile rows, then the compound ranges --
-    // whole tasks packed greedily so that a range spans at most one tile of aligned quads
-    // (a task of more than kTile calls gets a range of its own, scored in several tiles)
-    const uint32_t n_std = (P.n_single + kTile - 1) / kTile;
-    h->h_rng.clear();
+    // work items of k_score: the standalone rows in chunks of kItemRows (their descriptors are
+    // arithmetic in the kernel), then the compound tasks (whole tasks packed greedily into items of
+    // at most kItemRows rows and kItemTasks tasks; a task of more calls gets an item of its own,
+    // read in chunks)
+    h->h_items.clear();
+    for (uint32_t r0 = 0; r0 < P.n_single; r0 += kItemRows)
+        h->h_items.push_back(Item{r0, std::min<uint32_t>(r0 + kItemRows, P.n_single), 0u, 0u});
+    h->S.n_std_items = (uint32_t)h->h_items.size();
     if (nt) {
         const uint32_t* off = p->call_off;
         if (p->on_device) {
@@ -308,35 +333,33 @@ extern "C" int jit_sched_load(jit_sched* h, const jit_pool* p) {
             CK(cudaMemcpy(h->h_off.data(), p->call_off, 4 * (nt + 1), cudaMemcpyDeviceToHost));
             off = h->h_off.data();
         }
-        CRange cur{off[0], off[0], 0, 0};
+        Item cur{off[0], off[0], 0, 0};
         for (uint32_t t = 0; t < nt; ++t) {
-            // a range holds at most kTile rows of aligned quads and at most kTile tasks (the task
-            // sums live in kTile shared-memory slots; a shard can hold many empty tasks)
-            if (t > cur.t0 && (off[t + 1] - (cur.r0 & ~3u) > kTile || t - cur.t0 >= kTile)) {
+            if (t > cur.t0 && (off[t + 1] - cur.r0 > kItemRows || t - cur.t0 >= kItemTasks)) {
                 cur.r1 = off[t]; cur.t1 = t;
-                h->h_rng.push_back(cur);
+                h->h_items.push_back(cur);
                 cur.r0 = off[t]; cur.t0 = t;
             }
         }
         cur.r1 = off[nt]; cur.t1 = (uint32_t)nt;
-        h->h_rng.push_back(cur);
-        CK(cudaMemcpyAsync((void*)h->S.crange, h->h_rng.data(), sizeof(CRange) * h->h_rng.size(),
-                           cudaMemcpyHostToDevice, h->stream));
-        CK(cudaStreamSynchronize(h->stream));
+        h->h_items.push_back(cur);
     }
-    h->S.n_std = n_std;
-    h->S.n_crange = (uint32_t)h->h_rng.size();
-    {   // persistent grid: every CTA that fits (two tile buffers each), at most one per item
-        const void* kf = score_fn(h->debug, h->c.appb != 0);
-        int occ = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, kScoreThreads, score_smem_bytes(h->debug, h->n_groups)));
-        const uint32_t items = h->S.n_std + h->S.n_crange;
-        h->nb_score = std::max<uint32_t>(1, std::min<uint32_t>(items, (uint32_t)(h->n_sm * std::max(occ, 1))));
-    }
-    h->S.n_part = h->nb_score;
+    if (h->h_items.size() > h->item_cap) return set_err(h, JIT_ECAPACITY, "too many work items");
+    const uint32_t n_items = (uint32_t)h->h_items.size();
+    if (n_items)
+        CK(cudaMemcpyAsync(h->d_items, h->h_items.data(), sizeof(Item) * n_items, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->d_n_items, &n_items, 4, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    // persistent grid: every CTA that fits on the GPU (warps stride over the items), at most one
+    // warp per item
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, score_fn(h->debug, h->debug, h->c.appb != 0), kScoreThreads,
+                                                     score_smem_bytes(h->n_groups)));
+    const uint32_t nb = std::max<uint32_t>(1, std::min<uint32_t>((n_items + kScoreWarps - 1) / kScoreWarps,
+                                                                 (uint32_t)h->n_sm * (uint32_t)std::max(occ, 1)));
+    if (nb != h->nb_score) h->graph_dirty = true;
+    h->nb_score = nb;
     h->grid_pass = std::max<uint32_t>(1, std::min<uint32_t>((P.n + kPassThreads - 1) / kPassThreads, (uint32_t)h->n_sm * 4));
-    h->S.grid_pass = h->grid_pass;    // launch geometry of the exact path
-    if (!same_shape) h->graph_dirty = true;
     h->loaded = true;
     return JIT_OK;
 }
@@ -344,13 +367,15 @@ extern "C" int jit_sched_load(jit_sched* h, const jit_pool* p) {
 // ------------------------------------------------------------------------------------------
 // step
 // ------------------------------------------------------------------------------------------
+// mode 0: the step's pass (debug handles materialize every key); mode 1: the exact path's re-score
+// (every key materialized, nothing counted again)
 static void enqueue_score(jit_sched* h, cudaStream_t s, int64_t now, int64_t v, cudaEvent_t mid = nullptr,
-                          bool capturing = false) {
+                          bool capturing = false, int mode = 0) {
     Pool& P = h->P;
     Scratch& S = h->S;
-    void* args[] = {&P, &h->T, &h->d_groups, &h->n_groups, &h->c, &h->d_ctrl, &S, &now, &v};
-    cudaLaunchKernel(score_fn(h->debug, h->c.appb != 0), dim3(h->nb_score), dim3(kScoreThreads), args,
-                     score_smem_bytes(h->debug, h->n_groups), s);
+    void* args[] = {&P, &h->T, &h->d_groups, &h->n_groups, &h->c, &h->d_ctrl, &S, &now, &v, &mode};
+    cudaLaunchKernel(score_fn(h->debug || mode == 1, h->debug, h->c.appb != 0), dim3(h->nb_score), dim3(kScoreThreads),
+                     args, score_smem_bytes(h->n_groups), s);
     if (mid) cudaEventRecordWithFlags(mid, s, capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
 }
 
@@ -403,7 +428,7 @@ static int build_graph(jit_sched* h) {
     CK(cudaGraphGetNodes(g, nodes.data(), &nn));
     // locate the k_score kernel node (its (now, v) arguments are updated per launch) and the
     // timing event nodes
-    const void* score_kernel = score_fn(h->debug, h->c.appb != 0);
+    const void* score_kernel = score_fn(h->debug, h->debug, h->c.appb != 0);
     h->score_node = nullptr;
     for (auto& e : h->ev_node) e = nullptr;
     for (auto nd : nodes) {
@@ -442,7 +467,14 @@ static int launch_direct(jit_sched* h, int64_t now, int64_t v) {
     return JIT_OK;
 }
 
-static int launch_step(jit_sched* h, int64_t now, int64_t v) {
+static int launch_step(jit_sched* h, int64_t now, int64_t v, bool chain = false) {
+    if (h->unfinished && !chain)
+        return set_err(h, JIT_ESTATE, "a step_async step is unfinished: fetch its batch before a synchronous step");
+    // every 2^30 steps: keep the steps_waited stamps of long-waiting rows within reach (pool.cuh)
+    if (((++h->launched) & ((1ull << 30) - 1)) == 0 && h->P.n)
+        k_rebase<<<h->grid_pass, 256, 0, h->stream>>>(h->P, h->S);
+    h->unfinished = true;
+    h->arg_now = now; h->arg_v = v; h->arg_mode = 0;
     if (h->cfg.flags & JIT_CFG_NO_GRAPH) return launch_direct(h, now, v);
     if (h->graph_dirty) {
         CK(cudaGetLastError());
@@ -450,10 +482,10 @@ static int launch_step(jit_sched* h, int64_t now, int64_t v) {
         if (rc) return rc;
         CK(cudaGetLastError());
     }
-    h->arg_now = now; h->arg_v = v;
-    void** a = h->score_args;     // k_score(Pool, Table, const Group*, uint32_t, Cfg, Ctrl*, Scratch, now, v)
+    h->arg_now = now; h->arg_v = v; h->arg_mode = 0;
+    void** a = h->score_args;     // k_score(Pool, Table, const Group*, uint32_t, Cfg, Ctrl*, Scratch, now, v, mode)
     a[0] = &h->P; a[1] = &h->T; a[2] = &h->d_groups; a[3] = &h->n_groups; a[4] = &h->c; a[5] = &h->d_ctrl;
-    a[6] = &h->S; a[7] = &h->arg_now; a[8] = &h->arg_v;
+    a[6] = &h->S; a[7] = &h->arg_now; a[8] = &h->arg_v; a[9] = &h->arg_mode;
     cudaKernelNodeParams kp = h->score_params;
     kp.kernelParams = a;
     kp.extra = nullptr;
@@ -471,15 +503,25 @@ static int launch_step(jit_sched* h, int64_t now, int64_t v) {
     return JIT_OK;
 }
 
-static int finish_step(jit_sched* h, jit_batch* out) {
+// the exact path from the host (rare): re-score the pool with every key and cost materialized
+// (same step counter and pool state: the pass is idempotent), then the cost-weighted radix select
+static void enqueue_exact(jit_sched* h, cudaStream_t s) {
+    enqueue_score(h, s, h->arg_now, h->arg_v, nullptr, false, 1);
+    cudaMemsetAsync(h->S.hcnt, 0, 4 * 4096, s);
+    cudaMemsetAsync(h->S.hcost, 0, 8 * 4096, s);
+    exact::hist0(h->P, h->c, h->d_ctrl, h->S, h->grid_pass, 0, s);
+    enqueue_radix(h, s, 0, kLevels - 1);
+}
+
+static int finish_step_body(jit_sched* h, jit_batch* out) {
     CK(cudaStreamSynchronize(h->stream));
     CK(cudaGetLastError());
     if (getenv("JITSCHED_DEBUG_CTRL")) {
         Ctrl dc;
         CK(cudaMemcpy(&dc, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
-        fprintf(stderr, "[ctrl] device status %u err %u fb %u spec %u trace %x lerr %u chain %u | host status %u err %u "
-                "fb %u spec %u trace %x\n", dc.status, dc.error, dc.fallback, dc.spec_n, dc.trace, dc.launch_err, dc.chain,
-                h->h_ctrl->status, h->h_ctrl->error, h->h_ctrl->fallback, h->h_ctrl->spec_n, h->h_ctrl->trace);
+        fprintf(stderr, "[ctrl] device status %u err %u fb %u spec %u trace %x | host status %u err %u fb %u spec %u\n",
+                dc.status, dc.error, dc.fallback, dc.spec_n, dc.trace, h->h_ctrl->status, h->h_ctrl->error,
+                h->h_ctrl->fallback, h->h_ctrl->spec_n);
     }
     if (h->h_ctrl->status == ST_SPEC_BIG) {
         // a speculative set too large for k_spec's fast path (e.g. after a shift of the keys)
@@ -488,21 +530,19 @@ static int finish_step(jit_sched* h, jit_batch* out) {
         CK(cudaStreamSynchronize(h->stream));
     }
     const uint32_t st0 = h->h_ctrl->status;
-    if (st0 == ST_FALLBACK || (st0 == ST_RESOLVED && !h->h_ctrl->window_done && !h->h_ctrl->error)) {
+    const bool host_work = st0 == ST_FALLBACK || (st0 == ST_RESOLVED && !h->h_ctrl->window_done && !h->h_ctrl->error);
+    if (host_work) {
         // the speculative resolve could not be exact (first step after a load, a threshold far
         // off, heavy key ties) or Cd was too large for k_spec's window: the exact path --
         // cost-weighted radix select over every key, candidates, window -- from the host
-        Pool& P = h->P;
-        if (st0 == ST_FALLBACK) {
-            exact::hist0(P, h->c, h->d_ctrl, h->S, h->grid_pass, 0, h->stream);
-            enqueue_radix(h, h->stream, 0, kLevels - 1);
-        } else {
-            exact::group(P, h->c, h->d_ctrl, h->S, h->stream);
-        }
+        if (st0 == ST_FALLBACK) enqueue_exact(h, h->stream);
+        else exact::group(h->P, h->c, h->d_ctrl, h->S, h->stream);
         k_publish<<<1, 64, 0, h->stream>>>(h->d_ctrl, h->h_ctrl);
         CK(cudaGetLastError());
-        CK(cudaStreamSynchronize(h->stream));
     }
+    // the host's part of the step is done: chained steps may run again
+    CK(cudaMemsetAsync(&h->S.persist->host_pending, 0, 4, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
     const Ctrl& c = *h->h_ctrl;
     if (c.status == ST_ERROR || c.error) return set_err(h, JIT_EINVAL, "step: invalid input (error code %u)", c.error);
     if (out) {
@@ -534,10 +574,17 @@ static int finish_step(jit_sched* h, jit_batch* out) {
     return JIT_OK;
 }
 
+static int finish_step(jit_sched* h, jit_batch* out) {
+    const int rc = finish_step_body(h, out);
+    h->unfinished = false;
+    return rc;
+}
+
 extern "C" int jit_sched_step(jit_sched* h, const jit_step_in* in, jit_batch* out) {
     if (!h || !in) return JIT_EINVAL;
     if (!h->loaded) return set_err(h, JIT_ESTATE, "step before load");
-    if (in->v_token_ns <= 0) return set_err(h, JIT_EINVAL, "v_token must be > 0");
+    if (in->v_token_ns <= 0 || in->v_token_ns >= (1ll << 36)) return set_err(h, JIT_EINVAL, "v_token must be in (0, 2^36) ns");
+    if (h->unfinished) return set_err(h, JIT_ESTATE, "a step_async step is unfinished: fetch its batch first");
     if (in->n_progress) {
         if (in->n_progress > h->cfg.capacity) return set_err(h, JIT_ECAPACITY, "too many progress rows");
         const uint64_t m = in->n_progress;
@@ -554,9 +601,10 @@ extern "C" int jit_sched_step(jit_sched* h, const jit_step_in* in, jit_batch* ou
         memcpy(h->h_prog + m, in->prog_generated, 4 * m);
         memcpy(h->h_prog + 2 * m, in->prog_prefilled, 4 * m);
         memcpy(h->h_prog + 3 * m, in->prog_state, 4 * m);
-        CK(cudaMemcpyAsync(h->d_stage, h->h_prog, 16 * m, cudaMemcpyHostToDevice, h->stream));
-        k_progress<<<(uint32_t)((m + 255) / 256), 256, 0, h->stream>>>(h->P, h->d_stage, h->d_stage + m, h->d_stage + 2 * m,
-                                                                     h->d_stage + 3 * m, (uint32_t)m);
+        uint32_t* st = reinterpret_cast<uint32_t*>(h->d_load);
+        CK(cudaMemcpyAsync(st, h->h_prog, 16 * m, cudaMemcpyHostToDevice, h->stream));
+        k_progress<<<(uint32_t)((m + 255) / 256), 256, 0, h->stream>>>(h->P, h->S, st, st + m, st + 2 * m, st + 3 * m,
+                                                                     (uint32_t)m);
         CK(cudaGetLastError());
     }
     int rc = launch_step(h, in->now_ns, in->v_token_ns);
@@ -567,8 +615,8 @@ extern "C" int jit_sched_step(jit_sched* h, const jit_step_in* in, jit_batch* ou
 extern "C" int jit_sched_step_async(jit_sched* h, int64_t now_ns, int64_t v_token_ns) {
     if (!h) return JIT_EINVAL;
     if (!h->loaded) return set_err(h, JIT_ESTATE, "step before load");
-    if (v_token_ns <= 0) return set_err(h, JIT_EINVAL, "v_token must be > 0");
-    return launch_step(h, now_ns, v_token_ns);
+    if (v_token_ns <= 0 || v_token_ns >= (1ll << 36)) return set_err(h, JIT_EINVAL, "v_token must be in (0, 2^36) ns");
+    return launch_step(h, now_ns, v_token_ns, true);
 }
 
 extern "C" int jit_sched_fetch_batch(jit_sched* h, jit_batch* out) {
@@ -581,7 +629,11 @@ extern "C" int jit_sched_read_rows(jit_sched* h, double* key, double* rate, int6
     if (!h) return JIT_EINVAL;
     if (!h->loaded) return set_err(h, JIT_ESTATE, "read_rows before load");
     const uint64_t n = h->P.n;
-    if ((rate || t_rem || lhat) && !h->debug) return set_err(h, JIT_ESTATE, "rate/t_rem/lhat need JIT_CFG_DEBUG_ROWS");
+    // per-row keys, costs and debug outputs exist only on debug handles (every step materializes
+    // them there); a production step writes no per-row output
+    if ((key || pending || cost || rate || t_rem || lhat) && !h->debug)
+        return set_err(h, JIT_ESTATE, "key/cost/pending/rate/t_rem/lhat need JIT_CFG_DEBUG_ROWS");
+    if (h->unfinished) return set_err(h, JIT_ESTATE, "read_rows while a step is unfinished");
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(h->stream));
     std::vector<uint64_t> img;
@@ -597,11 +649,18 @@ extern "C" int jit_sched_read_rows(jit_sched* h, double* key, double* rate, int6
     if (t_rem) CK(cudaMemcpy(t_rem, h->P.dbg_trem, 8 * n, cudaMemcpyDeviceToHost));
     if (lhat) CK(cudaMemcpy(lhat, h->P.dbg_lhat, 4 * n, cudaMemcpyDeviceToHost));
     if (cost) CK(cudaMemcpy(cost, h->P.cost, 4 * n, cudaMemcpyDeviceToHost));
-    if (meta) {
-        CK(cudaMemcpy(meta, h->P.meta, 4 * n, cudaMemcpyDeviceToHost));
-        for (uint64_t r = 0; r < n; ++r) meta[r] &= 0xFFFFu;       // drop the internal epoch bits
+    if (meta || aux) {
+        // the caller's view of the hot rows: meta without the internal epoch / stamp bits, aux =
+        // dist_row | steps_waited (the stamp resolved against the step counter)
+        std::vector<HotRow> rows(n);
+        Persist ps;
+        CK(cudaMemcpy(rows.data(), h->P.rows, sizeof(HotRow) * n, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&ps, h->S.persist, sizeof ps, cudaMemcpyDeviceToHost));
+        for (uint64_t r = 0; r < n; ++r) {
+            if (meta) meta[r] = rows[r].meta & 0x7FFFu;
+            if (aux) aux[r] = l_row(rows[r].lrow) | (waited_of(rows[r].meta, rows[r].since, ps.steps) << 16);
+        }
     }
-    if (aux) CK(cudaMemcpy(aux, h->P.aux, 4 * n, cudaMemcpyDeviceToHost));
     return JIT_OK;
 }
 
@@ -651,6 +710,7 @@ extern "C" int jit_sched_time_scoring(jit_sched** hs, uint32_t n_handles, int64_
     for (uint32_t i = 0; i < n_handles; ++i) {
         if (!hs[i] || !hs[i]->loaded) return set_err(h, JIT_ESTATE, "time_scoring: handle %u not loaded", i);
         if (hs[i]->stream != h->stream) return set_err(h, JIT_EINVAL, "time_scoring: handles must share one stream");
+        if (hs[i]->unfinished) return set_err(h, JIT_ESTATE, "time_scoring: handle %u has an unfinished step", i);
     }
     cudaStream_t s = h->stream;
     cudaEvent_t e0 = h->ev[0], e1 = h->ev[1];
@@ -668,6 +728,26 @@ extern "C" int jit_sched_time_scoring(jit_sched** hs, uint32_t n_handles, int64_
     return JIT_OK;
 }
 
+extern "C" int jit_sched_counters(jit_sched* h, uint32_t* steps, uint32_t* fallbacks, uint32_t* skipped) {
+    if (!h) return JIT_EINVAL;
+    CK(cudaStreamSynchronize(h->stream));
+    Persist ps;
+    CK(cudaMemcpy(&ps, h->S.persist, sizeof ps, cudaMemcpyDeviceToHost));
+    if (steps) *steps = ps.steps;
+    if (fallbacks) *fallbacks = ps.fallbacks;
+    if (skipped) *skipped = ps.skipped;
+    return JIT_OK;
+}
+
+// diagnostics: the first n u64 of the exact path's sort scratch (where JIT_TIMELINE builds of
+// k_score leave their per-warp %globaltimer stamps)
+extern "C" int jit_sched_debug_scratch(jit_sched* h, uint64_t* out, uint32_t n) {
+    if (!h || !out) return JIT_EINVAL;
+    CK(cudaStreamSynchronize(h->stream));
+    CK(cudaMemcpy(out, h->S.sk, 8ull * n, cudaMemcpyDeviceToHost));
+    return JIT_OK;
+}
+
 extern "C" int jit_sched_phase_times(jit_sched* h, uint64_t* ns_out, uint32_t n_out) {
     if (!h || !ns_out) return JIT_EINVAL;
     CK(cudaStreamSynchronize(h->stream));
@@ -680,7 +760,6 @@ extern "C" void jit_sched_destroy(jit_sched* h) {
     if (h->exec) cudaGraphExecDestroy(h->exec);
     if (h->graph) cudaGraphDestroy(h->graph);
     if (h->cap) cudaStreamDestroy(h->cap);
-    if (h->cap2) cudaStreamDestroy(h->cap2);
     if (h->h_ctrl) cudaFreeHost(h->h_ctrl);
     if (h->h_batch) cudaFreeHost(h->h_batch);
     if (h->h_prog) cudaFreeHost(h->h_prog);
@@ -707,18 +786,23 @@ extern "C" int jit_shard_prefix(jit_sched* h, int64_t now_ns, int64_t v_token_ns
                                 uint32_t* n_out) {
     if (!h || !d_rec1 || !n_out) return JIT_EINVAL;
     if (!h->loaded) return set_err(h, JIT_ESTATE, "shard_prefix before load");
-    if (v_token_ns <= 0) return set_err(h, JIT_EINVAL, "v_token must be > 0");
+    if (v_token_ns <= 0 || v_token_ns >= (1ll << 36)) return set_err(h, JIT_EINVAL, "v_token must be in (0, 2^36) ns");
     if (cap < h->cfg.max_batch + 1) return set_err(h, JIT_ECAPACITY, "round-1 buffer needs max_batch+1 records");
     cudaStream_t s = h->stream;
     Pool& P = h->P;
     Scratch& S = h->S;
     if (!h->keys_ready) {
+        h->arg_now = now_ns; h->arg_v = v_token_ns;
         enqueue_score(h, s, now_ns, v_token_ns);
-        // k_spec only reduces the scoring partials (n_pending, min key, ...): the round-1 export
+        // k_spec only reduces the scoring partials (n_pending, errors, ...): the round-1 export
         // needs the full radix resolve below
         CK(exact::spec(P, h->c, h->d_ctrl, S, 1, s, false));
     }
-    h->keys_ready = false;                 // (after a failed fast attempt the keys are this step's)
+    h->keys_ready = false;                 // (after a failed fast attempt the pool state is this step's)
+    // every key and cost materialized for the radix select (idempotent re-score)
+    enqueue_score(h, s, h->arg_now, h->arg_v, nullptr, false, 1);
+    CK(cudaMemsetAsync(S.hcnt, 0, 4 * 4096, s));
+    CK(cudaMemsetAsync(S.hcost, 0, 8 * 4096, s));
     exact::hist0(P, h->c, h->d_ctrl, S, h->grid_pass, 1, s);
     for (uint32_t i = 0; i < kLevels - 1; ++i) exact::pass(P, h->c, h->d_ctrl, S, h->grid_pass, i, s);
     exact::compact(P, h->c, h->d_ctrl, S, h->grid_pass, s);
@@ -741,9 +825,10 @@ extern "C" int jit_shard_spec_export(jit_sched* h, int64_t now_ns, int64_t v_tok
                                      uint32_t rank) {
     if (!h || !d_out) return JIT_EINVAL;
     if (!h->loaded) return set_err(h, JIT_ESTATE, "shard_spec_export before load");
-    if (v_token_ns <= 0) return set_err(h, JIT_EINVAL, "v_token must be > 0");
+    if (v_token_ns <= 0 || v_token_ns >= (1ll << 36)) return set_err(h, JIT_EINVAL, "v_token must be in (0, 2^36) ns");
     if (cap_bytes < exact::spec_export_bytes()) return set_err(h, JIT_ECAPACITY, "export buffer needs %u bytes",
                                                                 exact::spec_export_bytes());
+    h->arg_now = now_ns; h->arg_v = v_token_ns;
     enqueue_score(h, h->stream, now_ns, v_token_ns);
     CK(exact::spec_export(h->S, h->d_ctrl, d_out, rank, h->stream));
     h->keys_ready = true;

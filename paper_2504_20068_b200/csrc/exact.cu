@@ -5,7 +5,7 @@
 #define JIT_EXACT_TU 1
 #include "common.cuh"
 #include "select.cuh"
-#include "score.cuh"
+#include "spec.cuh"
 #include "exact_api.h"
 
 namespace jit {

@@ -13,6 +13,82 @@
 #include "select.cuh"
 
 namespace jit {
+// --------------------------------------------------------------------------------------
+// per-row scoring of a standalone request: (a1) admission, (a2) length bound, (a3) t_rem,
+// (a5) key, (a6) cost.  Pure function of the row + config; returns what to write back.
+// --------------------------------------------------------------------------------------
+struct RowRes {
+    uint64_t img;
+    uint32_t cost, meta, lhat, aux;
+    bool pending, dropped, w_meta, w_lhat, err;
+    double rate; int64_t trem; uint32_t lhatc;
+};
+
+// Per-group constants in the form the scoring loop uses (staged to shared memory per CTA):
+//   t_rem = arrival + base + (Lhat-1)*tok - now      (LAT: base=TTFT, tok=TBT  [A9];
+//                                                     DDL: base=E2EL; BE: base=default deadline)
+//   G     = w_in_eff * L_i + w_out_eff * Lhat        (DDL: w_in, w_out; LAT: 0, w_out; BE: 0, 0)
+struct GroupFast {
+    int64_t base, tok;
+    uint32_t w_in_eff, w_out_eff, type, pad;
+};
+__host__ __device__ inline GroupFast make_fast(const Group& g) {
+    GroupFast f;
+    f.type = g.type; f.pad = 0;
+    f.base = g.type == kLAT ? g.ttft_ns : g.type == kDDL ? g.e2el_ns : g.type == kBE ? g.be_deadline_ns : 0;
+    f.tok = g.type == kLAT ? g.tbt_ns : 0;
+    f.w_in_eff = (g.type == kDDL || g.type == kCMP) ? g.w_in : 0;   // CMP: used by the compound pass
+    f.w_out_eff = g.type != kBE ? g.w_out : 0;
+    return f;
+}
+
+template <bool kDebug>
+__device__ __forceinline__ void score_standalone(const Cfg& c, const Table& T, const GroupFast* sg, uint32_t n_groups,
+                                                 const uint32_t* ovr, uint32_t row, int64_t now, int64_t v,
+                                                 int64_t arr, uint32_t L_i, uint32_t g, uint32_t pre,
+                                                 uint32_t lhat, uint32_t meta, uint32_t aux, RowRes& o) {
+    o.img = kNone; o.cost = 0; o.meta = meta; o.lhat = lhat; o.aux = aux;
+    o.pending = o.dropped = o.w_meta = o.w_lhat = o.err = false;
+    if (kDebug) { o.rate = 0.0; o.trem = 0; o.lhatc = 0; }
+    if (arr > now) return;
+    const uint32_t st = m_state(meta), fl = m_flags(meta);
+    if (st == kQueued && !(fl & kEver) && !(fl & kCompound) && now - arr > c.waiting) {   // (a1) P:545
+        o.meta = m_with_state(meta, kDropped); o.w_meta = true; o.dropped = true;
+        return;
+    }
+    if (st > kPreempted) return;
+    o.pending = true;
+    const uint32_t gi = m_group(meta);
+    const uint32_t drow = aux & 0xFFFFu;
+    if (gi >= n_groups || drow >= T.n_rows || (fl & kCompound)) { o.err = true; return; }
+    const GroupFast G = sg[gi];
+    if (G.type == kCMP) { o.err = true; return; }
+    // (a2) conservative remaining length, refreshed every R tokens; cached per epoch
+    const uint32_t ep = fastdiv(g, c.R, c.R_m, c.R_l);
+    if (lhat == 0 || ep >= 65536u || m_epoch(meta) != ep) {
+        lhat = cond_quantile(T, drow, ep * c.R, c.qn, c.qd);
+        o.lhat = lhat; o.w_lhat = true;
+        if (ep < 65536u) { o.meta = (meta & 0xFFFFu) | (ep << 16); o.w_meta = true; }
+    }
+    const uint32_t Lh = lhat > g + 1 ? lhat : g + 1;
+    const uint32_t len_rem = Lh - g;
+    o.cost = token_cost(L_i, pre, c.chunk);
+    const uint64_t t_gen = (uint64_t)len_rem * (uint64_t)v;
+    const int64_t trem = arr + G.base + (int64_t)(Lh - 1) * G.tok - now;  // (a3)
+    uint64_t Gk = (uint64_t)G.w_in_eff * L_i + (uint64_t)G.w_out_eff * Lh;  // (a5) A10/A11
+    if (fl & kOverride) Gk = __ldg(ovr + row);
+    if (trem <= 0) Gk = 0;                                      // A22
+    if (c.appb && t_gen > (uint64_t)(trem > 0 ? trem : 0)) Gk = 0;
+    const uint64_t Gp = Gk + (uint64_t)c.delta * fastdiv(aux >> 16, c.frame, c.F_m, c.F_l);
+    double key;
+    if (!make_key(Gp, t_gen, c.eps, &key)) { o.err = true; return; }
+    o.img = (uint64_t)__double_as_longlong(key);
+    if (kDebug) { o.rate = make_rate(len_rem, trem); o.trem = trem; o.lhatc = Lh; }
+}
+
+}  // namespace jit
+
+namespace jit {
 
 constexpr uint32_t kReplayThreads = 512;
 constexpr uint32_t kReplaySmemRows = 2048;    // rows sorted in shared memory up to this size
@@ -21,12 +97,13 @@ struct TraceMeta { uint32_t row_off, task_off, n_rows, n_tasks; };
 
 struct Spec { uint32_t trace, reserved; uint64_t load_num, load_den, slo_num, slo_den; };
 
-struct RLog { int64_t now_ns; uint32_t n_selected, total_tokens, n_candidates, b_star; double bp; uint64_t ids_hash; };
+struct RLog { int64_t now_ns; uint32_t n_selected, total_tokens, n_candidates, b_star; double bp; uint64_t ids_hash;
+              int64_t v_token_ns; };
 
 struct RResult {
     unsigned long long token_goodput, tokens_processed;
     int64_t sim_end_ns;
-    uint32_t request_goodput, n_done, n_dropped, steps, n_tasks_done, error;
+    uint32_t request_goodput, n_done, n_dropped, steps, n_tasks_done, n_tasks_dropped, error, pad;
 };
 
 struct ReplayArgs {
@@ -45,7 +122,7 @@ struct ReplayArgs {
 // per-CTA state slice layout
 struct RState {
     int64_t* arr; uint32_t *gen, *pre, *lhat, *meta, *aux, *late, *cost; uint64_t* img;
-    uint32_t *cur, *left, *tdone, *cb, *ce; int64_t *timer, *ta, *tD; unsigned long long* gdone;
+    uint32_t *cur, *left, *tdone, *cb, *ce, *tever; int64_t *timer, *ta, *tD; unsigned long long* gdone;
     uint64_t *tle, *ttot;
     u128* gA; uint32_t* gAv; uint64_t* gB; uint32_t* gBv; unsigned long long* gpc; u128* gpf;  // global sort scratch
     uint32_t* batch; int64_t* ring;
@@ -55,7 +132,7 @@ __host__ __device__ inline uint64_t replay_state_bytes(uint32_t M, uint32_t MT, 
     const uint64_t m = M + 64, mt = MT + 1;
     uint64_t b = 0;
     b += 8 * m + 4 * m * 7 + 8 * m;            // arr, gen..cost, img
-    b += 4 * mt * 5 + 8 * mt * 3 + 8 * mt + 16 * mt;   // task u32 x5, i64 x3, gdone, tle+ttot
+    b += 4 * mt * 6 + 8 * mt * 3 + 8 * mt + 16 * mt;   // task u32 x6, i64 x3, gdone, tle+ttot
     uint64_t p2 = 1;                            // bitonic sorts pad to a power of two
     while (p2 < m) p2 <<= 1;
     b += 16 * p2 + 4 * p2 + 8 * p2 + 4 * p2 + 8 * (m + 1) + 16 * (m + 1);
@@ -72,7 +149,7 @@ __device__ inline RState carve_state(unsigned char* p, uint32_t M, uint32_t MT, 
     s.meta = (uint32_t*)take(4 * m); s.aux = (uint32_t*)take(4 * m); s.late = (uint32_t*)take(4 * m);
     s.cost = (uint32_t*)take(4 * m); s.img = (uint64_t*)take(8 * m);
     s.cur = (uint32_t*)take(4 * mt); s.left = (uint32_t*)take(4 * mt); s.tdone = (uint32_t*)take(4 * mt);
-    s.cb = (uint32_t*)take(4 * mt); s.ce = (uint32_t*)take(4 * mt);
+    s.cb = (uint32_t*)take(4 * mt); s.ce = (uint32_t*)take(4 * mt); s.tever = (uint32_t*)take(4 * mt);
     s.timer = (int64_t*)take(8 * mt); s.ta = (int64_t*)take(8 * mt); s.tD = (int64_t*)take(8 * mt);
     s.gdone = (unsigned long long*)take(8 * mt); s.tle = (uint64_t*)take(8 * mt); s.ttot = (uint64_t*)take(8 * mt);
     uint64_t p2 = 1;
@@ -108,7 +185,7 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
     __shared__ u128 s_best[32];
     __shared__ uint32_t s_bi[32], s_bj[32];
     __shared__ unsigned long long s_good, s_tok, s_min;
-    __shared__ uint32_t s_reqg, s_done, s_drop, s_tdone, s_err, s_npend, s_cnt;
+    __shared__ uint32_t s_reqg, s_done, s_drop, s_tdone, s_tdrop, s_err, s_npend, s_cnt;
     __shared__ int64_t s_now, s_maxctx, s_nxt;
     __shared__ uint32_t s_steps, s_ring_n, s_ring_pos;
     __shared__ int64_t s_ring_sum;
@@ -156,7 +233,7 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
             sgf[g] = make_fast(G);
         }
         if (threadIdx.x == 0) {
-            s_good = 0; s_tok = 0; s_reqg = 0; s_done = 0; s_drop = 0; s_tdone = 0; s_err = 0;
+            s_good = 0; s_tok = 0; s_reqg = 0; s_done = 0; s_drop = 0; s_tdone = 0; s_tdrop = 0; s_err = 0;
             s_now = 0; s_steps = 0; s_ring_n = 0; s_ring_pos = 0; s_ring_sum = 0; s_stop = false;
             s_tguess = kNone;                              // no speculative threshold before the first step
         }
@@ -183,6 +260,7 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
             for (uint32_t u = 0; u < Sn && u < kMaxStages; ++u) tot += (uint64_t)st_pat[t * kMaxStages + u] * 1000000ull;
             S.ttot[t] = tot; S.tle[t] = 0;
             S.timer[t] = S.ta[t]; S.cur[t] = 0; S.cb[t] = 0; S.ce[t] = 0; S.left[t] = 0; S.tdone[t] = 0; S.gdone[t] = 0;
+            S.tever[t] = 0;
         }
         __syncthreads();
 
@@ -239,6 +317,29 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
             for (uint32_t t = threadIdx.x; t < nt; t += blockDim.x) {       // (a4) one thread per task
                 const uint32_t b = S.cb[t], e = S.ce[t];
                 if (S.tdone[t]) continue;
+                if (!S.tever[t] && now - S.ta[t] > c.waiting) {
+                    // (a1) P:545, A40: a task none of whose calls was ever scheduled is dropped once it
+                    // waited longer than waiting_time: its Queued / Waiting calls of every stage
+                    bool hit = false;
+                    for (uint32_t r = b; r < e; ++r) {
+                        const uint32_t st = m_state(S.meta[r]);
+                        hit |= st == kQueued || st == kWaiting;
+                    }
+                    if (hit) {
+                        const uint32_t Sn = A.t_nst[tm.task_off + t];
+                        for (uint32_t u = 0; u < Sn; ++u) {
+                            const uint32_t kk = t * kMaxStages + u;
+                            if (st_kind[kk] != 0) continue;
+                            for (uint32_t r = st_cb[kk]; r < st_ce[kk]; ++r) {
+                                const uint32_t st = m_state(S.meta[r]);
+                                if (st == kQueued || st == kWaiting) { S.meta[r] = m_with_state(S.meta[r], kDropped); ++my_drop; }
+                            }
+                        }
+                        S.tdone[t] = 1; S.timer[t] = INT64_MAX; S.cb[t] = 0; S.ce[t] = 0;
+                        atomicAdd(&s_tdrop, 1u);
+                        continue;
+                    }
+                }
                 uint64_t Tsum = 0, Gcur = 0; uint32_t cnt = 0;
                 for (uint32_t r = b; r < e; ++r) {
                     uint32_t meta = S.meta[r];
@@ -273,7 +374,6 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                     if (!make_key(Gp, t_gen, c.eps, &key)) my_err = 1;
                     S.img[r] = (uint64_t)__double_as_longlong(key);
                     S.cost[r] = token_cost(L_in[r], S.pre[r], c.chunk);
-                    if ((aux >> 16) < 0xFFFFu) S.aux[r] = aux + (1u << 16);
                     ++my_pend;
                 }
             }
@@ -446,7 +546,8 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                 __syncthreads();
             }
             const uint32_t nsel = s_nsel, i0 = s_bi[0];
-            // batch rows, bookkeeping (ever_scheduled, Running, undo steps_waited+1), max context
+            // batch rows, bookkeeping (ever_scheduled, Running), max context; a selected row keeps
+            // its steps_waited and is unmarked as pending (img) for the +1 of the others below
             int64_t myctx = 0;
             for (uint32_t k = threadIdx.x; k < nsel; k += blockDim.x) {
                 const uint32_t r = bBv[i0 + k];
@@ -454,15 +555,18 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                 uint32_t m = S.meta[r] | (kEver << 12);
                 if (m_state(m) == kQueued || m_state(m) == kPreempted) m = m_with_state(m, kRunning);
                 S.meta[r] = m;
-                const uint32_t aux = S.aux[r];
-                if ((aux >> 16) < 0xFFFFu) S.aux[r] = aux - (1u << 16);
+                if (tsk[r] != kNoTask) S.tever[tsk[r]] = 1;
                 const int64_t ctx = S.pre[r] < L_in[r] ? (int64_t)S.pre[r] + S.cost[r] : (int64_t)L_in[r] + S.gen[r];
                 myctx = ctx > myctx ? ctx : myctx;
             }
             if (threadIdx.x == 0) s_maxctx = 0;
             __syncthreads();
             atomicMax((unsigned long long*)&s_maxctx, (unsigned long long)myctx);
+            for (uint32_t k = threadIdx.x; k < nsel; k += blockDim.x) S.img[S.batch[k]] = kNone;
             __syncthreads();
+            // steps_waited + 1 (saturating) for every pending request left out (A12)
+            for (uint32_t r = threadIdx.x; r < n; r += blockDim.x)
+                if (S.img[r] != kNone && (S.aux[r] >> 16) < 0xFFFFu) S.aux[r] += 1u << 16;
             // ---- (a10) iteration latency and time advance
             const int64_t latency = A.c0 + A.c_att * s_maxctx + A.c_lin * (int64_t)nsel;
             const int64_t tnow = now + latency;
@@ -475,7 +579,7 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                     for (uint32_t k = 0; k < nsel; ++k) h = fnv1a_u32(h, S.batch[k]);
                     RLog L;
                     L.now_ns = tnow; L.n_selected = nsel; L.total_tokens = s_tot; L.n_candidates = ncd;
-                    L.b_star = s_bstar; L.bp = s_bp; L.ids_hash = h;
+                    L.b_star = s_bstar; L.bp = s_bp; L.ids_hash = h; L.v_token_ns = v;
                     A.log[(uint64_t)rep * A.log_steps + s_steps - 1] = L;
                 }
                 // v_token ring (Delta = frame_steps latencies)
@@ -524,7 +628,7 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
             RResult R;
             R.token_goodput = s_good; R.tokens_processed = s_tok; R.sim_end_ns = s_now;
             R.request_goodput = s_reqg; R.n_done = s_done; R.n_dropped = s_drop; R.steps = s_steps;
-            R.n_tasks_done = s_tdone; R.error = s_err;
+            R.n_tasks_done = s_tdone; R.n_tasks_dropped = s_tdrop; R.error = s_err; R.pad = 0;
             A.out[rep] = R;
         }
         __syncthreads();

@@ -1,8 +1,9 @@
 // select.cuh -- shared types of the pool step (Pool, Ctrl, Scratch, TaskInfo, ...), the row
 // scoring helpers used by the replay, and the EXACT path of the step (sm_100a).
 //
-// The step itself is k_score (score.cuh) -> k_spec (the speculative resolve).
-// When the speculation cannot be exact, finish_step (abi.cu) runs the exact path from the host:
+// The step itself is k_score (stream.cuh) -> k_spec (spec.cuh, the speculative
+// resolve).  When the speculation cannot be exact, finish_step (abi.cu) re-scores the pool with
+// every key materialized (k_score, kMat) and runs the exact path from the host:
 //   k_hist0    level-0 cost-weighted histogram of the composite key (key desc, id asc); the last
 //              CTA resolves the boundary bin
 //   k_pass     one more 12-bit digit while the boundary bucket is larger than kBucketCap
@@ -14,50 +15,17 @@
 //   k_publish  copies the control block to pinned host memory
 #pragma once
 #include "common.cuh"
+#include "pool.cuh"
 
 namespace jit {
 
 constexpr uint32_t kBucketCap = 4096;
 constexpr uint32_t kSpecCap = 8192;            // speculative set resolved in shared memory up to this size
 constexpr uint32_t kGroupSmemSort = 8192;     // |Cd| sorted in shared memory up to this size
-#ifndef JIT_SCORE_THREADS
-#define JIT_SCORE_THREADS 128
-#endif
-constexpr uint32_t kScoreThreads = JIT_SCORE_THREADS;
-#ifndef JIT_RPT
-#define JIT_RPT 2
-#endif
-constexpr uint32_t kRPT = JIT_RPT;               // consecutive rows per k_score thread (2 or 4)
-constexpr uint32_t kTile = kRPT * kScoreThreads;  // rows per k_score work item (tile)
 constexpr uint32_t kPassThreads = 512;
 
 enum : uint32_t { ST_RUN = 0, ST_HIST = 1, ST_COMPACT = 2, ST_RESOLVED = 3, ST_EMPTY = 4, ST_ERROR = 5, ST_FALLBACK = 6,
                   ST_SPEC_BIG = 7 };
-
-// per-task constants of the compound pass (a4), derived at load by k_task_prep from the task
-// arrays: absolute stage sub-deadline a_c + D_s (D_s = floor(D * t_<=s / t_total)),
-// absolute final deadline a_c + D, goodput of the finished stages; err = malformed pattern
-struct TaskInfo {
-    int64_t dls, dlf;
-    uint64_t gdone;
-    uint32_t err, pad;
-};
-
-struct Pool {
-    int64_t* arr;
-    uint32_t *len_in, *gen, *pre, *lhat, *meta, *aux, *id, *task, *ovr;
-    uint64_t* img;          // sort image = bits of the fp64 key; kNone when not pending
-    uint32_t* cost;         // token cost of the row this step (0 when not pending)
-    double* dbg_rate;       // optional debug outputs
-    int64_t* dbg_trem;
-    uint32_t* dbg_lhat;
-    uint32_t n, n_single, n_tasks, pad;
-    uint32_t* call_off;
-    int64_t *t_arr, *t_dl;
-    uint32_t *cur_stage, *n_stages, *pattern;
-    uint64_t* gdone;
-    TaskInfo* tinfo;
-};
 
 struct alignas(16) Ctrl {
     u128 prefix;                     // digits resolved so far (top bits of the composite key)
@@ -75,40 +43,55 @@ struct alignas(16) Ctrl {
     unsigned long long tot_cost;     // sum of the token costs of all pending rows
     uint32_t spec_n, spec_ovf, fallback, window_done;
     uint32_t n_refresh;                         // length-bound refreshes this step (a2)
-    uint32_t batch_on_host, pad_b;              // 1: the batch is in the pinned host mirror (fast path)
-    uint32_t chain;                             // (unused; kept for the control-block layout)
-    uint32_t trace, launch_err;                 // exact-path kernels that ran (bit mask) / device launch error
-    unsigned long long ts[12];                  // %globaltimer stamps of the single-CTA phases
+    uint32_t batch_on_host;                     // 1: the batch is in the pinned host mirror (fast path)
+    uint32_t steps, fallbacks;                  // the handle's counters after this step (Persist)
+    uint32_t trace, pad_t;                      // exact-path kernels that ran (bit mask)
+    unsigned long long ts[12];                  // %globaltimer stamps of the single-CTA phases (JIT_PHASE_STAMPS)
 };
 
-// state that survives across steps of one handle (not cleared by k_begin)
+// state that survives across steps of one handle (not cleared by a step)
 struct Persist {
     unsigned long long t_guess;      // speculative key-image threshold for the next step
-    uint32_t steps, fallbacks;
+    uint32_t steps;                  // step counter: the steps_waited stamps count against it
+    uint32_t fallbacks;              // steps resolved by the exact path (device count)
+    uint32_t host_pending;           // 1: the last step needs the host (exact path / big set / k_group)
+    uint32_t skipped;                // chained steps that did nothing because of host_pending
 };
 
-// per-CTA partial results of the scoring kernels (reduced by k_spec -- no global atomics)
+// the step's k_score partials, reduced by atomics (one set per CTA), read and reset by k_spec
 struct BlockPart {
-    unsigned long long min_img, tot_cost;
-    uint32_t n_pending, n_dropped, err, refresh;
+    unsigned long long cnt;          // pending (bits 0-31) | dropped this step (bits 32-63)
+    uint32_t refresh, err;
 };
-
-// compound CTA range of k_score: whole tasks [t0, t1) = call rows [r0, r1), packed greedily at
-// load so that r1 - (r0 & ~3) <= kTile unless one task alone is larger (then several tiles)
-struct CRange {
-    uint32_t r0, r1, t0, t1;
-};
-// key-image placeholder of a pending compound call between the two phases of a multi-tile
-// compound range: a NaN pattern carrying floor(steps_waited / Delta) (real key images are < 0x7FF0...)
-constexpr uint64_t kFramesTag = 0x7FF8000000000000ull;
 
 // %globaltimer (ns) stamp of a phase boundary, taken by thread 0 of a single-CTA kernel
+// (diagnostics only: compiled in with -DJIT_PHASE_STAMPS)
 __device__ __forceinline__ void stamp(Ctrl* ctrl, int i) {
+#ifdef JIT_PHASE_STAMPS
     if (threadIdx.x == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         ctrl->ts[i] = t;
     }
+#else
+    (void)ctrl; (void)i;
+#endif
+}
+
+// bookkeeping of one selected row (the batch of Alg. 1): ever_scheduled, Queued / Preempted ->
+// Running, and its steps_waited stamp moves with the counter (a selected request keeps its count)
+__device__ __forceinline__ void book_selected(const Pool& P, uint32_t r, uint32_t meta, uint32_t since, uint32_t sc) {
+    uint32_t mt = meta | (kEver << 12);
+    if (m_state(mt) == kQueued || m_state(mt) == kPreempted) mt = m_with_state(mt, kRunning);
+    *reinterpret_cast<uint2*>(&P.rows[r].meta) = make_uint2(mt, since_after_select(since, sc));
+    if (m_flags(meta) & kCompound) P.tever[P.task[r]] = 1u;      // the task has been scheduled (A40)
+}
+// thread 0 of the resolving kernel, after the batch: next step's speculative threshold and the counters
+__device__ __forceinline__ void finish_counters(Persist* ps, Ctrl* ctrl) {
+    ps->t_guess = (unsigned long long)__double_as_longlong(__dmul_rn(ctrl->thr, 0.85));
+    ps->steps += 1;
+    ps->fallbacks += ctrl->fallback;
+    ctrl->steps = ps->steps; ctrl->fallbacks = ps->fallbacks;
 }
 
 struct Scratch {
@@ -126,18 +109,18 @@ struct Scratch {
     uint32_t* out_rows;
     uint32_t cand_cap, pad;
     // the speculative set (kSpecCap entries): rows with key image >= t_guess, with what k_spec
-    // needs of them (key image, id, row, token cost, window length key)
+    // needs of them (key image, id, row, token cost, window length key, meta and since stamp)
     uint64_t* spec_img;
     uint32_t *spec_id, *spec_row, *spec_cost, *spec_len, *spec_meta, *spec_aux;
     Persist* persist;
-    BlockPart* part;         // (unused)
     BlockPart* gpart;        // the step's k_score partials, reduced atomically (reset by k_spec)
-    const CRange* crange;    // compound CTA ranges (n_crange)
-    uint32_t n_part, n_std, n_crange, pad3;   // partials = k_score CTAs; items = n_std tiles + ranges
+    const Item* items;       // work items of k_score (standalone row ranges, compound task ranges)
+    const uint32_t* n_items; // device count of items (appends grow it without a graph update)
+    uint32_t item_cap;         // capacity of items[] (every slot readable)
+    uint32_t n_std_items;      // items [0, n_std_items) are the standalone chunks of [0, n_single)
     unsigned int* spec_cnt;  // size of the speculative set (k_score atomics; reset by k_spec)
     Ctrl* h_ctrl;            // pinned host copy of the control block, written by the step's last kernel
     uint32_t* h_batch;       // pinned host mirror of the batch: ids | tokens | rows, (max_batch + 1) each
-    uint32_t nb_full, grid_pass;   // launch geometry of the exact path
 };
 
 // The last kernel of a step writes the control block straight into pinned host memory (no
@@ -288,80 +271,6 @@ __global__ void k_begin(Ctrl* ctrl, uint32_t* hcnt, unsigned long long* hcost, i
     if (tid == 0) { reset_ctrl(ctrl, now, v); *spec_cnt = 0; }
 }
 #endif  // !JIT_EXACT_TU
-
-// --------------------------------------------------------------------------------------
-// per-row scoring of a standalone request: (a1) admission, (a2) length bound, (a3) t_rem,
-// (a5) key, (a6) cost.  Pure function of the row + config; returns what to write back.
-// --------------------------------------------------------------------------------------
-struct RowRes {
-    uint64_t img;
-    uint32_t cost, meta, lhat, aux;
-    bool pending, dropped, w_meta, w_lhat, err;
-    double rate; int64_t trem; uint32_t lhatc;
-};
-
-// Per-group constants in the form the scoring loop uses (staged to shared memory per CTA):
-//   t_rem = arrival + base + (Lhat-1)*tok - now      (LAT: base=TTFT, tok=TBT  [A9];
-//                                                     DDL: base=E2EL; BE: base=default deadline)
-//   G     = w_in_eff * L_i + w_out_eff * Lhat        (DDL: w_in, w_out; LAT: 0, w_out; BE: 0, 0)
-struct GroupFast {
-    int64_t base, tok;
-    uint32_t w_in_eff, w_out_eff, type, pad;
-};
-__host__ __device__ inline GroupFast make_fast(const Group& g) {
-    GroupFast f;
-    f.type = g.type; f.pad = 0;
-    f.base = g.type == kLAT ? g.ttft_ns : g.type == kDDL ? g.e2el_ns : g.type == kBE ? g.be_deadline_ns : 0;
-    f.tok = g.type == kLAT ? g.tbt_ns : 0;
-    f.w_in_eff = (g.type == kDDL || g.type == kCMP) ? g.w_in : 0;   // CMP: used by the compound pass
-    f.w_out_eff = g.type != kBE ? g.w_out : 0;
-    return f;
-}
-
-template <bool kDebug>
-__device__ __forceinline__ void score_standalone(const Cfg& c, const Table& T, const GroupFast* sg, uint32_t n_groups,
-                                                 const uint32_t* ovr, uint32_t row, int64_t now, int64_t v,
-                                                 int64_t arr, uint32_t L_i, uint32_t g, uint32_t pre,
-                                                 uint32_t lhat, uint32_t meta, uint32_t aux, RowRes& o) {
-    o.img = kNone; o.cost = 0; o.meta = meta; o.lhat = lhat; o.aux = aux;
-    o.pending = o.dropped = o.w_meta = o.w_lhat = o.err = false;
-    if (kDebug) { o.rate = 0.0; o.trem = 0; o.lhatc = 0; }
-    if (arr > now) return;
-    const uint32_t st = m_state(meta), fl = m_flags(meta);
-    if (st == kQueued && !(fl & kEver) && !(fl & kCompound) && now - arr > c.waiting) {   // (a1) P:545
-        o.meta = m_with_state(meta, kDropped); o.w_meta = true; o.dropped = true;
-        return;
-    }
-    if (st > kPreempted) return;
-    o.pending = true;
-    const uint32_t gi = m_group(meta);
-    const uint32_t drow = aux & 0xFFFFu;
-    if (gi >= n_groups || drow >= T.n_rows || (fl & kCompound)) { o.err = true; return; }
-    const GroupFast G = sg[gi];
-    if (G.type == kCMP) { o.err = true; return; }
-    // (a2) conservative remaining length, refreshed every R tokens; cached per epoch
-    const uint32_t ep = fastdiv(g, c.R, c.R_m, c.R_l);
-    if (lhat == 0 || ep >= 65536u || m_epoch(meta) != ep) {
-        lhat = cond_quantile(T, drow, ep * c.R, c.qn, c.qd);
-        o.lhat = lhat; o.w_lhat = true;
-        if (ep < 65536u) { o.meta = (meta & 0xFFFFu) | (ep << 16); o.w_meta = true; }
-    }
-    const uint32_t Lh = lhat > g + 1 ? lhat : g + 1;
-    const uint32_t len_rem = Lh - g;
-    o.cost = token_cost(L_i, pre, c.chunk);
-    const uint64_t t_gen = (uint64_t)len_rem * (uint64_t)v;
-    const int64_t trem = arr + G.base + (int64_t)(Lh - 1) * G.tok - now;  // (a3)
-    uint64_t Gk = (uint64_t)G.w_in_eff * L_i + (uint64_t)G.w_out_eff * Lh;  // (a5) A10/A11
-    if (fl & kOverride) Gk = __ldg(ovr + row);
-    if (trem <= 0) Gk = 0;                                      // A22
-    if (c.appb && t_gen > (uint64_t)(trem > 0 ? trem : 0)) Gk = 0;
-    const uint64_t Gp = Gk + (uint64_t)c.delta * fastdiv(aux >> 16, c.frame, c.F_m, c.F_l);
-    double key;
-    if (!make_key(Gp, t_gen, c.eps, &key)) { o.err = true; return; }
-    o.img = (uint64_t)__double_as_longlong(key);
-    if ((aux >> 16) < 0xFFFFu) o.aux = aux + (1u << 16);       // steps_waited+1; undone if selected
-    if (kDebug) { o.rate = make_rate(len_rem, trem); o.trem = trem; o.lhatc = Lh; }
-}
 
 // ======================================================================================
 // The exact path (radix select .. window): compiled into the separately linked unit
@@ -679,27 +588,21 @@ static __device__ void window_select(const Pool& P, const Cfg& c, Ctrl* ctrl, co
     bi = s_bi[0]; bj = s_bj[0];
     stamp(ctrl, 9);
     const uint32_t ns = bj - bi + 1;
+    const uint32_t sc = S.persist->steps;
+    __syncthreads();
     for (uint32_t k = threadIdx.x; k < ns; k += blockDim.x) {
         const uint32_t r = sv[bi + k];
         S.out_ids[k] = P.id[r];
         S.out_tokens[k] = P.cost[r];
         S.out_rows[k] = r;
-        uint32_t m = P.meta[r] | (kEver << 12);
-        if (m_state(m) == kQueued || m_state(m) == kPreempted) m = m_with_state(m, kRunning);
-        P.meta[r] = m;
-        const uint32_t aux = P.aux[r];
-        if ((aux >> 16) < 0xFFFFu) P.aux[r] = aux - (1u << 16);
+        book_selected(P, r, P.rows[r].meta, P.rows[r].since, sc);
     }
     if (threadIdx.x == 0) {
         ctrl->n_selected = ns;
         ctrl->total_tokens = (uint32_t)(pc[bj + 1] - pc[bi]);
         ctrl->i_best = bi; ctrl->j_best = bj;
         ctrl->window_done = 1;
-        // next step's speculative threshold: this step's cutoff with a 15% margin
-        Persist* ps = S.persist;
-        ps->t_guess = (unsigned long long)__double_as_longlong(__dmul_rn(ctrl->thr, 0.85));
-        ps->steps += 1;
-        ps->fallbacks += ctrl->fallback;
+        finish_counters(S.persist, ctrl);      // next step's threshold: this cutoff with a 15% margin
     }
     stamp(ctrl, 10);
 }
@@ -729,7 +632,7 @@ static __device__ void group_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const
     else { sk = S.sk; sv = S.sv; }
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
         const uint32_t r = S.cand[i];
-        const uint64_t len = c.len_key ? (uint64_t)P.len_in[r] + P.gen[r] : (uint64_t)P.len_in[r];
+        const uint64_t len = c.len_key ? (uint64_t)P.rows[r].len_in + P.rows[r].gen : (uint64_t)P.rows[r].len_in;
         sk[i] = (len << 32) | P.id[r];                      // (len asc, id asc), A17/A18
         sv[i] = r;
     }
@@ -742,21 +645,60 @@ static __device__ void group_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const
 // k_publish: copies the control block to pinned host memory (end of the host-run exact path)
 __global__ void k_publish(const Ctrl* ctrl, Ctrl* host) { publish_ctrl(ctrl, host); }
 
-// progress updates from the engine, applied before scoring
-__global__ void k_progress(Pool P, const uint32_t* rows, const uint32_t* gen, const uint32_t* pre,
+// load: pack the caller's SoA pool into hot rows.  lrow = dist_row | L-hat unset; the count in
+// aux's high half becomes the frozen steps_waited (the first step stamps the pending rows).
+__global__ void k_pack(HotRow* rows, uint32_t n, const int64_t* arr, const uint32_t* len_in, const uint32_t* gen,
+                       const uint32_t* pre, const uint32_t* meta, const uint32_t* aux) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        HotRow q;
+        q.arr = arr[r]; q.len_in = len_in[r]; q.gen = gen[r]; q.pre = pre[r];
+        q.lrow = aux[r] & 0xFFFFu;
+        q.meta = meta[r] & ~(kStamped << 12);     // caller meta: bits 16-31 zero (validated)
+        q.since = aux[r] >> 16;
+        rows[r] = q;
+    }
+}
+
+// progress updates from the engine (keyed by row), applied before the step's pass.  A row
+// leaving the pending set freezes its steps_waited (sc = the handle's counter); the ranges the
+// pass relies on are checked (A: gen < 2^24, prefilled <= L_i, state <= Waiting, no way out of
+// Done / Dropped); a violation fails the step (gpart->err).
+__global__ void k_progress(Pool P, Scratch S, const uint32_t* rows_in, const uint32_t* gen, const uint32_t* pre,
                            const uint32_t* state, uint32_t n) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const uint32_t r = rows[i];
-    if (r >= P.n) return;
-    P.gen[r] = gen[i];
-    P.pre[r] = pre[i];
-    P.meta[r] = m_with_state(P.meta[r], state[i] & 0xFu);
+    const uint32_t r = rows_in[i];
+    if (r >= P.n) { atomicOr(&S.gpart->err, 8u); return; }
+    HotRow* rp = P.rows + r;
+    const uint32_t st = state[i], old_st = m_state(rp->meta);
+    if (gen[i] >= (1u << 24) || pre[i] > rp->len_in || st > kWaiting ||
+        ((old_st == kDone || old_st == kDropped) && st != old_st)) {
+        atomicOr(&S.gpart->err, 8u);
+        return;
+    }
+    uint32_t meta = m_with_state(rp->meta, st), since = rp->since;
+    if ((meta >> 12) & kStamped && st > kPreempted) {          // left the pending set: freeze
+        since = waited_of(meta, since, S.persist->steps);
+        meta &= ~(kStamped << 12);
+    }
+    rp->gen = gen[i];
+    rp->pre = pre[i];
+    *reinterpret_cast<uint2*>(&rp->meta) = make_uint2(meta, since);
+}
+
+// every 2^30 steps: keep the stamps of rows that wait for ever within 0xFFFF of the counter, so
+// that step - since never wraps (the count saturates at 0xFFFF anyway)
+__global__ void k_rebase(Pool P, Scratch S) {
+    const uint32_t sc = S.persist->steps;
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < P.n; r += gridDim.x * blockDim.x) {
+        HotRow* rp = P.rows + r;
+        if (((rp->meta >> 12) & kStamped) && sc - rp->since > 0xFFFFu) rp->since = sc - 0xFFFFu;
+    }
 }
 
 // load-time per-task constants (TaskInfo); D * le fits u64 when D < 2^40 ns and t_total < 2^24 ms
-__global__ void k_task_prep(Pool P) {
-    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < P.n_tasks; t += gridDim.x * blockDim.x) {
+__global__ void k_task_prep(Pool P, uint32_t t_begin) {
+    for (uint32_t t = t_begin + blockIdx.x * blockDim.x + threadIdx.x; t < P.n_tasks; t += gridDim.x * blockDim.x) {
         const int64_t a_c = P.t_arr[t], D = P.t_dl[t];
         const uint32_t s = P.cur_stage[t], Sn = P.n_stages[t];
         uint64_t le = 0, tot = 0;
@@ -764,38 +706,49 @@ __global__ void k_task_prep(Pool P) {
             const uint64_t ms = u < Sn ? P.pattern[(size_t)t * kMaxStages + u] : 0u;
             tot += ms; if (u <= s) le += ms;
         }
-        TaskInfo ti;
-        ti.err = (tot == 0 || Sn == 0 || Sn > kMaxStages || s >= Sn) ? 1u : 0u;
         const int64_t Ds = !tot ? 0
             : ((uint64_t)D < (1ull << 40) && tot < (1ull << 24)) ? (int64_t)((uint64_t)D * le / tot)
                                                                  : (int64_t)((u128)(uint64_t)D * le / tot);
+        TaskInfo ti;
         ti.dls = a_c + Ds;                // advisory stage deadline: missing it only sets rate = inf
         ti.dlf = a_c + D;                 // final deadline: missing it zeroes the task goodput (A43)
+        ti.ac = a_c;                      // admission of the task (A40)
         ti.gdone = P.gdone[t];
-        ti.pad = 0;
         P.tinfo[t] = ti;
+        uint32_t ever = 0;                // A40: some call of the task in the pool was scheduled
+        for (uint32_t r = P.call_off[t]; r < P.call_off[t + 1] && r < P.n; ++r)
+            ever |= (m_flags(P.rows[r].meta) & kEver) ? 1u : 0u;
+        P.tever[t] = ever;
     }
 }
 
 // load-time validation of a pool (layout rule of jit_pool, group types, ranges)
-__global__ void k_validate(Pool P, const Group* groups, uint32_t n_groups, uint32_t n_rows_tab, Ctrl* ctrl) {
+__global__ void k_validate(Pool P, const Group* groups, uint32_t n_groups, uint32_t n_rows_tab, uint32_t l_max,
+                           Ctrl* ctrl, uint32_t r_begin, uint32_t t_begin) {
     const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t seg_end = P.n_tasks ? P.call_off[P.n_tasks] : 0u;   // end of the compound CSR rows
     bool bad = false;
-    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < P.n; r += stride) {
-        const uint32_t meta = P.meta[r], aux = P.aux[r];
+    for (uint32_t r = r_begin + blockIdx.x * blockDim.x + threadIdx.x; r < P.n; r += stride) {
+        const HotRow q = P.rows[r];
+        const uint32_t meta = q.meta;
         const uint32_t gi = m_group(meta);
         const bool comp = (m_flags(meta) & kCompound) != 0;
-        if (gi >= n_groups || (aux & 0xFFFFu) >= n_rows_tab || P.len_in[r] == 0 || P.len_in[r] >= (1u << 24) ||
-            P.gen[r] >= (1u << 24) || (meta >> 16) != 0 || m_state(meta) > kWaiting) bad = true;
-        else if (r < P.n_single) {
-            if (comp || P.task[r] != kNoTask || groups[gi].type == kCMP) bad = true;
+        if (gi >= n_groups || l_row(q.lrow) >= n_rows_tab || q.len_in == 0 || q.len_in >= (1u << 24) ||
+            q.gen >= (1u << 24) || q.pre > q.len_in || (meta >> 16) != 0 || m_state(meta) > kWaiting ||
+            q.since > 0xFFFFu) bad = true;
+        else if (!comp) {
+            if (P.task[r] != kNoTask || groups[gi].type == kCMP || (r >= P.n_single && r < seg_end)) bad = true;
         } else {
             const uint32_t t = P.task[r];
-            if (!comp || t >= P.n_tasks || groups[gi].type != kCMP || (m_flags(meta) & kOverride)) bad = true;
+            if (t >= P.n_tasks || groups[gi].type != kCMP || (m_flags(meta) & kOverride)) bad = true;
             else if (r < P.call_off[t] || r >= P.call_off[t + 1]) bad = true;
+            // a call's goodput w_in L_i + w_out L-hat stays below 2^27 (the pass sums 32 calls in u32)
+            else if ((uint64_t)groups[gi].w_in * q.len_in + (uint64_t)groups[gi].w_out * (l_max + 1ull) >= (1ull << 27))
+                bad = true;
         }
+        if (!bad && (m_flags(meta) & kOverride) && groups[gi].type == kCMP) bad = true;
     }
-    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < P.n_tasks; t += stride) {
+    for (uint32_t t = t_begin + blockIdx.x * blockDim.x + threadIdx.x; t < P.n_tasks; t += stride) {
         const uint32_t S = P.n_stages[t], s = P.cur_stage[t];
         if (P.call_off[t] > P.call_off[t + 1] || S == 0 || S > kMaxStages || s >= S) bad = true;
         else {
@@ -804,7 +757,7 @@ __global__ void k_validate(Pool P, const Group* groups, uint32_t n_groups, uint3
             if (tot == 0) bad = true;
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && t_begin == 0) {   // a load: standalone rows, then the CSR
         if (P.n_tasks && (P.call_off[0] != P.n_single || P.call_off[P.n_tasks] != P.n)) bad = true;
         if (!P.n_tasks && P.n_single != P.n) bad = true;
     }

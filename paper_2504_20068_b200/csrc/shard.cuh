@@ -130,7 +130,7 @@ __global__ void k_export2(Pool P, Cfg c, Ctrl* ctrl, Scratch S, Rec2* out, uint3
         const uint32_t r = S.cand[i];
         Rec2 q;
         q.img = P.img[r]; q.id = P.id[r]; q.cost = P.cost[r];
-        q.len = c.len_key ? P.len_in[r] + P.gen[r] : P.len_in[r];
+        q.len = c.len_key ? P.rows[r].len_in + P.rows[r].gen : P.rows[r].len_in;
         q.row = r; q.rank = rank; q.pad = 0;
         out[i] = q;
     }
@@ -215,27 +215,23 @@ __global__ void __launch_bounds__(1024) k_group_rec(Pool P, Cfg c, Ctrl* ctrl, S
     __syncthreads();
     bi = s_bi[0]; bj = s_bj[0];
     const uint32_t ns = bj - bi + 1;
+    const uint32_t sc = S.persist->steps;
+    __syncthreads();
     for (uint32_t k = threadIdx.x; k < ns; k += blockDim.x) {
         const Rec2& q = all[sv[bi + k]];
         S.out_ids[k] = q.id;
         S.out_tokens[k] = q.cost;
         S.out_rows[k] = q.rank == rank ? q.row : 0xFFFFFFFFu;
-        if (q.rank == rank) {                          // bookkeeping for this shard's rows
-            const uint32_t r = q.row;
-            uint32_t m = P.meta[r] | (kEver << 12);
-            if (m_state(m) == kQueued || m_state(m) == kPreempted) m = m_with_state(m, kRunning);
-            P.meta[r] = m;
-            const uint32_t aux = P.aux[r];
-            if ((aux >> 16) < 0xFFFFu) P.aux[r] = aux - (1u << 16);
-        }
+        if (q.rank == rank)                            // bookkeeping for this shard's rows
+            book_selected(P, q.row, P.rows[q.row].meta, P.rows[q.row].since, sc);
     }
     if (threadIdx.x == 0) {
         ctrl->n_selected = ns;
         ctrl->n_cand = n;
         ctrl->total_tokens = (uint32_t)(S.pc[bj + 1] - S.pc[bi]);
         ctrl->window_done = 1;
-        // next step's speculative threshold (identical on every rank: thr is global)
-        S.persist->t_guess = (unsigned long long)__double_as_longlong(__dmul_rn(ctrl->thr, 0.85));
+        // next step's speculative threshold (identical on every rank: thr is global) and counters
+        finish_counters(S.persist, ctrl);
     }
 }
 

@@ -98,11 +98,13 @@ class jit_replay_cfg(C.Structure):
 
 class jit_replay_result(C.Structure):
     _fields_ = [("token_goodput", C.c_uint64), ("tokens_processed", C.c_uint64), ("sim_end_ns", C.c_int64)] + \
-               [(k, C.c_uint32) for k in ("request_goodput", "n_done", "n_dropped", "steps", "n_tasks_done", "error")]
+               [(k, C.c_uint32) for k in ("request_goodput", "n_done", "n_dropped", "steps", "n_tasks_done",
+                                          "n_tasks_dropped", "error", "reserved")]
 
 
 STEP_LOG_DTYPE = np.dtype([("now_ns", "<i8"), ("n_selected", "<u4"), ("total_tokens", "<u4"),
-                           ("n_candidates", "<u4"), ("b_star", "<u4"), ("bp", "<f8"), ("ids_hash", "<u8")])
+                           ("n_candidates", "<u4"), ("b_star", "<u4"), ("bp", "<f8"), ("ids_hash", "<u8"),
+                           ("v_token_ns", "<i8")])
 
 _lib = None
 EXPORTS = ("jit_sched_workspace_bytes", "jit_sched_init", "jit_sched_load", "jit_sched_step",
@@ -110,7 +112,7 @@ EXPORTS = ("jit_sched_workspace_bytes", "jit_sched_init", "jit_sched_load", "jit
            "jit_replay_workspace_bytes", "jit_sched_replay", "jit_sched_destroy", "jit_sched_last_error",
            "jit_sched_version", "jit_shard_prefix", "jit_shard_merge", "jit_shard_candidates", "jit_shard_finish",
            "jit_sched_phase_times", "jit_shard_spec_bytes", "jit_shard_spec_export", "jit_shard_spec_resolve",
-           "jit_sched_time_scoring")
+           "jit_sched_time_scoring", "jit_sched_counters", "jit_sched_debug_scratch")
 
 
 def load_library(path: str = LIB_PATH):
@@ -293,11 +295,14 @@ class Scheduler:
                 "batch_rows": self._rows[:k].copy()}
 
     def read_rows(self, debug: bool = True) -> dict:
+        """Per-row state after the last step: meta and aux (dist_row | steps_waited) always; keys,
+        costs, pending flags, rates, t_rem and L-hat only on debug handles (a production step
+        writes no per-row output)."""
         n = self.n
-        out = {"key": np.zeros(n, np.float64), "cost": np.zeros(n, np.uint32), "pending": np.zeros(n, np.uint32),
-               "meta": np.zeros(n, np.uint32), "aux": np.zeros(n, np.uint32)}
+        out = {"meta": np.zeros(n, np.uint32), "aux": np.zeros(n, np.uint32)}
         if debug:
-            out.update(rate=np.zeros(n, np.float64), t_rem=np.zeros(n, np.int64), lhat=np.zeros(n, np.uint32))
+            out.update(key=np.zeros(n, np.float64), cost=np.zeros(n, np.uint32), pending=np.zeros(n, np.uint32),
+                       rate=np.zeros(n, np.float64), t_rem=np.zeros(n, np.int64), lhat=np.zeros(n, np.uint32))
         g = lambda k: _p(out[k]) if k in out else None
         self._check(self.lib.jit_sched_read_rows(self.h, g("key"), g("rate"), g("t_rem"), g("lhat"), g("cost"),
                                                  g("pending"), g("meta"), g("aux")), self.h)
@@ -313,6 +318,18 @@ class Scheduler:
         t = (C.c_float * 5)()
         self._check(self.lib.jit_sched_kernel_times(self.h, C.c_int(-1), t, 5), self.h)
         return list(t)
+
+    def counters(self) -> dict:
+        """Device counters: resolved steps, exact-path steps, chained steps skipped."""
+        a, b, c = C.c_uint32(), C.c_uint32(), C.c_uint32()
+        self._check(self.lib.jit_sched_counters(self.h, C.byref(a), C.byref(b), C.byref(c)), self.h)
+        return {"steps": a.value, "fallbacks": b.value, "skipped": c.value}
+
+    def debug_scratch(self, n: int) -> np.ndarray:
+        """Diagnostics: the first n u64 of the sort scratch (JIT_TIMELINE stamps)."""
+        out = np.zeros(n, np.uint64)
+        self._check(self.lib.jit_sched_debug_scratch(self.h, _p(out), C.c_uint32(n)), self.h)
+        return out
 
     def phase_times(self):
         """%globaltimer stamps (ns, relative to the first) of the single-CTA resolve phases."""

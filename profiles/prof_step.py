@@ -14,14 +14,17 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--steps", type=int, default=6)
 ap.add_argument("--rot", type=int, default=3)
 ap.add_argument("--rows", type=int, default=1 << 20)
+ap.add_argument("--frac-compound", type=float, default=0.3)
 a = ap.parse_args()
-d = W.pool_snapshot(3, a.rows)
+d = W.pool_snapshot(3, a.rows, frac_compound=a.frac_compound)
 n, nt = len(d["pool"]["input_len"]), len(d["tasks"]["arrival_ns"])
 hs = []
 for i in range(a.rot):
     s = Scheduler(d["cfg"], d["groups"], d["table"], capacity=n, task_capacity=nt)
     s.load(d["pool"], d["tasks"])
-    s.step(d["now_ns"], d["v_token_ns"])
+    for _ in range(3):                     # first step: exact path (+ re-score); then the fast path
+        r = s.step(d["now_ns"], d["v_token_ns"])
+    print("handle", i, "fallback", r["fallback"], "n_spec", r["n_spec"])
     hs.append(s)
 for k in range(a.steps):
     hs[k % a.rot].step_async(d["now_ns"], d["v_token_ns"])

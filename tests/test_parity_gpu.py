@@ -34,7 +34,7 @@ def _compare(got, ref, rows=None, pool=None, ctx=""):
         assert np.array_equal(got["batch_ids"], ref["batch_ids"]), ctx
         assert np.array_equal(got["batch_tokens"], ref["batch_tokens"]), ctx
         assert np.array_equal(got["batch_rows"], ref["batch_rows"]), ctx
-    if rows is not None:
+    if rows is not None and "key" in rows:
         pend = ref["pending"].astype(bool)
         assert np.array_equal(rows["pending"].astype(bool), pend), ctx
         assert np.array_equal(rows["key"].view(np.uint64)[pend], ref["key"].view(np.uint64)[pend]), ctx
@@ -43,6 +43,7 @@ def _compare(got, ref, rows=None, pool=None, ctx=""):
             assert np.array_equal(rows["lhat"][pend], ref["lhat"][pend]), ctx
             assert np.array_equal(rows["t_rem"][pend], ref["t_rem"][pend]), ctx
             assert np.array_equal(rows["rate"].view(np.uint64)[pend], ref["rate"].view(np.uint64)[pend]), ctx
+    if rows is not None:
         assert np.array_equal(rows["meta"], ref["meta"]), ctx
         assert np.array_equal(rows["aux"], ref["aux"]), ctx
 
@@ -212,9 +213,9 @@ def test_speculative_paths_against_oracle_chain():
 
 def test_time_scoring_leaves_state_consistent():
     """bench.py's roofline timing (jit_sched_time_scoring: back-to-back k_score launches over
-    several handles) must leave each handle as L empty steps would: every pending row's
-    steps_waited advanced by L (saturating, P:467's wait counter), meta untouched, and the per-step
-    partials / speculative set consumed -- the next step still equals the oracle's."""
+    several handles) must leave each handle's pool as it was: the pass writes no per-row state in
+    the steady state and the step counter (steps_waited stamps) only moves with a resolved step;
+    the per-step partials / speculative set are consumed -- the next step equals the oracle's."""
     from paper_2504_20068_b200 import Scheduler
     L = 5
     ds, hs, pools = [], [], []
@@ -228,10 +229,6 @@ def test_time_scoring_leaves_state_consistent():
             ref = oracle.step(d["cfg"], d["groups"], d["table"], d["now_ns"], d["v_token_ns"], pool, d["tasks"])
             _compare(s.step(d["now_ns"], d["v_token_ns"]), ref)
             pool["meta"], pool["aux"] = ref["meta"], ref["aux"]
-        pend = ref["pending"].astype(bool)
-        waited = pool["aux"] >> 16
-        pool["aux"] = np.where(pend, (pool["aux"] & 0xFFFF) | (np.minimum(waited + L, 0xFFFF) << 16),
-                               pool["aux"]).astype(pool["aux"].dtype)
         ds.append(d); hs.append(s); pools.append(pool)
     ms = Scheduler.time_scoring(hs, ds[0]["now_ns"], ds[0]["v_token_ns"], L * len(hs))
     assert ms > 0

@@ -11,7 +11,7 @@ from tests import _builders as B
 pytestmark = pytest.mark.gpu
 
 RES_KEYS = ("token_goodput", "tokens_processed", "sim_end_ns", "request_goodput", "n_done", "n_dropped", "steps",
-            "n_tasks_done")
+            "n_tasks_done", "n_tasks_dropped")
 
 
 def _sched(d, cap=64):
