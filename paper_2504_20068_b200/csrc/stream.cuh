@@ -31,7 +31,7 @@ namespace jit {
 #define JIT_SCORE_MINB 4
 #endif
 #ifndef JIT_STAGES_W
-#define JIT_STAGES_W 3
+#define JIT_STAGES_W 2
 #endif
 constexpr uint32_t kStagesW = JIT_STAGES_W;     // shared-memory item slots per warp
 constexpr uint32_t kScoreThreads = JIT_SCORE_THREADS;
@@ -41,7 +41,8 @@ constexpr uint32_t kScoreWarps = kScoreThreads / 32;
 #endif
 constexpr uint32_t kR = JIT_ROWS_PER_LANE;      // hot rows per lane per item chunk
 constexpr uint32_t kItemRows = 32 * kR;         // rows per item (chunk)
-constexpr uint32_t kItemTasks = 32;             // tasks per compound item (shared-memory slots)
+constexpr uint32_t kItemTasks = 32;             // tasks per compound item (one per lane; <= 32)
+static_assert(kItemTasks <= 32, "a compound item's task sums live in one lane each");
 
 // per-group constants of the pass, with `now` folded in (per launch):
 //   t_rem = arr + bn + (Lhat - 1) * tok       bn = base - now (LAT: TTFT, DDL: E2EL, BE: default)
@@ -116,18 +117,14 @@ __device__ __forceinline__ void rare_row(const Table& T, const Cfg& c, HotRow* r
     ref += stale;
 }
 
-// the key image of a pending row: fl(G' 1e9 / B), B = fl(t_gen + eps) exact.  Unless every key is
-// wanted (kMat), the division runs only when A >= fl(t_lo B) with t_lo = t (1 - 2^-20): if
-// A < fl(t_lo B) then A/B < t (1 - 2^-21) and fl(A/B) < t, so the row cannot reach the set and
-// any image below t stands for its key.
-template <bool kMat>
-__device__ __forceinline__ uint64_t key_img(uint64_t Gp, double B, double t_lo, bool pend, uint32_t& err) {
-    const double A = __dmul_rn(__ull2double_rn(Gp), 1e9);
-    if (pend && Gp >= kTwo53 / 1000000000ull) err = 1;          // G' * 1e9 must stay an exact integer
-    uint64_t img = pend ? 0ull : kNone;
-    const bool need = pend && (kMat || !(A < __dmul_rn(t_lo, B)));
-    if (need) img = (uint64_t)__double_as_longlong(div_rn_int(A, B));
-    return img;
+// The pre-test in fp32: A_f = fl(G' 1e9) (G' < 2^24 and 1e9 are exact fp32 integers, one rounding),
+// B_f = fl(len_rem v_f + eps_f) (v_f, eps_f rounded), t_lo_f = t (1 - 2^-16) rounded toward zero.
+// If A_f < fl(t_lo_f B_f) then A/B < t (1 - 2^-16)(1 + 2^-22) / (1 - 2^-24) < t (1 - 2^-17), so
+// fl(A/B) < t: the row cannot reach the speculative set.
+__device__ __forceinline__ bool below_t(uint32_t Gp, uint32_t len_rem, float v_f, float eps_f, float t_lo_f) {
+    const float Af = __fmul_rn(__uint2float_rn(Gp), 1e9f);
+    const float Bf = __fmaf_rn(__uint2float_rn(len_rem), v_f, eps_f);
+    return Af < __fmul_rn(t_lo_f, Bf);
 }
 
 // ---- per-warp ring of item slots fed by bulk asynchronous copies (PTX, sm_90+)
@@ -222,9 +219,10 @@ __device__ __forceinline__ void spec_rows(const Scratch& S, const Pool& P, const
 template <bool kMat, bool kDebug, bool kAppB>
 __device__ __forceinline__ void std_item(const Pool& P, const Table& T, const GroupNow* sg, const Cfg& c,
                                          const Scratch& S, int64_t now, double v_d, int64_t v, uint32_t sc,
-                                         uint64_t t_img, double t_lo, const Item& it, WarpSlot* sl, Part& A) {
+                                         uint64_t t_img, float t_lo_f, const Item& it, WarpSlot* sl, Part& A) {
     const uint32_t lane = threadIdx.x & 31;
     const double eps_d = (double)c.eps;
+    const float v_f = (float)v, eps_f = (float)c.eps;
     const int64_t drop_before = now - c.waiting;           // now - arr > waiting <=> arr < now - waiting
     const uint32_t nr = it.r1 - it.r0;
     HotRow q[kR];
@@ -258,7 +256,7 @@ __device__ __forceinline__ void std_item(const Pool& P, const Table& T, const Gr
         }
     }
     // (a3) t_rem, (a5) goodput (A9-A11, A22), starvation inflation (A12), the pre-test
-    double Ak[kR], Bk[kR];
+    uint32_t Gk32[kR], Lr[kR];
     uint32_t div_m = 0;
 #pragma unroll
     for (uint32_t k = 0; k < kR; ++k) {
@@ -275,9 +273,8 @@ __device__ __forceinline__ void std_item(const Pool& P, const Table& T, const Gr
         const uint32_t waited = min(sc - x.since, 0xFFFFu);
         const uint64_t Gp = Gk + (uint64_t)c.delta * fastdiv(waited, c.frame, c.F_m, c.F_l);
         if (pend && Gp >= kTwo53 / 1000000000ull) A.err = 1;   // G' * 1e9 must stay an exact integer
-        Bk[k] = __fma_rn(__uint2double_rn(len_rem), v_d, eps_d);      // < 2^53: v, eps < 2^36
-        Ak[k] = __dmul_rn(__uint2double_rn((uint32_t)Gp), 1e9);
-        div_m |= (uint32_t)(pend && (kMat || !(Ak[k] < __dmul_rn(t_lo, Bk[k])))) << k;
+        Gk32[k] = (uint32_t)Gp; Lr[k] = len_rem;
+        div_m |= (uint32_t)(pend && (kMat || !below_t((uint32_t)Gp, len_rem, v_f, eps_f, t_lo_f))) << k;
         if (kDebug && 32 * k + lane < nr) {
             const uint32_t r = it.r0 + 32 * k + lane;
             P.dbg_rate[r] = pend ? make_rate(len_rem, trem) : 0.0;
@@ -291,7 +288,9 @@ __device__ __forceinline__ void std_item(const Pool& P, const Table& T, const Gr
     if (__any_sync(0xffffffffu, div_m)) {
 #pragma unroll
         for (uint32_t k = 0; k < kR; ++k)
-            if ((div_m >> k) & 1u) img[k] = (uint64_t)__double_as_longlong(div_rn_int(Ak[k], Bk[k]));
+            if ((div_m >> k) & 1u)
+                img[k] = (uint64_t)__double_as_longlong(div_rn_int(__dmul_rn(__uint2double_rn(Gk32[k]), 1e9),
+                                                                   __fma_rn(__uint2double_rn(Lr[k]), v_d, eps_d)));
     }
     A.pend += __popc(pend_m);
     uint32_t mem_m = 0;
@@ -317,6 +316,7 @@ struct TaskSlots {
     uint32_t F[kItemTasks];       // 4: task dropped (A40)
     unsigned long long G[kItemTasks];   // sum of the calls' goodput, then the task goodput G_task
     double B[kItemTasks];         // fl(t_gen + eps) of the task, -1 when out of the exact range
+    float Bf[kItemTasks];         // fl32 of it (the pre-test)
 };
 
 // phase A of a chunk of calls (rows base + 32 k + lane): pending / drop / regime / bound (a1, a2),
@@ -327,7 +327,8 @@ template <typename RowAt, typename TaskAt, typename WriteBack>
 __device__ __forceinline__ void cmp_phase_a(const Pool& P, const Table& T, const GroupNow* sg, const Cfg& c,
                                             int64_t now, uint32_t sc, const Item& it, uint32_t base, TaskSlots& ts,
                                             RowAt row_at, TaskAt task_at, WriteBack write_back, uint32_t* lt,
-                                            uint32_t* fr, uint32_t& pend_m, Part& A) {
+                                            uint32_t* fr, uint32_t& pend_m, uint32_t& accT,
+                                            unsigned long long& accG, Part& A) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t ntl = it.t1 - it.t0;
     HotRow q[kR];
@@ -376,24 +377,39 @@ __device__ __forceinline__ void cmp_phase_a(const Pool& P, const Table& T, const
             if (g64 >> 27) A.err = 1;            // a slab's sum (32 calls) must fit 32 bits (validated at load)
             Tl = Lh - x.gen; Gc = (uint32_t)g64;
         }
+        if (base + 32 * k >= it.r1) continue;                 // warp-uniform: the slab is empty
+#ifdef JIT_SEGSCAN
+        // segmented inclusive scan over the slab (tasks are contiguous lane ranges), then the last
+        // lane of each task's segment adds the segment's sums into the task's slot
+        uint32_t sT = Tl, sG = Gc;
+#pragma unroll
+        for (uint32_t d = 1; d < 32; d <<= 1) {
+            const uint32_t oT = __shfl_up_sync(0xffffffffu, sT, d), oG = __shfl_up_sync(0xffffffffu, sG, d);
+            const uint32_t ol = __shfl_up_sync(0xffffffffu, lt[k], d);
+            if (lane >= d && ol == lt[k]) { sT += oT; sG += oG; }
+        }
+        const uint32_t nl = __shfl_down_sync(0xffffffffu, lt[k], 1);
+        if (lt[k] < ntl && (lane == 31 || nl != lt[k])) { ts.T[lt[k]] += sT; ts.G[lt[k]] += sG; }
+        __syncwarp();
+#else
         // the slab's tasks: from lane 0's to the last row's (rows ordered by task)
         const uint32_t last = base + 32 * k + 31 < it.r1 ? 31u : it.r1 - 1 - (base + 32 * k);
-        if (base + 32 * k >= it.r1) continue;                 // warp-uniform: the slab is empty
         const uint32_t tf = __shfl_sync(0xffffffffu, lt[k], 0), tl = __shfl_sync(0xffffffffu, lt[k], last);
         if (tf >= ntl || tl >= ntl) continue;                 // malformed (A.err already set)
         for (uint32_t t = tf; t <= tl; ++t) {                  // warp-uniform (usually 1-3 tasks)
             const bool mine = lt[k] == t;
             const uint32_t sT = __reduce_add_sync(0xffffffffu, mine ? Tl : 0u);
             const uint32_t sG = __reduce_add_sync(0xffffffffu, mine ? Gc : 0u);
-            if (lane == 0) { ts.T[t] += sT; ts.G[t] += sG; }
+            if (lane == (t & 31u)) { accT += sT; accG += sG; }  // task t's sums live in lane t % 32
         }
+#endif
     }
 }
 
 template <bool kMat, bool kDebug, bool kAppB>
 __device__ __forceinline__ void cmp_item(const Pool& P, const Table& T, const GroupNow* sg, const Cfg& c,
                                          const Scratch& S, int64_t now, int64_t v, uint32_t sc, uint64_t t_img,
-                                         double t_lo, const Item& it, WarpSlot* sl, TaskSlots& ts, Part& A) {
+                                         float t_lo_f, const Item& it, WarpSlot* sl, TaskSlots& ts, Part& A) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t ntl = it.t1 - it.t0;
     const bool big = it.r1 - it.r0 > kItemRows;             // read from global memory, in chunks
@@ -410,11 +426,24 @@ __device__ __forceinline__ void cmp_item(const Pool& P, const Table& T, const Gr
         ts.F[i] = (!ever && now - tinfo_at(i).ac > c.waiting) ? 4u : 0u;
     }
     __syncwarp();
-    uint32_t lt[kR], fr[kR], pend_m = 0;
+#ifdef JIT_TIMELINE
+    auto gtc = []() { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; };
+    unsigned long long* tlc = reinterpret_cast<unsigned long long*>(S.sk) + 16ull * (blockIdx.x * kScoreWarps + (threadIdx.x >> 5)) + 8;
+    const unsigned long long c0 = gtc();
+#endif
+    uint32_t lt[kR], fr[kR], pend_m = 0, accT = 0;
+    unsigned long long accG = 0;                            // task `lane`'s sums (kItemTasks <= 32)
     for (uint32_t base = it.r0; base < it.r1; base += kItemRows)   // warp-uniform trip count
         cmp_phase_a(P, T, sg, c, now, sc, it, base, ts, row_at, task_at,
-                    [&](uint32_t r, const HotRow& x) { if (!big) sl->rows[r - it.r0] = x; }, lt, fr, pend_m, A);
+                    [&](uint32_t r, const HotRow& x) { if (!big) sl->rows[r - it.r0] = x; }, lt, fr, pend_m,
+                    accT, accG, A);
+#ifndef JIT_SEGSCAN
+    if (lane < ntl) { ts.T[lane] = accT; ts.G[lane] = accG; }
+#endif
     __syncwarp();
+#ifdef JIT_TIMELINE
+    const unsigned long long c1 = gtc();
+#endif
     // ---- per task: G_task and fl(t_gen + eps) (a4)
     for (uint32_t i = lane; i < ntl; i += 32) {
         uint64_t Gt = 0;
@@ -429,9 +458,12 @@ __device__ __forceinline__ void cmp_item(const Pool& P, const Table& T, const Gr
             const uint64_t Bi = t_gen + (uint64_t)c.eps;
             if (Bi < kTwo53 && Bi >= t_gen && t_gen / (uint64_t)v == Tsum) Bd = __ull2double_rn(Bi);
         }
-        ts.G[i] = Gt; ts.B[i] = Bd;
+        ts.G[i] = Gt; ts.B[i] = Bd; ts.Bf[i] = Bd < 0.0 ? 1.0f : __double2float_rn(Bd);
     }
     __syncwarp();
+#ifdef JIT_TIMELINE
+    const unsigned long long c2 = gtc();
+#endif
     // ---- phase B: the key of every pending call (a5 over the task aggregate); a one-chunk item
     // keeps phase A's per-call values in registers, a big one recomputes them chunk by chunk
     for (uint32_t base = it.r0; base < it.r1; base += kItemRows) {   // warp-uniform trip count
@@ -447,7 +479,8 @@ __device__ __forceinline__ void cmp_item(const Pool& P, const Table& T, const Gr
                 fr[k] = fastdiv(min(sc - x.since, 0xFFFFu), c.frame, c.F_m, c.F_l);
             }
         }
-        double Ak[kR], Bk[kR];
+        uint32_t Gk32[kR];
+        double Bk[kR];
         uint32_t div_m = 0;
 #pragma unroll
         for (uint32_t k = 0; k < kR; ++k) {
@@ -457,9 +490,11 @@ __device__ __forceinline__ void cmp_item(const Pool& P, const Table& T, const Gr
             if (pend && Bd < 0.0) A.err = 1;
             const uint64_t Gp = ts.G[j] + (uint64_t)c.delta * fr[k];
             if (pend && Gp >= kTwo53 / 1000000000ull) A.err = 1;
-            Ak[k] = __dmul_rn(__uint2double_rn((uint32_t)Gp), 1e9);
+            Gk32[k] = (uint32_t)Gp;
             Bk[k] = Bd < 0.0 ? 1.0 : Bd;
-            div_m |= (uint32_t)(pend && (kMat || !(Ak[k] < __dmul_rn(t_lo, Bk[k])))) << k;
+            // the fp32 pre-test with B_f = fl(B) (relative error 2^-24, within below_t's margin)
+            const bool below = __fmul_rn(__uint2float_rn((uint32_t)Gp), 1e9f) < __fmul_rn(t_lo_f, ts.Bf[j]);
+            div_m |= (uint32_t)(pend && (kMat || !below)) << k;
             if (kDebug && base + 32 * k + lane < it.r1) {
                 const uint32_t r = base + 32 * k + lane;
                 const HotRow x = row_at(r);
@@ -479,7 +514,8 @@ __device__ __forceinline__ void cmp_item(const Pool& P, const Table& T, const Gr
         if (__any_sync(0xffffffffu, div_m)) {
 #pragma unroll
             for (uint32_t k = 0; k < kR; ++k)
-                if ((div_m >> k) & 1u) img[k] = (uint64_t)__double_as_longlong(div_rn_int(Ak[k], Bk[k]));
+                if ((div_m >> k) & 1u)
+                    img[k] = (uint64_t)__double_as_longlong(div_rn_int(__dmul_rn(__uint2double_rn(Gk32[k]), 1e9), Bk[k]));
         }
         A.pend += __popc(pend_m);
         uint32_t mem_m = 0;
@@ -498,6 +534,9 @@ __device__ __forceinline__ void cmp_item(const Pool& P, const Table& T, const Gr
         spec_rows(S, P, c, mem_m, img, base, [&](uint32_t, uint32_t r) { return row_at(r); });
     }
     __syncwarp();
+#ifdef JIT_TIMELINE
+    if (lane == 0) { tlc[0] += c1 - c0; tlc[1] += c2 - c1; tlc[2] += gtc() - c2; tlc[3] += 1; }
+#endif
 }
 
 // per-CTA reduction of the warps' partials, one set of global atomics per CTA
@@ -551,7 +590,8 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
     // diagnostic builds: %globaltimer per warp (start, prologue done, items done, end) -> S.sk
     auto gt = []() { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; };
     const unsigned long long tl0 = gt();
-    unsigned long long* tl = reinterpret_cast<unsigned long long*>(S.sk) + 8ull * (blockIdx.x * kScoreWarps + warp);
+    unsigned long long* tl = reinterpret_cast<unsigned long long*>(S.sk) + 16ull * (blockIdx.x * kScoreWarps + warp);
+    if (lane == 0) for (int z = 8; z < 16; ++z) tl[z] = 0;
 #endif
     const uint32_t W = gridDim.x * kScoreWarps;
     const uint32_t i0 = blockIdx.x * kScoreWarps + warp;
@@ -602,9 +642,11 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
     if (blockIdx.x == 0 && threadIdx.x == 0 && mode == 0) { ctrl->now = now; ctrl->v = v; }
     const uint64_t t_img = mode == 0 ? ps.t_guess : kNone;
     const uint32_t sc = ps.steps;
-    // t_lo = t (1 - 2^-20); no threshold (kNone): nothing can join, no key is needed
-    const double t_lo = t_img == kNone ? __longlong_as_double(0x7FF0000000000000ll)
-                                       : __dmul_rn(__longlong_as_double((long long)t_img), 1.0 - 9.5367431640625e-07);
+    // t_lo_f = t (1 - 2^-16) rounded toward zero (below_t); no threshold (kNone): nothing can
+    // join, no key is needed
+    const float t_lo_f = t_img == kNone ? __int_as_float(0x7F800000)
+                                        : __double2float_rz(__dmul_rn(__longlong_as_double((long long)t_img),
+                                                                      1.0 - 1.52587890625e-05));
     __syncthreads();
     pdl_launch_dependents();                               // k_spec may launch now (it waits for us)
 #ifdef JIT_TIMELINE
@@ -633,13 +675,13 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
 #ifdef JIT_SKIP_STD
         if (it.t1 == it.t0) { if (lane == 0 && ws->slot[s].rows[0].gen == 0xFFFFFFFFu) A.err = 1; } else
 #else
-        if (it.t1 == it.t0) std_item<kMat, kDebug, kAppB>(P, T, sg, c, S, now, v_d, v, sc, t_img, t_lo, it, &ws->slot[s], A);
+        if (it.t1 == it.t0) std_item<kMat, kDebug, kAppB>(P, T, sg, c, S, now, v_d, v, sc, t_img, t_lo_f, it, &ws->slot[s], A);
         else
 #endif
 #ifdef JIT_SKIP_CMP
         { if (lane == 0 && ws->slot[s].rows[0].gen == 0xFFFFFFFFu) A.err = 1; }
 #else
-        cmp_item<kMat, kDebug, kAppB>(P, T, sg, c, S, now, v, sc, t_img, t_lo, it, &ws->slot[s], ws->ts, A);
+        cmp_item<kMat, kDebug, kAppB>(P, T, sg, c, S, now, v, sc, t_img, t_lo_f, it, &ws->slot[s], ws->ts, A);
 #endif
         __syncwarp();                                      // every lane is done with the slot
 #ifdef JIT_TIMELINE

@@ -20,8 +20,10 @@ for i in range(6):
         s.step(d["now_ns"], d["v_token_ns"])
     hs.append(s)
 for rep in range(3):
+    for h in hs:
+        h.debug_scratch(1)
     ms = Scheduler.time_scoring(hs, d["now_ns"], d["v_token_ns"], 6)
-    t = hs[-1].debug_scratch(8 * 148 * 64).reshape(-1, 8).astype(np.int64)
+    t = hs[-1].debug_scratch(16 * 148 * 64).reshape(-1, 16).astype(np.int64)
     t = t[t[:, 0] > 0]
     t0 = t[:, 0].min()
     st, pro, items, wait, epi, end = t[:, 0] - t0, t[:, 1] - t[:, 0], t[:, 2] - t[:, 1], t[:, 4], t[:, 3] - t[:, 2], t[:, 3] - t0
@@ -31,5 +33,8 @@ for rep in range(3):
         print(f"  {name:10s} ns  {q(a)}")
     ts_, ns_ = t[:, 6] & ((1 << 48) - 1), t[:, 6] >> 48
     tc_, nc_ = t[:, 7] & ((1 << 48) - 1), t[:, 7] >> 48
+    nc = t[:, 11].sum()
+    if nc:
+        print(f"  cmp item phases ns: A {t[:, 8].sum() / nc:.0f}  per-task {t[:, 9].sum() / nc:.0f}  B {t[:, 10].sum() / nc:.0f}")
     print(f"  per std item ns {ts_.sum() / max(ns_.sum(), 1):.0f} ({ns_.sum()} items); per cmp item ns "
           f"{tc_.sum() / max(nc_.sum(), 1):.0f} ({nc_.sum()} items)")
