@@ -128,16 +128,37 @@ typedef struct jit_pool {
     const uint64_t* goodput_done;     /* goodput of the task's finished calls */
 } jit_pool;
 
-/* Per-step input.  Progress updates (optional) are applied before scoring: row indices into
- * the loaded pool and their new generated / prefilled / state values (host arrays). */
+/* Per-step input: the step's clock and v_token, and what changed since the previous step, applied
+ * in this order before the step's pass (the API of P:544: requests arrive with their SLO
+ * parameters; the engine reports generation progress; compound tasks advance stage by stage):
+ *  - arrivals (optional): new requests appended to the resident pool, in the jit_pool layout of
+ *    jit_sched_load -- standalone rows first, then whole new compound tasks whose call_off is
+ *    relative to the arrivals' own rows (call_off[0] = n_single, call_off[n_tasks] = n) and whose
+ *    task fields index the arrivals' own tasks (0 .. n_tasks-1).  The library appends them after the
+ *    current rows / tasks (a new task gets the index previous n_tasks + its own).  Ids must be new.
+ *    Capacity is fixed at init: JIT_ECAPACITY when rows or tasks would exceed it (reload to compact).
+ *  - task updates (optional): per updated task (index into the resident tasks) its new current
+ *    stage, the goodput of its finished calls, and optionally an absolute stage sub-deadline
+ *    a_c + D_s (tu_stage_deadline_ns[i] < 0 or NULL: derived from the pattern).  The
+ *    calls of a newly released stage become schedulable through progress (state Queued).
+ *  - progress (optional): per request its tokens generated, prompt tokens prefilled and state;
+ *    keyed by request id (progress_by_id = 1) or by pool row (0).  Done and Dropped are final;
+ *    generated < 2^24 and prefilled <= L_i.  A violation fails the step (JIT_EINVAL).
+ * Every array is a host array of the stated count. */
 typedef struct jit_step_in {
     int64_t now_ns;
-    int64_t v_token_ns;            /* average per-token generation time v_token */
-    uint32_t n_progress, reserved;
-    const uint32_t* prog_row;
+    int64_t v_token_ns;            /* average per-token generation time v_token, < 2^36 ns */
+    uint32_t n_progress, progress_by_id;
+    const uint32_t* prog_key;      /* request ids (progress_by_id = 1) or pool rows */
     const uint32_t* prog_generated;
     const uint32_t* prog_prefilled;
     const uint32_t* prog_state;
+    const struct jit_pool* arrivals;   /* NULL: none */
+    uint32_t n_task_updates, reserved;
+    const uint32_t* tu_task;
+    const uint32_t* tu_cur_stage;
+    const uint64_t* tu_goodput_done;
+    const int64_t* tu_stage_deadline_ns;  /* NULL, or per update: absolute a_c + D_s (< 0: from the pattern) */
 } jit_step_in;
 
 /* Selected batch (BestGroup, Alg. 1), in window order (len asc, id asc; A20).

@@ -61,7 +61,7 @@ class _Pool(C.Structure):
 class _Tasks(C.Structure):
     _fields_ = [("n", C.c_uint32), ("_pad", C.c_uint32)] + \
                [(k, C.c_void_p) for k in ("call_off", "arrival_ns", "deadline_ns", "cur_stage", "n_stages",
-                                          "pattern_ms", "goodput_done")]
+                                          "pattern_ms", "goodput_done", "stage_deadline_ns")]
 
 
 class _Result(C.Structure):
@@ -187,6 +187,8 @@ def step(cfg, groups, table, now_ns: int, v_token_ns: int, pool, tasks=None, row
             "n_stages": _arr(tasks["n_stages"], np.uint32), "pattern_ms": _arr(tasks["pattern_ms"], np.uint32),
             "goodput_done": _arr(tasks["goodput_done"], np.uint64),
         }
+        if tasks.get("stage_deadline_ns") is not None:
+            tcols["stage_deadline_ns"] = _arr(tasks["stage_deadline_ns"], np.int64)
         keep.append(tcols)
         tp = _Tasks()
         tp.n = len(tcols["arrival_ns"])

@@ -80,6 +80,8 @@ typedef struct {
     const uint32_t* n_stages;
     const uint32_t* pattern_ms;   /* n * MAX_STAGES matched-pattern stage times */
     const uint64_t* goodput_done;
+    const int64_t* stage_deadline_ns;   /* NULL, or per task: the stage sub-deadline a_c + D_s given by the
+                                           caller (SURVEY 8(b) task updates); < 0: from the pattern */
 } og_tasks;
 
 typedef struct {
@@ -236,6 +238,7 @@ typedef struct {
     const uint32_t* call_begin; const uint32_t* call_end;   /* current-stage rows */
     const int64_t* arrival_ns; const int64_t* deadline_ns;  /* a_c, D */
     const uint64_t* t_le_s; const uint64_t* t_total;        /* phi(s) = t_le_s / t_total */
+    const int64_t* stage_deadline_ns;                        /* NULL or per task (< 0: from phi) */
     const uint64_t* goodput_done;
     const uint8_t* ever;                                     /* 1: some call of the task was scheduled */
     uint8_t* dropped;                                        /* out (may be NULL): 1 if dropped now */
@@ -355,6 +358,7 @@ static int gmax_step(const og_config* cfg, const og_group* G, uint32_t n_groups,
             if (TV->t_total[t] == 0) { rc = OG_EINVAL; break; }
             int64_t Ds = (int64_t)((u128)(uint64_t)TV->deadline_ns[t] * TV->t_le_s[t] / TV->t_total[t]);
             int64_t t_rem = TV->arrival_ns[t] + Ds - now;                  /* advisory */
+            if (TV->stage_deadline_ns && TV->stage_deadline_ns[t] >= 0) t_rem = TV->stage_deadline_ns[t] - now;
             uint64_t t_gen = Tsum * (uint64_t)v_token;
             if (cfg->appb_filter && t_gen > (uint64_t)(t_rem > 0 ? t_rem : 0)) Gtask = 0;
             for (uint32_t r = TV->call_begin[t]; r < TV->call_end[t]; ++r) {
@@ -510,7 +514,7 @@ int og_step(const og_config* cfg, const og_group* groups, uint32_t n_groups,
         tv.n = nt; tv.call_begin = cb; tv.call_end = ce; tv.arrival_ns = tasks->arrival_ns;
         tv.deadline_ns = tasks->deadline_ns; tv.t_le_s = tle; tv.t_total = tt;
         tv.goodput_done = tasks->goodput_done;
-        tv.ever = tever; tv.dropped = NULL;
+        tv.ever = tever; tv.dropped = NULL; tv.stage_deadline_ns = tasks->stage_deadline_ns;
         tvp = &tv;
     }
     uint32_t* sel = (uint32_t*)malloc(sizeof(uint32_t) * (n ? n : 1));
@@ -695,7 +699,7 @@ int og_replay(const og_config* cfg, const og_group* groups_in, uint32_t n_groups
         if (steps >= rc->n_steps) break;
 
         int64_t v = ring_n ? ring_sum / (int64_t)ring_n : rc->v_token0_ns;
-        task_view tv = { nt, cb, ce, ta, tD, tle, ttot, gdone, tever, tdrop };
+        task_view tv = { nt, cb, ce, ta, tD, tle, ttot, NULL, gdone, tever, tdrop };
         og_result res;
         int st = gmax_step(cfg, G, n_groups, T, now, v, n, id, arr, tr->input_len, gen, pre, meta, aux,
                            tr->task, tr->override_R, &tv, &res, sel, selc, NULL);

@@ -31,12 +31,14 @@ struct jit_sched {
     Item* d_items = nullptr;          // k_score work items (S.items), capacity item_cap
     uint32_t* d_n_items = nullptr;    // their count (S.n_items)
     uint32_t item_cap = 0;
-    unsigned char* d_load = nullptr;  // load / delta staging (32 B per row of capacity)
+    unsigned char* d_load = nullptr;  // load / per-step delta staging (48 B per row + 72 B per task of capacity)
     Ctrl* d_ctrl = nullptr;
     Ctrl* h_ctrl = nullptr;           // pinned
     uint32_t* h_batch = nullptr;      // pinned: the fast path writes the batch here (ids | tokens | rows)
-    uint32_t* h_prog = nullptr;       // pinned staging of progress rows (4 x prog_cap)
-    uint64_t prog_cap = 0;
+    unsigned char* h_pin = nullptr;   // pinned staging of the per-step deltas (one H2D copy)
+    uint64_t pin_cap = 0, load_bytes = 0, delta_h2d_bytes = 0;
+    std::vector<unsigned char> h_delta;
+    uint32_t n_items_host = 0;
     cudaStream_t stream = nullptr;    // caller's stream
     cudaStream_t cap = nullptr;       // private capture stream
     cudaGraph_t graph = nullptr;
@@ -119,6 +121,11 @@ static void carve(Carve& cv, const jit_config* cfg, const jit_len_table* tab, Po
     P.cur_stage = cv.take<uint32_t>(NT); P.n_stages = cv.take<uint32_t>(NT);
     P.pattern = cv.take<uint32_t>(NT * kMaxStages); P.gdone = cv.take<uint64_t>(NT);
     P.tinfo = cv.take<TaskInfo>(NT); P.tever = cv.take<uint32_t>(NT + 4);   // + bulk-copy padding
+    P.crng = cv.take<uint2>(NT + 2);
+    uint64_t mc = 1024;
+    while (mc < 2 * N) mc <<= 1;
+    P.idmap = cv.take<unsigned long long>(mc);
+    P.map_mask = (uint32_t)(mc - 1);
     T.edges = cv.take<uint32_t>(tab->n_bins);
     T.cum = cv.take<uint32_t>((uint64_t)tab->n_rows * tab->n_bins);
     groups = cv.take<Group>(256);
@@ -143,7 +150,25 @@ static void carve(Carve& cv, const jit_config* cfg, const jit_len_table* tab, Po
     n_items = cv.take<uint32_t>(1);
     S.items = items; S.n_items = n_items;
     ctrl = cv.take<Ctrl>(1);
-    load = cv.take<unsigned char>(32 * N);
+    // load / per-step delta staging: 48 B per row (the SoA fields of jit_pool) + 72 B per task
+    load = cv.take<unsigned char>(48 * N + 72 * NT + 256);
+}
+// staging layout of a jit_pool's arrays (rows of capacity N, tasks of capacity NT)
+struct Stage {
+    int64_t* arr; uint32_t *len_in, *gen, *pre, *meta, *aux, *id, *task, *ovr;
+    uint32_t* call_off; int64_t *t_arr, *t_dl; uint32_t *cur_stage, *n_stages, *pattern; uint64_t* gdone;
+};
+static Stage stage_layout(unsigned char* base, uint64_t N, uint64_t NT) {
+    Stage st;
+    st.arr = reinterpret_cast<int64_t*>(base);
+    uint32_t* u = reinterpret_cast<uint32_t*>(base + 8 * N);
+    st.len_in = u; st.gen = u + N; st.pre = u + 2 * N; st.meta = u + 3 * N; st.aux = u + 4 * N; st.id = u + 5 * N;
+    st.task = u + 6 * N; st.ovr = u + 7 * N;
+    unsigned char* t = base + 40 * N;
+    st.t_arr = reinterpret_cast<int64_t*>(t); st.t_dl = st.t_arr + NT; st.gdone = reinterpret_cast<uint64_t*>(st.t_dl + NT);
+    uint32_t* tu = reinterpret_cast<uint32_t*>(st.gdone + NT);
+    st.cur_stage = tu; st.n_stages = tu + NT; st.call_off = tu + 2 * NT; st.pattern = tu + 3 * NT + 8;
+    return st;
 }
 
 static int check_config(jit_sched* h, const jit_config* c, const jit_len_table* t) {
@@ -216,6 +241,7 @@ extern "C" int jit_sched_init(const jit_config* cfg, const jit_slo_group* groups
     cv.base = reinterpret_cast<unsigned char*>(((uintptr_t)dev_workspace + 255) & ~(uintptr_t)255);
     carve(cv, cfg, table, h->P, h->S, h->T, h->d_groups, h->d_ctrl, h->d_items, h->d_n_items, h->d_load);
     h->item_cap = item_capacity(((uint64_t)cfg->capacity + 63) & ~63ull, (uint64_t)cfg->task_capacity + 1);
+    h->load_bytes = 48 * (((uint64_t)cfg->capacity + 63) & ~63ull) + 72 * ((uint64_t)cfg->task_capacity + 1);
     h->S.item_cap = h->item_cap;
     h->T.n_rows = table->n_rows; h->T.n_bins = table->n_bins; h->T.l_max = table->l_max;
     h->T.unit = 1;
@@ -262,6 +288,22 @@ extern "C" int jit_sched_init(const jit_config* cfg, const jit_slo_group* groups
 // ------------------------------------------------------------------------------------------
 // load
 // ------------------------------------------------------------------------------------------
+// compound work items: whole tasks [t0, t0 + nt) (call rows [r0 + off[t], r0 + off[t + 1]) with
+// off relative) packed greedily into items of at most kItemRows rows and kItemTasks tasks; a task
+// of more calls gets an item of its own (read in chunks)
+static void add_task_items(std::vector<Item>& items, const uint32_t* off, uint32_t r0, uint32_t t0, uint32_t nt) {
+    Item cur{r0 + off[0], r0 + off[0], t0, t0};
+    for (uint32_t t = 0; t < nt; ++t) {
+        if (t0 + t > cur.t0 && (r0 + off[t + 1] - cur.r0 > kItemRows || t0 + t - cur.t0 >= kItemTasks)) {
+            cur.r1 = r0 + off[t]; cur.t1 = t0 + t;
+            items.push_back(cur);
+            cur.r0 = r0 + off[t]; cur.t0 = t0 + t;
+        }
+    }
+    cur.r1 = r0 + off[nt]; cur.t1 = t0 + nt;
+    items.push_back(cur);
+}
+
 extern "C" int jit_sched_load(jit_sched* h, const jit_pool* p) {
     if (!h || !p) return JIT_EINVAL;
     if (p->n > h->cfg.capacity || p->n_tasks > h->cfg.task_capacity)
@@ -312,16 +354,19 @@ extern "C" int jit_sched_load(jit_sched* h, const jit_pool* p) {
     k_begin<<<4, 1024, 0, h->stream>>>(h->d_ctrl, h->S.hcnt, h->S.hcost, 0, 1, h->S.spec_cnt);
     CK(cudaMemsetAsync(h->S.gpart, 0, sizeof(BlockPart), h->stream));
     const uint32_t vb = (uint32_t)std::min<uint64_t>((n + 255) / 256 + 1, (uint64_t)h->n_sm * 8);
-    k_validate<<<vb, 256, 0, h->stream>>>(P, h->d_groups, h->n_groups, h->T.n_rows, h->T.l_max, h->d_ctrl, 0u, 0u);
+    if (nt) k_crng_from_off<<<(uint32_t)std::min<uint64_t>((nt + 255) / 256, (uint64_t)h->n_sm * 8), 256, 0, h->stream>>>(P);
+    k_validate<<<vb, 256, 0, h->stream>>>(P, h->d_groups, h->n_groups, h->T.n_rows, h->T.l_max, &h->d_ctrl->error, 0u,
+                                          P.n_single, 0u);
     if (nt) k_task_prep<<<(uint32_t)std::min<uint64_t>((nt + 255) / 256, (uint64_t)h->n_sm * 8), 256, 0, h->stream>>>(P, 0u);
+    // request id -> row map (the progress of a step is keyed by id)
+    CK(cudaMemsetAsync(P.idmap, 0xFF, 8ull * (P.map_mask + 1ull), h->stream));
+    if (n) k_map_insert<<<vb, 256, 0, h->stream>>>(P, 0u, (uint32_t)n, &h->d_ctrl->error);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(h->h_ctrl, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     if (h->h_ctrl->error) { h->loaded = false; return set_err(h, JIT_EINVAL, "invalid pool (layout / ranges / groups)"); }
     // work items of k_score: the standalone rows in chunks of kItemRows (their descriptors are
-    // arithmetic in the kernel), then the compound tasks (whole tasks packed greedily into items of
-    // at most kItemRows rows and kItemTasks tasks; a task of more calls gets an item of its own,
-    // read in chunks)
+    // arithmetic in the kernel), then the compound tasks
     h->h_items.clear();
     for (uint32_t r0 = 0; r0 < P.n_single; r0 += kItemRows)
         h->h_items.push_back(Item{r0, std::min<uint32_t>(r0 + kItemRows, P.n_single), 0u, 0u});
@@ -333,22 +378,14 @@ extern "C" int jit_sched_load(jit_sched* h, const jit_pool* p) {
             CK(cudaMemcpy(h->h_off.data(), p->call_off, 4 * (nt + 1), cudaMemcpyDeviceToHost));
             off = h->h_off.data();
         }
-        Item cur{off[0], off[0], 0, 0};
-        for (uint32_t t = 0; t < nt; ++t) {
-            if (t > cur.t0 && (off[t + 1] - cur.r0 > kItemRows || t - cur.t0 >= kItemTasks)) {
-                cur.r1 = off[t]; cur.t1 = t;
-                h->h_items.push_back(cur);
-                cur.r0 = off[t]; cur.t0 = t;
-            }
-        }
-        cur.r1 = off[nt]; cur.t1 = (uint32_t)nt;
-        h->h_items.push_back(cur);
+        add_task_items(h->h_items, off, 0u, 0u, (uint32_t)nt);
     }
     if (h->h_items.size() > h->item_cap) return set_err(h, JIT_ECAPACITY, "too many work items");
     const uint32_t n_items = (uint32_t)h->h_items.size();
+    h->n_items_host = n_items;
     if (n_items)
         CK(cudaMemcpyAsync(h->d_items, h->h_items.data(), sizeof(Item) * n_items, cudaMemcpyHostToDevice, h->stream));
-    CK(cudaMemcpyAsync(h->d_n_items, &n_items, 4, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->d_n_items, &h->n_items_host, 4, cudaMemcpyHostToDevice, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     // persistent grid: every CTA that fits on the GPU (warps stride over the items), at most one
     // warp per item
@@ -580,34 +617,140 @@ static int finish_step(jit_sched* h, jit_batch* out) {
     return rc;
 }
 
+// ------------------------------------------------------------------------------------------
+// per-step deltas (arrivals, task updates, progress): packed into one pinned buffer, one H2D copy
+// into the device staging area, then applied by kernels on the library stream before the step
+// ------------------------------------------------------------------------------------------
+struct HostPack {
+    std::vector<unsigned char>* buf;
+    uint64_t off = 0;
+    template <typename T>
+    uint64_t put(const T* src, uint64_t count) {          // returns the 16-B aligned offset
+        off = (off + 15) & ~15ull;
+        const uint64_t at = off;
+        if (buf->size() < off + sizeof(T) * count) buf->resize(off + sizeof(T) * count);
+        if (count) memcpy(buf->data() + at, src, sizeof(T) * count);
+        off += sizeof(T) * count;
+        return at;
+    }
+};
+
+static int apply_deltas(jit_sched* h, const jit_step_in* in) {
+    const jit_pool* a = in->arrivals;
+    const uint32_t na = a ? a->n : 0u, nat = a ? a->n_tasks : 0u, ntu = in->n_task_updates, m = in->n_progress;
+    if (!na && !nat && !ntu && !m) return JIT_OK;
+    Pool& P = h->P;
+    if (a) {
+        if (a->on_device) return set_err(h, JIT_EINVAL, "arrivals must be host arrays");
+        if (a->n_single > a->n) return set_err(h, JIT_EINVAL, "arrivals: n_single > n");
+        if ((uint64_t)P.n + na > h->cfg.capacity || (uint64_t)P.n_tasks + nat > h->cfg.task_capacity)
+            return set_err(h, JIT_ECAPACITY, "arrivals exceed the pool capacity (reload to compact)");
+        if (nat) {
+            if (!a->call_off || !a->task_arrival_ns || !a->task_deadline_ns || !a->cur_stage || !a->n_stages ||
+                !a->pattern_ms || !a->goodput_done) return set_err(h, JIT_EINVAL, "arrivals: missing task arrays");
+            if (a->call_off[0] != a->n_single || a->call_off[nat] != na)
+                return set_err(h, JIT_EINVAL, "arrivals: call_off must span the compound rows");
+            for (uint32_t t = 0; t < nat; ++t)
+                if (a->call_off[t] > a->call_off[t + 1]) return set_err(h, JIT_EINVAL, "arrivals: call_off not monotone");
+        } else if (a->n_single != na) {
+            return set_err(h, JIT_EINVAL, "arrivals: compound rows without tasks");
+        }
+    }
+    if (m > h->cfg.capacity) return set_err(h, JIT_ECAPACITY, "too many progress rows");
+    std::vector<unsigned char>& hb = h->h_delta;
+    HostPack pk{&hb};
+    uint64_t o_arr = 0, o_u[8] = {}, o_t[8] = {}, o_tu[4] = {}, o_pg[4] = {};
+    if (na) {
+        o_arr = pk.put(a->arrival_ns, na);
+        const uint32_t* f[8] = {a->input_len, a->generated, a->prefilled, a->meta, a->aux, a->id, a->task, a->override_R};
+        for (int i = 0; i < 8; ++i) o_u[i] = pk.put(f[i], na);
+    }
+    if (nat) {
+        o_t[0] = pk.put(a->call_off, nat + 1); o_t[1] = pk.put(a->task_arrival_ns, nat); o_t[2] = pk.put(a->task_deadline_ns, nat);
+        o_t[3] = pk.put(a->cur_stage, nat); o_t[4] = pk.put(a->n_stages, nat); o_t[5] = pk.put(a->pattern_ms, (uint64_t)nat * kMaxStages);
+        o_t[6] = pk.put(a->goodput_done, nat);
+    }
+    if (ntu) {
+        if (!in->tu_task || !in->tu_cur_stage || !in->tu_goodput_done) return set_err(h, JIT_EINVAL, "task updates: missing arrays");
+        o_tu[0] = pk.put(in->tu_task, ntu); o_tu[1] = pk.put(in->tu_cur_stage, ntu); o_tu[2] = pk.put(in->tu_goodput_done, ntu);
+        if (in->tu_stage_deadline_ns) o_tu[3] = pk.put(in->tu_stage_deadline_ns, ntu);
+    }
+    if (m) {
+        o_pg[0] = pk.put(in->prog_key, m); o_pg[1] = pk.put(in->prog_generated, m);
+        o_pg[2] = pk.put(in->prog_prefilled, m); o_pg[3] = pk.put(in->prog_state, m);
+    }
+    const uint64_t bytes = (pk.off + 15) & ~15ull;
+    if (bytes > h->load_bytes) return set_err(h, JIT_ECAPACITY, "step deltas exceed the staging area");
+    if (bytes > h->pin_cap) {                              // pinned mirror, grown on demand
+        if (h->h_pin) cudaFreeHost(h->h_pin);
+        h->h_pin = nullptr; h->pin_cap = 0;
+        CK(cudaMallocHost(&h->h_pin, std::max<uint64_t>(bytes, 1 << 16)));
+        h->pin_cap = std::max<uint64_t>(bytes, 1 << 16);
+    }
+    memcpy(h->h_pin, hb.data(), pk.off);
+    unsigned char* d = h->d_load;
+    CK(cudaMemcpyAsync(d, h->h_pin, bytes, cudaMemcpyHostToDevice, h->stream));
+    h->delta_h2d_bytes = bytes;
+    cudaStream_t s = h->stream;
+    if (na) {
+        Arrivals A{};
+        A.arr = reinterpret_cast<const int64_t*>(d + o_arr);
+        const uint32_t** fu[8] = {&A.len_in, &A.gen, &A.pre, &A.meta, &A.aux, &A.id, &A.task, &A.ovr};
+        for (int i = 0; i < 8; ++i) *fu[i] = reinterpret_cast<const uint32_t*>(d + o_u[i]);
+        if (nat) {
+            A.call_off = reinterpret_cast<const uint32_t*>(d + o_t[0]);
+            A.t_arr = reinterpret_cast<const int64_t*>(d + o_t[1]); A.t_dl = reinterpret_cast<const int64_t*>(d + o_t[2]);
+            A.cur_stage = reinterpret_cast<const uint32_t*>(d + o_t[3]); A.n_stages = reinterpret_cast<const uint32_t*>(d + o_t[4]);
+            A.pattern = reinterpret_cast<const uint32_t*>(d + o_t[5]); A.gdone = reinterpret_cast<const uint64_t*>(d + o_t[6]);
+        }
+        A.n = na; A.n_single = a->n_single; A.n_tasks = nat; A.n0 = P.n; A.t0 = P.n_tasks;
+        const uint32_t n0 = P.n, t0 = P.n_tasks;
+        const uint32_t g = (uint32_t)std::min<uint64_t>((std::max(na, nat) + 255) / 256 + 1, (uint64_t)h->n_sm * 8);
+        k_append<<<g, 256, 0, s>>>(P, A);
+        P.n = n0 + na; P.n_tasks = t0 + nat;
+        uint32_t* err = &h->S.gpart->err;
+        k_validate<<<g, 256, 0, s>>>(P, h->d_groups, h->n_groups, h->T.n_rows, h->T.l_max, err, n0, n0 + a->n_single, t0);
+        if (nat) k_task_prep<<<g, 256, 0, s>>>(P, t0);
+        k_map_insert<<<g, 256, 0, s>>>(P, n0, P.n, err);
+        CK(cudaGetLastError());
+        // their work items: standalone chunks, then the new tasks (table-driven descriptors)
+        const size_t i0 = h->h_items.size();
+        for (uint32_t r0 = n0; r0 < n0 + a->n_single; r0 += kItemRows)
+            h->h_items.push_back(Item{r0, std::min<uint32_t>(r0 + kItemRows, n0 + a->n_single), 0u, 0u});
+        if (nat) add_task_items(h->h_items, a->call_off, n0, t0, nat);
+        if (h->h_items.size() > h->item_cap) return set_err(h, JIT_ECAPACITY, "too many work items (reload to compact)");
+        const uint32_t n_items = (uint32_t)h->h_items.size();
+        CK(cudaMemcpyAsync(h->d_items + i0, h->h_items.data() + i0, sizeof(Item) * (n_items - i0), cudaMemcpyHostToDevice, s));
+        h->n_items_host = n_items;
+        CK(cudaMemcpyAsync(h->d_n_items, &h->n_items_host, 4, cudaMemcpyHostToDevice, s));
+        h->grid_pass = std::max<uint32_t>(1, std::min<uint32_t>((P.n + kPassThreads - 1) / kPassThreads, (uint32_t)h->n_sm * 4));
+    }
+    if (ntu) {
+        k_task_update<<<(ntu + 255) / 256, 256, 0, s>>>(P, reinterpret_cast<const uint32_t*>(d + o_tu[0]),
+                                                       reinterpret_cast<const uint32_t*>(d + o_tu[1]),
+                                                       reinterpret_cast<const uint64_t*>(d + o_tu[2]),
+                                                       in->tu_stage_deadline_ns ? reinterpret_cast<const int64_t*>(d + o_tu[3]) : nullptr,
+                                                       ntu, h->S);
+        CK(cudaGetLastError());
+    }
+    if (m) {
+        k_progress<<<(m + 255) / 256, 256, 0, s>>>(P, h->S, reinterpret_cast<const uint32_t*>(d + o_pg[0]),
+                                                   reinterpret_cast<const uint32_t*>(d + o_pg[1]),
+                                                   reinterpret_cast<const uint32_t*>(d + o_pg[2]),
+                                                   reinterpret_cast<const uint32_t*>(d + o_pg[3]), m, in->progress_by_id ? 1 : 0);
+        CK(cudaGetLastError());
+    }
+    return JIT_OK;
+}
+
 extern "C" int jit_sched_step(jit_sched* h, const jit_step_in* in, jit_batch* out) {
     if (!h || !in) return JIT_EINVAL;
     if (!h->loaded) return set_err(h, JIT_ESTATE, "step before load");
     if (in->v_token_ns <= 0 || in->v_token_ns >= (1ll << 36)) return set_err(h, JIT_EINVAL, "v_token must be in (0, 2^36) ns");
     if (h->unfinished) return set_err(h, JIT_ESTATE, "a step_async step is unfinished: fetch its batch first");
-    if (in->n_progress) {
-        if (in->n_progress > h->cfg.capacity) return set_err(h, JIT_ECAPACITY, "too many progress rows");
-        const uint64_t m = in->n_progress;
-        // one H2D copy: the four arrays are packed into pinned staging first (grown on demand;
-        // the previous step has completed, so the staging is free)
-        if (m > h->prog_cap) {
-            if (h->h_prog) cudaFreeHost(h->h_prog);
-            h->h_prog = nullptr; h->prog_cap = 0;
-            const uint64_t cap = std::max<uint64_t>(m, 4096);
-            CK(cudaMallocHost(&h->h_prog, 16 * cap));
-            h->prog_cap = cap;
-        }
-        memcpy(h->h_prog, in->prog_row, 4 * m);
-        memcpy(h->h_prog + m, in->prog_generated, 4 * m);
-        memcpy(h->h_prog + 2 * m, in->prog_prefilled, 4 * m);
-        memcpy(h->h_prog + 3 * m, in->prog_state, 4 * m);
-        uint32_t* st = reinterpret_cast<uint32_t*>(h->d_load);
-        CK(cudaMemcpyAsync(st, h->h_prog, 16 * m, cudaMemcpyHostToDevice, h->stream));
-        k_progress<<<(uint32_t)((m + 255) / 256), 256, 0, h->stream>>>(h->P, h->S, st, st + m, st + 2 * m, st + 3 * m,
-                                                                     (uint32_t)m);
-        CK(cudaGetLastError());
-    }
-    int rc = launch_step(h, in->now_ns, in->v_token_ns);
+    int rc = apply_deltas(h, in);
+    if (rc) return rc;
+    rc = launch_step(h, in->now_ns, in->v_token_ns);
     if (rc) return rc;
     return finish_step(h, out);
 }
@@ -762,7 +905,7 @@ extern "C" void jit_sched_destroy(jit_sched* h) {
     if (h->cap) cudaStreamDestroy(h->cap);
     if (h->h_ctrl) cudaFreeHost(h->h_ctrl);
     if (h->h_batch) cudaFreeHost(h->h_batch);
-    if (h->h_prog) cudaFreeHost(h->h_prog);
+    if (h->h_pin) cudaFreeHost(h->h_pin);
     for (auto e : h->ev) if (e) cudaEventDestroy(e);
     for (auto e : h->slots) cudaEventDestroy(e);
     delete h;

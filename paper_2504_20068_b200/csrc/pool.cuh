@@ -85,6 +85,23 @@ struct Pool {
     uint64_t* gdone;
     TaskInfo* tinfo;
     uint32_t* tever;        // per task: 1 once any of its calls was scheduled (admission, A40)
+    uint2* crng;            // per task: its call rows [begin, end) (load: the CSR; arrivals: appended blocks)
+    unsigned long long* idmap;   // request id -> row: open addressing, (id << 32) | row, empty = ~0
+    uint32_t map_mask, pad2;     // capacity - 1 (a power of two >= 2 x rows)
 };
+
+constexpr unsigned long long kMapEmpty = ~0ull;
+__host__ __device__ __forceinline__ uint32_t map_hash(uint32_t id, uint32_t mask) {
+    return (id * 0x9E3779B1u) & mask;
+}
+// the row of request `id`, or 0xFFFFFFFF
+__device__ __forceinline__ uint32_t map_find(const Pool& P, uint32_t id) {
+    for (uint32_t h = map_hash(id, P.map_mask), n = 0; n <= P.map_mask; h = (h + 1) & P.map_mask, ++n) {
+        const unsigned long long e = P.idmap[h];
+        if (e == kMapEmpty) return 0xFFFFFFFFu;
+        if ((uint32_t)(e >> 32) == id) return (uint32_t)e;
+    }
+    return 0xFFFFFFFFu;
+}
 
 }  // namespace jit

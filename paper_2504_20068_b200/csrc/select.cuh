@@ -659,15 +659,15 @@ __global__ void k_pack(HotRow* rows, uint32_t n, const int64_t* arr, const uint3
     }
 }
 
-// progress updates from the engine (keyed by row), applied before the step's pass.  A row
-// leaving the pending set freezes its steps_waited (sc = the handle's counter); the ranges the
-// pass relies on are checked (A: gen < 2^24, prefilled <= L_i, state <= Waiting, no way out of
-// Done / Dropped); a violation fails the step (gpart->err).
-__global__ void k_progress(Pool P, Scratch S, const uint32_t* rows_in, const uint32_t* gen, const uint32_t* pre,
-                           const uint32_t* state, uint32_t n) {
+// progress updates from the engine (keyed by request id or by row), applied before the step's
+// pass.  A row leaving the pending set freezes its steps_waited (the handle's counter); the ranges
+// the pass relies on are checked (generated < 2^24, prefilled <= L_i, state <= Waiting, no way out
+// of Done / Dropped, known id); a violation fails the step (gpart->err).
+__global__ void k_progress(Pool P, Scratch S, const uint32_t* key, const uint32_t* gen, const uint32_t* pre,
+                           const uint32_t* state, uint32_t n, int by_id) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const uint32_t r = rows_in[i];
+    const uint32_t r = by_id ? map_find(P, key[i]) : key[i];
     if (r >= P.n) { atomicOr(&S.gpart->err, 8u); return; }
     HotRow* rp = P.rows + r;
     const uint32_t st = state[i], old_st = m_state(rp->meta);
@@ -684,6 +684,82 @@ __global__ void k_progress(Pool P, Scratch S, const uint32_t* rows_in, const uin
     rp->gen = gen[i];
     rp->pre = pre[i];
     *reinterpret_cast<uint2*>(&rp->meta) = make_uint2(meta, since);
+}
+
+// request id -> row map: insert rows [r0, r1) (a duplicate id fails the load / step)
+__global__ void k_map_insert(Pool P, uint32_t r0, uint32_t r1, uint32_t* err) {
+    for (uint32_t r = r0 + blockIdx.x * blockDim.x + threadIdx.x; r < r1; r += gridDim.x * blockDim.x) {
+        const uint32_t id = P.id[r];
+        const unsigned long long e = ((unsigned long long)id << 32) | r;
+        for (uint32_t h = map_hash(id, P.map_mask), k = 0; k <= P.map_mask; h = (h + 1) & P.map_mask, ++k) {
+            const unsigned long long old = atomicCAS(&P.idmap[h], kMapEmpty, e);
+            if (old == kMapEmpty) break;
+            if ((uint32_t)(old >> 32) == id) { atomicOr(err, 16u); break; }
+        }
+    }
+}
+
+// arrivals: the new rows / tasks (staged SoA, arrival-local task indices and call offsets) appended
+// after rows n0 and tasks t0 of the resident pool
+struct Arrivals {
+    const int64_t* arr; const uint32_t *len_in, *gen, *pre, *meta, *aux, *id, *task, *ovr;
+    const uint32_t* call_off; const int64_t *t_arr, *t_dl; const uint32_t *cur_stage, *n_stages, *pattern;
+    const uint64_t* gdone;
+    uint32_t n, n_single, n_tasks, n0, t0, pad;
+};
+__global__ void k_append(Pool P, Arrivals A) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += stride) {
+        const uint32_t r = A.n0 + i;
+        HotRow q;
+        q.arr = A.arr[i]; q.len_in = A.len_in[i]; q.gen = A.gen[i]; q.pre = A.pre[i];
+        q.lrow = A.aux[i] & 0xFFFFu;
+        q.meta = A.meta[i] & ~(kStamped << 12);
+        q.since = A.aux[i] >> 16;
+        P.rows[r] = q;
+        P.id[r] = A.id[i];
+        P.task[r] = A.task[i] == kNoTask ? kNoTask : A.t0 + A.task[i];
+        P.ovr[r] = A.ovr[i];
+    }
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < A.n_tasks; t += stride) {
+        const uint32_t g = A.t0 + t;
+        P.t_arr[g] = A.t_arr[t]; P.t_dl[g] = A.t_dl[t]; P.cur_stage[g] = A.cur_stage[t]; P.n_stages[g] = A.n_stages[t];
+        for (uint32_t u = 0; u < kMaxStages; ++u) P.pattern[(size_t)g * kMaxStages + u] = A.pattern[(size_t)t * kMaxStages + u];
+        P.gdone[g] = A.gdone[t];
+        P.crng[g] = make_uint2(A.n0 + A.call_off[t], A.n0 + A.call_off[t + 1]);
+    }
+}
+
+// task updates: a new current stage (its sub-deadline from the pattern, or given), the goodput of
+// the finished calls
+__global__ void k_task_update(Pool P, const uint32_t* task, const uint32_t* stage, const uint64_t* gdone,
+                              const int64_t* dls, uint32_t n, Scratch S) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t t = task[i];
+    if (t >= P.n_tasks || stage[i] >= P.n_stages[t]) { atomicOr(&S.gpart->err, 8u); return; }
+    P.cur_stage[t] = stage[i];
+    P.gdone[t] = gdone[i];
+    TaskInfo ti = P.tinfo[t];
+    ti.gdone = gdone[i];
+    if (dls && dls[i] >= 0) {
+        ti.dls = dls[i];
+    } else {
+        uint64_t le = 0, tot = 0;
+        for (uint32_t u = 0; u < kMaxStages; ++u) {
+            const uint64_t ms = u < P.n_stages[t] ? P.pattern[(size_t)t * kMaxStages + u] : 0u;
+            tot += ms; if (u <= stage[i]) le += ms;
+        }
+        const int64_t D = P.t_dl[t];
+        ti.dls = P.t_arr[t] + (tot ? (int64_t)((u128)(uint64_t)D * le / tot) : 0);
+    }
+    P.tinfo[t] = ti;
+}
+
+// load: every task's call rows from the CSR
+__global__ void k_crng_from_off(Pool P) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < P.n_tasks; t += gridDim.x * blockDim.x)
+        P.crng[t] = make_uint2(P.call_off[t], P.call_off[t + 1]);
 }
 
 // every 2^30 steps: keep the stamps of rows that wait for ever within 0xFFFF of the counter, so
@@ -716,17 +792,18 @@ __global__ void k_task_prep(Pool P, uint32_t t_begin) {
         ti.gdone = P.gdone[t];
         P.tinfo[t] = ti;
         uint32_t ever = 0;                // A40: some call of the task in the pool was scheduled
-        for (uint32_t r = P.call_off[t]; r < P.call_off[t + 1] && r < P.n; ++r)
+        for (uint32_t r = P.crng[t].x; r < P.crng[t].y && r < P.n; ++r)
             ever |= (m_flags(P.rows[r].meta) & kEver) ? 1u : 0u;
         P.tever[t] = ever;
     }
 }
 
-// load-time validation of a pool (layout rule of jit_pool, group types, ranges)
+// validation of loaded / appended rows [r_begin, n) and tasks [t_begin, n_tasks): rows
+// [r_begin, std_end) are standalone, the rest compound calls inside their task's rows (crng);
+// group types, ranges.  A load (t_begin == 0) also checks the CSR layout of jit_pool.
 __global__ void k_validate(Pool P, const Group* groups, uint32_t n_groups, uint32_t n_rows_tab, uint32_t l_max,
-                           Ctrl* ctrl, uint32_t r_begin, uint32_t t_begin) {
+                           uint32_t* err, uint32_t r_begin, uint32_t std_end, uint32_t t_begin) {
     const uint32_t stride = gridDim.x * blockDim.x;
-    const uint32_t seg_end = P.n_tasks ? P.call_off[P.n_tasks] : 0u;   // end of the compound CSR rows
     bool bad = false;
     for (uint32_t r = r_begin + blockIdx.x * blockDim.x + threadIdx.x; r < P.n; r += stride) {
         const HotRow q = P.rows[r];
@@ -735,13 +812,13 @@ __global__ void k_validate(Pool P, const Group* groups, uint32_t n_groups, uint3
         const bool comp = (m_flags(meta) & kCompound) != 0;
         if (gi >= n_groups || l_row(q.lrow) >= n_rows_tab || q.len_in == 0 || q.len_in >= (1u << 24) ||
             q.gen >= (1u << 24) || q.pre > q.len_in || (meta >> 16) != 0 || m_state(meta) > kWaiting ||
-            q.since > 0xFFFFu) bad = true;
+            q.since > 0xFFFFu || comp != (r >= std_end)) bad = true;
         else if (!comp) {
-            if (P.task[r] != kNoTask || groups[gi].type == kCMP || (r >= P.n_single && r < seg_end)) bad = true;
+            if (P.task[r] != kNoTask || groups[gi].type == kCMP) bad = true;
         } else {
             const uint32_t t = P.task[r];
-            if (t >= P.n_tasks || groups[gi].type != kCMP || (m_flags(meta) & kOverride)) bad = true;
-            else if (r < P.call_off[t] || r >= P.call_off[t + 1]) bad = true;
+            if (t >= P.n_tasks || t < t_begin || groups[gi].type != kCMP || (m_flags(meta) & kOverride)) bad = true;
+            else if (r < P.crng[t].x || r >= P.crng[t].y) bad = true;
             // a call's goodput w_in L_i + w_out L-hat stays below 2^27 (the pass sums 32 calls in u32)
             else if ((uint64_t)groups[gi].w_in * q.len_in + (uint64_t)groups[gi].w_out * (l_max + 1ull) >= (1ull << 27))
                 bad = true;
@@ -750,18 +827,18 @@ __global__ void k_validate(Pool P, const Group* groups, uint32_t n_groups, uint3
     }
     for (uint32_t t = t_begin + blockIdx.x * blockDim.x + threadIdx.x; t < P.n_tasks; t += stride) {
         const uint32_t S = P.n_stages[t], s = P.cur_stage[t];
-        if (P.call_off[t] > P.call_off[t + 1] || S == 0 || S > kMaxStages || s >= S) bad = true;
+        if (P.crng[t].x > P.crng[t].y || P.crng[t].y > P.n || S == 0 || S > kMaxStages || s >= S) bad = true;
         else {
             uint64_t tot = 0;
             for (uint32_t u = 0; u < S; ++u) tot += P.pattern[t * kMaxStages + u];
             if (tot == 0) bad = true;
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0 && t_begin == 0) {   // a load: standalone rows, then the CSR
+    if (blockIdx.x == 0 && threadIdx.x == 0 && t_begin == 0 && r_begin == 0) {   // a load: the CSR of jit_pool
         if (P.n_tasks && (P.call_off[0] != P.n_single || P.call_off[P.n_tasks] != P.n)) bad = true;
         if (!P.n_tasks && P.n_single != P.n) bad = true;
     }
-    if (bad) atomicOr(&ctrl->error, 2u);
+    if (bad) atomicOr(err, 2u);
 }
 
 #endif  // !JIT_EXACT_TU

@@ -62,8 +62,10 @@ class jit_pool(C.Structure):
 
 class jit_step_in(C.Structure):
     _fields_ = [("now_ns", C.c_int64), ("v_token_ns", C.c_int64), ("n_progress", C.c_uint32),
-                ("reserved", C.c_uint32), ("prog_row", C.c_void_p), ("prog_generated", C.c_void_p),
-                ("prog_prefilled", C.c_void_p), ("prog_state", C.c_void_p)]
+                ("progress_by_id", C.c_uint32), ("prog_key", C.c_void_p), ("prog_generated", C.c_void_p),
+                ("prog_prefilled", C.c_void_p), ("prog_state", C.c_void_p), ("arrivals", C.c_void_p),
+                ("n_task_updates", C.c_uint32), ("reserved", C.c_uint32), ("tu_task", C.c_void_p),
+                ("tu_cur_stage", C.c_void_p), ("tu_goodput_done", C.c_void_p), ("tu_stage_deadline_ns", C.c_void_p)]
 
 
 class jit_batch(C.Structure):
@@ -260,20 +262,44 @@ class Scheduler:
         self.n = p.n
 
     # ------------------------------------------------------------------ step
-    def step(self, now_ns: int, v_token_ns: int, progress=None) -> dict:
+    def step(self, now_ns: int, v_token_ns: int, progress=None, arrivals=None, arrival_tasks=None,
+             task_updates=None) -> dict:
+        """One GMAX step.  progress: dict with "id" (request ids) or "row" (pool rows) and generated,
+        prefilled, state; arrivals (+ arrival_tasks): new requests in the load layout (their task
+        fields / call_off local to the arrivals), appended to the pool; task_updates: dict task,
+        cur_stage, goodput_done (+ optional stage_deadline_ns)."""
         si = jit_step_in()
         si.now_ns = int(now_ns)
         si.v_token_ns = int(v_token_ns)
         keep = []
         if progress is not None:
-            arrs = [_c(progress[k], np.uint32) for k in ("row", "generated", "prefilled", "state")]
+            by_id = "id" in progress
+            arrs = [_c(progress["id" if by_id else "row"], np.uint32)] + \
+                   [_c(progress[k], np.uint32) for k in ("generated", "prefilled", "state")]
             keep += arrs
             si.n_progress = len(arrs[0])
-            si.prog_row, si.prog_generated, si.prog_prefilled, si.prog_state = [_p(a) for a in arrs]
+            si.progress_by_id = 1 if by_id else 0
+            si.prog_key, si.prog_generated, si.prog_prefilled, si.prog_state = [_p(a) for a in arrs]
+        if arrivals is not None:
+            ap, akeep = self.make_pool(arrivals, arrival_tasks)
+            keep += akeep + [ap]
+            si.arrivals = C.cast(C.pointer(ap), C.c_void_p)
+        if task_updates is not None:
+            tu = [_c(task_updates["task"], np.uint32), _c(task_updates["cur_stage"], np.uint32),
+                  _c(task_updates["goodput_done"], np.uint64)]
+            keep += tu
+            si.n_task_updates = len(tu[0])
+            si.tu_task, si.tu_cur_stage, si.tu_goodput_done = [_p(a) for a in tu]
+            if task_updates.get("stage_deadline_ns") is not None:
+                dl = _c(task_updates["stage_deadline_ns"], np.int64)
+                keep.append(dl)
+                si.tu_stage_deadline_ns = _p(dl)
         b = jit_batch()
         b.capacity = self.max_batch
         b.ids, b.tokens, b.rows = _p(self._ids), _p(self._tok), _p(self._rows)
         rc = self._check(self.lib.jit_sched_step(self.h, C.byref(si), C.byref(b)), self.h)
+        if arrivals is not None:
+            self.n += len(arrivals["input_len"])
         return self._batch_dict(rc, b)
 
     def step_async(self, now_ns: int, v_token_ns: int):

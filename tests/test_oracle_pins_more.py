@@ -321,3 +321,28 @@ def test_step_lhat_matches_bruteforce_through_memo():
             assert int(out["lhat"][r]) == exp
             checked += 1
     assert checked > 500
+
+
+# ------------------------------------------------------------------------------------------
+# a stage sub-deadline given by the caller (SURVEY 8(b) task updates) replaces phi(s) D
+# ------------------------------------------------------------------------------------------
+
+def test_explicit_stage_deadline_replaces_pattern():
+    groups = W.make_groups([(W.CMP, 0, 0, 40 * S_, 0)])
+    tab = B.table_from_supports([(30, 30)], 64)
+    a_c, now, D = 0, 7 * S_, 40 * S_
+    p = B.pool([dict(id=0, L_i=5, pre=5, g=2, group=0, state=W.Q_RUNNING, flags=W.F_EVER | W.F_COMPOUND, task=0)])
+    pat = np.zeros((1, 8), np.uint32)
+    pat[0, :2] = [3, 1]                                   # stage 0: phi = 3/4 -> D_s = 30 s
+    base = {"call_off": np.array([0, 1], np.uint32), "arrival_ns": np.array([a_c], np.int64),
+            "deadline_ns": np.array([D], np.int64), "cur_stage": np.array([0], np.uint32),
+            "n_stages": np.array([2], np.uint32), "pattern_ms": pat, "goodput_done": np.zeros(1, np.uint64)}
+    ref = oracle.step(_cfg(), groups, tab, now, 15 * MS, p, base)
+    assert ref["t_rem"][0] == a_c + 30 * S_ - now
+    same = oracle.step(_cfg(), groups, tab, now, 15 * MS, p, dict(base, stage_deadline_ns=np.array([a_c + 30 * S_])))
+    assert same["t_rem"][0] == ref["t_rem"][0] and same["key"][0] == ref["key"][0]
+    neg = oracle.step(_cfg(), groups, tab, now, 15 * MS, p, dict(base, stage_deadline_ns=np.array([-1])))
+    assert neg["t_rem"][0] == ref["t_rem"][0]             # < 0: from the pattern
+    other = oracle.step(_cfg(), groups, tab, now, 15 * MS, p, dict(base, stage_deadline_ns=np.array([12 * S_])))
+    assert other["t_rem"][0] == 12 * S_ - now             # the key does not depend on t_rem (A1)
+    assert other["key"][0] == ref["key"][0]
