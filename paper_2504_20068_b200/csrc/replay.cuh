@@ -112,7 +112,7 @@ struct ReplayArgs {
     const int64_t *t_arr, *t_dl; const uint32_t* t_nst;
     const uint32_t* st_kind; const int64_t* st_exec; const uint32_t *st_pat, *st_cb, *st_ce;
     const Spec* specs;
-    uint32_t n_replays, n_steps, log_steps, max_rows, max_tasks, n_groups, pad0, pad1;
+    uint32_t n_replays, n_steps, log_steps, max_rows, max_tasks, n_groups, state_smem, pad1;
     int64_t v0, c0, c_att, c_lin;
     Table T; const Group* groups; Cfg c;
     unsigned char* state; uint64_t state_stride;
@@ -138,6 +138,30 @@ __host__ __device__ inline uint64_t replay_state_bytes(uint32_t M, uint32_t MT, 
     b += 16 * p2 + 4 * p2 + 8 * p2 + 4 * p2 + 8 * (m + 1) + 16 * (m + 1);
     b += 4 * (uint64_t)(max_batch + 1) + 8 * 1024;
     return b + 64 * 32;                         // alignment slack
+}
+
+// the per-replay state without the global sort scratch (rows, tasks, batch, v_token ring): kept
+// in shared memory when it fits beside the sort buffers (traces of <= kReplaySmemRows rows)
+__host__ __device__ inline uint64_t replay_core_bytes(uint32_t M, uint32_t MT, uint32_t max_batch) {
+    const uint64_t m = M + 64, mt = MT + 1;
+    auto r = [](uint64_t b) { return (b + 63) & ~63ull; };
+    return r(8 * m) + 7 * r(4 * m) + r(8 * m) + 6 * r(4 * mt) + 6 * r(8 * mt) + r(4 * (uint64_t)(max_batch + 1)) +
+           r(8 * 1024);
+}
+__device__ inline RState carve_core(unsigned char* p, uint32_t M, uint32_t MT, uint32_t max_batch) {
+    const uint64_t m = M + 64, mt = MT + 1;
+    RState s{};
+    auto take = [&](uint64_t bytes) { unsigned char* q = p; p += (bytes + 63) & ~63ull; return q; };
+    s.arr = (int64_t*)take(8 * m);
+    s.gen = (uint32_t*)take(4 * m); s.pre = (uint32_t*)take(4 * m); s.lhat = (uint32_t*)take(4 * m);
+    s.meta = (uint32_t*)take(4 * m); s.aux = (uint32_t*)take(4 * m); s.late = (uint32_t*)take(4 * m);
+    s.cost = (uint32_t*)take(4 * m); s.img = (uint64_t*)take(8 * m);
+    s.cur = (uint32_t*)take(4 * mt); s.left = (uint32_t*)take(4 * mt); s.tdone = (uint32_t*)take(4 * mt);
+    s.cb = (uint32_t*)take(4 * mt); s.ce = (uint32_t*)take(4 * mt); s.tever = (uint32_t*)take(4 * mt);
+    s.timer = (int64_t*)take(8 * mt); s.ta = (int64_t*)take(8 * mt); s.tD = (int64_t*)take(8 * mt);
+    s.gdone = (unsigned long long*)take(8 * mt); s.tle = (uint64_t*)take(8 * mt); s.ttot = (uint64_t*)take(8 * mt);
+    s.batch = (uint32_t*)take(4 * (uint64_t)(max_batch + 1)); s.ring = (int64_t*)take(8 * 1024);
+    return s;
 }
 
 __device__ inline RState carve_state(unsigned char* p, uint32_t M, uint32_t MT, uint32_t max_batch) {
@@ -168,12 +192,15 @@ __device__ __forceinline__ uint64_t call_R(const Group& g, uint32_t L_i, uint32_
     return (uint64_t)g.w_in * L_i + (uint64_t)g.w_out * L_o;
 }
 
-// block-wide chunked exclusive scan helpers over an array produced by a functor
+__host__ __device__ inline uint32_t replay_groups_bytes(uint32_t n_groups) {
+    return (uint32_t)(((sizeof(Group) + sizeof(GroupFast)) * n_groups + 63) & ~63ull);
+}
+
 __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
-    Group* sg = reinterpret_cast<Group*>(smem);                                   // 256 groups
-    GroupFast* sgf = reinterpret_cast<GroupFast*>(smem + sizeof(Group) * 256);   // their scoring form
-    unsigned char* sbuf = smem + (sizeof(Group) + sizeof(GroupFast)) * 256;
+    Group* sg = reinterpret_cast<Group*>(smem);                                   // the SLO groups
+    GroupFast* sgf = reinterpret_cast<GroupFast*>(smem + sizeof(Group) * A.n_groups);   // their scoring form
+    unsigned char* sbuf = smem + replay_groups_bytes(A.n_groups);
     // region A (24 cap + 64 B): pending sort (u128 key + u32 row), later reused for the
     // window prefix sums (u64 cost + u128 fixed-point key); region B: Cd sort (u64 + u32)
     u128* sA = reinterpret_cast<u128*>(sbuf);
@@ -198,7 +225,11 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
     const Cfg c = A.c;
     const Table T = A.T;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    RState S = carve_state(A.state + (uint64_t)blockIdx.x * A.state_stride, A.max_rows, A.max_tasks, c.max_batch);
+    // the replay state in shared memory (behind the sort buffers) when it fits, else in this CTA's
+    // global slice
+    RState S = A.state_smem ? carve_core(sbuf + 36 * kReplaySmemRows + 64, A.max_rows, A.max_tasks, c.max_batch)
+                            : carve_state(A.state + (uint64_t)blockIdx.x * A.state_stride, A.max_rows, A.max_tasks,
+                                          c.max_batch);
 
     for (uint32_t rep = blockIdx.x; rep < A.n_replays; rep += gridDim.x) {
         const Spec sp = A.specs[rep];
@@ -635,8 +666,9 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
     }
 }
 
-inline uint32_t replay_smem_bytes() {
-    return (uint32_t)((sizeof(Group) + sizeof(GroupFast)) * 256 + 36 * kReplaySmemRows + 64);
+// dynamic shared memory of k_replay: groups, sort buffers, (the replay state)
+inline uint32_t replay_smem_bytes(uint32_t n_groups, uint64_t core) {
+    return (uint32_t)(replay_groups_bytes(n_groups) + 36 * kReplaySmemRows + 64 + core);
 }
 
 }  // namespace jit
