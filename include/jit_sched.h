@@ -215,17 +215,28 @@ int jit_sched_read_rows(jit_sched* h, double* key, double* rate, int64_t* t_rem,
 int jit_sched_kernel_times(jit_sched* h, int enable, float* ms_out, uint32_t n_out);
 
 /* Measurement: `launches` back-to-back launches of the scoring kernel (k_score, rows (a1)-(a6)),
- * rotating over n_handles loaded handles that share one stream, timed with CUDA events around
- * the sequence; *ms_per_launch = average.  Each launch advances steps_waited like a step whose
- * batch is empty (the pools' state changes); the per-step accumulators are reset afterwards. */
+ * rotating over n_handles loaded handles that share one stream, timed with CUDA events around the
+ * sequence; *ms_per_launch = average.  The pass writes no per-row state in the steady state and the
+ * step counter moves only with a resolved step, so the pools are left as they were (the per-step
+ * accumulators and speculative sets are reset afterwards).  flags & JIT_TIME_FORCE_REFRESH: every
+ * cached length bound is invalidated before each launch (untimed; each launch timed alone), i.e.
+ * the pass with a stale bound on every row (SURVEY 8(d) "forced refresh"). */
+#define JIT_TIME_FORCE_REFRESH 1u
 int jit_sched_time_scoring(jit_sched** hs, uint32_t n_handles, int64_t now_ns, int64_t v_token_ns, uint32_t launches,
-                           float* ms_per_launch);
+                           uint32_t flags, float* ms_per_launch);
 
 /* Device counters of the handle (synchronizes its stream): steps resolved since init (the
  * steps_waited stamps count against this counter), steps resolved by the exact radix path, and
  * chained jit_sched_step_async steps that did nothing because an earlier step of the chain still
  * needed the host (each of those must be re-run; a timed region must see 0). */
 int jit_sched_counters(jit_sched* h, uint32_t* steps, uint32_t* fallbacks, uint32_t* skipped);
+
+/* Tests: set the device step counter that the steps_waited stamps count against (every stamped
+ * row's stamp moves with it, so no count changes) and the host's count of launched steps (the
+ * stamp rebase of pool.cuh runs each time it reaches a multiple of 2^30), so that the counter's
+ * wrap at 2^32 and the rebase are reached in a few steps.  JIT_ESTATE with an unfinished async
+ * step. */
+int jit_sched_debug_set_counter(jit_sched* h, uint32_t steps, uint64_t launched);
 
 /* Diagnostics: copy the first n u64 of the exact path's sort scratch to host memory `out`
  * (JIT_TIMELINE builds of the scoring kernel leave per-warp %globaltimer stamps there). */

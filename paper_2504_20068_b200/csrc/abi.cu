@@ -846,8 +846,14 @@ extern "C" int jit_sched_kernel_times(jit_sched* h, int enable, float* ms_out, u
 // events around the whole sequence: the kernel's average duration with its launch overlapped by
 // the previous kernel (a single launch bracketed by event nodes also counts the node's launch
 // latency).  Each handle's per-step accumulators are reset afterwards (outside the timing).
+// Back-to-back k_score launches rotating over handles (that share one stream), timed with CUDA
+// events around the whole sequence: the kernel's average duration with its launch overlapped by
+// the previous kernel (a single launch bracketed by event nodes also counts the node's launch
+// latency).  flags & JIT_TIME_FORCE_REFRESH: every cached length bound is invalidated before each
+// launch (untimed) and each launch is timed alone (events around it): the pass with a stale bound
+// on every row.  Each handle's per-step accumulators are reset afterwards (outside the timing).
 extern "C" int jit_sched_time_scoring(jit_sched** hs, uint32_t n_handles, int64_t now_ns, int64_t v_token_ns,
-                                      uint32_t launches, float* ms_per_launch) {
+                                      uint32_t launches, uint32_t flags, float* ms_per_launch) {
     if (!hs || !n_handles || !launches || !ms_per_launch) return JIT_EINVAL;
     jit_sched* h = hs[0];
     for (uint32_t i = 0; i < n_handles; ++i) {
@@ -858,12 +864,26 @@ extern "C" int jit_sched_time_scoring(jit_sched** hs, uint32_t n_handles, int64_
     cudaStream_t s = h->stream;
     cudaEvent_t e0 = h->ev[0], e1 = h->ev[1];
     CK(cudaStreamSynchronize(s));
-    CK(cudaEventRecord(e0, s));
-    for (uint32_t k = 0; k < launches; ++k) enqueue_score(hs[k % n_handles], s, now_ns, v_token_ns);
-    CK(cudaEventRecord(e1, s));
-    CK(cudaEventSynchronize(e1));
     float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (flags & JIT_TIME_FORCE_REFRESH) {
+        for (uint32_t k = 0; k < launches; ++k) {
+            jit_sched* hk = hs[k % n_handles];
+            k_invalidate_bounds<<<hk->grid_pass, 256, 0, s>>>(hk->P);
+            CK(cudaEventRecord(e0, s));
+            enqueue_score(hk, s, now_ns, v_token_ns);
+            CK(cudaEventRecord(e1, s));
+            CK(cudaEventSynchronize(e1));
+            float t = 0.f;
+            CK(cudaEventElapsedTime(&t, e0, e1));
+            ms += t;
+        }
+    } else {
+        CK(cudaEventRecord(e0, s));
+        for (uint32_t k = 0; k < launches; ++k) enqueue_score(hs[k % n_handles], s, now_ns, v_token_ns);
+        CK(cudaEventRecord(e1, s));
+        CK(cudaEventSynchronize(e1));
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+    }
     *ms_per_launch = ms / (float)launches;
     for (uint32_t i = 0; i < n_handles; ++i)       // consume the accumulated partials / sets
         CK(exact::spec(hs[i]->P, hs[i]->c, hs[i]->d_ctrl, hs[i]->S, 1, s, false));
@@ -879,6 +899,24 @@ extern "C" int jit_sched_counters(jit_sched* h, uint32_t* steps, uint32_t* fallb
     if (steps) *steps = ps.steps;
     if (fallbacks) *fallbacks = ps.fallbacks;
     if (skipped) *skipped = ps.skipped;
+    return JIT_OK;
+}
+
+// tests: move the device step counter (the steps_waited stamps count against it) and the host's
+// launch count (the stamp rebase runs when it reaches a multiple of 2^30), so that the counter
+// wrap and the rebase are exercised in a few steps
+extern "C" int jit_sched_debug_set_counter(jit_sched* h, uint32_t steps, uint64_t launched) {
+    if (!h) return JIT_EINVAL;
+    if (h->unfinished) return set_err(h, JIT_ESTATE, "fetch the unfinished step first");
+    CK(cudaStreamSynchronize(h->stream));
+    Persist ps;
+    CK(cudaMemcpy(&ps, h->S.persist, sizeof ps, cudaMemcpyDeviceToHost));
+    const uint32_t d = steps - ps.steps;         // keep every stamped row's count: shift its stamp too
+    if (h->P.n) k_shift_stamps<<<h->grid_pass, 256, 0, h->stream>>>(h->P, d);
+    ps.steps = steps;
+    CK(cudaMemcpyAsync(h->S.persist, &ps, sizeof ps, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    h->launched = launched;
     return JIT_OK;
 }
 

@@ -756,6 +756,12 @@ __global__ void k_task_update(Pool P, const uint32_t* task, const uint32_t* stag
     P.tinfo[t] = ti;
 }
 
+// measurement only (jit_sched_time_scoring, JIT_TIME_FORCE_REFRESH): every cached bound stale
+__global__ void k_invalidate_bounds(Pool P) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < P.n; r += gridDim.x * blockDim.x)
+        P.rows[r].meta &= 0xFFFFu;                          // epoch field 0: unset
+}
+
 // load: every task's call rows from the CSR
 __global__ void k_crng_from_off(Pool P) {
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < P.n_tasks; t += gridDim.x * blockDim.x)
@@ -769,6 +775,14 @@ __global__ void k_rebase(Pool P, Scratch S) {
     for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < P.n; r += gridDim.x * blockDim.x) {
         HotRow* rp = P.rows + r;
         if (((rp->meta >> 12) & kStamped) && sc - rp->since > 0xFFFFu) rp->since = sc - 0xFFFFu;
+    }
+}
+
+// tests (jit_sched_debug_set_counter): the counter moves by d, every stamp with it
+__global__ void k_shift_stamps(Pool P, uint32_t d) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < P.n; r += gridDim.x * blockDim.x) {
+        HotRow* rp = P.rows + r;
+        if ((rp->meta >> 12) & kStamped) rp->since += d;
     }
 }
 

@@ -114,7 +114,8 @@ EXPORTS = ("jit_sched_workspace_bytes", "jit_sched_init", "jit_sched_load", "jit
            "jit_replay_workspace_bytes", "jit_sched_replay", "jit_sched_destroy", "jit_sched_last_error",
            "jit_sched_version", "jit_shard_prefix", "jit_shard_merge", "jit_shard_candidates", "jit_shard_finish",
            "jit_sched_phase_times", "jit_shard_spec_bytes", "jit_shard_spec_export", "jit_shard_spec_resolve",
-           "jit_sched_time_scoring", "jit_sched_counters", "jit_sched_debug_scratch")
+           "jit_sched_time_scoring", "jit_sched_counters", "jit_sched_debug_scratch",
+           "jit_sched_debug_set_counter")
 
 
 def load_library(path: str = LIB_PATH):
@@ -189,6 +190,7 @@ class Scheduler:
         self._keep = []
         self.cfg_dict = dict(cfg)
         self.c = make_config(cfg, capacity, task_capacity, device, C.c_void_p(stream.cuda_stream), debug)
+        self.debug = bool(debug)
         self.groups, self.n_groups = make_groups(groups)
         edges = _c(table["edges"], np.uint32)
         cum = _c(table["cum"], np.uint32)
@@ -351,6 +353,10 @@ class Scheduler:
         self._check(self.lib.jit_sched_counters(self.h, C.byref(a), C.byref(b), C.byref(c)), self.h)
         return {"steps": a.value, "fallbacks": b.value, "skipped": c.value}
 
+    def debug_set_counter(self, steps: int, launched: int):
+        """Tests: move the device step counter (stamps move with it) and the launch count."""
+        self._check(self.lib.jit_sched_debug_set_counter(self.h, C.c_uint32(steps), C.c_uint64(launched)), self.h)
+
     def debug_scratch(self, n: int) -> np.ndarray:
         """Diagnostics: the first n u64 of the sort scratch (JIT_TIMELINE stamps)."""
         out = np.zeros(n, np.uint64)
@@ -393,13 +399,14 @@ class Scheduler:
         return self._batch_dict(rc, b)
 
     @staticmethod
-    def time_scoring(handles, now_ns: int, v_token_ns: int, launches: int) -> float:
-        """Average ms of back-to-back k_score launches rotating over `handles` (same stream)."""
+    def time_scoring(handles, now_ns: int, v_token_ns: int, launches: int, force_refresh: bool = False) -> float:
+        """Average ms of back-to-back k_score launches rotating over `handles` (same stream);
+        force_refresh: every cached length bound stale before each launch (each launch timed alone)."""
         lib = load_library()
         arr = (C.c_void_p * len(handles))(*[h.h.value for h in handles])
         ms = C.c_float()
         rc = lib.jit_sched_time_scoring(arr, C.c_uint32(len(handles)), C.c_int64(now_ns), C.c_int64(v_token_ns),
-                                        C.c_uint32(launches), C.byref(ms))
+                                        C.c_uint32(launches), C.c_uint32(1 if force_refresh else 0), C.byref(ms))
         handles[0]._check(rc, handles[0].h)
         return float(ms.value)
 
