@@ -44,7 +44,8 @@ class _Config(C.Structure):
     _fields_ = [(k, C.c_uint32) for k in ("token_budget", "max_batch", "prefill_chunk", "refine_interval",
                                           "frame_steps", "q_num", "q_den", "p_num", "p_den", "delta_starve",
                                           "len_key", "appb_filter")] + \
-               [("eps_ns", C.c_int64), ("waiting_ns", C.c_int64)]
+               [("eps_ns", C.c_int64), ("waiting_ns", C.c_int64)] + \
+               [(k, C.c_uint32) for k in ("preempt", "pmtn_num", "pmtn_den", "_pad2")] + [("io_bw_tps", C.c_uint64)]
 
 
 class _Table(C.Structure):
@@ -66,8 +67,8 @@ class _Tasks(C.Structure):
 
 class _Result(C.Structure):
     _fields_ = [(k, C.c_uint32) for k in ("n_pending", "n_selected", "total_tokens", "n_candidates", "b_star",
-                                          "n_dropped_now", "error", "_pad")] + \
-               [("bp", C.c_double), ("thr", C.c_double)]
+                                          "n_dropped_now", "error", "n_preempted")] + \
+               [("bp", C.c_double), ("thr", C.c_double), ("stall_ns", C.c_int64)]
 
 
 class _RowsOut(C.Structure):
@@ -91,12 +92,12 @@ class _ReplayCfg(C.Structure):
 class _ReplayResult(C.Structure):
     _fields_ = [("token_goodput", C.c_uint64), ("tokens_processed", C.c_uint64), ("sim_end_ns", C.c_int64)] + \
                [(k, C.c_uint32) for k in ("request_goodput", "n_done", "n_dropped", "steps", "n_tasks_done",
-                                          "n_tasks_dropped", "error", "_pad")]
+                                          "n_tasks_dropped", "error", "n_preempted")]
 
 
 STEP_LOG_DTYPE = np.dtype([("now_ns", "<i8"), ("n_selected", "<u4"), ("total_tokens", "<u4"),
                            ("n_candidates", "<u4"), ("b_star", "<u4"), ("bp", "<f8"), ("ids_hash", "<u8"),
-                           ("v_token_ns", "<i8")])
+                           ("v_token_ns", "<i8"), ("n_preempted", "<u4"), ("_pad", "<u4"), ("stall_ns", "<i8")])
 
 
 def _load():
@@ -122,8 +123,9 @@ def _ptr(a):
 
 def _mk_config(cfg):
     c = _Config()
+    gate_defaults = {"preempt": 0, "pmtn_num": 1, "pmtn_den": 10, "_pad2": 0, "io_bw_tps": 10 ** 6}
     for k, _ in _Config._fields_:
-        setattr(c, k, int(cfg[k]))
+        setattr(c, k, int(cfg.get(k, gate_defaults.get(k, 0)) if k in gate_defaults else cfg[k]))
     return c
 
 
@@ -156,11 +158,14 @@ def length_bound(table, row: int, g: int, R: int, q_num: int, q_den: int) -> int
     return int(lib.og_length_bound(C.byref(t), row, g, R, q_num, q_den))
 
 
-def step(cfg, groups, table, now_ns: int, v_token_ns: int, pool, tasks=None, rows_out: bool = True):
+def step(cfg, groups, table, now_ns: int, v_token_ns: int, pool, tasks=None, rows_out: bool = True,
+         frame_open: bool = True):
     """One GMAX step (Alg. 1 Schedule) over a pool snapshot.
 
     ``pool`` is a dict of numpy arrays (id, arrival_ns, input_len, generated, prefilled, meta, aux,
-    task, override_R).  meta/aux are copied and the updated copies are returned.
+    task, override_R).  meta/aux are copied and the updated copies are returned.  With
+    ``cfg["preempt"]`` the preemption gate (NEXT-1, reading A46) filters the proposal;
+    ``frame_open`` says whether this step is a frame boundary (preemption allowed).
     """
     lib = _load()
     keep = []
@@ -207,12 +212,14 @@ def step(cfg, groups, table, now_ns: int, v_token_ns: int, pool, tasks=None, row
         ro = _RowsOut(*[_ptr(out_rows[k]) for k in ("key", "rate", "t_rem", "lhat", "cost", "pending")])
     rc = lib.og_step(C.byref(c), g, C.c_uint32(ng), C.byref(t), C.c_int64(now_ns), C.c_int64(v_token_ns),
                      C.byref(p), C.byref(tp) if tp is not None else None, C.byref(res),
-                     _ptr(ids), _ptr(toks), _ptr(rows), C.byref(ro) if ro is not None else None)
+                     _ptr(ids), _ptr(toks), _ptr(rows), C.byref(ro) if ro is not None else None,
+                     C.c_uint32(1 if frame_open else 0))
     k = res.n_selected
     out = {"status": rc, "n_pending": res.n_pending, "n_selected": k, "total_tokens": res.total_tokens,
            "n_candidates": res.n_candidates, "b_star": res.b_star, "n_dropped_now": res.n_dropped_now,
            "bp": res.bp, "thr": res.thr, "batch_ids": ids[:k].copy(), "batch_tokens": toks[:k].copy(),
-           "batch_rows": rows[:k].copy(), "meta": cols["meta"], "aux": cols["aux"]}
+           "batch_rows": rows[:k].copy(), "meta": cols["meta"], "aux": cols["aux"],
+           "n_preempted": res.n_preempted, "stall_ns": res.stall_ns}
     out.update(out_rows)
     return out
 
@@ -252,7 +259,7 @@ def replay(cfg, groups, table, trace, rcfg, log: bool = False, log_ids: bool = F
     out = {"status": st, "token_goodput": res.token_goodput, "tokens_processed": res.tokens_processed,
            "sim_end_ns": res.sim_end_ns, "request_goodput": res.request_goodput, "n_done": res.n_done,
            "n_dropped": res.n_dropped, "steps": res.steps, "n_tasks_done": res.n_tasks_done,
-           "n_tasks_dropped": res.n_tasks_dropped}
+           "n_tasks_dropped": res.n_tasks_dropped, "n_preempted": res.n_preempted}
     if log:
         out["log"] = L[:res.steps].copy()
     if log_ids:

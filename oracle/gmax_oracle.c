@@ -50,6 +50,9 @@ typedef struct {
     uint32_t q_num, q_den, p_num, p_den, delta_starve;
     uint32_t len_key, appb_filter;
     int64_t eps_ns, waiting_ns;
+    /* NEXT-1 preemption gate (reading A46): 0 = off (the step re-selects every iteration, A30) */
+    uint32_t preempt, pmtn_num, pmtn_den, _pad2;   /* delta_pmtn = pmtn_num / pmtn_den (App. D.2) */
+    uint64_t io_bw_tps;                            /* KV swap bandwidth, tokens per second */
 } og_config;
 
 typedef struct {
@@ -86,8 +89,9 @@ typedef struct {
 
 typedef struct {
     uint32_t n_pending, n_selected, total_tokens, n_candidates, b_star, n_dropped_now;
-    uint32_t error, _pad;
+    uint32_t error, n_preempted;   /* n_preempted: running requests evicted by the gate (A46) */
     double bp, thr;
+    int64_t stall_ns;              /* KV swap stall of the evicted requests (A46) */
 } og_result;
 
 typedef struct {          /* optional per-row outputs (each pointer may be NULL) */
@@ -244,6 +248,91 @@ typedef struct {
     uint8_t* dropped;                                        /* out (may be NULL): 1 if dropped now */
 } task_view;
 
+/* ------------------------------------------------------------------------------------ */
+/* NEXT-1: the preemption gate over GMAX's proposal (reading A46).                       */
+/* §4.2: "performs preemption only when the projected gain from admitting a    */
+/* higher-priority request exceeds [goodput_loss = stall_duration x token_generation_    */
+/* speed]" and "scheduling updates are restricted to discrete time frames (Delta = 50    */
+/* decoding steps)"; App. D.2: A may preempt the running B only if           */
+/* R(A)/R(B) > 1 + delta (delta_pmtn = 0.1); S:313-321 preemption_check.          */
+/*                                                                                        */
+/* Running set P = the pending requests in state Running (with the gate on, Running means */
+/* "in the batch the engine executes": the gate's bookkeeping keeps it so).  Q = GMAX's    */
+/* window (a9).  Walk, in this order:                                                      */
+/*  1. P in (key desc, id asc): a running request keeps its slot while |F| < B_max and its */
+/*     cost fits the budget; one that does not fit is evicted (no gate: it cannot run).    */
+/*  2. I = Q \ P in (key desc, id asc).  A newcomer takes a free slot when one is left and */
+/*     its cost fits.  Otherwise, only at a frame boundary, it is paired with the weakest   */
+/*     running request still kept and not in Q (P walked from its end: key asc, later id   */
+/*     first); the swap happens iff                                                        */
+/*        cost(in) <= budget_left + cost(out),                                             */
+/*        key(in) > key(out) * fl((den + num) / den)                 (App. D.2 ratio),     */
+/*        (key(in) - key(out)) * fl(Delta * v / 1e9) > fl(stall(out) / v),   */
+/*     with stall(out) = floor(kv(out) * 1e9 / io_bw) ns, kv = prefilled + generated tokens */
+/*     (KV size = context length), gen speed 1/v tokens per ns, the gain counted     */
+/*     over one frame of Delta steps.  A failed pair skips the newcomer (the candidate stays).*/
+/* Every floating-point operation is one IEEE round-to-nearest operation in this order.   */
+/* ------------------------------------------------------------------------------------ */
+static void gate(const og_config* cfg, uint32_t n, const uint32_t* id, const uint32_t* input_len,
+                 const uint32_t* generated, const uint32_t* prefilled, const uint32_t* meta,
+                 const double* key, const uint32_t* cost, const uint8_t* pend,
+                 const by_len_t* Q, uint32_t nq, int64_t v_token, uint32_t frame_open,
+                 uint8_t* inF, uint8_t* evict, og_result* res) {
+    (void)input_len;
+    uint8_t* inQ = (uint8_t*)calloc(n ? n : 1, 1);
+    for (uint32_t i = 0; i < nq; ++i) inQ[Q[i].row] = 1;
+    by_key_t* P = (by_key_t*)malloc(sizeof(by_key_t) * (n ? n : 1));
+    by_key_t* I = (by_key_t*)malloc(sizeof(by_key_t) * (nq ? nq : 1));
+    uint32_t np = 0, ni = 0;
+    for (uint32_t r = 0; r < n; ++r)
+        if (pend[r] && m_state(meta[r]) == ST_RUNNING) { P[np].key = key[r]; P[np].id = id[r]; P[np].row = r; ++np; }
+    for (uint32_t i = 0; i < nq; ++i) {
+        uint32_t r = Q[i].row;
+        if (m_state(meta[r]) != ST_RUNNING) { I[ni].key = key[r]; I[ni].id = id[r]; I[ni].row = r; ++ni; }
+    }
+    qsort(P, np, sizeof(by_key_t), cmp_key_desc_id_asc);
+    qsort(I, ni, sizeof(by_key_t), cmp_key_desc_id_asc);
+    uint64_t budget = cfg->token_budget;
+    uint32_t slots = cfg->max_batch;
+    /* 1. running requests continue while they fit */
+    for (uint32_t k = 0; k < np; ++k) {
+        uint32_t r = P[k].row;
+        if (slots >= 1 && cost[r] <= budget) { inF[r] = 1; --slots; budget -= cost[r]; }
+        else evict[r] = 1;
+    }
+    /* 2. newcomers: a free slot, else a gated swap at a frame boundary */
+    double onepd = (double)((uint64_t)cfg->pmtn_den + cfg->pmtn_num) / (double)cfg->pmtn_den;
+    double fs = (double)((uint64_t)cfg->frame_steps * (uint64_t)v_token) / 1e9;
+    uint32_t o = np;                                   /* candidates: P[o-1], P[o-2], ... */
+    for (uint32_t k = 0; k < ni; ++k) {
+        uint32_t r = I[k].row;
+        if (slots >= 1 && cost[r] <= budget) { inF[r] = 1; --slots; budget -= cost[r]; continue; }
+        if (!frame_open) continue;
+        while (o > 0 && !(inF[P[o - 1].row] && !inQ[P[o - 1].row])) --o;
+        if (o == 0) continue;
+        uint32_t q = P[o - 1].row;
+        uint64_t kv = (uint64_t)prefilled[q] + generated[q];
+        int64_t stall = (int64_t)((u128)kv * 1000000000u / cfg->io_bw_tps);
+        double loss = (double)stall / (double)v_token;
+        double gain = (key[r] - key[q]) * fs;
+        if (cost[r] <= budget + cost[q] && key[r] > key[q] * onepd && gain > loss) {
+            inF[q] = 0; evict[q] = 1; inF[r] = 1;
+            budget = budget + cost[q] - cost[r];
+            --o;
+        }
+    }
+    uint32_t ns = 0, tot = 0, ne = 0; int64_t stall_sum = 0;
+    for (uint32_t r = 0; r < n; ++r) {
+        if (inF[r]) { ++ns; tot += cost[r]; }
+        if (evict[r]) {
+            ++ne;
+            stall_sum += (int64_t)((u128)((uint64_t)prefilled[r] + generated[r]) * 1000000000u / cfg->io_bw_tps);
+        }
+    }
+    res->n_selected = ns; res->total_tokens = tot; res->n_preempted = ne; res->stall_ns = stall_sum;
+    free(inQ); free(P); free(I);
+}
+
 /* The step.  On return, selected[0..n_selected) holds ROW indices in batch order. */
 static int gmax_step(const og_config* cfg, const og_group* G, uint32_t n_groups,
                      const og_table* T, int64_t now, int64_t v_token,
@@ -253,13 +342,15 @@ static int gmax_step(const og_config* cfg, const og_group* G, uint32_t n_groups,
                      const uint32_t* task, const uint32_t* override_R,
                      const task_view* TV,
                      og_result* res, uint32_t* selected, uint32_t* sel_cost,
-                     const og_rows_out* ro) {
+                     const og_rows_out* ro, uint32_t frame_open) {
     memset(res, 0, sizeof(*res));
     if (cfg->refine_interval == 0 || cfg->frame_steps == 0 || cfg->q_den == 0 ||
         cfg->p_den == 0 || cfg->q_num == 0 || cfg->q_num > cfg->q_den || cfg->p_num == 0 ||
         cfg->p_num > cfg->p_den || cfg->prefill_chunk == 0 ||
         cfg->prefill_chunk > cfg->token_budget || cfg->max_batch == 0 || v_token <= 0 ||
-        cfg->eps_ns <= 0) { res->error = 1; return OG_EINVAL; }
+        cfg->eps_ns <= 0 || (cfg->preempt && (cfg->pmtn_den == 0 || cfg->io_bw_tps == 0))) {
+        res->error = 1; return OG_EINVAL;
+    }
 
     double* key = (double*)calloc(n ? n : 1, sizeof(double));
     uint32_t* lhat = (uint32_t*)calloc(n ? n : 1, sizeof(uint32_t));
@@ -442,20 +533,42 @@ static int gmax_step(const og_config* cfg, const og_group* G, uint32_t n_groups,
             u128 score = pf[j + 1] - pf[i];
             if (!have || score > best) { best = score; bi = i; bj = j; have = 1; }
         }
-        uint32_t tot = 0;
-        for (uint32_t i = bi; i <= bj; ++i) {
-            selected[i - bi] = Cd[i].row;
-            if (sel_cost) sel_cost[i - bi] = cost[Cd[i].row];
-            tot += cost[Cd[i].row];
-        }
-        res->n_selected = bj - bi + 1; res->total_tokens = tot; res->n_candidates = ncd;
-        res->b_star = bstar; res->bp = bp; res->thr = thr;
-
-        /* bookkeeping after selection: ever_scheduled / Running for the batch, and
-         * steps_waited += 1 (saturating at 0xFFFF) for every pending request left out; a selected
-         * request keeps its counter ("per frame" waited; reading A12) */
+        res->n_candidates = ncd; res->b_star = bstar; res->bp = bp; res->thr = thr;
         uint8_t* insel = (uint8_t*)calloc(n, 1);
-        for (uint32_t i = 0; i < res->n_selected; ++i) insel[selected[i]] = 1;
+        uint8_t* evict = (uint8_t*)calloc(n, 1);
+        if (!cfg->preempt) {
+            /* BestGroup is the batch */
+            uint32_t tot = 0;
+            for (uint32_t i = bi; i <= bj; ++i) {
+                selected[i - bi] = Cd[i].row;
+                if (sel_cost) sel_cost[i - bi] = cost[Cd[i].row];
+                tot += cost[Cd[i].row];
+                insel[Cd[i].row] = 1;
+            }
+            res->n_selected = bj - bi + 1; res->total_tokens = tot;
+        } else {
+            gate(cfg, n, id, input_len, generated, prefilled, meta, key, cost, pend, Cd + bi, bj - bi + 1,
+                 v_token, frame_open, insel, evict, res);
+            /* the batch in window order (len asc, id asc; A20) */
+            by_len_t* F = (by_len_t*)malloc(sizeof(by_len_t) * (res->n_selected ? res->n_selected : 1));
+            uint32_t f = 0;
+            for (uint32_t r = 0; r < n; ++r) {
+                if (!insel[r]) continue;
+                F[f].len = cfg->len_key ? (uint64_t)input_len[r] + generated[r] : (uint64_t)input_len[r];
+                F[f].id = id[r]; F[f].row = r; ++f;
+            }
+            qsort(F, f, sizeof(by_len_t), cmp_len_asc_id_asc);
+            for (uint32_t i = 0; i < f; ++i) {
+                selected[i] = F[i].row;
+                if (sel_cost) sel_cost[i] = cost[F[i].row];
+            }
+            free(F);
+        }
+
+        /* bookkeeping after selection: ever_scheduled / Running for the batch, Preempted for the
+         * requests the gate evicted, and steps_waited += 1 (saturating at 0xFFFF) for every
+         * pending request left out; a selected request keeps its counter ("per frame"
+         * waited; reading A12) */
         for (uint32_t r = 0; r < n; ++r) {
             if (!pend[r]) continue;
             if (insel[r]) {
@@ -464,11 +577,13 @@ static int gmax_step(const og_config* cfg, const og_group* G, uint32_t n_groups,
                 if (m_state(m) == ST_QUEUED || m_state(m) == ST_PREEMPTED) m = m_set_state(m, ST_RUNNING);
                 meta[r] = m;
             } else {
+                if (evict[r]) meta[r] = m_set_state(meta[r], ST_PREEMPTED);
                 uint32_t w = a_waited(aux[r]);
                 if (w < 0xFFFFu) ++w;
                 aux[r] = (aux[r] & 0xFFFFu) | (w << 16);
             }
         }
+        free(evict);
         free(insel); free(pf); free(pc); free(Cd); free(P);
     }
 out:
@@ -484,7 +599,7 @@ int og_step(const og_config* cfg, const og_group* groups, uint32_t n_groups,
             const og_table* T, int64_t now_ns, int64_t v_token_ns,
             const og_pool* pool, const og_tasks* tasks,
             og_result* res, uint32_t* batch_ids, uint32_t* batch_tokens, uint32_t* batch_rows,
-            const og_rows_out* ro) {
+            const og_rows_out* ro, uint32_t frame_open) {
     uint32_t n = pool->n;
     og_reset_memo();                 /* the memo lives for one call only */
     task_view tv; task_view* tvp = NULL;
@@ -521,7 +636,7 @@ int og_step(const og_config* cfg, const og_group* groups, uint32_t n_groups,
     uint32_t* sc = (uint32_t*)malloc(sizeof(uint32_t) * (n ? n : 1));
     int rc = gmax_step(cfg, groups, n_groups, T, now_ns, v_token_ns, n, pool->id, pool->arrival_ns,
                        pool->input_len, pool->generated, pool->prefilled, pool->meta, pool->aux,
-                       pool->task, pool->override_R, tvp, res, sel, sc, ro);
+                       pool->task, pool->override_R, tvp, res, sel, sc, ro, frame_open);
     if (rc == OG_OK) {
         for (uint32_t i = 0; i < res->n_selected; ++i) {
             if (batch_ids) batch_ids[i] = pool->id[sel[i]];
@@ -567,7 +682,7 @@ typedef struct {
 typedef struct {
     uint64_t token_goodput, tokens_processed;
     int64_t sim_end_ns;
-    uint32_t request_goodput, n_done, n_dropped, steps, n_tasks_done, n_tasks_dropped, error, _pad;
+    uint32_t request_goodput, n_done, n_dropped, steps, n_tasks_done, n_tasks_dropped, error, n_preempted;
 } og_replay_result;
 
 typedef struct {
@@ -576,6 +691,8 @@ typedef struct {
     double bp;
     uint64_t ids_hash;
     int64_t v_token_ns;   /* the v_token the step's keys used */
+    uint32_t n_preempted, _pad;   /* requests the gate evicted this step (A46) */
+    int64_t stall_ns;             /* their KV swap stall, part of this iteration's latency */
 } og_step_log;
 
 static uint64_t fnv1a_ids(const uint32_t* ids, uint32_t n) {
@@ -702,7 +819,8 @@ int og_replay(const og_config* cfg, const og_group* groups_in, uint32_t n_groups
         task_view tv = { nt, cb, ce, ta, tD, tle, ttot, NULL, gdone, tever, tdrop };
         og_result res;
         int st = gmax_step(cfg, G, n_groups, T, now, v, n, id, arr, tr->input_len, gen, pre, meta, aux,
-                           tr->task, tr->override_R, &tv, &res, sel, selc, NULL);
+                           tr->task, tr->override_R, &tv, &res, sel, selc, NULL,
+                           cfg->frame_steps && steps % cfg->frame_steps == 0);
         out->n_dropped += res.n_dropped_now;
         if (st == OG_EINVAL) { ret = OG_EINVAL; goto done; }
         /* A40: a dropped task ends without goodput; the calls of its later stages are dropped too */
@@ -739,6 +857,9 @@ int og_replay(const og_config* cfg, const og_group* groups_in, uint32_t n_groups
             if (ctx > maxctx) maxctx = ctx;
         }
         int64_t latency = rc->c0_ns + rc->c_att_ns * maxctx + rc->c_lin_ns * (int64_t)res.n_selected;
+        /* NEXT-1 (A46): the KV swap-out of the requests the gate evicted stalls this iteration */
+        latency += res.stall_ns;
+        out->n_preempted += res.n_preempted;
         now += latency;
         ++steps;
         out->tokens_processed += res.total_tokens;
@@ -749,6 +870,7 @@ int og_replay(const og_config* cfg, const og_group* groups_in, uint32_t n_groups
             L->n_candidates = res.n_candidates; L->b_star = res.b_star; L->bp = res.bp;
             L->ids_hash = fnv1a_ids(selid, res.n_selected);
             L->v_token_ns = v;
+            L->n_preempted = res.n_preempted; L->_pad = 0; L->stall_ns = res.stall_ns;
             if (log_ids) memcpy(log_ids + (size_t)(steps - 1) * cfg->max_batch, selid, 4 * res.n_selected);
         }
         /* progress of the executed batch (iteration end = token timestamp) */

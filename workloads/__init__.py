@@ -46,7 +46,10 @@ def default_config(**over) -> dict:
     waiting 5 s P:545) and the readings for the unspecified ones (q, eps, delta_starve)."""
     cfg = dict(token_budget=8192, max_batch=8192, prefill_chunk=512, refine_interval=50, frame_steps=50,
                q_num=95, q_den=100, p_num=95, p_den=100, delta_starve=1, len_key=0, appb_filter=0,
-               eps_ns=1000, waiting_ns=5 * S_)
+               eps_ns=1000, waiting_ns=5 * S_,
+               # NEXT-1 gate (reading A46): off by default; delta_pmtn = 0.1 (P:1359), KV swap
+               # bandwidth 10^6 tokens/s (S:440)
+               preempt=0, pmtn_num=1, pmtn_den=10, io_bw_tps=10 ** 6)
     cfg.update(over)
     return cfg
 
