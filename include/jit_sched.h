@@ -99,6 +99,14 @@ typedef struct jit_config {
     uint32_t flags;            /* JIT_CFG_* */
     int32_t device;            /* CUDA device ordinal */
     void* stream;              /* cudaStream_t for all device work */
+    /* NEXT-1 preemption gate (reading A46; §4.2, App. D.2): 0 = off, the
+     * batch is GMAX's window every step (A30).  On: Running means "in the executing batch"; a
+     * running request keeps its slot unless, at a frame boundary (every frame_steps steps),
+     * a proposed request beats it by R(in)/R(out) > 1 + pmtn_num/pmtn_den and its gain over a
+     * frame exceeds the KV swap loss (KV = prefilled + generated tokens at io_bw_tps tokens/s).
+     * Implemented in the trace replay (jit_sched_replay). */
+    uint32_t preempt, pmtn_num, pmtn_den, reserved2;
+    uint64_t io_bw_tps;
 } jit_config;
 
 /* A pool snapshot (SoA, n rows).  Layout rule: standalone rows first, then compound calls
@@ -290,7 +298,8 @@ typedef struct jit_replay_result {
     int64_t sim_end_ns;
     uint32_t request_goodput, n_done, n_dropped, steps, n_tasks_done;
     uint32_t n_tasks_dropped;      /* compound tasks dropped by admission (never scheduled, A40) */
-    uint32_t error, reserved;
+    uint32_t error;
+    uint32_t n_preempted;          /* running requests the preemption gate evicted (A46) */
 } jit_replay_result;
 
 typedef struct jit_step_log {
@@ -299,6 +308,8 @@ typedef struct jit_step_log {
     double bp;
     uint64_t ids_hash;             /* FNV-1a 64 over the batch ids (u32 LE) in batch order */
     int64_t v_token_ns;            /* the v_token the step's keys used */
+    uint32_t n_preempted, reserved;   /* requests the gate evicted this step (A46) */
+    int64_t stall_ns;              /* their KV swap stall, included in this step's latency */
 } jit_step_log;
 
 /* Device workspace for a replay call. */

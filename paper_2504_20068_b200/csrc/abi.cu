@@ -177,7 +177,7 @@ static int check_config(jit_sched* h, const jit_config* c, const jit_len_table* 
     if (c->refine_interval == 0 || c->frame_steps == 0 || c->q_den == 0 || c->q_num == 0 || c->q_num > c->q_den ||
         c->p_den == 0 || c->p_num == 0 || c->p_num > c->p_den || c->prefill_chunk == 0 ||
         c->prefill_chunk > c->token_budget || c->max_batch == 0 || c->eps_ns <= 0 || c->eps_ns >= (1ll << 36) ||
-        c->waiting_ns < 0)
+        c->waiting_ns < 0 || (c->preempt && (c->pmtn_den == 0 || c->io_bw_tps == 0)))
         return set_err(h, JIT_EINVAL, "invalid scheduler constants (ConfigError, S:417)");
     if (t->n_rows == 0 || t->n_rows > 65536 || t->n_bins == 0 || t->l_max == 0 || t->l_max >= 65536)
         return set_err(h, JIT_EINVAL, "invalid length table shape");
@@ -255,6 +255,9 @@ extern "C" int jit_sched_init(const jit_config* cfg, const jit_slo_group* groups
     c.p = (double)c.pn / (double)c.pd;      // IEEE division, correctly rounded like __ddiv_rn
     fastdiv_magic(c.R, &c.R_m, &c.R_l);
     fastdiv_magic(c.frame, &c.F_m, &c.F_l);
+    c.preempt = cfg->preempt ? 1u : 0u; c.pmtn_num = cfg->pmtn_num; c.pmtn_den = cfg->pmtn_den ? cfg->pmtn_den : 1u;
+    c.io_bw = cfg->io_bw_tps ? cfg->io_bw_tps : 1ull;
+    c.onepd = (double)((uint64_t)c.pmtn_den + c.pmtn_num) / (double)c.pmtn_den;   // one IEEE division
     CK(cudaMemcpyAsync((void*)h->T.edges, table->edges, 4ull * table->n_bins, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemcpyAsync((void*)h->T.cum, table->cum, 4ull * table->n_rows * table->n_bins, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemcpyAsync(h->d_groups, groups, sizeof(Group) * n_groups, cudaMemcpyHostToDevice, h->stream));

@@ -98,12 +98,12 @@ struct TraceMeta { uint32_t row_off, task_off, n_rows, n_tasks; };
 struct Spec { uint32_t trace, reserved; uint64_t load_num, load_den, slo_num, slo_den; };
 
 struct RLog { int64_t now_ns; uint32_t n_selected, total_tokens, n_candidates, b_star; double bp; uint64_t ids_hash;
-              int64_t v_token_ns; };
+              int64_t v_token_ns; uint32_t n_preempted, pad; int64_t stall_ns; };
 
 struct RResult {
     unsigned long long token_goodput, tokens_processed;
     int64_t sim_end_ns;
-    uint32_t request_goodput, n_done, n_dropped, steps, n_tasks_done, n_tasks_dropped, error, pad;
+    uint32_t request_goodput, n_done, n_dropped, steps, n_tasks_done, n_tasks_dropped, error, n_preempted;
 };
 
 struct ReplayArgs {
@@ -221,6 +221,8 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
     __shared__ uint64_t s_thr_img, s_tguess;
     __shared__ uint32_t s_m, s_spec_ok;
     __shared__ bool s_stop;
+    __shared__ uint32_t s_npre, s_gate_n;           // NEXT-1 gate: evictions this step / total; P+I count
+    __shared__ unsigned long long s_stall;
 
     const Cfg c = A.c;
     const Table T = A.T;
@@ -267,7 +269,9 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
             s_good = 0; s_tok = 0; s_reqg = 0; s_done = 0; s_drop = 0; s_tdone = 0; s_tdrop = 0; s_err = 0;
             s_now = 0; s_steps = 0; s_ring_n = 0; s_ring_pos = 0; s_ring_sum = 0; s_stop = false;
             s_tguess = kNone;                              // no speculative threshold before the first step
+            s_npre = 0; s_stall = 0;
         }
+        uint32_t n_preempted_total = 0;                    // (thread 0)
         __syncthreads();
         for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
             const bool comp = tsk[r] != kNoTask;
@@ -408,7 +412,9 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                     ++my_pend;
                 }
             }
-            // compound rows outside a released stage are never pending
+            // compound rows outside a released stage are never pending (after the task pass: it
+            // may have dropped a task's calls just now, A40)
+            __syncthreads();
             for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
                 const uint32_t meta = S.meta[r];
                 if ((m_flags(meta) & kCompound) && (S.arr[r] > now || m_state(meta) > kPreempted)) { S.img[r] = kNone; S.cost[r] = 0; }
@@ -493,6 +499,17 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                 __syncthreads();
                 if (s_spec_ok) break;
             }
+#ifdef JIT_REPLAY_DUMP_STEP
+            if (threadIdx.x == 0 && s_steps == JIT_REPLAY_DUMP_STEP) {
+                printf("dump step %u m %u np %u bstar %u spec_ok %u\n", s_steps, s_m, np, s_bstar, s_spec_ok);
+                for (uint32_t r = 0; r < n; ++r)
+                    if (S.img[r] != kNone)
+                        printf("row %u key %.10f cost %u st %u w %u pre %u gen %u L %u\n", r,
+                               __longlong_as_double((long long)S.img[r]), S.cost[r], m_state(S.meta[r]), S.aux[r] >> 16,
+                               S.pre[r], S.gen[r], L_in[r]);
+            }
+            __syncthreads();
+#endif
             if (threadIdx.x == 0) s_tguess = (uint64_t)__double_as_longlong(__dmul_rn(s_thr, 0.85));
             const uint32_t np_sorted = s_m;   // rows in the sorted prefix array bA (Cd is a prefix of it)
             // ---- (a8) Cd = prefix of the key-ordered list with key >= thr
@@ -576,12 +593,113 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                 }
                 __syncthreads();
             }
-            const uint32_t nsel = s_nsel, i0 = s_bi[0];
+            uint32_t nsel = s_nsel;
+            const uint32_t* selv = bBv + s_bi[0];          // the batch rows: GMAX's window ...
+            if (c.preempt) {
+                // ---- NEXT-1 preemption gate (reading A46; App. D.2):
+                // P = pending & Running, I = window \ P, both in (key desc, id asc); a single thread
+                // walks them (|P| + |I| <= 2 B_max), marks in S.late bits 1 (in window), 2 (in the
+                // batch), 3 (evicted); then the batch is put in window order (len asc, id asc).
+                const bool frame_open = s_steps % c.frame == 0;
+                for (uint32_t k = threadIdx.x; k < nsel; k += blockDim.x) S.late[selv[k]] |= 2u;
+                __syncthreads();
+                uint32_t cnt = 0;
+                for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
+                    const bool run = S.img[r] != kNone && m_state(S.meta[r]) == kRunning;
+                    cnt += run || ((S.late[r] & 2u) && !run);
+                }
+                uint64_t tot;
+                uint32_t pos = (uint32_t)block_exclusive_scan_u64(cnt, s_scan, &tot);
+                const uint32_t ng = (uint32_t)tot;
+                for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
+                    const bool run = S.img[r] != kNone && m_state(S.meta[r]) == kRunning;
+                    if (run || (S.late[r] & 2u)) {
+                        bA[pos] = ((u128)(run ? 0u : 1u) << 96) | make_ck(S.img[r], r);
+                        bAv[pos] = r; ++pos;
+                    }
+                }
+                uint32_t g2 = 1;
+                while (g2 < ng) g2 <<= 1;
+                for (uint32_t i = ng + threadIdx.x; i < g2; i += blockDim.x) { bA[i] = ~(u128)0; bAv[i] = 0; }
+                __syncthreads();
+                block_sort<u128>(bA, bAv, g2);
+                if (threadIdx.x == 0) {
+                    uint64_t budget = c.token_budget;
+                    uint32_t slots = c.max_batch, np_run = 0;
+                    while (np_run < ng && (uint32_t)(bA[np_run] >> 96) == 0u) ++np_run;
+                    for (uint32_t k = 0; k < np_run; ++k) {          // 1. running requests keep their slot
+                        const uint32_t r = bAv[k], cs = S.cost[r];
+                        if (slots >= 1 && cs <= budget) { S.late[r] |= 4u; --slots; budget -= cs; }
+                        else S.late[r] |= 8u;                        // does not fit: evicted
+                    }
+                    const double fs = __ddiv_rn(__ull2double_rn((uint64_t)c.frame * (uint64_t)v), 1e9);
+                    uint32_t o = np_run;
+                    for (uint32_t k = np_run; k < ng; ++k) {         // 2. newcomers
+                        const uint32_t r = bAv[k], cs = S.cost[r];
+                        if (slots >= 1 && cs <= budget) { S.late[r] |= 4u; --slots; budget -= cs; continue; }
+                        if (!frame_open) continue;
+                        while (o > 0 && !((S.late[bAv[o - 1]] & 4u) && !(S.late[bAv[o - 1]] & 2u))) --o;
+                        if (o == 0) continue;
+                        const uint32_t q = bAv[o - 1];
+                        const uint64_t kv = (uint64_t)S.pre[q] + S.gen[q];
+                        const int64_t st = (int64_t)((u128)kv * 1000000000u / c.io_bw);
+                        const double loss = __ddiv_rn(__ll2double_rn(st), __ll2double_rn(v));
+                        const double ki = __longlong_as_double((long long)S.img[r]);
+                        const double kq = __longlong_as_double((long long)S.img[q]);
+                        const double gain = __dmul_rn(__dsub_rn(ki, kq), fs);
+                        if (cs <= budget + S.cost[q] && ki > __dmul_rn(kq, c.onepd) && gain > loss) {
+                            S.late[q] = (S.late[q] & ~4u) | 8u;
+                            S.late[r] |= 4u;
+                            budget = budget + S.cost[q] - cs;
+                            --o;
+                        }
+                    }
+                    s_npre = 0; s_stall = 0;
+                }
+                __syncthreads();
+                // the batch in window order; evicted rows become Preempted (their KV is swapped out)
+                uint32_t cf = 0, myev = 0, mytok = 0;
+                unsigned long long mystall = 0;
+                for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
+                    const uint32_t lt = S.late[r];
+                    cf += (lt >> 2) & 1u;
+                    if (lt & 4u) mytok += S.cost[r];
+                    if (lt & 8u) {
+                        ++myev;
+                        mystall += (unsigned long long)((u128)((uint64_t)S.pre[r] + S.gen[r]) * 1000000000u / c.io_bw);
+                        S.meta[r] = m_with_state(S.meta[r], kPreempted);
+                    }
+                }
+                pos = (uint32_t)block_exclusive_scan_u64(cf, s_scan, &tot);
+                const uint32_t nf = (uint32_t)tot;
+                for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
+                    if (S.late[r] & 4u) {
+                        const uint64_t len = c.len_key ? (uint64_t)L_in[r] + S.gen[r] : (uint64_t)L_in[r];
+                        bB[pos] = (len << 32) | r; bBv[pos] = r; ++pos;
+                    }
+                }
+                uint32_t f2 = 1;
+                while (f2 < nf) f2 <<= 1;
+                for (uint32_t i = nf + threadIdx.x; i < f2; i += blockDim.x) { bB[i] = ~0ull; bBv[i] = 0; }
+                myev = warp_sum(myev); mytok = warp_sum(mytok);
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) mystall += __shfl_xor_sync(0xffffffffu, mystall, off);
+                if (lane == 0) { atomicAdd(&s_npre, myev); atomicAdd(&s_stall, mystall); }
+                __syncthreads();
+                block_sort<uint64_t>(bB, bBv, f2);
+                for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) S.late[r] &= 1u;   // marks off
+                if (threadIdx.x == 0) { s_nsel = nf; s_tot = 0; }
+                __syncthreads();
+                if (lane == 0) atomicAdd(&s_tot, mytok);
+                nsel = nf;
+                selv = bBv;                                  // ... or the gated batch
+                __syncthreads();
+            }
             // batch rows, bookkeeping (ever_scheduled, Running), max context; a selected row keeps
             // its steps_waited and is unmarked as pending (img) for the +1 of the others below
             int64_t myctx = 0;
             for (uint32_t k = threadIdx.x; k < nsel; k += blockDim.x) {
-                const uint32_t r = bBv[i0 + k];
+                const uint32_t r = selv[k];
                 S.batch[k] = r;
                 uint32_t m = S.meta[r] | (kEver << 12);
                 if (m_state(m) == kQueued || m_state(m) == kPreempted) m = m_with_state(m, kRunning);
@@ -599,18 +717,22 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
             for (uint32_t r = threadIdx.x; r < n; r += blockDim.x)
                 if (S.img[r] != kNone && (S.aux[r] >> 16) < 0xFFFFu) S.aux[r] += 1u << 16;
             // ---- (a10) iteration latency and time advance
-            const int64_t latency = A.c0 + A.c_att * s_maxctx + A.c_lin * (int64_t)nsel;
+            // + the KV swap stall of the requests the gate evicted (NEXT-1, A46)
+            const int64_t stall = c.preempt ? (int64_t)s_stall : 0;
+            const int64_t latency = A.c0 + A.c_att * s_maxctx + A.c_lin * (int64_t)nsel + stall;
             const int64_t tnow = now + latency;
             if (threadIdx.x == 0) {
                 s_now = tnow;
                 s_steps += 1;
                 s_tok += s_tot;
+                if (c.preempt) n_preempted_total += s_npre;
                 if (A.log && s_steps <= A.log_steps) {
                     uint64_t h = 1469598103934665603ull;
                     for (uint32_t k = 0; k < nsel; ++k) h = fnv1a_u32(h, S.batch[k]);
                     RLog L;
                     L.now_ns = tnow; L.n_selected = nsel; L.total_tokens = s_tot; L.n_candidates = ncd;
                     L.b_star = s_bstar; L.bp = s_bp; L.ids_hash = h; L.v_token_ns = v;
+                    L.n_preempted = c.preempt ? s_npre : 0u; L.pad = 0; L.stall_ns = stall;
                     A.log[(uint64_t)rep * A.log_steps + s_steps - 1] = L;
                 }
                 // v_token ring (Delta = frame_steps latencies)
@@ -659,7 +781,7 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
             RResult R;
             R.token_goodput = s_good; R.tokens_processed = s_tok; R.sim_end_ns = s_now;
             R.request_goodput = s_reqg; R.n_done = s_done; R.n_dropped = s_drop; R.steps = s_steps;
-            R.n_tasks_done = s_tdone; R.n_tasks_dropped = s_tdrop; R.error = s_err; R.pad = 0;
+            R.n_tasks_done = s_tdone; R.n_tasks_dropped = s_tdrop; R.error = s_err; R.n_preempted = n_preempted_total;
             A.out[rep] = R;
         }
         __syncthreads();

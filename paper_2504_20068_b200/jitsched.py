@@ -44,7 +44,9 @@ _CFG_U32 = ("token_budget", "max_batch", "prefill_chunk", "refine_interval", "fr
 class jit_config(C.Structure):
     _fields_ = [(k, C.c_uint32) for k in _CFG_U32] + \
                [("eps_ns", C.c_int64), ("waiting_ns", C.c_int64), ("capacity", C.c_uint32),
-                ("task_capacity", C.c_uint32), ("flags", C.c_uint32), ("device", C.c_int32), ("stream", C.c_void_p)]
+                ("task_capacity", C.c_uint32), ("flags", C.c_uint32), ("device", C.c_int32), ("stream", C.c_void_p),
+                ("preempt", C.c_uint32), ("pmtn_num", C.c_uint32), ("pmtn_den", C.c_uint32), ("reserved2", C.c_uint32),
+                ("io_bw_tps", C.c_uint64)]
 
 
 _POOL_ROWS = (("id", np.uint32), ("arrival_ns", np.int64), ("input_len", np.uint32), ("generated", np.uint32),
@@ -101,12 +103,12 @@ class jit_replay_cfg(C.Structure):
 class jit_replay_result(C.Structure):
     _fields_ = [("token_goodput", C.c_uint64), ("tokens_processed", C.c_uint64), ("sim_end_ns", C.c_int64)] + \
                [(k, C.c_uint32) for k in ("request_goodput", "n_done", "n_dropped", "steps", "n_tasks_done",
-                                          "n_tasks_dropped", "error", "reserved")]
+                                          "n_tasks_dropped", "error", "n_preempted")]
 
 
 STEP_LOG_DTYPE = np.dtype([("now_ns", "<i8"), ("n_selected", "<u4"), ("total_tokens", "<u4"),
                            ("n_candidates", "<u4"), ("b_star", "<u4"), ("bp", "<f8"), ("ids_hash", "<u8"),
-                           ("v_token_ns", "<i8")])
+                           ("v_token_ns", "<i8"), ("n_preempted", "<u4"), ("reserved", "<u4"), ("stall_ns", "<i8")])
 
 _lib = None
 EXPORTS = ("jit_sched_workspace_bytes", "jit_sched_init", "jit_sched_load", "jit_sched_step",
@@ -164,6 +166,10 @@ def make_config(cfg: dict, capacity: int, task_capacity: int, device: int = 0, s
     c.flags = (JIT_CFG_DEBUG_ROWS if debug else 0) | (JIT_CFG_NO_GRAPH if os.environ.get("JITSCHED_NO_GRAPH") else 0)
     c.device = int(device)
     c.stream = stream
+    c.preempt = int(cfg.get("preempt", 0))
+    c.pmtn_num = int(cfg.get("pmtn_num", 1))
+    c.pmtn_den = int(cfg.get("pmtn_den", 10))
+    c.io_bw_tps = int(cfg.get("io_bw_tps", 10 ** 6))
     return c
 
 

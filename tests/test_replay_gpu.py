@@ -101,3 +101,21 @@ def test_many_small_random_traces():
         res, log = s.replay([d["trace"]], [_spec(rc)], rc, log_steps=rc["n_steps"])
         _cmp(res[0], log[0], ref, f"random {it}")
         s.close()
+
+
+def test_task_drops_in_the_same_step_as_scoring():
+    """Mixed traces whose compound tasks are dropped by admission (A40) while other rows are
+    scored: the dropped calls must leave the pending set in that very step (regression: the
+    compound-row cleanup once raced the task pass)."""
+    rng = np.random.default_rng(701)
+    for it in range(4):
+        d = W.trace_mixed(300 + it, n_rows=int(rng.integers(20, 500)), rate_per_s=float(rng.uniform(2, 60)))
+        d["cfg"] = W.default_config(token_budget=int(rng.integers(600, 4000)), max_batch=int(rng.integers(1, 48)),
+                                    prefill_chunk=512, refine_interval=int(rng.choice([1, 50])),
+                                    frame_steps=int(rng.choice([1, 2, 7, 50])))
+        rc = dict(d["rcfg"], n_steps=3000)
+        ref = oracle.replay(d["cfg"], d["groups"], d["table"], d["trace"], rc, log=True)
+        s = _sched(d, cap=512)
+        res, log = s.replay([d["trace"]], [_spec(rc)], rc, log_steps=rc["n_steps"])
+        _cmp(res[0], log[0], ref, f"drops {it}")
+        s.close()
