@@ -45,7 +45,8 @@ class _Config(C.Structure):
                                           "frame_steps", "q_num", "q_den", "p_num", "p_den", "delta_starve",
                                           "len_key", "appb_filter")] + \
                [("eps_ns", C.c_int64), ("waiting_ns", C.c_int64)] + \
-               [(k, C.c_uint32) for k in ("preempt", "pmtn_num", "pmtn_den", "_pad2")] + [("io_bw_tps", C.c_uint64)]
+               [(k, C.c_uint32) for k in ("preempt", "pmtn_num", "pmtn_den", "_pad2")] + [("io_bw_tps", C.c_uint64)] + \
+               [(k, C.c_uint32) for k in ("fair_num", "fair_den")]
 
 
 class _Table(C.Structure):
@@ -56,7 +57,7 @@ class _Table(C.Structure):
 class _Pool(C.Structure):
     _fields_ = [("n", C.c_uint32), ("_pad", C.c_uint32)] + \
                [(k, C.c_void_p) for k in ("id", "arrival_ns", "input_len", "generated", "prefilled", "meta",
-                                          "aux", "task", "override_R")]
+                                          "aux", "task", "override_R", "fair")]
 
 
 class _Tasks(C.Structure):
@@ -80,13 +81,14 @@ class _Trace(C.Structure):
                [(k, C.c_void_p) for k in ("arrival_ns", "input_len", "true_out", "group", "dist_row", "override_R",
                                           "task", "task_arrival_ns", "task_deadline_ns", "task_n_stages",
                                           "stage_kind", "stage_exec_ns", "stage_pattern_ms", "stage_call_begin",
-                                          "stage_call_end")]
+                                          "stage_call_end", "fair")]
 
 
 class _ReplayCfg(C.Structure):
     _fields_ = [("n_steps", C.c_uint32), ("log_ids", C.c_uint32)] + \
                [(k, C.c_int64) for k in ("v_token0_ns", "c0_ns", "c_att_ns", "c_lin_ns")] + \
-               [(k, C.c_uint64) for k in ("load_num", "load_den", "slo_num", "slo_den")]
+               [(k, C.c_uint64) for k in ("load_num", "load_den", "slo_num", "slo_den")] + \
+               [(k, C.c_uint32) for k in ("p_adapt", "eps_num", "eps_den", "window_frames")] + [("seed", C.c_uint64)]
 
 
 class _ReplayResult(C.Structure):
@@ -97,7 +99,7 @@ class _ReplayResult(C.Structure):
 
 STEP_LOG_DTYPE = np.dtype([("now_ns", "<i8"), ("n_selected", "<u4"), ("total_tokens", "<u4"),
                            ("n_candidates", "<u4"), ("b_star", "<u4"), ("bp", "<f8"), ("ids_hash", "<u8"),
-                           ("v_token_ns", "<i8"), ("n_preempted", "<u4"), ("_pad", "<u4"), ("stall_ns", "<i8")])
+                           ("v_token_ns", "<i8"), ("n_preempted", "<u4"), ("p_num", "<u4"), ("stall_ns", "<i8")])
 
 
 def _load():
@@ -123,7 +125,8 @@ def _ptr(a):
 
 def _mk_config(cfg):
     c = _Config()
-    gate_defaults = {"preempt": 0, "pmtn_num": 1, "pmtn_den": 10, "_pad2": 0, "io_bw_tps": 10 ** 6}
+    gate_defaults = {"preempt": 0, "pmtn_num": 1, "pmtn_den": 10, "_pad2": 0, "io_bw_tps": 10 ** 6,
+                     "fair_num": 0, "fair_den": 1}
     for k, _ in _Config._fields_:
         setattr(c, k, int(cfg.get(k, gate_defaults.get(k, 0)) if k in gate_defaults else cfg[k]))
     return c
@@ -180,6 +183,8 @@ def step(cfg, groups, table, now_ns: int, v_token_ns: int, pool, tasks=None, row
         "aux": np.array(pool["aux"], dtype=np.uint32), "task": _arr(pool["task"], np.uint32),
         "override_R": _arr(pool["override_R"], np.uint32),
     }
+    if pool.get("fair") is not None:
+        cols["fair"] = _arr(pool["fair"], np.uint32)
     p = _Pool()
     p.n = n
     for k, v in cols.items():
@@ -238,6 +243,8 @@ def replay(cfg, groups, table, trace, rcfg, log: bool = False, log_ids: bool = F
              "stage_exec_ns": np.int64, "stage_pattern_ms": np.uint32, "stage_call_begin": np.uint32,
              "stage_call_end": np.uint32}
     cols = {}
+    if trace.get("fair") is not None:
+        types = dict(types, fair=np.uint32)
     for k, dt in types.items():
         a = _arr(trace[k], dt)
         if a.size == 0:
@@ -251,6 +258,8 @@ def replay(cfg, groups, table, trace, rcfg, log: bool = False, log_ids: bool = F
     rc.log_ids = 1 if log_ids else 0
     for k in ("v_token0_ns", "c0_ns", "c_att_ns", "c_lin_ns", "load_num", "load_den", "slo_num", "slo_den"):
         setattr(rc, k, int(rcfg[k]))
+    for k, dflt in (("p_adapt", 0), ("eps_num", 1), ("eps_den", 10), ("window_frames", 100), ("seed", 0)):
+        setattr(rc, k, int(rcfg.get(k, dflt)))
     res = _ReplayResult()
     L = np.zeros(max(rc.n_steps, 1), STEP_LOG_DTYPE) if log else None
     LI = np.zeros(max(rc.n_steps, 1) * int(cfg["max_batch"]), np.uint32) if log_ids else None

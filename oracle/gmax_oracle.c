@@ -53,6 +53,8 @@ typedef struct {
     /* NEXT-1 preemption gate (reading A46): 0 = off (the step re-selects every iteration, A30) */
     uint32_t preempt, pmtn_num, pmtn_den, _pad2;   /* delta_pmtn = pmtn_num / pmtn_den (App. D.2) */
     uint64_t io_bw_tps;                            /* KV swap bandwidth, tokens per second */
+    /* NEXT-2 fairness blend (§4.3, reading A47): f = fair_num / fair_den, 0 = off */
+    uint32_t fair_num, fair_den;
 } og_config;
 
 typedef struct {
@@ -72,6 +74,7 @@ typedef struct {
     uint32_t* aux;        /* in/out: dist_row bits 0-15, steps_waited 16-31 */
     const uint32_t* task; /* NO_TASK for standalone requests */
     const uint32_t* override_R;
+    const uint32_t* fair; /* NULL or Fair(r) per request (NEXT-2 blend, A47); NULL reads as 0 */
 } og_pool;
 
 typedef struct {
@@ -199,6 +202,17 @@ static int make_key(uint64_t Gp, uint64_t t_gen, int64_t eps, double* out) {
 }
 
 /* reported JIT rate (tokens/s): len_rem * 10^9 / t_rem; +inf when t_rem <= 0 (A38) */
+/* NEXT-2 (§4.3): priority'(r) = (1 - f) * priority(r) + f * Fair(r), f = num / den,
+ * Fair(r) a developer-supplied non-negative integer score in key units (reading A47).  Written
+ * over the common denominator: fl( fl( fl(key * (den - num)) + num * Fair ) / den ), three IEEE
+ * operations in this order (num * Fair is an exact integer < 2^53).  f = 0 leaves the key. */
+static double blend_fair(double key, uint32_t fair, uint32_t num, uint32_t den) {
+    if (num == 0) return key;
+    double a = key * (double)(den - num);
+    double b = (double)((uint64_t)num * fair);
+    return (a + b) / (double)den;
+}
+
 static double make_rate(uint64_t len_rem, int64_t t_rem) {
     if (t_rem <= 0) return __builtin_inf();
     return (double)(len_rem * 1000000000ull) / (double)t_rem;
@@ -339,7 +353,7 @@ static int gmax_step(const og_config* cfg, const og_group* G, uint32_t n_groups,
                      uint32_t n, const uint32_t* id, const int64_t* arrival,
                      const uint32_t* input_len, const uint32_t* generated,
                      const uint32_t* prefilled, uint32_t* meta, uint32_t* aux,
-                     const uint32_t* task, const uint32_t* override_R,
+                     const uint32_t* task, const uint32_t* override_R, const uint32_t* fair,
                      const task_view* TV,
                      og_result* res, uint32_t* selected, uint32_t* sel_cost,
                      const og_rows_out* ro, uint32_t frame_open) {
@@ -348,7 +362,8 @@ static int gmax_step(const og_config* cfg, const og_group* G, uint32_t n_groups,
         cfg->p_den == 0 || cfg->q_num == 0 || cfg->q_num > cfg->q_den || cfg->p_num == 0 ||
         cfg->p_num > cfg->p_den || cfg->prefill_chunk == 0 ||
         cfg->prefill_chunk > cfg->token_budget || cfg->max_batch == 0 || v_token <= 0 ||
-        cfg->eps_ns <= 0 || (cfg->preempt && (cfg->pmtn_den == 0 || cfg->io_bw_tps == 0))) {
+        cfg->eps_ns <= 0 || (cfg->preempt && (cfg->pmtn_den == 0 || cfg->io_bw_tps == 0)) ||
+        (cfg->fair_num && cfg->fair_num > cfg->fair_den)) {
         res->error = 1; return OG_EINVAL;
     }
 
@@ -461,6 +476,10 @@ static int gmax_step(const og_config* cfg, const og_group* G, uint32_t n_groups,
             }
         }
     }
+    /* NEXT-2 fairness blend of every pending request's priority (A47), before (a7)-(a9) */
+    if (rc == OG_OK && cfg->fair_num)
+        for (uint32_t r = 0; r < n; ++r)
+            if (pend[r]) key[r] = blend_fair(key[r], fair ? fair[r] : 0u, cfg->fair_num, cfg->fair_den);
     /* every row of a task range must be a compound call of that task with a CMP group */
     if (rc == OG_OK && TV)
         for (uint32_t t = 0; t < TV->n && rc == OG_OK; ++t)
@@ -636,7 +655,7 @@ int og_step(const og_config* cfg, const og_group* groups, uint32_t n_groups,
     uint32_t* sc = (uint32_t*)malloc(sizeof(uint32_t) * (n ? n : 1));
     int rc = gmax_step(cfg, groups, n_groups, T, now_ns, v_token_ns, n, pool->id, pool->arrival_ns,
                        pool->input_len, pool->generated, pool->prefilled, pool->meta, pool->aux,
-                       pool->task, pool->override_R, tvp, res, sel, sc, ro, frame_open);
+                       pool->task, pool->override_R, pool->fair, tvp, res, sel, sc, ro, frame_open);
     if (rc == OG_OK) {
         for (uint32_t i = 0; i < res->n_selected; ++i) {
             if (batch_ids) batch_ids[i] = pool->id[sel[i]];
@@ -671,12 +690,17 @@ typedef struct {
     const uint32_t* stage_pattern_ms;      /* n_tasks*8: matched-pattern stage time */
     const uint32_t* stage_call_begin;      /* n_tasks*8: rows of an LLM stage */
     const uint32_t* stage_call_end;
+    const uint32_t* fair;                  /* NULL or Fair(r) per row (NEXT-2 blend, A47) */
 } og_trace;
 
 typedef struct {
     uint32_t n_steps, log_ids;
     int64_t v_token0_ns, c0_ns, c_att_ns, c_lin_ns;
     uint64_t load_num, load_den, slo_num, slo_den;   /* arrival' = a*load_den/load_num; SLO' = t*slo_num/slo_den */
+    /* NEXT-2 online adaptation of p (reading A48): epsilon-greedy over P_GRID, one arm per
+     * window of window_frames frames (window_frames * frame_steps steps); 0 = off */
+    uint32_t p_adapt, eps_num, eps_den, window_frames;
+    uint64_t seed;
 } og_replay_cfg;
 
 typedef struct {
@@ -691,7 +715,7 @@ typedef struct {
     double bp;
     uint64_t ids_hash;
     int64_t v_token_ns;   /* the v_token the step's keys used */
-    uint32_t n_preempted, _pad;   /* requests the gate evicted this step (A46) */
+    uint32_t n_preempted, p_num;  /* requests the gate evicted this step (A46); the cutoff p_num used (A48) */
     int64_t stall_ns;             /* their KV swap stall, part of this iteration's latency */
 } og_step_log;
 
@@ -702,13 +726,42 @@ static uint64_t fnv1a_ids(const uint32_t* ids, uint32_t n) {
     return h;
 }
 
+/* NEXT-2 online p ("automates and continuously adapts p online by exploring different
+ * thresholds and converging to those that maximize end-to-end goodput"; reading A48, after SPEC
+ * S:361): arms P_GRID / 100; each window of W = window_frames * frame_steps steps runs one arm and
+ * scores it by the token goodput earned in that window.  Untried arms go first, in grid order;
+ * then with probability eps_num / eps_den a uniformly drawn arm, else the arm of the highest
+ * mean window goodput (sum / count compared exactly by cross products; the lowest index on a
+ * tie).  The draws come from the counter-based splitmix64 of (seed + window index). */
+static const uint32_t P_GRID[4] = { 80, 90, 95, 100 };
+static uint64_t splitmix64_at(uint64_t x) {
+    uint64_t z = x * 0x9E3779B97F4A7C15ull + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+static uint32_t next_arm(const og_replay_cfg* rc, const uint64_t* gsum, const uint32_t* gcnt, uint64_t window) {
+    for (uint32_t a = 0; a < 4; ++a) if (gcnt[a] == 0) return a;
+    uint64_t u = splitmix64_at(rc->seed + window);
+    if (u % rc->eps_den < rc->eps_num) return (uint32_t)((u >> 32) % 4u);
+    uint32_t best = 0;
+    for (uint32_t a = 1; a < 4; ++a)        /* mean_a > mean_best <=> sum_a * cnt_best > sum_best * cnt_a */
+        if ((u128)gsum[a] * gcnt[best] > (u128)gsum[best] * gcnt[a]) best = a;
+    return best;
+}
+
 int og_replay(const og_config* cfg, const og_group* groups_in, uint32_t n_groups,
               const og_table* T, const og_trace* tr, const og_replay_cfg* rc,
               og_replay_result* out, og_step_log* log, uint32_t* log_ids) {
     memset(out, 0, sizeof(*out));
     og_reset_memo();
     uint32_t n = tr->n_rows, nt = tr->n_tasks;
-    if (!rc->load_num || !rc->load_den || !rc->slo_num || !rc->slo_den || n_groups > 256) { out->error = 1; return OG_EINVAL; }
+    if (!rc->load_num || !rc->load_den || !rc->slo_num || !rc->slo_den || n_groups > 256 ||
+        (rc->p_adapt && (!rc->eps_den || rc->eps_num > rc->eps_den || !rc->window_frames))) { out->error = 1; return OG_EINVAL; }
+    og_config cf = *cfg;                        /* p_num changes per window when p adapts (A48) */
+    uint64_t gsum[4] = {0, 0, 0, 0}, g_start = 0, window = 0;
+    uint32_t gcnt[4] = {0, 0, 0, 0}, arm = 0;
+    if (rc->p_adapt) { cf.p_num = P_GRID[0]; cf.p_den = 100; }
     /* SLO scaling of the group table (§6.4 P:784-786 sweep shape) */
     og_group G[256];
     for (uint32_t g = 0; g < n_groups; ++g) {
@@ -818,8 +871,8 @@ int og_replay(const og_config* cfg, const og_group* groups_in, uint32_t n_groups
         int64_t v = ring_n ? ring_sum / (int64_t)ring_n : rc->v_token0_ns;
         task_view tv = { nt, cb, ce, ta, tD, tle, ttot, NULL, gdone, tever, tdrop };
         og_result res;
-        int st = gmax_step(cfg, G, n_groups, T, now, v, n, id, arr, tr->input_len, gen, pre, meta, aux,
-                           tr->task, tr->override_R, &tv, &res, sel, selc, NULL,
+        int st = gmax_step(&cf, G, n_groups, T, now, v, n, id, arr, tr->input_len, gen, pre, meta, aux,
+                           tr->task, tr->override_R, tr->fair, &tv, &res, sel, selc, NULL,
                            cfg->frame_steps && steps % cfg->frame_steps == 0);
         out->n_dropped += res.n_dropped_now;
         if (st == OG_EINVAL) { ret = OG_EINVAL; goto done; }
@@ -870,7 +923,7 @@ int og_replay(const og_config* cfg, const og_group* groups_in, uint32_t n_groups
             L->n_candidates = res.n_candidates; L->b_star = res.b_star; L->bp = res.bp;
             L->ids_hash = fnv1a_ids(selid, res.n_selected);
             L->v_token_ns = v;
-            L->n_preempted = res.n_preempted; L->_pad = 0; L->stall_ns = res.stall_ns;
+            L->n_preempted = res.n_preempted; L->p_num = cf.p_num; L->stall_ns = res.stall_ns;
             if (log_ids) memcpy(log_ids + (size_t)(steps - 1) * cfg->max_batch, selid, 4 * res.n_selected);
         }
         /* progress of the executed batch (iteration end = token timestamp) */
@@ -912,6 +965,14 @@ int og_replay(const og_config* cfg, const og_group* groups_in, uint32_t n_groups
         /* v_token: floor of the trailing mean of the last Delta latencies */
         if (ring_n < cfg->frame_steps) { lat_ring[ring_n++] = latency; ring_sum += latency; }
         else { ring_sum += latency - lat_ring[ring_pos]; lat_ring[ring_pos] = latency; ring_pos = (ring_pos + 1) % cfg->frame_steps; }
+        /* NEXT-2 online p (A48): the window's goodput scores its arm; the next arm is chosen */
+        if (rc->p_adapt && steps % ((uint64_t)rc->window_frames * cfg->frame_steps) == 0) {
+            gsum[arm] += out->token_goodput - g_start; gcnt[arm] += 1;
+            g_start = out->token_goodput;
+            window += 1;
+            arm = next_arm(rc, gsum, gcnt, window);
+            cf.p_num = P_GRID[arm];
+        }
     }
     out->steps = steps; out->sim_end_ns = now;
 done:
