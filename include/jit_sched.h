@@ -107,6 +107,10 @@ typedef struct jit_config {
      * Implemented in the trace replay (jit_sched_replay). */
     uint32_t preempt, pmtn_num, pmtn_den, reserved2;
     uint64_t io_bw_tps;
+    /* NEXT-2 fairness blend (§4.3, reading A47): priority' = (1-f) priority + f Fair(r)
+     * with f = fair_num / fair_den (0 = off), Fair(r) the pool's per-request `fair` score, as
+     * fl(fl(fl(key * (den - num)) + num * Fair) / den).  Step and replay. */
+    uint32_t fair_num, fair_den;
 } jit_config;
 
 /* A pool snapshot (SoA, n rows).  Layout rule: standalone rows first, then compound calls
@@ -134,6 +138,7 @@ typedef struct jit_pool {
     const uint32_t* n_stages;         /* S <= JIT_MAX_STAGES */
     const uint32_t* pattern_ms;       /* n_tasks * 8: matched-pattern stage times (phi) */
     const uint64_t* goodput_done;     /* goodput of the task's finished calls */
+    const uint32_t* fair;             /* NULL (= 0) or Fair(r) per row, key units (NEXT-2, A47) */
 } jit_pool;
 
 /* Per-step input: the step's clock and v_token, and what changed since the previous step, applied
@@ -278,6 +283,7 @@ typedef struct jit_trace {
     const uint32_t* stage_pattern_ms;  /* matched-pattern stage time (phi) */
     const uint32_t* stage_call_begin;  /* rows of an LLM stage: [begin, end) */
     const uint32_t* stage_call_end;
+    const uint32_t* fair;              /* NULL (= 0) or Fair(r) per row (NEXT-2 blend, A47) */
 } jit_trace;
 
 typedef struct jit_replay_spec {
@@ -291,6 +297,11 @@ typedef struct jit_replay_cfg {
     uint32_t n_steps, n_replays, log_steps, reserved;   /* log_steps: rows of the step log */
     int64_t v_token0_ns, c0_ns, c_att_ns, c_lin_ns;
     const jit_replay_spec* specs;  /* n_replays */
+    /* NEXT-2 online p (reading A48): 1 = epsilon-greedy over p in {0.80, 0.90, 0.95, 1.00},
+     * one arm per window of window_frames * frame_steps steps, scored by the window's token
+     * goodput; explore with probability eps_num / eps_den (splitmix64 of seed + window index) */
+    uint32_t p_adapt, eps_num, eps_den, window_frames;
+    uint64_t seed;
 } jit_replay_cfg;
 
 typedef struct jit_replay_result {
@@ -308,7 +319,8 @@ typedef struct jit_step_log {
     double bp;
     uint64_t ids_hash;             /* FNV-1a 64 over the batch ids (u32 LE) in batch order */
     int64_t v_token_ns;            /* the v_token the step's keys used */
-    uint32_t n_preempted, reserved;   /* requests the gate evicted this step (A46) */
+    uint32_t n_preempted;          /* requests the gate evicted this step (A46) */
+    uint32_t p_num;                /* the cutoff p (in 1/100 when adapting, A48) this step used */
     int64_t stall_ns;              /* their KV swap stall, included in this step's latency */
 } jit_step_log;
 

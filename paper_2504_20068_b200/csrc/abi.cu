@@ -113,6 +113,7 @@ static void carve(Carve& cv, const jit_config* cfg, const jit_len_table* tab, Po
     const bool dbg = (cfg->flags & JIT_CFG_DEBUG_ROWS) != 0;
     P.rows = cv.take<HotRow>(N);
     P.id = cv.take<uint32_t>(N); P.task = cv.take<uint32_t>(N); P.ovr = cv.take<uint32_t>(N);
+    P.fair = cv.take<uint32_t>(N);
     P.img = cv.take<uint64_t>(N); P.cost = cv.take<uint32_t>(N);
     P.dbg_rate = dbg ? cv.take<double>(N) : nullptr;
     P.dbg_trem = dbg ? cv.take<int64_t>(N) : nullptr;
@@ -177,7 +178,8 @@ static int check_config(jit_sched* h, const jit_config* c, const jit_len_table* 
     if (c->refine_interval == 0 || c->frame_steps == 0 || c->q_den == 0 || c->q_num == 0 || c->q_num > c->q_den ||
         c->p_den == 0 || c->p_num == 0 || c->p_num > c->p_den || c->prefill_chunk == 0 ||
         c->prefill_chunk > c->token_budget || c->max_batch == 0 || c->eps_ns <= 0 || c->eps_ns >= (1ll << 36) ||
-        c->waiting_ns < 0 || (c->preempt && (c->pmtn_den == 0 || c->io_bw_tps == 0)))
+        c->waiting_ns < 0 || (c->preempt && (c->pmtn_den == 0 || c->io_bw_tps == 0)) ||
+        (c->fair_num && c->fair_num > c->fair_den))
         return set_err(h, JIT_EINVAL, "invalid scheduler constants (ConfigError, S:417)");
     if (t->n_rows == 0 || t->n_rows > 65536 || t->n_bins == 0 || t->l_max == 0 || t->l_max >= 65536)
         return set_err(h, JIT_EINVAL, "invalid length table shape");
@@ -258,6 +260,7 @@ extern "C" int jit_sched_init(const jit_config* cfg, const jit_slo_group* groups
     c.preempt = cfg->preempt ? 1u : 0u; c.pmtn_num = cfg->pmtn_num; c.pmtn_den = cfg->pmtn_den ? cfg->pmtn_den : 1u;
     c.io_bw = cfg->io_bw_tps ? cfg->io_bw_tps : 1ull;
     c.onepd = (double)((uint64_t)c.pmtn_den + c.pmtn_num) / (double)c.pmtn_den;   // one IEEE division
+    c.fair_num = cfg->fair_num; c.fair_den = cfg->fair_num ? cfg->fair_den : 1u;
     CK(cudaMemcpyAsync((void*)h->T.edges, table->edges, 4ull * table->n_bins, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemcpyAsync((void*)h->T.cum, table->cum, 4ull * table->n_rows * table->n_bins, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemcpyAsync(h->d_groups, groups, sizeof(Group) * n_groups, cudaMemcpyHostToDevice, h->stream));
@@ -341,6 +344,8 @@ extern "C" int jit_sched_load(jit_sched* h, const jit_pool* p) {
         CK(cudaMemcpyAsync(P.id, p->id, 4 * n, kind, h->stream));
         CK(cudaMemcpyAsync(P.task, p->task, 4 * n, kind, h->stream));
         CK(cudaMemcpyAsync(P.ovr, p->override_R, 4 * n, kind, h->stream));
+        if (p->fair) CK(cudaMemcpyAsync(P.fair, p->fair, 4 * n, kind, h->stream));
+        else CK(cudaMemsetAsync(P.fair, 0, 4 * n, h->stream));
     }
     if (nt) {
         CK(cudaMemcpyAsync(P.call_off, p->call_off, 4 * (nt + 1), kind, h->stream));
@@ -662,11 +667,12 @@ static int apply_deltas(jit_sched* h, const jit_step_in* in) {
     if (m > h->cfg.capacity) return set_err(h, JIT_ECAPACITY, "too many progress rows");
     std::vector<unsigned char>& hb = h->h_delta;
     HostPack pk{&hb};
-    uint64_t o_arr = 0, o_u[8] = {}, o_t[8] = {}, o_tu[4] = {}, o_pg[4] = {};
+    uint64_t o_arr = 0, o_u[8] = {}, o_t[8] = {}, o_tu[4] = {}, o_pg[4] = {}, o_fair = 0;
     if (na) {
         o_arr = pk.put(a->arrival_ns, na);
         const uint32_t* f[8] = {a->input_len, a->generated, a->prefilled, a->meta, a->aux, a->id, a->task, a->override_R};
         for (int i = 0; i < 8; ++i) o_u[i] = pk.put(f[i], na);
+        if (a->fair) o_fair = pk.put(a->fair, na);
     }
     if (nat) {
         o_t[0] = pk.put(a->call_off, nat + 1); o_t[1] = pk.put(a->task_arrival_ns, nat); o_t[2] = pk.put(a->task_deadline_ns, nat);
@@ -700,6 +706,7 @@ static int apply_deltas(jit_sched* h, const jit_step_in* in) {
         A.arr = reinterpret_cast<const int64_t*>(d + o_arr);
         const uint32_t** fu[8] = {&A.len_in, &A.gen, &A.pre, &A.meta, &A.aux, &A.id, &A.task, &A.ovr};
         for (int i = 0; i < 8; ++i) *fu[i] = reinterpret_cast<const uint32_t*>(d + o_u[i]);
+        A.fair = a->fair ? reinterpret_cast<const uint32_t*>(d + o_fair) : nullptr;
         if (nat) {
             A.call_off = reinterpret_cast<const uint32_t*>(d + o_t[0]);
             A.t_arr = reinterpret_cast<const int64_t*>(d + o_t[1]); A.t_dl = reinterpret_cast<const int64_t*>(d + o_t[2]);

@@ -73,6 +73,7 @@ struct Item {
 struct Pool {
     HotRow* rows;
     uint32_t *id, *task, *ovr;
+    uint32_t* fair;         // Fair(r) of the NEXT-2 blend (read only when it is on)
     uint64_t* img;          // materialized key images (exact path / debug): kNone when not pending
     uint32_t* cost;         // materialized token costs (0 when not pending)
     double* dbg_rate;       // optional debug outputs

@@ -46,7 +46,7 @@ template <bool kDebug>
 __device__ __forceinline__ void score_standalone(const Cfg& c, const Table& T, const GroupFast* sg, uint32_t n_groups,
                                                  const uint32_t* ovr, uint32_t row, int64_t now, int64_t v,
                                                  int64_t arr, uint32_t L_i, uint32_t g, uint32_t pre,
-                                                 uint32_t lhat, uint32_t meta, uint32_t aux, RowRes& o) {
+                                                 uint32_t lhat, uint32_t meta, uint32_t aux, uint32_t fair, RowRes& o) {
     o.img = kNone; o.cost = 0; o.meta = meta; o.lhat = lhat; o.aux = aux;
     o.pending = o.dropped = o.w_meta = o.w_lhat = o.err = false;
     if (kDebug) { o.rate = 0.0; o.trem = 0; o.lhatc = 0; }
@@ -82,6 +82,7 @@ __device__ __forceinline__ void score_standalone(const Cfg& c, const Table& T, c
     const uint64_t Gp = Gk + (uint64_t)c.delta * fastdiv(aux >> 16, c.frame, c.F_m, c.F_l);
     double key;
     if (!make_key(Gp, t_gen, c.eps, &key)) { o.err = true; return; }
+    if (c.fair_num) key = blend_fair(key, fair, c.fair_num, c.fair_den);   // NEXT-2 (A47)
     o.img = (uint64_t)__double_as_longlong(key);
     if (kDebug) { o.rate = make_rate(len_rem, trem); o.trem = trem; o.lhatc = Lh; }
 }
@@ -98,7 +99,7 @@ struct TraceMeta { uint32_t row_off, task_off, n_rows, n_tasks; };
 struct Spec { uint32_t trace, reserved; uint64_t load_num, load_den, slo_num, slo_den; };
 
 struct RLog { int64_t now_ns; uint32_t n_selected, total_tokens, n_candidates, b_star; double bp; uint64_t ids_hash;
-              int64_t v_token_ns; uint32_t n_preempted, pad; int64_t stall_ns; };
+              int64_t v_token_ns; uint32_t n_preempted, p_num; int64_t stall_ns; };
 
 struct RResult {
     unsigned long long token_goodput, tokens_processed;
@@ -108,7 +109,7 @@ struct RResult {
 
 struct ReplayArgs {
     const TraceMeta* traces;
-    const int64_t* arrival; const uint32_t *len_in, *true_out, *group, *dist_row, *ovr, *task;
+    const int64_t* arrival; const uint32_t *len_in, *true_out, *group, *dist_row, *ovr, *task, *fair;
     const int64_t *t_arr, *t_dl; const uint32_t* t_nst;
     const uint32_t* st_kind; const int64_t* st_exec; const uint32_t *st_pat, *st_cb, *st_ce;
     const Spec* specs;
@@ -117,7 +118,18 @@ struct ReplayArgs {
     Table T; const Group* groups; Cfg c;
     unsigned char* state; uint64_t state_stride;
     RResult* out; RLog* log;
+    uint32_t p_adapt, eps_num, eps_den, window_frames;   // NEXT-2 online p (A48)
+    uint64_t seed;
 };
+
+// NEXT-2 online p (A48): the arms p = kPGrid[a] / 100 and the counter-based draw
+__constant__ uint32_t kPGrid[4] = {80, 90, 95, 100};
+__device__ __forceinline__ uint64_t splitmix64_at(uint64_t x) {
+    uint64_t z = x * 0x9E3779B97F4A7C15ull + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
 
 // per-CTA state slice layout
 struct RState {
@@ -223,6 +235,9 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
     __shared__ bool s_stop;
     __shared__ uint32_t s_npre, s_gate_n;           // NEXT-1 gate: evictions this step / total; P+I count
     __shared__ unsigned long long s_stall;
+    __shared__ double s_p;                            // the cutoff p of this step (A48 adapts it)
+    __shared__ uint32_t s_pnum, s_arm, s_gcnt[4];
+    __shared__ unsigned long long s_gsum[4], s_gstart, s_window;
 
     const Cfg c = A.c;
     const Table T = A.T;
@@ -270,6 +285,10 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
             s_now = 0; s_steps = 0; s_ring_n = 0; s_ring_pos = 0; s_ring_sum = 0; s_stop = false;
             s_tguess = kNone;                              // no speculative threshold before the first step
             s_npre = 0; s_stall = 0;
+            s_arm = 0; s_gstart = 0; s_window = 0;
+            for (int a = 0; a < 4; ++a) { s_gcnt[a] = 0; s_gsum[a] = 0; }
+            s_pnum = A.p_adapt ? kPGrid[0] : c.pn;
+            s_p = A.p_adapt ? __ddiv_rn((double)kPGrid[0], 100.0) : c.p;
         }
         uint32_t n_preempted_total = 0;                    // (thread 0)
         __syncthreads();
@@ -343,7 +362,7 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                 if (m_flags(meta) & kCompound) continue;
                 RowRes o;
                 score_standalone<false>(c, T, sgf, A.n_groups, ovr, r, now, v, S.arr[r], L_in[r], S.gen[r], S.pre[r],
-                                        S.lhat[r], meta, S.aux[r], o);
+                                        S.lhat[r], meta, S.aux[r], A.fair ? A.fair[tm.row_off + r] : 0u, o);
                 S.img[r] = o.img; S.cost[r] = o.cost; S.aux[r] = o.aux;
                 if (o.w_meta) S.meta[r] = o.meta;
                 if (o.w_lhat) S.lhat[r] = o.lhat;
@@ -407,6 +426,7 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                     const uint64_t Gp = Gt + (uint64_t)c.delta * ((aux >> 16) / c.frame);
                     double key;
                     if (!make_key(Gp, t_gen, c.eps, &key)) my_err = 1;
+                    if (c.fair_num) key = blend_fair(key, A.fair ? A.fair[tm.row_off + r] : 0u, c.fair_num, c.fair_den);
                     S.img[r] = (uint64_t)__double_as_longlong(key);
                     S.cost[r] = token_cost(L_in[r], S.pre[r], c.chunk);
                     ++my_pend;
@@ -490,7 +510,7 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                     s_bstar = fits;
                     const double bp = __longlong_as_double((long long)ck_img(bA[fits - 1]));
                     s_bp = bp;
-                    s_thr = __dmul_rn(c.p, bp);
+                    s_thr = __dmul_rn(s_p, bp);
                     s_thr_img = (uint64_t)__double_as_longlong(s_thr);
                     // speculative attempt: exact iff the walk stopped inside S (or S = all pending)
                     // and Cd = {key >= thr} lies in S
@@ -732,7 +752,7 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                     RLog L;
                     L.now_ns = tnow; L.n_selected = nsel; L.total_tokens = s_tot; L.n_candidates = ncd;
                     L.b_star = s_bstar; L.bp = s_bp; L.ids_hash = h; L.v_token_ns = v;
-                    L.n_preempted = c.preempt ? s_npre : 0u; L.pad = 0; L.stall_ns = stall;
+                    L.n_preempted = c.preempt ? s_npre : 0u; L.p_num = s_pnum; L.stall_ns = stall;
                     A.log[(uint64_t)rep * A.log_steps + s_steps - 1] = L;
                 }
                 // v_token ring (Delta = frame_steps latencies)
@@ -773,6 +793,28 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                         S.cur[t] += 1; S.cb[t] = 0; S.ce[t] = 0; S.timer[t] = tnow;
                     }
                 }
+            }
+            __syncthreads();
+            // NEXT-2 online p (A48): at the end of a window its token goodput scores its arm; the
+            // next arm: an untried one in grid order, else explore (prob eps) or the best mean
+            if (A.p_adapt && threadIdx.x == 0 && s_steps % (A.window_frames * c.frame) == 0) {
+                const uint32_t a0 = s_arm;
+                s_gsum[a0] += s_good - s_gstart; s_gcnt[a0] += 1;
+                s_gstart = s_good;
+                s_window += 1;
+                uint32_t nxt = 4;
+                for (uint32_t a = 0; a < 4 && nxt == 4; ++a) if (s_gcnt[a] == 0) nxt = a;
+                if (nxt == 4) {
+                    const uint64_t u = splitmix64_at(A.seed + s_window);
+                    if (u % A.eps_den < A.eps_num) nxt = (uint32_t)((u >> 32) % 4u);
+                    else {
+                        nxt = 0;
+                        for (uint32_t a = 1; a < 4; ++a)
+                            if ((u128)s_gsum[a] * s_gcnt[nxt] > (u128)s_gsum[nxt] * s_gcnt[a]) nxt = a;
+                    }
+                }
+                s_arm = nxt; s_pnum = kPGrid[nxt];
+                s_p = __ddiv_rn((double)kPGrid[nxt], 100.0);
             }
             __syncthreads();
         }

@@ -703,6 +703,7 @@ __global__ void k_map_insert(Pool P, uint32_t r0, uint32_t r1, uint32_t* err) {
 // after rows n0 and tasks t0 of the resident pool
 struct Arrivals {
     const int64_t* arr; const uint32_t *len_in, *gen, *pre, *meta, *aux, *id, *task, *ovr;
+    const uint32_t* fair;       // NULL: 0
     const uint32_t* call_off; const int64_t *t_arr, *t_dl; const uint32_t *cur_stage, *n_stages, *pattern;
     const uint64_t* gdone;
     uint32_t n, n_single, n_tasks, n0, t0, pad;
@@ -720,6 +721,7 @@ __global__ void k_append(Pool P, Arrivals A) {
         P.id[r] = A.id[i];
         P.task[r] = A.task[i] == kNoTask ? kNoTask : A.t0 + A.task[i];
         P.ovr[r] = A.ovr[i];
+        P.fair[r] = A.fair ? A.fair[i] : 0u;
     }
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < A.n_tasks; t += stride) {
         const uint32_t g = A.t0 + t;

@@ -225,6 +225,7 @@ __device__ __forceinline__ void std_item(const Pool& P, const Table& T, const Gr
     const float v_f = (float)v, eps_f = (float)c.eps;
     const int64_t drop_before = now - c.waiting;           // now - arr > waiting <=> arr < now - waiting
     const uint32_t nr = it.r1 - it.r0;
+    const bool blend = c.fair_num != 0;                    // NEXT-2: no pre-test, exact keys blended
     HotRow q[kR];
     uint32_t pend_m = 0, rare_m = 0, drop_m = 0;
 #pragma unroll
@@ -274,7 +275,7 @@ __device__ __forceinline__ void std_item(const Pool& P, const Table& T, const Gr
         const uint64_t Gp = Gk + (uint64_t)c.delta * fastdiv(waited, c.frame, c.F_m, c.F_l);
         if (pend && Gp >= kTwo53 / 1000000000ull) A.err = 1;   // G' * 1e9 must stay an exact integer
         Gk32[k] = (uint32_t)Gp; Lr[k] = len_rem;
-        div_m |= (uint32_t)(pend && (kMat || !below_t((uint32_t)Gp, len_rem, v_f, eps_f, t_lo_f))) << k;
+        div_m |= (uint32_t)(pend && (kMat || blend || !below_t((uint32_t)Gp, len_rem, v_f, eps_f, t_lo_f))) << k;
         if (kDebug && 32 * k + lane < nr) {
             const uint32_t r = it.r0 + 32 * k + lane;
             P.dbg_rate[r] = pend ? make_rate(len_rem, trem) : 0.0;
@@ -291,6 +292,14 @@ __device__ __forceinline__ void std_item(const Pool& P, const Table& T, const Gr
             if ((div_m >> k) & 1u)
                 img[k] = (uint64_t)__double_as_longlong(div_rn_int(__dmul_rn(__uint2double_rn(Gk32[k]), 1e9),
                                                                    __fma_rn(__uint2double_rn(Lr[k]), v_d, eps_d)));
+        if (blend) {                                       // NEXT-2 fairness blend (A47), every pending row
+#pragma unroll
+            for (uint32_t k = 0; k < kR; ++k)
+                if ((div_m >> k) & 1u)
+                    img[k] = (uint64_t)__double_as_longlong(blend_fair(__longlong_as_double((long long)img[k]),
+                                                                       __ldg(P.fair + it.r0 + 32 * k + lane),
+                                                                       c.fair_num, c.fair_den));
+        }
     }
     A.pend += __popc(pend_m);
     uint32_t mem_m = 0;
@@ -494,7 +503,7 @@ __device__ __forceinline__ void cmp_item(const Pool& P, const Table& T, const Gr
             Bk[k] = Bd < 0.0 ? 1.0 : Bd;
             // the fp32 pre-test with B_f = fl(B) (relative error 2^-24, within below_t's margin)
             const bool below = __fmul_rn(__uint2float_rn((uint32_t)Gp), 1e9f) < __fmul_rn(t_lo_f, ts.Bf[j]);
-            div_m |= (uint32_t)(pend && (kMat || !below)) << k;
+            div_m |= (uint32_t)(pend && (kMat || c.fair_num || !below)) << k;
             if (kDebug && base + 32 * k + lane < it.r1) {
                 const uint32_t r = base + 32 * k + lane;
                 const HotRow x = row_at(r);
@@ -516,6 +525,14 @@ __device__ __forceinline__ void cmp_item(const Pool& P, const Table& T, const Gr
             for (uint32_t k = 0; k < kR; ++k)
                 if ((div_m >> k) & 1u)
                     img[k] = (uint64_t)__double_as_longlong(div_rn_int(__dmul_rn(__uint2double_rn(Gk32[k]), 1e9), Bk[k]));
+            if (c.fair_num) {                              // NEXT-2 fairness blend (A47)
+#pragma unroll
+                for (uint32_t k = 0; k < kR; ++k)
+                    if ((div_m >> k) & 1u)
+                        img[k] = (uint64_t)__double_as_longlong(blend_fair(__longlong_as_double((long long)img[k]),
+                                                                           __ldg(P.fair + base + 32 * k + lane),
+                                                                           c.fair_num, c.fair_den));
+            }
         }
         A.pend += __popc(pend_m);
         uint32_t mem_m = 0;

@@ -46,7 +46,7 @@ class jit_config(C.Structure):
                [("eps_ns", C.c_int64), ("waiting_ns", C.c_int64), ("capacity", C.c_uint32),
                 ("task_capacity", C.c_uint32), ("flags", C.c_uint32), ("device", C.c_int32), ("stream", C.c_void_p),
                 ("preempt", C.c_uint32), ("pmtn_num", C.c_uint32), ("pmtn_den", C.c_uint32), ("reserved2", C.c_uint32),
-                ("io_bw_tps", C.c_uint64)]
+                ("io_bw_tps", C.c_uint64), ("fair_num", C.c_uint32), ("fair_den", C.c_uint32)]
 
 
 _POOL_ROWS = (("id", np.uint32), ("arrival_ns", np.int64), ("input_len", np.uint32), ("generated", np.uint32),
@@ -59,7 +59,8 @@ _POOL_TASKS = (("call_off", np.uint32), ("task_arrival_ns", np.int64), ("task_de
 
 class jit_pool(C.Structure):
     _fields_ = [("n", C.c_uint32), ("n_single", C.c_uint32), ("n_tasks", C.c_uint32), ("on_device", C.c_int32)] + \
-               [(k, C.c_void_p) for k, _ in _POOL_ROWS] + [(k, C.c_void_p) for k, _ in _POOL_TASKS]
+               [(k, C.c_void_p) for k, _ in _POOL_ROWS] + [(k, C.c_void_p) for k, _ in _POOL_TASKS] + \
+               [("fair", C.c_void_p)]
 
 
 class jit_step_in(C.Structure):
@@ -86,7 +87,8 @@ _TRACE = (("arrival_ns", np.int64), ("input_len", np.uint32), ("true_out", np.ui
 
 
 class jit_trace(C.Structure):
-    _fields_ = [("n_rows", C.c_uint32), ("n_tasks", C.c_uint32)] + [(k, C.c_void_p) for k, _ in _TRACE]
+    _fields_ = [("n_rows", C.c_uint32), ("n_tasks", C.c_uint32)] + [(k, C.c_void_p) for k, _ in _TRACE] + \
+               [("fair", C.c_void_p)]
 
 
 class jit_replay_spec(C.Structure):
@@ -97,7 +99,8 @@ class jit_replay_spec(C.Structure):
 class jit_replay_cfg(C.Structure):
     _fields_ = [("n_steps", C.c_uint32), ("n_replays", C.c_uint32), ("log_steps", C.c_uint32),
                 ("reserved", C.c_uint32), ("v_token0_ns", C.c_int64), ("c0_ns", C.c_int64), ("c_att_ns", C.c_int64),
-                ("c_lin_ns", C.c_int64), ("specs", C.c_void_p)]
+                ("c_lin_ns", C.c_int64), ("specs", C.c_void_p), ("p_adapt", C.c_uint32), ("eps_num", C.c_uint32),
+                ("eps_den", C.c_uint32), ("window_frames", C.c_uint32), ("seed", C.c_uint64)]
 
 
 class jit_replay_result(C.Structure):
@@ -108,7 +111,7 @@ class jit_replay_result(C.Structure):
 
 STEP_LOG_DTYPE = np.dtype([("now_ns", "<i8"), ("n_selected", "<u4"), ("total_tokens", "<u4"),
                            ("n_candidates", "<u4"), ("b_star", "<u4"), ("bp", "<f8"), ("ids_hash", "<u8"),
-                           ("v_token_ns", "<i8"), ("n_preempted", "<u4"), ("reserved", "<u4"), ("stall_ns", "<i8")])
+                           ("v_token_ns", "<i8"), ("n_preempted", "<u4"), ("p_num", "<u4"), ("stall_ns", "<i8")])
 
 _lib = None
 EXPORTS = ("jit_sched_workspace_bytes", "jit_sched_init", "jit_sched_load", "jit_sched_step",
@@ -170,6 +173,8 @@ def make_config(cfg: dict, capacity: int, task_capacity: int, device: int = 0, s
     c.pmtn_num = int(cfg.get("pmtn_num", 1))
     c.pmtn_den = int(cfg.get("pmtn_den", 10))
     c.io_bw_tps = int(cfg.get("io_bw_tps", 10 ** 6))
+    c.fair_num = int(cfg.get("fair_num", 0))
+    c.fair_den = int(cfg.get("fair_den", 1))
     return c
 
 
@@ -249,6 +254,10 @@ class Scheduler:
             a = conv(pool[k], dt)
             keep.append(a)
             setattr(p, k, _p(a))
+        if pool.get("fair") is not None:               # NEXT-2 Fair(r) (A47)
+            a = conv(pool["fair"], np.uint32)
+            keep.append(a)
+            p.fair = _p(a)
         if tasks is not None and len(tasks["arrival_ns"]):
             tmap = {"task_arrival_ns": "arrival_ns", "task_deadline_ns": "deadline_ns"}
             p.n_tasks = len(tasks["arrival_ns"])
@@ -449,6 +458,10 @@ class Scheduler:
                     a = np.zeros(1, dt)
                 keep.append(a)
                 setattr(tarr[i], k, _p(a))
+            if tr.get("fair") is not None:
+                a = _c(tr["fair"], np.uint32)
+                keep.append(a)
+                tarr[i].fair = _p(a)
             tarr[i].n_rows = len(tr["input_len"])
             tarr[i].n_tasks = len(tr["task_arrival_ns"])
         sp = (jit_replay_spec * len(specs))()
@@ -462,6 +475,8 @@ class Scheduler:
         rc.log_steps = int(log_steps)
         for k in ("v_token0_ns", "c0_ns", "c_att_ns", "c_lin_ns"):
             setattr(rc, k, int(rcfg[k]))
+        for k, dflt in (("p_adapt", 0), ("eps_num", 1), ("eps_den", 10), ("window_frames", 100), ("seed", 0)):
+            setattr(rc, k, int(rcfg.get(k, dflt)))
         rc.specs = C.cast(sp, C.c_void_p)
         nbytes = C.c_uint64()
         self._check(self.lib.jit_replay_workspace_bytes(C.byref(self.c), tarr, C.c_uint32(len(traces)), C.byref(rc),
