@@ -29,7 +29,7 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-std=c11", "-fPIC", "-shared",
-                               "-o", tmp, _SRC])
+                               "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -274,3 +274,65 @@ def replay(cfg, groups, table, trace, rcfg, log: bool = False, log_ids: bool = F
     if log_ids:
         out["log_ids"] = LI.reshape(max(rc.n_steps, 1), int(cfg["max_batch"]))[:res.steps].copy()
     return out
+
+
+class _Patterns(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("_pad", C.c_uint32)] + \
+               [(k, C.c_void_p) for k in ("n_stages", "ident", "in_len", "out", "t_ms", "reuse")]
+
+
+class _Queries(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("_pad", C.c_uint32)] + [(k, C.c_void_p) for k in ("stage", "ident", "in_len", "out")]
+
+
+def _mk_patterns(store, keep):
+    P = _Patterns()
+    P.n = len(store["n_stages"])
+    for k in ("n_stages", "ident", "in_len", "out", "t_ms", "reuse"):
+        a = _arr(store[k], np.uint32)
+        keep.append(a)
+        setattr(P, k, _ptr(a))
+    return P
+
+
+def _mk_queries(queries, keep):
+    Q = _Queries()
+    Q.n = len(queries["stage"])
+    for k in ("stage", "ident", "in_len", "out"):
+        a = _arr(queries[k], np.uint32)
+        keep.append(a)
+        setattr(Q, k, _ptr(a))
+    return Q
+
+
+def kernel_sim(a: int, b: int) -> float:
+    """Gaussian-kernel similarity of two attributes (§4.1, sigma of S:250)."""
+    lib = _load()
+    lib.og_kernel_sim.restype = C.c_double
+    return float(lib.og_kernel_sim(C.c_uint32(a), C.c_uint32(b)))
+
+
+def match_scores(store, queries) -> np.ndarray:
+    """[n_queries, n_patterns] similarity scores (-1 = pruned), NEXT-3 (reading A49)."""
+    lib = _load()
+    lib.og_match_score.restype = C.c_double
+    keep = []
+    P = _mk_patterns(store, keep)
+    Q = _mk_queries(queries, keep)
+    out = np.zeros((Q.n, P.n), np.float64)
+    for q in range(Q.n):
+        for p in range(P.n):
+            out[q, p] = lib.og_match_score(C.byref(P), C.c_uint32(p), C.byref(Q), C.c_uint32(q))
+    return out
+
+
+def match(store, queries):
+    """Best stored pattern per query and its score (-1 / -1.0 = NoMatch), NEXT-3 (A49)."""
+    lib = _load()
+    keep = []
+    P = _mk_patterns(store, keep)
+    Q = _mk_queries(queries, keep)
+    best = np.zeros(max(Q.n, 1), np.int32)
+    score = np.zeros(max(Q.n, 1), np.float64)
+    lib.og_match(C.byref(P), C.byref(Q), _ptr(best), _ptr(score))
+    return best[:Q.n].copy(), score[:Q.n].copy()

@@ -26,6 +26,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <math.h>
 
 typedef unsigned __int128 u128;
 
@@ -981,4 +982,74 @@ done:
     free(cur); free(left); free(tdone); free(timer); free(ta); free(tD); free(gdone); free(cb); free(ce); free(tle); free(ttot);
     free(tever); free(tdrop);
     return ret;
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* NEXT-3: pattern-graph matching (§4.1; SPEC patterns S:160-263; reading A49). */
+/* A pattern graph is stage-structured (<= 8 stages, the pattern store of Fig. 6): stage u */
+/* has an identity (kind << 31 | model / tool id), an input-length attribute in_len (the   */
+/* edges into its LLM calls), a node attribute out (LLM output length, or the tool's       */
+/* execution time in ms) and its execution time t_u (ms).  A query is a task at stage s:   */
+/* identities of stages 0..s are revealed, stages 0..s-1 are complete.                     */
+/*  - prefix pruning ("prunes past patterns whose prefix structures diverge"): a     */
+/*    pattern survives iff it has > s stages and the identities of stages 0..s match;     */
+/*  - similarity: Gaussian kernels k(a,b) = exp(-(a-b)^2 / (2 sigma^2)),       */
+/*    sigma = max(0.25 max(a,b), 1), over the node attributes of stages 0..s-1 and  */
+/*    the input lengths of the LLM stages 1..s; the score is their arithmetic mean in      */
+/*    stage order, nodes first then edges per stage; no term -> score 1;           */
+/*  - the best pattern: the highest score, then the higher reuse count, then the lower    */
+/*    index; -1 when every pattern is pruned (NoMatch).                            */
+/* ------------------------------------------------------------------------------------ */
+typedef struct {
+    uint32_t n, _pad;
+    const uint32_t* n_stages;     /* [n] */
+    const uint32_t* ident;        /* [n*8] kind << 31 | id */
+    const uint32_t* in_len;       /* [n*8] */
+    const uint32_t* out;          /* [n*8] */
+    const uint32_t* t_ms;         /* [n*8] */
+    const uint32_t* reuse;        /* [n] */
+} og_patterns;
+
+typedef struct {
+    uint32_t n, _pad;
+    const uint32_t* stage;        /* [n] revealed stage s */
+    const uint32_t* ident;        /* [n*8] */
+    const uint32_t* in_len;       /* [n*8] */
+    const uint32_t* out;          /* [n*8] */
+} og_queries;
+
+double og_kernel_sim(uint32_t a, uint32_t b) {
+    double mx = (double)(a > b ? a : b);
+    double sigma = 0.25 * mx;
+    if (sigma < 1.0) sigma = 1.0;
+    double d = (double)a - (double)b;
+    return exp(-(d * d) / (2.0 * sigma * sigma));
+}
+
+/* the score of pattern p for query q, or -1 when pruned */
+double og_match_score(const og_patterns* P, uint32_t p, const og_queries* Q, uint32_t q) {
+    uint32_t s = Q->stage[q];
+    if (s >= MAX_STAGES || P->n_stages[p] <= s) return -1.0;
+    for (uint32_t u = 0; u <= s; ++u)
+        if (P->ident[p * MAX_STAGES + u] != Q->ident[q * MAX_STAGES + u]) return -1.0;
+    double sum = 0.0; uint32_t cnt = 0;
+    for (uint32_t u = 0; u <= s; ++u) {
+        uint32_t id = Q->ident[q * MAX_STAGES + u];
+        if (u < s) { sum += og_kernel_sim(Q->out[q * MAX_STAGES + u], P->out[p * MAX_STAGES + u]); ++cnt; }
+        if (u >= 1 && !(id >> 31)) { sum += og_kernel_sim(Q->in_len[q * MAX_STAGES + u], P->in_len[p * MAX_STAGES + u]); ++cnt; }
+    }
+    return cnt ? sum / (double)cnt : 1.0;
+}
+
+int og_match(const og_patterns* P, const og_queries* Q, int32_t* best, double* score) {
+    for (uint32_t q = 0; q < Q->n; ++q) {
+        int32_t b = -1; double bs = -1.0;
+        for (uint32_t p = 0; p < P->n; ++p) {
+            double sc = og_match_score(P, p, Q, q);
+            if (sc < 0.0) continue;
+            if (b < 0 || sc > bs || (sc == bs && P->reuse[p] > P->reuse[b])) { b = (int32_t)p; bs = sc; }
+        }
+        best[q] = b; score[q] = bs;
+    }
+    return OG_OK;
 }

@@ -549,3 +549,75 @@ def edf_adversary(T: int = 10, N: int = 9, M: int = 100, v_ns: int = 10 * MS) ->
     rcfg = dict(n_steps=1000, v_token0_ns=v_ns, c0_ns=v_ns, c_att_ns=0, c_lin_ns=0,
                 load_num=1, load_den=1, slo_num=1, slo_den=1)
     return {"trace": tr, "groups": groups, "table": table, "cfg": cfg, "rcfg": rcfg}
+
+
+# ----------------------------------------------------------------------------------------
+# NEXT-3 pattern graphs (§4.1): a store of ~500 stage-structured graphs drawn from
+# families (deep-research / agentic shapes: LLM plan -> tool -> LLM fan-out -> ... -> LLM
+# summary), and queries = fresh instances revealed up to a random stage.
+# ----------------------------------------------------------------------------------------
+
+TOOL = 1 << 31
+
+
+def _pattern_families(rng, n_families):
+    fams = []
+    for f in range(n_families):
+        S = int(rng.integers(2, MAX_STAGES + 1))
+        ident, base_in, base_out, base_t = [], [], [], []
+        for u in range(S):
+            tool = u % 2 == 1 and rng.random() < 0.7
+            ident.append((TOOL | int(rng.integers(0, 6))) if tool else int(rng.integers(0, 4)))
+            base_in.append(0 if tool else int(rng.lognormal(np.log(800), 0.8)))
+            base_out.append(int(rng.lognormal(np.log(300 if tool else 250), 0.7)))   # tool: exec ms
+            base_t.append(int(rng.lognormal(np.log(1500), 0.8)))
+        fams.append((S, ident, base_in, base_out, base_t))
+    return fams
+
+
+def _instance(rng, fam, noise=0.3, swap=0.15):
+    S, ident, bi, bo, bt = fam
+    ident = list(ident)
+    if rng.random() < swap:                       # a divergent branch of the family
+        u = int(rng.integers(0, S))
+        ident[u] = (ident[u] & TOOL) | int(rng.integers(0, 6 if ident[u] & TOOL else 4))
+    jit = lambda x: max(1, int(round(x * rng.lognormal(0.0, noise)))) if x else 0
+    return S, ident, [jit(x) for x in bi], [jit(x) for x in bo], [jit(x) for x in bt]
+
+
+def pattern_store(seed: int = 61, n_patterns: int = 500, n_families: int = 24) -> dict:
+    rng = rng_for(seed)
+    fams = _pattern_families(rng, n_families)
+    st = {k: np.zeros((n_patterns, MAX_STAGES), np.uint32) for k in ("ident", "in_len", "out", "t_ms")}
+    st["n_stages"] = np.zeros(n_patterns, np.uint32)
+    for p in range(n_patterns):
+        S, ident, i_, o_, t_ = _instance(rng, fams[int(rng.integers(0, n_families))])
+        st["n_stages"][p] = S
+        for u in range(S):
+            st["ident"][p, u], st["in_len"][p, u], st["out"][p, u], st["t_ms"][p, u] = ident[u], i_[u], o_[u], t_[u]
+    st["reuse"] = rng.integers(1, 60, n_patterns).astype(np.uint32)
+    st["families"] = fams
+    return st
+
+
+def pattern_queries(seed: int, store: dict, n_queries: int, foreign: float = 0.05) -> dict:
+    """fresh instances of the store's families (a few of unknown families: NoMatch), revealed up
+    to a random stage s: identities and input lengths of stages 0..s, outputs of stages 0..s-1"""
+    rng = rng_for(seed)
+    fams = store["families"]
+    other = _pattern_families(rng, 4)
+    q = {k: np.zeros((n_queries, MAX_STAGES), np.uint32) for k in ("ident", "in_len", "out")}
+    q["stage"] = np.zeros(n_queries, np.uint32)
+    q["true_t_ms"] = np.zeros((n_queries, MAX_STAGES), np.uint32)
+    for i in range(n_queries):
+        fam = other[int(rng.integers(0, 4))] if rng.random() < foreign else fams[int(rng.integers(0, len(fams)))]
+        S, ident, i_, o_, t_ = _instance(rng, fam)
+        s = int(rng.integers(0, S))
+        q["stage"][i] = s
+        for u in range(S):
+            if u <= s:
+                q["ident"][i, u], q["in_len"][i, u] = ident[u], i_[u]
+            if u < s:
+                q["out"][i, u] = o_[u]
+            q["true_t_ms"][i, u] = t_[u]
+    return q
