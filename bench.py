@@ -473,6 +473,96 @@ def config_lines(args, dev, stream, Scheduler):
     return out
 
 
+def next_lines(args, dev, stream, Scheduler):
+    """SURVEY 8(f) rows built this round, each measured beside the oracle:
+    NEXT-1 preemption gate (C5 replays), NEXT-2 fairness blend (C3 k_score) and online p
+    (C5 replays), NEXT-3 pattern matching (C4-scale queries x a 500-graph store)."""
+    import torch
+    import oracle
+    out = {}
+    # ---- NEXT-1 / NEXT-2 in the replay: a slice of the C5 sweep with the gate, with online p
+    traces = [W.trace_mixed(k) for k in range(3)]
+    d = traces[0]
+    sweep = W.c5_sweep()
+    specs = [dict(sweep[i], trace=i % 3) for i in range(0, 4096, 16)]        # 256 sweep points
+    variants = {"plain": (d["cfg"], d["rcfg"]),
+                "gate": (dict(d["cfg"], preempt=1), d["rcfg"]),
+                "online_p": (d["cfg"], dict(d["rcfg"], p_adapt=1, eps_num=1, eps_den=10, window_frames=4, seed=1))}
+    for name, (cfg, rc) in variants.items():
+        rs = Scheduler(cfg, d["groups"], d["table"], capacity=4096, task_capacity=1024, device=dev, stream=stream)
+        rs.replay([t["trace"] for t in traces], specs[:8], rc)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res, _ = rs.replay([t["trace"] for t in traces], specs, rc)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        rs.close()
+        steps = sum(int(r["steps"]) for r in res)
+        # the oracle on a bounded sample (4 replays), to check and to time
+        t0 = time.perf_counter()
+        same, osteps = True, 0
+        for j in range(4):
+            sp = specs[j * 64]
+            rcj = dict(rc, **{k: sp[k] for k in ("load_num", "load_den", "slo_num", "slo_den")})
+            t = traces[sp["trace"]]
+            ref = oracle.replay(cfg, t["groups"], t["table"], t["trace"], rcj)
+            same &= all(int(res[j * 64][k]) == int(ref[k]) for k in ("token_goodput", "steps", "sim_end_ns"))
+            osteps += ref["steps"]
+        tc = time.perf_counter() - t0
+        out[f"replay_{name}"] = {
+            "metric": "replayed serving steps/sec (C5 sweep slice)", "value": steps / (ms / 1e3), "unit": "steps/s",
+            "replays": len(specs), "token_goodput_sum": int(sum(int(r["token_goodput"]) for r in res)),
+            "n_preempted_sum": int(sum(int(r["n_preempted"]) for r in res)), "equal_to_oracle_sample": bool(same),
+            "cpu_baseline": {"value": osteps / tc, "unit": "steps/s", "cores": 1, "kind": "oracle",
+                             "sample": "4 of the replays on 1 core"},
+            "workload": "C5(i) slice: 256 (load, SLO-scale) points x 4096 steps of 2048-row mixed traces"}
+    # ---- NEXT-2 blend in the pool step: k_score over C3 with f = 1/10 (every pending row keyed exactly)
+    dd = W.pool_snapshot(3, 1 << 20)
+    rng = np.random.default_rng(3)
+    pool = dict(dd["pool"], fair=rng.integers(0, 400, len(dd["pool"]["id"])).astype(np.uint32))
+    hs = []
+    for _ in range(6):
+        sb = Scheduler(dict(dd["cfg"], fair_num=1, fair_den=10), dd["groups"], dd["table"], capacity=len(pool["id"]),
+                       task_capacity=len(dd["tasks"]["arrival_ns"]), device=dev, stream=stream)
+        sb.load(pool, dd["tasks"])
+        for _ in range(3):
+            sb.step(dd["now_ns"], dd["v_token_ns"])
+        hs.append(sb)
+    k_ms = Scheduler.time_scoring(hs, dd["now_ns"], dd["v_token_ns"], 30)
+    for sb in hs:
+        sb.close()
+    out["blend_k_score"] = {"metric": "k_score ms per 2^20-row C3 pool with the fairness blend (f = 1/10)",
+                            "value": k_ms, "unit": "ms", "alg_bytes": alg_bytes(dd) + 4 * len(pool["id"]),
+                            "note": "the blend needs every pending key exactly (no fp32 pre-test) plus Fair(r)"}
+    # ---- NEXT-3: pattern matching, C4-scale
+    store = W.pattern_store(61, n_patterns=500)
+    q = W.pattern_queries(62, store, 100_000)
+    ms_ = Scheduler(dd["cfg"], dd["groups"], dd["table"], capacity=64, task_capacity=8, device=dev, stream=stream)
+    ms_.match(store, q)
+    kms = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        best, score = ms_.match(store, q)
+        wall = (time.perf_counter() - t0) * 1e3
+        kms.append(ms_.last_match_ms())
+    ms_.close()
+    sub = {k: v[:200] for k, v in q.items()}
+    t0 = time.perf_counter()
+    ob, _ = oracle.match(store, sub)
+    tc = time.perf_counter() - t0
+    out["match"] = {"metric": "compound tasks matched/sec (500-graph store)", "value": 100_000 / (np.median(kms) / 1e3),
+                    "unit": "queries/s", "kernel_ms": float(np.median(kms)), "call_ms_wall": wall,
+                    "pairs_per_s": 100_000 * 500 / (np.median(kms) / 1e3),
+                    "agree_with_oracle_sample": float((ob == best[:200]).mean()),
+                    "cpu_baseline": {"value": 200 / tc, "unit": "queries/s", "cores": 1, "kind": "oracle",
+                                     "sample": "200 queries x 500 graphs on 1 core"},
+                    "workload": "100K queries (C4's task count) revealed at random stages, 500 stored graphs "
+                                "from 24 families"}
+    return out
+
+
 # ------------------------------------------------------------------------------------------
 # N = 1: the C3 step
 # ------------------------------------------------------------------------------------------
@@ -578,6 +668,8 @@ def run_single(args, dev, stream):
     e2e = e2e_leg(args, d, dev, stream, Scheduler)
     e2e["full_reload"] = full_reload_e2e(d, dev, stream, Scheduler)
     configs = None if args.no_configs else config_lines(args, dev, stream, Scheduler)
+    if configs is not None:
+        configs["next"] = next_lines(args, dev, stream, Scheduler)
     replay = None if args.no_replay else replay_leg(args, 1, 0, dev, stream, lambda: None, lambda x: x, lambda x: x,
                                                     cpu=not args.no_cpu)
     cpu = None

@@ -335,6 +335,51 @@ int jit_sched_replay(jit_sched* h, const jit_trace* traces, uint32_t n_traces, c
                      void* dev_workspace, uint64_t ws_bytes, jit_replay_result* out, jit_step_log* log);
 
 /* ---------------------------------------------------------------------------------------
+ * NEXT-3: pattern-graph matching (§4.1; reading A49).  A stored pattern graph is
+ * stage-structured (<= JIT_MAX_STAGES stages): per stage an identity (kind << 31 | model or
+ * tool id, kind 1 = tool), an input-length attribute (edges into its LLM calls), a node
+ * attribute (LLM output length, or tool execution time in ms) and the stage time t_u in ms.
+ * A query is a compound task revealed up to stage s: identities and input lengths of stages
+ * 0..s, node attributes of stages 0..s-1.  Patterns whose identities differ on stages 0..s (or
+ * with <= s stages) are pruned; the rest score the mean of Gaussian-kernel similarities
+ * exp(-(a-b)^2 / (2 sigma^2)), sigma = max(0.25 max(a,b), 1), over those attributes;
+ * the best is (score desc, reuse desc, index asc); -1 / -1.0 when everything is pruned.
+ * All arrays are host arrays, row-major [n][8] for per-stage fields.
+ * --------------------------------------------------------------------------------------- */
+typedef struct jit_pattern_store {
+    uint32_t n_patterns, reserved;
+    const uint32_t* n_stages;      /* [n] 1..8 */
+    const uint32_t* ident;         /* [n*8] */
+    const uint32_t* in_len;        /* [n*8] */
+    const uint32_t* out;           /* [n*8] */
+    const uint32_t* t_ms;          /* [n*8] stage times (phi); sum > 0 */
+    const uint32_t* reuse;         /* [n] reuse count (tie-break) */
+} jit_pattern_store;
+
+typedef struct jit_match_query {
+    uint32_t n, reserved;
+    const uint32_t* stage;         /* [n] revealed stage s */
+    const uint32_t* ident;         /* [n*8] */
+    const uint32_t* in_len;        /* [n*8] */
+    const uint32_t* out;           /* [n*8] (stages < s) */
+    const uint32_t* task;          /* [n] resident task index (apply), or NULL */
+} jit_match_query;
+
+/* Device workspace for one jit_sched_match call. */
+int jit_match_workspace_bytes(uint32_t n_patterns, uint32_t n_queries, uint64_t* bytes);
+
+/* Match every query against the store on h's device (one warp per query).  best / score: host
+ * arrays of q->n.  apply = 1: each matched query's task in the resident pool takes the pattern's
+ * stage count and stage times (phi(s) = t_<=s / t_total, D_s = phi(s) D) -- the query's
+ * stage must be the task's current stage (JIT_EINVAL otherwise).  JIT_EINVAL on a malformed
+ * pattern (0 or > 8 stages, zero total time). */
+int jit_sched_match(jit_sched* h, const jit_pattern_store* store, const jit_match_query* q, void* dev_workspace,
+                    uint64_t ws_bytes, int32_t* best, double* score, uint32_t apply);
+
+/* Device time (CUDA events on h's stream) of the matching kernel of the last jit_sched_match. */
+int jit_sched_last_match_ms(jit_sched* h, float* ms);
+
+/* ---------------------------------------------------------------------------------------
  * Exact sharded step over W ranks (north_star "pool sharded by request id ... NCCL allgather
  * of candidates followed by a global merge").  Each rank loads its shard (ids
  * unique across ranks) and calls, in order, with the caller allgathering in between:

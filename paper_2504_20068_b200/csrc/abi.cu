@@ -11,6 +11,7 @@
 #include "jit_sched.h"
 #include "common.cuh"
 #include "select.cuh"
+#include "match.cuh"
 #include "stream.cuh"
 #include "replay.cuh"
 #include "shard.cuh"
@@ -49,6 +50,7 @@ struct jit_sched {
     int arg_mode = 0;
     int64_t arg_now = 0, arg_v = 0;
     bool loaded = false, graph_dirty = true, timing = false, debug = false, pdl = true;
+    float match_ms = 0.f;             // device time of the last k_match (jit_sched_last_match_ms)
     bool keys_ready = false;          // k_score already ran this step (fast sharded attempt)
     bool unfinished = false;          // a step was launched and not finished (step_async)
     uint64_t launched = 0;            // steps launched (the stamp rebase runs every 2^30)
@@ -1081,4 +1083,104 @@ extern "C" int jit_shard_finish(jit_sched* h, const void* d_all_rec2, uint32_t n
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(h->h_ctrl, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
     return finish_step(h, out);
+}
+
+// ------------------------------------------------------------------------------------------
+// NEXT-3: batch pattern-graph matching (match.cuh)
+// ------------------------------------------------------------------------------------------
+static uint64_t match_layout(uint32_t np, uint32_t nq, uint64_t* off) {
+    uint64_t o = 0;
+    auto take = [&](uint64_t b) { o = (o + 255) & ~255ull; const uint64_t r = o; o += b; return r; };
+    off[0] = take(4ull * np * (4 * kMaxStages + 2));            // patterns: ident, in, out, t_ms, n_stages, reuse
+    off[1] = take(4ull * nq * (3 * kMaxStages + 2));            // queries: ident, in, out, stage, task
+    off[2] = take(4ull * nq);                                   // best
+    off[3] = take(8ull * nq);                                   // score
+    return o + 256;
+}
+
+extern "C" int jit_match_workspace_bytes(uint32_t n_patterns, uint32_t n_queries, uint64_t* bytes) {
+    if (!bytes) return JIT_EINVAL;
+    uint64_t off[4];
+    *bytes = match_layout(n_patterns, n_queries, off);
+    return JIT_OK;
+}
+
+extern "C" int jit_sched_match(jit_sched* h, const jit_pattern_store* st, const jit_match_query* q, void* dev_workspace,
+                               uint64_t ws_bytes, int32_t* best, double* score, uint32_t apply) {
+    if (!h) return JIT_EINVAL;
+    if (!st || !q || !best || !score || !st->n_stages || !st->ident || !st->in_len || !st->out || !st->t_ms ||
+        !st->reuse || (q->n && (!q->stage || !q->ident || !q->in_len || !q->out)))
+        return set_err(h, JIT_EINVAL, "match: null arrays");
+    if (apply && !q->task) return set_err(h, JIT_EINVAL, "match: apply needs query task indices");
+    const uint32_t np = st->n_patterns, nq = q->n;
+    for (uint32_t p = 0; p < np; ++p) {                          // a pattern must define phi
+        const uint32_t S = st->n_stages[p];
+        uint64_t tot = 0;
+        for (uint32_t u = 0; u < S && u < kMaxStages; ++u) tot += st->t_ms[(uint64_t)p * kMaxStages + u];
+        if (S == 0 || S > kMaxStages || tot == 0) return set_err(h, JIT_EINVAL, "match: pattern %u malformed", p);
+    }
+    if (nq == 0) return JIT_OK;
+    uint64_t off[4];
+    const uint64_t need = match_layout(np, nq, off);
+    if (!dev_workspace || ws_bytes < need) return set_err(h, JIT_ECAPACITY, "match workspace too small");
+    unsigned char* base = reinterpret_cast<unsigned char*>(((uintptr_t)dev_workspace + 255) & ~(uintptr_t)255);
+    cudaStream_t s = h->stream;
+    uint32_t* pw = reinterpret_cast<uint32_t*>(base + off[0]);
+    uint32_t* qw = reinterpret_cast<uint32_t*>(base + off[1]);
+    const uint64_t P8 = (uint64_t)np * kMaxStages, Q8 = (uint64_t)nq * kMaxStages;
+    if (np) {
+        CK(cudaMemcpyAsync(pw, st->ident, 4 * P8, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(pw + P8, st->in_len, 4 * P8, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(pw + 2 * P8, st->out, 4 * P8, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(pw + 3 * P8, st->t_ms, 4 * P8, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(pw + 4 * P8, st->n_stages, 4ull * np, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(pw + 4 * P8 + np, st->reuse, 4ull * np, cudaMemcpyHostToDevice, s));
+    }
+    CK(cudaMemcpyAsync(qw, q->ident, 4 * Q8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(qw + Q8, q->in_len, 4 * Q8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(qw + 2 * Q8, q->out, 4 * Q8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(qw + 3 * Q8, q->stage, 4ull * nq, cudaMemcpyHostToDevice, s));
+    if (q->task) CK(cudaMemcpyAsync(qw + 3 * Q8 + nq, q->task, 4ull * nq, cudaMemcpyHostToDevice, s));
+    PatternsDev G{pw + 4 * P8, pw, pw + P8, pw + 2 * P8, pw + 3 * P8, pw + 4 * P8 + np, np};
+    QueriesDev Q{qw + 3 * Q8, qw, qw + Q8, qw + 2 * Q8, q->task ? qw + 3 * Q8 + nq : nullptr, nq};
+    int32_t* d_best = reinterpret_cast<int32_t*>(base + off[2]);
+    double* d_score = reinterpret_cast<double*>(base + off[3]);
+    const uint32_t staged = np <= kMatchSmemPatterns ? 1u : 0u;
+    const uint32_t smem = staged ? 4u * np * kMatchWords : 0u;
+    CK(cudaFuncSetAttribute(k_match, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4u * kMatchSmemPatterns * kMatchWords)));
+    const uint32_t warps_per_cta = kMatchThreads / 32;
+    const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((nq + warps_per_cta - 1) / warps_per_cta,
+                                                                   (uint32_t)h->n_sm * 2));
+    cudaEvent_t ev[2];
+    CK(cudaEventCreate(&ev[0])); CK(cudaEventCreate(&ev[1]));
+    CK(cudaEventRecord(ev[0], s));
+    k_match<<<grid, kMatchThreads, smem, s>>>(G, Q, d_best, d_score, staged);
+    CK(cudaEventRecord(ev[1], s));
+    CK(cudaGetLastError());
+    if (apply) {
+        uint32_t* err = &h->S.gpart->err;
+        k_apply_match<<<(nq + 255) / 256, 256, 0, s>>>(h->P, G, Q, d_best, err);
+        if (h->P.n_tasks) k_task_prep<<<std::max<uint32_t>(1, std::min<uint32_t>((h->P.n_tasks + 255) / 256, (uint32_t)h->n_sm * 8)), 256, 0, s>>>(h->P, 0u);
+        CK(cudaGetLastError());
+    }
+    CK(cudaMemcpyAsync(best, d_best, 4ull * nq, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(score, d_score, 8ull * nq, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaEventElapsedTime(&h->match_ms, ev[0], ev[1]));
+    cudaEventDestroy(ev[0]); cudaEventDestroy(ev[1]);
+    if (apply) {
+        uint32_t e = 0;
+        CK(cudaMemcpy(&e, &h->S.gpart->err, 4, cudaMemcpyDeviceToHost));
+        if (e & 16u) {
+            CK(cudaMemset(&h->S.gpart->err, 0, 4));
+            return set_err(h, JIT_EINVAL, "match: a query's stage is not its task's current stage");
+        }
+    }
+    return JIT_OK;
+}
+
+extern "C" int jit_sched_last_match_ms(jit_sched* h, float* ms) {
+    if (!h || !ms) return JIT_EINVAL;
+    *ms = h->match_ms;
+    return JIT_OK;
 }

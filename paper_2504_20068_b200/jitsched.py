@@ -91,6 +91,16 @@ class jit_trace(C.Structure):
                [("fair", C.c_void_p)]
 
 
+class jit_pattern_store(C.Structure):
+    _fields_ = [("n_patterns", C.c_uint32), ("reserved", C.c_uint32)] + \
+               [(k, C.c_void_p) for k in ("n_stages", "ident", "in_len", "out", "t_ms", "reuse")]
+
+
+class jit_match_query(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("reserved", C.c_uint32)] + \
+               [(k, C.c_void_p) for k in ("stage", "ident", "in_len", "out", "task")]
+
+
 class jit_replay_spec(C.Structure):
     _fields_ = [("trace", C.c_uint32), ("reserved", C.c_uint32), ("load_num", C.c_uint64), ("load_den", C.c_uint64),
                 ("slo_num", C.c_uint64), ("slo_den", C.c_uint64)]
@@ -120,7 +130,8 @@ EXPORTS = ("jit_sched_workspace_bytes", "jit_sched_init", "jit_sched_load", "jit
            "jit_sched_version", "jit_shard_prefix", "jit_shard_merge", "jit_shard_candidates", "jit_shard_finish",
            "jit_sched_phase_times", "jit_shard_spec_bytes", "jit_shard_spec_export", "jit_shard_spec_resolve",
            "jit_sched_time_scoring", "jit_sched_counters", "jit_sched_debug_scratch",
-           "jit_sched_debug_set_counter")
+           "jit_sched_debug_set_counter", "jit_match_workspace_bytes", "jit_sched_match",
+           "jit_sched_last_match_ms")
 
 
 def load_library(path: str = LIB_PATH):
@@ -367,6 +378,39 @@ class Scheduler:
         a, b, c = C.c_uint32(), C.c_uint32(), C.c_uint32()
         self._check(self.lib.jit_sched_counters(self.h, C.byref(a), C.byref(b), C.byref(c)), self.h)
         return {"steps": a.value, "fallbacks": b.value, "skipped": c.value}
+
+    def match(self, store: dict, queries: dict, apply: bool = False):
+        """NEXT-3 pattern-graph matching on the GPU (jit_sched_match): best pattern index and score
+        per query; apply=True writes the matched stage structure into the queries' resident tasks
+        (queries["task"])."""
+        torch = _torch()
+        keep = []
+        st = jit_pattern_store()
+        st.n_patterns = len(store["n_stages"])
+        for k in ("n_stages", "ident", "in_len", "out", "t_ms", "reuse"):
+            a = _c(store[k], np.uint32)
+            keep.append(a)
+            setattr(st, k, _p(a))
+        q = jit_match_query()
+        q.n = len(queries["stage"])
+        for k in ("stage", "ident", "in_len", "out") + (("task",) if apply else ()):
+            a = _c(queries[k], np.uint32)
+            keep.append(a)
+            setattr(q, k, _p(a))
+        nb = C.c_uint64()
+        self._check(self.lib.jit_match_workspace_bytes(C.c_uint32(st.n_patterns), C.c_uint32(q.n), C.byref(nb)), self.h)
+        ws = torch.empty(int(nb.value) + 256, dtype=torch.uint8, device=f"cuda:{self.device}")
+        best = np.zeros(max(q.n, 1), np.int32)
+        score = np.zeros(max(q.n, 1), np.float64)
+        self._check(self.lib.jit_sched_match(self.h, C.byref(st), C.byref(q), C.c_void_p(ws.data_ptr()),
+                                             C.c_uint64(ws.numel()), _p(best), _p(score), C.c_uint32(1 if apply else 0)),
+                    self.h)
+        return best[:q.n].copy(), score[:q.n].copy()
+
+    def last_match_ms(self) -> float:
+        ms = C.c_float()
+        self._check(self.lib.jit_sched_last_match_ms(self.h, C.byref(ms)), self.h)
+        return float(ms.value)
 
     def debug_set_counter(self, steps: int, launched: int):
         """Tests: move the device step counter (stamps move with it) and the launch count."""
