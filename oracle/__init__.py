@@ -49,9 +49,28 @@ class _Config(C.Structure):
                [(k, C.c_uint32) for k in ("fair_num", "fair_den")]
 
 
+class _Forest(C.Structure):
+    _fields_ = [(k, C.c_uint32) for k in ("n_trees", "n_nodes", "n_samples", "n_features")] + \
+               [(k, C.c_void_p) for k in ("root", "feature", "threshold", "left", "right", "samples")]
+
+
 class _Table(C.Structure):
     _fields_ = [("n_rows", C.c_uint32), ("n_bins", C.c_uint32), ("l_max", C.c_uint32), ("_pad", C.c_uint32),
-                ("edges", C.c_void_p), ("cum", C.c_void_p)]
+                ("edges", C.c_void_p), ("cum", C.c_void_p), ("forest", C.c_void_p)]
+
+
+def _mk_forest(forest, keep):
+    F = _Forest()
+    F.n_trees, F.n_nodes = len(forest["root"]), len(forest["feature"])
+    F.n_samples, F.n_features = len(forest["samples"]), 4
+    for k in ("root", "feature", "threshold", "left", "right", "samples"):
+        a = _arr(forest[k], np.uint32)
+        if a.size == 0:
+            a = np.zeros(1, np.uint32)
+        keep.append(a)
+        setattr(F, k, _ptr(a))
+    keep.append(F)
+    return F
 
 
 class _Pool(C.Structure):
@@ -150,6 +169,9 @@ def _mk_table(table, keep):
     t.l_max = int(table["l_max"])
     t.edges = _ptr(edges)
     t.cum = _ptr(cum)
+    if table.get("forest") is not None:          # NEXT-4: (a2) from the QRF (A50)
+        F = _mk_forest(table["forest"], keep)
+        t.forest = C.cast(C.pointer(F), C.c_void_p)
     return t
 
 
@@ -336,3 +358,14 @@ def match(store, queries):
     score = np.zeros(max(Q.n, 1), np.float64)
     lib.og_match(C.byref(P), C.byref(Q), _ptr(best), _ptr(score))
     return best[:Q.n].copy(), score[:Q.n].copy()
+
+
+def qrf_quantile(forest, x, anchor: int, q_num: int, q_den: int, l_max: int) -> int:
+    """NEXT-4 (A50): Q_q of the pooled leaf samples above `anchor` for features x (4 ints)."""
+    lib = _load()
+    lib.og_qrf_quantile.restype = C.c_uint32
+    keep = []
+    F = _mk_forest(forest, keep)
+    xa = _arr(np.asarray(x), np.uint32)
+    return int(lib.og_qrf_quantile(C.byref(F), _ptr(xa), C.c_uint32(anchor), C.c_uint32(q_num), C.c_uint32(q_den),
+                                   C.c_uint32(l_max)))

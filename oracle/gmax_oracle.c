@@ -58,10 +58,26 @@ typedef struct {
     uint32_t fair_num, fair_den;
 } og_config;
 
+/* NEXT-4: a quantile regression forest (§4.1; SPEC estimator S:92-158; reading A50).
+ * Nodes of all trees in one array: an inner node sends x to `left` iff x[feature] <= threshold,
+ * else to `right`; a leaf (feature = OG_LEAF) holds samples[threshold .. threshold + left), its
+ * training targets.  Features: x = (L_i, dist_row, anchor R*floor(g/R), SLO group). */
+#define OG_LEAF 0xFFFFFFFFu
+typedef struct {
+    uint32_t n_trees, n_nodes, n_samples, n_features;
+    const uint32_t* root;
+    const uint32_t* feature;
+    const uint32_t* threshold;
+    const uint32_t* left;
+    const uint32_t* right;
+    const uint32_t* samples;
+} og_forest;
+
 typedef struct {
     uint32_t n_rows, n_bins, l_max, _pad;
     const uint32_t* edges;
     const uint32_t* cum;
+    const og_forest* forest;   /* NULL: the table; else (a2) queries the forest (NEXT-4, A50) */
 } og_table;
 
 typedef struct {
@@ -163,6 +179,42 @@ static uint32_t cond_quantile(const og_table* T, uint32_t row, uint32_t anchor,
         return *m;
     }
     return cond_quantile_scan(T, row, anchor, q_num, q_den);
+}
+
+/* NEXT-4 (A50): Q_q over the pooled leaf samples of the trees' leaves for x, conditioned on
+ * L > anchor like (a2): the ceil(q m)-th smallest of the m pooled samples above the anchor
+ * (type-1 quantile, A4; every tree's leaf contributes its samples once); none -> L_max (A7). */
+static int cmp_u32(const void* a, const void* b) {
+    uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+    return (x > y) - (x < y);
+}
+uint32_t og_qrf_quantile(const og_forest* F, const uint32_t* x, uint32_t anchor, uint32_t q_num, uint32_t q_den,
+                         uint32_t l_max) {
+    uint32_t cap = 0;
+    uint32_t* leaf_off = (uint32_t*)malloc(sizeof(uint32_t) * (F->n_trees ? F->n_trees : 1));
+    uint32_t* leaf_cnt = (uint32_t*)malloc(sizeof(uint32_t) * (F->n_trees ? F->n_trees : 1));
+    for (uint32_t t = 0; t < F->n_trees; ++t) {
+        uint32_t v = F->root[t];
+        while (F->feature[v] != OG_LEAF)
+            v = x[F->feature[v]] <= F->threshold[v] ? F->left[v] : F->right[v];
+        leaf_off[t] = F->threshold[v]; leaf_cnt[t] = F->left[v];
+        cap += F->left[v];
+    }
+    uint32_t* pool = (uint32_t*)malloc(sizeof(uint32_t) * (cap ? cap : 1));
+    uint32_t m = 0;
+    for (uint32_t t = 0; t < F->n_trees; ++t)
+        for (uint32_t i = 0; i < leaf_cnt[t]; ++i) {
+            uint32_t y = F->samples[leaf_off[t] + i];
+            if (y > anchor) pool[m++] = y;
+        }
+    uint32_t q = l_max;
+    if (m) {
+        qsort(pool, m, sizeof(uint32_t), cmp_u32);
+        uint64_t k = ((uint64_t)q_num * m + q_den - 1) / q_den;   /* ceil(q m) >= 1 */
+        q = pool[k - 1];
+    }
+    free(pool); free(leaf_off); free(leaf_cnt);
+    return q;
 }
 
 /* exported for the pins: Lhat = max(Q_q(L | L > R*floor(g/R)), g + 1) */
@@ -418,7 +470,13 @@ static int gmax_step(const og_config* cfg, const og_group* G, uint32_t n_groups,
         uint32_t g = generated[r];
         /* (a2) PredictLength: conditional upper quantile, refined every R tokens */
         uint32_t anchor = cfg->refine_interval * (g / cfg->refine_interval);
-        uint32_t q = cond_quantile(T, a_row(aux[r]), anchor, cfg->q_num, cfg->q_den, cfg->refine_interval);
+        uint32_t q;
+        if (T->forest) {                                        /* NEXT-4: the QRF (A50) */
+            uint32_t x[4] = { input_len[r], a_row(aux[r]), anchor, gi };
+            q = og_qrf_quantile(T->forest, x, anchor, cfg->q_num, cfg->q_den, T->l_max);
+        } else {
+            q = cond_quantile(T, a_row(aux[r]), anchor, cfg->q_num, cfg->q_den, cfg->refine_interval);
+        }
         lhat[r] = q > g + 1 ? q : g + 1;
         cost[r] = token_cost(input_len[r], prefilled[r], cfg->prefill_chunk);
         if (m_flags(m) & FL_COMPOUND) continue;                 /* handled by (a4) below */

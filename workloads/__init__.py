@@ -621,3 +621,62 @@ def pattern_queries(seed: int, store: dict, n_queries: int, foreign: float = 0.0
                 q["out"][i, u] = o_[u]
             q["true_t_ms"][i, u] = t_[u]
     return q
+
+
+# ----------------------------------------------------------------------------------------
+# NEXT-4: a quantile regression forest over (L_i, dist_row, anchor, group) -> L_o, trained on
+# synthetic requests drawn like the pool's (extremely randomized splits, bootstrap rows, leaves
+# keep their sorted targets: Meinshausen-style QRF).  Input generation only: the
+# method's arithmetic (the quantile at inference) lives in the oracle and the kernels.
+# ----------------------------------------------------------------------------------------
+
+def forest_training_set(seed: int, n: int, n_buckets: int = 16, l_max: int = 8192, R: int = 50):
+    rng = rng_for(seed)
+    app = rng.integers(0, 4, n)
+    keys = [APPS[a][0] for a in app]
+    L_in = np.array([int(_draw_in(rng, k, None)) for k in keys], np.int64)
+    b = _bucket(L_in, n_buckets)
+    mu = _out_mu(app, b, n_buckets)
+    sig = np.array([LOGN[APPS[a][1]][1] for a in app])
+    L_o = np.clip(np.rint(rng.lognormal(mu, sig)), 1, l_max).astype(np.int64)
+    g = (rng.random(n) * L_o).astype(np.int64)                   # generated so far, < L_o
+    anchor = R * (g // R)
+    group = rng.integers(0, 16, n)
+    X = np.stack([L_in, app * n_buckets + b, anchor, group], 1).astype(np.int64)
+    return X, L_o
+
+
+def build_forest(seed: int = 91, n_trees: int = 32, max_depth: int = 10, min_leaf: int = 5, n_train: int = 6000,
+                 X=None, y=None) -> dict:
+    rng = rng_for(seed)
+    if X is None:
+        X, y = forest_training_set(seed + 1, n_train)
+    feat, thr, left, right, root, samples = [], [], [], [], [], []
+
+    def grow(idx, depth):
+        v = len(feat)
+        feat.append(0); thr.append(0); left.append(0); right.append(0)
+        if depth < max_depth and len(idx) >= 2 * min_leaf:
+            for _ in range(8):                                  # a few random (feature, threshold) draws
+                f = int(rng.integers(0, X.shape[1]))
+                vals = X[idx, f]
+                t = int(vals[int(rng.integers(0, len(idx)))])
+                m = vals <= t
+                if min_leaf <= m.sum() <= len(idx) - min_leaf:
+                    feat[v], thr[v] = f, t
+                    left[v] = grow(idx[m], depth + 1)
+                    right[v] = grow(idx[~m], depth + 1)
+                    return v
+        feat[v] = 0xFFFFFFFF
+        thr[v] = len(samples)
+        ys = np.sort(y[idx])
+        samples.extend(int(a) for a in ys)
+        left[v] = len(ys)
+        return v
+
+    for _ in range(n_trees):
+        boot = rng.integers(0, len(y), len(y))
+        root.append(grow(boot, 0))
+    u = lambda a: np.array(a, np.uint32)
+    return {"root": u(root), "feature": u(feat), "threshold": u(thr), "left": u(left), "right": u(right),
+            "samples": u(samples)}
