@@ -560,6 +560,32 @@ def next_lines(args, dev, stream, Scheduler):
                                      "sample": "200 queries x 500 graphs on 1 core"},
                     "workload": "100K queries (C4's task count) revealed at random stages, 500 stored graphs "
                                 "from 24 families"}
+    # ---- NEXT-4: QRF length bounds for a 2^20-request refresh (every bound of a fresh pool)
+    F = W.build_forest(91)
+    X, _ = W.forest_training_set(5, 1 << 20)
+    g = (np.random.default_rng(5).random(len(X)) * 2000).astype(np.uint32)
+    qs = Scheduler(dd["cfg"], dd["groups"], dd["table"], capacity=64, task_capacity=8, device=dev, stream=stream)
+    qs.attach_forest(F)
+    qs.qrf_bound(X[:1024].astype(np.uint32), g[:1024])
+    kq = []
+    for _ in range(3):
+        bounds, kms_q = qs.qrf_bound(X.astype(np.uint32), g)
+        kq.append(kms_q)
+    qs.close()
+    t0 = time.perf_counter()
+    R = dd["cfg"]["refine_interval"]
+    ok = 0
+    for i in range(300):
+        a = R * (int(g[i]) // R)
+        v = max(oracle.qrf_quantile(F, [int(X[i, 0]), int(X[i, 1]), a, int(X[i, 3])], a, 95, 100, 8192), int(g[i]) + 1)
+        ok += int(v == bounds[i])
+    tc = time.perf_counter() - t0
+    out["qrf"] = {"metric": "QRF length bounds/sec (2^20 requests)", "value": len(X) / (np.median(kq) / 1e3),
+                  "unit": "bounds/s", "kernel_ms": float(np.median(kq)), "trees": len(F["root"]),
+                  "nodes": len(F["feature"]), "samples": len(F["samples"]), "agree_with_oracle_sample": ok / 300,
+                  "cpu_baseline": {"value": 300 / tc, "unit": "bounds/s", "cores": 1, "kind": "oracle",
+                                   "sample": "300 requests on 1 core"},
+                  "workload": "2^20 synthetic requests (C3 input mix), 32-tree forest of depth 10 on 6K samples"}
     return out
 
 

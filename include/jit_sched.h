@@ -380,6 +380,42 @@ int jit_sched_match(jit_sched* h, const jit_pattern_store* store, const jit_matc
 int jit_sched_last_match_ms(jit_sched* h, float* ms);
 
 /* ---------------------------------------------------------------------------------------
+ * NEXT-4: a quantile regression forest in (a2) (§4.1; reading A50).
+ * All trees' nodes in one array; an inner node sends x to `left` iff x[feature] <= threshold,
+ * else to `right`; a leaf (feature = 0xFFFFFFFF) holds samples[threshold .. threshold + left),
+ * its training targets sorted ascending (1 <= sample <= l_max).  Features x = (L_i, dist_row,
+ * anchor R*floor(g/R), SLO group).  The bound: the ceil(q m)-th smallest of the m pooled leaf
+ * samples above the anchor (every tree's leaf contributes its samples once), L_max when m = 0,
+ * then max(., g + 1) -- the table's conditional quantile with the forest's leaves as the sample.
+ * --------------------------------------------------------------------------------------- */
+typedef struct jit_forest {
+    uint32_t n_trees, n_nodes, n_samples, reserved;   /* n_trees <= 64, depth <= 64 */
+    const uint32_t* root;          /* [n_trees] */
+    const uint32_t* feature;       /* [n_nodes] 0..3, or 0xFFFFFFFF for a leaf */
+    const uint32_t* threshold;     /* [n_nodes] split value; leaf: first sample */
+    const uint32_t* left;          /* [n_nodes] left child; leaf: sample count */
+    const uint32_t* right;         /* [n_nodes] */
+    const uint32_t* samples;       /* [n_samples] */
+} jit_forest;
+
+/* Device bytes a forest needs (jit_sched_attach_forest's buffer). */
+int jit_forest_bytes(const jit_forest* f, uint64_t* bytes);
+
+/* Copy forest f (host arrays, validated) into dev_buf, which the caller keeps alive while it is
+ * attached, and make it h's length estimator for steps and replays (f = NULL: back to the
+ * table).  Invalidates every cached bound. */
+int jit_sched_attach_forest(jit_sched* h, const jit_forest* f, void* dev_buf, uint64_t bytes);
+
+/* Workspace for jit_sched_qrf_bound over n queries. */
+int jit_qrf_workspace_bytes(uint32_t n, uint64_t* bytes);
+
+/* Batch length bounds from the attached forest (one thread per query): x [n*4] = (L_i, dist_row,
+ * -, group) host array (the anchor is derived from g with h's R), g [n] tokens generated; out [n]
+ * = max(Q, g + 1).  kernel_ms (optional): device time of the kernel. */
+int jit_sched_qrf_bound(jit_sched* h, const uint32_t* x, const uint32_t* g, uint32_t n, void* dev_workspace,
+                        uint64_t ws_bytes, uint32_t* out, float* kernel_ms);
+
+/* ---------------------------------------------------------------------------------------
  * Exact sharded step over W ranks (north_star "pool sharded by request id ... NCCL allgather
  * of candidates followed by a global merge").  Each rank loads its shard (ids
  * unique across ranks) and calls, in order, with the caller allgathering in between:

@@ -1184,3 +1184,132 @@ extern "C" int jit_sched_last_match_ms(jit_sched* h, float* ms) {
     *ms = h->match_ms;
     return JIT_OK;
 }
+
+// ------------------------------------------------------------------------------------------
+// NEXT-4: the quantile regression forest in (a2)
+// ------------------------------------------------------------------------------------------
+static uint64_t forest_layout(const jit_forest* f, uint64_t* off) {
+    uint64_t o = 0;
+    auto take = [&](uint64_t b) { o = (o + 255) & ~255ull; const uint64_t r = o; o += b; return r; };
+    off[0] = take(sizeof(ForestDev));
+    off[1] = take(4ull * f->n_trees);
+    for (int i = 0; i < 4; ++i) off[2 + i] = take(4ull * f->n_nodes);
+    off[6] = take(4ull * std::max<uint32_t>(f->n_samples, 1));
+    return o + 256;
+}
+
+static int forest_check(jit_sched* h, const jit_forest* f, uint32_t l_max) {
+    if (!f->root || !f->feature || !f->threshold || !f->left || !f->right || !f->samples)
+        return set_err(h, JIT_EINVAL, "forest: null arrays");
+    if (f->n_trees == 0 || f->n_trees > kMaxTrees) return set_err(h, JIT_EINVAL, "forest: 1..%u trees", kMaxTrees);
+    for (uint32_t v = 0; v < f->n_nodes; ++v) {
+        if (f->feature[v] == kLeaf) {
+            const uint64_t e = (uint64_t)f->threshold[v] + f->left[v];
+            if (e > f->n_samples) return set_err(h, JIT_EINVAL, "forest: leaf %u beyond the samples", v);
+            for (uint64_t i = f->threshold[v]; i < e; ++i) {
+                if (f->samples[i] == 0 || f->samples[i] > l_max) return set_err(h, JIT_EINVAL, "forest: sample out of [1, l_max]");
+                if (i > f->threshold[v] && f->samples[i] < f->samples[i - 1]) return set_err(h, JIT_EINVAL, "forest: leaf %u not sorted", v);
+            }
+        } else if (f->feature[v] >= 4 || f->left[v] >= f->n_nodes || f->right[v] >= f->n_nodes) {
+            return set_err(h, JIT_EINVAL, "forest: node %u malformed", v);
+        }
+    }
+    for (uint32_t t = 0; t < f->n_trees; ++t) {                 // every path ends in a leaf within 64 levels
+        if (f->root[t] >= f->n_nodes) return set_err(h, JIT_EINVAL, "forest: bad root");
+        std::vector<std::pair<uint32_t, uint32_t>> st{{f->root[t], 0u}};
+        while (!st.empty()) {
+            const auto [v, d] = st.back();
+            st.pop_back();
+            if (d > 64) return set_err(h, JIT_EINVAL, "forest: tree %u deeper than 64 (or cyclic)", t);
+            if (f->feature[v] != kLeaf) { st.push_back({f->left[v], d + 1}); st.push_back({f->right[v], d + 1}); }
+        }
+    }
+    return JIT_OK;
+}
+
+extern "C" int jit_forest_bytes(const jit_forest* f, uint64_t* bytes) {
+    if (!f || !bytes) return JIT_EINVAL;
+    uint64_t off[7];
+    *bytes = forest_layout(f, off);
+    return JIT_OK;
+}
+
+extern "C" int jit_sched_attach_forest(jit_sched* h, const jit_forest* f, void* dev_buf, uint64_t bytes) {
+    if (!h) return JIT_EINVAL;
+    if (h->unfinished) return set_err(h, JIT_ESTATE, "fetch the unfinished step first");
+    if (!f) {
+        h->T.forest = nullptr;
+    } else {
+        int rc = forest_check(h, f, h->T.l_max);
+        if (rc) return rc;
+        uint64_t off[7];
+        const uint64_t need = forest_layout(f, off);
+        if (!dev_buf || bytes < need) return set_err(h, JIT_ECAPACITY, "forest buffer too small");
+        unsigned char* base = reinterpret_cast<unsigned char*>(((uintptr_t)dev_buf + 255) & ~(uintptr_t)255);
+        cudaStream_t s = h->stream;
+        ForestDev F{};
+        uint32_t* d[6];
+        const uint32_t* src[6] = {f->root, f->feature, f->threshold, f->left, f->right, f->samples};
+        const uint64_t cnt[6] = {f->n_trees, f->n_nodes, f->n_nodes, f->n_nodes, f->n_nodes, f->n_samples};
+        for (int i = 0; i < 6; ++i) {
+            d[i] = reinterpret_cast<uint32_t*>(base + off[1 + i]);
+            if (cnt[i]) CK(cudaMemcpyAsync(d[i], src[i], 4 * cnt[i], cudaMemcpyHostToDevice, s));
+        }
+        F.root = d[0]; F.feature = d[1]; F.threshold = d[2]; F.left = d[3]; F.right = d[4]; F.samples = d[5];
+        F.n_trees = f->n_trees; F.n_nodes = f->n_nodes; F.n_samples = f->n_samples;
+        CK(cudaMemcpyAsync(base + off[0], &F, sizeof F, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+        h->T.forest = reinterpret_cast<const ForestDev*>(base + off[0]);
+    }
+    // every cached bound came from the other estimator: refresh them all; the step graph holds T
+    if (h->P.n) k_invalidate_bounds<<<h->grid_pass, 256, 0, h->stream>>>(h->P);
+    CK(cudaGetLastError());
+    h->graph_dirty = true;
+    CK(cudaStreamSynchronize(h->stream));
+    return JIT_OK;
+}
+
+__global__ void k_qrf_batch(Table T, Cfg c, const uint32_t* x, const uint32_t* g, uint32_t n, uint32_t* out) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t gi = g[i], anchor = c.R * (gi / c.R);
+        const uint32_t q = qrf_bound(T.forest, x[4 * i], x[4 * i + 1], anchor, x[4 * i + 3], anchor, c.qn, c.qd, T.l_max);
+        out[i] = q > gi + 1 ? q : gi + 1;                        // A5 clamp
+    }
+}
+
+extern "C" int jit_qrf_workspace_bytes(uint32_t n, uint64_t* bytes) {
+    if (!bytes) return JIT_EINVAL;
+    *bytes = 24ull * n + 1024;
+    return JIT_OK;
+}
+
+extern "C" int jit_sched_qrf_bound(jit_sched* h, const uint32_t* x, const uint32_t* g, uint32_t n, void* dev_workspace,
+                                   uint64_t ws_bytes, uint32_t* out, float* kernel_ms) {
+    if (!h) return JIT_EINVAL;
+    if (!h->T.forest) return set_err(h, JIT_ESTATE, "no forest attached");
+    if (!x || !g || !out) return set_err(h, JIT_EINVAL, "qrf: null arrays");
+    if (n == 0) return JIT_OK;
+    if (!dev_workspace || ws_bytes < 24ull * n + 1024) return set_err(h, JIT_ECAPACITY, "qrf workspace too small");
+    for (uint32_t i = 0; i < n; ++i)
+        if (g[i] >= (1u << 24)) return set_err(h, JIT_EINVAL, "qrf: generated >= 2^24");
+    unsigned char* base = reinterpret_cast<unsigned char*>(((uintptr_t)dev_workspace + 255) & ~(uintptr_t)255);
+    uint32_t* dx = reinterpret_cast<uint32_t*>(base);
+    uint32_t* dg = dx + 4ull * n;
+    uint32_t* dout = dg + n;
+    cudaStream_t s = h->stream;
+    CK(cudaMemcpyAsync(dx, x, 16ull * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dg, g, 4ull * n, cudaMemcpyHostToDevice, s));
+    cudaEvent_t ev[2];
+    CK(cudaEventCreate(&ev[0])); CK(cudaEventCreate(&ev[1]));
+    CK(cudaEventRecord(ev[0], s));
+    k_qrf_batch<<<std::min<uint32_t>((n + 127) / 128, (uint32_t)h->n_sm * 16), 128, 0, s>>>(h->T, h->c, dx, dg, n, dout);
+    CK(cudaEventRecord(ev[1], s));
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, dout, 4ull * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+    cudaEventDestroy(ev[0]); cudaEventDestroy(ev[1]);
+    if (kernel_ms) *kernel_ms = ms;
+    return JIT_OK;
+}

@@ -66,7 +66,8 @@ __device__ __forceinline__ void score_standalone(const Cfg& c, const Table& T, c
     // (a2) conservative remaining length, refreshed every R tokens; cached per epoch
     const uint32_t ep = fastdiv(g, c.R, c.R_m, c.R_l);
     if (lhat == 0 || ep >= 65536u || m_epoch(meta) != ep) {
-        lhat = cond_quantile(T, drow, ep * c.R, c.qn, c.qd);
+        lhat = T.forest ? qrf_bound(T.forest, L_i, drow, ep * c.R, gi, ep * c.R, c.qn, c.qd, T.l_max)
+                        : cond_quantile(T, drow, ep * c.R, c.qn, c.qd);
         o.lhat = lhat; o.w_lhat = true;
         if (ep < 65536u) { o.meta = (meta & 0xFFFFu) | (ep << 16); o.w_meta = true; }
     }
@@ -402,7 +403,9 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                     uint32_t lhat = S.lhat[r];
                     const uint32_t ep = g / c.R;
                     if (lhat == 0 || ep >= 65536u || m_epoch(meta) != ep) {
-                        lhat = cond_quantile(T, S.aux[r] & 0xFFFFu, ep * c.R, c.qn, c.qd);
+                        lhat = T.forest ? qrf_bound(T.forest, L_in[r], S.aux[r] & 0xFFFFu, ep * c.R, m_group(meta),
+                                                    ep * c.R, c.qn, c.qd, T.l_max)
+                                        : cond_quantile(T, S.aux[r] & 0xFFFFu, ep * c.R, c.qn, c.qd);
                         S.lhat[r] = lhat;
                         if (ep < 65536u) S.meta[r] = (meta & 0xFFFFu) | (ep << 16);
                     }

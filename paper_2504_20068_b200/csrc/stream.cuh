@@ -88,7 +88,7 @@ struct Rare {
 __device__ __noinline__ Rare row_rare(const uint32_t* edges, const uint32_t* cum, uint32_t n_bins, uint32_t l_max,
                                       uint32_t unit, uint32_t R, uint32_t qn, uint32_t qd, HotRow* rp, uint32_t meta,
                                       uint32_t since, uint32_t lrow, bool pend, bool drop, bool stale, uint32_t ep,
-                                      uint32_t sc) {
+                                      uint32_t sc, const ForestDev* forest, uint32_t len_in) {
     const bool stamped = (meta >> 12) & kStamped;
     if (drop || pend != stamped) {
         if (pend) {                                     // became pending: count from here on
@@ -101,7 +101,8 @@ __device__ __noinline__ Rare row_rare(const uint32_t* edges, const uint32_t* cum
         if (drop) meta = m_with_state(meta, kDropped);
     }
     if (stale) {                                        // refreshed every R tokens
-        const uint32_t lh = cond_quantile_v(edges, cum, n_bins, l_max, unit, l_row(lrow), ep * R, qn, qd);
+        const uint32_t lh = forest ? qrf_bound(forest, len_in, l_row(lrow), ep * R, m_group(meta), ep * R, qn, qd, l_max)
+                                   : cond_quantile_v(edges, cum, n_bins, l_max, unit, l_row(lrow), ep * R, qn, qd);
         lrow = l_row(lrow) | (lh << 16);
         rp->lrow = lrow;
         meta = (meta & 0xFFFFu) | (ep < 65535u ? (ep + 1u) << 16 : 0u);   // epoch field = floor(g/R) + 1
@@ -112,7 +113,7 @@ __device__ __noinline__ Rare row_rare(const uint32_t* edges, const uint32_t* cum
 __device__ __forceinline__ void rare_row(const Table& T, const Cfg& c, HotRow* rp, HotRow& q, bool pend, bool drop,
                                          bool stale, uint32_t ep, uint32_t sc, uint32_t& ref) {
     const Rare o = row_rare(T.edges, T.cum, T.n_bins, T.l_max, T.unit, c.R, c.qn, c.qd, rp, q.meta, q.since, q.lrow,
-                            pend, drop, stale, ep, sc);
+                            pend, drop, stale, ep, sc, T.forest, q.len_in);
     q.meta = o.meta; q.since = o.since; q.lrow = o.lrow;
     ref += stale;
 }

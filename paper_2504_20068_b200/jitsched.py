@@ -101,6 +101,11 @@ class jit_match_query(C.Structure):
                [(k, C.c_void_p) for k in ("stage", "ident", "in_len", "out", "task")]
 
 
+class jit_forest(C.Structure):
+    _fields_ = [(k, C.c_uint32) for k in ("n_trees", "n_nodes", "n_samples", "reserved")] + \
+               [(k, C.c_void_p) for k in ("root", "feature", "threshold", "left", "right", "samples")]
+
+
 class jit_replay_spec(C.Structure):
     _fields_ = [("trace", C.c_uint32), ("reserved", C.c_uint32), ("load_num", C.c_uint64), ("load_den", C.c_uint64),
                 ("slo_num", C.c_uint64), ("slo_den", C.c_uint64)]
@@ -131,7 +136,8 @@ EXPORTS = ("jit_sched_workspace_bytes", "jit_sched_init", "jit_sched_load", "jit
            "jit_sched_phase_times", "jit_shard_spec_bytes", "jit_shard_spec_export", "jit_shard_spec_resolve",
            "jit_sched_time_scoring", "jit_sched_counters", "jit_sched_debug_scratch",
            "jit_sched_debug_set_counter", "jit_match_workspace_bytes", "jit_sched_match",
-           "jit_sched_last_match_ms")
+           "jit_sched_last_match_ms", "jit_forest_bytes", "jit_sched_attach_forest", "jit_qrf_workspace_bytes",
+           "jit_sched_qrf_bound")
 
 
 def load_library(path: str = LIB_PATH):
@@ -411,6 +417,44 @@ class Scheduler:
         ms = C.c_float()
         self._check(self.lib.jit_sched_last_match_ms(self.h, C.byref(ms)), self.h)
         return float(ms.value)
+
+    def attach_forest(self, forest):
+        """NEXT-4: make the QRF `forest` (dict of arrays) this handle's length estimator (None: the table)."""
+        torch = _torch()
+        if forest is None:
+            self._check(self.lib.jit_sched_attach_forest(self.h, None, None, C.c_uint64(0)), self.h)
+            self._forest_buf = None
+            return
+        keep = []
+        f = jit_forest()
+        f.n_trees, f.n_nodes, f.n_samples = len(forest["root"]), len(forest["feature"]), len(forest["samples"])
+        for k in ("root", "feature", "threshold", "left", "right", "samples"):
+            a = _c(forest[k], np.uint32)
+            if a.size == 0:
+                a = np.zeros(1, np.uint32)
+            keep.append(a)
+            setattr(f, k, _p(a))
+        nb = C.c_uint64()
+        self._check(self.lib.jit_forest_bytes(C.byref(f), C.byref(nb)), self.h)
+        buf = torch.empty(int(nb.value) + 256, dtype=torch.uint8, device=f"cuda:{self.device}")
+        self._check(self.lib.jit_sched_attach_forest(self.h, C.byref(f), C.c_void_p(buf.data_ptr()),
+                                                     C.c_uint64(buf.numel())), self.h)
+        self._forest_buf = buf                       # must outlive the attachment
+
+    def qrf_bound(self, x, g):
+        """Batch length bounds from the attached forest: (bounds, kernel ms)."""
+        torch = _torch()
+        x = _c(x, np.uint32)
+        g = _c(g, np.uint32)
+        n = len(g)
+        nb = C.c_uint64()
+        self._check(self.lib.jit_qrf_workspace_bytes(C.c_uint32(n), C.byref(nb)), self.h)
+        ws = torch.empty(int(nb.value) + 256, dtype=torch.uint8, device=f"cuda:{self.device}")
+        out = np.zeros(max(n, 1), np.uint32)
+        ms = C.c_float()
+        self._check(self.lib.jit_sched_qrf_bound(self.h, _p(x), _p(g), C.c_uint32(n), C.c_void_p(ws.data_ptr()),
+                                                 C.c_uint64(ws.numel()), _p(out), C.byref(ms)), self.h)
+        return out[:n].copy(), float(ms.value)
 
     def debug_set_counter(self, steps: int, launched: int):
         """Tests: move the device step counter (stamps move with it) and the launch count."""
