@@ -369,3 +369,53 @@ def qrf_quantile(forest, x, anchor: int, q_num: int, q_den: int, l_max: int) -> 
     xa = _arr(np.asarray(x), np.uint32)
     return int(lib.og_qrf_quantile(C.byref(F), _ptr(xa), C.c_uint32(anchor), C.c_uint32(q_num), C.c_uint32(q_den),
                                    C.c_uint32(l_max)))
+
+
+def multi_step(cfg, groups, table, now_ns: int, v_tokens, pools):
+    """NEXT-2 power-of-K (A51): one GMAX step on each of M replicas' pools of dummies (replica m
+    keyed with v_tokens[m]), cross-replica assignment (smallest v, then lower index) and sibling
+    removal (other replicas' dummies of an assigned request become Moved).  Returns per replica a
+    dict like step()'s (meta / aux updated copies)."""
+    lib = _load()
+    keep = []
+    c = _mk_config(cfg)
+    g, ng = _mk_groups(groups)
+    t = _mk_table(table, keep)
+    M = len(pools)
+    parr = (C.c_void_p * M)()
+    cols_all = []
+    for m, pool in enumerate(pools):
+        cols = {
+            "id": _arr(pool["id"], np.uint32), "arrival_ns": _arr(pool["arrival_ns"], np.int64),
+            "input_len": _arr(pool["input_len"], np.uint32), "generated": _arr(pool["generated"], np.uint32),
+            "prefilled": _arr(pool["prefilled"], np.uint32), "meta": np.array(pool["meta"], dtype=np.uint32),
+            "aux": np.array(pool["aux"], dtype=np.uint32), "task": _arr(pool["task"], np.uint32),
+            "override_R": _arr(pool["override_R"], np.uint32),
+        }
+        if pool.get("fair") is not None:
+            cols["fair"] = _arr(pool["fair"], np.uint32)
+        p = _Pool()
+        p.n = len(cols["id"])
+        for k, vv in cols.items():
+            setattr(p, k, _ptr(vv))
+        keep.append(p)
+        cols_all.append(cols)
+        parr[m] = C.cast(C.pointer(p), C.c_void_p)
+    res = (_Result * M)()
+    rows = [np.zeros(max(len(cl["id"]), 1), np.uint32) for cl in cols_all]
+    toks = [np.zeros(max(len(cl["id"]), 1), np.uint32) for cl in cols_all]
+    rptr = (C.c_void_p * M)(*[_ptr(a) for a in rows])
+    tptr = (C.c_void_p * M)(*[_ptr(a) for a in toks])
+    va = _arr(np.asarray(v_tokens), np.int64)
+    rc = lib.og_multi_step(C.byref(c), g, C.c_uint32(ng), C.byref(t), C.c_int64(now_ns), C.c_uint32(M), _ptr(va),
+                           parr, res, rptr, tptr)
+    out = []
+    for m in range(M):
+        k = res[m].n_selected
+        r = rows[m][:k].copy()
+        out.append({"status": rc if rc < 0 else (1 if res[m].n_pending == 0 else 0), "n_pending": res[m].n_pending,
+                    "n_selected": k, "total_tokens": res[m].total_tokens, "n_candidates": res[m].n_candidates,
+                    "b_star": res[m].b_star, "n_dropped_now": res[m].n_dropped_now, "bp": res[m].bp, "thr": res[m].thr,
+                    "batch_rows": r, "batch_ids": cols_all[m]["id"][r].copy(), "batch_tokens": toks[m][:k].copy(),
+                    "meta": cols_all[m]["meta"], "aux": cols_all[m]["aux"]})
+    return out

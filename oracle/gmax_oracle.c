@@ -36,7 +36,8 @@ typedef unsigned __int128 u128;
 
 enum { OG_LAT = 0, OG_DDL = 1, OG_CMP = 2, OG_BE = 3 };           /* §3 P:209-216 + BE P:216 */
 enum { ST_QUEUED = 0, ST_RUNNING = 1, ST_PREEMPTED = 2, ST_DONE = 3, ST_DROPPED = 4,
-       ST_WAITING = 5 /* compound call of a stage not yet released */ };
+       ST_WAITING = 5 /* compound call of a stage not yet released */,
+       ST_MOVED = 6   /* NEXT-2 power-of-K: the request was assigned to another replica */ };
 enum { FL_EVER = 1u, FL_COMPOUND = 2u, FL_OVERRIDE = 4u };
 #define NO_TASK 0xFFFFFFFFu
 #define MAX_STAGES 8u
@@ -1110,4 +1111,75 @@ int og_match(const og_patterns* P, const og_queries* Q, int32_t* best, double* s
         best[q] = b; score[q] = bs;
     }
     return OG_OK;
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* NEXT-2 power-of-K over M model replicas (§4.3, reading A51).                 */
+/* Every request has dummies on K sampled replicas (replica m's pool holds its dummies,    */
+/* standalone requests only); a dummy on replica m is keyed with m's v_token, so it carries */
+/* a replica-specific priority.  Each replica runs GMAX over its own pool ("scheduling     */
+/* proceeds as usual over the enlarged set").  A request proposed by several replicas in   */
+/* the same step is assigned to the one where its priority is highest: key_m = A /         */
+/* (len_rem v_m + eps) with A and len_rem replica-independent, so the smallest v_m, ties to */
+/* the lower index; it leaves the other replicas' batches (no refill).  "Once a request is */
+/* assigned to a replica, its other dummies are removed": every other replica's dummy of   */
+/* an assigned request becomes Moved (terminal, never pending).                             */
+/* ------------------------------------------------------------------------------------ */
+int og_multi_step(const og_config* cfg, const og_group* G, uint32_t n_groups, const og_table* T, int64_t now,
+                  uint32_t M, const int64_t* v, og_pool* const* pools, og_result* res,
+                  uint32_t* const* batch_rows, uint32_t* const* batch_tokens) {
+    uint32_t** sel = (uint32_t**)calloc(M, sizeof(uint32_t*));
+    uint32_t** scst = (uint32_t**)calloc(M, sizeof(uint32_t*));
+    int* st = (int*)calloc(M, sizeof(int));
+    uint32_t* nprop = NULL;            /* each replica's proposal size (before the assignment) */
+    int ret = OG_OK;
+    /* 1. every replica's GMAX step on its own dummies */
+    for (uint32_t m = 0; m < M; ++m) {
+        og_pool* P = pools[m];
+        for (uint32_t r = 0; r < P->n; ++r)
+            if (P->task[r] != NO_TASK) { ret = OG_EINVAL; goto done; }     /* standalone requests only */
+        sel[m] = (uint32_t*)malloc(sizeof(uint32_t) * (P->n ? P->n : 1));
+        scst[m] = (uint32_t*)malloc(sizeof(uint32_t) * (P->n ? P->n : 1));
+        og_reset_memo();
+        st[m] = gmax_step(cfg, G, n_groups, T, now, v[m], P->n, P->id, P->arrival_ns, P->input_len,
+                          P->generated, P->prefilled, P->meta, P->aux, P->task, P->override_R, P->fair,
+                          NULL, &res[m], sel[m], scst[m], NULL, 1);
+        if (st[m] == OG_EINVAL) { ret = OG_EINVAL; goto done; }
+    }
+    /* 2. the winner of every proposed request: the smallest v, then the lower replica index */
+    nprop = (uint32_t*)calloc(M, sizeof(uint32_t));
+    for (uint32_t m = 0; m < M; ++m) nprop[m] = st[m] == OG_OK ? res[m].n_selected : 0u;
+    for (uint32_t m = 0; m < M; ++m) {
+        if (st[m] != OG_OK) continue;
+        uint32_t k = 0, tot = 0;
+        for (uint32_t i = 0; i < nprop[m]; ++i) {
+            uint32_t id = pools[m]->id[sel[m][i]];
+            uint32_t win = m;
+            for (uint32_t w = 0; w < M; ++w) {
+                if (w == m || st[w] != OG_OK) continue;
+                for (uint32_t j = 0; j < nprop[w]; ++j)
+                    if (pools[w]->id[sel[w][j]] == id && (v[w] < v[win] || (v[w] == v[win] && w < win))) win = w;
+            }
+            if (win != m) continue;
+            batch_rows[m][k] = sel[m][i]; batch_tokens[m][k] = scst[m][i]; tot += scst[m][i]; ++k;
+        }
+        res[m].n_selected = k; res[m].total_tokens = tot;
+    }
+    /* 3. sibling removal: a request proposed anywhere is assigned to its winner; every dummy of it
+     * on another replica (proposed there or not) becomes Moved */
+    for (uint32_t w = 0; w < M; ++w) {
+        if (st[w] != OG_OK) continue;
+        for (uint32_t j = 0; j < res[w].n_selected; ++j) {
+            uint32_t id = pools[w]->id[batch_rows[w][j]];
+            for (uint32_t m = 0; m < M; ++m) {
+                if (m == w) continue;
+                for (uint32_t r = 0; r < pools[m]->n; ++r)
+                    if (pools[m]->id[r] == id) pools[m]->meta[r] = m_set_state(pools[m]->meta[r], ST_MOVED);
+            }
+        }
+    }
+done:
+    for (uint32_t m = 0; m < M; ++m) { free(sel[m]); free(scst[m]); res[m].error = st[m] == OG_EINVAL; }
+    free(sel); free(scst); free(st); free(nprop);
+    return ret;
 }

@@ -21,7 +21,7 @@ SEED0 = 250420068
 NO_TASK = 0xFFFFFFFF
 MAX_STAGES = 8
 LAT, DDL, CMP, BE = 0, 1, 2, 3
-Q_QUEUED, Q_RUNNING, Q_PREEMPTED, Q_DONE, Q_DROPPED, Q_WAITING = 0, 1, 2, 3, 4, 5
+Q_QUEUED, Q_RUNNING, Q_PREEMPTED, Q_DONE, Q_DROPPED, Q_WAITING, Q_MOVED = 0, 1, 2, 3, 4, 5, 6
 F_EVER, F_COMPOUND, F_OVERRIDE = 1, 2, 4
 MS = 1_000_000
 S_ = 1_000_000_000
@@ -680,3 +680,23 @@ def build_forest(seed: int = 91, n_trees: int = 32, max_depth: int = 10, min_lea
     u = lambda a: np.array(a, np.uint32)
     return {"root": u(root), "feature": u(feat), "threshold": u(thr), "left": u(left), "right": u(right),
             "samples": u(samples)}
+
+
+def replica_pools(d: dict, M: int, K: int, seed: int = 7):
+    """NEXT-2 power-of-K inputs: the standalone rows of pool snapshot d, each given dummies on K
+    of M replicas sampled without replacement; returns M standalone pools (rows in id
+    order of the base pool)."""
+    rng = rng_for(seed)
+    p = d["pool"]
+    ns = int(p["n_single"])
+    keys = ("id", "arrival_ns", "input_len", "generated", "prefilled", "meta", "aux", "task", "override_R")
+    pick = np.zeros((ns, M), bool)
+    for i in range(ns):
+        pick[i, rng.permutation(M)[:K]] = True
+    pools = []
+    for m in range(M):
+        sel = np.nonzero(pick[:, m])[0]
+        q = {k: np.asarray(p[k])[:ns][sel].copy() for k in keys}
+        q["n_single"] = len(sel)
+        pools.append(q)
+    return pools
