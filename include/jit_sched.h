@@ -53,7 +53,8 @@ enum {
 /* SLO types, §3; best effort P:216 */
 enum { JIT_LAT = 0, JIT_DDL = 1, JIT_CMP = 2, JIT_BE = 3 };
 /* request states + WAITING = compound call whose stage is not released yet */
-enum { JIT_QUEUED = 0, JIT_RUNNING = 1, JIT_PREEMPTED = 2, JIT_DONE = 3, JIT_DROPPED = 4, JIT_WAITING = 5 };
+enum { JIT_QUEUED = 0, JIT_RUNNING = 1, JIT_PREEMPTED = 2, JIT_DONE = 3, JIT_DROPPED = 4, JIT_WAITING = 5,
+       JIT_MOVED = 6      /* power-of-K: the request was assigned to another replica (terminal) */ };
 /* request flags */
 enum { JIT_F_EVER = 1, JIT_F_COMPOUND = 2, JIT_F_OVERRIDE = 4 };
 #define JIT_NO_TASK 0xFFFFFFFFu
@@ -458,6 +459,32 @@ int jit_shard_spec_resolve(jit_sched* h, const void* d_all, uint32_t world, uint
 int jit_shard_merge(jit_sched* h, const void* d_all_rec1, uint32_t n_all);
 int jit_shard_candidates(jit_sched* h, void* d_rec2, uint32_t cap, uint32_t rank, uint32_t* n_out);
 int jit_shard_finish(jit_sched* h, const void* d_all_rec2, uint32_t n_all, uint32_t rank, jit_batch* out);
+
+/* ---------------------------------------------------------------------------------------
+ * NEXT-2 power-of-K over M model replicas (§4.3: "each request has dummies on K
+ * replicas ... once a request is assigned to a replica, its other dummies are removed";
+ * DESIGN.md reading A51).  One handle per replica holds that replica's dummies (a standalone
+ * pool: JIT_EINVAL with compound tasks; request ids shared across replicas) and runs the
+ * ordinary step with the replica's own v_token (jit_sched_step).  Then:
+ *   jit_multi_export     writes the replica's proposal -- a 32-byte header (the step's v_token,
+ *                        replica index, count, capacity, resolved flag) and the batch ids in
+ *                        window order -- to d_out (device, jit_multi_record_bytes() bytes;
+ *                        asynchronous on cfg.stream).
+ *   -- concatenate the M records in replica order (an allgather across ranks, one replica per
+ *      GPU; or device copies on one GPU) --
+ *   jit_multi_reconcile  every replica, against the union d_all (device, M records): a request
+ *                        proposed by several replicas is assigned to the one with the smallest
+ *                        v_token (priority G / (len_rem v + eps) is highest there), ties to the
+ *                        lower index; the replica's batch keeps the requests it won in window
+ *                        order (no refill) and `out` gets that batch (other fields as the step
+ *                        left them); every dummy in this pool of a request assigned to another
+ *                        replica becomes JIT_MOVED (terminal, never pending).
+ * All replicas must share max_batch (capacity of the records).  Records whose header does not
+ * match its slot fail with JIT_EINVAL.  Returns JIT_OK, or JIT_EMPTY if this replica's step had
+ * no pending request. */
+uint64_t jit_multi_record_bytes(const jit_sched* h);
+int jit_multi_export(jit_sched* h, uint32_t replica, void* d_out);
+int jit_multi_reconcile(jit_sched* h, const void* d_all, uint32_t n_replicas, uint32_t replica, jit_batch* out);
 
 void jit_sched_destroy(jit_sched* h);
 const char* jit_sched_last_error(const jit_sched* h);

@@ -15,6 +15,7 @@
 #include "stream.cuh"
 #include "replay.cuh"
 #include "shard.cuh"
+#include "multi.cuh"
 #include "exact_api.h"
 
 using namespace jit;
@@ -54,6 +55,7 @@ struct jit_sched {
     bool keys_ready = false;          // k_score already ran this step (fast sharded attempt)
     bool unfinished = false;          // a step was launched and not finished (step_async)
     uint64_t launched = 0;            // steps launched (the stamp rebase runs every 2^30)
+    unsigned long long multi_epoch = 0;   // power-of-K reconciles so far (tags S.mwin words)
     cudaEvent_t ev[6] = {};
     cudaGraphNode_t ev_node[5] = {};      // event-record nodes of the timed graph
     std::vector<cudaEvent_t> slots;       // 5 events per recorded step
@@ -142,6 +144,7 @@ static void carve(Carve& cv, const jit_config* cfg, const jit_len_table* tab, Po
     S.out_ids = cv.take<uint32_t>(cfg->max_batch + 1); S.out_tokens = cv.take<uint32_t>(cfg->max_batch + 1);
     S.out_rows = cv.take<uint32_t>(cfg->max_batch + 1);
     S.cand_cap = (uint32_t)N;
+    S.mwin = cv.take<unsigned long long>(N);
     S.spec_img = cv.take<uint64_t>(kSpecCap);
     S.spec_id = cv.take<uint32_t>(kSpecCap); S.spec_row = cv.take<uint32_t>(kSpecCap);
     S.spec_cost = cv.take<uint32_t>(kSpecCap); S.spec_len = cv.take<uint32_t>(kSpecCap);
@@ -1083,6 +1086,60 @@ extern "C" int jit_shard_finish(jit_sched* h, const void* d_all_rec2, uint32_t n
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(h->h_ctrl, h->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
     return finish_step(h, out);
+}
+
+// ------------------------------------------------------------------------------------------
+// NEXT-2: power-of-K over M replicas (multi.cuh): export after a step, reconcile against the union
+// ------------------------------------------------------------------------------------------
+extern "C" uint64_t jit_multi_record_bytes(const jit_sched* h) {
+    return h ? multi_rec_bytes(h->cfg.max_batch) : 0;
+}
+
+extern "C" int jit_multi_export(jit_sched* h, uint32_t replica, void* d_out) {
+    if (!h || !d_out) return JIT_EINVAL;
+    if (!h->loaded) return set_err(h, JIT_ESTATE, "multi_export before load");
+    if (h->unfinished) return set_err(h, JIT_ESTATE, "multi_export while a step is unfinished");
+    if (replica >= kMaxReplicas) return set_err(h, JIT_EINVAL, "replica index %u >= %u", replica, kMaxReplicas);
+    k_multi_export<<<(h->cfg.max_batch + 255) / 256 + 1, 256, 0, h->stream>>>(h->d_ctrl, h->S, replica, h->cfg.max_batch,
+                                                                               (unsigned char*)d_out);
+    CK(cudaGetLastError());
+    return JIT_OK;
+}
+
+extern "C" int jit_multi_reconcile(jit_sched* h, const void* d_all, uint32_t n_replicas, uint32_t replica, jit_batch* out) {
+    if (!h || !d_all) return JIT_EINVAL;
+    if (!h->loaded) return set_err(h, JIT_ESTATE, "multi_reconcile before load");
+    if (h->unfinished) return set_err(h, JIT_ESTATE, "multi_reconcile while a step is unfinished");
+    if (n_replicas == 0 || n_replicas > kMaxReplicas || replica >= n_replicas)
+        return set_err(h, JIT_EINVAL, "replica %u of %u (at most %u replicas)", replica, n_replicas, kMaxReplicas);
+    if (h->P.n_tasks) return set_err(h, JIT_EINVAL, "power-of-K replicas hold standalone requests only");
+    const uint32_t cap = h->cfg.max_batch;
+    const uint64_t rb = multi_rec_bytes(cap);
+    const unsigned long long ep = ++h->multi_epoch;
+    const unsigned char* all = (const unsigned char*)d_all;
+    const uint32_t grid = (uint32_t)std::min<uint64_t>(((uint64_t)n_replicas * cap + 255) / 256, 8ull * h->n_sm);
+    k_multi_mark<<<grid, 256, 0, h->stream>>>(h->P, h->S, h->d_ctrl, all, rb, n_replicas, replica, cap, h->S.mwin, ep);
+    k_multi_moved<<<grid, 256, 0, h->stream>>>(h->P, h->S, h->d_ctrl, all, rb, n_replicas, replica, cap, h->S.mwin, ep);
+    k_multi_finish<<<1, kMultiThreads, 0, h->stream>>>(h->S, h->d_ctrl, all, rb, n_replicas, replica, cap, h->S.mwin, ep);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->stream));
+    const Ctrl& c = *h->h_ctrl;
+    if (c.error) return set_err(h, JIT_EINVAL, "multi_reconcile: invalid records or pool (error code %u)", c.error);
+    if (out) {
+        out->n_pending = c.n_pending; out->n_dropped = c.n_dropped; out->status = c.status;
+        out->n_refresh = c.n_refresh; out->fallback = c.fallback; out->n_spec = c.spec_n;
+        out->n_selected = c.status == ST_RESOLVED ? c.n_selected : 0;
+        out->total_tokens = c.status == ST_RESOLVED ? c.total_tokens : 0;
+        out->n_candidates = c.n_cand; out->b_star = c.b_star; out->bp = c.bp; out->thr = c.thr;
+        if (out->n_selected > out->capacity && (out->ids || out->tokens || out->rows))
+            return set_err(h, JIT_ECAPACITY, "batch capacity %u < %u", out->capacity, out->n_selected);
+        const uint32_t* hb = h->h_batch;
+        const uint64_t B = cap + 1;
+        if (out->ids) memcpy(out->ids, hb, 4ull * out->n_selected);
+        if (out->tokens) memcpy(out->tokens, hb + B, 4ull * out->n_selected);
+        if (out->rows) memcpy(out->rows, hb + 2 * B, 4ull * out->n_selected);
+    }
+    return c.status == ST_RESOLVED ? JIT_OK : JIT_EMPTY;
 }
 
 // ------------------------------------------------------------------------------------------

@@ -121,6 +121,7 @@ struct Scratch {
     unsigned int* spec_cnt;  // size of the speculative set (k_score atomics; reset by k_spec)
     Ctrl* h_ctrl;            // pinned host copy of the control block, written by the step's last kernel
     uint32_t* h_batch;       // pinned host mirror of the batch: ids | tokens | rows, (max_batch + 1) each
+    unsigned long long* mwin;   // NEXT-2 power-of-K: per row (epoch << 8) | (255 - winner rank) (multi.cuh)
 };
 
 // The last kernel of a step writes the control block straight into pinned host memory (no
@@ -661,8 +662,8 @@ __global__ void k_pack(HotRow* rows, uint32_t n, const int64_t* arr, const uint3
 
 // progress updates from the engine (keyed by request id or by row), applied before the step's
 // pass.  A row leaving the pending set freezes its steps_waited (the handle's counter); the ranges
-// the pass relies on are checked (generated < 2^24, prefilled <= L_i, state <= Waiting, no way out
-// of Done / Dropped, known id); a violation fails the step (gpart->err).
+// the pass relies on are checked (generated < 2^24, prefilled <= L_i, state <= Moved, no way out
+// of Done / Dropped / Moved, known id); a violation fails the step (gpart->err).
 __global__ void k_progress(Pool P, Scratch S, const uint32_t* key, const uint32_t* gen, const uint32_t* pre,
                            const uint32_t* state, uint32_t n, int by_id) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -671,8 +672,8 @@ __global__ void k_progress(Pool P, Scratch S, const uint32_t* key, const uint32_
     if (r >= P.n) { atomicOr(&S.gpart->err, 8u); return; }
     HotRow* rp = P.rows + r;
     const uint32_t st = state[i], old_st = m_state(rp->meta);
-    if (gen[i] >= (1u << 24) || pre[i] > rp->len_in || st > kWaiting ||
-        ((old_st == kDone || old_st == kDropped) && st != old_st)) {
+    if (gen[i] >= (1u << 24) || pre[i] > rp->len_in || st > kMoved ||
+        ((old_st == kDone || old_st == kDropped || old_st == kMoved) && st != old_st)) {
         atomicOr(&S.gpart->err, 8u);
         return;
     }
@@ -827,7 +828,7 @@ __global__ void k_validate(Pool P, const Group* groups, uint32_t n_groups, uint3
         const uint32_t gi = m_group(meta);
         const bool comp = (m_flags(meta) & kCompound) != 0;
         if (gi >= n_groups || l_row(q.lrow) >= n_rows_tab || q.len_in == 0 || q.len_in >= (1u << 24) ||
-            q.gen >= (1u << 24) || q.pre > q.len_in || (meta >> 16) != 0 || m_state(meta) > kWaiting ||
+            q.gen >= (1u << 24) || q.pre > q.len_in || (meta >> 16) != 0 || m_state(meta) > kMoved ||
             q.since > 0xFFFFu || comp != (r >= std_end)) bad = true;
         else if (!comp) {
             if (P.task[r] != kNoTask || groups[gi].type == kCMP) bad = true;

@@ -137,7 +137,7 @@ EXPORTS = ("jit_sched_workspace_bytes", "jit_sched_init", "jit_sched_load", "jit
            "jit_sched_time_scoring", "jit_sched_counters", "jit_sched_debug_scratch",
            "jit_sched_debug_set_counter", "jit_match_workspace_bytes", "jit_sched_match",
            "jit_sched_last_match_ms", "jit_forest_bytes", "jit_sched_attach_forest", "jit_qrf_workspace_bytes",
-           "jit_sched_qrf_bound")
+           "jit_sched_qrf_bound", "jit_multi_record_bytes", "jit_multi_export", "jit_multi_reconcile")
 
 
 def load_library(path: str = LIB_PATH):
@@ -156,6 +156,8 @@ def load_library(path: str = LIB_PATH):
             if name not in ("jit_sched_last_error", "jit_sched_version", "jit_sched_destroy"):
                 getattr(lib, name).restype = C.c_int
         lib.jit_shard_spec_bytes.restype = C.c_uint32
+        lib.jit_multi_record_bytes.restype = C.c_uint64
+        lib.jit_multi_record_bytes.argtypes = [C.c_void_p]
         _lib = lib
     return _lib
 
@@ -532,6 +534,24 @@ class Scheduler:
             return None
         return self._batch_dict(rc, b)
 
+    # ------------------------------------------------- NEXT-2 power-of-K (one handle per replica)
+    def multi_record_bytes(self) -> int:
+        return int(self.lib.jit_multi_record_bytes(self.h))
+
+    def multi_export(self, buf, replica: int):
+        """Write this replica's proposal (the last step's batch ids + header) into device tensor buf."""
+        self._check(self.lib.jit_multi_export(self.h, C.c_uint32(replica), C.c_void_p(buf.data_ptr())), self.h)
+
+    def multi_reconcile(self, all_buf, n_replicas: int, replica: int) -> dict:
+        """Reconcile against the M concatenated proposals (device tensor): the batch this replica
+        keeps; the dummies of requests assigned elsewhere become Moved."""
+        b = jit_batch()
+        b.capacity = self.max_batch
+        b.ids, b.tokens, b.rows = _p(self._ids), _p(self._tok), _p(self._rows)
+        rc = self._check(self.lib.jit_multi_reconcile(self.h, C.c_void_p(all_buf.data_ptr()), C.c_uint32(n_replicas),
+                                                      C.c_uint32(replica), C.byref(b)), self.h)
+        return self._batch_dict(rc, b)
+
     # ------------------------------------------------------------------ replay
     def replay(self, traces, specs, rcfg: dict, log_steps: int = 0):
         """Run len(specs) independent replays; traces: list of trace dicts; specs: list of dicts
@@ -581,3 +601,27 @@ class Scheduler:
         if log is not None:
             log = log.reshape(len(specs), log_steps)
         return out, log
+
+
+def multi_step(scheds, now_ns: int, v_token_ns, allgather=None, replica: int = 0) -> list:
+    """NEXT-2 power-of-K step over M replica handles (§4.3): every replica steps with
+    its own v_token, exports its proposal, the M records are concatenated and every replica
+    reconciles.  Local replicas (allgather None): `scheds` are all M handles, the records are
+    concatenated on the device.  One replica per rank: `scheds` = [this rank's handle], `replica` =
+    its index, `allgather` concatenates the ranks' records in rank order (torch.distributed over
+    NCCL).  Returns the reconciled batch of each handle in `scheds`."""
+    torch = _torch()
+    rb = scheds[0].multi_record_bytes()
+    dev = f"cuda:{scheds[0].device}"
+    for s, v in zip(scheds, v_token_ns):
+        s.step(now_ns, v)
+    if allgather is None:
+        M = len(scheds)
+        allb = torch.empty(M * rb, dtype=torch.uint8, device=dev)
+        for m, s in enumerate(scheds):
+            s.multi_export(allb[m * rb:(m + 1) * rb], m)
+        return [s.multi_reconcile(allb, M, m) for m, s in enumerate(scheds)]
+    rec = torch.empty(rb, dtype=torch.uint8, device=dev)
+    scheds[0].multi_export(rec, replica)
+    allb = allgather(rec)
+    return [scheds[0].multi_reconcile(allb, allb.numel() // rb, replica)]

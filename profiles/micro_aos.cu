@@ -46,6 +46,67 @@ __device__ __forceinline__ Row ldrow(const Row* p) {
     return r;
 }
 
+__device__ __forceinline__ Row ldrow8(const Row* p) {
+    uint32_t a0, a1, a2, a3, a4, a5, a6, a7;
+    asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3), "=r"(a4), "=r"(a5), "=r"(a6), "=r"(a7) : "l"(p));
+    Row r;
+    r.arr = (int64_t)(((uint64_t)a1 << 32) | a0); r.li = a2; r.ge = a3; r.pr = a4; r.lr = a5; r.me = a6; r.si = a7;
+    return r;
+}
+
+// one 256-bit load per row (sm_100: LDG.E.256), R rows per lane, lane-strided in a warp's 32R-row item
+template <int R, int M, int T>
+__global__ void __launch_bounds__(T) k_v8(const Row* rows, uint32_t n, unsigned long long* out) {
+    const uint32_t w = (blockIdx.x * T + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const uint32_t base = w * 32 * R + lane;
+    Row q[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        const uint32_t r = base + 32 * k;
+        if (r < n) q[k] = ldrow8(rows + r); else q[k] = Row{};
+    }
+    uint64_t v = 0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        uint64_t x = (uint64_t)q[k].arr ^ q[k].li ^ q[k].ge ^ q[k].pr ^ q[k].lr ^ q[k].me ^ q[k].si;
+        if (M) x = fake_math<M>(x, q[k].li, q[k].ge);
+        v ^= x;
+    }
+    sink(v, out);
+}
+
+// persistent: grid-stride over 32R-row warp items with the next item's rows loaded before the
+// current item's math (register double buffer)
+template <int R, int M, int T>
+__global__ void __launch_bounds__(T) k_v8p(const Row* rows, uint32_t n, unsigned long long* out) {
+    const uint32_t W = gridDim.x * (T / 32), lane = threadIdx.x & 31;
+    uint32_t w = (blockIdx.x * T + threadIdx.x) >> 5;
+    const uint32_t nit = (n + 32 * R - 1) / (32 * R);
+    Row q[R], nx[R];
+    auto load = [&](Row* d, uint32_t it) {
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const uint32_t r = it * 32 * R + lane + 32 * k;
+            if (it < nit && r < n) d[k] = ldrow8(rows + r); else d[k] = Row{};
+        }
+    };
+    load(q, w);
+    uint64_t v = 0;
+    for (; w < nit; w += W) {
+        load(nx, w + W);
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            uint64_t x = (uint64_t)q[k].arr ^ q[k].li ^ q[k].ge ^ q[k].pr ^ q[k].lr ^ q[k].me ^ q[k].si;
+            if (M) x = fake_math<M>(x, q[k].li, q[k].ge);
+            v ^= x;
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) q[k] = nx[k];
+    }
+    sink(v, out);
+}
+
 template <int M>
 __global__ void __launch_bounds__(256) k_aos1(const Row* rows, uint32_t n, unsigned long long* out) {
     const uint32_t r = blockIdx.x * 256 + threadIdx.x;
@@ -130,6 +191,23 @@ int main() {
     timeit("aosW R=4 math=8", [&](int c) { k_aosW<4, 8><<<N / 1024, 256>>>(rows[c], N, out); });
     timeit("aosW R=4 math=16", [&](int c) { k_aosW<4, 16><<<N / 1024, 256>>>(rows[c], N, out); });
     timeit("aosW R=8", [&](int c) { k_aosW<8, 0><<<N / 2048, 256>>>(rows[c], N, out); });
+    timeit("v8 R=1 T=256", [&](int c) { k_v8<1, 0, 256><<<N / 256, 256>>>(rows[c], N, out); });
+    timeit("v8 R=2 T=256", [&](int c) { k_v8<2, 0, 256><<<N / 512, 256>>>(rows[c], N, out); });
+    timeit("v8 R=4 T=256", [&](int c) { k_v8<4, 0, 256><<<N / 1024, 256>>>(rows[c], N, out); });
+    timeit("v8 R=4 T=128", [&](int c) { k_v8<4, 0, 128><<<N / 512, 128>>>(rows[c], N, out); });
+    timeit("v8 R=2 T=256 math=8", [&](int c) { k_v8<2, 8, 256><<<N / 512, 256>>>(rows[c], N, out); });
+    timeit("v8 R=2 T=256 math=16", [&](int c) { k_v8<2, 16, 256><<<N / 512, 256>>>(rows[c], N, out); });
+    timeit("v8 R=4 T=256 math=8", [&](int c) { k_v8<4, 8, 256><<<N / 1024, 256>>>(rows[c], N, out); });
+    timeit("v8 R=4 T=256 math=16", [&](int c) { k_v8<4, 16, 256><<<N / 1024, 256>>>(rows[c], N, out); });
+    for (int cps : {4, 6, 8}) {
+        char nm[64];
+        snprintf(nm, 64, "v8p R=2 T=256 cps=%d", cps);
+        timeit(nm, [&](int c) { k_v8p<2, 0, 256><<<148 * cps, 256>>>(rows[c], N, out); });
+        snprintf(nm, 64, "v8p R=2 T=256 cps=%d math=8", cps);
+        timeit(nm, [&](int c) { k_v8p<2, 8, 256><<<148 * cps, 256>>>(rows[c], N, out); });
+        snprintf(nm, 64, "v8p R=2 T=256 cps=%d math=16", cps);
+        timeit(nm, [&](int c) { k_v8p<2, 16, 256><<<148 * cps, 256>>>(rows[c], N, out); });
+    }
     timeit("soa1", [&](int c) { k_soa1<0><<<N / 256, 256>>>(soa[c], N, out); });
     timeit("soa1 math=8", [&](int c) { k_soa1<8><<<N / 256, 256>>>(soa[c], N, out); });
     // a plain device-to-device copy of the same 32 MiB (read + write) for reference
