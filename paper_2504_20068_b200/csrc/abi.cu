@@ -16,6 +16,10 @@
 #include "replay.cuh"
 #include "shard.cuh"
 #include "multi.cuh"
+
+#ifndef JIT_CMP_COST
+#define JIT_CMP_COST 3
+#endif
 #include "exact_api.h"
 
 using namespace jit;
@@ -56,6 +60,7 @@ struct jit_sched {
     bool unfinished = false;          // a step was launched and not finished (step_async)
     uint64_t launched = 0;            // steps launched (the stamp rebase runs every 2^30)
     unsigned long long multi_epoch = 0;   // power-of-K reconciles so far (tags S.mwin words)
+    uint32_t bal_w_graph = 0;             // S.bal_w captured in the step graph
     cudaEvent_t ev[6] = {};
     cudaGraphNode_t ev_node[5] = {};      // event-record nodes of the timed graph
     std::vector<cudaEvent_t> slots;       // 5 events per recorded step
@@ -115,25 +120,44 @@ static void carve(Carve& cv, const jit_config* cfg, const jit_len_table* tab, Po
     const uint64_t N = ((uint64_t)cfg->capacity + 63) & ~63ull;
     const uint64_t NT = (uint64_t)cfg->task_capacity + 1;
     const bool dbg = (cfg->flags & JIT_CFG_DEBUG_ROWS) != 0;
+    // what every step touches first, packed together ahead of the pool (few pages: the step's
+    // first loads and the resolve stay on a handful of TLB entries): control state, SLO groups, the
+    // speculative set, the batch, the work items; then the hot rows and the compound pass's task
+    // arrays; the exact path's and the loaders' scratch last
+    S.persist = cv.take<Persist>(1);
+    S.spec_cnt = cv.take<unsigned int>(1);
+    S.gpart = cv.take<BlockPart>(1);
+    ctrl = cv.take<Ctrl>(1);
+    n_items = cv.take<uint32_t>(1);
+    groups = cv.take<Group>(256);
+    S.out_ids = cv.take<uint32_t>(cfg->max_batch + 1); S.out_tokens = cv.take<uint32_t>(cfg->max_batch + 1);
+    S.out_rows = cv.take<uint32_t>(cfg->max_batch + 1);
+    S.spec_img = cv.take<uint64_t>(kSpecCap);
+    S.spec_id = cv.take<uint32_t>(kSpecCap); S.spec_row = cv.take<uint32_t>(kSpecCap);
+    S.spec_cost = cv.take<uint32_t>(kSpecCap); S.spec_len = cv.take<uint32_t>(kSpecCap);
+    S.spec_meta = cv.take<uint32_t>(kSpecCap); S.spec_aux = cv.take<uint32_t>(kSpecCap);
+    items = cv.take<Item>(item_capacity(N, NT));
+    S.items = items; S.n_items = n_items;
     P.rows = cv.take<HotRow>(N);
-    P.id = cv.take<uint32_t>(N); P.task = cv.take<uint32_t>(N); P.ovr = cv.take<uint32_t>(N);
+    P.task = cv.take<uint32_t>(N);
+    P.call_off = cv.take<uint32_t>(NT + 8);
+    P.tinfo = cv.take<TaskInfo>(NT); P.tever = cv.take<uint32_t>(NT + 4);   // + bulk-copy padding
+    P.crng = cv.take<uint2>(NT + 2);
+    P.id = cv.take<uint32_t>(N); P.ovr = cv.take<uint32_t>(N);
     P.fair = cv.take<uint32_t>(N);
     P.img = cv.take<uint64_t>(N); P.cost = cv.take<uint32_t>(N);
     P.dbg_rate = dbg ? cv.take<double>(N) : nullptr;
     P.dbg_trem = dbg ? cv.take<int64_t>(N) : nullptr;
     P.dbg_lhat = dbg ? cv.take<uint32_t>(N) : nullptr;
-    P.call_off = cv.take<uint32_t>(NT + 8); P.t_arr = cv.take<int64_t>(NT); P.t_dl = cv.take<int64_t>(NT);
+    P.t_arr = cv.take<int64_t>(NT); P.t_dl = cv.take<int64_t>(NT);
     P.cur_stage = cv.take<uint32_t>(NT); P.n_stages = cv.take<uint32_t>(NT);
     P.pattern = cv.take<uint32_t>(NT * kMaxStages); P.gdone = cv.take<uint64_t>(NT);
-    P.tinfo = cv.take<TaskInfo>(NT); P.tever = cv.take<uint32_t>(NT + 4);   // + bulk-copy padding
-    P.crng = cv.take<uint2>(NT + 2);
     uint64_t mc = 1024;
     while (mc < 2 * N) mc <<= 1;
     P.idmap = cv.take<unsigned long long>(mc);
     P.map_mask = (uint32_t)(mc - 1);
     T.edges = cv.take<uint32_t>(tab->n_bins);
     T.cum = cv.take<uint32_t>((uint64_t)tab->n_rows * tab->n_bins);
-    groups = cv.take<Group>(256);
     S.hcnt = cv.take<uint32_t>(4096); S.hcost = cv.take<unsigned long long>(4096);
     S.bucket_ck = cv.take<u128>(kBucketCap); S.bucket_cost = cv.take<uint32_t>(kBucketCap);
     uint64_t P2 = 1;                       // bitonic sorts pad |Cd| to a power of two
@@ -141,21 +165,8 @@ static void carve(Carve& cv, const jit_config* cfg, const jit_len_table* tab, Po
     S.cand = cv.take<uint32_t>(N); S.sk = cv.take<uint64_t>(P2); S.sv = cv.take<uint32_t>(P2);
     S.pc = cv.take<unsigned long long>(N + 1);
     S.pf = cv.take<u128>(P2 + 1);          // also the u128 sort keys of the shard merge (pow2 slots)
-    S.out_ids = cv.take<uint32_t>(cfg->max_batch + 1); S.out_tokens = cv.take<uint32_t>(cfg->max_batch + 1);
-    S.out_rows = cv.take<uint32_t>(cfg->max_batch + 1);
     S.cand_cap = (uint32_t)N;
     S.mwin = cv.take<unsigned long long>(N);
-    S.spec_img = cv.take<uint64_t>(kSpecCap);
-    S.spec_id = cv.take<uint32_t>(kSpecCap); S.spec_row = cv.take<uint32_t>(kSpecCap);
-    S.spec_cost = cv.take<uint32_t>(kSpecCap); S.spec_len = cv.take<uint32_t>(kSpecCap);
-    S.spec_meta = cv.take<uint32_t>(kSpecCap); S.spec_aux = cv.take<uint32_t>(kSpecCap);
-    S.persist = cv.take<Persist>(1);
-    S.spec_cnt = cv.take<unsigned int>(1);
-    S.gpart = cv.take<BlockPart>(1);
-    items = cv.take<Item>(item_capacity(N, NT));
-    n_items = cv.take<uint32_t>(1);
-    S.items = items; S.n_items = n_items;
-    ctrl = cv.take<Ctrl>(1);
     // load / per-step delta staging: 48 B per row (the SoA fields of jit_pool) + 72 B per task
     load = cv.take<unsigned char>(48 * N + 72 * NT + 256);
 }
@@ -396,6 +407,15 @@ extern "C" int jit_sched_load(jit_sched* h, const jit_pool* p) {
     if (h->h_items.size() > h->item_cap) return set_err(h, JIT_ECAPACITY, "too many work items");
     const uint32_t n_items = (uint32_t)h->h_items.size();
     h->n_items_host = n_items;
+    h->S.n_ring_h = n_items - h->S.n_std_items;
+    // a compound call costs k_score about JIT_CMP_COST standalone rows (profiles: per-row
+    // instruction counts); the standalone slabs are spread against the ring items accordingly
+    {
+        const uint64_t n_ring = n_items - h->S.n_std_items, n_cmp = (uint64_t)P.n - P.n_single;
+        h->S.bal_w = n_ring ? (uint32_t)std::min<uint64_t>(1u << 24, 256ull * JIT_CMP_COST * n_cmp / (32ull * n_ring)) : 0u;
+        if (h->S.bal_w != h->bal_w_graph) h->graph_dirty = true;
+        h->bal_w_graph = h->S.bal_w;
+    }
     if (n_items)
         CK(cudaMemcpyAsync(h->d_items, h->h_items.data(), sizeof(Item) * n_items, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemcpyAsync(h->d_n_items, &h->n_items_host, 4, cudaMemcpyHostToDevice, h->stream));
@@ -737,6 +757,7 @@ static int apply_deltas(jit_sched* h, const jit_step_in* in) {
         const uint32_t n_items = (uint32_t)h->h_items.size();
         CK(cudaMemcpyAsync(h->d_items + i0, h->h_items.data() + i0, sizeof(Item) * (n_items - i0), cudaMemcpyHostToDevice, s));
         h->n_items_host = n_items;
+        h->S.n_ring_h = n_items - h->S.n_std_items;
         CK(cudaMemcpyAsync(h->d_n_items, &h->n_items_host, 4, cudaMemcpyHostToDevice, s));
         h->grid_pass = std::max<uint32_t>(1, std::min<uint32_t>((P.n + kPassThreads - 1) / kPassThreads, (uint32_t)h->n_sm * 4));
     }

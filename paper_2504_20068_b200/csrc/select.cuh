@@ -118,6 +118,8 @@ struct Scratch {
     const uint32_t* n_items; // device count of items (appends grow it without a graph update)
     uint32_t item_cap;         // capacity of items[] (every slot readable)
     uint32_t n_std_items;      // items [0, n_std_items) are the standalone chunks of [0, n_single)
+    uint32_t bal_w;            // k_score balance: cost of one ring item in 1/256 standalone slabs (std_slabs)
+    uint32_t n_ring_h;         // ring items at launch (host count; only balances the standalone slabs)
     unsigned int* spec_cnt;  // size of the speculative set (k_score atomics; reset by k_spec)
     Ctrl* h_ctrl;            // pinned host copy of the control block, written by the step's last kernel
     uint32_t* h_batch;       // pinned host mirror of the batch: ids | tokens | rows, (max_batch + 1) each

@@ -42,6 +42,10 @@ constexpr uint32_t kScoreWarps = kScoreThreads / 32;
 constexpr uint32_t kR = JIT_ROWS_PER_LANE;      // hot rows per lane per item chunk
 constexpr uint32_t kItemRows = 32 * kR;         // rows per item (chunk)
 constexpr uint32_t kItemTasks = 32;             // tasks per compound item (one per lane; <= 32)
+#ifndef JIT_STD_ROWS_PER_LANE
+#define JIT_STD_ROWS_PER_LANE 2
+#endif
+constexpr uint32_t kRs = JIT_STD_ROWS_PER_LANE;  // standalone rows per lane per chunk (direct loads)
 static_assert(kItemTasks <= 32, "a compound item's task sums live in one lane each");
 
 // per-group constants of the pass, with `now` folded in (per launch):
@@ -202,38 +206,49 @@ __device__ __forceinline__ HotRow ld_row_s(const HotRow* p) {
 }
 
 // the rows with key >= t join the speculative set (one ballot per row slab; rare)
-template <typename RowAt>
+template <uint32_t KR, typename RowAt>
 __device__ __forceinline__ void spec_rows(const Scratch& S, const Pool& P, const Cfg& c, uint32_t mem_m,
                                           const uint64_t* img, uint32_t base, RowAt row_at) {
     const uint32_t lane = threadIdx.x & 31;
     if (!__any_sync(0xffffffffu, mem_m)) return;
 #pragma unroll
-    for (uint32_t k = 0; k < kR; ++k) {
+    for (uint32_t k = 0; k < KR; ++k) {
         const bool take = (mem_m >> k) & 1u;
         const uint32_t r = base + 32 * k + lane;
         spec_add(S, P, c, take, img[k], r, take ? row_at(k, r) : HotRow{0, 0, 0, 0, 0, 0, 0});
     }
 }
 
-// ---- one standalone item: rows [it.r0, it.r1), staged in slot `sl`; kR rows per lane whose
-// arithmetic chains interleave (warp votes only per item: rare work, divisions, set members)
-template <bool kMat, bool kDebug, bool kAppB>
-__device__ __forceinline__ void std_item(const Pool& P, const Table& T, const GroupNow* sg, const Cfg& c,
+// 256-bit load of a hot row straight from global memory (sm_100: LDG.E.256), read once per
+// pass (no L1 allocation, evict-first in L2: the pool streams through L2 once per step)
+__device__ __forceinline__ HotRow ld_row_g(const HotRow* p) {
+    uint32_t a0, a1, a2, a3, a4, a5, a6, a7;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3), "=r"(a4), "=r"(a5), "=r"(a6), "=r"(a7) : "l"(p));
+    HotRow r;
+    r.arr = (int64_t)(((uint64_t)a1 << 32) | a0);
+    r.len_in = a2; r.gen = a3; r.pre = a4; r.lrow = a5; r.meta = a6; r.since = a7;
+    return r;
+}
+
+// ---- standalone rows r0 + 32 k + lane (k < KR, valid while 32 k + lane < nr), already loaded in
+// q; KR rows per lane whose arithmetic chains interleave (warp votes only per chunk: rare work,
+// divisions, set members)
+template <bool kMat, bool kDebug, bool kAppB, uint32_t KR>
+__device__ __forceinline__ void std_core(const Pool& P, const Table& T, const GroupNow* sg, const Cfg& c,
                                          const Scratch& S, int64_t now, double v_d, int64_t v, uint32_t sc,
-                                         uint64_t t_img, float t_lo_f, const Item& it, WarpSlot* sl, Part& A) {
+                                         uint64_t t_img, float t_lo_f, uint32_t r0, uint32_t nr, HotRow (&q)[KR],
+                                         Part& A) {
     const uint32_t lane = threadIdx.x & 31;
     const double eps_d = (double)c.eps;
     const float v_f = (float)v, eps_f = (float)c.eps;
     const int64_t drop_before = now - c.waiting;           // now - arr > waiting <=> arr < now - waiting
-    const uint32_t nr = it.r1 - it.r0;
     const bool blend = c.fair_num != 0;                    // NEXT-2: no pre-test, exact keys blended
-    HotRow q[kR];
     uint32_t pend_m = 0, rare_m = 0, drop_m = 0;
 #pragma unroll
-    for (uint32_t k = 0; k < kR; ++k) {                    // (a1) admission / pending; what is rare
+    for (uint32_t k = 0; k < KR; ++k) {                    // (a1) admission / pending; what is rare
         const uint32_t o = 32 * k + lane;
         const bool valid = o < nr;
-        q[k] = valid ? ld_row_s(sl->rows + o) : HotRow{0, 0, 0, 0, 0, 0, 0};
         const HotRow& x = q[k];
         const uint32_t st = m_state(x.meta), fl = m_flags(x.meta);
         const bool arrived = valid && x.arr <= now;
@@ -249,19 +264,19 @@ __device__ __forceinline__ void std_item(const Pool& P, const Table& T, const Gr
     A.drop += __popc(drop_m);
     if (__any_sync(0xffffffffu, rare_m)) {                 // stamp regime, stale bound (rare)
 #pragma unroll
-        for (uint32_t k = 0; k < kR; ++k) {
+        for (uint32_t k = 0; k < KR; ++k) {
             if (!((rare_m >> k) & 1u)) continue;
             const bool pend = (pend_m >> k) & 1u;
             const uint32_t ep = fastdiv(q[k].gen, c.R, c.R_m, c.R_l);
-            rare_row(T, c, P.rows + it.r0 + 32 * k + lane, q[k], pend, (drop_m >> k) & 1u,
+            rare_row(T, c, P.rows + r0 + 32 * k + lane, q[k], pend, (drop_m >> k) & 1u,
                      pend && m_epoch(q[k].meta) != ep + 1u, ep, sc, A.ref);
         }
     }
     // (a3) t_rem, (a5) goodput (A9-A11, A22), starvation inflation (A12), the pre-test
-    uint32_t Gk32[kR], Lr[kR];
+    uint32_t Gk32[KR], Lr[KR];
     uint32_t div_m = 0;
 #pragma unroll
-    for (uint32_t k = 0; k < kR; ++k) {
+    for (uint32_t k = 0; k < KR; ++k) {
         const HotRow& x = q[k];
         const bool pend = (pend_m >> k) & 1u;
         const uint32_t Lh = max(l_hat(x.lrow), x.gen + 1);
@@ -269,7 +284,7 @@ __device__ __forceinline__ void std_item(const Pool& P, const Table& T, const Gr
         const GroupNow G = sg[m_group(x.meta)];
         const int64_t trem = x.arr + G.bn + (int64_t)((uint64_t)(Lh - 1) * G.tok);
         uint64_t Gk = (uint64_t)G.w_in * x.len_in + (uint64_t)G.w_out * Lh;
-        if (m_flags(x.meta) & kOverride) Gk = __ldg(P.ovr + it.r0 + 32 * k + lane);   // App. D sets R(k)
+        if (m_flags(x.meta) & kOverride) Gk = __ldg(P.ovr + r0 + 32 * k + lane);   // App. D sets R(k)
         if (trem <= 0) Gk = 0;
         if (kAppB && (uint64_t)len_rem * (uint64_t)v > (uint64_t)(trem > 0 ? trem : 0)) Gk = 0;
         const uint32_t waited = min(sc - x.since, 0xFFFFu);
@@ -278,44 +293,56 @@ __device__ __forceinline__ void std_item(const Pool& P, const Table& T, const Gr
         Gk32[k] = (uint32_t)Gp; Lr[k] = len_rem;
         div_m |= (uint32_t)(pend && (kMat || blend || !below_t((uint32_t)Gp, len_rem, v_f, eps_f, t_lo_f))) << k;
         if (kDebug && 32 * k + lane < nr) {
-            const uint32_t r = it.r0 + 32 * k + lane;
+            const uint32_t r = r0 + 32 * k + lane;
             P.dbg_rate[r] = pend ? make_rate(len_rem, trem) : 0.0;
             P.dbg_trem[r] = pend ? trem : 0;
             P.dbg_lhat[r] = pend ? Lh : 0u;
         }
     }
-    uint64_t img[kR];
+    uint64_t img[KR];
 #pragma unroll
-    for (uint32_t k = 0; k < kR; ++k) img[k] = ((pend_m >> k) & 1u) ? 0ull : kNone;   // 0: below t
+    for (uint32_t k = 0; k < KR; ++k) img[k] = ((pend_m >> k) & 1u) ? 0ull : kNone;   // 0: below t
     if (__any_sync(0xffffffffu, div_m)) {
 #pragma unroll
-        for (uint32_t k = 0; k < kR; ++k)
+        for (uint32_t k = 0; k < KR; ++k)
             if ((div_m >> k) & 1u)
                 img[k] = (uint64_t)__double_as_longlong(div_rn_int(__dmul_rn(__uint2double_rn(Gk32[k]), 1e9),
                                                                    __fma_rn(__uint2double_rn(Lr[k]), v_d, eps_d)));
         if (blend) {                                       // NEXT-2 fairness blend (A47), every pending row
 #pragma unroll
-            for (uint32_t k = 0; k < kR; ++k)
+            for (uint32_t k = 0; k < KR; ++k)
                 if ((div_m >> k) & 1u)
                     img[k] = (uint64_t)__double_as_longlong(blend_fair(__longlong_as_double((long long)img[k]),
-                                                                       __ldg(P.fair + it.r0 + 32 * k + lane),
+                                                                       __ldg(P.fair + r0 + 32 * k + lane),
                                                                        c.fair_num, c.fair_den));
         }
     }
     A.pend += __popc(pend_m);
     uint32_t mem_m = 0;
 #pragma unroll
-    for (uint32_t k = 0; k < kR; ++k) {
+    for (uint32_t k = 0; k < KR; ++k) {
         const uint32_t o = 32 * k + lane;
         mem_m |= (uint32_t)(((pend_m >> k) & 1u) && img[k] >= t_img) << k;
         if (kMat && o < nr) {
             const bool pend = (pend_m >> k) & 1u;
-            P.img[it.r0 + o] = img[k];
-            P.cost[it.r0 + o] = pend ? token_cost(q[k].len_in, q[k].pre, c.chunk) : 0u;
+            P.img[r0 + o] = img[k];
+            P.cost[r0 + o] = pend ? token_cost(q[k].len_in, q[k].pre, c.chunk) : 0u;
             if (pend && img[k] < A.mn) A.mn = img[k];
         }
     }
-    spec_rows(S, P, c, mem_m, img, it.r0, [&](uint32_t k, uint32_t) { return q[k]; });
+    spec_rows<KR>(S, P, c, mem_m, img, r0, [&](uint32_t k, uint32_t) { return q[k]; });
+}
+
+// one standalone item staged in the ring slot `sl` (rows appended after a load)
+template <bool kMat, bool kDebug, bool kAppB>
+__device__ __forceinline__ void std_item(const Pool& P, const Table& T, const GroupNow* sg, const Cfg& c,
+                                         const Scratch& S, int64_t now, double v_d, int64_t v, uint32_t sc,
+                                         uint64_t t_img, float t_lo_f, const Item& it, WarpSlot* sl, Part& A) {
+    const uint32_t lane = threadIdx.x & 31, nr = it.r1 - it.r0;
+    HotRow q[kR];
+#pragma unroll
+    for (uint32_t k = 0; k < kR; ++k) q[k] = 32 * k + lane < nr ? ld_row_s(sl->rows + 32 * k + lane) : HotRow{0, 0, 0, 0, 0, 0, 0};
+    std_core<kMat, kDebug, kAppB, kR>(P, T, sg, c, S, now, v_d, v, sc, t_img, t_lo_f, it.r0, nr, q, A);
 }
 
 // ---- one compound item: whole tasks [it.t0, it.t1) on rows [it.r0, it.r1), staged in slot
@@ -466,7 +493,12 @@ __device__ __forceinline__ void cmp_item(const Pool& P, const Table& T, const Gr
             const uint64_t t_gen = Tsum * (uint64_t)v;
             if (kAppB && t_gen > (uint64_t)(trem > 0 ? trem : 0)) Gt = 0;
             const uint64_t Bi = t_gen + (uint64_t)c.eps;
+            // exact range: Tsum v without overflow (high word 0), + eps below 2^53
+#ifdef JIT_DIV64
             if (Bi < kTwo53 && Bi >= t_gen && t_gen / (uint64_t)v == Tsum) Bd = __ull2double_rn(Bi);
+#else
+            if (Bi < kTwo53 && Bi >= t_gen && __umul64hi(Tsum, (uint64_t)v) == 0) Bd = __ull2double_rn(Bi);
+#endif
         }
         ts.G[i] = Gt; ts.B[i] = Bd; ts.Bf[i] = Bd < 0.0 ? 1.0f : __double2float_rn(Bd);
     }
@@ -549,7 +581,7 @@ __device__ __forceinline__ void cmp_item(const Pool& P, const Table& T, const Gr
                 if (pend && img[k] < A.mn) A.mn = img[k];
             }
         }
-        spec_rows(S, P, c, mem_m, img, base, [&](uint32_t, uint32_t r) { return row_at(r); });
+        spec_rows<kR>(S, P, c, mem_m, img, base, [&](uint32_t, uint32_t r) { return row_at(r); });
     }
     __syncwarp();
 #ifdef JIT_TIMELINE
@@ -595,6 +627,28 @@ __host__ __device__ constexpr uint32_t score_smem_bytes(uint32_t n_groups) {
     return (uint32_t)(((sizeof(GroupNow) * n_groups + 127) & ~127ull) + sizeof(WarpSmem) * kScoreWarps);
 }
 
+// The standalone slabs of warp w (of W): a warp that owns more ring items (compound tasks, cost
+// bal_w / 256 slabs each) gets fewer slabs, so that every warp's share of the pass is about the
+// same.  Closed form: quota q = max(0, t - bal_w * ring items) in 1/256 slab, t = the mean share;
+// warp w starts at f(w) = floor(n32 * (sum of the quotas before it) / (sum of all quotas)).  f is
+// evaluated in fp64 with one reciprocal (no 64-bit division at kernel entry): the same monotone expression
+// on every warp, so consecutive ranges meet exactly; the last warp ends at n32.
+__device__ __forceinline__ void std_slabs(uint32_t w, uint32_t W, uint32_t n32, uint32_t n_ring, uint32_t bal_w,
+                                          uint32_t& s0, uint32_t& s1) {
+    const uint64_t B = bal_w, T = (uint64_t)n32 * 256u + B * n_ring;
+    const uint64_t t = (uint64_t)__double2ull_rd(__dmul_rn(__ull2double_rn(T), __drcp_rn((double)W)));
+    const uint32_t base = n_ring / W, ex = n_ring - base * W;
+    const uint64_t qhi = t > B * (base + 1) ? t - B * (base + 1) : 0, qlo = t > B * base ? t - B * base : 0;
+    auto pre = [&](uint64_t x) { return (x < ex ? x : ex) * qhi + (x > ex ? x - ex : 0) * qlo; };
+    const double tot = __ull2double_rn(pre(W)), n = (double)n32, rt = __drcp_rn(tot);
+    auto f = [&](uint32_t x) -> uint32_t {
+        if (x >= W) return n32;
+        return min(n32, (uint32_t)__double2uint_rd(__dmul_rn(__dmul_rn(n, __ull2double_rn(pre(x))), rt)));
+    };
+    s0 = tot > 0.0 ? f(w) : 0u;
+    s1 = tot > 0.0 ? f(w + 1) : 0u;
+}
+
 // mode 0: a step (partials counted, speculative set collected); mode 1: re-score for the exact
 // path (kMat; keys and costs only, nothing counted again -- the pool state is already this
 // step's, so the pass is idempotent)
@@ -613,28 +667,61 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
 #endif
     const uint32_t W = gridDim.x * kScoreWarps;
     const uint32_t i0 = blockIdx.x * kScoreWarps + warp;
+    uint32_t s0 = 0, s1 = 0;
+    HotRow cur[kRs], nxt[kRs];
+    auto load = [&](HotRow* q, uint32_t sb) {
+#pragma unroll
+        for (uint32_t k = 0; k < kRs; ++k) {
+            const uint32_t r = 32 * (sb + k) + lane;
+            q[k] = (sb + k < s1 && r < P.n_single) ? ld_row_g(P.rows + r) : HotRow{0, 0, 0, 0, 0, 0, 0};
+        }
+    };
     // every independent global load of the prologue at once (one round trip): the handle's
-    // counters, the item count and this warp's item descriptors (item j in lane j; beyond 32 read
-    // when needed; the items array is readable up to its capacity)
-    const Persist ps = *S.persist;
-    const uint32_t n_items = *S.n_items;
+    // counters and the item count (one thread per CTA: every warp reading the same line would queue
+    // 4x the requests on one L2 slice), the SLO groups, this warp's ring-item descriptors (ring item
+    // j in lane j; beyond 32 read when needed; the items array is readable up to its capacity).
+    // The ring items are items [n_std_items, n_items): compound tasks and standalone rows appended
+    // since the load.
+    __shared__ Persist s_ps;
+    __shared__ uint32_t s_n_items;
+    if (threadIdx.x == 0) { s_ps = *S.persist; s_n_items = *S.n_items; }
+    const uint32_t nstd = S.n_std_items;
     Item dsc{0, 0, 0, 0};
-    if (i0 + lane * W < S.item_cap) dsc = S.items[i0 + lane * W];
+    if (nstd + i0 + lane * W < S.item_cap) dsc = S.items[nstd + i0 + lane * W];
     Group g0{};
     if (threadIdx.x < n_groups) g0 = groups[threadIdx.x];
+    // while those are in flight: this warp's standalone slabs (balanced against the ring items it
+    // owns, std_slabs; the host's ring count at launch) and the first chunk's row loads
+#if !defined(JIT_SKIP_STD) && !defined(JIT_DEV_NRING)
+    std_slabs(i0, W, (P.n_single + 31) >> 5, S.n_ring_h, S.bal_w, s0, s1);
+#ifndef JIT_ROWS_AFTER_PS
+    if (s0 < s1) load(cur, s0);
+#endif
+#endif
+    __syncthreads();
+    const Persist ps = s_ps;
+    const uint32_t n_items = s_n_items;
     if (mode == 0 && ps.host_pending) {                    // chained after a step that needs the host
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&S.persist->skipped, 1u);
         return;
     }
+#if !defined(JIT_SKIP_STD) && !defined(JIT_DEV_NRING) && defined(JIT_ROWS_AFTER_PS)
+    if (s0 < s1) load(cur, s0);
+#endif
+#ifdef JIT_TIMELINE
+    const unsigned long long tpa = gt();
+#endif
     GroupNow* sg = reinterpret_cast<GroupNow*>(smem);
     WarpSmem* ws = reinterpret_cast<WarpSmem*>(smem + ((sizeof(GroupNow) * n_groups + 127) & ~127ull)) + warp;
-    const uint32_t n_mine = i0 < n_items ? (n_items - i0 + W - 1) / W : 0u;   // items i0 + j W of this warp
+    const uint32_t n_ring = n_items > nstd ? n_items - nstd : 0u;
+    const uint32_t n_mine = i0 < n_ring ? (n_ring - i0 + W - 1) / W : 0u;   // ring items i0 + j W of this warp
+#if !defined(JIT_SKIP_STD) && defined(JIT_DEV_NRING)
+    std_slabs(i0, W, (P.n_single + 31) >> 5, n_ring, S.bal_w, s0, s1);
+    if (s0 < s1) load(cur, s0);
+#endif
     const uint64_t pol = evict_first_policy();
     auto item_j = [&](uint32_t j) -> Item {                // warp-uniform j
-        const uint32_t i = i0 + j * W;
-        if (i < S.n_std_items)                             // standalone chunks come first: arithmetic
-            return Item{i * kItemRows, min(i * kItemRows + kItemRows, P.n_single), 0u, 0u};
-        if (j >= 32) return S.items[i];
+        if (j >= 32) return S.items[nstd + i0 + j * W];
         return Item{__shfl_sync(0xffffffffu, dsc.r0, j), __shfl_sync(0xffffffffu, dsc.r1, j),
                     __shfl_sync(0xffffffffu, dsc.t0, j), __shfl_sync(0xffffffffu, dsc.t1, j)};
     };
@@ -646,6 +733,9 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
         const Item it = item_j(s);
         if (lane == 0) issue_item(P, it, &ws->slot[s], &ws->bar[s], pol);
     }
+#ifdef JIT_TIMELINE
+    const unsigned long long tpb = gt();
+#endif
     for (uint32_t g = threadIdx.x; g < n_groups; g += kScoreThreads) {
         const Group G = g < kScoreThreads ? g0 : groups[g];
         GroupNow x;
@@ -665,6 +755,9 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
     const float t_lo_f = t_img == kNone ? __int_as_float(0x7F800000)
                                         : __double2float_rz(__dmul_rn(__longlong_as_double((long long)t_img),
                                                                       1.0 - 1.52587890625e-05));
+#ifdef JIT_TIMELINE
+    const unsigned long long tpc = gt();
+#endif
     __syncthreads();
     pdl_launch_dependents();                               // k_spec may launch now (it waits for us)
 #ifdef JIT_TIMELINE
@@ -674,6 +767,24 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
 #endif
     Part A{0u, 0u, 0u, 0u, kNone};
     const double v_d = (double)v;
+#ifndef JIT_SKIP_STD
+    // ---- the standalone rows [0, n_single): kRs rows per lane read with 256-bit loads straight
+    // into registers, the next chunk's loads issued before the current chunk is scored
+    for (uint32_t sb = s0; sb < s1; sb += kRs) {           // warp-uniform
+        if (sb + kRs < s1) load(nxt, sb + kRs);
+        const uint32_t nr = min(32u * min(s1 - sb, kRs), P.n_single - 32u * sb);
+#ifdef JIT_STD_FLOOR
+        if (cur[0].gen == 0xFFFFFFFFu || cur[kRs - 1].gen == 0xFFFFFFFFu) A.err = 1;
+#else
+        std_core<kMat, kDebug, kAppB, kRs>(P, T, sg, c, S, now, v_d, v, sc, t_img, t_lo_f, 32u * sb, nr, cur, A);
+#endif
+#pragma unroll
+        for (uint32_t k = 0; k < kRs; ++k) cur[k] = nxt[k];
+    }
+#endif
+#ifdef JIT_TIMELINE
+    tls = gt() - tl1; nls = (s1 - s0 + kRs - 1) / kRs;     // the standalone phase and its chunks
+#endif
     uint32_t s = 0, par = 0;                               // ring position and its phase parity
     for (uint32_t j = 0; j < n_mine; ++j) {
         const Item it = item_j(j);
@@ -690,12 +801,8 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
         if (lane == 0 && ws->slot[s].rows[0].gen == 0xFFFFFFFFu) A.err = 1;
         if (false)
 #endif
-#ifdef JIT_SKIP_STD
-        if (it.t1 == it.t0) { if (lane == 0 && ws->slot[s].rows[0].gen == 0xFFFFFFFFu) A.err = 1; } else
-#else
         if (it.t1 == it.t0) std_item<kMat, kDebug, kAppB>(P, T, sg, c, S, now, v_d, v, sc, t_img, t_lo_f, it, &ws->slot[s], A);
         else
-#endif
 #ifdef JIT_SKIP_CMP
         { if (lane == 0 && ws->slot[s].rows[0].gen == 0xFFFFFFFFu) A.err = 1; }
 #else
@@ -703,7 +810,7 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
 #endif
         __syncwarp();                                      // every lane is done with the slot
 #ifdef JIT_TIMELINE
-        if (it.t1 == it.t0) { tls += gt() - tw1; ++nls; } else { tlc += gt() - tw1; ++nlc; }
+        tlc += gt() - tw1; ++nlc;
 #endif
         if (j + kStagesW < n_mine) {
             const Item nx = item_j(j + kStagesW);
@@ -717,7 +824,8 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
     store_part(S.gpart, ctrl, A, mode == 0, kMat);
 #ifdef JIT_TIMELINE
     if (lane == 0) { tl[0] = tl0; tl[1] = tl1; tl[2] = tl2; tl[3] = gt(); tl[4] = tlw; tl[5] = n_mine;
-                     tl[6] = tls | ((unsigned long long)nls << 48); tl[7] = tlc | ((unsigned long long)nlc << 48); }
+                     tl[6] = tls | ((unsigned long long)nls << 48); tl[7] = tlc | ((unsigned long long)nlc << 48);
+                     tl[12] = tpa - tl0; tl[13] = tpb - tl0; tl[14] = tpc - tl0; }
 #endif
 }
 

@@ -33,8 +33,9 @@ for rep in range(3):
         print(f"  {name:10s} ns  {q(a)}")
     ts_, ns_ = t[:, 6] & ((1 << 48) - 1), t[:, 6] >> 48
     tc_, nc_ = t[:, 7] & ((1 << 48) - 1), t[:, 7] >> 48
+    print(f"  prologue: persist in {q(t[:, 12])}; ring filled {q(t[:, 13])}; groups done {q(t[:, 14])}")
     nc = t[:, 11].sum()
     if nc:
         print(f"  cmp item phases ns: A {t[:, 8].sum() / nc:.0f}  per-task {t[:, 9].sum() / nc:.0f}  B {t[:, 10].sum() / nc:.0f}")
-    print(f"  per std item ns {ts_.sum() / max(ns_.sum(), 1):.0f} ({ns_.sum()} items); per cmp item ns "
-          f"{tc_.sum() / max(nc_.sum(), 1):.0f} ({nc_.sum()} items)")
+    print(f"  standalone phase ns {q(ts_)}; per chunk {ts_.sum() / max(ns_.sum(), 1):.0f} ({ns_.sum()} chunks)")
+    print(f"  ring items ns {q(tc_)}; per item {tc_.sum() / max(nc_.sum(), 1):.0f} ({nc_.sum()} items)")
