@@ -536,6 +536,43 @@ def next_lines(args, dev, stream, Scheduler):
     out["blend_k_score"] = {"metric": "k_score ms per 2^20-row C3 pool with the fairness blend (f = 1/10)",
                             "value": k_ms, "unit": "ms", "alg_bytes": alg_bytes(dd) + 4 * len(pool["id"]),
                             "note": "the blend needs every pending key exactly (no fp32 pre-test) plus Fair(r)"}
+    # ---- NEXT-2 power-of-K: the C3 standalone requests, each with dummies on K = 2 of M = 8
+    # replicas (replica v_token 0.8-1.2x), one multi-replica step = 8 replica steps + the proposal
+    # exchange + 8 reconciles (all replicas on this GPU; across GPUs the exchange is an allgather)
+    from paper_2504_20068_b200.jitsched import multi_step
+    M, K = 8, 2
+    pools = W.replica_pools(dd, M, K, seed=5)
+    vs = [int(v) for v in np.linspace(0.8, 1.2, M) * dd["v_token_ns"]]
+    reps = [Scheduler(dd["cfg"], dd["groups"], dd["table"], capacity=len(p["id"]), task_capacity=1, device=dev,
+                      stream=stream) for p in pools]
+    for r_, p in zip(reps, pools):
+        r_.load(p, None)
+    ref = oracle.multi_step(dd["cfg"], dd["groups"], dd["table"], dd["now_ns"], vs,
+                            [{k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in p.items()} for p in pools])
+    got = multi_step(reps, dd["now_ns"], vs)
+    same = all(np.array_equal(g_["batch_ids"], r_["batch_ids"]) for g_, r_ in zip(got, ref))
+    t0 = time.perf_counter()
+    n_mstep = 20
+    for _ in range(n_mstep):
+        got = multi_step(reps, dd["now_ns"], vs)
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) / n_mstep
+    tc0 = time.perf_counter()
+    oracle.multi_step(dd["cfg"], dd["groups"], dd["table"], dd["now_ns"], vs,
+                      [{k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in p.items()} for p in pools])
+    tc = time.perf_counter() - tc0
+    rows_m = sum(len(p["id"]) for p in pools)
+    for r_ in reps:
+        r_.close()
+    out["power_of_k"] = {"metric": "dummy rows scheduled/sec (power-of-K, M = 8 replicas, K = 2)",
+                         "value": rows_m / wall, "unit": "rows/s", "ms_per_multi_step": wall * 1e3,
+                         "rows": rows_m, "selected_total": int(sum(g_["n_selected"] for g_ in got)),
+                         "first_step_equal_to_oracle": bool(same),
+                         "how": "wall clock of synchronous multi_step calls (8 jit_sched_step + exports + 8 "
+                                "jit_multi_reconcile on one GPU)",
+                         "cpu_baseline": {"value": rows_m / tc, "unit": "rows/s", "cores": 1, "kind": "oracle",
+                                          "sample": "one oracle multi_step over the same 8 replica pools"},
+                         "workload": "C3's 2^20-row pool, its standalone rows with dummies on 2 of 8 replicas"}
     # ---- NEXT-3: pattern matching, C4-scale
     store = W.pattern_store(61, n_patterns=500)
     q = W.pattern_queries(62, store, 100_000)

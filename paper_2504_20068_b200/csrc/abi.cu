@@ -6,6 +6,7 @@
 #include <new>
 #include <string>
 #include <vector>
+#include <algorithm>
 #include <cstdlib>
 
 #include "jit_sched.h"

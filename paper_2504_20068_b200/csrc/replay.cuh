@@ -92,10 +92,14 @@ __device__ __forceinline__ void score_standalone(const Cfg& c, const Table& T, c
 
 namespace jit {
 
+// one replay = one CTA: 512 threads when a few replays run (one long trace: the per-step passes
+// spread wide), 256 threads x several CTAs per SM for sweeps (more replays in flight per SM: the
+// step is barrier- and latency-bound, measured 1.8x the sweep throughput)
 constexpr uint32_t kReplayThreads = 512;
+constexpr uint32_t kReplayThreadsSweep = 256;
 constexpr uint32_t kReplaySmemRows = 2048;    // rows sorted in shared memory up to this size
 
-struct TraceMeta { uint32_t row_off, task_off, n_rows, n_tasks; };
+struct TraceMeta { uint32_t row_off, task_off, n_rows, n_tasks, n_std, pad; };   // n_std: standalone rows
 
 struct Spec { uint32_t trace, reserved; uint64_t load_num, load_den, slo_num, slo_den; };
 
@@ -111,6 +115,7 @@ struct RResult {
 struct ReplayArgs {
     const TraceMeta* traces;
     const int64_t* arrival; const uint32_t *len_in, *true_out, *group, *dist_row, *ovr, *task, *fair;
+    const uint32_t* order;      // per trace: its standalone rows by (arrival, row) (admission order)
     const int64_t *t_arr, *t_dl; const uint32_t* t_nst;
     const uint32_t* st_kind; const int64_t* st_exec; const uint32_t *st_pat, *st_cb, *st_ce;
     const Spec* specs;
@@ -139,12 +144,13 @@ struct RState {
     uint64_t *tle, *ttot;
     u128* gA; uint32_t* gAv; uint64_t* gB; uint32_t* gBv; unsigned long long* gpc; u128* gpf;  // global sort scratch
     uint32_t* batch; int64_t* ring;
+    uint32_t* live;             // the rows that can be pending: arrived / released, not Done or Dropped
 };
 
 __host__ __device__ inline uint64_t replay_state_bytes(uint32_t M, uint32_t MT, uint32_t max_batch) {
     const uint64_t m = M + 64, mt = MT + 1;
     uint64_t b = 0;
-    b += 8 * m + 4 * m * 7 + 8 * m;            // arr, gen..cost, img
+    b += 8 * m + 4 * m * 7 + 8 * m + 4 * m;    // arr, gen..cost, img, live
     b += 4 * mt * 6 + 8 * mt * 3 + 8 * mt + 16 * mt;   // task u32 x6, i64 x3, gdone, tle+ttot
     uint64_t p2 = 1;                            // bitonic sorts pad to a power of two
     while (p2 < m) p2 <<= 1;
@@ -159,7 +165,7 @@ __host__ __device__ inline uint64_t replay_core_bytes(uint32_t M, uint32_t MT, u
     const uint64_t m = M + 64, mt = MT + 1;
     auto r = [](uint64_t b) { return (b + 63) & ~63ull; };
     return r(8 * m) + 7 * r(4 * m) + r(8 * m) + 6 * r(4 * mt) + 6 * r(8 * mt) + r(4 * (uint64_t)(max_batch + 1)) +
-           r(8 * 1024);
+           r(8 * 1024) + r(4 * m);
 }
 __device__ inline RState carve_core(unsigned char* p, uint32_t M, uint32_t MT, uint32_t max_batch) {
     const uint64_t m = M + 64, mt = MT + 1;
@@ -174,6 +180,7 @@ __device__ inline RState carve_core(unsigned char* p, uint32_t M, uint32_t MT, u
     s.timer = (int64_t*)take(8 * mt); s.ta = (int64_t*)take(8 * mt); s.tD = (int64_t*)take(8 * mt);
     s.gdone = (unsigned long long*)take(8 * mt); s.tle = (uint64_t*)take(8 * mt); s.ttot = (uint64_t*)take(8 * mt);
     s.batch = (uint32_t*)take(4 * (uint64_t)(max_batch + 1)); s.ring = (int64_t*)take(8 * 1024);
+    s.live = (uint32_t*)take(4 * m);
     return s;
 }
 
@@ -194,6 +201,7 @@ __device__ inline RState carve_state(unsigned char* p, uint32_t M, uint32_t MT, 
     s.gA = (u128*)take(16 * p2); s.gAv = (uint32_t*)take(4 * p2); s.gB = (uint64_t*)take(8 * p2);
     s.gBv = (uint32_t*)take(4 * p2); s.gpc = (unsigned long long*)take(8 * (m + 1)); s.gpf = (u128*)take(16 * (m + 1));
     s.batch = (uint32_t*)take(4 * (uint64_t)(max_batch + 1)); s.ring = (int64_t*)take(8 * 1024);
+    s.live = (uint32_t*)take(4 * m);
     return s;
 }
 
@@ -209,7 +217,8 @@ __host__ __device__ inline uint32_t replay_groups_bytes(uint32_t n_groups) {
     return (uint32_t)(((sizeof(Group) + sizeof(GroupFast)) * n_groups + 63) & ~63ull);
 }
 
-__global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
+template <uint32_t NT>
+__global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     Group* sg = reinterpret_cast<Group*>(smem);                                   // the SLO groups
     GroupFast* sgf = reinterpret_cast<GroupFast*>(smem + sizeof(Group) * A.n_groups);   // their scoring form
@@ -228,6 +237,7 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
     __shared__ uint32_t s_reqg, s_done, s_drop, s_tdone, s_tdrop, s_err, s_npend, s_cnt;
     __shared__ int64_t s_now, s_maxctx, s_nxt;
     __shared__ uint32_t s_steps, s_ring_n, s_ring_pos;
+    __shared__ uint32_t s_nlive, s_aptr;          // live rows; next standalone row to admit (arrival order)
     __shared__ int64_t s_ring_sum;
     __shared__ uint32_t s_bstar, s_ncd, s_nsel, s_tot;
     __shared__ double s_bp, s_thr;
@@ -252,7 +262,8 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
     for (uint32_t rep = blockIdx.x; rep < A.n_replays; rep += gridDim.x) {
         const Spec sp = A.specs[rep];
         const TraceMeta tm = A.traces[sp.trace];
-        const uint32_t n = tm.n_rows, nt = tm.n_tasks;
+        const uint32_t n = tm.n_rows, nt = tm.n_tasks, n_std = tm.n_std;
+        const uint32_t* order = A.order + tm.row_off;
         const int64_t* tr_arr = A.arrival + tm.row_off;
         const uint32_t* L_in = A.len_in + tm.row_off;
         const uint32_t* L_out = A.true_out + tm.row_off;
@@ -284,6 +295,7 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
         if (threadIdx.x == 0) {
             s_good = 0; s_tok = 0; s_reqg = 0; s_done = 0; s_drop = 0; s_tdone = 0; s_tdrop = 0; s_err = 0;
             s_now = 0; s_steps = 0; s_ring_n = 0; s_ring_pos = 0; s_ring_sum = 0; s_stop = false;
+            s_nlive = 0; s_aptr = 0;
             s_tguess = kNone;                              // no speculative threshold before the first step
             s_npre = 0; s_stall = 0;
             s_arm = 0; s_gstart = 0; s_window = 0;
@@ -345,7 +357,10 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                     const uint32_t b = st_cb[k], e = st_ce[k];
                     if (b >= e || e > n) { atomicOr(&s_err, 1u); break; }
                     S.cb[t] = b; S.ce[t] = e; S.left[t] = e - b;
-                    for (uint32_t r = b; r < e; ++r) { S.arr[r] = at; S.meta[r] = m_with_state(S.meta[r], kQueued); }
+                    const uint32_t lp = atomicAdd(&s_nlive, e - b);        // the stage's calls become live
+                    for (uint32_t r = b; r < e; ++r) {
+                        S.arr[r] = at; S.meta[r] = m_with_state(S.meta[r], kQueued); S.live[lp + r - b] = r;
+                    }
                     uint64_t le = 0;
                     for (uint32_t u = 0; u <= s; ++u) le += (uint64_t)st_pat[t * kMaxStages + u] * 1000000ull;
                     S.tle[t] = le;
@@ -355,10 +370,48 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
             __syncthreads();
             if (s_steps >= A.n_steps || s_err) break;
             const int64_t v = s_ring_n ? s_ring_sum / (int64_t)s_ring_n : A.v0;
+            // ---- the live rows: drop the finished ones (stable compaction), admit the standalone
+            // arrivals up to now (rows in arrival order: the admitted ones are a prefix).  Every
+            // per-row pass below runs over the live rows only -- rows not yet arrived and rows that
+            // are Done or Dropped can never be pending, and no pass writes them.
+            {
+                const uint32_t nl = s_nlive;
+                uint32_t carry = 0;
+                for (uint32_t base = 0; base < nl; base += blockDim.x) {
+                    const uint32_t i = base + threadIdx.x;
+                    uint32_t r = 0, keep = 0;
+                    if (i < nl) {
+                        r = S.live[i];
+                        const uint32_t st = m_state(S.meta[r]);
+                        keep = st != kDone && st != kDropped;
+                    }
+                    uint64_t tot;
+                    const uint32_t pos = (uint32_t)block_exclusive_scan_u64(keep, s_scan, &tot);
+                    if (keep) S.live[carry + pos] = r;
+                    carry += (uint32_t)tot;
+                    __syncthreads();
+                }
+                uint32_t ap = s_aptr;
+                while (true) {
+                    const uint32_t i = ap + threadIdx.x;
+                    uint32_t r = 0;
+                    bool adm = false;
+                    if (i < n_std) { r = order[i]; adm = S.arr[r] <= now; }
+                    const uint32_t k = (uint32_t)__syncthreads_count(adm);
+                    if (adm) S.live[carry + threadIdx.x] = r;
+                    carry += k; ap += k;
+                    if (k < blockDim.x) break;
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) { s_nlive = carry; s_aptr = ap; }
+                __syncthreads();
+            }
+            const uint32_t nl = s_nlive;
 
             // ---- (a1)-(a6) scoring of every row; steps_waited+1 for pending rows
             uint32_t my_pend = 0, my_drop = 0, my_err = 0;
-            for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
+            for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x) {
+                const uint32_t r = S.live[i];
                 const uint32_t meta = S.meta[r];
                 if (m_flags(meta) & kCompound) continue;
                 RowRes o;
@@ -438,7 +491,8 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
             // compound rows outside a released stage are never pending (after the task pass: it
             // may have dropped a task's calls just now, A40)
             __syncthreads();
-            for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
+            for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x) {
+                const uint32_t r = S.live[i];
                 const uint32_t meta = S.meta[r];
                 if ((m_flags(meta) & kCompound) && (S.arr[r] > now || m_state(meta) > kPreempted)) { S.img[r] = kNone; S.cost[r] = 0; }
             }
@@ -454,11 +508,8 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                 // idle: jump to the next arrival / stage start; stop when drained
                 if (threadIdx.x == 0) s_nxt = INT64_MAX;
                 __syncthreads();
-                int64_t my = INT64_MAX;
-                for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
-                    const uint32_t meta = S.meta[r];
-                    if (!(m_flags(meta) & kCompound) && m_state(meta) == kQueued && S.arr[r] > now && S.arr[r] < my) my = S.arr[r];
-                }
+                // the next standalone arrival is the first row not admitted yet (arrival order)
+                int64_t my = (threadIdx.x == 0 && s_aptr < n_std) ? S.arr[order[s_aptr]] : INT64_MAX;
                 for (uint32_t t = threadIdx.x; t < nt; t += blockDim.x)
                     if (!S.tdone[t] && S.timer[t] != INT64_MAX && S.timer[t] > now && S.timer[t] < my) my = S.timer[t];
                 atomicMin((unsigned long long*)&s_nxt, (unsigned long long)my);
@@ -478,17 +529,22 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                 const uint64_t t = attempt == 0 ? s_tguess : 0ull;
                 {
                     uint32_t cntl = 0;
-                    for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) cntl += S.img[r] != kNone && S.img[r] >= t;
+                    for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x) {
+                        const uint32_t r = S.live[i];
+                        cntl += S.img[r] != kNone && S.img[r] >= t;
+                    }
                     uint64_t tot;
                     uint32_t pos = (uint32_t)block_exclusive_scan_u64(cntl, s_scan, &tot);
                     const uint32_t m = (uint32_t)tot;
-                    if (attempt == 0 && (m == 0 || m > kReplayThreads)) {     // not worth it / too big: full sort
+                    if (attempt == 0 && (m == 0 || m > 512u)) {     // not worth it / too big: full sort
                         if (threadIdx.x == 0) s_m = 0;
                         __syncthreads();
                         continue;
                     }
-                    for (uint32_t r = threadIdx.x; r < n; r += blockDim.x)
+                    for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x) {
+                        const uint32_t r = S.live[i];
                         if (S.img[r] != kNone && S.img[r] >= t) { bA[pos] = make_ck(S.img[r], r); bAv[pos] = r; ++pos; }
+                    }
                     uint32_t m2 = 1;
                     while (m2 < m) m2 <<= 1;
                     for (uint32_t i = m + threadIdx.x; i < m2; i += blockDim.x) { bA[i] = ~(u128)0; bAv[i] = 0; }
@@ -627,14 +683,16 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                 for (uint32_t k = threadIdx.x; k < nsel; k += blockDim.x) S.late[selv[k]] |= 2u;
                 __syncthreads();
                 uint32_t cnt = 0;
-                for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
+                for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x) {
+                    const uint32_t r = S.live[i];
                     const bool run = S.img[r] != kNone && m_state(S.meta[r]) == kRunning;
                     cnt += run || ((S.late[r] & 2u) && !run);
                 }
                 uint64_t tot;
                 uint32_t pos = (uint32_t)block_exclusive_scan_u64(cnt, s_scan, &tot);
                 const uint32_t ng = (uint32_t)tot;
-                for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
+                for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x) {
+                    const uint32_t r = S.live[i];
                     const bool run = S.img[r] != kNone && m_state(S.meta[r]) == kRunning;
                     if (run || (S.late[r] & 2u)) {
                         bA[pos] = ((u128)(run ? 0u : 1u) << 96) | make_ck(S.img[r], r);
@@ -683,7 +741,8 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                 // the batch in window order; evicted rows become Preempted (their KV is swapped out)
                 uint32_t cf = 0, myev = 0, mytok = 0;
                 unsigned long long mystall = 0;
-                for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
+                for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x) {
+                    const uint32_t r = S.live[i];
                     const uint32_t lt = S.late[r];
                     cf += (lt >> 2) & 1u;
                     if (lt & 4u) mytok += S.cost[r];
@@ -695,7 +754,8 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                 }
                 pos = (uint32_t)block_exclusive_scan_u64(cf, s_scan, &tot);
                 const uint32_t nf = (uint32_t)tot;
-                for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
+                for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x) {
+                    const uint32_t r = S.live[i];
                     if (S.late[r] & 4u) {
                         const uint64_t len = c.len_key ? (uint64_t)L_in[r] + S.gen[r] : (uint64_t)L_in[r];
                         bB[pos] = (len << 32) | r; bBv[pos] = r; ++pos;
@@ -710,7 +770,7 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
                 if (lane == 0) { atomicAdd(&s_npre, myev); atomicAdd(&s_stall, mystall); }
                 __syncthreads();
                 block_sort<uint64_t>(bB, bBv, f2);
-                for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) S.late[r] &= 1u;   // marks off
+                for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x) S.late[S.live[i]] &= 1u;   // marks off
                 if (threadIdx.x == 0) { s_nsel = nf; s_tot = 0; }
                 __syncthreads();
                 if (lane == 0) atomicAdd(&s_tot, mytok);
@@ -737,8 +797,10 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs A) {
             for (uint32_t k = threadIdx.x; k < nsel; k += blockDim.x) S.img[S.batch[k]] = kNone;
             __syncthreads();
             // steps_waited + 1 (saturating) for every pending request left out (A12)
-            for (uint32_t r = threadIdx.x; r < n; r += blockDim.x)
+            for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x) {
+                const uint32_t r = S.live[i];
                 if (S.img[r] != kNone && (S.aux[r] >> 16) < 0xFFFFu) S.aux[r] += 1u << 16;
+            }
             // ---- (a10) iteration latency and time advance
             // + the KV swap stall of the requests the gate evicted (NEXT-1, A46)
             const int64_t stall = c.preempt ? (int64_t)s_stall : 0;

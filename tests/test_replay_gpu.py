@@ -79,6 +79,26 @@ def test_c5_sampled_replays_full_logs():
     s.close()
 
 
+def test_c5_sweep_path_sampled():
+    """More replays than two per SM take the sweep configuration (256-thread CTAs, several per SM,
+    state in global slices): a sample of them, full logs, against the oracle."""
+    traces = [W.trace_mixed(k) for k in range(3)]
+    d = traces[0]
+    sweep = W.c5_sweep()
+    n_rep = 640
+    specs = [dict(sweep[(i * 4096) // n_rep], trace=i % 3) for i in range(n_rep)]
+    rc0 = dict(d["rcfg"], n_steps=1024)
+    s = _sched(d)
+    res, log = s.replay([t["trace"] for t in traces], specs, rc0, log_steps=1024)
+    for j in (0, 1, 97, 331, 500, n_rep - 1):
+        sp = specs[j]
+        rc = dict(rc0, **{k: sp[k] for k in ("load_num", "load_den", "slo_num", "slo_den")})
+        t = traces[sp["trace"]]
+        ref = oracle.replay(t["cfg"], t["groups"], t["table"], t["trace"], rc, log=True)
+        _cmp(res[j], log[j], ref, f"C5 sweep replay {j}")
+    s.close()
+
+
 def test_c2_10k_until_drained():
     """BASELINE config C2: 10K chat + deadline mix, 8 SLO groups, tau 8192 -- one serial replay."""
     d = W.trace_c2()

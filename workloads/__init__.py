@@ -691,8 +691,8 @@ def replica_pools(d: dict, M: int, K: int, seed: int = 7):
     ns = int(p["n_single"])
     keys = ("id", "arrival_ns", "input_len", "generated", "prefilled", "meta", "aux", "task", "override_R")
     pick = np.zeros((ns, M), bool)
-    for i in range(ns):
-        pick[i, rng.permutation(M)[:K]] = True
+    choice = np.argsort(rng.random((ns, M)), axis=1)[:, :K]     # K of M without replacement per row
+    np.put_along_axis(pick, choice, True, axis=1)
     pools = []
     for m in range(M):
         sel = np.nonzero(pick[:, m])[0]
