@@ -217,8 +217,19 @@ __host__ __device__ inline uint32_t replay_groups_bytes(uint32_t n_groups) {
     return (uint32_t)(((sizeof(Group) + sizeof(GroupFast)) * n_groups + 63) & ~63ull);
 }
 
+// diagnostics (-DJIT_REPLAY_STAMPS): %globaltimer per step phase of replay 0, printed at its end
+#ifdef JIT_REPLAY_STAMPS
+#define RSTAMP(i) do { if (threadIdx.x == 0 && rep == 0) { unsigned long long t_; \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); if ((i) > 0) s_ph[(i)] += t_ - s_ph_last; s_ph_last = t_; } } while (0)
+#else
+#define RSTAMP(i) do {} while (0)
+#endif
 template <uint32_t NT>
 __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
+#ifdef JIT_REPLAY_STAMPS
+    __shared__ unsigned long long s_ph[16], s_ph_last;
+    if (threadIdx.x < 16) s_ph[threadIdx.x] = 0;
+#endif
     extern __shared__ __align__(16) unsigned char smem[];
     Group* sg = reinterpret_cast<Group*>(smem);                                   // the SLO groups
     GroupFast* sgf = reinterpret_cast<GroupFast*>(smem + sizeof(Group) * A.n_groups);   // their scoring form
@@ -276,11 +287,6 @@ __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
         const uint32_t* st_pat = A.st_pat + (uint64_t)tm.task_off * kMaxStages;
         const uint32_t* st_cb = A.st_cb + (uint64_t)tm.task_off * kMaxStages;
         const uint32_t* st_ce = A.st_ce + (uint64_t)tm.task_off * kMaxStages;
-        const bool in_smem = n <= kReplaySmemRows;
-        u128* bA = in_smem ? sA : S.gA;
-        uint32_t* bAv = in_smem ? sAv : S.gAv;
-        uint64_t* bB = in_smem ? sB : S.gB;
-        uint32_t* bBv = in_smem ? sBv : S.gBv;
 
         // ---- setup: SLO-scaled groups, initial row and task state
         for (uint32_t g = threadIdx.x; g < A.n_groups; g += blockDim.x) {
@@ -333,6 +339,7 @@ __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
 
         while (!s_err) {
             const int64_t now = s_now;
+            RSTAMP(0);
             // ---- stage starts whose time has come (task arrival or the end of the previous stage)
             for (uint32_t t = threadIdx.x; t < nt; t += blockDim.x) {
                 const uint32_t Sn = A.t_nst[tm.task_off + t];
@@ -368,6 +375,7 @@ __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
                 }
             }
             __syncthreads();
+            RSTAMP(1);
             if (s_steps >= A.n_steps || s_err) break;
             const int64_t v = s_ring_n ? s_ring_sum / (int64_t)s_ring_n : A.v0;
             // ---- the live rows: drop the finished ones (stable compaction), admit the standalone
@@ -405,8 +413,16 @@ __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
                 __syncthreads();
                 if (threadIdx.x == 0) { s_nlive = carry; s_aptr = ap; }
                 __syncthreads();
+                RSTAMP(2);
             }
             const uint32_t nl = s_nlive;
+            // every sort / prefix array of the step holds at most the live rows: shared memory when
+            // they fit (whatever the trace length), else this CTA's global scratch
+            const bool in_smem = nl <= kReplaySmemRows;
+            u128* bA = in_smem ? sA : S.gA;
+            uint32_t* bAv = in_smem ? sAv : S.gAv;
+            uint64_t* bB = in_smem ? sB : S.gB;
+            uint32_t* bBv = in_smem ? sBv : S.gBv;
 
             // ---- (a1)-(a6) scoring of every row; steps_waited+1 for pending rows
             uint32_t my_pend = 0, my_drop = 0, my_err = 0;
@@ -502,6 +518,7 @@ __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
             __syncthreads();
             if (lane == 0) { atomicAdd(&s_npend, my_pend); atomicAdd(&s_drop, my_drop); if (my_err) atomicOr(&s_err, 1u); }
             __syncthreads();
+            RSTAMP(3);
             if (s_err) break;
             const uint32_t np = s_npend;
             if (np == 0) {
@@ -574,6 +591,9 @@ __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
                     // speculative attempt: exact iff the walk stopped inside S (or S = all pending)
                     // and Cd = {key >= thr} lies in S
                     s_spec_ok = attempt == 1 || m == np || (fits < m && s_thr_img >= t);
+#ifdef JIT_REPLAY_STAMPS
+                    if (rep == 0) { s_ph[10] += attempt; s_ph[11] += np; s_ph[12] += m; s_ph[13] += (attempt == 0 && s_m == 0); }
+#endif
                 }
                 __syncthreads();
                 if (s_spec_ok) break;
@@ -588,6 +608,7 @@ __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
                                S.pre[r], S.gen[r], L_in[r]);
             }
             __syncthreads();
+            RSTAMP(4);
 #endif
             if (threadIdx.x == 0) s_tguess = (uint64_t)__double_as_longlong(__dmul_rn(s_thr, 0.85));
             const uint32_t np_sorted = s_m;   // rows in the sorted prefix array bA (Cd is a prefix of it)
@@ -634,6 +655,7 @@ __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
                 }
                 if (threadIdx.x == 0) { pc[ncd] = carry_c; pf[ncd] = carry_f; }
                 __syncthreads();
+                RSTAMP(5);
             }
             {
                 u128 best = 0; uint32_t bi = 0xFFFFFFFFu, bj = 0;
@@ -655,6 +677,7 @@ __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
                 }
                 if (lane == 0) { s_best[wid] = best; s_bi[wid] = bi; s_bj[wid] = bj; }
                 __syncthreads();
+                RSTAMP(6);
                 if (wid == 0) {
                     const uint32_t nw = blockDim.x >> 5;
                     best = lane < nw ? s_best[lane] : (u128)0; bi = lane < nw ? s_bi[lane] : 0xFFFFFFFFu; bj = lane < nw ? s_bj[lane] : 0;
@@ -671,6 +694,7 @@ __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
                     }
                 }
                 __syncthreads();
+                RSTAMP(7);
             }
             uint32_t nsel = s_nsel;
             const uint32_t* selv = bBv + s_bi[0];          // the batch rows: GMAX's window ...
@@ -796,6 +820,7 @@ __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
             atomicMax((unsigned long long*)&s_maxctx, (unsigned long long)myctx);
             for (uint32_t k = threadIdx.x; k < nsel; k += blockDim.x) S.img[S.batch[k]] = kNone;
             __syncthreads();
+            RSTAMP(8);
             // steps_waited + 1 (saturating) for every pending request left out (A12)
             for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x) {
                 const uint32_t r = S.live[i];
@@ -860,6 +885,7 @@ __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
                 }
             }
             __syncthreads();
+            RSTAMP(9);
             // NEXT-2 online p (A48): at the end of a window its token goodput scores its arm; the
             // next arm: an untried one in grid order, else explore (prob eps) or the best mean
             if (A.p_adapt && threadIdx.x == 0 && s_steps % (A.window_frames * c.frame) == 0) {
@@ -890,6 +916,13 @@ __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
             R.request_goodput = s_reqg; R.n_done = s_done; R.n_dropped = s_drop; R.steps = s_steps;
             R.n_tasks_done = s_tdone; R.n_tasks_dropped = s_tdrop; R.error = s_err; R.n_preempted = n_preempted_total;
             A.out[rep] = R;
+#ifdef JIT_REPLAY_STAMPS
+            if (rep == 0) {
+                printf("replay 0: %u steps, ns/step:", s_steps);
+                for (int i = 1; i < 14; ++i) printf(" p%d=%llu", i, s_ph[i] / (s_steps ? s_steps : 1));
+                printf("\n");
+            }
+#endif
         }
         __syncthreads();
     }
