@@ -484,7 +484,7 @@ def next_lines(args, dev, stream, Scheduler):
     traces = [W.trace_mixed(k) for k in range(3)]
     d = traces[0]
     sweep = W.c5_sweep()
-    specs = [dict(sweep[i], trace=i % 3) for i in range(0, 4096, 16)]        # 256 sweep points
+    specs = [dict(sweep[i], trace=i % 3) for i in range(0, 4096, 8)]         # 512 sweep points
     variants = {"plain": (d["cfg"], d["rcfg"]),
                 "gate": (dict(d["cfg"], preempt=1), d["rcfg"]),
                 "online_p": (d["cfg"], dict(d["rcfg"], p_adapt=1, eps_num=1, eps_den=10, window_frames=4, seed=1))}
@@ -504,11 +504,11 @@ def next_lines(args, dev, stream, Scheduler):
         t0 = time.perf_counter()
         same, osteps = True, 0
         for j in range(4):
-            sp = specs[j * 64]
+            sp = specs[j * 128]
             rcj = dict(rc, **{k: sp[k] for k in ("load_num", "load_den", "slo_num", "slo_den")})
             t = traces[sp["trace"]]
             ref = oracle.replay(cfg, t["groups"], t["table"], t["trace"], rcj)
-            same &= all(int(res[j * 64][k]) == int(ref[k]) for k in ("token_goodput", "steps", "sim_end_ns"))
+            same &= all(int(res[j * 128][k]) == int(ref[k]) for k in ("token_goodput", "steps", "sim_end_ns"))
             osteps += ref["steps"]
         tc = time.perf_counter() - t0
         out[f"replay_{name}"] = {
@@ -517,7 +517,7 @@ def next_lines(args, dev, stream, Scheduler):
             "n_preempted_sum": int(sum(int(r["n_preempted"]) for r in res)), "equal_to_oracle_sample": bool(same),
             "cpu_baseline": {"value": osteps / tc, "unit": "steps/s", "cores": 1, "kind": "oracle",
                              "sample": "4 of the replays on 1 core"},
-            "workload": "C5(i) slice: 256 (load, SLO-scale) points x 4096 steps of 2048-row mixed traces"}
+            "workload": "C5(i) slice: 512 (load, SLO-scale) points x 4096 steps of 2048-row mixed traces"}
     # ---- NEXT-2 blend in the pool step: k_score over C3 with f = 1/10 (every pending row keyed exactly)
     dd = W.pool_snapshot(3, 1 << 20)
     rng = np.random.default_rng(3)

@@ -13,3 +13,6 @@ ncu --set full --warp-sampling-interval 0 --clock-control none --import-source o
 ncu --set full --warp-sampling-interval 0 --clock-control none --import-source on -k regex:"^k_spec" -s 12 -c 1 \
     -o gpurun_out/prof_spec -f $P >> gpurun_out/ncu_full.log 2>&1
 ls -la gpurun_out | tail -5
+# the replay kernel: one capture of the C5 sweep configuration (256-thread CTAs)
+ncu --set full --warp-sampling-interval 0 --clock-control none --import-source on -k regex:k_replay -c 1 \
+    -o gpurun_out/prof_replay -f python profiles/prof_replay.py 640 512 >> gpurun_out/ncu_full.log 2>&1
