@@ -729,10 +729,20 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
         for (uint32_t s = 0; s < kStagesW; ++s) mbar_init(&ws->bar[s], 1);
         mbar_init_fence();
     }
-    for (uint32_t s = 0; s < kStagesW && s < n_mine; ++s) {   // fill the ring
-        const Item it = item_j(s);
-        if (lane == 0) issue_item(P, it, &ws->slot[s], &ws->bar[s], pol);
-    }
+    // fill the ring: the ring items' bytes stream in while the warp scores its standalone slabs.
+    // Issued after the first standalone chunk (JIT_RING_EARLY: here), so that the prologue does not
+    // wait for the item descriptors
+    bool ring_filled = false;
+    auto fill_ring = [&]() {
+        for (uint32_t s = 0; s < kStagesW && s < n_mine; ++s) {
+            const Item it = item_j(s);
+            if (lane == 0) issue_item(P, it, &ws->slot[s], &ws->bar[s], pol);
+        }
+        ring_filled = true;
+    };
+#ifdef JIT_RING_EARLY
+    fill_ring();
+#endif
 #ifdef JIT_TIMELINE
     const unsigned long long tpb = gt();
 #endif
@@ -780,8 +790,10 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
 #endif
 #pragma unroll
         for (uint32_t k = 0; k < kRs; ++k) cur[k] = nxt[k];
+        if (!ring_filled) fill_ring();
     }
 #endif
+    if (!ring_filled) fill_ring();
 #ifdef JIT_TIMELINE
     tls = gt() - tl1; nls = (s1 - s0 + kRs - 1) / kRs;     // the standalone phase and its chunks
 #endif
