@@ -470,6 +470,35 @@ def config_lines(args, dev, stream, Scheduler):
                              "50% in a 1-call stage), tau 8192, B_max 8192; 3 rotated copies"}
     for h in hs:
         h.close()
+    # ---- C3 token-budget sweep (tau 2,048 to 65,536, B_max = tau): synchronous steps
+    d3 = W.pool_snapshot(3, 1 << 20)
+    n3, nt3 = len(d3["pool"]["input_len"]), len(d3["tasks"]["arrival_ns"])
+    sweep = {}
+    for tau in (2048, 8192, 65536):
+        cfg = dict(d3["cfg"], token_budget=tau, max_batch=tau)
+        hs = []
+        for _ in range(4):                               # 4 x 36 MB > L2
+            s = Scheduler(cfg, d3["groups"], d3["table"], capacity=n3, task_capacity=nt3, device=dev, stream=stream)
+            s.load(d3["pool"], d3["tasks"])
+            for _ in range(3):
+                s.step(d3["now_ns"], d3["v_token_ns"])
+            hs.append(s)
+        torch.cuda.synchronize()
+        K = 24
+        t0 = time.perf_counter()
+        for k in range(K):
+            last = hs[k % 4].step(d3["now_ns"], d3["v_token_ns"])
+        torch.cuda.synchronize()
+        ms = (time.perf_counter() - t0) / K * 1e3
+        sweep[str(tau)] = {"ms_per_step_wall": ms, "requests_per_s": n3 / (ms / 1e3), "b_star": int(last["b_star"]),
+                           "n_candidates": int(last["n_candidates"]), "n_selected": int(last["n_selected"]),
+                           "n_spec": int(last["n_spec"]), "fallback": int(last["fallback"])}
+        for h in hs:
+            h.close()
+    out["C3_tau_sweep"] = {"metric": "pending requests scheduled/sec (1M pool) vs token budget", "unit": "requests/s",
+                           "points": sweep,
+                           "how": "synchronous jit_sched_step (host round trip included), wall clock, 4 rotated copies",
+                           "workload": "C3 pool (2^20 rows) with tau = B_max in {2048, 8192, 65536}"}
     return out
 
 
@@ -695,6 +724,7 @@ def run_single(args, dev, stream):
     n_b2b = max(60, K)
     k_b2b = Scheduler.time_scoring(hs, now, v, n_b2b)      # (3) k_score back to back
     k_refresh = Scheduler.time_scoring(hs, now, v, 12, force_refresh=True)   # (4) every bound stale
+    k_refresh2 = Scheduler.time_scoring(hs, now, v, 30, refresh_2pct=True)  # (5) every 50th bound stale
     for _ in range(3):
         for k in range(20):
             hs[k % rot].step_async(now, v)
@@ -724,6 +754,9 @@ def run_single(args, dev, stream):
                 "forced_refresh": {"k_score_ms": k_refresh, "frac": hot / (k_refresh / 1e3) / 1e9 / hbm,
                                    "how": "every cached length bound invalidated before each launch (untimed); each "
                                           "launch timed alone, so it also carries its launch latency"},
+                "refresh_2pct": {"k_score_ms": k_refresh2, "frac": hot / (k_refresh2 / 1e3) / 1e9 / hbm,
+                                 "how": "every 50th row's cached bound invalidated before each launch (SURVEY 8(d)'s "
+                                        "steady state of about 2% refresh); each launch timed alone"},
                 "kernel_ms_event_nodes": {"k_score": kt[0], "k_spec": kt[2], "step_graph": kt[4]},
                 "first_step_after_load_ms": float(np.median(first_ms)), "ms_per_step_with_event_nodes": ms_events}
     for s in hs:
@@ -820,6 +853,36 @@ def run_sharded(args, ws, rank, dev, stream, barrier, allmax, allsum):
                     "how": f"per rank: 30 back-to-back k_score launches over {rot} copies of its shard, max over ranks"}
     except Exception as ex:  # pragma: no cover
         roofline = {"error": str(ex)[:200]}
+    # C5(ii)'s local / collective / merge breakdown: CUDA events on the stream around the export
+    # (k_score + the speculative set), the allgather and the union resolve; speculative steps only
+    breakdown = None
+    try:
+        parts = []
+        for k in range(2 * rot):
+            st = sts[k % rot]
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            barrier()
+            ev[0].record(stream)
+            st.s.shard_spec_export(now, v, st.spec, st.rank)
+            ev[1].record(stream)
+            allb = st.allgather(st.spec)
+            ev[2].record(stream)
+            r = st.s.shard_spec_resolve(allb, st.world, st.rank)
+            ev[3].record(stream)
+            if r is None:                                # exact protocol this step: not part of the breakdown
+                st._exact(now, v)
+                continue
+            torch.cuda.synchronize()
+            parts.append([ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])])
+        if parts:
+            med = np.median(np.array(parts), axis=0)
+            breakdown = {"local_ms": allmax(float(med[0])), "collective_ms": allmax(float(med[1])),
+                         "merge_ms": allmax(float(med[2])), "steps": len(parts),
+                         "how": "median over speculative steps of CUDA-event intervals on the library stream around "
+                                "jit_shard_spec_export (k_score + set export), the allgather, jit_shard_spec_resolve "
+                                "(union resolve + batch readback); max over ranks"}
+    except Exception as ex:  # pragma: no cover
+        breakdown = {"error": str(ex)[:200]}
     for s in hs[1:]:
         s.close()
     # e2e: the sharded step with each step's deltas... the exchange is the step; wall clock, max over ranks
@@ -852,7 +915,7 @@ def run_sharded(args, ws, rank, dev, stream, barrier, allmax, allsum):
                            "l2": f"{rot} rotated shard copies per rank (>= 4x the L2 of hot state)",
                            "parallelism": f"sharded pool over {ws} ranks: speculative sets allgathered over NCCL and "
                                           "resolved identically on every rank (exact 2-round protocol as fallback)",
-                           "steps_speculative": n_fast, "steps_exact_protocol": n_exact,
+                           "steps_speculative": n_fast, "steps_exact_protocol": n_exact, "breakdown": breakdown,
                            "last_batch": {"n_selected": out["n_selected"], "b_star": out["b_star"],
                                           "n_candidates": out["n_candidates"]}},
                 "roofline": roofline, "cpu_baseline": None, "e2e": e2e,

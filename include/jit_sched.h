@@ -234,8 +234,10 @@ int jit_sched_kernel_times(jit_sched* h, int enable, float* ms_out, uint32_t n_o
  * step counter moves only with a resolved step, so the pools are left as they were (the per-step
  * accumulators and speculative sets are reset afterwards).  flags & JIT_TIME_FORCE_REFRESH: every
  * cached length bound is invalidated before each launch (untimed; each launch timed alone), i.e.
- * the pass with a stale bound on every row (SURVEY 8(d) "forced refresh"). */
+ * the pass with a stale bound on every row (SURVEY 8(d) "forced refresh"); flags & JIT_TIME_REFRESH_2PCT: the
+ * same with every 50th row stale (the steady state's ~2% refresh). */
 #define JIT_TIME_FORCE_REFRESH 1u
+#define JIT_TIME_REFRESH_2PCT 2u   /* every 50th row's bound invalidated before each launch (SURVEY 8(d) "about 2%") */
 int jit_sched_time_scoring(jit_sched** hs, uint32_t n_handles, int64_t now_ns, int64_t v_token_ns, uint32_t launches,
                            uint32_t flags, float* ms_per_launch);
 

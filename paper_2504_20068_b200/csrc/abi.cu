@@ -902,10 +902,11 @@ extern "C" int jit_sched_time_scoring(jit_sched** hs, uint32_t n_handles, int64_
     cudaEvent_t e0 = h->ev[0], e1 = h->ev[1];
     CK(cudaStreamSynchronize(s));
     float ms = 0.f;
-    if (flags & JIT_TIME_FORCE_REFRESH) {
+    if (flags & (JIT_TIME_FORCE_REFRESH | JIT_TIME_REFRESH_2PCT)) {
         for (uint32_t k = 0; k < launches; ++k) {
             jit_sched* hk = hs[k % n_handles];
-            k_invalidate_bounds<<<hk->grid_pass, 256, 0, s>>>(hk->P);
+            if (flags & JIT_TIME_FORCE_REFRESH) k_invalidate_bounds<<<hk->grid_pass, 256, 0, s>>>(hk->P);
+            else k_invalidate_bounds<<<hk->grid_pass, 256, 0, s>>>(hk->P, 50u, k % 50u);
             CK(cudaEventRecord(e0, s));
             enqueue_score(hk, s, now_ns, v_token_ns);
             CK(cudaEventRecord(e1, s));

@@ -762,9 +762,10 @@ __global__ void k_task_update(Pool P, const uint32_t* task, const uint32_t* stag
 }
 
 // measurement only (jit_sched_time_scoring, JIT_TIME_FORCE_REFRESH): every cached bound stale
-__global__ void k_invalidate_bounds(Pool P) {
+// every `stride`-th row from `phase` (stride 1: all) gets its cached length bound invalidated
+__global__ void k_invalidate_bounds(Pool P, uint32_t stride = 1, uint32_t phase = 0) {
     for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < P.n; r += gridDim.x * blockDim.x)
-        P.rows[r].meta &= 0xFFFFu;                          // epoch field 0: unset
+        if (stride == 1 || r % stride == phase) P.rows[r].meta &= 0xFFFFu;   // epoch field 0: unset
 }
 
 // load: every task's call rows from the CSR
