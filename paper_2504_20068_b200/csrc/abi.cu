@@ -159,6 +159,7 @@ static void carve(Carve& cv, const jit_config* cfg, const jit_len_table* tab, Po
     P.map_mask = (uint32_t)(mc - 1);
     T.edges = cv.take<uint32_t>(tab->n_bins);
     T.cum = cv.take<uint32_t>((uint64_t)tab->n_rows * tab->n_bins);
+    T.lhat0 = cv.take<uint32_t>(tab->n_rows);
     S.hcnt = cv.take<uint32_t>(4096); S.hcost = cv.take<unsigned long long>(4096);
     S.bucket_ck = cv.take<u128>(kBucketCap); S.bucket_cost = cv.take<uint32_t>(kBucketCap);
     uint64_t P2 = 1;                       // bitonic sorts pad |Cd| to a power of two
@@ -281,6 +282,9 @@ extern "C" int jit_sched_init(const jit_config* cfg, const jit_slo_group* groups
     CK(cudaMemcpyAsync((void*)h->T.edges, table->edges, 4ull * table->n_bins, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemcpyAsync((void*)h->T.cum, table->cum, 4ull * table->n_rows * table->n_bins, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemcpyAsync(h->d_groups, groups, sizeof(Group) * n_groups, cudaMemcpyHostToDevice, h->stream));
+    // every table row's bound at anchor 0 (the rows with g < R: seeded at load / arrival)
+    k_lhat0<<<(table->n_rows + 127) / 128, 128, 0, h->stream>>>(h->T, c.qn, c.qd);
+    CK(cudaGetLastError());
     CK(cudaMallocHost(&h->h_ctrl, sizeof(Ctrl)));
     CK(cudaMallocHost(&h->h_batch, 3ull * 4 * (cfg->max_batch + 1)));
     h->S.h_batch = h->h_batch;
@@ -381,7 +385,7 @@ extern "C" int jit_sched_load(jit_sched* h, const jit_pool* p) {
     const uint32_t vb = (uint32_t)std::min<uint64_t>((n + 255) / 256 + 1, (uint64_t)h->n_sm * 8);
     if (nt) k_crng_from_off<<<(uint32_t)std::min<uint64_t>((nt + 255) / 256, (uint64_t)h->n_sm * 8), 256, 0, h->stream>>>(P);
     k_validate<<<vb, 256, 0, h->stream>>>(P, h->d_groups, h->n_groups, h->T.n_rows, h->T.l_max, &h->d_ctrl->error, 0u,
-                                          P.n_single, 0u);
+                                          P.n_single, 0u, h->T.forest ? nullptr : h->T.lhat0, h->c.R);
     if (nt) k_task_prep<<<(uint32_t)std::min<uint64_t>((nt + 255) / 256, (uint64_t)h->n_sm * 8), 256, 0, h->stream>>>(P, 0u);
     // request id -> row map (the progress of a step is keyed by id)
     CK(cudaMemsetAsync(P.idmap, 0xFF, 8ull * (P.map_mask + 1ull), h->stream));
@@ -710,12 +714,29 @@ static int apply_deltas(jit_sched* h, const jit_step_in* in) {
         o_tu[0] = pk.put(in->tu_task, ntu); o_tu[1] = pk.put(in->tu_cur_stage, ntu); o_tu[2] = pk.put(in->tu_goodput_done, ntu);
         if (in->tu_stage_deadline_ns) o_tu[3] = pk.put(in->tu_stage_deadline_ns, ntu);
     }
+    // the arrivals' work items (standalone chunks, then the new tasks), staged with the deltas
+    const size_t i0 = h->h_items.size();
+    uint64_t o_items = 0;
+    if (na) {
+        const uint32_t n0 = P.n, t0 = P.n_tasks;
+        for (uint32_t r0 = n0; r0 < n0 + a->n_single; r0 += kItemRows)
+            h->h_items.push_back(Item{r0, std::min<uint32_t>(r0 + kItemRows, n0 + a->n_single), 0u, 0u});
+        if (nat) add_task_items(h->h_items, a->call_off, n0, t0, nat);
+        if (h->h_items.size() > h->item_cap) {
+            h->h_items.resize(i0);
+            return set_err(h, JIT_ECAPACITY, "too many work items (reload to compact)");
+        }
+        o_items = pk.put(h->h_items.data() + i0, h->h_items.size() - i0);
+    }
     if (m) {
         o_pg[0] = pk.put(in->prog_key, m); o_pg[1] = pk.put(in->prog_generated, m);
         o_pg[2] = pk.put(in->prog_prefilled, m); o_pg[3] = pk.put(in->prog_state, m);
     }
     const uint64_t bytes = (pk.off + 15) & ~15ull;
-    if (bytes > h->load_bytes) return set_err(h, JIT_ECAPACITY, "step deltas exceed the staging area");
+    if (bytes > h->load_bytes) {
+        h->h_items.resize(i0);
+        return set_err(h, JIT_ECAPACITY, "step deltas exceed the staging area");
+    }
     if (bytes > h->pin_cap) {                              // pinned mirror, grown on demand
         if (h->h_pin) cudaFreeHost(h->h_pin);
         h->h_pin = nullptr; h->pin_cap = 0;
@@ -740,26 +761,28 @@ static int apply_deltas(jit_sched* h, const jit_step_in* in) {
             A.pattern = reinterpret_cast<const uint32_t*>(d + o_t[5]); A.gdone = reinterpret_cast<const uint64_t*>(d + o_t[6]);
         }
         A.n = na; A.n_single = a->n_single; A.n_tasks = nat; A.n0 = P.n; A.t0 = P.n_tasks;
-        const uint32_t n0 = P.n, t0 = P.n_tasks;
-        const uint32_t g = (uint32_t)std::min<uint64_t>((std::max(na, nat) + 255) / 256 + 1, (uint64_t)h->n_sm * 8);
-        k_append<<<g, 256, 0, s>>>(P, A);
-        P.n = n0 + na; P.n_tasks = t0 + nat;
-        uint32_t* err = &h->S.gpart->err;
-        k_validate<<<g, 256, 0, s>>>(P, h->d_groups, h->n_groups, h->T.n_rows, h->T.l_max, err, n0, n0 + a->n_single, t0);
-        if (nat) k_task_prep<<<g, 256, 0, s>>>(P, t0);
-        k_map_insert<<<g, 256, 0, s>>>(P, n0, P.n, err);
-        CK(cudaGetLastError());
-        // their work items: standalone chunks, then the new tasks (table-driven descriptors)
-        const size_t i0 = h->h_items.size();
-        for (uint32_t r0 = n0; r0 < n0 + a->n_single; r0 += kItemRows)
-            h->h_items.push_back(Item{r0, std::min<uint32_t>(r0 + kItemRows, n0 + a->n_single), 0u, 0u});
-        if (nat) add_task_items(h->h_items, a->call_off, n0, t0, nat);
-        if (h->h_items.size() > h->item_cap) return set_err(h, JIT_ECAPACITY, "too many work items (reload to compact)");
         const uint32_t n_items = (uint32_t)h->h_items.size();
-        CK(cudaMemcpyAsync(h->d_items + i0, h->h_items.data() + i0, sizeof(Item) * (n_items - i0), cudaMemcpyHostToDevice, s));
+        A.items_src = reinterpret_cast<const Item*>(d + o_items); A.items_dst = h->d_items + i0;
+        A.n_items_dst = h->d_n_items; A.n_new_items = n_items - (uint32_t)i0; A.n_items = n_items;
+        const uint32_t n0 = P.n, t0 = P.n_tasks;
+        const uint32_t g = (uint32_t)std::min<uint64_t>((std::max(std::max(na, nat), A.n_new_items) + 255) / 256 + 1,
+                                                        (uint64_t)h->n_sm * 8);
+        uint32_t* err = &h->S.gpart->err;
+        const uint32_t* lh0 = h->T.forest ? nullptr : h->T.lhat0;
+        if (!nat) {                                       // standalone requests only: one launch
+            P.n = n0 + na;
+            k_arrive_std<<<g, 256, 0, s>>>(P, A, h->d_groups, h->n_groups, h->T.n_rows, h->T.l_max, err, lh0, h->c.R);
+        } else {
+            k_append<<<g, 256, 0, s>>>(P, A);
+            P.n = n0 + na; P.n_tasks = t0 + nat;
+            k_validate<<<g, 256, 0, s>>>(P, h->d_groups, h->n_groups, h->T.n_rows, h->T.l_max, err, n0, n0 + a->n_single,
+                                         t0, lh0, h->c.R);
+            k_task_prep<<<g, 256, 0, s>>>(P, t0);
+            k_map_insert<<<g, 256, 0, s>>>(P, n0, P.n, err);
+        }
+        CK(cudaGetLastError());
         h->n_items_host = n_items;
         h->S.n_ring_h = n_items - h->S.n_std_items;
-        CK(cudaMemcpyAsync(h->d_n_items, &h->n_items_host, 4, cudaMemcpyHostToDevice, s));
         h->grid_pass = std::max<uint32_t>(1, std::min<uint32_t>((P.n + kPassThreads - 1) / kPassThreads, (uint32_t)h->n_sm * 4));
     }
     if (ntu) {

@@ -650,6 +650,21 @@ __global__ void k_publish(const Ctrl* ctrl, Ctrl* host) { publish_ctrl(ctrl, hos
 
 // load: pack the caller's SoA pool into hot rows.  lrow = dist_row | L-hat unset; the count in
 // aux's high half becomes the frozen steps_waited (the first step stamps the pending rows).
+// A row with g < R has the anchor 0, so its cached bound is the table row's unconditioned
+// quantile Q_q(L | L > 0): set from the per-row table (lhat0, nullptr with a forest) when a row
+// enters the pool (k_validate after a load / an arrival), epoch field 1 -- the bound the pass's
+// refresh would compute, without a search on the step's path.
+__device__ __forceinline__ void seed_bound(HotRow& q, const uint32_t* lhat0, uint32_t n_rows, uint32_t R) {
+    const uint32_t drow = q.lrow & 0xFFFFu;
+    if (lhat0 && q.gen < R && drow < n_rows) {
+        q.lrow = drow | (__ldg(lhat0 + drow) << 16);
+        q.meta = (q.meta & 0xFFFFu) | (1u << 16);
+    }
+}
+__global__ void k_lhat0(Table T, uint32_t qn, uint32_t qd) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < T.n_rows; r += gridDim.x * blockDim.x)
+        T.lhat0[r] = cond_quantile(T, r, 0u, qn, qd);
+}
 __global__ void k_pack(HotRow* rows, uint32_t n, const int64_t* arr, const uint32_t* len_in, const uint32_t* gen,
                        const uint32_t* pre, const uint32_t* meta, const uint32_t* aux) {
     for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
@@ -690,16 +705,42 @@ __global__ void k_progress(Pool P, Scratch S, const uint32_t* key, const uint32_
 }
 
 // request id -> row map: insert rows [r0, r1) (a duplicate id fails the load / step)
-__global__ void k_map_insert(Pool P, uint32_t r0, uint32_t r1, uint32_t* err) {
-    for (uint32_t r = r0 + blockIdx.x * blockDim.x + threadIdx.x; r < r1; r += gridDim.x * blockDim.x) {
-        const uint32_t id = P.id[r];
-        const unsigned long long e = ((unsigned long long)id << 32) | r;
-        for (uint32_t h = map_hash(id, P.map_mask), k = 0; k <= P.map_mask; h = (h + 1) & P.map_mask, ++k) {
-            const unsigned long long old = atomicCAS(&P.idmap[h], kMapEmpty, e);
-            if (old == kMapEmpty) break;
-            if ((uint32_t)(old >> 32) == id) { atomicOr(err, 16u); break; }
-        }
+__device__ __forceinline__ void map_insert_row(const Pool& P, uint32_t id, uint32_t r, uint32_t* err) {
+    const unsigned long long e = ((unsigned long long)id << 32) | r;
+    for (uint32_t h = map_hash(id, P.map_mask), k = 0; k <= P.map_mask; h = (h + 1) & P.map_mask, ++k) {
+        const unsigned long long old = atomicCAS(&P.idmap[h], kMapEmpty, e);
+        if (old == kMapEmpty) break;
+        if ((uint32_t)(old >> 32) == id) { atomicOr(err, 16u); break; }
     }
+}
+__global__ void k_map_insert(Pool P, uint32_t r0, uint32_t r1, uint32_t* err) {
+    for (uint32_t r = r0 + blockIdx.x * blockDim.x + threadIdx.x; r < r1; r += gridDim.x * blockDim.x)
+        map_insert_row(P, P.id[r], r, err);
+}
+
+// the range / layout checks of one loaded or appended row (k_validate, k_arrive_std)
+__device__ __forceinline__ bool row_invalid(const Pool& P, const Group* groups, uint32_t n_groups, uint32_t n_rows_tab,
+                                            uint32_t l_max, uint32_t r, const HotRow& q, uint32_t std_end,
+                                            uint32_t t_begin) {
+    const uint32_t meta = q.meta;
+    const uint32_t gi = m_group(meta);
+    const bool comp = (m_flags(meta) & kCompound) != 0;
+    bool rb = false;
+    if (gi >= n_groups || l_row(q.lrow) >= n_rows_tab || q.len_in == 0 || q.len_in >= (1u << 24) ||
+        q.gen >= (1u << 24) || q.pre > q.len_in || (meta >> 16) != 0 || m_state(meta) > kMoved ||
+        q.since > 0xFFFFu || comp != (r >= std_end)) rb = true;
+    else if (!comp) {
+        if (P.task[r] != kNoTask || groups[gi].type == kCMP) rb = true;
+    } else {
+        const uint32_t t = P.task[r];
+        if (t >= P.n_tasks || t < t_begin || groups[gi].type != kCMP || (m_flags(meta) & kOverride)) rb = true;
+        else if (r < P.crng[t].x || r >= P.crng[t].y) rb = true;
+        // a call's goodput w_in L_i + w_out L-hat stays below 2^27 (the pass sums 32 calls in u32)
+        else if ((uint64_t)groups[gi].w_in * q.len_in + (uint64_t)groups[gi].w_out * (l_max + 1ull) >= (1ull << 27))
+            rb = true;
+    }
+    if (!rb && (m_flags(meta) & kOverride) && groups[gi].type == kCMP) rb = true;
+    return rb;
 }
 
 // arrivals: the new rows / tasks (staged SoA, arrival-local task indices and call offsets) appended
@@ -710,9 +751,15 @@ struct Arrivals {
     const uint32_t* call_off; const int64_t *t_arr, *t_dl; const uint32_t *cur_stage, *n_stages, *pattern;
     const uint64_t* gdone;
     uint32_t n, n_single, n_tasks, n0, t0, pad;
+    const Item* items_src;      // the arrivals' new work items (staged with the deltas) ...
+    Item* items_dst;            // ... copied to the item array here, with its new count
+    uint32_t* n_items_dst;
+    uint32_t n_new_items, n_items;
 };
 __global__ void k_append(Pool P, Arrivals A) {
     const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n_new_items; i += stride) A.items_dst[i] = A.items_src[i];
+    if (blockIdx.x == 0 && threadIdx.x == 0) *A.n_items_dst = A.n_items;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += stride) {
         const uint32_t r = A.n0 + i;
         HotRow q;
@@ -733,6 +780,35 @@ __global__ void k_append(Pool P, Arrivals A) {
         P.gdone[g] = A.gdone[t];
         P.crng[g] = make_uint2(A.n0 + A.call_off[t], A.n0 + A.call_off[t + 1]);
     }
+}
+
+// standalone-only arrivals in one launch: each new row appended, validated (row_invalid), its
+// bound seeded (seed_bound) and its id inserted in the map; the new work items copied
+__global__ void k_arrive_std(Pool P, Arrivals A, const Group* groups, uint32_t n_groups, uint32_t n_rows_tab,
+                             uint32_t l_max, uint32_t* err, const uint32_t* lhat0, uint32_t R) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n_new_items; i += stride) A.items_dst[i] = A.items_src[i];
+    if (blockIdx.x == 0 && threadIdx.x == 0) *A.n_items_dst = A.n_items;
+    bool bad = false;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += stride) {
+        const uint32_t r = A.n0 + i;
+        HotRow q;
+        q.arr = A.arr[i]; q.len_in = A.len_in[i]; q.gen = A.gen[i]; q.pre = A.pre[i];
+        q.lrow = A.aux[i] & 0xFFFFu;
+        q.meta = A.meta[i] & ~(kStamped << 12);
+        q.since = A.aux[i] >> 16;
+        const uint32_t id = A.id[i];
+        P.id[r] = id;
+        P.task[r] = A.task[i];                           // standalone: kNoTask (checked)
+        P.ovr[r] = A.ovr[i];
+        P.fair[r] = A.fair ? A.fair[i] : 0u;
+        const bool rb = row_invalid(P, groups, n_groups, n_rows_tab, l_max, r, q, A.n0 + A.n, 0u);
+        bad |= rb;
+        if (!rb && lhat0 && q.gen < R) seed_bound(q, lhat0, n_rows_tab, R);
+        P.rows[r] = q;
+        map_insert_row(P, id, r, err);
+    }
+    if (bad) atomicOr(err, 2u);
 }
 
 // task updates: a new current stage (its sub-deadline from the pattern, or given), the goodput of
@@ -822,28 +898,19 @@ __global__ void k_task_prep(Pool P, uint32_t t_begin) {
 // [r_begin, std_end) are standalone, the rest compound calls inside their task's rows (crng);
 // group types, ranges.  A load (t_begin == 0) also checks the CSR layout of jit_pool.
 __global__ void k_validate(Pool P, const Group* groups, uint32_t n_groups, uint32_t n_rows_tab, uint32_t l_max,
-                           uint32_t* err, uint32_t r_begin, uint32_t std_end, uint32_t t_begin) {
+                           uint32_t* err, uint32_t r_begin, uint32_t std_end, uint32_t t_begin,
+                           const uint32_t* lhat0, uint32_t R) {
     const uint32_t stride = gridDim.x * blockDim.x;
     bool bad = false;
     for (uint32_t r = r_begin + blockIdx.x * blockDim.x + threadIdx.x; r < P.n; r += stride) {
-        const HotRow q = P.rows[r];
-        const uint32_t meta = q.meta;
-        const uint32_t gi = m_group(meta);
-        const bool comp = (m_flags(meta) & kCompound) != 0;
-        if (gi >= n_groups || l_row(q.lrow) >= n_rows_tab || q.len_in == 0 || q.len_in >= (1u << 24) ||
-            q.gen >= (1u << 24) || q.pre > q.len_in || (meta >> 16) != 0 || m_state(meta) > kMoved ||
-            q.since > 0xFFFFu || comp != (r >= std_end)) bad = true;
-        else if (!comp) {
-            if (P.task[r] != kNoTask || groups[gi].type == kCMP) bad = true;
-        } else {
-            const uint32_t t = P.task[r];
-            if (t >= P.n_tasks || t < t_begin || groups[gi].type != kCMP || (m_flags(meta) & kOverride)) bad = true;
-            else if (r < P.crng[t].x || r >= P.crng[t].y) bad = true;
-            // a call's goodput w_in L_i + w_out L-hat stays below 2^27 (the pass sums 32 calls in u32)
-            else if ((uint64_t)groups[gi].w_in * q.len_in + (uint64_t)groups[gi].w_out * (l_max + 1ull) >= (1ull << 27))
-                bad = true;
+        HotRow q = P.rows[r];
+        const bool rb = row_invalid(P, groups, n_groups, n_rows_tab, l_max, r, q, std_end, t_begin);
+        bad |= rb;
+        if (!rb && lhat0 && q.gen < R) {                   // seed the bound of a row with g < R
+            seed_bound(q, lhat0, n_rows_tab, R);
+            P.rows[r].lrow = q.lrow;
+            P.rows[r].meta = q.meta;
         }
-        if (!bad && (m_flags(meta) & kOverride) && groups[gi].type == kCMP) bad = true;
     }
     for (uint32_t t = t_begin + blockIdx.x * blockDim.x + threadIdx.x; t < P.n_tasks; t += stride) {
         const uint32_t S = P.n_stages[t], s = P.cur_stage[t];

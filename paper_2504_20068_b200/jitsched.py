@@ -240,6 +240,15 @@ class Scheduler:
         self._tok = np.zeros(self.max_batch, np.uint32)
         self._rows = np.zeros(self.max_batch, np.uint32)
         self.n = 0
+        # per-step marshalling: the step's host arrays are copied into one persistent staging buffer
+        # and passed as base + offset (one ctypes address lookup per handle, not one per array);
+        # the jit_step_in / jit_batch structs are reused
+        self._stage = {}
+        self._si = jit_step_in()
+        self._ap = jit_pool()
+        self._b = jit_batch()
+        self._b.capacity = self.max_batch
+        self._b.ids, self._b.tokens, self._b.rows = _p(self._ids), _p(self._tok), _p(self._rows)
 
     def _check(self, rc, h):
         if rc < 0:
@@ -298,12 +307,67 @@ class Scheduler:
         self.n = p.n
 
     # ------------------------------------------------------------------ step
+    def _staged(self, name, a, dt):
+        """Copy host array `a` into this handle's persistent staging array for field `name` (grown
+        on demand); returns its address (a plain int, cached with the array)."""
+        n = len(a)
+        buf = self._stage.get(name)
+        if buf is None or buf[0].size < n:
+            arr = np.zeros(max(n, 1024), dt)
+            buf = (arr, arr.ctypes.data)
+            self._stage[name] = buf
+        np.copyto(buf[0][:n], a, casting="unsafe")
+        return buf[1]
+
+    def _fast_step(self, now_ns, v_token_ns, progress, arrivals):
+        """step() for the serving loop: host numpy progress / standalone arrivals, staged in one
+        buffer (the C call copies them into its own pinned staging before returning)."""
+        si = self._si
+        si.now_ns = int(now_ns)
+        si.v_token_ns = int(v_token_ns)
+        if progress is not None:
+            by_id = "id" in progress
+            key = progress["id" if by_id else "row"]
+            si.n_progress = len(key)
+            si.progress_by_id = 1 if by_id else 0
+            si.prog_key = self._staged("p_key", key, np.uint32)
+            si.prog_generated = self._staged("p_gen", progress["generated"], np.uint32)
+            si.prog_prefilled = self._staged("p_pre", progress["prefilled"], np.uint32)
+            si.prog_state = self._staged("p_state", progress["state"], np.uint32)
+        else:
+            si.n_progress = 0
+            si.prog_key = si.prog_generated = si.prog_prefilled = si.prog_state = None
+        na = 0
+        if arrivals is not None:
+            na = len(arrivals["input_len"])
+            ap = self._ap
+            ap.n = na
+            ap.n_single = int(arrivals.get("n_single", na))
+            ap.n_tasks = 0
+            ap.on_device = 0
+            for k, dt in _POOL_ROWS:
+                setattr(ap, k, self._staged("a_" + k, arrivals[k], dt))
+            ap.fair = self._staged("a_fair", arrivals["fair"], np.uint32) if arrivals.get("fair") is not None else None
+            si.arrivals = C.addressof(ap)
+        else:
+            si.arrivals = None
+        si.n_task_updates = 0
+        b = self._b
+        rc = self._check(self.lib.jit_sched_step(self.h, C.byref(si), C.byref(b)), self.h)
+        self.n += na
+        return self._batch_dict(rc, b)
+
     def step(self, now_ns: int, v_token_ns: int, progress=None, arrivals=None, arrival_tasks=None,
              task_updates=None) -> dict:
         """One GMAX step.  progress: dict with "id" (request ids) or "row" (pool rows) and generated,
         prefilled, state; arrivals (+ arrival_tasks): new requests in the load layout (their task
         fields / call_off local to the arrivals), appended to the pool; task_updates: dict task,
         cur_stage, goodput_done (+ optional stage_deadline_ns)."""
+        if arrival_tasks is None and task_updates is None and \
+                (arrivals is None or (isinstance(arrivals["input_len"], np.ndarray) and
+                                      int(arrivals.get("n_single", len(arrivals["input_len"]))) ==
+                                      len(arrivals["input_len"]))):
+            return self._fast_step(now_ns, v_token_ns, progress, arrivals)
         si = jit_step_in()
         si.now_ns = int(now_ns)
         si.v_token_ns = int(v_token_ns)
