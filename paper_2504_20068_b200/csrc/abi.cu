@@ -18,6 +18,8 @@
 #include "shard.cuh"
 #include "multi.cuh"
 
+constexpr uint32_t kSpecFastCap = 256;   // k_spec's fast-path set size (spec.cuh kSpecFast)
+
 #ifndef JIT_CMP_COST
 #define JIT_CMP_COST 3
 #endif
@@ -62,6 +64,8 @@ struct jit_sched {
     uint64_t launched = 0;            // steps launched (the stamp rebase runs every 2^30)
     unsigned long long multi_epoch = 0;   // power-of-K reconciles so far (tags S.mwin words)
     uint32_t bal_w_graph = 0;             // S.bal_w captured in the step graph
+    bool big_mode = false;                // the step graph chains k_spec_big_chain (large speculative sets)
+    uint32_t small_streak = 0;            // consecutive finished steps whose set fit k_spec (leave big mode)
     cudaEvent_t ev[6] = {};
     cudaGraphNode_t ev_node[5] = {};      // event-record nodes of the timed graph
     std::vector<cudaEvent_t> slots;       // 5 events per recorded step
@@ -484,7 +488,7 @@ static int build_graph(jit_sched* h) {
     if (h->timing) cudaEventRecordWithFlags(h->ev[0], s, cudaEventRecordExternal);
     enqueue_score(h, s, 0, 1, h->timing ? h->ev[1] : nullptr, true);
     if (h->timing) cudaEventRecordWithFlags(h->ev[2], s, cudaEventRecordExternal);
-    const cudaError_t le = exact::spec(h->P, h->c, h->d_ctrl, S, 0, s, !h->timing && h->pdl);
+    const cudaError_t le = exact::spec(h->P, h->c, h->d_ctrl, S, 0, s, !h->timing && h->pdl, h->big_mode);
     if (h->timing) {
         cudaEventRecordWithFlags(h->ev[3], s, cudaEventRecordExternal);
         cudaEventRecordWithFlags(h->ev[4], s, cudaEventRecordExternal);
@@ -536,7 +540,7 @@ static int launch_direct(jit_sched* h, int64_t now, int64_t v) {
     if (ev) cudaEventRecord(e[0], s);
     enqueue_score(h, s, now, v, ev ? e[1] : nullptr, false);
     if (ev) cudaEventRecord(e[2], s);
-    CK(exact::spec(h->P, h->c, h->d_ctrl, h->S, 0, s, !ev && h->pdl));
+    CK(exact::spec(h->P, h->c, h->d_ctrl, h->S, 0, s, !ev && h->pdl, h->big_mode));
     if (ev) { cudaEventRecord(e[3], s); cudaEventRecord(e[4], s); }
     CK(cudaGetLastError());
     return JIT_OK;
@@ -599,10 +603,20 @@ static int finish_step_body(jit_sched* h, jit_batch* out) {
                 h->h_ctrl->fallback, h->h_ctrl->spec_n);
     }
     if (h->h_ctrl->status == ST_SPEC_BIG) {
-        // a speculative set too large for k_spec's fast path (e.g. after a shift of the keys)
+        // a speculative set too large for k_spec's fast path (e.g. after a shift of the keys): resolve
+        // it now, and chain the big-set resolve in the step graph from here on (big mode) so that
+        // such steps stay on the device
         exact::spec_big(h->P, h->c, h->d_ctrl, h->S, h->stream);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(h->stream));
+        if (!h->big_mode) { h->big_mode = true; h->graph_dirty = true; }
+        h->small_streak = 0;
+    } else if (h->big_mode) {                             // back to the lean graph after 8 small sets
+        if (h->h_ctrl->spec_n <= kSpecFastCap) {
+            if (++h->small_streak >= 8) { h->big_mode = false; h->graph_dirty = true; h->small_streak = 0; }
+        } else {
+            h->small_streak = 0;
+        }
     }
     const uint32_t st0 = h->h_ctrl->status;
     const bool host_work = st0 == ST_FALLBACK || (st0 == ST_RESOLVED && !h->h_ctrl->window_done && !h->h_ctrl->error);

@@ -21,10 +21,12 @@ cudaError_t init_attributes() {
         cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(k_spec_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSpecSmem)) !=
         cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(k_spec_big_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSpecSmem)) !=
+        cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(k_spec_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSpecSmem)) !=
         cudaSuccess) return e;
     // one shared-memory carveout for every kernel of the step (see abi.cu)
-    const void* ks[] = {(const void*)k_spec, (const void*)k_spec_big,
+    const void* ks[] = {(const void*)k_spec, (const void*)k_spec_big, (const void*)k_spec_big_chain,
                         (const void*)k_hist0, (const void*)k_pass, (const void*)k_compact, (const void*)k_resolve,
                         (const void*)k_cand, (const void*)k_group};
     for (const void* k : ks)
@@ -33,7 +35,8 @@ cudaError_t init_attributes() {
     return cudaSuccess;
 }
 
-cudaError_t spec(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int reduce_only, cudaStream_t s, bool pdl) {
+cudaError_t spec(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int reduce_only, cudaStream_t s, bool pdl,
+                 bool big_chain) {
     cudaLaunchConfig_t cfg = {};
     // k_spec only runs the small-set resolve (a larger set goes to k_spec_big): its smem is small
     cfg.gridDim = dim3(1); cfg.blockDim = dim3(kSpecThreads); cfg.dynamicSmemBytes = kSpecFastSmem; cfg.stream = s;
@@ -41,7 +44,10 @@ cudaError_t spec(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int 
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at; cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, k_spec, P, c, ctrl, S, reduce_only);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_spec, P, c, ctrl, S, reduce_only, (int)big_chain);
+    if (e != cudaSuccess || !big_chain) return e;
+    k_spec_big_chain<<<1, kSpecThreads, kSpecSmem, s>>>(P, c, ctrl, S);
+    return cudaGetLastError();
 }
 cudaError_t spec_export(const Scratch& S, Ctrl* ctrl, void* out, uint32_t rank, cudaStream_t s) {
     k_spec_export<<<1, kSpecThreads, 0, s>>>(ctrl, S, reinterpret_cast<unsigned char*>(out), rank);

@@ -15,7 +15,8 @@ cudaError_t init_attributes();
 // the window, or mark the step for the host-driven exact path (status FALLBACK / window_done 0);
 // publishes the control block to pinned host memory.  pdl: programmatic dependent launch after
 // k_score (its launch overlaps k_score; it waits with griddepcontrol.wait)
-cudaError_t spec(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int reduce_only, cudaStream_t s, bool pdl);
+cudaError_t spec(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int reduce_only, cudaStream_t s, bool pdl,
+                 bool big_chain = false);
 // fast sharded step: export this rank's speculative set + totals (after k_score), and resolve the
 // allgathered union on every rank (status FALLBACK: run the exact two-round protocol)
 cudaError_t spec_export(const Scratch& S, Ctrl* ctrl, void* out, uint32_t rank, cudaStream_t s);

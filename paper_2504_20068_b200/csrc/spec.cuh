@@ -326,7 +326,8 @@ static __device__ void spec_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const 
 // end to the device copy and the pinned host mirror -- no load round trip on the tail.
 // (now / v, word 1, are left as k_score wrote them: nothing reads them back.)
 static_assert(offsetof(Ctrl, now) == 16 && offsetof(Ctrl, v) == 24, "ctrl word 1 = (now, v)");
-__global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl, Scratch S, int reduce_only) {
+__global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl, Scratch S, int reduce_only,
+                                                      int big_chain) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ Ctrl s_ctrl;
     __shared__ uint32_t s_skip;
@@ -341,7 +342,7 @@ __global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl
     __syncthreads();
     if (threadIdx.x == 0 && !reduce_only) {
         const uint32_t st = s_ctrl.status;
-        S.persist->host_pending = (st == ST_FALLBACK || st == ST_SPEC_BIG ||
+        S.persist->host_pending = (st == ST_FALLBACK || (st == ST_SPEC_BIG && !big_chain) ||
                                    (st == ST_RESOLVED && !s_ctrl.window_done && !s_ctrl.error)) ? 1u : 0u;
     }
     for (uint32_t i = threadIdx.x; i < sizeof(Ctrl) / 16; i += blockDim.x) {
@@ -354,6 +355,24 @@ __global__ void __launch_bounds__(kSpecThreads) k_spec(Pool P, Cfg c, Ctrl* ctrl
 __global__ void __launch_bounds__(kSpecThreads) k_spec_big(Pool P, Cfg c, Ctrl* ctrl, Scratch S) {
     extern __shared__ __align__(16) unsigned char smem[];
     spec_body<true>(P, c, ctrl, S, 0, smem);
+    publish_ctrl(ctrl, S.h_ctrl);
+}
+// The big-set resolve chained in the step graph (the handle's "big mode", chosen by the host when
+// the speculative sets outgrow k_spec's fast path, e.g. C4): runs only when k_spec left
+// ST_SPEC_BIG, so a step resolves on the device without a host round trip; else it returns.
+__global__ void __launch_bounds__(kSpecThreads) k_spec_big_chain(Pool P, Cfg c, Ctrl* ctrl, Scratch S) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint32_t s_go;
+    if (threadIdx.x == 0) s_go = ctrl->status == ST_SPEC_BIG;
+    __syncthreads();
+    if (!s_go) return;
+    spec_body<true>(P, c, ctrl, S, 0, smem);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t st = ctrl->status;
+        S.persist->host_pending = (st == ST_FALLBACK || st == ST_SPEC_BIG ||
+                                   (st == ST_RESOLVED && !ctrl->window_done && !ctrl->error)) ? 1u : 0u;
+    }
     publish_ctrl(ctrl, S.h_ctrl);
 }
 

@@ -193,3 +193,32 @@ def test_step_counter_wrap_and_stamp_rebase():
         d2["pool"] = st
         _chain(d2, s, 30, f"case {it} across the wrap")
         s.close()
+
+
+def test_big_sets_resolve_on_device_in_chained_steps():
+    """Speculative sets larger than k_spec's fast path (C4-shaped pool): after the first such step
+    the handle chains the big-set resolve in its step graph, so chained step_async steps resolve on
+    the device (no host path, nothing skipped); every step still equals the oracle chain."""
+    from .test_parity_gpu import _compare, _sched
+    d = W.pool_c4(n_tasks=20_000, table_draws=1 << 15)
+    s = _sched(d, debug=False)
+    s.load(d["pool"], d["tasks"])
+    pool = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in d["pool"].items()}
+    refs = []
+    for k in range(6):
+        ref = oracle.step(d["cfg"], d["groups"], d["table"], d["now_ns"], d["v_token_ns"], pool, d["tasks"])
+        pool["meta"], pool["aux"] = ref["meta"], ref["aux"]
+        refs.append(ref)
+    for k in range(2):                                   # exact path, then a host-resolved big set
+        _compare(s.step(d["now_ns"], d["v_token_ns"]), refs[k], ctx=f"C4 step {k}")
+    c0 = s.counters()
+    for k in range(2, 5):
+        s.step_async(d["now_ns"], d["v_token_ns"])
+    got = s.fetch()
+    c1 = s.counters()
+    assert got["n_spec"] > 256, got["n_spec"]
+    assert c1["fallbacks"] == c0["fallbacks"] and c1["skipped"] == c0["skipped"], (c0, c1)
+    assert c1["steps"] == c0["steps"] + 3
+    _compare(got, refs[4], s.read_rows(debug=False), ctx="C4 chained step 4")
+    _compare(s.step(d["now_ns"], d["v_token_ns"]), refs[5], ctx="C4 step 5")
+    s.close()
