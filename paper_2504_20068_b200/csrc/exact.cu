@@ -46,7 +46,11 @@ cudaError_t spec(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int 
     cfg.attrs = at; cfg.numAttrs = pdl ? 1 : 0;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, k_spec, P, c, ctrl, S, reduce_only, (int)big_chain);
     if (e != cudaSuccess || !big_chain) return e;
+    // big mode: the big-set resolve, then the window over a large Cd (k_group runs only when the
+    // resolve left it undone), then the host flag and the published control block
     k_spec_big_chain<<<1, kSpecThreads, kSpecSmem, s>>>(P, c, ctrl, S);
+    k_group<<<1, 1024, 12 * kGroupSmemSort, s>>>(P, c, ctrl, S);
+    k_chain_publish<<<1, 64, 0, s>>>(ctrl, S.persist, S.h_ctrl);
     return cudaGetLastError();
 }
 cudaError_t spec_export(const Scratch& S, Ctrl* ctrl, void* out, uint32_t rank, cudaStream_t s) {

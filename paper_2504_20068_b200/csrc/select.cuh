@@ -648,6 +648,7 @@ static __device__ void group_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const
 // k_publish: copies the control block to pinned host memory (end of the host-run exact path)
 __global__ void k_publish(const Ctrl* ctrl, Ctrl* host) { publish_ctrl(ctrl, host); }
 
+
 // load: pack the caller's SoA pool into hot rows.  lrow = dist_row | L-hat unset; the count in
 // aux's high half becomes the frozen steps_waited (the first step stamps the pending rows).
 // A row with g < R has the anchor 0, so its cached bound is the table row's unconditioned

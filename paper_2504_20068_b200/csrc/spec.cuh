@@ -357,23 +357,27 @@ __global__ void __launch_bounds__(kSpecThreads) k_spec_big(Pool P, Cfg c, Ctrl* 
     spec_body<true>(P, c, ctrl, S, 0, smem);
     publish_ctrl(ctrl, S.h_ctrl);
 }
+// the tail of a big-mode step graph (after k_spec_big_chain and k_group): whether the host still
+// has work (exact path), then the control block to pinned host memory
+__global__ void k_chain_publish(Ctrl* ctrl, Persist* ps, Ctrl* host) {
+    if (threadIdx.x == 0) {
+        const uint32_t st = ctrl->status;
+        ps->host_pending = (st == ST_FALLBACK || st == ST_SPEC_BIG ||
+                            (st == ST_RESOLVED && !ctrl->window_done && !ctrl->error)) ? 1u : 0u;
+    }
+    publish_ctrl(ctrl, host);
+}
 // The big-set resolve chained in the step graph (the handle's "big mode", chosen by the host when
 // the speculative sets outgrow k_spec's fast path, e.g. C4): runs only when k_spec left
 // ST_SPEC_BIG, so a step resolves on the device without a host round trip; else it returns.
+// Followed by k_group (a large Cd's window) and k_chain_publish.
 __global__ void __launch_bounds__(kSpecThreads) k_spec_big_chain(Pool P, Cfg c, Ctrl* ctrl, Scratch S) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t s_go;
     if (threadIdx.x == 0) s_go = ctrl->status == ST_SPEC_BIG;
     __syncthreads();
     if (!s_go) return;
-    spec_body<true>(P, c, ctrl, S, 0, smem);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const uint32_t st = ctrl->status;
-        S.persist->host_pending = (st == ST_FALLBACK || st == ST_SPEC_BIG ||
-                                   (st == ST_RESOLVED && !ctrl->window_done && !ctrl->error)) ? 1u : 0u;
-    }
-    publish_ctrl(ctrl, S.h_ctrl);
+    spec_body<true>(P, c, ctrl, S, 0, smem);             // host flag and publish: k_chain_publish
 }
 
 // ---- fast sharded step (the speculative variant): every rank scores its shard and
