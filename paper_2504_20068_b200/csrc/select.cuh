@@ -536,7 +536,7 @@ static __device__ void window_select(const Pool& P, const Cfg& c, Ctrl* ctrl, co
     for (uint32_t i = n + threadIdx.x; i < n2; i += blockDim.x) { sk[i] = ~0ull; sv[i] = 0; }
     __syncthreads();
     stamp(ctrl, 6);
-    block_sort<uint64_t>(sk, sv, n2);
+    block_sort_wide(sk, sv, n2);
     stamp(ctrl, 7);
     uint64_t carry_c = 0;
     u128 carry_f = 0;
