@@ -67,6 +67,7 @@ __device__ __forceinline__ void score_standalone(const Cfg& c, const Table& T, c
     const uint32_t ep = fastdiv(g, c.R, c.R_m, c.R_l);
     if (lhat == 0 || ep >= 65536u || m_epoch(meta) != ep) {
         lhat = T.forest ? qrf_bound(T.forest, L_i, drow, ep * c.R, gi, ep * c.R, c.qn, c.qd, T.l_max)
+                        : ep == 0 ? __ldg(T.lhat0 + drow)    // anchor 0: the per-row table (k_lhat0)
                         : cond_quantile(T, drow, ep * c.R, c.qn, c.qd);
         o.lhat = lhat; o.w_lhat = true;
         if (ep < 65536u) { o.meta = (meta & 0xFFFFu) | (ep << 16); o.w_meta = true; }
@@ -97,6 +98,8 @@ namespace jit {
 // step is barrier- and latency-bound, measured 1.8x the sweep throughput)
 constexpr uint32_t kReplayThreads = 512;
 constexpr uint32_t kReplayThreadsSweep = 256;
+constexpr uint32_t kReplayThreadsTiny = 64;     // traces of <= 64 rows (e.g. C1): two warps, cheap barriers
+constexpr uint32_t kReplayTinyRows = 64;
 constexpr uint32_t kReplaySmemRows = 2048;    // rows sorted in shared memory up to this size
 
 struct TraceMeta { uint32_t row_off, task_off, n_rows, n_tasks, n_std, pad; };   // n_std: standalone rows
@@ -474,6 +477,7 @@ __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
                     if (lhat == 0 || ep >= 65536u || m_epoch(meta) != ep) {
                         lhat = T.forest ? qrf_bound(T.forest, L_in[r], S.aux[r] & 0xFFFFu, ep * c.R, m_group(meta),
                                                     ep * c.R, c.qn, c.qd, T.l_max)
+                                        : ep == 0 ? __ldg(T.lhat0 + (S.aux[r] & 0xFFFFu))
                                         : cond_quantile(T, S.aux[r] & 0xFFFFu, ep * c.R, c.qn, c.qd);
                         S.lhat[r] = lhat;
                         if (ep < 65536u) S.meta[r] = (meta & 0xFFFFu) | (ep << 16);
