@@ -541,6 +541,98 @@ __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
                 continue;
             }
 
+            // ---- (a7)-(a9) for at most 32 pending rows: warp 0 alone, everything in registers and
+            // shuffles (the block's many short barrier-separated phases dominate a small step);
+            // the same orders, sums and tie-breaks as the general path below, so the same batch.
+            // Not in the sweep configuration (its registers would cost the sweep's occupancy).
+            if (NT != kReplayThreadsSweep && np <= 32u) {
+                if (wid == 0) {
+                    // the pending rows (img != kNone) of the live list, compacted to lanes 0..np-1
+                    uint32_t cnt = 0;
+                    for (uint32_t base = 0; base < nl; base += 32) {
+                        const uint32_t i = base + lane;
+                        const uint32_t r = i < nl ? S.live[i] : 0u;
+                        const bool p = i < nl && S.img[r] != kNone;
+                        const unsigned pm = __ballot_sync(0xffffffffu, p);
+                        if (p) bAv[cnt + __popc(pm & ((1u << lane) - 1u))] = r;
+                        cnt += __popc(pm);
+                    }
+                    __syncwarp();
+                    const bool own = lane < np;
+                    uint32_t row = own ? bAv[lane] : 0u;
+                    u128 ck = own ? make_ck(S.img[row], row) : ~(u128)0;
+                    // (a7) ascending composite key (key desc, id asc): 32-lane bitonic network
+                    for (uint32_t size = 2; size <= 32; size <<= 1)
+                        for (uint32_t j = size >> 1; j > 0; j >>= 1) {
+                            const u128 ok = shfl_xor_u128(ck, (int)j);
+                            const uint32_t orow = __shfl_xor_sync(0xffffffffu, row, (int)j);
+                            const bool up = (lane & size) == 0, lower = (lane & j) == 0;
+                            if (lower == up ? (ok < ck) : (ok > ck)) { ck = ok; row = orow; }
+                        }
+                    const uint64_t img = own ? ck_img(ck) : kNone;
+                    uint64_t pre = own ? (uint64_t)S.cost[row] : 0ull;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint64_t y = __shfl_up_sync(0xffffffffu, pre, o);
+                        if (lane >= (uint32_t)o) pre += y;
+                    }
+                    const bool fits = own && lane + 1 <= c.max_batch && pre <= c.token_budget;
+                    const uint32_t bstar = __popc(__ballot_sync(0xffffffffu, fits));
+                    const uint64_t bp_img = __shfl_sync(0xffffffffu, img, bstar ? bstar - 1 : 0);
+                    const double bp = __longlong_as_double((long long)bp_img);
+                    const double thr = __dmul_rn(s_p, bp);
+                    const uint64_t thr_img = (uint64_t)__double_as_longlong(thr);
+                    // (a8) Cd = the prefix with key >= thr; (a9) its (len, id) order
+                    const bool cd = own && img >= thr_img;
+                    const uint32_t ncd_w = __popc(__ballot_sync(0xffffffffu, cd));
+                    uint64_t wk = cd ? (((uint64_t)(c.len_key ? L_in[row] + S.gen[row] : L_in[row]) << 32) | row) : ~0ull;
+                    for (uint32_t size = 2; size <= 32; size <<= 1)
+                        for (uint32_t j = size >> 1; j > 0; j >>= 1) {
+                            const uint64_t ok = __shfl_xor_sync(0xffffffffu, wk, (int)j);
+                            const uint32_t orow = __shfl_xor_sync(0xffffffffu, row, (int)j);
+                            const bool up = (lane & size) == 0, lower = (lane & j) == 0;
+                            if (lower == up ? (ok < wk) : (ok > wk)) { wk = ok; row = orow; }
+                        }
+                    const bool inw = lane < ncd_w;
+                    const uint64_t cv = inw ? (uint64_t)S.cost[row] : 0ull;
+                    const u128 fv = inw ? (u128)fixed_point(__longlong_as_double((long long)S.img[row])) : (u128)0;
+                    uint64_t pci = cv;                                  // inclusive prefix sums in window order
+                    u128 pfi = fv;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint64_t yc = __shfl_up_sync(0xffffffffu, pci, o);
+                        const u128 yf = shfl_up_u128(pfi, o);
+                        if (lane >= (uint32_t)o) { pci += yc; pfi += yf; }
+                    }
+                    const uint64_t pce = pci - cv;                      // exclusive (pc[i])
+                    const u128 pfe = pfi - fv;
+                    // the window of start i: the largest j <= min(ncd - 1, i + B_max - 1) with
+                    // pc[j + 1] <= pc[i] + tau (a uniform 5-step binary search over the lanes)
+                    const uint64_t lim = pce + c.token_budget;
+                    uint32_t lo = lane, hi = inw ? (uint32_t)min((uint64_t)ncd_w - 1, (uint64_t)lane + c.max_batch - 1) : lane;
+                    for (int it = 0; it < 5; ++it) {
+                        const uint32_t mid = lo < hi ? (lo + hi + 1) >> 1 : lo;
+                        const uint64_t v = __shfl_sync(0xffffffffu, pci, mid);
+                        if (lo < hi) { if (v <= lim) lo = mid; else hi = mid - 1; }
+                    }
+                    const uint64_t hi64 = __shfl_sync(0xffffffffu, (uint64_t)(pfi >> 64), lo);
+                    const uint64_t lo64 = __shfl_sync(0xffffffffu, (uint64_t)pfi, lo);
+                    u128 best = (((u128)hi64 << 64) | lo64) - pfe;
+                    uint32_t bi = inw ? lane : 0xFFFFFFFFu, bj = lo;
+                    for (int o = 16; o > 0; o >>= 1) {                  // first maximum (strict >)
+                        const u128 ob = shfl_xor_u128(best, o);
+                        const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o), oj = __shfl_xor_sync(0xffffffffu, bj, o);
+                        if ((oi != 0xFFFFFFFFu) && (bi == 0xFFFFFFFFu || ob > best || (ob == best && oi < bi))) { best = ob; bi = oi; bj = oj; }
+                    }
+                    if (inw) bBv[lane] = row;                           // window order, the batch = [bi, bj]
+                    const uint64_t tot = __shfl_sync(0xffffffffu, pci, bj) - __shfl_sync(0xffffffffu, pce, bi);
+                    if (lane == 0) {
+                        s_bstar = bstar; s_bp = bp; s_thr = thr; s_thr_img = thr_img;
+                        s_tguess = (uint64_t)__double_as_longlong(__dmul_rn(thr, 0.85));
+                        s_m = np; s_ncd = ncd_w; s_nsel = bj - bi + 1; s_tot = (uint32_t)tot; s_bi[0] = bi;
+                    }
+                }
+                __syncthreads();
+                RSTAMP(7);
+            } else {
             // ---- (a7) order pending by (key desc, id asc).  Attempt 0 sorts only the speculative
             // set S = {key >= t} (t = 0.85 x the previous step's cutoff): S is a prefix of the
             // priority order, so its budget walk is exact when it stops inside S (or S holds every
@@ -700,6 +792,7 @@ __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
                 __syncthreads();
                 RSTAMP(7);
             }
+            }
             uint32_t nsel = s_nsel;
             const uint32_t* selv = bBv + s_bi[0];          // the batch rows: GMAX's window ...
             if (c.preempt) {
@@ -844,7 +937,7 @@ __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
                     uint64_t h = 1469598103934665603ull;
                     for (uint32_t k = 0; k < nsel; ++k) h = fnv1a_u32(h, S.batch[k]);
                     RLog L;
-                    L.now_ns = tnow; L.n_selected = nsel; L.total_tokens = s_tot; L.n_candidates = ncd;
+                    L.now_ns = tnow; L.n_selected = nsel; L.total_tokens = s_tot; L.n_candidates = s_ncd;
                     L.b_star = s_bstar; L.bp = s_bp; L.ids_hash = h; L.v_token_ns = v;
                     L.n_preempted = c.preempt ? s_npre : 0u; L.p_num = s_pnum; L.stall_ns = stall;
                     A.log[(uint64_t)rep * A.log_steps + s_steps - 1] = L;
