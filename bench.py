@@ -739,6 +739,7 @@ def run_single(args, dev, stream):
     k_b2b = Scheduler.time_scoring(hs, now, v, n_b2b)      # (3) k_score back to back
     k_refresh = Scheduler.time_scoring(hs, now, v, 12, force_refresh=True)   # (4) every bound stale
     k_refresh2 = Scheduler.time_scoring(hs, now, v, 30, refresh_2pct=True)  # (5) every 50th bound stale
+    k_floor = Scheduler.time_scoring(hs, now, v, n_b2b, read_floor=True)   # (6) the rows read, nothing else
     for _ in range(3):
         for k in range(20):
             hs[k % rot].step_async(now, v)
@@ -768,6 +769,13 @@ def run_single(args, dev, stream):
                 "forced_refresh": {"k_score_ms": k_refresh, "frac": hot / (k_refresh / 1e3) / 1e9 / hbm,
                                    "how": "every cached length bound invalidated before each launch (untimed); each "
                                           "launch timed alone, so it also carries its launch latency"},
+                "read_floor": {"ms": k_floor, "gbs": n * 32 / (k_floor / 1e3) / 1e9,
+                               "frac_of_peak": n * 32 / (k_floor / 1e3) / 1e9 / hbm,
+                               "k_score_over_floor": k_floor / k_b2b * (hot / (n * 32)),
+                               "how": "the pool's 32-B hot rows read with k_score's load pattern (256-bit loads, next "
+                                      "chunk in flight) and nothing else, back to back over the same rotated copies: "
+                                      "the achievable time of this footprint; k_score_over_floor = the floor's GB/s "
+                                      "over k_score's"},
                 "refresh_2pct": {"k_score_ms": k_refresh2, "frac": hot / (k_refresh2 / 1e3) / 1e9 / hbm,
                                  "how": "every 50th row's cached bound invalidated before each launch (SURVEY 8(d)'s "
                                         "steady state of about 2% refresh); each launch timed alone"},

@@ -238,6 +238,7 @@ int jit_sched_kernel_times(jit_sched* h, int enable, float* ms_out, uint32_t n_o
  * same with every 50th row stale (the steady state's ~2% refresh). */
 #define JIT_TIME_FORCE_REFRESH 1u
 #define JIT_TIME_REFRESH_2PCT 2u   /* every 50th row's bound invalidated before each launch (SURVEY 8(d) "about 2%") */
+#define JIT_TIME_READ_FLOOR 4u     /* instead of k_score: the hot rows read with its load pattern and nothing else */
 int jit_sched_time_scoring(jit_sched** hs, uint32_t n_handles, int64_t now_ns, int64_t v_token_ns, uint32_t launches,
                            uint32_t flags, float* ms_per_launch);
 

@@ -939,6 +939,19 @@ extern "C" int jit_sched_time_scoring(jit_sched** hs, uint32_t n_handles, int64_
     cudaEvent_t e0 = h->ev[0], e1 = h->ev[1];
     CK(cudaStreamSynchronize(s));
     float ms = 0.f;
+    if (flags & JIT_TIME_READ_FLOOR) {
+        // the hot rows of each handle read with k_score's load pattern and nothing else
+        CK(cudaEventRecord(e0, s));
+        for (uint32_t k = 0; k < launches; ++k) {
+            jit_sched* hk = hs[k % n_handles];
+            k_read_floor<<<4 * hk->n_sm, 256, 0, s>>>(hk->P.rows, hk->P.n, reinterpret_cast<unsigned long long*>(hk->S.sk));
+        }
+        CK(cudaEventRecord(e1, s));
+        CK(cudaEventSynchronize(e1));
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        *ms_per_launch = ms / (float)launches;
+        return JIT_OK;
+    }
     if (flags & (JIT_TIME_FORCE_REFRESH | JIT_TIME_REFRESH_2PCT)) {
         for (uint32_t k = 0; k < launches; ++k) {
             jit_sched* hk = hs[k % n_handles];

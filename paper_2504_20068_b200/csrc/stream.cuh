@@ -841,4 +841,32 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
 #endif
 }
 
+// Measurement only (jit_sched_time_scoring, JIT_TIME_READ_FLOOR): the pool's hot rows read the
+// way k_score reads its standalone slabs (256-bit loads, 2 rows per lane, the next chunk in flight)
+// and nothing else -- the achievable time of this footprint, the denominator k_score is compared
+// with beside the copy peak.
+__global__ void __launch_bounds__(256) k_read_floor(const HotRow* rows, uint32_t n, unsigned long long* sink) {
+    const uint32_t lane = threadIdx.x & 31, W = gridDim.x * 8, w = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const uint32_t n32 = (n + 31) >> 5, s0 = (uint32_t)((uint64_t)n32 * w / W), s1 = (uint32_t)((uint64_t)n32 * (w + 1) / W);
+    uint64_t acc = 0;
+    HotRow cur[2], nxt[2];
+    auto load = [&](HotRow* q, uint32_t sb) {
+#pragma unroll
+        for (uint32_t k = 0; k < 2; ++k) {
+            const uint32_t r = 32 * (sb + k) + lane;
+            q[k] = (sb + k < s1 && r < n) ? ld_row_g(rows + r) : HotRow{0, 0, 0, 0, 0, 0, 0};
+        }
+    };
+    if (s0 < s1) load(cur, s0);
+    for (uint32_t sb = s0; sb < s1; sb += 2) {
+        if (sb + 2 < s1) load(nxt, sb + 2);
+#pragma unroll
+        for (uint32_t k = 0; k < 2; ++k)
+            acc ^= (uint64_t)cur[k].arr ^ cur[k].len_in ^ cur[k].gen ^ cur[k].pre ^ cur[k].lrow ^ cur[k].meta ^ cur[k].since;
+#pragma unroll
+        for (uint32_t k = 0; k < 2; ++k) cur[k] = nxt[k];
+    }
+    if (acc == 0x0123456789ABCDEFull) sink[blockIdx.x & 63] = acc;       // keeps the loads alive
+}
+
 }  // namespace jit

@@ -569,7 +569,7 @@ class Scheduler:
 
     @staticmethod
     def time_scoring(handles, now_ns: int, v_token_ns: int, launches: int, force_refresh: bool = False,
-                     refresh_2pct: bool = False) -> float:
+                     refresh_2pct: bool = False, read_floor: bool = False) -> float:
         """Average ms of back-to-back k_score launches rotating over `handles` (same stream);
         force_refresh: every cached length bound stale before each launch (each launch timed alone)."""
         lib = load_library()
@@ -577,7 +577,8 @@ class Scheduler:
         ms = C.c_float()
         rc = lib.jit_sched_time_scoring(arr, C.c_uint32(len(handles)), C.c_int64(now_ns), C.c_int64(v_token_ns),
                                         C.c_uint32(launches),
-                                        C.c_uint32((1 if force_refresh else 0) | (2 if refresh_2pct else 0)), C.byref(ms))
+                                        C.c_uint32((1 if force_refresh else 0) | (2 if refresh_2pct else 0) |
+                                                   (4 if read_floor else 0)), C.byref(ms))
         handles[0]._check(rc, handles[0].h)
         return float(ms.value)
 
