@@ -94,10 +94,15 @@ __device__ __forceinline__ void score_standalone(const Cfg& c, const Table& T, c
 namespace jit {
 
 // one replay = one CTA: 512 threads when a few replays run (one long trace: the per-step passes
-// spread wide), 256 threads x several CTAs per SM for sweeps (more replays in flight per SM: the
-// step is barrier- and latency-bound, measured 1.8x the sweep throughput)
+// spread wide), 128 threads x 8 CTAs per SM for sweeps (more replays in flight per SM: the step is
+// barrier- and latency-bound).  C5(i) sweep on B200 (profiles/sweep_variants.py): 256 threads x 3
+// CTAs (2048 sort rows in shared memory) 9.8 M steps/s; 128 x 6 (1024 rows) 11.0; 128 x 6 (512)
+// 12.5; 128 x 8 (512 rows, 64 registers) 13.0; 128 x 8 (256) 12.2; 96 x 8 11.4; 64 x 12 8.9.
+// A step whose live rows exceed the shared sort buffers sorts in the CTA's global slice.
 constexpr uint32_t kReplayThreads = 512;
-constexpr uint32_t kReplayThreadsSweep = 256;
+constexpr uint32_t kReplayThreadsSweep = 128;
+constexpr uint32_t kReplaySweepRows = 512;     // sweep CTAs: rows sorted in shared memory
+constexpr uint32_t kReplaySweepCtas = 8;       // sweep CTAs per SM (launch bounds: <= 64 registers)
 constexpr uint32_t kReplayThreadsTiny = 64;     // traces of <= 64 rows (e.g. C1): two warps, cheap barriers
 constexpr uint32_t kReplayTinyRows = 64;
 constexpr uint32_t kReplaySmemRows = 2048;    // rows sorted in shared memory up to this size
@@ -227,8 +232,8 @@ __host__ __device__ inline uint32_t replay_groups_bytes(uint32_t n_groups) {
 #else
 #define RSTAMP(i) do {} while (0)
 #endif
-template <uint32_t NT>
-__global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
+template <uint32_t NT, uint32_t SR, bool kSweep, uint32_t MINB>
+__global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
 #ifdef JIT_REPLAY_STAMPS
     __shared__ unsigned long long s_ph[16], s_ph_last;
     if (threadIdx.x < 16) s_ph[threadIdx.x] = 0;
@@ -240,9 +245,9 @@ __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
     // region A (24 cap + 64 B): pending sort (u128 key + u32 row), later reused for the
     // window prefix sums (u64 cost + u128 fixed-point key); region B: Cd sort (u64 + u32)
     u128* sA = reinterpret_cast<u128*>(sbuf);
-    uint32_t* sAv = reinterpret_cast<uint32_t*>(sbuf + 16 * kReplaySmemRows);
-    uint64_t* sB = reinterpret_cast<uint64_t*>(sbuf + 24 * kReplaySmemRows + 64);
-    uint32_t* sBv = reinterpret_cast<uint32_t*>(sbuf + 32 * kReplaySmemRows + 64);
+    uint32_t* sAv = reinterpret_cast<uint32_t*>(sbuf + 16 * SR);
+    uint64_t* sB = reinterpret_cast<uint64_t*>(sbuf + 24 * SR + 64);
+    uint32_t* sBv = reinterpret_cast<uint32_t*>(sbuf + 32 * SR + 64);
     __shared__ uint64_t s_scan[32];
     __shared__ u128 s_scan128[32];
     __shared__ u128 s_best[32];
@@ -269,7 +274,7 @@ __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     // the replay state in shared memory (behind the sort buffers) when it fits, else in this CTA's
     // global slice
-    RState S = A.state_smem ? carve_core(sbuf + 36 * kReplaySmemRows + 64, A.max_rows, A.max_tasks, c.max_batch)
+    RState S = A.state_smem ? carve_core(sbuf + 36 * SR + 64, A.max_rows, A.max_tasks, c.max_batch)
                             : carve_state(A.state + (uint64_t)blockIdx.x * A.state_stride, A.max_rows, A.max_tasks,
                                           c.max_batch);
 
@@ -421,7 +426,7 @@ __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
             const uint32_t nl = s_nlive;
             // every sort / prefix array of the step holds at most the live rows: shared memory when
             // they fit (whatever the trace length), else this CTA's global scratch
-            const bool in_smem = nl <= kReplaySmemRows;
+            const bool in_smem = nl <= SR;
             u128* bA = in_smem ? sA : S.gA;
             uint32_t* bAv = in_smem ? sAv : S.gAv;
             uint64_t* bB = in_smem ? sB : S.gB;
@@ -545,7 +550,7 @@ __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
             // shuffles (the block's many short barrier-separated phases dominate a small step);
             // the same orders, sums and tie-breaks as the general path below, so the same batch.
             // Not in the sweep configuration (its registers would cost the sweep's occupancy).
-            if (NT != kReplayThreadsSweep && np <= 32u) {
+            if (!kSweep && np <= 32u) {
                 if (wid == 0) {
                     // the pending rows (img != kNone) of the live list, compacted to lanes 0..np-1
                     uint32_t cnt = 0;
@@ -732,7 +737,7 @@ __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
             // ---- (a9) sort Cd by (len, id); windows within tau / B_max; first argmax
             block_sort<uint64_t>(bB, bBv, m2);
             unsigned long long* pc = in_smem ? reinterpret_cast<unsigned long long*>(sA) : S.gpc;   // reuse region A
-            u128* pf = in_smem ? reinterpret_cast<u128*>(sbuf + ((8 * (kReplaySmemRows + 1) + 15) & ~15u)) : S.gpf;
+            u128* pf = in_smem ? reinterpret_cast<u128*>(sbuf + ((8 * (SR + 1) + 15) & ~15u)) : S.gpf;
             {
                 uint64_t carry_c = 0; u128 carry_f = 0;
                 for (uint32_t base = 0; base < ncd; base += blockDim.x) {
@@ -1026,8 +1031,8 @@ __global__ void __launch_bounds__(NT) k_replay(ReplayArgs A) {
 }
 
 // dynamic shared memory of k_replay: groups, sort buffers, (the replay state)
-inline uint32_t replay_smem_bytes(uint32_t n_groups, uint64_t core) {
-    return (uint32_t)(replay_groups_bytes(n_groups) + 36 * kReplaySmemRows + 64 + core);
+inline uint32_t replay_smem_bytes(uint32_t n_groups, uint64_t core, uint32_t sort_rows = kReplaySmemRows) {
+    return (uint32_t)(replay_groups_bytes(n_groups) + 36 * sort_rows + 64 + core);
 }
 
 }  // namespace jit
