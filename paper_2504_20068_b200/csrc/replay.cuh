@@ -97,7 +97,8 @@ namespace jit {
 // spread wide), 128 threads x 8 CTAs per SM for sweeps (more replays in flight per SM: the step is
 // barrier- and latency-bound).  C5(i) sweep on B200 (profiles/sweep_variants.py): 256 threads x 3
 // CTAs (2048 sort rows in shared memory) 9.8 M steps/s; 128 x 6 (1024 rows) 11.0; 128 x 6 (512)
-// 12.5; 128 x 8 (512 rows, 64 registers) 13.0; 128 x 8 (256) 12.2; 96 x 8 11.4; 64 x 12 8.9.
+// 12.5; 128 x 8 (512 rows, 64 registers) 13.0; 128 x 8 (256) 12.2; 96 x 8 11.4; 64 x 12 8.9; then
+// the warp path for <= 32 pending rows in sweeps too (+5%) and rank sorts for sets of 129-384 keys.
 // A step whose live rows exceed the shared sort buffers sorts in the CTA's global slice.
 constexpr uint32_t kReplayThreads = 512;
 constexpr uint32_t kReplayThreadsSweep = 128;
@@ -225,14 +226,15 @@ __host__ __device__ inline uint32_t replay_groups_bytes(uint32_t n_groups) {
     return (uint32_t)(((sizeof(Group) + sizeof(GroupFast)) * n_groups + 63) & ~63ull);
 }
 
-// diagnostics (-DJIT_REPLAY_STAMPS): %globaltimer per step phase of replay 0, printed at its end
+// diagnostics (-DJIT_REPLAY_STAMPS=k): %globaltimer per step phase of replay k - 1, printed at its end
 #ifdef JIT_REPLAY_STAMPS
-#define RSTAMP(i) do { if (threadIdx.x == 0 && rep == 0) { unsigned long long t_; \
+constexpr uint32_t kStampRep = JIT_REPLAY_STAMPS - 1;
+#define RSTAMP(i) do { if (threadIdx.x == 0 && rep == kStampRep) { unsigned long long t_; \
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); if ((i) > 0) s_ph[(i)] += t_ - s_ph_last; s_ph_last = t_; } } while (0)
 #else
 #define RSTAMP(i) do {} while (0)
 #endif
-template <uint32_t NT, uint32_t SR, bool kSweep, uint32_t MINB>
+template <uint32_t NT, uint32_t SR, uint32_t MINB>
 __global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
 #ifdef JIT_REPLAY_STAMPS
     __shared__ unsigned long long s_ph[16], s_ph_last;
@@ -549,8 +551,7 @@ __global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
             // ---- (a7)-(a9) for at most 32 pending rows: warp 0 alone, everything in registers and
             // shuffles (the block's many short barrier-separated phases dominate a small step);
             // the same orders, sums and tie-breaks as the general path below, so the same batch.
-            // Not in the sweep configuration (its registers would cost the sweep's occupancy).
-            if (!kSweep && np <= 32u) {
+            if (np <= 32u) {
                 if (wid == 0) {
                     // the pending rows (img != kNone) of the live list, compacted to lanes 0..np-1
                     uint32_t cnt = 0;
@@ -668,7 +669,9 @@ __global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
                     for (uint32_t i = m + threadIdx.x; i < m2; i += blockDim.x) { bA[i] = ~(u128)0; bAv[i] = 0; }
                     if (threadIdx.x == 0) s_m = m;
                     __syncthreads();
-                    block_sort<u128>(bA, bAv, m2);
+                    RSTAMP(4);
+                    block_sort_small<u128>(bA, bAv, m, m2);
+                    RSTAMP(14);
                 }
                 const uint32_t m = s_m;
                 // B* = longest prefix within tau and B_max (monotone predicate -> count)
@@ -693,10 +696,11 @@ __global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
                     // and Cd = {key >= thr} lies in S
                     s_spec_ok = attempt == 1 || m == np || (fits < m && s_thr_img >= t);
 #ifdef JIT_REPLAY_STAMPS
-                    if (rep == 0) { s_ph[10] += attempt; s_ph[11] += np; s_ph[12] += m; s_ph[13] += (attempt == 0 && s_m == 0); }
+                    if (rep == kStampRep) { s_ph[10] += attempt; s_ph[11] += np; s_ph[12] += m; s_ph[13] += (attempt == 0 && s_m == 0); }
 #endif
                 }
                 __syncthreads();
+                RSTAMP(15);
                 if (s_spec_ok) break;
             }
 #ifdef JIT_REPLAY_DUMP_STEP
@@ -735,7 +739,7 @@ __global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
             }
             __syncthreads();
             // ---- (a9) sort Cd by (len, id); windows within tau / B_max; first argmax
-            block_sort<uint64_t>(bB, bBv, m2);
+            block_sort_small<uint64_t>(bB, bBv, ncd, m2);
             unsigned long long* pc = in_smem ? reinterpret_cast<unsigned long long*>(sA) : S.gpc;   // reuse region A
             u128* pf = in_smem ? reinterpret_cast<u128*>(sbuf + ((8 * (SR + 1) + 15) & ~15u)) : S.gpf;
             {
@@ -1019,9 +1023,9 @@ __global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
             R.n_tasks_done = s_tdone; R.n_tasks_dropped = s_tdrop; R.error = s_err; R.n_preempted = n_preempted_total;
             A.out[rep] = R;
 #ifdef JIT_REPLAY_STAMPS
-            if (rep == 0) {
-                printf("replay 0: %u steps, ns/step:", s_steps);
-                for (int i = 1; i < 14; ++i) printf(" p%d=%llu", i, s_ph[i] / (s_steps ? s_steps : 1));
+            if (rep == kStampRep) {
+                printf("replay %u: %u steps, ns/step:", kStampRep, s_steps);
+                for (int i = 1; i < 16; ++i) printf(" p%d=%llu", i, s_ph[i] / (s_steps ? s_steps : 1));
                 printf("\n");
             }
 #endif
