@@ -629,9 +629,11 @@ static int finish_step_body(jit_sched* h, jit_batch* out) {
         k_publish<<<1, 64, 0, h->stream>>>(h->d_ctrl, h->h_ctrl);
         CK(cudaGetLastError());
     }
-    // the host's part of the step is done: chained steps may run again
+    // the host's part of the step is done: chained steps may run again (stream-ordered before the
+    // next step; only the host's own work needs waiting for -- the fast path's control block and
+    // batch were complete at the first synchronize)
     CK(cudaMemsetAsync(&h->S.persist->host_pending, 0, 4, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
+    if (host_work) CK(cudaStreamSynchronize(h->stream));
     const Ctrl& c = *h->h_ctrl;
     if (c.status == ST_ERROR || c.error) return set_err(h, JIT_EINVAL, "step: invalid input (error code %u)", c.error);
     if (out) {
