@@ -102,6 +102,7 @@ namespace jit {
 // A step whose live rows exceed the shared sort buffers sorts in the CTA's global slice.
 constexpr uint32_t kReplayThreads = 512;
 constexpr uint32_t kReplayThreadsSweep = 128;
+constexpr uint32_t kReplayThreadsMid = 256;    // sweeps of fewer than 6 replays per SM: 3 CTAs per SM
 constexpr uint32_t kReplaySweepRows = 512;     // sweep CTAs: rows sorted in shared memory
 constexpr uint32_t kReplaySweepCtas = 8;       // sweep CTAs per SM (launch bounds: <= 64 registers)
 constexpr uint32_t kReplayThreadsTiny = 64;     // traces of <= 64 rows (e.g. C1): two warps, cheap barriers

@@ -79,18 +79,19 @@ def test_c5_sampled_replays_full_logs():
     s.close()
 
 
-def test_c5_sweep_path_sampled():
-    """More replays than two per SM take the sweep configuration (256-thread CTAs, several per SM,
-    state in global slices): a sample of them, full logs, against the oracle."""
+@pytest.mark.parametrize("n_rep", [640, 1024])
+def test_c5_sweep_path_sampled(n_rep):
+    """More replays than two per SM take a sweep configuration, state in global slices: 256-thread
+    CTAs (3 per SM) below 6 replays per SM (640), 128-thread CTAs (8 per SM, 512 sort rows in
+    shared memory) from there (1024): a sample of them, full logs, against the oracle."""
     traces = [W.trace_mixed(k) for k in range(3)]
     d = traces[0]
     sweep = W.c5_sweep()
-    n_rep = 640
     specs = [dict(sweep[(i * 4096) // n_rep], trace=i % 3) for i in range(n_rep)]
     rc0 = dict(d["rcfg"], n_steps=1024)
     s = _sched(d)
     res, log = s.replay([t["trace"] for t in traces], specs, rc0, log_steps=1024)
-    for j in (0, 1, 97, 331, 500, n_rep - 1):
+    for j in (0, 1, 97, 331, 500, 777 % n_rep, n_rep - 1):
         sp = specs[j]
         rc = dict(rc0, **{k: sp[k] for k in ("load_num", "load_den", "slo_num", "slo_den")})
         t = traces[sp["trace"]]
