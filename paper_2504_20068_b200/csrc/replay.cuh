@@ -152,6 +152,7 @@ struct RState {
     int64_t* arr; uint32_t *gen, *pre, *lhat, *meta, *aux, *late, *cost; uint64_t* img;
     uint32_t *cur, *left, *tdone, *cb, *ce, *tever; int64_t *timer, *ta, *tD; unsigned long long* gdone;
     uint64_t *tle, *ttot;
+    unsigned long long *tT, *tG; int64_t* tDs;   // per-step stage sums (len_rem, goodput); D_s
     u128* gA; uint32_t* gAv; uint64_t* gB; uint32_t* gBv; unsigned long long* gpc; u128* gpf;  // global sort scratch
     uint32_t* batch; int64_t* ring;
     uint32_t* live;             // the rows that can be pending: arrived / released, not Done or Dropped
@@ -161,7 +162,7 @@ __host__ __device__ inline uint64_t replay_state_bytes(uint32_t M, uint32_t MT, 
     const uint64_t m = M + 64, mt = MT + 1;
     uint64_t b = 0;
     b += 8 * m + 4 * m * 7 + 8 * m + 4 * m;    // arr, gen..cost, img, live
-    b += 4 * mt * 6 + 8 * mt * 3 + 8 * mt + 16 * mt;   // task u32 x6, i64 x3, gdone, tle+ttot
+    b += 4 * mt * 6 + 8 * mt * 3 + 8 * mt + 16 * mt + 24 * mt;   // task u32 x6, i64 x3, gdone, tle+ttot, tT+tG+tDs
     uint64_t p2 = 1;                            // bitonic sorts pad to a power of two
     while (p2 < m) p2 <<= 1;
     b += 16 * p2 + 4 * p2 + 8 * p2 + 4 * p2 + 8 * (m + 1) + 16 * (m + 1);
@@ -174,7 +175,7 @@ __host__ __device__ inline uint64_t replay_state_bytes(uint32_t M, uint32_t MT, 
 __host__ __device__ inline uint64_t replay_core_bytes(uint32_t M, uint32_t MT, uint32_t max_batch) {
     const uint64_t m = M + 64, mt = MT + 1;
     auto r = [](uint64_t b) { return (b + 63) & ~63ull; };
-    return r(8 * m) + 7 * r(4 * m) + r(8 * m) + 6 * r(4 * mt) + 6 * r(8 * mt) + r(4 * (uint64_t)(max_batch + 1)) +
+    return r(8 * m) + 7 * r(4 * m) + r(8 * m) + 6 * r(4 * mt) + 9 * r(8 * mt) + r(4 * (uint64_t)(max_batch + 1)) +
            r(8 * 1024) + r(4 * m);
 }
 __device__ inline RState carve_core(unsigned char* p, uint32_t M, uint32_t MT, uint32_t max_batch) {
@@ -189,6 +190,7 @@ __device__ inline RState carve_core(unsigned char* p, uint32_t M, uint32_t MT, u
     s.cb = (uint32_t*)take(4 * mt); s.ce = (uint32_t*)take(4 * mt); s.tever = (uint32_t*)take(4 * mt);
     s.timer = (int64_t*)take(8 * mt); s.ta = (int64_t*)take(8 * mt); s.tD = (int64_t*)take(8 * mt);
     s.gdone = (unsigned long long*)take(8 * mt); s.tle = (uint64_t*)take(8 * mt); s.ttot = (uint64_t*)take(8 * mt);
+    s.tT = (unsigned long long*)take(8 * mt); s.tG = (unsigned long long*)take(8 * mt); s.tDs = (int64_t*)take(8 * mt);
     s.batch = (uint32_t*)take(4 * (uint64_t)(max_batch + 1)); s.ring = (int64_t*)take(8 * 1024);
     s.live = (uint32_t*)take(4 * m);
     return s;
@@ -206,6 +208,7 @@ __device__ inline RState carve_state(unsigned char* p, uint32_t M, uint32_t MT, 
     s.cb = (uint32_t*)take(4 * mt); s.ce = (uint32_t*)take(4 * mt); s.tever = (uint32_t*)take(4 * mt);
     s.timer = (int64_t*)take(8 * mt); s.ta = (int64_t*)take(8 * mt); s.tD = (int64_t*)take(8 * mt);
     s.gdone = (unsigned long long*)take(8 * mt); s.tle = (uint64_t*)take(8 * mt); s.ttot = (uint64_t*)take(8 * mt);
+    s.tT = (unsigned long long*)take(8 * mt); s.tG = (unsigned long long*)take(8 * mt); s.tDs = (int64_t*)take(8 * mt);
     uint64_t p2 = 1;
     while (p2 < m) p2 <<= 1;
     s.gA = (u128*)take(16 * p2); s.gAv = (uint32_t*)take(4 * p2); s.gB = (uint64_t*)take(8 * p2);
@@ -238,8 +241,8 @@ constexpr uint32_t kStampRep = JIT_REPLAY_STAMPS - 1;
 template <uint32_t NT, uint32_t SR, uint32_t MINB>
 __global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
 #ifdef JIT_REPLAY_STAMPS
-    __shared__ unsigned long long s_ph[16], s_ph_last;
-    if (threadIdx.x < 16) s_ph[threadIdx.x] = 0;
+    __shared__ unsigned long long s_ph[20], s_ph_last;
+    if (threadIdx.x < 20) s_ph[threadIdx.x] = 0;
 #endif
     extern __shared__ __align__(16) unsigned char smem[];
     Group* sg = reinterpret_cast<Group*>(smem);                                   // the SLO groups
@@ -258,6 +261,7 @@ __global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
     __shared__ unsigned long long s_good, s_tok, s_min;
     __shared__ uint32_t s_reqg, s_done, s_drop, s_tdone, s_tdrop, s_err, s_npend, s_cnt;
     __shared__ int64_t s_now, s_maxctx, s_nxt;
+    __shared__ long long s_tmin;                  // <= every task timer: no stage starts before it
     __shared__ uint32_t s_steps, s_ring_n, s_ring_pos;
     __shared__ uint32_t s_nlive, s_aptr;          // live rows; next standalone row to admit (arrival order)
     __shared__ int64_t s_ring_sum;
@@ -312,7 +316,7 @@ __global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
         if (threadIdx.x == 0) {
             s_good = 0; s_tok = 0; s_reqg = 0; s_done = 0; s_drop = 0; s_tdone = 0; s_tdrop = 0; s_err = 0;
             s_now = 0; s_steps = 0; s_ring_n = 0; s_ring_pos = 0; s_ring_sum = 0; s_stop = false;
-            s_nlive = 0; s_aptr = 0;
+            s_nlive = 0; s_aptr = 0; s_tmin = LLONG_MAX;
             s_tguess = kNone;                              // no speculative threshold before the first step
             s_npre = 0; s_stall = 0;
             s_arm = 0; s_gstart = 0; s_window = 0;
@@ -342,7 +346,8 @@ __global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
             if (Sn == 0 || Sn > kMaxStages) atomicOr(&s_err, 1u);
             uint64_t tot = 0;
             for (uint32_t u = 0; u < Sn && u < kMaxStages; ++u) tot += (uint64_t)st_pat[t * kMaxStages + u] * 1000000ull;
-            S.ttot[t] = tot; S.tle[t] = 0;
+            S.ttot[t] = tot; S.tle[t] = 0; S.tDs[t] = 0;
+            atomicMin(&s_tmin, (long long)S.ta[t]);
             S.timer[t] = S.ta[t]; S.cur[t] = 0; S.cb[t] = 0; S.ce[t] = 0; S.left[t] = 0; S.tdone[t] = 0; S.gdone[t] = 0;
             S.tever[t] = 0;
         }
@@ -351,7 +356,10 @@ __global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
         while (!s_err) {
             const int64_t now = s_now;
             RSTAMP(0);
-            // ---- stage starts whose time has come (task arrival or the end of the previous stage)
+            // ---- stage starts whose time has come (task arrival or the end of the previous stage);
+            // none before s_tmin (a lower bound of every timer), so most steps skip the task walk
+            if (now >= s_tmin) {
+            long long my_min = LLONG_MAX;
             for (uint32_t t = threadIdx.x; t < nt; t += blockDim.x) {
                 const uint32_t Sn = A.t_nst[tm.task_off + t];
                 while (!S.tdone[t] && S.timer[t] <= now) {
@@ -382,8 +390,16 @@ __global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
                     uint64_t le = 0;
                     for (uint32_t u = 0; u <= s; ++u) le += (uint64_t)st_pat[t * kMaxStages + u] * 1000000ull;
                     S.tle[t] = le;
+                    // D_s = floor(D t_<=s / t_total) (A43): fixed until the next stage release
+                    S.tDs[t] = S.ttot[t] ? (int64_t)((u128)(uint64_t)S.tD[t] * le / S.ttot[t]) : 0;
                     S.timer[t] = INT64_MAX;
                 }
+                if (!S.tdone[t] && S.timer[t] < my_min) my_min = S.timer[t];
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) s_tmin = LLONG_MAX;
+            __syncthreads();
+            if (my_min != LLONG_MAX) atomicMin(&s_tmin, my_min);
             }
             __syncthreads();
             RSTAMP(1);
@@ -449,12 +465,18 @@ __global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
                 if (o.w_lhat) S.lhat[r] = o.lhat;
                 my_pend += o.img != kNone; my_drop += o.dropped; my_err |= o.err;
             }
-            for (uint32_t t = threadIdx.x; t < nt; t += blockDim.x) {       // (a4) one thread per task
-                const uint32_t b = S.cb[t], e = S.ce[t];
+            RSTAMP(16);
+            // (a4) compound tasks, in three passes: per task the admission drop (A40) and the reset
+            // of its stage sums; per live call (in parallel) the refreshed bound and its share of the
+            // stage sums (integer atomics: order independent); per live call its key from its task's
+            // sums.  The same rows, sums and keys as one thread walking each task's stage.
+            for (uint32_t t = threadIdx.x; t < nt; t += blockDim.x) {
                 if (S.tdone[t]) continue;
+                S.tT[t] = 0; S.tG[t] = 0;
                 if (!S.tever[t] && now - S.ta[t] > c.waiting) {
                     // (a1) P:545, A40: a task none of whose calls was ever scheduled is dropped once it
                     // waited longer than waiting_time: its Queued / Waiting calls of every stage
+                    const uint32_t b = S.cb[t], e = S.ce[t];
                     bool hit = false;
                     for (uint32_t r = b; r < e; ++r) {
                         const uint32_t st = m_state(S.meta[r]);
@@ -472,58 +494,54 @@ __global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
                         }
                         S.tdone[t] = 1; S.timer[t] = INT64_MAX; S.cb[t] = 0; S.ce[t] = 0;
                         atomicAdd(&s_tdrop, 1u);
-                        continue;
                     }
-                }
-                uint64_t Tsum = 0, Gcur = 0; uint32_t cnt = 0;
-                for (uint32_t r = b; r < e; ++r) {
-                    uint32_t meta = S.meta[r];
-                    if (S.arr[r] > now || m_state(meta) > kPreempted) { S.img[r] = kNone; S.cost[r] = 0; continue; }
-                    const uint32_t g = S.gen[r];
-                    uint32_t lhat = S.lhat[r];
-                    const uint32_t ep = g / c.R;
-                    if (lhat == 0 || ep >= 65536u || m_epoch(meta) != ep) {
-                        lhat = T.forest ? qrf_bound(T.forest, L_in[r], S.aux[r] & 0xFFFFu, ep * c.R, m_group(meta),
-                                                    ep * c.R, c.qn, c.qd, T.l_max)
-                                        : ep == 0 ? __ldg(T.lhat0 + (S.aux[r] & 0xFFFFu))
-                                        : cond_quantile(T, S.aux[r] & 0xFFFFu, ep * c.R, c.qn, c.qd);
-                        S.lhat[r] = lhat;
-                        if (ep < 65536u) S.meta[r] = (meta & 0xFFFFu) | (ep << 16);
-                    }
-                    const uint32_t Lh = lhat > g + 1 ? lhat : g + 1;
-                    Tsum += Lh - g;
-                    const Group& G = sg[m_group(meta)];
-                    Gcur += (uint64_t)G.w_in * L_in[r] + (uint64_t)G.w_out * Lh;
-                    ++cnt;
-                }
-                if (!cnt) continue;
-                uint64_t Gt = S.gdone[t] + Gcur;
-                if (S.ta[t] + S.tD[t] <= now) Gt = 0;
-                const int64_t Ds = S.ttot[t] ? (int64_t)((u128)(uint64_t)S.tD[t] * S.tle[t] / S.ttot[t]) : 0;
-                const int64_t trem = S.ta[t] + Ds - now;
-                const uint64_t t_gen = Tsum * (uint64_t)v;
-                if (c.appb && t_gen > (uint64_t)(trem > 0 ? trem : 0)) Gt = 0;
-                for (uint32_t r = b; r < e; ++r) {
-                    const uint32_t meta = S.meta[r];
-                    if (S.arr[r] > now || m_state(meta) > kPreempted) continue;
-                    const uint32_t aux = S.aux[r];
-                    const uint64_t Gp = Gt + (uint64_t)c.delta * ((aux >> 16) / c.frame);
-                    double key;
-                    if (!make_key(Gp, t_gen, c.eps, &key)) my_err = 1;
-                    if (c.fair_num) key = blend_fair(key, A.fair ? A.fair[tm.row_off + r] : 0u, c.fair_num, c.fair_den);
-                    S.img[r] = (uint64_t)__double_as_longlong(key);
-                    S.cost[r] = token_cost(L_in[r], S.pre[r], c.chunk);
-                    ++my_pend;
                 }
             }
-            // compound rows outside a released stage are never pending (after the task pass: it
-            // may have dropped a task's calls just now, A40)
+            __syncthreads();
+            // the live compound rows are exactly the calls of the tasks' current stages that are
+            // not Done / Dropped; the pending ones (arrived, state <= Preempted) contribute
+            for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x) {
+                const uint32_t r = S.live[i];
+                const uint32_t meta = S.meta[r];
+                if (!(m_flags(meta) & kCompound)) continue;
+                if (S.arr[r] > now || m_state(meta) > kPreempted) { S.img[r] = kNone; S.cost[r] = 0; continue; }
+                const uint32_t g = S.gen[r];
+                uint32_t lhat = S.lhat[r];
+                const uint32_t ep = g / c.R;
+                if (lhat == 0 || ep >= 65536u || m_epoch(meta) != ep) {
+                    lhat = T.forest ? qrf_bound(T.forest, L_in[r], S.aux[r] & 0xFFFFu, ep * c.R, m_group(meta),
+                                                ep * c.R, c.qn, c.qd, T.l_max)
+                                    : ep == 0 ? __ldg(T.lhat0 + (S.aux[r] & 0xFFFFu))
+                                    : cond_quantile(T, S.aux[r] & 0xFFFFu, ep * c.R, c.qn, c.qd);
+                    S.lhat[r] = lhat;
+                    if (ep < 65536u) S.meta[r] = (meta & 0xFFFFu) | (ep << 16);
+                }
+                const uint32_t Lh = lhat > g + 1 ? lhat : g + 1;
+                const Group& G = sg[m_group(meta)];
+                const uint32_t t = tsk[r];
+                atomicAdd(&S.tT[t], (unsigned long long)(Lh - g));
+                atomicAdd(&S.tG[t], (unsigned long long)((uint64_t)G.w_in * L_in[r] + (uint64_t)G.w_out * Lh));
+            }
             __syncthreads();
             for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x) {
                 const uint32_t r = S.live[i];
                 const uint32_t meta = S.meta[r];
-                if ((m_flags(meta) & kCompound) && (S.arr[r] > now || m_state(meta) > kPreempted)) { S.img[r] = kNone; S.cost[r] = 0; }
+                if (!(m_flags(meta) & kCompound) || S.arr[r] > now || m_state(meta) > kPreempted) continue;
+                const uint32_t t = tsk[r];
+                uint64_t Gt = S.gdone[t] + S.tG[t];
+                if (S.ta[t] + S.tD[t] <= now) Gt = 0;
+                const int64_t trem = S.ta[t] + S.tDs[t] - now;
+                const uint64_t t_gen = S.tT[t] * (uint64_t)v;
+                if (c.appb && t_gen > (uint64_t)(trem > 0 ? trem : 0)) Gt = 0;
+                const uint64_t Gp = Gt + (uint64_t)c.delta * ((S.aux[r] >> 16) / c.frame);
+                double key;
+                if (!make_key(Gp, t_gen, c.eps, &key)) my_err = 1;
+                if (c.fair_num) key = blend_fair(key, A.fair ? A.fair[tm.row_off + r] : 0u, c.fair_num, c.fair_den);
+                S.img[r] = (uint64_t)__double_as_longlong(key);
+                S.cost[r] = token_cost(L_in[r], S.pre[r], c.chunk);
+                ++my_pend;
             }
+            RSTAMP(17);
             my_pend = warp_sum(my_pend); my_drop = warp_sum(my_drop);
             my_err = __reduce_or_sync(0xffffffffu, my_err);
             if (threadIdx.x == 0) { s_npend = 0; }
@@ -988,6 +1006,7 @@ __global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
                     atomicAdd(&S.gdone[t], (unsigned long long)call_R(G, L_in[r], L_out[r]));
                     if (atomicSub(&S.left[t], 1u) == 1u) {
                         S.cur[t] += 1; S.cb[t] = 0; S.ce[t] = 0; S.timer[t] = tnow;
+                        atomicMin(&s_tmin, (long long)tnow);
                     }
                 }
             }
@@ -1026,7 +1045,7 @@ __global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
 #ifdef JIT_REPLAY_STAMPS
             if (rep == kStampRep) {
                 printf("replay %u: %u steps, ns/step:", kStampRep, s_steps);
-                for (int i = 1; i < 16; ++i) printf(" p%d=%llu", i, s_ph[i] / (s_steps ? s_steps : 1));
+                for (int i = 1; i < 18; ++i) printf(" p%d=%llu", i, s_ph[i] / (s_steps ? s_steps : 1));
                 printf("\n");
             }
 #endif
