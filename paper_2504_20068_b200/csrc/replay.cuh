@@ -102,7 +102,14 @@ namespace jit {
 // A step whose live rows exceed the shared sort buffers sorts in the CTA's global slice.
 constexpr uint32_t kReplayThreads = 512;
 constexpr uint32_t kReplayThreadsSweep = 128;
-constexpr uint32_t kReplayThreadsMid = 256;    // sweeps of fewer than 6 replays per SM: 3 CTAs per SM
+constexpr uint32_t kReplayThreadsMid = 256;
+#ifndef JIT_REPLAY_MARGIN
+#define JIT_REPLAY_MARGIN 0.97
+#endif
+// next step's speculative threshold: this cutoff x margin.  C5(i) sweep on B200 (steps/s; full
+// re-sorts after a failed check per 4096 steps of the highest-load replay): 0.85 16.0 M; 0.90
+// 17.2 M; 0.95 18.4 M (102); 0.97 18.75 M (121); 0.99 18.8 M (153)
+constexpr double kReplayMargin = JIT_REPLAY_MARGIN;    // sweeps of fewer than 6 replays per SM: 3 CTAs per SM
 constexpr uint32_t kReplaySweepRows = 512;     // sweep CTAs: rows sorted in shared memory
 constexpr uint32_t kReplaySweepCtas = 8;       // sweep CTAs per SM (launch bounds: <= 64 registers)
 constexpr uint32_t kReplayThreadsTiny = 64;     // traces of <= 64 rows (e.g. C1): two warps, cheap barriers
@@ -498,6 +505,7 @@ __global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
                 }
             }
             __syncthreads();
+            RSTAMP(18);
             // the live compound rows are exactly the calls of the tasks' current stages that are
             // not Done / Dropped; the pending ones (arrived, state <= Preempted) contribute
             for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x) {
@@ -523,6 +531,7 @@ __global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
                 atomicAdd(&S.tG[t], (unsigned long long)((uint64_t)G.w_in * L_in[r] + (uint64_t)G.w_out * Lh));
             }
             __syncthreads();
+            RSTAMP(19);
             for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x) {
                 const uint32_t r = S.live[i];
                 const uint32_t meta = S.meta[r];
@@ -651,7 +660,7 @@ __global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
                     const uint64_t tot = __shfl_sync(0xffffffffu, pci, bj) - __shfl_sync(0xffffffffu, pce, bi);
                     if (lane == 0) {
                         s_bstar = bstar; s_bp = bp; s_thr = thr; s_thr_img = thr_img;
-                        s_tguess = (uint64_t)__double_as_longlong(__dmul_rn(thr, 0.85));
+                        s_tguess = (uint64_t)__double_as_longlong(__dmul_rn(thr, kReplayMargin));
                         s_m = np; s_ncd = ncd_w; s_nsel = bj - bi + 1; s_tot = (uint32_t)tot; s_bi[0] = bi;
                     }
                 }
@@ -659,7 +668,7 @@ __global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
                 RSTAMP(7);
             } else {
             // ---- (a7) order pending by (key desc, id asc).  Attempt 0 sorts only the speculative
-            // set S = {key >= t} (t = 0.85 x the previous step's cutoff): S is a prefix of the
+            // set S = {key >= t} (t = kReplayMargin x the previous step's cutoff): S is a prefix of the
             // priority order, so its budget walk is exact when it stops inside S (or S holds every
             // pending row), and Cd lies in S when thr >= t.  Otherwise attempt 1
             // sorts every pending row.  Both give the same B*, bp, thr and Cd.
@@ -734,7 +743,7 @@ __global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
             __syncthreads();
             RSTAMP(4);
 #endif
-            if (threadIdx.x == 0) s_tguess = (uint64_t)__double_as_longlong(__dmul_rn(s_thr, 0.85));
+            if (threadIdx.x == 0) s_tguess = (uint64_t)__double_as_longlong(__dmul_rn(s_thr, kReplayMargin));
             const uint32_t np_sorted = s_m;   // rows in the sorted prefix array bA (Cd is a prefix of it)
             // ---- (a8) Cd = prefix of the key-ordered list with key >= thr
             {
@@ -1045,7 +1054,8 @@ __global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
 #ifdef JIT_REPLAY_STAMPS
             if (rep == kStampRep) {
                 printf("replay %u: %u steps, ns/step:", kStampRep, s_steps);
-                for (int i = 1; i < 18; ++i) printf(" p%d=%llu", i, s_ph[i] / (s_steps ? s_steps : 1));
+                for (int i = 1; i < 20; ++i) printf(" p%d=%llu", i, s_ph[i] / (s_steps ? s_steps : 1));
+                printf(" full_sorts=%llu", s_ph[10]);
                 printf("\n");
             }
 #endif
