@@ -257,7 +257,7 @@ static __device__ __forceinline__ void spec_fast(const Pool& P, const Cfg& c, Ct
         ctrl->total_tokens = (uint32_t)(pc[bj + 1] - pc[bi]);
         ctrl->i_best = bi; ctrl->j_best = bj;
         ctrl->window_done = 1; ctrl->batch_on_host = 1;
-        finish_counters(S.persist, ctrl);               // next step's threshold: this cutoff with a 15% margin
+        finish_counters(S.persist, ctrl);               // next step's threshold: this cutoff with a 3% margin
     }
     stamp(ctrl, 7);
 }
@@ -824,7 +824,7 @@ static __device__ void spec_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const 
         ctrl->total_tokens = (uint32_t)(pc[bj + 1] - pc[bi]);
         ctrl->i_best = bi; ctrl->j_best = bj;
         ctrl->window_done = 1;
-        finish_counters(S.persist, ctrl);               // next step's threshold: this cutoff with a 15% margin
+        finish_counters(S.persist, ctrl);               // next step's threshold: this cutoff with a 3% margin
     }
     stamp(ctrl, 8);
 }

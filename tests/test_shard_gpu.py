@@ -72,6 +72,11 @@ def test_virtual_shards_consecutive_steps_fast_path(world, rows):
     from paper_2504_20068_b200 import Scheduler
     from paper_2504_20068_b200.sharded import ShardedStep, shard_pool, virtual_shards_step
     d = W.pool_snapshot(31, rows, table_draws=1 << 16)
+    if rows >= (1 << 21):
+        # a union beyond the small-set path (> 256 entries, the histogram resolve): with the 3%
+        # speculative margin tau = 8192 gives ~220 entries over 2^21 rows, so the C3 tau-sweep's
+        # largest budget
+        d["cfg"] = W.default_config(token_budget=65536, max_batch=65536)
     steps = []
     for r in range(world):
         sp, st = shard_pool(d["pool"], d["tasks"], r, world)
