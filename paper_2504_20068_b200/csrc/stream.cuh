@@ -415,20 +415,6 @@ __device__ __forceinline__ void cmp_phase_a(const Pool& P, const Table& T, const
             Tl = Lh - x.gen; Gc = (uint32_t)g64;
         }
         if (base + 32 * k >= it.r1) continue;                 // warp-uniform: the slab is empty
-#ifdef JIT_SEGSCAN
-        // segmented inclusive scan over the slab (tasks are contiguous lane ranges), then the last
-        // lane of each task's segment adds the segment's sums into the task's slot
-        uint32_t sT = Tl, sG = Gc;
-#pragma unroll
-        for (uint32_t d = 1; d < 32; d <<= 1) {
-            const uint32_t oT = __shfl_up_sync(0xffffffffu, sT, d), oG = __shfl_up_sync(0xffffffffu, sG, d);
-            const uint32_t ol = __shfl_up_sync(0xffffffffu, lt[k], d);
-            if (lane >= d && ol == lt[k]) { sT += oT; sG += oG; }
-        }
-        const uint32_t nl = __shfl_down_sync(0xffffffffu, lt[k], 1);
-        if (lt[k] < ntl && (lane == 31 || nl != lt[k])) { ts.T[lt[k]] += sT; ts.G[lt[k]] += sG; }
-        __syncwarp();
-#else
         // the slab's tasks: from lane 0's to the last row's (rows ordered by task)
         const uint32_t last = base + 32 * k + 31 < it.r1 ? 31u : it.r1 - 1 - (base + 32 * k);
         const uint32_t tf = __shfl_sync(0xffffffffu, lt[k], 0), tl = __shfl_sync(0xffffffffu, lt[k], last);
@@ -439,7 +425,6 @@ __device__ __forceinline__ void cmp_phase_a(const Pool& P, const Table& T, const
             const uint32_t sG = __reduce_add_sync(0xffffffffu, mine ? Gc : 0u);
             if (lane == (t & 31u)) { accT += sT; accG += sG; }  // task t's sums live in lane t % 32
         }
-#endif
     }
 }
 
@@ -474,9 +459,7 @@ __device__ __forceinline__ void cmp_item(const Pool& P, const Table& T, const Gr
         cmp_phase_a(P, T, sg, c, now, sc, it, base, ts, row_at, task_at,
                     [&](uint32_t r, const HotRow& x) { if (!big) sl->rows[r - it.r0] = x; }, lt, fr, pend_m,
                     accT, accG, A);
-#ifndef JIT_SEGSCAN
     if (lane < ntl) { ts.T[lane] = accT; ts.G[lane] = accG; }
-#endif
     __syncwarp();
 #ifdef JIT_TIMELINE
     const unsigned long long c1 = gtc();
@@ -494,11 +477,7 @@ __device__ __forceinline__ void cmp_item(const Pool& P, const Table& T, const Gr
             if (kAppB && t_gen > (uint64_t)(trem > 0 ? trem : 0)) Gt = 0;
             const uint64_t Bi = t_gen + (uint64_t)c.eps;
             // exact range: Tsum v without overflow (high word 0), + eps below 2^53
-#ifdef JIT_DIV64
-            if (Bi < kTwo53 && Bi >= t_gen && t_gen / (uint64_t)v == Tsum) Bd = __ull2double_rn(Bi);
-#else
             if (Bi < kTwo53 && Bi >= t_gen && __umul64hi(Tsum, (uint64_t)v) == 0) Bd = __ull2double_rn(Bi);
-#endif
         }
         ts.G[i] = Gt; ts.B[i] = Bd; ts.Bf[i] = Bd < 0.0 ? 1.0f : __double2float_rn(Bd);
     }
@@ -692,11 +671,9 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
     if (threadIdx.x < n_groups) g0 = groups[threadIdx.x];
     // while those are in flight: this warp's standalone slabs (balanced against the ring items it
     // owns, std_slabs; the host's ring count at launch) and the first chunk's row loads
-#if !defined(JIT_SKIP_STD) && !defined(JIT_DEV_NRING)
+#ifndef JIT_SKIP_STD
     std_slabs(i0, W, (P.n_single + 31) >> 5, S.n_ring_h, S.bal_w, s0, s1);
-#ifndef JIT_ROWS_AFTER_PS
     if (s0 < s1) load(cur, s0);
-#endif
 #endif
     __syncthreads();
     const Persist ps = s_ps;
@@ -705,9 +682,6 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&S.persist->skipped, 1u);
         return;
     }
-#if !defined(JIT_SKIP_STD) && !defined(JIT_DEV_NRING) && defined(JIT_ROWS_AFTER_PS)
-    if (s0 < s1) load(cur, s0);
-#endif
 #ifdef JIT_TIMELINE
     const unsigned long long tpa = gt();
 #endif
@@ -715,10 +689,6 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
     WarpSmem* ws = reinterpret_cast<WarpSmem*>(smem + ((sizeof(GroupNow) * n_groups + 127) & ~127ull)) + warp;
     const uint32_t n_ring = n_items > nstd ? n_items - nstd : 0u;
     const uint32_t n_mine = i0 < n_ring ? (n_ring - i0 + W - 1) / W : 0u;   // ring items i0 + j W of this warp
-#if !defined(JIT_SKIP_STD) && defined(JIT_DEV_NRING)
-    std_slabs(i0, W, (P.n_single + 31) >> 5, n_ring, S.bal_w, s0, s1);
-    if (s0 < s1) load(cur, s0);
-#endif
     const uint64_t pol = evict_first_policy();
     auto item_j = [&](uint32_t j) -> Item {                // warp-uniform j
         if (j >= 32) return S.items[nstd + i0 + j * W];
@@ -730,8 +700,8 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
         mbar_init_fence();
     }
     // fill the ring: the ring items' bytes stream in while the warp scores its standalone slabs.
-    // Issued after the first standalone chunk (JIT_RING_EARLY: here), so that the prologue does not
-    // wait for the item descriptors
+    // Issued after the first standalone chunk, so that the prologue does not wait for the item
+    // descriptors
     bool ring_filled = false;
     auto fill_ring = [&]() {
         for (uint32_t s = 0; s < kStagesW && s < n_mine; ++s) {
@@ -740,9 +710,6 @@ __global__ void __launch_bounds__(kScoreThreads, JIT_SCORE_MINB) k_score(Pool P,
         }
         ring_filled = true;
     };
-#ifdef JIT_RING_EARLY
-    fill_ring();
-#endif
 #ifdef JIT_TIMELINE
     const unsigned long long tpb = gt();
 #endif
