@@ -15,7 +15,7 @@ cudaError_t init_attributes() {
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)((sizeof(u128) + 4) * kBucketCap))) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(k_group, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(12 * kGroupSmemSort))) !=
+    if ((e = cudaFuncSetAttribute(k_group, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kGroupSmemBytes))) !=
         cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(k_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSpecSmem)) !=
         cudaSuccess) return e;
@@ -49,7 +49,7 @@ cudaError_t spec(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, int 
     // big mode: the big-set resolve, then the window over a large Cd (k_group runs only when the
     // resolve left it undone), then the host flag and the published control block
     k_spec_big_chain<<<1, kSpecThreads, kSpecSmem, s>>>(P, c, ctrl, S);
-    k_group<<<1, 1024, 12 * kGroupSmemSort, s>>>(P, c, ctrl, S);
+    k_group<<<1, 1024, kGroupSmemBytes, s>>>(P, c, ctrl, S);
     k_chain_publish<<<1, 64, 0, s>>>(ctrl, S.persist, S.h_ctrl);
     return cudaGetLastError();
 }
@@ -83,7 +83,7 @@ void cand(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, uint32_t gr
     k_cand<<<grid, kPassThreads, 0, s>>>(P, c, ctrl, S, only_after_fallback);
 }
 void group(const Pool& P, const Cfg& c, Ctrl* ctrl, const Scratch& S, cudaStream_t s) {
-    k_group<<<1, 1024, 12 * kGroupSmemSort, s>>>(P, c, ctrl, S);
+    k_group<<<1, 1024, kGroupSmemBytes, s>>>(P, c, ctrl, S);
 }
 
 }  // namespace exact

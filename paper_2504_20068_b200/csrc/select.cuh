@@ -22,6 +22,10 @@ namespace jit {
 constexpr uint32_t kBucketCap = 4096;
 constexpr uint32_t kSpecCap = 8192;            // speculative set resolved in shared memory up to this size
 constexpr uint32_t kGroupSmemSort = 8192;     // |Cd| sorted in shared memory up to this size
+constexpr uint32_t kGroupSmemWin = 4096;      // |Cd| whose window prefix sums live in shared memory
+constexpr uint32_t kGroupPfOff = (12 * kGroupSmemSort + 8 * (kGroupSmemWin + 1) + 15) & ~15u;
+constexpr uint32_t kGroupSmemBytes = kGroupPfOff + 16 * (kGroupSmemWin + 1);   // k_group's dynamic smem
+static_assert(kGroupSmemBytes <= 227 * 1024, "k_group shared memory");
 constexpr uint32_t kPassThreads = 512;
 
 enum : uint32_t { ST_RUN = 0, ST_HIST = 1, ST_COMPACT = 2, ST_RESOLVED = 3, ST_EMPTY = 4, ST_ERROR = 5, ST_FALLBACK = 6,
@@ -645,7 +649,11 @@ static __device__ void group_body(const Pool& P, const Cfg& c, Ctrl* ctrl, const
         sk[i] = (len << 32) | P.id[r];                      // (len asc, id asc), A17/A18
         sv[i] = r;
     }
-    window_select(P, c, ctrl, S, sk, sv, n, S.pc, S.pf);
+    // the window's prefix sums (read by every start's binary search) in shared memory when they fit
+    const bool win_smem = n <= kGroupSmemWin;
+    window_select(P, c, ctrl, S, sk, sv, n,
+                  win_smem ? reinterpret_cast<unsigned long long*>(smem + 12 * kGroupSmemSort) : S.pc,
+                  win_smem ? reinterpret_cast<u128*>(smem + kGroupPfOff) : S.pf);
 }
 
 #endif  // JIT_EXACT_TU
