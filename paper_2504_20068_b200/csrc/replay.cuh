@@ -780,9 +780,8 @@ __global__ void __launch_bounds__(NT, MINB) k_replay(ReplayArgs A) {
                         cv = S.cost[r];
                         fv = (u128)fixed_point(__longlong_as_double((long long)S.img[r]));
                     }
-                    uint64_t tc; u128 tf;
-                    const uint64_t ec = block_exclusive_scan_u64(cv, s_scan, &tc);
-                    const u128 ef = block_exclusive_scan_u128(fv, s_scan128, &tf);
+                    uint64_t tc, ec; u128 tf, ef;
+                    block_exclusive_scan_pair(cv, fv, s_scan, s_scan128, ec, ef, tc, tf);
                     if (i < ncd) { pc[i] = carry_c + ec; pf[i] = carry_f + ef; }
                     carry_c += tc; carry_f += tf;
                 }

@@ -317,6 +317,40 @@ __device__ __forceinline__ u128 block_exclusive_scan_u128(u128 v, u128* scratch,
     return base + x - v;
 }
 
+// the window's two prefix sums (token cost u64, fixed-point key u128) in ONE exclusive block scan:
+// three barriers for the pair instead of three each
+__device__ __forceinline__ void block_exclusive_scan_pair(uint64_t vc, u128 vf, uint64_t* scr_c, u128* scr_f,
+                                                          uint64_t& ec, u128& ef, uint64_t& tc, u128& tf) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint64_t xc = vc;
+    u128 xf = vf;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t yc = __shfl_up_sync(0xffffffffu, xc, o);
+        const u128 yf = shfl_up_u128(xf, o);
+        if (lane >= o) { xc += yc; xf += yf; }
+    }
+    if (lane == 31) { scr_c[wid] = xc; scr_f[wid] = xf; }
+    __syncthreads();
+    if (wid == 0) {
+        uint64_t sc = lane < nw ? scr_c[lane] : 0ull;
+        u128 sf = lane < nw ? scr_f[lane] : (u128)0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t yc = __shfl_up_sync(0xffffffffu, sc, o);
+            const u128 yf = shfl_up_u128(sf, o);
+            if (lane >= o) { sc += yc; sf += yf; }
+        }
+        if (lane < nw) { scr_c[lane] = sc; scr_f[lane] = sf; }
+    }
+    __syncthreads();
+    const uint64_t bc = wid ? scr_c[wid - 1] : 0ull;
+    const u128 bf = wid ? scr_f[wid - 1] : (u128)0;
+    tc = scr_c[nw - 1]; tf = scr_f[nw - 1];
+    __syncthreads();
+    ec = bc + xc - vc; ef = bf + xf - vf;
+}
+
 #ifdef JIT_EXACT_TU
 // The exact path (host-launched by finish_step when the speculative resolve cannot be exact):
 // k_hist0 -> k_pass x <= 7 -> k_compact -> k_resolve -> k_cand -> k_group; each kernel returns at
@@ -558,9 +592,8 @@ static __device__ void window_select(const Pool& P, const Cfg& c, Ctrl* ctrl, co
             cv = P.cost[r];
             fv = (u128)fixed_point(__longlong_as_double((long long)P.img[r]));
         }
-        uint64_t tc; u128 tf;
-        const uint64_t ec = block_exclusive_scan_u64(cv, s_scan, &tc);
-        const u128 ef = block_exclusive_scan_u128(fv, s_scan128, &tf);
+        uint64_t tc, ec; u128 tf, ef;
+        block_exclusive_scan_pair(cv, fv, s_scan, s_scan128, ec, ef, tc, tf);
         if (i < n) { pc[i] = carry_c + ec; pf[i] = carry_f + ef; }
         carry_c += tc; carry_f += tf;
     }
