@@ -1,10 +1,12 @@
 // replay.cuh -- (a10) persistent trace replay: one CTA per replay (grid-stride over replays).
 //
-// Each CTA owns one replay at a time; the request state lives in a per-CTA global slice
-// (L2-resident: 2048 rows x 44 B), the selection working set in shared memory when it fits.
-// Per simulated iteration: stage releases / tool timers -> GMAX step over the
-// replay's rows (a1-a9, block-level: bitonic sort of the pending composite keys, block scan
-// of costs for B*/bp, cutoff, bitonic sort of Cd by (len, id), u64/u128 prefix windows) ->
+// Each CTA owns one replay at a time; the request state lives in shared memory for a few small
+// traces, else in a per-CTA global slice (L2-resident), the selection working set in shared
+// memory when it fits.  Per simulated iteration: stage releases / tool timers ->
+// GMAX step over the replay's live rows (a1-a9, block-level: speculative sort of the pending
+// composite keys {key >= t} -- bitonic, or rank sort for 129-384 keys, or one warp's registers
+// for <= 32 pending rows --, block scan of costs for B*/bp, cutoff, sort of Cd by (len, id),
+// one fused u64/u128 prefix scan for the windows) ->
 // iteration latency c0 + c_att*max ctx + c_lin*|batch| -> token emission and goodput
 // accounting (§3) -> stage barriers -> v_token = floor(trailing mean of Delta
 // latencies).  Integer sums are order independent, so results are deterministic.
