@@ -89,3 +89,84 @@ class FakeShardSched:
                 "batch_tokens": np.array([a["cost"][k] for k in sel], np.uint32), "b_star": self.b_star, "bp": self.bp,
                 "thr": self.thr, "n_candidates": len(a),
                 "total_tokens": int(sum(int(a["cost"][k]) for k in sel))}
+
+
+SPEC_DT = np.dtype([("img", "<u8"), ("id", "<u4"), ("cost", "<u4"), ("len", "<u4"), ("pad", "<u4")])
+SPEC_CAP = 1024
+
+
+class FakeSpecShardSched(FakeShardSched):
+    """Adds the speculative tier (jit_shard_spec_export / _resolve): every rank exports its rows
+    with key >= t (t = fl(0.97 x the previous cutoff), identical on every rank), and every rank
+    resolves the union -- exact when the budget walk stops inside the union (or the union holds
+    every pending request) and thr >= t; otherwise None (the exact protocol)."""
+
+    def __init__(self, d, max_batch, capacity):
+        super().__init__(d, max_batch, capacity)
+        self.t = None
+
+    def shard_spec_bytes(self):
+        return 16 + SPEC_DT.itemsize * SPEC_CAP
+
+    def shard_spec_export(self, now, v, buf, rank):
+        d, cfg = self.d, self.d["cfg"]
+        self.out = oracle.step(cfg, d["groups"], d["table"], now, v, d["pool"], d["tasks"])
+        key, pend = self.out["key"], self.out["pending"].astype(bool)
+        b = buf.numpy()
+        hdr = b[:16].view(np.uint32)
+        hdr[0] = int(pend.sum())
+        if self.t is None:
+            hdr[1] = 0xFFFFFFFF                               # no threshold yet: exact protocol
+            return
+        rows = [r for r in np.nonzero(pend)[0] if np.float64(key[r]).view(np.uint64) >= self.t]
+        assert len(rows) <= SPEC_CAP
+        hdr[1] = len(rows)
+        rec = b[16:].view(SPEC_DT)
+        for i, r in enumerate(rows):
+            ln = int(d["pool"]["input_len"][r]) + (int(d["pool"]["generated"][r]) if cfg["len_key"] else 0)
+            rec[i] = (np.float64(key[r]).view(np.uint64), d["pool"]["id"][r], self.out["cost"][r], ln, 0)
+
+    def shard_spec_resolve(self, allb, world, rank):
+        cfg = self.d["cfg"]
+        b = allb.numpy().reshape(world, -1)
+        hdrs = [b[w, :16].view(np.uint32) for w in range(world)]
+        if any(h[1] == 0xFFFFFFFF for h in hdrs):
+            return None
+        n_pend = sum(int(h[0]) for h in hdrs)
+        u = np.concatenate([b[w, 16:].view(SPEC_DT)[:int(hdrs[w][1])] for w in range(world)])
+        if n_pend == 0 or len(u) == 0:
+            return None
+        whole = len(u) == n_pend
+        order = sorted(range(len(u)), key=lambda i: (-u["img"][i].view(np.float64), int(u["id"][i])))
+        m, s = 0, 0
+        while m < len(order) and m + 1 <= cfg["max_batch"] and s + int(u["cost"][order[m]]) <= cfg["token_budget"]:
+            s += int(u["cost"][order[m]])
+            m += 1
+        if m == 0 or (m == len(order) and not whole):
+            return None
+        bp = float(u["img"][order[m - 1]].view(np.float64))
+        thr = (cfg["p_num"] / cfg["p_den"]) * bp
+        if not whole and np.float64(thr).view(np.uint64) < self.t:
+            return None
+        cd = u[[i for i in range(len(u)) if u["img"][i].view(np.float64) >= thr]]
+        a = np.zeros(len(cd), REC2_DT)
+        for f in ("img", "id", "cost", "len"):
+            a[f] = cd[f]
+        self.b_star, self.bp, self.thr = m, bp, thr
+        out = self.shard_finish(_as_rec2(a), rank)
+        return out
+
+    def shard_finish(self, all2, rank):
+        out = super().shard_finish(all2, rank)
+        self.t = np.float64(0.97 * self.thr).view(np.uint64)   # identical on every rank
+        return out
+
+
+class _as_rec2:
+    """numpy REC2 array in the shape shard_finish expects (a tensor-like with .numpy())."""
+
+    def __init__(self, a):
+        self.a = a
+
+    def numpy(self):
+        return self.a.view(np.uint8)

@@ -38,7 +38,7 @@ def _worker(rank, world, port, seed, q):
     import oracle
     import workloads as W
     from paper_2504_20068_b200.sharded import ShardedStep, shard_pool
-    from tests._fake_shard import FakeShardSched
+    from tests._fake_shard import FakeShardSched, FakeSpecShardSched
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -59,6 +59,25 @@ def _worker(rank, world, port, seed, q):
                       got["thr"] == ref["thr"] and got["b_star"] == ref["b_star"] and
                       got["n_candidates"] == ref["n_candidates"])
             results.append(bool(ok))
+        # the speculative tier over gloo: a first step through the exact protocol leaves the
+        # threshold, the next step on the same pool resolves the union of the exported sets
+        n_spec = 0
+        for it in range(4):
+            d = W.random_small_pool(rng, int(rng.integers(20, 80)))
+            ref = oracle.step(d["cfg"], d["groups"], d["table"], d["now_ns"], d["v_token_ns"], d["pool"], d["tasks"])
+            sp, st = shard_pool(d["pool"], d["tasks"], rank, world)
+            fake = FakeSpecShardSched(dict(d, pool=sp, tasks=st), d["cfg"]["max_batch"], max(len(sp["input_len"]), 1))
+            step = ShardedStep(fake, rank, world, _gloo_allgather(), device="cpu")
+            for k in range(2):
+                got = step.step(d["now_ns"], d["v_token_ns"])
+                ok = True
+                if ref["status"] == 0:
+                    ok = (list(got["batch_ids"]) == list(ref["batch_ids"]) and got["bp"] == ref["bp"] and
+                          got["thr"] == ref["thr"] and got["b_star"] == ref["b_star"] and
+                          got["n_candidates"] == ref["n_candidates"])
+                    n_spec += got["path"] == "speculative"
+                results.append(bool(ok))
+        results.append(n_spec > 0)
         q.put((rank, results))
     finally:
         dist.destroy_process_group()
