@@ -153,6 +153,15 @@ def c3_config(n, nt, ws, rot, extra=None):
     return cfg
 
 
+def c5ii_config(ws, n, rot):
+    """the N > 1 config dict both arms print (the sharded C5(ii) pool)"""
+    return {"workload": f"C5(ii): {ws} x {n}-row shards of one pool (C3 generator), sharded by request id, "
+                        "tau 8192, B_max 8192", "rows_total": ws * n, "rows_per_gpu": n,
+            "l2": f"{rot} rotated shard copies per rank (>= 4x the L2 of hot state)",
+            "parallelism": f"sharded pool over {ws} ranks: speculative sets allgathered over NCCL and resolved "
+                           "identically on every rank (exact 2-round protocol as fallback)"}
+
+
 def rot_for(args, hot):
     """pool copies rotated so that their hot state exceeds 4x the L2 (at least 6)"""
     return args.rot or max(6, -(-4 * L2_BYTES // hot))
@@ -188,7 +197,7 @@ def run_reference(args, ws, rank):
     """The reference arm: the CPU oracle as it stands, on this arm's config (rank 0 only)."""
     if rank != 0:
         return
-    rows = args.rows or (1 << 20)
+    rows = args.rows or (1 << 20 if ws == 1 else 1 << 21)
     d = W.pool_snapshot(3, rows)
     n = len(d["pool"]["input_len"])
     nt = len(d["tasks"]["arrival_ns"])
@@ -198,12 +207,16 @@ def run_reference(args, ws, rank):
         oracle_step_timing(d, budget_s=0.0, max_steps=1)
     t, k = oracle_step_timing(d, budget_s=60.0, max_steps=max(1, min(args.steps, 20)))
     v = n / t
-    rot = rot_for(args, alg_bytes(d))
+    if ws == 1:
+        cfg = c3_config(n, nt, 1, rot_for(args, alg_bytes(d)))
+        sample = f"{k} oracle steps over the full C3 pool ({n} rows), 1 core of {cpu_model()}"
+    else:                                   # the sharded pool's config; the sample: one rank's shard
+        cfg = c5ii_config(ws, n, args.rot or max(2, -(-4 * L2_BYTES // alg_bytes(d))))
+        sample = f"{k} oracle steps over one {n}-row shard of the C5(ii) pool, 1 core of {cpu_model()}"
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": k,
             "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": c3_config(n, nt, 1, rot),
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{k} oracle steps over the full C3 pool ({n} rows), 1 core of {cpu_model()}"},
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -799,11 +812,11 @@ def run_single(args, dev, stream):
     line = {"metric": METRIC, "value": n / (ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": Wm,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": c3_config(n, nt, 1, rot, {"device_steps_resolved": steps_dev, "fast_path_fallbacks": fallback,
-                                                "chained_steps_skipped": skipped,
-                                                "host_submit_us_per_step": round(host_us[0], 2),
-                                                "last_batch": {"n_selected": sel["n_selected"], "b_star": sel["b_star"],
-                                                               "n_candidates": sel["n_candidates"]}}),
+            "config": c3_config(n, nt, 1, rot),
+            "run": {"device_steps_resolved": steps_dev, "fast_path_fallbacks": fallback,
+                    "chained_steps_skipped": skipped, "host_submit_us_per_step": round(host_us[0], 2),
+                    "last_batch": {"n_selected": sel["n_selected"], "b_star": sel["b_star"],
+                                   "n_candidates": sel["n_candidates"]}},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "configs": configs,
             "gpu_launches": 2 * K, "clocks": clocks, "replay": replay}
     print(json.dumps(line), flush=True)
@@ -932,14 +945,11 @@ def run_sharded(args, ws, rank, dev, stream, barrier, allmax, allsum):
         line = {"metric": METRIC, "value": total / (ms / 1e3), "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": Wm,
                 "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
-                "config": {"workload": f"C5(ii): {ws} x {n}-row shards of one pool (C3 generator), sharded by request "
-                                       "id, tau 8192, B_max 8192", "rows_total": int(total), "rows_per_gpu": n,
-                           "l2": f"{rot} rotated shard copies per rank (>= 4x the L2 of hot state)",
-                           "parallelism": f"sharded pool over {ws} ranks: speculative sets allgathered over NCCL and "
-                                          "resolved identically on every rank (exact 2-round protocol as fallback)",
-                           "steps_speculative": n_fast, "steps_exact_protocol": n_exact, "breakdown": breakdown,
-                           "last_batch": {"n_selected": out["n_selected"], "b_star": out["b_star"],
-                                          "n_candidates": out["n_candidates"]}},
+                "config": c5ii_config(ws, n, rot),
+                "run": {"rows_total": int(total), "steps_speculative": n_fast, "steps_exact_protocol": n_exact,
+                        "breakdown": breakdown,
+                        "last_batch": {"n_selected": out["n_selected"], "b_star": out["b_star"],
+                                       "n_candidates": out["n_candidates"]}},
                 "roofline": roofline, "cpu_baseline": None, "e2e": e2e,
                 "gpu_launches": 3 * n_fast + 18 * n_exact, "clocks": clocks, "replay": replay}
         print(json.dumps(line), flush=True)

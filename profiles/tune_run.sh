@@ -11,7 +11,7 @@ try:
     r = d["roofline"]
     print("$name", "ms/step %.4f" % d["ms_per_step"], "k_score b2b us %.2f" % (r["k_score_ms"] * 1e3),
           "nodes", {k: round(v * 1e3, 2) for k, v in r["kernel_ms_event_nodes"].items()}, "frac %.3f" % r["frac"],
-          "fb", d["config"]["fast_path_fallbacks"], "skip", d["config"]["chained_steps_skipped"])
+          "fb", d["run"]["fast_path_fallbacks"], "skip", d["run"]["chained_steps_skipped"])
 except Exception as e:
     print("$name failed", e, open("gpurun_out/tune_$name.log").read()[-800:])
 PY
