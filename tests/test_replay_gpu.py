@@ -140,3 +140,24 @@ def test_task_drops_in_the_same_step_as_scoring():
         res, log = s.replay([d["trace"]], [_spec(rc)], rc, log_steps=rc["n_steps"])
         _cmp(res[0], log[0], ref, f"drops {it}")
         s.close()
+
+
+@pytest.mark.parametrize("n_rep", [400, 900])
+def test_sweep_configs_short(n_rep):
+    """Both sweep configurations (256-thread CTAs below 6 replays per SM, 128-thread CTAs x 8 per
+    SM from there) on short replays -- sized for the sanitizers (profiles/sanitize.sh): sampled
+    replays against the oracle, full logs."""
+    traces = [W.trace_mixed(k) for k in range(2)]
+    d = traces[0]
+    sweep = W.c5_sweep()
+    specs = [dict(sweep[(i * 4093) % 4096], trace=i % 2) for i in range(n_rep)]
+    rc0 = dict(d["rcfg"], n_steps=24)
+    s = _sched(d)
+    res, log = s.replay([t["trace"] for t in traces], specs, rc0, log_steps=24)
+    for j in (0, n_rep // 2, n_rep - 1):
+        sp = specs[j]
+        rc = dict(rc0, **{k: sp[k] for k in ("load_num", "load_den", "slo_num", "slo_den")})
+        t = traces[sp["trace"]]
+        ref = oracle.replay(t["cfg"], t["groups"], t["table"], t["trace"], rc, log=True)
+        _cmp(res[j], log[j], ref, f"short sweep replay {j}")
+    s.close()
